@@ -1,0 +1,147 @@
+/*
+ * qmb200.h -- C ABI of the B200 block-sparse quadtree multiply (libqmb200.so).
+ *
+ * The reference (arXiv 2011.11762, Python package `quadmat` under pkg/src/quadmat) has no
+ * native code and no FFI; its multiply is the recursive task graph
+ *   MatrixSession.multiply        session.py:160-171
+ *   -> ops.multiply_spec          ops.py:582-608
+ *   -> "multiply" task body       ops.py:197-245   (+ "add" ops.py:147-169, "assemble" ops.py:134-139)
+ *   -> BlockSparseLeaf.multiply   leaves/block_sparse.py:112-132 (numpy dgemm per block triple)
+ * Each entry point below replaces one layer of that stack; the per-function comment names it.
+ * A maintainer binding this library from the reference would load it with ctypes and call the
+ * functions from a replacement "multiply" task body.
+ *
+ * Conventions
+ *  - All pointers marked (device) are CUDA device pointers owned by the caller; the library never
+ *    allocates or frees caller memory and never returns owned allocations. Scratch comes from a
+ *    caller-provided workspace (size queried with the *_workspace_bytes functions).
+ *  - Every call is stream-ordered on the caller's stream (a cudaStream_t passed as void*; NULL is
+ *    the legacy default stream). Only qm_spgemm_count synchronises (it returns sizes to the host).
+ *  - Return value: QM_OK (0) or a negative QM_ERR_* code; qm_last_error() returns a thread-local
+ *    message for the last failure on the calling thread.
+ *  - The library is reentrant: no mutable globals other than the thread-local error string and a
+ *    relaxed launch counter.
+ *
+ * Data layout ("quadtree key" order)
+ *  A matrix is nnzb dense bs x bs float64 blocks, row-major (the BlockSparseLeaf block payload,
+ *  block_sparse.py:226-231), stored contiguously in ascending order of their uint64 quadtree key
+ *      qkey(bi, bj) = morton(bi / nbl, bj / nbl) << (2*lbits) | (bi % nbl) << lbits | (bj % nbl)
+ *  where nbl = leaf_dim / bs blocks per leaf side, lbits = ceil(log2(nbl)), and morton() interleaves
+ *  the leaf-grid coordinates with the row bit high (NW, NE, SW, SE = quadtree.py:128-129). That is
+ *  exactly the order in which canonical_bytes (quadtree.py:293-318) visits the blocks: depth-first
+ *  over the tree, then BlockSparseLeaf.encode's sorted (bi, bj) order inside a leaf.
+ */
+#ifndef QMB200_H
+#define QMB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define QM_API __attribute__((visibility("default")))
+#else
+#define QM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QM_ABI_VERSION 1
+
+enum qm_status {
+  QM_OK = 0,
+  QM_ERR_INVALID = -1,     /* bad argument / nonconformant operands (DimensionMismatch, Configuration) */
+  QM_ERR_CUDA = -2,        /* a CUDA runtime call or kernel launch failed */
+  QM_ERR_WORKSPACE = -3,   /* caller workspace smaller than the queried size */
+  QM_ERR_UNSUPPORTED = -4, /* block size / layout not supported by this build */
+};
+
+/* Geometry of one quadtree matrix: MatrixParams (quadtree.py:24-44) + BlockSparseLeaf.block_size. */
+typedef struct qm_layout {
+  int64_t n_logical; /* MatrixParams.n_logical */
+  int32_t leaf_dim;  /* MatrixParams.leaf_dim; must be a multiple of block_size */
+  int32_t depth;     /* MatrixParams.depth (leaf_dim << depth >= n_logical) */
+  int32_t block_size;/* BlockSparseLeaf.block_size */
+  int32_t reserved;  /* must be 0 */
+} qm_layout;
+
+/* ---- library info --------------------------------------------------------------------------- */
+QM_API int qm_abi_version(void);
+QM_API const char *qm_last_error(void);
+/* Number of kernels this library has launched in this process (relaxed counter; for bench). */
+QM_API uint64_t qm_launch_count(void);
+
+/* ---- quadtree keys ---------------------------------------------------------------------------- */
+/* Replaces the quadrant recursion of build_from_triplets (quadtree.py:112-142) for block placement:
+ * keys[i] = qkey(bi[i], bj[i]) on the device. */
+QM_API int qm_encode_keys(const qm_layout *layout, const int32_t *bi /*device*/, const int32_t *bj /*device*/,
+                   int64_t n, uint64_t *keys /*device*/, void *stream);
+/* Inverse: (bi, bj) block coordinates of each key. */
+QM_API int qm_decode_keys(const qm_layout *layout, const uint64_t *keys /*device*/, int64_t n,
+                   int32_t *bi /*device*/, int32_t *bj /*device*/, void *stream);
+
+/* ---- symbolic phase (replaces the recursive task expansion, ops.py:197-245 + engine.py:196-326) */
+/* Persistent workspace for one product; valid from qm_spgemm_count until qm_spgemm_fill returns. */
+QM_API size_t qm_spgemm_workspace_bytes(const qm_layout *layout, int64_t nA, int64_t nB);
+/* Builds block-row indexes of A and B inside ws, counts the C blocks of the symbolic product
+ * (every (i,j) with some k such that A(i,k) and B(k,j) are stored) and the product triples.
+ * Synchronises `stream` and writes the two counts to host memory. */
+QM_API int qm_spgemm_count(const qm_layout *layout, const uint64_t *a_keys /*device, sorted*/, int64_t nA,
+                    const uint64_t *b_keys /*device, sorted*/, int64_t nB, void *ws, size_t ws_bytes,
+                    int64_t *n_c_out /*host*/, int64_t *n_triples_out /*host*/, void *stream);
+QM_API size_t qm_spgemm_fill_workspace_bytes(const qm_layout *layout, int64_t nC);
+/* Emits the C key set in quadtree-key order (c_keys[nC]), the triple offsets c_tptr[nC+1] and the
+ * triples tri[2*nT] = (a_index, b_index) pairs, grouped by C block, k ascending within a group --
+ * the order of BlockSparseLeaf.multiply's k loop (block_sparse.py:121-129). */
+QM_API int qm_spgemm_fill(const qm_layout *layout, const uint64_t *a_keys, int64_t nA, const uint64_t *b_keys,
+                   int64_t nB, void *ws, size_t ws_bytes, void *fill_ws, size_t fill_ws_bytes,
+                   uint64_t *c_keys /*device*/, int64_t *c_tptr /*device*/, uint32_t *tri /*device*/,
+                   void *stream);
+
+/* ---- numeric phase (replaces BlockSparseLeaf.multiply + add, block_sparse.py:112-152) ------- */
+/* c_blocks[m] = sum over t in [c_tptr[m], c_tptr[m+1]) of A[tri[2t]] * B[tri[2t+1]] (fp64),
+ * c_sumsq[m] = squared Frobenius norm of the block, c_nonzero[m] = any entry != 0
+ * (the np.any test of _set_block, block_sparse.py:37-41). *zero_count (device, int64) is
+ * incremented once per exactly-zero C block; the caller zeroes it first. */
+QM_API int qm_numeric(const qm_layout *layout, const double *a_blocks, const double *b_blocks,
+               const uint32_t *tri, const int64_t *c_tptr, int64_t nC, double *c_blocks,
+               double *c_sumsq, uint8_t *c_nonzero, int64_t *zero_count, void *stream);
+/* Which numeric kernel qm_numeric uses for this block size: 1 = DMMA (mma.sync f64 tensor core),
+ * 0 = generic FP64 SIMT (odd block sizes). */
+QM_API int qm_numeric_path(int32_t block_size);
+
+/* ---- exact-zero compaction (replaces _put_leaf / _set_block dropping, ops.py:119-122) --------- */
+QM_API size_t qm_compact_workspace_bytes(int64_t nC);
+/* Stream-compacts the C blocks whose c_nonzero flag is set into the *_out arrays (order kept). */
+QM_API int qm_compact(int32_t block_size, int64_t nC, const uint8_t *c_nonzero, const uint64_t *keys_in,
+               const double *blocks_in, const double *sumsq_in, uint64_t *keys_out,
+               double *blocks_out, double *sumsq_out, void *ws, size_t ws_bytes, void *stream);
+
+/* ---- per-block statistics, gather (halo packing) ------------------------------------------- */
+/* sumsq[i] = sum of squares of block i, nonzero[i] = any entry != 0 (nonzero may be NULL). */
+QM_API int qm_block_stats(int32_t block_size, int64_t n, const double *blocks, double *sumsq,
+                   uint8_t *nonzero, void *stream);
+/* dst[i] = src[idx[i]] for whole bs x bs blocks (packs halo blocks for the NVLink exchange). */
+QM_API int qm_gather_blocks(int32_t block_size, const double *src, const int64_t *idx, int64_t n,
+                     double *dst, void *stream);
+
+/* ---- synthetic inputs (device side of the block-keyed generator) -------- */
+/* For each key, fills the block with numpy's default_rng([seed, matrix_id, bi, bj]).uniform(-1, 1,
+ * (bs, bs)) -- bit-identical PCG64 + SeedSequence -- then zeroes entries outside the element
+ * pattern: pattern 0 = dense (clipped to n_logical), 1 = band |i - j| <= half_bw, 2 = band of ones
+ * (the reference generators' value 1.0, generators.py:251-265; no random draws). */
+QM_API int qm_generate_blocks(const qm_layout *layout, const uint64_t *keys, int64_t n, uint64_t seed,
+                       uint32_t matrix_id, int32_t pattern, int64_t half_bw, double *blocks,
+                       double *sumsq, void *stream);
+
+/* ---- FP64 peak microbenchmarks (roofline denominator; MEASURED_PEAKS.json has no FP64) ------ */
+/* Runs `iters` dependent-chain-free DMMA (kind 0) or DFMA (kind 1) steps on `ctas` CTAs of
+ * `threads` threads; returns the flop count of the launch in *flops. */
+QM_API int qm_fp64_peak_kernel(int kind, int ctas, int threads, int64_t iters, double *sink,
+                        double *flops, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QMB200_H */

@@ -1,0 +1,142 @@
+"""ctypes binding of libqmb200.so (include/qmb200.h).
+
+The library is loaded from the package directory (built in-tree by ``_build.build``). There is no
+CPU fallback: when the library or a CUDA device is missing, every compute entry point raises
+``DeviceUnavailableError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+from .errors import (
+    ConfigurationError,
+    DeviceUnavailableError,
+    DimensionMismatchError,
+    QuadmatError,
+    StoreCapacityError,
+)
+
+LIB_PATH = Path(__file__).resolve().parent / "libqmb200.so"
+
+QM_OK, QM_ERR_INVALID, QM_ERR_CUDA, QM_ERR_WORKSPACE, QM_ERR_UNSUPPORTED = 0, -1, -2, -3, -4
+
+# Every symbol include/qmb200.h declares (tests check the .so exports all of them).
+EXPORTS = (
+    "qm_abi_version",
+    "qm_last_error",
+    "qm_launch_count",
+    "qm_encode_keys",
+    "qm_decode_keys",
+    "qm_spgemm_workspace_bytes",
+    "qm_spgemm_count",
+    "qm_spgemm_fill_workspace_bytes",
+    "qm_spgemm_fill",
+    "qm_numeric",
+    "qm_numeric_path",
+    "qm_compact_workspace_bytes",
+    "qm_compact",
+    "qm_block_stats",
+    "qm_gather_blocks",
+    "qm_generate_blocks",
+    "qm_fp64_peak_kernel",
+)
+
+
+class QmLayout(ctypes.Structure):
+    _fields_ = [
+        ("n_logical", ctypes.c_int64),
+        ("leaf_dim", ctypes.c_int32),
+        ("depth", ctypes.c_int32),
+        ("block_size", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+
+def make_layout(params, block_size: int) -> QmLayout:
+    return QmLayout(params.n_logical, params.leaf_dim, params.depth, block_size, 0)
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+_SZ = ctypes.c_size_t
+_LP = ctypes.POINTER(QmLayout)
+
+_SIGS = {
+    "qm_abi_version": (ctypes.c_int, []),
+    "qm_last_error": (ctypes.c_char_p, []),
+    "qm_launch_count": (ctypes.c_uint64, []),
+    "qm_encode_keys": (ctypes.c_int, [_LP, _P, _P, _I64, _P, _P]),
+    "qm_decode_keys": (ctypes.c_int, [_LP, _P, _I64, _P, _P, _P]),
+    "qm_spgemm_workspace_bytes": (_SZ, [_LP, _I64, _I64]),
+    "qm_spgemm_count": (ctypes.c_int, [_LP, _P, _I64, _P, _I64, _P, _SZ, ctypes.POINTER(_I64),
+                                       ctypes.POINTER(_I64), _P]),
+    "qm_spgemm_fill_workspace_bytes": (_SZ, [_LP, _I64]),
+    "qm_spgemm_fill": (ctypes.c_int, [_LP, _P, _I64, _P, _I64, _P, _SZ, _P, _SZ, _P, _P, _P, _P]),
+    "qm_numeric": (ctypes.c_int, [_LP, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P]),
+    "qm_numeric_path": (ctypes.c_int, [_I32]),
+    "qm_compact_workspace_bytes": (_SZ, [_I64]),
+    "qm_compact": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "qm_block_stats": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P]),
+    "qm_gather_blocks": (ctypes.c_int, [_I32, _P, _P, _I64, _P, _P]),
+    "qm_generate_blocks": (ctypes.c_int, [_LP, _P, _I64, ctypes.c_uint64, ctypes.c_uint32, _I32,
+                                          _I64, _P, _P, _P]),
+    "qm_fp64_peak_kernel": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _I64, _P,
+                                           ctypes.POINTER(ctypes.c_double), _P]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
+    """Load (once) and type the library. Raises DeviceUnavailableError if it is not built."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = Path(path) if path else LIB_PATH
+        if not p.exists():
+            raise DeviceUnavailableError(
+                f"{p} is not built; run paper_2011_11762_b200._build.build() (nvcc, sm_100a)"
+            )
+        lib = ctypes.CDLL(str(p))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.qm_abi_version() != 1:
+            raise ConfigurationError(f"libqmb200 ABI {lib.qm_abi_version()} != 1")
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def check(rc: int, what: str) -> None:
+    """Map a qm_status onto the reference's exception types."""
+    if rc == QM_OK:
+        return
+    msg = (load().qm_last_error() or b"").decode(errors="replace")
+    text = f"{what}: {msg}"
+    if rc == QM_ERR_INVALID:
+        if "dimension" in msg or "conform" in msg:
+            raise DimensionMismatchError(text)
+        raise ConfigurationError(text)
+    if rc == QM_ERR_UNSUPPORTED:
+        raise ConfigurationError(text)
+    if rc == QM_ERR_CUDA and ("out of memory" in msg or "memory allocation" in msg):
+        raise StoreCapacityError(text)
+    raise QuadmatError(f"{text} (status {rc})")
+
+
+def ptr(t) -> int:
+    """Raw device pointer of a torch tensor (None -> NULL)."""
+    return 0 if t is None else int(t.data_ptr())
+
+
+def stream_handle(stream) -> int:
+    return 0 if stream is None else int(stream.cuda_stream)

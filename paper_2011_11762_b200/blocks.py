@@ -1,0 +1,162 @@
+"""Device-resident block storage: the B200 replacement of the chunk store for this path.
+
+The reference keeps every quadtree node as an immutable encoded chunk in a ChunkStore
+(chunkstore.py:66-138; leaf payload = BlockSparseLeaf.encode, block_sparse.py:226-231). Here a
+matrix is one ``BlockSet``: three torch tensors on one device --
+
+    keys   int64[n]        ascending quadtree keys (layout.qkey)
+    blocks float64[n,bs,bs] row-major block payloads (the leaf payload's block bytes)
+    sumsq  float64[n]      squared Frobenius norm per block (block_norms, block_sparse.py:41)
+
+``QuadChunk`` stands in for ``ChunkId`` as ``Matrix.root`` (``is_nil``, identity equality), and
+``DeviceStore`` keeps the reference's byte budget (StoreCapacityError, chunkstore.py:86-90).
+Memory is owned by PyTorch; libqmb200 only ever sees raw pointers.
+"""
+
+from __future__ import annotations
+
+import itertools
+import math
+import threading
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .errors import ContractViolationError, StoreCapacityError
+
+
+@dataclass
+class BlockSet:
+    keys: torch.Tensor
+    blocks: torch.Tensor
+    sumsq: torch.Tensor
+
+    @property
+    def n(self) -> int:
+        return int(self.keys.shape[0])
+
+    @property
+    def bs(self) -> int:
+        return int(self.blocks.shape[1])
+
+    @property
+    def device(self) -> torch.device:
+        return self.blocks.device
+
+    @property
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (self.keys, self.blocks, self.sumsq))
+
+    @staticmethod
+    def empty(bs: int, device) -> "BlockSet":
+        return BlockSet(
+            torch.empty(0, dtype=torch.int64, device=device),
+            torch.empty((0, bs, bs), dtype=torch.float64, device=device),
+            torch.empty(0, dtype=torch.float64, device=device),
+        )
+
+    @staticmethod
+    def from_numpy(keys: np.ndarray, blocks: np.ndarray, sumsq: np.ndarray | None, device,
+                   pin: bool = False) -> "BlockSet":
+        if sumsq is None:
+            sumsq = np.einsum("nij,nij->n", blocks, blocks) if blocks.size else np.zeros(0)
+        k = torch.from_numpy(np.ascontiguousarray(keys, dtype=np.int64))
+        b = torch.from_numpy(np.ascontiguousarray(blocks, dtype=np.float64))
+        s = torch.from_numpy(np.ascontiguousarray(sumsq, dtype=np.float64))
+        dev = torch.device(device)
+        if dev.type == "cpu":
+            return BlockSet(k, b, s)
+        return BlockSet(k.to(dev, non_blocking=pin), b.to(dev, non_blocking=pin),
+                        s.to(dev, non_blocking=pin))
+
+    def to_host(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        return (self.keys.cpu().numpy(), self.blocks.cpu().numpy(), self.sumsq.cpu().numpy())
+
+
+class QuadChunk:
+    """Root handle of a matrix value (replaces ``ChunkId``; chunkstore.py:27-41)."""
+
+    __slots__ = ("id", "blockset", "explicit_zero", "__weakref__")
+
+    def __init__(self, cid: int, blockset: BlockSet | None, explicit_zero: bool = False):
+        self.id = cid
+        self.blockset = blockset
+        self.explicit_zero = explicit_zero
+
+    @property
+    def is_nil(self) -> bool:
+        return self.id == 0
+
+    @property
+    def n_blocks(self) -> int:
+        return 0 if self.blockset is None else self.blockset.n
+
+    def require(self) -> BlockSet:
+        if self.blockset is None:
+            raise ContractViolationError("nil chunk id cannot be dereferenced")
+        return self.blockset
+
+    def __eq__(self, other):
+        return isinstance(other, QuadChunk) and other.id == self.id
+
+    def __hash__(self):
+        return hash(self.id)
+
+    def __repr__(self):
+        return "NIL" if self.id == 0 else f"QuadChunk({self.id}, blocks={self.n_blocks})"
+
+
+NIL = QuadChunk(0, None)
+
+
+class DeviceStore:
+    """Byte-budgeted registry of matrix values on one device.
+
+    Unlike the reference store (which never frees) a value's memory is released
+    when the last Python reference to its ``QuadChunk`` goes away; the budget counts live bytes.
+    """
+
+    def __init__(self, device, max_bytes: int | None = None):
+        self.device = torch.device(device)
+        self._max_bytes = max_bytes
+        self._live = 0
+        self._ids = itertools.count(1)
+        self._lock = threading.Lock()
+        self.n_registered = 0
+
+    def _release(self, nbytes: int):
+        with self._lock:
+            self._live -= nbytes
+
+    def register(self, blockset: BlockSet, explicit_zero: bool = False) -> QuadChunk:
+        if blockset.n == 0 and not explicit_zero:
+            return NIL
+        size = blockset.nbytes
+        with self._lock:
+            if self._max_bytes is not None and self._live + size > self._max_bytes:
+                raise StoreCapacityError(
+                    f"store capacity exhausted: {self._live} + {size} > {self._max_bytes} bytes"
+                )
+            self._live += size
+            self.n_registered += 1
+            cid = next(self._ids)
+        chunk = QuadChunk(cid, blockset, explicit_zero)
+        weakref.finalize(chunk, self._release, size)
+        return chunk
+
+    def check_room(self, extra_bytes: int):
+        if self._max_bytes is not None and self._live + extra_bytes > self._max_bytes:
+            raise StoreCapacityError(
+                f"store capacity exhausted: {self._live} + {extra_bytes} > {self._max_bytes} bytes"
+            )
+
+    @property
+    def total_bytes(self) -> int:
+        return self._live
+
+    def norm_of(self, chunk: QuadChunk) -> float:
+        if chunk.is_nil or chunk.blockset is None or chunk.blockset.n == 0:
+            return 0.0
+        return math.sqrt(float(chunk.blockset.sumsq.sum().item()))

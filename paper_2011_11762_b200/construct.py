@@ -1,0 +1,107 @@
+"""Host-side construction of block sets (the caller side of the path).
+
+``blocks_from_triplets`` reproduces the reference's normalised build bit for bit:
+quadtree.build_from_triplets (quadtree.py:90-142) partitions entries by quadrant, keeping their
+input order, and BlockSparseLeaf.from_triplets (leaves/block_sparse.py:47-68) stable-sorts a leaf's
+entries by block and sums duplicates with ``np.add.at`` into a zero block, dropping blocks that are
+exactly zero (``np.any``, :37-41). A single stable sort by quadtree key yields the same per-block
+entry order, so duplicate sums are identical; the result is the stored block set in key order.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .errors import ContractViolationError, OutOfRangeError
+from .layout import Geometry
+
+
+def _check_range(n_logical: int, rows: np.ndarray, cols: np.ndarray):
+    if rows.size and (
+        rows.min() < 0 or rows.max() >= n_logical or cols.min() < 0 or cols.max() >= n_logical
+    ):
+        raise OutOfRangeError(f"entry index outside [0, {n_logical})")
+
+
+def mirror_symmetric(rows, cols, vals, leaf_dim: int):
+    """session.py:88-100: symmetric input is upper-triangle triplets; entries inside a diagonal
+    leaf tile are mirrored so diagonal leaves hold full blocks."""
+    if np.any(rows > cols):
+        raise ContractViolationError("symmetric matrices are built from upper-triangle triplets")
+    mirror = (rows != cols) & (rows // leaf_dim == cols // leaf_dim)
+    return (
+        np.concatenate([rows, cols[mirror]]),
+        np.concatenate([cols, rows[mirror]]),
+        np.concatenate([vals, vals[mirror]]),
+    )
+
+
+def blocks_from_triplets(geom: Geometry, rows, cols, vals):
+    """Returns (keys int64[n], blocks float64[n,bs,bs]) of the stored (nonzero) blocks."""
+    rows = np.asarray(rows, dtype=np.int64).ravel()
+    cols = np.asarray(cols, dtype=np.int64).ravel()
+    vals = np.asarray(vals, dtype=np.float64).ravel()
+    _check_range(geom.params.n_logical, rows, cols)
+    bs = geom.bs
+    if rows.size == 0:
+        return np.zeros(0, np.int64), np.zeros((0, bs, bs))
+    bi, lr = np.divmod(rows, bs)
+    bj, lc = np.divmod(cols, bs)
+    key = geom.qkey(bi, bj)
+    order = np.argsort(key, kind="stable")
+    ks = key[order]
+    starts = np.flatnonzero(np.concatenate([[True], ks[1:] != ks[:-1]]))
+    ukeys = ks[starts]
+    blk_of = np.repeat(np.arange(starts.size), np.diff(np.append(starts, ks.size)))
+    flat = blk_of * (bs * bs) + lr[order] * bs + lc[order]
+    buf = np.zeros(starts.size * bs * bs)
+    v = vals[order]
+    if np.unique(flat).size == flat.size:
+        buf[flat] = v + 0.0  # 0.0 + v as np.add.at does (turns -0.0 into +0.0)
+    else:
+        np.add.at(buf, flat, v)
+    blocks = buf.reshape(starts.size, bs, bs)
+    keep = np.any(blocks != 0.0, axis=(1, 2)) | np.isnan(blocks).any(axis=(1, 2))
+    return ukeys[keep], np.ascontiguousarray(blocks[keep])
+
+
+def blocks_from_tiles(geom: Geometry, tile_fn, support_fn):
+    """quadtree.build_from_tiles (quadtree.py:145-193) for block-sparse leaves: walks the tree,
+    skipping subtrees without support, and cuts each leaf tile into blocks (from_dense,
+    block_sparse.py:70-83). Returns (keys, blocks) in key order."""
+    p = geom.params
+    bs, nbl = geom.bs, geom.nbl
+    keys, blocks = [], []
+
+    def build(level, r0, c0):
+        dim = p.node_dim(level)
+        if r0 >= p.n_logical or c0 >= p.n_logical:
+            return
+        if not support_fn(r0, min(r0 + dim, p.n_logical), c0, min(c0 + dim, p.n_logical)):
+            return
+        if level == p.depth:
+            tile = tile_fn(r0, c0)
+            if tile is None or not np.any(tile):
+                return
+            t = np.asarray(tile, dtype=np.float64).reshape(nbl, bs, nbl, bs).transpose(0, 2, 1, 3)
+            for bi in range(nbl):
+                for bj in range(nbl):
+                    blk = t[bi, bj]
+                    if np.any(blk):
+                        keys.append(geom.qkey(r0 // bs + bi, c0 // bs + bj))
+                        blocks.append(np.ascontiguousarray(blk))
+            return
+        half = dim // 2
+        for dr, dc in ((0, 0), (0, half), (half, 0), (half, half)):
+            build(level + 1, r0 + dr, c0 + dc)
+
+    build(0, 0, 0)
+    if not keys:
+        return np.zeros(0, np.int64), np.zeros((0, bs, bs))
+    return np.asarray(keys, dtype=np.int64).ravel(), np.stack(blocks)
+
+
+def identity_triplets(n: int, c: float):
+    """add_scaled_identity on a nil matrix (ops.py:253-270): c on the logical diagonal only."""
+    d = np.arange(n, dtype=np.int64)
+    return d, d, np.full(n, float(c))

@@ -1,0 +1,184 @@
+// C-ABI plumbing of libqmb200: error state, launch counter, key encode/decode, exact-zero
+// compaction and block gather (halo packing).
+#include <cub/cub.cuh>
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <atomic>
+
+#include "qm_common.cuh"
+
+namespace qm {
+
+static thread_local char t_err[1024] = "";
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(t_err, sizeof(t_err), fmt, ap);
+  va_end(ap);
+}
+
+void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+int launch_block_stats(int bs, int64_t n, const double *blocks, double *sumsq, uint8_t *nonzero,
+                       int64_t *zero_count, cudaStream_t st);
+
+namespace {
+
+inline int grid_for(int64_t n, int threads = 256) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)g;
+}
+
+__global__ void k_encode(const int32_t *bi, const int32_t *bj, int64_t n, int nbl, int lbits,
+                         uint64_t *keys) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+       x += (int64_t)gridDim.x * blockDim.x)
+    keys[x] = qkey((uint32_t)bi[x], (uint32_t)bj[x], nbl, lbits);
+}
+
+__global__ void k_decode(const uint64_t *keys, int64_t n, int nbl, int lbits, int32_t *bi,
+                         int32_t *bj) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t r, c;
+    qkey_decode(keys[x], nbl, lbits, &r, &c);
+    bi[x] = (int32_t)r;
+    bj[x] = (int32_t)c;
+  }
+}
+
+__global__ void k_flags_to_i64(const uint8_t *f, int64_t n, int64_t *out) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+       x += (int64_t)gridDim.x * blockDim.x)
+    out[x] = f[x] ? 1 : 0;
+}
+
+// One CTA per block: copies the kept blocks to their compacted slot.
+__global__ void __launch_bounds__(256) k_compact(int bs, int64_t n, const uint8_t *flags,
+                                                 const int64_t *pos, const uint64_t *keys_in,
+                                                 const double *blocks_in, const double *sumsq_in,
+                                                 uint64_t *keys_out, double *blocks_out,
+                                                 double *sumsq_out) {
+  const int64_t elems = (int64_t)bs * bs;
+  for (int64_t m = blockIdx.x; m < n; m += gridDim.x) {
+    if (!flags[m]) continue;
+    const int64_t d = pos[m];
+    if (threadIdx.x == 0) {
+      keys_out[d] = keys_in[m];
+      if (sumsq_out) sumsq_out[d] = sumsq_in[m];
+    }
+    const double *s = blocks_in + (size_t)m * elems;
+    double *o = blocks_out + (size_t)d * elems;
+    for (int64_t e = threadIdx.x; e < elems; e += blockDim.x) o[e] = s[e];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_gather_blocks(int bs, const double *src, const int64_t *idx,
+                                                       int64_t n, double *dst) {
+  const int64_t elems = (int64_t)bs * bs;
+  for (int64_t m = blockIdx.x; m < n; m += gridDim.x) {
+    const double *s = src + (size_t)idx[m] * elems;
+    double *o = dst + (size_t)m * elems;
+    if ((elems & 1) == 0) {
+      const double2 *s2 = reinterpret_cast<const double2 *>(s);
+      double2 *o2 = reinterpret_cast<double2 *>(o);
+      for (int64_t e = threadIdx.x; e < elems / 2; e += blockDim.x) o2[e] = s2[e];
+    } else {
+      for (int64_t e = threadIdx.x; e < elems; e += blockDim.x) o[e] = s[e];
+    }
+  }
+}
+
+size_t compact_cub_bytes(int64_t n) {
+  size_t b = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t *)nullptr, (int64_t *)nullptr, n);
+  return b;
+}
+
+}  // namespace
+}  // namespace qm
+
+using namespace qm;
+
+extern "C" int qm_abi_version(void) { return QM_ABI_VERSION; }
+
+extern "C" const char *qm_last_error(void) { return qm::t_err; }
+
+extern "C" uint64_t qm_launch_count(void) { return qm::g_launches.load(std::memory_order_relaxed); }
+
+extern "C" int qm_encode_keys(const qm_layout *layout, const int32_t *bi, const int32_t *bj, int64_t n,
+                              uint64_t *keys, void *stream) {
+  Geometry g;
+  int rc = make_geometry(layout, &g);
+  if (rc != QM_OK) return rc;
+  if (n <= 0) return QM_OK;
+  k_encode<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(bi, bj, n, g.nbl, g.lbits, keys);
+  QM_LAUNCHED("k_encode");
+  return QM_OK;
+}
+
+extern "C" int qm_decode_keys(const qm_layout *layout, const uint64_t *keys, int64_t n, int32_t *bi,
+                              int32_t *bj, void *stream) {
+  Geometry g;
+  int rc = make_geometry(layout, &g);
+  if (rc != QM_OK) return rc;
+  if (n <= 0) return QM_OK;
+  k_decode<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(keys, n, g.nbl, g.lbits, bi, bj);
+  QM_LAUNCHED("k_decode");
+  return QM_OK;
+}
+
+extern "C" size_t qm_compact_workspace_bytes(int64_t nC) {
+  Carver cv(nullptr, 0);
+  cv.take<int64_t>(nC);
+  cv.take<int64_t>(nC);
+  cv.take<char>(compact_cub_bytes(nC));
+  return cv.off;
+}
+
+extern "C" int qm_compact(int32_t block_size, int64_t nC, const uint8_t *c_nonzero,
+                          const uint64_t *keys_in, const double *blocks_in, const double *sumsq_in,
+                          uint64_t *keys_out, double *blocks_out, double *sumsq_out, void *ws,
+                          size_t ws_bytes, void *stream) {
+  if (block_size < 1 || nC < 0) {
+    set_error("qm_compact: bad arguments");
+    return QM_ERR_INVALID;
+  }
+  if (nC == 0) return QM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Carver cv(ws, ws_bytes);
+  int64_t *f64 = cv.take<int64_t>(nC);
+  int64_t *pos = cv.take<int64_t>(nC);
+  size_t cb = compact_cub_bytes(nC);
+  void *cub = cv.take<char>(cb);
+  if (!cv.ok() || !ws) {
+    set_error("qm_compact: workspace %zu < required %zu", ws_bytes, cv.off);
+    return QM_ERR_WORKSPACE;
+  }
+  k_flags_to_i64<<<grid_for(nC), 256, 0, st>>>(c_nonzero, nC, f64);
+  QM_LAUNCHED("k_flags_to_i64");
+  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub, cb, f64, pos, nC, st));
+  int64_t grid = std::min<int64_t>(nC, 148 * 16);
+  k_compact<<<(int)grid, 256, 0, st>>>(block_size, nC, c_nonzero, pos, keys_in, blocks_in, sumsq_in,
+                                       keys_out, blocks_out, sumsq_out);
+  QM_LAUNCHED("k_compact");
+  return QM_OK;
+}
+
+extern "C" int qm_gather_blocks(int32_t block_size, const double *src, const int64_t *idx, int64_t n,
+                                double *dst, void *stream) {
+  if (block_size < 1 || n < 0) {
+    set_error("qm_gather_blocks: bad arguments");
+    return QM_ERR_INVALID;
+  }
+  if (n == 0) return QM_OK;
+  int64_t grid = std::min<int64_t>(n, 148 * 16);
+  k_gather_blocks<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(block_size, src, idx, n, dst);
+  QM_LAUNCHED("k_gather_blocks");
+  return QM_OK;
+}

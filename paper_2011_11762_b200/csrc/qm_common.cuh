@@ -1,0 +1,128 @@
+// Shared helpers of libqmb200: error reporting, launch accounting, quadtree-key arithmetic.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/qmb200.h"
+
+namespace qm {
+
+// Thread-local last-error message (qm_last_error).
+void set_error(const char *fmt, ...);
+// Counts one kernel launch (qm_launch_count).
+void note_launch(int n = 1);
+
+#define QM_CUDA_TRY(expr)                                                                   \
+  do {                                                                                      \
+    cudaError_t qm_e_ = (expr);                                                             \
+    if (qm_e_ != cudaSuccess) {                                                             \
+      qm::set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(qm_e_), __FILE__,    \
+                    __LINE__);                                                              \
+      return QM_ERR_CUDA;                                                                   \
+    }                                                                                       \
+  } while (0)
+
+// Launch check: records the launch and turns a launch error into a QM_ERR_CUDA return.
+#define QM_LAUNCHED(name)                                                                   \
+  do {                                                                                      \
+    qm::note_launch();                                                                      \
+    cudaError_t qm_e_ = cudaGetLastError();                                                 \
+    if (qm_e_ != cudaSuccess) {                                                             \
+      qm::set_error("launch of %s failed: %s", name, cudaGetErrorString(qm_e_));           \
+      return QM_ERR_CUDA;                                                                   \
+    }                                                                                       \
+  } while (0)
+
+// Derived geometry of a qm_layout.
+struct Geometry {
+  int32_t bs;     // block size
+  int32_t nbl;    // blocks per leaf side = leaf_dim / bs
+  int32_t lbits;  // bits of the in-leaf coordinate = ceil(log2(nbl))
+  int32_t depth;  // quadtree depth
+  int64_t nbg;    // blocks per matrix side = nbl << depth
+};
+
+inline int make_geometry(const qm_layout *l, Geometry *g) {
+  if (!l) { set_error("layout is NULL"); return QM_ERR_INVALID; }
+  if (l->block_size < 1 || l->leaf_dim < 1 || l->depth < 0 || l->n_logical < 1) {
+    set_error("invalid layout (n=%lld leaf_dim=%d depth=%d bs=%d)", (long long)l->n_logical,
+              l->leaf_dim, l->depth, l->block_size);
+    return QM_ERR_INVALID;
+  }
+  if (l->leaf_dim % l->block_size != 0) {
+    set_error("block size %d must divide leaf dimension %d", l->block_size, l->leaf_dim);
+    return QM_ERR_INVALID;
+  }
+  g->bs = l->block_size;
+  g->nbl = l->leaf_dim / l->block_size;
+  int lb = 0;
+  while ((1 << lb) < g->nbl) ++lb;
+  g->lbits = lb;
+  g->depth = l->depth;
+  g->nbg = (int64_t)g->nbl << l->depth;
+  if (2 * (l->depth + lb) > 62 || g->nbg > (int64_t)1 << 30) {
+    set_error("layout too large for 64-bit quadtree keys (depth=%d lbits=%d)", l->depth, lb);
+    return QM_ERR_UNSUPPORTED;
+  }
+  return QM_OK;
+}
+
+// Interleave: bit b of x -> bit 2b.
+__host__ __device__ __forceinline__ uint64_t spread_bits(uint32_t x) {
+  uint64_t v = x;
+  v = (v | (v << 16)) & 0x0000FFFF0000FFFFull;
+  v = (v | (v << 8)) & 0x00FF00FF00FF00FFull;
+  v = (v | (v << 4)) & 0x0F0F0F0F0F0F0F0Full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+
+// Inverse of spread_bits on the even bits of v.
+__host__ __device__ __forceinline__ uint32_t compact_bits(uint64_t v) {
+  v &= 0x5555555555555555ull;
+  v = (v | (v >> 1)) & 0x3333333333333333ull;
+  v = (v | (v >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+  v = (v | (v >> 4)) & 0x00FF00FF00FF00FFull;
+  v = (v | (v >> 8)) & 0x0000FFFF0000FFFFull;
+  v = (v | (v >> 16)) & 0x00000000FFFFFFFFull;
+  return (uint32_t)v;
+}
+
+// Quadtree key of block (bi, bj): Morton over the leaf grid (row bit high, so NW<NE<SW<SE as in
+// quadtree.py:128-129), then row-major inside the leaf (BlockSparseLeaf.encode sorts (bi, bj)).
+__host__ __device__ __forceinline__ uint64_t qkey(uint32_t bi, uint32_t bj, int nbl, int lbits) {
+  uint32_t li = bi / nbl, lj = bj / nbl;
+  uint32_t ri = bi - li * nbl, rj = bj - lj * nbl;
+  uint64_t m = (spread_bits(li) << 1) | spread_bits(lj);
+  return (m << (2 * lbits)) | ((uint64_t)ri << lbits) | rj;
+}
+
+__host__ __device__ __forceinline__ void qkey_decode(uint64_t key, int nbl, int lbits, uint32_t *bi,
+                                                     uint32_t *bj) {
+  uint64_t local = key & ((1ull << (2 * lbits)) - 1ull);
+  uint32_t ri = (uint32_t)(local >> lbits);
+  uint32_t rj = (uint32_t)(local & ((1ull << lbits) - 1ull));
+  uint64_t m = key >> (2 * lbits);
+  uint32_t li = compact_bits(m >> 1), lj = compact_bits(m);
+  *bi = li * nbl + ri;
+  *bj = lj * nbl + rj;
+}
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// Bump allocator over a caller workspace.
+struct Carver {
+  char *base;
+  size_t cap, off;
+  Carver(void *p, size_t c) : base((char *)p), cap(c), off(0) {}
+  template <class T> T *take(size_t count) {
+    size_t at = align_up(off);
+    off = at + align_up(count * sizeof(T));
+    return base ? (T *)(base + at) : nullptr;
+  }
+  bool ok() const { return off <= cap; }
+};
+
+}  // namespace qm

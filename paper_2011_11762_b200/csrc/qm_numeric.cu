@@ -1,0 +1,386 @@
+// Numeric phase: grouped FP64 block products accumulated per C block.
+//
+// Replaces BlockSparseLeaf.multiply (leaves/block_sparse.py:112-132: `prod = a @ b`,
+// `acc = acc + prod`) and the cross-level sums of _add_body / BlockSparseLeaf.add
+// (ops.py:147-159, block_sparse.py:134-152). Each C block is owned by one CTA for its whole k list,
+// accumulated in registers, with no atomics and a fixed summation order; the epilogue fuses the
+// exact-zero test and the Frobenius norm of _set_block (block_sparse.py:37-41).
+//
+// Tensor-core path (block sizes 16/32/64/128): sm_100a has no FP64 tcgen05 kind, so FP64 tensor
+// math is the warp-level mma.sync.m8n8k4.f64 (SASS DMMA). Operands are staged into padded shared
+// memory (row stride = cols + 4 doubles, which makes both fragment patterns bank-conflict free) by
+// a multi-stage cp.async pipeline that streams k-panels continuously across triples and C blocks.
+// CTAs are persistent and walk C blocks in quadtree-key order (grid-stride), so concurrently
+// running CTAs touch neighbouring block rows/columns of A and B and reuse them from L2.
+#include <cuda_runtime.h>
+
+#include "qm_common.cuh"
+
+namespace qm {
+namespace {
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// D = A(8x4, row) * B(4x8, col) + D, fp64. Fragments: a = A[lane>>2][lane&3],
+// b = B[lane&3][lane>>2], d = D[lane>>2][2*(lane&3) + {0,1}].
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int BS_, int WARPS_M_, int WARPS_N_, int KP_, int STAGES_, int MINB_>
+struct DmmaCfg {
+  static constexpr int BS = BS_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, KP = KP_, STAGES = STAGES_;
+  static constexpr int MINB = MINB_;
+  static constexpr int NTHR = 32 * WARPS_M * WARPS_N;
+  static constexpr int TM = BS / WARPS_M, TN = BS / WARPS_N;  // warp tile
+  static constexpr int MT = TM / 8, NT = TN / 8;               // mma tiles per warp
+  static constexpr int NP = BS / KP;                           // k panels per triple
+  static constexpr int LDA = KP + 4, LDB = BS + 4;             // padded smem row strides (doubles)
+  static constexpr int A_ELEMS = BS * LDA, B_ELEMS = KP * LDB;
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_ELEMS * sizeof(double) + 64 * sizeof(double);
+  static_assert(BS % (8 * WARPS_M) == 0 && BS % (8 * WARPS_N) == 0, "warp tiling");
+  static_assert(BS % KP == 0 && KP % 4 == 0, "panel");
+};
+
+// Stage cursor: C block `item`, triple t of [t, tend), k panel p.
+struct Cursor {
+  int64_t item, t, tend;
+  int p;
+};
+
+template <class Cfg>
+__device__ __forceinline__ void cursor_start(Cursor &c, int64_t item, int64_t nC, const int64_t *tptr) {
+  c.item = item;
+  c.p = 0;
+  if (item < nC) {
+    c.t = tptr[item];
+    c.tend = tptr[item + 1];
+  } else {
+    c.t = c.tend = 0;
+  }
+}
+
+template <class Cfg>
+__device__ __forceinline__ void cursor_next(Cursor &c, int64_t nC, const int64_t *tptr) {
+  if (++c.p == Cfg::NP) {
+    c.p = 0;
+    if (++c.t == c.tend) cursor_start<Cfg>(c, c.item + gridDim.x, nC, tptr);
+  }
+}
+
+template <class Cfg>
+__device__ __forceinline__ void issue_stage(double *stage, const double *__restrict__ A,
+                                            const double *__restrict__ B, const uint2 *__restrict__ tri,
+                                            const Cursor &c) {
+  constexpr int BS = Cfg::BS, KP = Cfg::KP;
+  const uint2 ab = tri[c.t];
+  const double *asrc = A + (size_t)ab.x * (BS * BS) + c.p * KP;
+  const double *bsrc = B + (size_t)ab.y * (BS * BS) + (size_t)c.p * KP * BS;
+  double *sA = stage;
+  double *sB = stage + Cfg::A_ELEMS;
+  constexpr int ACH = KP / 2;  // 16-byte chunks per A panel row
+  for (int q = threadIdx.x; q < BS * ACH; q += Cfg::NTHR) {
+    int r = q / ACH, cc = q % ACH;
+    cp_async16(sA + r * Cfg::LDA + 2 * cc, asrc + (size_t)r * BS + 2 * cc);
+  }
+  constexpr int BCH = BS / 2;  // 16-byte chunks per B panel row
+  for (int q = threadIdx.x; q < KP * BCH; q += Cfg::NTHR) {
+    int r = q / BCH, cc = q % BCH;
+    cp_async16(sB + r * Cfg::LDB + 2 * cc, bsrc + (size_t)r * BS + 2 * cc);
+  }
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
+    k_numeric_dmma(const double *__restrict__ A, const double *__restrict__ B,
+                   const uint2 *__restrict__ tri, const int64_t *__restrict__ tptr, int64_t nC,
+                   double *__restrict__ C, double *__restrict__ csq, uint8_t *__restrict__ cnz,
+                   int64_t *__restrict__ zero_count) {
+  extern __shared__ __align__(16) double smem[];
+  double *red = smem + (size_t)Cfg::STAGES * Cfg::STAGE_ELEMS;  // 64 doubles for the epilogue
+  constexpr int BS = Cfg::BS, MT = Cfg::MT, NT = Cfg::NT, STAGES = Cfg::STAGES;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int wm0 = (warp / Cfg::WARPS_N) * Cfg::TM;
+  const int wn0 = (warp % Cfg::WARPS_N) * Cfg::TN;
+
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  Cursor L, Cc;
+  cursor_start<Cfg>(L, blockIdx.x, nC, tptr);
+  Cc = L;
+
+#pragma unroll 1
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (L.item < nC) {
+      issue_stage<Cfg>(smem + (size_t)s * Cfg::STAGE_ELEMS, A, B, tri, L);
+      cursor_next<Cfg>(L, nC, tptr);
+    }
+    cp_async_commit();
+  }
+  int cs = 0, ls = STAGES - 1;
+
+#pragma unroll 1
+  while (Cc.item < nC) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    if (L.item < nC) {
+      issue_stage<Cfg>(smem + (size_t)ls * Cfg::STAGE_ELEMS, A, B, tri, L);
+      cursor_next<Cfg>(L, nC, tptr);
+    }
+    cp_async_commit();
+    ls = (ls + 1 == STAGES) ? 0 : ls + 1;
+
+    const double *sA = smem + (size_t)cs * Cfg::STAGE_ELEMS;
+    const double *sB = sA + Cfg::A_ELEMS;
+    const double *pa = sA + (wm0 + g) * Cfg::LDA + tq;
+    const double *pb = sB + tq * Cfg::LDB + wn0 + g;
+#pragma unroll
+    for (int ks = 0; ks < Cfg::KP / 4; ++ks) {
+      double af[MT], bf[NT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) af[i] = pa[i * 8 * Cfg::LDA + ks * 4];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) bf[j] = pb[ks * 4 * Cfg::LDB + j * 8];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    cs = (cs + 1 == STAGES) ? 0 : cs + 1;
+
+    if (Cc.p == Cfg::NP - 1 && Cc.t + 1 == Cc.tend) {
+      // Epilogue: store the C block, fused sum of squares + nonzero test (fixed order).
+      const int64_t m = Cc.item;
+      double *cb = C + (size_t)m * (BS * BS);
+      double ss = 0.0;
+      bool nz = false;
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const double v0 = acc[i][j][0], v1 = acc[i][j][1];
+          *reinterpret_cast<double2 *>(cb + (size_t)(wm0 + i * 8 + g) * BS + wn0 + j * 8 + 2 * tq) =
+              make_double2(v0, v1);
+          ss = fma(v0, v0, ss);
+          ss = fma(v1, v1, ss);
+          nz |= (v0 != 0.0) | (v1 != 0.0);
+          acc[i][j][0] = acc[i][j][1] = 0.0;
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      const bool wnz = __any_sync(0xffffffffu, nz);
+      if (lane == 0) {
+        red[warp] = ss;
+        red[32 + warp] = wnz ? 1.0 : 0.0;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double tot = 0.0, anynz = 0.0;
+        for (int w = 0; w < Cfg::NTHR / 32; ++w) {
+          tot += red[w];
+          anynz += red[32 + w];
+        }
+        csq[m] = tot;
+        cnz[m] = anynz != 0.0;
+        if (anynz == 0.0 && zero_count) atomicAdd((unsigned long long *)zero_count, 1ull);
+      }
+    }
+    cursor_next<Cfg>(Cc, nC, tptr);
+  }
+  cp_async_wait<0>();
+}
+
+// Generic FP64 SIMT path for block sizes without a tensor-core variant: one CTA per
+// (C block, 32x32 sub-tile), 4 outputs per thread.
+__global__ void __launch_bounds__(256) k_numeric_generic(const double *__restrict__ A,
+                                                         const double *__restrict__ B,
+                                                         const uint2 *__restrict__ tri,
+                                                         const int64_t *__restrict__ tptr, int64_t nC,
+                                                         int bs, double *__restrict__ C) {
+  __shared__ double As[32][33];
+  __shared__ double Bs[32][33];
+  const int nsub = (bs + 31) / 32;
+  const int64_t nwork = nC * nsub * nsub;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const int64_t m = w / (nsub * nsub);
+    const int sub = (int)(w % (nsub * nsub));
+    const int r0 = (sub / nsub) * 32, c0 = (sub % nsub) * 32;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t t = tptr[m]; t < tptr[m + 1]; ++t) {
+      const uint2 ab = tri[t];
+      const double *a = A + (size_t)ab.x * bs * bs;
+      const double *b = B + (size_t)ab.y * bs * bs;
+      for (int kc = 0; kc < bs; kc += 32) {
+        for (int q = 0; q < 4; ++q) {
+          const int r = ty + 8 * q;
+          As[r][tx] = (r0 + r < bs && kc + tx < bs) ? a[(size_t)(r0 + r) * bs + kc + tx] : 0.0;
+          Bs[r][tx] = (kc + r < bs && c0 + tx < bs) ? b[(size_t)(kc + r) * bs + c0 + tx] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < 32; ++kk) {
+          const double bv = Bs[kk][tx];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q] = fma(As[ty + 8 * q][kk], bv, acc[q]);
+        }
+        __syncthreads();
+      }
+    }
+    double *cb = C + (size_t)m * bs * bs;
+    for (int q = 0; q < 4; ++q) {
+      const int r = r0 + ty + 8 * q, c = c0 + tx;
+      if (r < bs && c < bs) cb[(size_t)r * bs + c] = acc[q];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_block_stats(const double *__restrict__ blocks, int64_t n,
+                                                     int bs, double *sumsq, uint8_t *nonzero,
+                                                     int64_t *zero_count) {
+  __shared__ double red[8];
+  __shared__ int rnz[8];
+  const int64_t elems = (int64_t)bs * bs;
+  for (int64_t m = blockIdx.x; m < n; m += gridDim.x) {
+    const double *b = blocks + (size_t)m * elems;
+    double ss = 0.0;
+    bool nz = false;
+    for (int64_t e = threadIdx.x; e < elems; e += blockDim.x) {
+      const double v = b[e];
+      ss = fma(v, v, ss);
+      nz |= v != 0.0;
+    }
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const bool wnz = __any_sync(0xffffffffu, nz);
+    if ((threadIdx.x & 31) == 0) {
+      red[threadIdx.x >> 5] = ss;
+      rnz[threadIdx.x >> 5] = wnz;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      int any = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        tot += red[w];
+        any |= rnz[w];
+      }
+      if (sumsq) sumsq[m] = tot;
+      if (nonzero) nonzero[m] = (uint8_t)any;
+      if (!any && zero_count) atomicAdd((unsigned long long *)zero_count, 1ull);
+    }
+    __syncthreads();
+  }
+}
+
+int g_sm_count = 0;
+
+int sm_count() {
+  if (g_sm_count == 0) {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    g_sm_count = n > 0 ? n : 148;
+  }
+  return g_sm_count;
+}
+
+template <class Cfg>
+int launch_dmma(const double *A, const double *B, const uint2 *tri, const int64_t *tptr, int64_t nC,
+                double *C, double *csq, uint8_t *cnz, int64_t *zc, cudaStream_t st) {
+  static bool configured = false;  // benign race: idempotent attribute set
+  if (!configured) {
+    QM_CUDA_TRY(cudaFuncSetAttribute(k_numeric_dmma<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)Cfg::SMEM));
+    configured = true;
+  }
+  int per_sm = 0;
+  QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_numeric_dmma<Cfg>, Cfg::NTHR,
+                                                            Cfg::SMEM));
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)sm_count() * per_sm;
+  if (grid > nC) grid = nC;
+  k_numeric_dmma<Cfg><<<(int)grid, Cfg::NTHR, Cfg::SMEM, st>>>(A, B, tri, tptr, nC, C, csq, cnz, zc);
+  QM_LAUNCHED("k_numeric_dmma");
+  return QM_OK;
+}
+
+//                       BS  WM WN  KP  STAGES MINB
+using Cfg16 = DmmaCfg<16, 1, 2, 16, 4, 8>;
+using Cfg32 = DmmaCfg<32, 2, 2, 32, 4, 3>;
+using Cfg64 = DmmaCfg<64, 2, 2, 32, 3, 2>;
+using Cfg128 = DmmaCfg<128, 2, 4, 16, 4, 1>;
+
+}  // namespace
+
+int launch_block_stats(int bs, int64_t n, const double *blocks, double *sumsq, uint8_t *nonzero,
+                       int64_t *zero_count, cudaStream_t st) {
+  if (n <= 0) return QM_OK;
+  int64_t grid = std::min<int64_t>(n, (int64_t)sm_count() * 16);
+  k_block_stats<<<(int)grid, 256, 0, st>>>(blocks, n, bs, sumsq, nonzero, zero_count);
+  QM_LAUNCHED("k_block_stats");
+  return QM_OK;
+}
+
+int numeric_sm_count() { return sm_count(); }
+
+}  // namespace qm
+
+using namespace qm;
+
+extern "C" int qm_numeric_path(int32_t bs) {
+  return (bs == 16 || bs == 32 || bs == 64 || bs == 128) ? 1 : 0;
+}
+
+extern "C" int qm_numeric(const qm_layout *layout, const double *a_blocks, const double *b_blocks,
+                          const uint32_t *tri, const int64_t *c_tptr, int64_t nC, double *c_blocks,
+                          double *c_sumsq, uint8_t *c_nonzero, int64_t *zero_count, void *stream) {
+  Geometry g;
+  int rc = make_geometry(layout, &g);
+  if (rc != QM_OK) return rc;
+  if (nC < 0) {
+    set_error("qm_numeric: negative nC");
+    return QM_ERR_INVALID;
+  }
+  if (nC == 0) return QM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint2 *t2 = (const uint2 *)tri;
+  switch (g.bs) {
+    case 16: return launch_dmma<Cfg16>(a_blocks, b_blocks, t2, c_tptr, nC, c_blocks, c_sumsq, c_nonzero, zero_count, st);
+    case 32: return launch_dmma<Cfg32>(a_blocks, b_blocks, t2, c_tptr, nC, c_blocks, c_sumsq, c_nonzero, zero_count, st);
+    case 64: return launch_dmma<Cfg64>(a_blocks, b_blocks, t2, c_tptr, nC, c_blocks, c_sumsq, c_nonzero, zero_count, st);
+    case 128: return launch_dmma<Cfg128>(a_blocks, b_blocks, t2, c_tptr, nC, c_blocks, c_sumsq, c_nonzero, zero_count, st);
+    default: break;
+  }
+  const int nsub = (g.bs + 31) / 32;
+  int64_t work = nC * nsub * nsub;
+  int64_t grid = std::min<int64_t>(work, (int64_t)sm_count() * 8);
+  k_numeric_generic<<<(int)grid, 256, 0, st>>>(a_blocks, b_blocks, t2, c_tptr, nC, g.bs, c_blocks);
+  QM_LAUNCHED("k_numeric_generic");
+  return launch_block_stats(g.bs, nC, c_blocks, c_sumsq, c_nonzero, zero_count, st);
+}
+
+extern "C" int qm_block_stats(int32_t block_size, int64_t n, const double *blocks, double *sumsq,
+                              uint8_t *nonzero, void *stream) {
+  if (block_size < 1 || n < 0) {
+    set_error("qm_block_stats: bad arguments");
+    return QM_ERR_INVALID;
+  }
+  return launch_block_stats(block_size, n, blocks, sumsq, nonzero, nullptr, (cudaStream_t)stream);
+}

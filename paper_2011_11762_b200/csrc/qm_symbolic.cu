@@ -1,0 +1,520 @@
+// Symbolic phase of C = A*B on quadtree-key-ordered block matrices.
+//
+// Replaces the reference's recursive task expansion: _multiply_body (ops.py:197-241) spawns, for
+// every non-nil (A-node, B-node) pair, C_ij <- A_i0*B_0j + A_i1*B_1j, and nil operands end the
+// recursion through _multiply_fallback (ops.py:244-245, engine.py:306-307). The non-nil leaf-level
+// multiply tasks are exactly the block triples (i,k,j) with A(i,k) and B(k,j) stored, and the C
+// block set is the set of (i,j) reached. Here that set is computed per C block-row with a windowed
+// dense accumulator in shared memory:
+//   1. block-row indexes of A and B (stable radix sort by row; quadtree keys are monotone in the
+//      column for a fixed row, so each row comes out k-ascending),
+//   2. k_sym_count:    per row i -> #distinct j, #triples,
+//   3. k_sym_emit_c:   per row i -> C keys in j order + per-C triple counts,
+//   4. radix sort of C keys into quadtree-key order, exclusive scan of counts -> c_tptr,
+//   5. k_sym_emit_tri: per row i -> (a_index, b_index) triples at their final positions, k
+//      ascending within each C block (BlockSparseLeaf.multiply's k loop, block_sparse.py:121-129).
+#include <cub/cub.cuh>
+
+#include "qm_common.cuh"
+
+namespace qm {
+namespace {
+
+constexpr int kWin = 4096;   // j-window of the per-row accumulator (slots)
+constexpr int kNT = 256;     // threads per row CTA
+constexpr int kPer = kWin / kNT;
+
+__global__ void k_decode_rows(const uint64_t *keys, int64_t n, int nbl, int lbits, uint32_t *row,
+                              uint32_t *col, uint32_t *iota) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t bi, bj;
+    qkey_decode(keys[x], nbl, lbits, &bi, &bj);
+    row[x] = bi;
+    col[x] = bj;
+    iota[x] = (uint32_t)x;
+  }
+}
+
+// rp[r] = first position in the sorted row array with row >= r, r in [0, nbg].
+__global__ void k_row_ptr(const uint32_t *srow, int64_t n, int64_t nbg, uint32_t *rp) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= nbg;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)srow[mid] < r) lo = mid + 1; else hi = mid;
+    }
+    rp[r] = (uint32_t)lo;
+  }
+}
+
+__global__ void k_gather_u32(const uint32_t *src, const uint32_t *idx, int64_t n, uint32_t *dst) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+       x += (int64_t)gridDim.x * blockDim.x)
+    dst[x] = src[idx[x]];
+}
+
+// ---- block-level reductions / scans (deterministic, fixed order) ------------------------------
+
+template <class T, class Op>
+__device__ T block_reduce(T v, Op op, T *red /* smem[32] */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  T r = red[0];
+  for (int w = 1; w < nw; ++w) r = op(r, red[w]);
+  return r;
+}
+
+// Exclusive scan of one uint32 per thread; returns the prefix and writes the block total.
+__device__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *total, uint32_t *wsum /* smem[32] */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  __syncthreads();
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  uint32_t before = 0, tot = 0;
+  for (int w = 0; w < nw; ++w) {
+    if (w < warp) before += wsum[w];
+    tot += wsum[w];
+  }
+  *total = tot;
+  return before + inc - v;
+}
+
+struct RowSpan {
+  uint32_t a0, a1;     // A row entries
+  uint64_t nt;         // triples of the row
+  uint32_t jmin, jmax; // column span of the C row
+};
+
+// Triple count and column span of C row i (all threads get the result).
+__device__ RowSpan row_span(int64_t i, const uint32_t *a_rp, const uint32_t *a_scol,
+                            const uint32_t *b_rp, const uint32_t *b_scol, uint64_t *red64,
+                            uint32_t *red32) {
+  RowSpan s;
+  s.a0 = a_rp[i];
+  s.a1 = a_rp[i + 1];
+  uint64_t nt = 0;
+  uint32_t jmin = 0xffffffffu, jmax = 0;
+  for (uint32_t x = s.a0 + threadIdx.x; x < s.a1; x += blockDim.x) {
+    uint32_t k = a_scol[x];
+    uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
+    if (b1 > b0) {
+      nt += b1 - b0;
+      jmin = min(jmin, b_scol[b0]);
+      jmax = max(jmax, b_scol[b1 - 1]);
+    }
+  }
+  s.nt = block_reduce(nt, [](uint64_t a, uint64_t b) { return a + b; }, red64);
+  s.jmin = block_reduce(jmin, [](uint32_t a, uint32_t b) { return min(a, b); }, red32);
+  s.jmax = block_reduce(jmax, [](uint32_t a, uint32_t b) { return max(a, b); }, red32);
+  return s;
+}
+
+// First position in b_scol[b0, b1) with column >= j.
+__device__ __forceinline__ uint32_t lower_bound_col(const uint32_t *b_scol, uint32_t b0, uint32_t b1,
+                                                    uint32_t j) {
+  while (b0 < b1) {
+    uint32_t mid = (b0 + b1) >> 1;
+    if (b_scol[mid] < j) b0 = mid + 1; else b1 = mid;
+  }
+  return b0;
+}
+
+// Calls f(x, y, j) for every pair (A entry x of the row, B entry y of row k(x)) whose column j is
+// inside [wbase, wbase + kWin). Warps take A entries, lanes take B entries; no ordering.
+template <class F>
+__device__ void for_window_pairs(const RowSpan &s, uint32_t wbase, bool multi, const uint32_t *a_scol,
+                                 const uint32_t *b_rp, const uint32_t *b_scol, F f) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint32_t wend = wbase + kWin;
+  for (uint32_t x = s.a0 + warp; x < s.a1; x += nw) {
+    uint32_t k = a_scol[x];
+    uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
+    if (multi) b0 = lower_bound_col(b_scol, b0, b1, wbase);
+    for (uint32_t y = b0 + lane; y < b1; y += 32) {
+      uint32_t j = b_scol[y];
+      if (j >= wend) break;
+      f(x, y, j);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const uint32_t *a_scol,
+                                                   const uint32_t *b_rp, const uint32_t *b_scol,
+                                                   int64_t nbg, uint32_t *rowC, uint64_t *rowT) {
+  __shared__ uint32_t bm[kWin / 32];
+  __shared__ uint64_t red64[32];
+  __shared__ uint32_t red32[32];
+  for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
+    RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
+    uint32_t total = 0;
+    if (s.nt > 0) {
+      const bool multi = (s.jmax - s.jmin) >= (uint32_t)kWin;
+      for (uint64_t wb = s.jmin; wb <= s.jmax; wb += kWin) {
+        const uint32_t wbase = (uint32_t)wb;
+        for (int w = threadIdx.x; w < kWin / 32; w += blockDim.x) bm[w] = 0u;
+        __syncthreads();
+        for_window_pairs(s, wbase, multi, a_scol, b_rp, b_scol, [&](uint32_t, uint32_t, uint32_t j) {
+          uint32_t o = j - wbase;
+          atomicOr(&bm[o >> 5], 1u << (o & 31));
+        });
+        __syncthreads();
+        uint32_t c = 0;
+        for (int w = threadIdx.x; w < kWin / 32; w += blockDim.x) c += __popc(bm[w]);
+        total += block_reduce(c, [](uint32_t a, uint32_t b) { return a + b; }, red32);
+      }
+    }
+    if (threadIdx.x == 0) {
+      rowC[i] = total;
+      rowT[i] = s.nt;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kNT) k_sym_emit_c(const uint32_t *a_rp, const uint32_t *a_scol,
+                                                    const uint32_t *b_rp, const uint32_t *b_scol,
+                                                    int64_t nbg, int nbl, int lbits,
+                                                    const uint64_t *rowC_off, uint64_t *rm_key,
+                                                    uint32_t *rm_cnt) {
+  __shared__ uint32_t cnt[kWin];
+  __shared__ uint64_t red64[32];
+  __shared__ uint32_t red32[32];
+  for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
+    RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
+    if (s.nt > 0) {
+      uint64_t out = rowC_off[i];
+      const bool multi = (s.jmax - s.jmin) >= (uint32_t)kWin;
+      for (uint64_t wb = s.jmin; wb <= s.jmax; wb += kWin) {
+        const uint32_t wbase = (uint32_t)wb;
+        for (int w = threadIdx.x; w < kWin; w += blockDim.x) cnt[w] = 0u;
+        __syncthreads();
+        for_window_pairs(s, wbase, multi, a_scol, b_rp, b_scol,
+                         [&](uint32_t, uint32_t, uint32_t j) { atomicAdd(&cnt[j - wbase], 1u); });
+        __syncthreads();
+        const int s0 = threadIdx.x * kPer;
+        uint32_t mine = 0;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) mine += cnt[s0 + q] != 0u;
+        uint32_t total;
+        uint32_t pos = block_exclusive_scan(mine, &total, red32);
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+          uint32_t c = cnt[s0 + q];
+          if (c) {
+            rm_key[out + pos] = qkey((uint32_t)i, wbase + s0 + q, nbl, lbits);
+            rm_cnt[out + pos] = c;
+            ++pos;
+          }
+        }
+        out += total;
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kNT) k_sym_emit_tri(
+    const uint32_t *a_rp, const uint32_t *a_scol, const uint32_t *a_perm, const uint32_t *b_rp,
+    const uint32_t *b_scol, const uint32_t *b_perm, int64_t nbg, const uint64_t *rowC_off,
+    const uint32_t *inv, const int64_t *c_tptr, uint2 *tri) {
+  __shared__ union {
+    uint32_t cnt[kWin];
+    int64_t cur[kWin];
+  } u;
+  __shared__ uint64_t red64[32];
+  __shared__ uint32_t red32[32];
+  for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
+    RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
+    if (s.nt > 0) {
+      uint64_t out = rowC_off[i];
+      const bool multi = (s.jmax - s.jmin) >= (uint32_t)kWin;
+      for (uint64_t wb = s.jmin; wb <= s.jmax; wb += kWin) {
+        const uint32_t wbase = (uint32_t)wb;
+        const uint32_t wend = wbase + kWin;
+        for (int w = threadIdx.x; w < kWin; w += blockDim.x) u.cnt[w] = 0u;
+        __syncthreads();
+        for_window_pairs(s, wbase, multi, a_scol, b_rp, b_scol,
+                         [&](uint32_t, uint32_t, uint32_t j) { atomicAdd(&u.cnt[j - wbase], 1u); });
+        __syncthreads();
+        const int s0 = threadIdx.x * kPer;
+        uint32_t flags = 0, mine = 0;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q)
+          if (u.cnt[s0 + q]) { flags |= 1u << q; ++mine; }
+        uint32_t total;
+        uint32_t pos = block_exclusive_scan(mine, &total, red32);  // contains __syncthreads
+        __syncthreads();  // every thread has read its cnt slots; the union now becomes cursors
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+          if (flags & (1u << q)) {
+            u.cur[s0 + q] = c_tptr[inv[out + pos]];
+            ++pos;
+          }
+        }
+        __syncthreads();
+        // k ascending: A row entries one at a time; within one entry every column j is distinct,
+        // so each cursor slot is bumped by at most one thread per step.
+        for (uint32_t x = s.a0; x < s.a1; ++x) {
+          const uint32_t k = a_scol[x];
+          const uint32_t ai = a_perm[x];
+          uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
+          if (multi) b0 = lower_bound_col(b_scol, b0, b1, wbase);
+          for (uint32_t y = b0 + threadIdx.x; y < b1; y += blockDim.x) {
+            uint32_t j = b_scol[y];
+            if (j >= wend) break;
+            int64_t p = u.cur[j - wbase]++;
+            tri[p] = make_uint2(ai, b_perm[y]);
+          }
+          __syncthreads();
+        }
+        out += total;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_inv_counts(const uint32_t *perm, const uint32_t *rm_cnt, int64_t nC, uint32_t *inv,
+                             int64_t *cnt_q) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nC;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t c = perm[p];
+    inv[c] = (uint32_t)p;
+    cnt_q[p] = rm_cnt[c];
+  }
+}
+
+__global__ void k_iota(uint32_t *v, int64_t n) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+       x += (int64_t)gridDim.x * blockDim.x)
+    v[x] = (uint32_t)x;
+}
+
+inline int grid_for(int64_t n, int threads = 256) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)g;
+}
+
+inline int bits_for(uint64_t maxval) {
+  int b = 1;
+  while (b < 64 && (maxval >> b) != 0) ++b;
+  return b;
+}
+
+// Workspace of the count phase (persists into the fill phase).
+struct SymWs {
+  uint32_t *a_row, *a_col, *a_iota, *a_srow, *a_perm, *a_scol, *a_rp;
+  uint32_t *b_row, *b_col, *b_iota, *b_srow, *b_perm, *b_scol, *b_rp;
+  uint32_t *rowC;
+  uint64_t *rowT, *rowC_off, *rowT_off;
+  void *cub;
+  size_t cub_bytes;
+};
+
+size_t cub_bytes_count(int64_t nmax, int64_t nbg) {
+  size_t a = 0, b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                  (uint32_t *)nullptr, (uint32_t *)nullptr, (int64_t)nmax, 0, 32);
+  cub::DeviceScan::InclusiveSum(nullptr, b, (uint64_t *)nullptr, (uint64_t *)nullptr, (int64_t)nbg);
+  return std::max(a, b);
+}
+
+SymWs carve_sym(Carver &cv, int64_t nA, int64_t nB, int64_t nbg) {
+  SymWs w;
+  w.a_row = cv.take<uint32_t>(nA); w.a_col = cv.take<uint32_t>(nA); w.a_iota = cv.take<uint32_t>(nA);
+  w.a_srow = cv.take<uint32_t>(nA); w.a_perm = cv.take<uint32_t>(nA); w.a_scol = cv.take<uint32_t>(nA);
+  w.a_rp = cv.take<uint32_t>(nbg + 1);
+  w.b_row = cv.take<uint32_t>(nB); w.b_col = cv.take<uint32_t>(nB); w.b_iota = cv.take<uint32_t>(nB);
+  w.b_srow = cv.take<uint32_t>(nB); w.b_perm = cv.take<uint32_t>(nB); w.b_scol = cv.take<uint32_t>(nB);
+  w.b_rp = cv.take<uint32_t>(nbg + 1);
+  w.rowC = cv.take<uint32_t>(nbg);
+  w.rowT = cv.take<uint64_t>(nbg);
+  w.rowC_off = cv.take<uint64_t>(nbg + 1);
+  w.rowT_off = cv.take<uint64_t>(nbg + 1);
+  w.cub_bytes = cub_bytes_count(std::max(nA, nB), nbg);
+  w.cub = cv.take<char>(w.cub_bytes);
+  return w;
+}
+
+struct FillWs {
+  uint64_t *rm_key;
+  uint32_t *rm_cnt, *rm_iota, *perm, *inv;
+  int64_t *cnt_q;
+  void *cub;
+  size_t cub_bytes;
+};
+
+FillWs carve_fill(Carver &cv, int64_t nC, int key_bits) {
+  FillWs w;
+  w.rm_key = cv.take<uint64_t>(nC);
+  w.rm_cnt = cv.take<uint32_t>(nC);
+  w.rm_iota = cv.take<uint32_t>(nC);
+  w.perm = cv.take<uint32_t>(nC);
+  w.inv = cv.take<uint32_t>(nC);
+  w.cnt_q = cv.take<int64_t>(nC);
+  size_t a = 0, b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (uint64_t *)nullptr, (uint64_t *)nullptr,
+                                  (uint32_t *)nullptr, (uint32_t *)nullptr, (int64_t)nC, 0, key_bits);
+  cub::DeviceScan::InclusiveSum(nullptr, b, (int64_t *)nullptr, (int64_t *)nullptr, (int64_t)nC);
+  w.cub_bytes = std::max(a, b);
+  w.cub = cv.take<char>(w.cub_bytes);
+  return w;
+}
+
+// Block-row index of one operand: rows sorted stably, columns gathered, row pointers.
+int build_rows(const uint64_t *keys, int64_t n, const Geometry &g, uint32_t *row, uint32_t *col,
+               uint32_t *iota, uint32_t *srow, uint32_t *perm, uint32_t *scol, uint32_t *rp,
+               void *cub, size_t cub_bytes, cudaStream_t st) {
+  if (n > 0) {
+    k_decode_rows<<<grid_for(n), 256, 0, st>>>(keys, n, g.nbl, g.lbits, row, col, iota);
+    QM_LAUNCHED("k_decode_rows");
+    size_t tb = cub_bytes;
+    QM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub, tb, row, srow, iota, perm, n, 0,
+                                                bits_for((uint64_t)(g.nbg - 1)), st));
+    QM_CUDA_TRY(cudaGetLastError());
+    k_gather_u32<<<grid_for(n), 256, 0, st>>>(col, perm, n, scol);
+    QM_LAUNCHED("k_gather_u32");
+  }
+  k_row_ptr<<<grid_for(g.nbg + 1), 256, 0, st>>>(srow, n, g.nbg, rp);
+  QM_LAUNCHED("k_row_ptr");
+  return QM_OK;
+}
+
+int row_grid(int64_t nbg) {
+  int64_t g = nbg;
+  if (g > 148 * 64) g = 148 * 64;
+  return (int)std::max<int64_t>(g, 1);
+}
+
+}  // namespace
+}  // namespace qm
+
+using namespace qm;
+
+extern "C" size_t qm_spgemm_workspace_bytes(const qm_layout *layout, int64_t nA, int64_t nB) {
+  Geometry g;
+  if (make_geometry(layout, &g) != QM_OK) return 0;
+  Carver cv(nullptr, 0);
+  carve_sym(cv, nA, nB, g.nbg);
+  return cv.off;
+}
+
+extern "C" int qm_spgemm_count(const qm_layout *layout, const uint64_t *a_keys, int64_t nA,
+                               const uint64_t *b_keys, int64_t nB, void *ws, size_t ws_bytes,
+                               int64_t *n_c_out, int64_t *n_triples_out, void *stream) {
+  Geometry g;
+  int rc = make_geometry(layout, &g);
+  if (rc != QM_OK) return rc;
+  if (nA < 0 || nB < 0 || nA >= (int64_t)1 << 32 || nB >= (int64_t)1 << 32 || !n_c_out || !n_triples_out) {
+    set_error("qm_spgemm_count: bad sizes or output pointers");
+    return QM_ERR_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  Carver cv(ws, ws_bytes);
+  SymWs w = carve_sym(cv, nA, nB, g.nbg);
+  if (!cv.ok() || !ws) {
+    set_error("qm_spgemm_count: workspace %zu bytes < required %zu", ws_bytes, cv.off);
+    return QM_ERR_WORKSPACE;
+  }
+  *n_c_out = 0;
+  *n_triples_out = 0;
+  rc = build_rows(a_keys, nA, g, w.a_row, w.a_col, w.a_iota, w.a_srow, w.a_perm, w.a_scol, w.a_rp,
+                  w.cub, w.cub_bytes, st);
+  if (rc != QM_OK) return rc;
+  rc = build_rows(b_keys, nB, g, w.b_row, w.b_col, w.b_iota, w.b_srow, w.b_perm, w.b_scol, w.b_rp,
+                  w.cub, w.cub_bytes, st);
+  if (rc != QM_OK) return rc;
+  k_sym_count<<<row_grid(g.nbg), kNT, 0, st>>>(w.a_rp, w.a_scol, w.b_rp, w.b_scol, g.nbg, w.rowC,
+                                               w.rowT);
+  QM_LAUNCHED("k_sym_count");
+  QM_CUDA_TRY(cudaMemsetAsync(w.rowC_off, 0, sizeof(uint64_t), st));
+  QM_CUDA_TRY(cudaMemsetAsync(w.rowT_off, 0, sizeof(uint64_t), st));
+  size_t tb = w.cub_bytes;
+  QM_CUDA_TRY(cub::DeviceScan::InclusiveSum(w.cub, tb, w.rowC, w.rowC_off + 1, g.nbg, st));
+  tb = w.cub_bytes;
+  QM_CUDA_TRY(cub::DeviceScan::InclusiveSum(w.cub, tb, w.rowT, w.rowT_off + 1, g.nbg, st));
+  uint64_t tot[2];
+  QM_CUDA_TRY(cudaMemcpyAsync(&tot[0], w.rowC_off + g.nbg, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  QM_CUDA_TRY(cudaMemcpyAsync(&tot[1], w.rowT_off + g.nbg, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  QM_CUDA_TRY(cudaStreamSynchronize(st));
+  if (tot[0] >= (1ull << 32)) {
+    set_error("product has %llu C blocks; this build indexes C with 32 bits", (unsigned long long)tot[0]);
+    return QM_ERR_UNSUPPORTED;
+  }
+  *n_c_out = (int64_t)tot[0];
+  *n_triples_out = (int64_t)tot[1];
+  return QM_OK;
+}
+
+extern "C" size_t qm_spgemm_fill_workspace_bytes(const qm_layout *layout, int64_t nC) {
+  Geometry g;
+  if (make_geometry(layout, &g) != QM_OK) return 0;
+  Carver cv(nullptr, 0);
+  carve_fill(cv, nC, 2 * (g.depth + g.lbits) > 0 ? 2 * (g.depth + g.lbits) : 1);
+  return cv.off;
+}
+
+extern "C" int qm_spgemm_fill(const qm_layout *layout, const uint64_t *a_keys, int64_t nA,
+                              const uint64_t *b_keys, int64_t nB, void *ws, size_t ws_bytes,
+                              void *fill_ws, size_t fill_ws_bytes, uint64_t *c_keys,
+                              int64_t *c_tptr, uint32_t *tri, void *stream) {
+  (void)a_keys;
+  (void)b_keys;
+  Geometry g;
+  int rc = make_geometry(layout, &g);
+  if (rc != QM_OK) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  Carver cv(ws, ws_bytes);
+  SymWs w = carve_sym(cv, nA, nB, g.nbg);
+  if (!cv.ok() || !ws) {
+    set_error("qm_spgemm_fill: workspace too small");
+    return QM_ERR_WORKSPACE;
+  }
+  // Read back the sizes computed by qm_spgemm_count (stream-ordered, tiny).
+  uint64_t tot[2];
+  QM_CUDA_TRY(cudaMemcpyAsync(&tot[0], w.rowC_off + g.nbg, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  QM_CUDA_TRY(cudaMemcpyAsync(&tot[1], w.rowT_off + g.nbg, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  QM_CUDA_TRY(cudaStreamSynchronize(st));
+  const int64_t nC = (int64_t)tot[0];
+  const int key_bits = std::max(1, 2 * (g.depth + g.lbits));
+  Carver fv(fill_ws, fill_ws_bytes);
+  FillWs f = carve_fill(fv, nC, key_bits);
+  if (!fv.ok() || (nC > 0 && !fill_ws)) {
+    set_error("qm_spgemm_fill: fill workspace %zu bytes < required %zu", fill_ws_bytes, fv.off);
+    return QM_ERR_WORKSPACE;
+  }
+  QM_CUDA_TRY(cudaMemsetAsync(c_tptr, 0, sizeof(int64_t), st));
+  if (nC == 0) return QM_OK;
+  k_sym_emit_c<<<row_grid(g.nbg), kNT, 0, st>>>(w.a_rp, w.a_scol, w.b_rp, w.b_scol, g.nbg, g.nbl,
+                                                g.lbits, w.rowC_off, f.rm_key, f.rm_cnt);
+  QM_LAUNCHED("k_sym_emit_c");
+  k_iota<<<grid_for(nC), 256, 0, st>>>(f.rm_iota, nC);
+  QM_LAUNCHED("k_iota");
+  size_t tb = f.cub_bytes;
+  QM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(f.cub, tb, f.rm_key, c_keys, f.rm_iota, f.perm, nC, 0,
+                                              key_bits, st));
+  k_inv_counts<<<grid_for(nC), 256, 0, st>>>(f.perm, f.rm_cnt, nC, f.inv, f.cnt_q);
+  QM_LAUNCHED("k_inv_counts");
+  tb = f.cub_bytes;
+  QM_CUDA_TRY(cub::DeviceScan::InclusiveSum(f.cub, tb, f.cnt_q, c_tptr + 1, nC, st));
+  k_sym_emit_tri<<<row_grid(g.nbg), kNT, 0, st>>>(w.a_rp, w.a_scol, w.a_perm, w.b_rp, w.b_scol,
+                                                  w.b_perm, g.nbg, w.rowC_off, f.inv, c_tptr,
+                                                  (uint2 *)tri);
+  QM_LAUNCHED("k_sym_emit_tri");
+  return QM_OK;
+}
