@@ -1,0 +1,427 @@
+"""Benchmark of the hot path: C = A*B block-sparse quadtree multiply (FP64) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2-131072] [--impl ours|reference]
+
+One step = one full product of the configured BASELINE workload (symbolic phase + DMMA numeric
+phase + exact-zero compaction) through the drop-in API's multiply path, inputs resident in HBM
+(inputs are larger than L2, so no flush is needed between steps). Prints ONE JSON line (rank 0).
+
+  metric  leaf-GEMM GFLOP/s (FP64) = 2*bs^3*T / time, T = block triples
+  e2e     the same metric through MatrixSession.multiply with host (pinned) operands: H2D of A
+          and B and D2H of C inside the timed region
+  roofline  the numeric kernel (dominant) against the measured FP64 tensor peak (a DMMA
+          microbenchmark run in-process; MEASURED_PEAKS.json has no FP64 figure)
+  cpu_baseline  the numpy oracle port (reference algorithm) on a bounded sample, all host cores
+
+``--impl reference`` times the reference's algorithm on the host CPU (the oracle port: the
+reference is pure Python and does not travel to the GPU box) on a bounded sample per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+DEFAULT_CONFIG = "C2-131072"
+FP64_NOMINAL_TFLOPS = 37.0  # B200 FP64 tensor datasheet class figure; floor of the roofline peak
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default=DEFAULT_CONFIG)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-target-s", type=float, default=12.0)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[3:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU side: oracle port on a bounded sample
+# ---------------------------------------------------------------------------------------------
+
+def cpu_sample(cfg_name: str, target_s: float, threads: int):
+    """Builds a bounded sample of the workload for the oracle port: the first R C block rows of
+    the product (their A rows and the B rows they touch), R sized by a short probe so one pass
+    takes about target_s seconds on `threads` host threads."""
+    from oracle import spgemm_oracle as O
+    from paper_2011_11762_b200 import generators as G
+
+    cfg = G.CONFIGS[cfg_name]
+    geom = cfg.geometry
+    pat = G.config_pattern(cfg)
+    if cfg.kind == "decay":
+        _, (ka, ba), (kb, bb) = G.config_operands_host(cfg)
+    else:
+        ka, kb = G.config_keys(cfg, 0), G.config_keys(cfg, 1)
+        ba = bb = None
+    ai, ak = geom.decode(ka)
+    bk, _ = geom.decode(kb)
+    og = O.Geom(cfg.n, cfg.bs, cfg.bs)
+
+    def sample(rows_hi):
+        sel = ai < rows_hi
+        ka_s = ka[sel]
+        kb_s = kb[np.isin(bk, np.unique(ak[sel]))]
+        if ba is None:
+            a_s = G.host_blocks(geom, ka_s, cfg.seed, 0, pat, cfg.half_bw)
+            b_s = G.host_blocks(geom, kb_s, cfg.seed, 1, pat, cfg.half_bw)
+        else:
+            a_s = ba[np.searchsorted(ka, ka_s)]
+            b_s = bb[np.searchsorted(kb, kb_s)]
+        return ka_s, a_s, kb_s, b_s
+
+    def run(s):
+        t0 = time.perf_counter()
+        _, _, T = O.multiply(og, *[s[0], s[1], s[2], s[3]], threads=threads)
+        return time.perf_counter() - t0, T
+
+    probe_rows = max(1, geom.nbg // 64)
+    s = sample(probe_rows)
+    dt, T = run(s)
+    rows = int(min(geom.nbg, max(1, probe_rows * target_s / max(dt, 1e-3))))
+    s = sample(rows)
+    return cfg, s, run, rows
+
+
+def cpu_baseline(cfg_name: str, target_s: float) -> dict:
+    from oracle import spgemm_oracle as O
+
+    threads = O.default_threads()
+    cfg, s, run, rows = cpu_sample(cfg_name, target_s, threads)
+    dt, T = run(s)
+    return {"value": 2.0 * cfg.bs ** 3 * T / dt / 1e9, "unit": "GFLOP/s", "cores": threads,
+            "kind": "port",
+            "sample": f"{cfg_name}: first {rows} of {cfg.geometry.nbg} C block rows ({T} triples) "
+                      f"through oracle/spgemm_oracle.py (reference summation order, numpy/OpenBLAS "
+                      f"dgemm per block, {threads} threads), {dt:.2f} s"}
+
+
+# ---------------------------------------------------------------------------------------------
+# FP64 tensor peak (roofline denominator)
+# ---------------------------------------------------------------------------------------------
+
+def fp64_peak(lib, torch, dev) -> dict:
+    import ctypes
+
+    sink = torch.zeros(1, dtype=torch.float64, device=dev)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    out = {}
+    for kind, name, threads, iters in ((0, "dmma", 256, 40000), (1, "dfma", 256, 200000)):
+        flops = ctypes.c_double(0)
+        best = 0.0
+        for rep in range(4):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            st = torch.cuda.current_stream(dev)
+            s.record(st)
+            rc = lib.qm_fp64_peak_kernel(kind, sms * 4, threads, iters, sink.data_ptr(),
+                                         ctypes.byref(flops), st.cuda_stream)
+            e.record(st)
+            e.synchronize()
+            if rc:
+                raise RuntimeError("fp64 peak kernel failed")
+            if rep:
+                best = max(best, flops.value / (s.elapsed_time(e) * 1e-3) / 1e12)
+        out[name] = best
+    return out
+
+
+# ---------------------------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2011_11762_b200 import MatrixSession, _ffi, spgemm
+    from paper_2011_11762_b200 import generators as G
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = _ffi.load()
+    cfg = G.CONFIGS[args.config]
+    ses = MatrixSession(device=dev)
+    geom, a, b = G.config_operands_device(cfg, dev)
+    if cfg.same_operand:
+        b = a
+    layout = _ffi.make_layout(geom.params, geom.bs)
+    stream = torch.cuda.Stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step(stats=None, events=None):
+        return spgemm.multiply_blocks(layout, a, b, stream=stream, stats=stats, events=events)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 0)):
+            step()
+        torch.cuda.synchronize()
+        stats = spgemm.MultiplyStats()
+        step(stats=stats)
+        torch.cuda.synchronize()
+        evs = [{k: torch.cuda.Event(enable_timing=True) for k in ("symbolic", "numeric", "end")}
+               for _ in range(args.steps)]
+        t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clocks = ClockSampler(local)
+        barrier()
+        torch.cuda.synchronize()
+        clocks.start()
+        l0 = lib.qm_launch_count()
+        t_start.record(stream)
+        for k in range(args.steps):
+            c = step(events=evs[k])
+            del c
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        launches = lib.qm_launch_count() - l0
+        clock = clocks.stop()
+        barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    numeric_ms = [e["numeric"].elapsed_time(e["end"]) for e in evs]
+    symbolic_ms = [e["symbolic"].elapsed_time(e["numeric"]) for e in evs]
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    flops = stats.flops
+    value = flops * args.steps * world / (total_ms * 1e-3) / 1e9
+    ms_per_step = total_ms / args.steps
+    nk_ms = statistics.mean(numeric_ms)
+    bs = geom.bs
+    alg_bytes = 8 * bs * bs * (a.n + b.n + stats.n_c) + 8 * (a.n + b.n + stats.n_c) + 8 * stats.n_triples
+    peaks = fp64_peak(lib, torch, dev)
+    peak = max(peaks["dmma"], peaks["dfma"], FP64_NOMINAL_TFLOPS)
+    achieved = flops / (nk_ms * 1e-3) / 1e12
+    line = {
+        "metric": "block-sparse multiply leaf-GEMM GFLOP/s (FP64)",
+        "value": round(value, 2),
+        "unit": "GFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic: block-keyed uniform[-1,1] values (numpy PCG64 streams, generated on device)",
+        "config": {"workload": cfg.name, "kind": cfg.kind, "n": cfg.n, "block_size": bs,
+                   "half_bandwidth": cfg.half_bw, "leaf_dim": bs, "nnzb_a": a.n, "nnzb_b": b.n,
+                   "nnzb_c": stats.n_c, "triples": stats.n_triples,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (no flush)"},
+        "phases_ms": {"symbolic": round(statistics.mean(symbolic_ms), 4), "numeric": round(nk_ms, 4)},
+        "roofline": {"bound": "tensor", "kernel": "k_numeric_dmma", "achieved": round(achieved, 3),
+                     "peak": round(peak, 3), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                     "peak_source": f"max(measured DMMA {peaks['dmma']:.2f}, measured DFMA "
+                                    f"{peaks['dfma']:.2f}, nominal {FP64_NOMINAL_TFLOPS}) TFLOP/s; "
+                                    "MEASURED_PEAKS.json has no FP64 figure",
+                     "algorithmic_bytes": alg_bytes,
+                     "hbm_gbs_at_alg_bytes": round(alg_bytes / (nk_ms * 1e-3) / 1e9, 1),
+                     "traffic": None},
+        "clocks": clock,
+        "gpu_launches": int(launches),
+        "launches_per_step": round(launches / args.steps, 2),
+    }
+    if not args.no_e2e:
+        line["e2e"] = run_e2e(args, torch, ses, geom, a, b, dev, world, dist)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(args.config, args.cpu_target_s)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, torch, ses, geom, a, b, dev, world, dist):
+    """MatrixSession.multiply with host operands: pinned H2D of A and B, D2H of C, per step."""
+    from paper_2011_11762_b200.blocks import BlockSet
+
+    def pinned(t):
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t)
+        return h
+
+    ha = [pinned(t) for t in (a.keys, a.blocks, a.sumsq)]
+    hb = ha if b is a else [pinned(t) for t in (b.keys, b.blocks, b.sumsq)]
+    h2d = sum(t.numel() * t.element_size() for t in ha) + (0 if b is a else sum(t.numel() * t.element_size() for t in hb))
+    out_host = {}
+
+    def step():
+        da = BlockSet(*[t.to(dev, non_blocking=True) for t in ha])
+        db = da if hb is ha else BlockSet(*[t.to(dev, non_blocking=True) for t in hb])
+        c = ses.multiply(ses.matrix_from_blockset(geom, da), ses.matrix_from_blockset(geom, db))
+        cs = c.root.blockset
+        if "k" not in out_host:
+            out_host["k"] = torch.empty(cs.keys.shape, dtype=cs.keys.dtype, pin_memory=True)
+            out_host["b"] = torch.empty(cs.blocks.shape, dtype=cs.blocks.dtype, pin_memory=True)
+            out_host["s"] = torch.empty(cs.sumsq.shape, dtype=cs.sumsq.dtype, pin_memory=True)
+        out_host["k"].copy_(cs.keys, non_blocking=True)
+        out_host["b"].copy_(cs.blocks, non_blocking=True)
+        out_host["s"].copy_(cs.sumsq, non_blocking=True)
+        return sum(t.numel() * t.element_size() for t in (cs.keys, cs.blocks, cs.sumsq))
+
+    steps = max(1, min(args.steps, 3))
+    step()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    s.record()
+    d2h = 0
+    for _ in range(steps):
+        d2h = step()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    flops = ses.last_multiply.flops
+    return {"value": round(flops * steps * world / (ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "ms_per_step": round(ms / steps, 3), "api": "MatrixSession.multiply"}
+
+
+# ---------------------------------------------------------------------------------------------
+# reference arm (host CPU, oracle port)
+# ---------------------------------------------------------------------------------------------
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from oracle import spgemm_oracle as O
+
+    threads = O.default_threads()
+    target = max(2.0, min(args.cpu_target_s, 150.0 / max(1, args.steps + args.warmup)))
+    cfg, s, run, rows = cpu_sample(args.config, target, threads)
+    for _ in range(max(args.warmup, 0)):
+        run(s)
+    times = []
+    T = 0
+    for _ in range(args.steps):
+        dt, T = run(s)
+        times.append(dt)
+    tot = sum(times)
+    value = 2.0 * cfg.bs ** 3 * T * args.steps / tot / 1e9
+    sample = (f"{cfg.name}: first {rows} of {cfg.geometry.nbg} C block rows ({T} triples) per step; "
+              f"oracle/spgemm_oracle.py = the reference's algorithm and summation order on numpy/"
+              f"OpenBLAS dgemm, {threads} host threads")
+    line = {
+        "metric": "block-sparse multiply leaf-GEMM GFLOP/s (FP64)",
+        "value": round(value, 3),
+        "unit": "GFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(tot / args.steps * 1e3, 2),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic: block-keyed uniform[-1,1] values (numpy PCG64 streams)",
+        "config": {"workload": cfg.name, "n": cfg.n, "block_size": cfg.bs, "half_bandwidth": cfg.half_bw},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -71,7 +71,19 @@ def _walk(geom: Geometry, leaves: np.ndarray, visit_leaf, visit_branch, visit_ni
 
 
 def canonical_bytes(geom: Geometry, keys: np.ndarray, blocks: np.ndarray, explicit_zero=False) -> bytes:
-    """quadtree.canonical_bytes (quadtree.py:293-318) of the matrix held as a flat block set."""
+    """quadtree.canonical_bytes (quadtree.py:293-318) of the matrix held as a flat block set.
+
+    Block norms are computed with single-threaded BLAS: np.linalg.norm is a ddot, which OpenBLAS
+    threads (changing the summation order) above ~10^4 elements. The reference's bench and golden
+    runs hold BLAS at one thread (bench.py:117 threadpool_limits(1)); so does this bridge.
+    """
+    from threadpoolctl import threadpool_limits  # noqa: PLC0415
+
+    with threadpool_limits(limits=1, user_api="blas"):
+        return _canonical_bytes(geom, keys, blocks, explicit_zero)
+
+
+def _canonical_bytes(geom: Geometry, keys: np.ndarray, blocks: np.ndarray, explicit_zero=False) -> bytes:
     leaves, starts, ends = leaf_runs(geom, keys)
     parts: list[bytes] = []
     empty_leaf = _LEAF_HDR.pack(b"B", geom.params.leaf_dim, geom.bs, 0)

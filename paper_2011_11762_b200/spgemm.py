@@ -136,8 +136,11 @@ def compact(bs: int, c: BlockSet, nz: torch.Tensor, n_zero: int, stream=None) ->
 
 
 def multiply_blocks(layout, a: BlockSet, b: BlockSet, stream=None,
-                    stats: MultiplyStats | None = None) -> BlockSet:
-    """Full regular product of two conformant block sets on their CUDA device."""
+                    stats: MultiplyStats | None = None, events: dict | None = None) -> BlockSet:
+    """Full regular product of two conformant block sets on their CUDA device.
+
+    ``events`` (optional): CUDA events recorded on the stream around the phases, keys
+    "symbolic", "numeric", "end" -- used by bench.py to time the numeric kernel alone."""
     _require_cuda(a.blocks)
     _require_cuda(b.blocks)
     if a.device != b.device:
@@ -151,6 +154,8 @@ def multiply_blocks(layout, a: BlockSet, b: BlockSet, stream=None,
         stream = torch.cuda.current_stream(a.device)
     if a.n == 0 or b.n == 0:
         return BlockSet.empty(bs, a.device)
+    if events is not None:
+        events["symbolic"].record(stream)
     plan = symbolic(layout, a, b, stream)
     if stats is not None:
         stats.n_a, stats.n_b = a.n, b.n
@@ -158,7 +163,11 @@ def multiply_blocks(layout, a: BlockSet, b: BlockSet, stream=None,
         stats.flops = 2 * bs ** 3 * plan.n_triples
     if plan.n_c == 0:
         return BlockSet.empty(bs, a.device)
+    if events is not None:
+        events["numeric"].record(stream)
     c, nz, zc = numeric(layout, a, b, plan, stream)
+    if events is not None:
+        events["end"].record(stream)
     n_zero = _sync_item(zc, stream)
     c = compact(bs, c, nz, n_zero, stream)
     if stats is not None:

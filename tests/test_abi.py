@@ -1,0 +1,49 @@
+"""The C-ABI library loads and exports every symbol include/qmb200.h declares (no GPU needed)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2011_11762_b200 import _ffi, _build
+from paper_2011_11762_b200.layout import MatrixParams
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "qmb200.h"
+
+
+def header_symbols():
+    return sorted(set(re.findall(r"QM_API\s+[\w\s\*]+?\b(qm_\w+)\s*\(", HEADER.read_text())))
+
+
+def test_library_is_built_in_tree():
+    assert _build.LIB.exists(), "run __graft_entry__.build() first"
+    assert _build.LIB.parent.name == "paper_2011_11762_b200"
+
+
+def test_exports_every_header_symbol():
+    lib = _ffi.load()
+    names = header_symbols()
+    assert len(names) >= 15
+    assert sorted(_ffi.EXPORTS) == names
+    for name in names:
+        assert hasattr(lib, name), name
+
+
+def test_abi_version_and_host_queries():
+    lib = _ffi.load()
+    assert lib.qm_abi_version() == 1
+    lay = _ffi.make_layout(MatrixParams.create(4096, 64), 64)
+    assert lib.qm_spgemm_workspace_bytes(ctypes.byref(lay), 556, 556) > 0
+    assert lib.qm_compact_workspace_bytes(1016) > 0
+    assert [lib.qm_numeric_path(b) for b in (16, 32, 64, 128, 8, 12)] == [1, 1, 1, 1, 0, 0]
+
+
+def test_invalid_layout_is_reported_not_crashed():
+    lib = _ffi.load()
+    bad = _ffi.QmLayout(100, 12, 3, 5, 0)  # 5 does not divide 12
+    rc = lib.qm_encode_keys(ctypes.byref(bad), None, None, 10, None, None)
+    assert rc == _ffi.QM_ERR_INVALID
+    assert b"divide" in lib.qm_last_error()
+    with pytest.raises(Exception):
+        _ffi.check(rc, "qm_encode_keys")

@@ -1,0 +1,217 @@
+"""GPU parity: libqmb200 through the drop-in API against the reference's outputs and the oracle.
+
+Bar (BASELINE.json north_star): the set of nonzero C blocks bit-exact; values within relative
+Frobenius error 1e-12 in float64 (TOL below); integer-valued products bit-exact (canonical bytes).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import helpers
+from oracle import spgemm_oracle as O
+from paper_2011_11762_b200 import (
+    ConfigurationError,
+    ContractViolationError,
+    DimensionMismatchError,
+    MatrixSession,
+    _ffi,
+    bridge,
+    spgemm,
+)
+from paper_2011_11762_b200 import generators as G
+from paper_2011_11762_b200.layout import Geometry, MatrixParams
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12  # north_star: relative Frobenius error in float64
+
+
+@pytest.fixture(scope="module")
+def ses():
+    return helpers.gpu_session()
+
+
+def _host(m):
+    return m.root.blockset.to_host() if not m.root.is_nil else (np.zeros(0, np.int64), None, None)
+
+
+def test_native_library_is_the_path(ses):
+    lib = _ffi.load()
+    before = lib.qm_launch_count()
+    a = helpers.build(ses, helpers.random_sparse(128, 0.05, 1), 64, 64)
+    c = ses.multiply(a, a)
+    assert lib.qm_launch_count() > before  # the product ran in libqmb200 kernels
+    assert c.root.blockset.blocks.is_cuda
+    assert lib.qm_numeric_path(64) == 1 and lib.qm_numeric_path(12) == 0
+
+
+@pytest.mark.parametrize("ci", range(12))
+def test_small_cases_match_reference(ses, ci):
+    g, cases = helpers.small_cases()
+    n, leaf, bs, da_, db_, sa, sb = cases[ci]
+    da, db = helpers.random_sparse(n, da_, sa), helpers.random_sparse(n, db_, sb)
+    c = ses.multiply(helpers.build(ses, da, leaf, bs), helpers.build(ses, db, leaf, bs))
+    kc, bc, _ = _host(c)
+    np.testing.assert_array_equal(kc, g[f"c{ci}_keys"])  # C block set bit-exact
+    assert helpers.rel(bc, g[f"c{ci}_blocks"]) <= TOL
+    assert helpers.rel(ses.to_dense(c), da @ db) <= TOL
+
+
+def test_integer_product_is_bit_exact(ses):
+    """The reference's schedule-independence case (test_acceptance.py:315-325): canonical bytes of
+    C = A*A on the value-1.0 band equal the reference's, and sum(C) = flop_count_exact / 2."""
+    g = helpers.load("band_ones")
+    case = G.ExperimentCase("banded", 8192, 64)
+    a = G.generate(ses.store, case, 128, "block_sparse", 32)
+    c = ses.multiply(a, a)
+    assert helpers.sha(ses.canonical(c)) == bytes(g["sha"])
+    assert c.root.blockset.blocks.sum().item() == G.flop_count_exact(case) // 2
+
+
+@pytest.mark.parametrize("name", ["C1", "C3s", "C4s", "C2-16384"])
+def test_configs_match_reference(ses, name):
+    g = helpers.load(name)
+    cfg = G.CONFIGS.get(name) or {
+        "C3s": G.BaselineConfig("C3s", "random", 8192, 64, per_row=8),
+        "C4s": G.BaselineConfig("C4s", "decay", 4096, 64, same_operand=True),
+    }[name]
+    geom, a, b = G.config_operands_device(cfg, ses.device)
+    ma = ses.matrix_from_blockset(geom, a)
+    mb = ma if cfg.same_operand else ses.matrix_from_blockset(geom, b)
+    c = ses.multiply(ma, mb)
+    kc, bc, sq = _host(c)
+    np.testing.assert_array_equal(kc, g["c_keys"])
+    norms = np.array([np.linalg.norm(x) for x in bc])
+    assert np.max(np.abs(norms - g["c_norms"]) / g["c_norms"]) <= TOL
+    np.testing.assert_allclose(np.sqrt(sq), g["c_norms"], rtol=TOL)  # fused epilogue norms
+    checks = np.einsum("nij,ij->n", bc, helpers.check_weights(cfg.bs))
+    assert helpers.rel(checks, g["c_checks"]) <= TOL
+    assert helpers.rel(bc[g["sample_idx"]], g["sample_blocks"]) <= TOL
+    assert abs(np.linalg.norm(bc) - g["c_frob"][0]) <= TOL * g["c_frob"][0]
+
+
+@pytest.mark.parametrize("name", ["C1", "C3s"])
+def test_full_product_vs_oracle(ses, name):
+    cfg = G.CONFIGS.get(name) or G.BaselineConfig("C3s", "random", 8192, 64, per_row=8)
+    geom, (ka, ba), (kb, bb) = G.config_operands_host(cfg)
+    kc, bc, _ = O.multiply(O.Geom(cfg.n, cfg.bs, cfg.bs), ka, ba, kb, bb)
+    c = ses.multiply(ses.matrix_from_blocks(geom, ka, ba), ses.matrix_from_blocks(geom, kb, bb))
+    k2, b2, _ = _host(c)
+    np.testing.assert_array_equal(k2, kc)
+    assert helpers.rel(b2, bc) <= TOL
+
+
+@pytest.mark.parametrize("bs,n,pattern", [(64, 4096, 1), (32, 1000, 1), (128, 1024, 0), (16, 300, 0), (12, 96, 1)])
+def test_device_generator_matches_numpy_streams(bs, n, pattern):
+    geom = Geometry(MatrixParams.create(n, bs), bs)
+    keys = G.banded_block_keys(geom, 100)
+    dev = G.device_blocks(geom, keys, seed=7, matrix_id=1, pattern=pattern, half_bw=100, device="cuda:0")
+    host = G.host_blocks(geom, keys, 7, 1, pattern, 100)
+    np.testing.assert_array_equal(dev.blocks.cpu().numpy(), host)  # bit-identical PCG64 streams
+    np.testing.assert_allclose(dev.sumsq.cpu().numpy(), np.einsum("nij,nij->n", host, host), rtol=1e-14)
+
+
+@pytest.mark.parametrize("kind,n,bs,per_row", [
+    ("banded", 4096, 64, 0), ("random", 8192, 64, 8), ("random", 1 << 17, 16, 8), ("banded", 3000, 8, 0)])
+def test_symbolic_phase_matches_oracle_exactly(ses, kind, n, bs, per_row):
+    """Triples, their grouping and k order (block_sparse.py:121-129) equal the oracle's; the
+    random 8192-wide grid exercises the multi-window accumulator (window 4096 columns)."""
+    cfg = G.BaselineConfig("t", kind, n, bs, half_bw=300, per_row=per_row)
+    geom = cfg.geometry
+    ka, kb = G.config_keys(cfg, 0), G.config_keys(cfg, 1)
+    dev = ses.device
+    a = G.BlockSet(torch.from_numpy(ka).to(dev), torch.empty((ka.size, 1, 1), dtype=torch.float64, device=dev),
+                   torch.empty(ka.size, dtype=torch.float64, device=dev))
+    b = G.BlockSet(torch.from_numpy(kb).to(dev), torch.empty((kb.size, 1, 1), dtype=torch.float64, device=dev),
+                   torch.empty(kb.size, dtype=torch.float64, device=dev))
+    layout = _ffi.make_layout(geom.params, bs)
+    plan = spgemm.symbolic(layout, a, b)
+    kc, cptr, ta, tb, _ = O.symbolic(O.Geom(n, bs, bs), ka, kb)
+    np.testing.assert_array_equal(plan.c_keys.cpu().numpy(), kc)
+    np.testing.assert_array_equal(plan.c_tptr.cpu().numpy(), cptr)
+    tri = plan.tri.cpu().numpy().view(np.uint32).reshape(-1, 2).astype(np.int64)
+    np.testing.assert_array_equal(tri[:, 0], ta)
+    np.testing.assert_array_equal(tri[:, 1], tb)
+
+
+def test_identity_multiply_is_bit_exact(ses):
+    """test_ops.py:118-126."""
+    da = helpers.random_sparse(256, 0.05, 13)
+    for leaf, bs in ((64, 64), (64, 16), (32, 8)):
+        a = helpers.build(ses, da, leaf, bs)
+        eye = ses.identity(256, leaf_dim=leaf, block_size=bs)
+        assert ses.canonical(ses.multiply(eye, a)) == ses.canonical(a)
+        assert ses.canonical(ses.multiply(a, eye)) == ses.canonical(a)
+
+
+def test_nil_and_explicit_zero_operands(ses):
+    """test_ops.py:129-134, test_acceptance.py:381-430."""
+    a = helpers.build(ses, helpers.random_sparse(64, 0.2, 14), 16, 8)
+    z = ses.zeros(64, leaf_dim=16, block_size=8)
+    ze = ses.zeros(64, leaf_dim=16, block_size=8, explicit=True)
+    for x, y in ((a, z), (z, a), (a, ze), (ze, a), (z, z)):
+        assert ses.multiply(x, y).root.is_nil
+
+
+def test_exactly_zero_blocks_are_dropped(ses):
+    """An exactly cancelling C block is not stored (_set_block np.any, block_sparse.py:37-41)."""
+    bs, n = 64, 256
+    rng = np.random.default_rng(3)
+    x = rng.integers(-3, 4, (bs, bs)).astype(float)
+    y = rng.integers(-3, 4, (bs, bs)).astype(float)
+    da = np.zeros((n, n))
+    db = np.zeros((n, n))
+    da[0:bs, 0:bs] = x
+    da[0:bs, bs:2 * bs] = x
+    db[0:bs, 0:bs] = y
+    db[bs:2 * bs, 0:bs] = -y          # C(0,0) = xy - xy = 0 exactly
+    db[bs:2 * bs, 3 * bs:4 * bs] = y  # C(0,3) = xy survives
+    c = ses.multiply(helpers.build(ses, da, bs, bs), helpers.build(ses, db, bs, bs))
+    kc, bc, _ = _host(c)
+    geom = Geometry(MatrixParams.create(n, bs), bs)
+    assert list(kc) == list(geom.qkey(np.array([0]), np.array([3])))
+    np.testing.assert_array_equal(bc[0], x @ y)
+
+
+@pytest.mark.parametrize("leaf,bs", [(4, 2), (8, 4), (24, 8), (48, 12), (32, 16), (96, 32), (64, 64), (256, 128), (128, 64)])
+def test_block_size_variants_vs_dense(ses, leaf, bs):
+    n = 3 * leaf + 5  # padded, multi-level tree
+    da, db = helpers.random_sparse(n, 0.05, leaf), helpers.random_sparse(n, 0.05, bs + 100)
+    c = ses.multiply(helpers.build(ses, da, leaf, bs), helpers.build(ses, db, leaf, bs))
+    assert helpers.rel(ses.to_dense(c), da @ db) <= TOL
+    host = MatrixSession(device="cpu")
+    ka, ba, _ = helpers.build(host, da, leaf, bs).root.blockset.to_host()
+    kb, bb, _ = helpers.build(host, db, leaf, bs).root.blockset.to_host()
+    # block set = symbolic product minus exactly-zero blocks (tiny sparse blocks do cancel)
+    kc, bc, _ = O.multiply(O.Geom(n, leaf, bs), ka, ba, kb, bb)
+    np.testing.assert_array_equal(c.root.blockset.keys.cpu().numpy(), kc)
+    assert helpers.rel(c.root.blockset.blocks.cpu().numpy(), bc) <= TOL
+
+
+def test_conformance_errors(ses):
+    a = helpers.build(ses, helpers.random_sparse(64, 0.1, 1), 16, 8)
+    b = helpers.build(ses, helpers.random_sparse(128, 0.1, 2), 16, 8)
+    c = helpers.build(ses, helpers.random_sparse(64, 0.1, 3), 16, 4)
+    with pytest.raises(DimensionMismatchError):
+        ses.multiply(a, b)
+    with pytest.raises(ConfigurationError):
+        ses.multiply(a, c)
+    with pytest.raises(ContractViolationError):
+        ses.multiply(a)
+    with pytest.raises(ConfigurationError):
+        ses.multiply(a, a, variant="approximate", tau=0.5)
+
+
+def test_c2_131072_sampled_blocks_and_counts(ses):
+    """Full-size C2 (BASELINE configs[1] largest): symbolic counts equal SURVEY.md 8(d) and
+    sampled C block rows equal the oracle's on regenerated operand blocks."""
+    cfg = G.CONFIGS["C2-131072"]
+    geom, a, b = G.config_operands_device(cfg, ses.device)
+    c = ses.multiply(ses.matrix_from_blockset(geom, a), ses.matrix_from_blockset(geom, b))
+    st = ses.last_multiply
+    assert (st.n_c, st.n_triples) == (67312, 589832)
+    rows = np.r_[0, np.random.default_rng(0).choice(geom.nbg, 12, replace=False), geom.nbg - 1]
+    kc, bc = helpers.oracle_rows(cfg, rows)
+    keys_all = c.root.blockset.keys.cpu().numpy()
+    got = helpers.lookup(keys_all, c.root.blockset.blocks, kc)
+    assert helpers.rel(got, bc) <= TOL
