@@ -270,6 +270,10 @@ def run_ours(args):
     nk_ms = statistics.mean(numeric_ms)
     bs = geom.bs
     alg_bytes = 8 * bs * bs * (a.n + b.n + stats.n_c) + 8 * (a.n + b.n + stats.n_c) + 8 * stats.n_triples
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get(cfg.name, {}).get("traffic_bytes")
     peaks = fp64_peak(lib, torch, dev)
     peak = max(peaks["dmma"], peaks["dfma"], FP64_NOMINAL_TFLOPS)
     achieved = flops / (nk_ms * 1e-3) / 1e12
@@ -299,7 +303,9 @@ def run_ours(args):
                                     "MEASURED_PEAKS.json has no FP64 figure",
                      "algorithmic_bytes": alg_bytes,
                      "hbm_gbs_at_alg_bytes": round(alg_bytes / (nk_ms * 1e-3) / 1e9, 1),
-                     "traffic": None},
+                     "traffic": traffic,
+                     "traffic_note": "dram read+write bytes of one k_numeric_dmma launch from a "
+                                     "committed ncu --set full capture (profiles/ncu_traffic.json)"},
         "clocks": clock,
         "gpu_launches": int(launches),
         "launches_per_step": round(launches / args.steps, 2),
