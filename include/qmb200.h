@@ -104,11 +104,12 @@ QM_API int qm_spgemm_fill(const qm_layout *layout, const uint64_t *a_keys, int64
  * c_sumsq[m] = squared Frobenius norm of the block, c_nonzero[m] = any entry != 0
  * (the np.any test of _set_block, block_sparse.py:37-41). *zero_count (device, int64) is
  * incremented once per exactly-zero C block; the caller zeroes it first. */
-QM_API int qm_numeric(const qm_layout *layout, const double *a_blocks, const double *b_blocks,
-               const uint32_t *tri, const int64_t *c_tptr, int64_t nC, double *c_blocks,
-               double *c_sumsq, uint8_t *c_nonzero, int64_t *zero_count, void *stream);
-/* Which numeric kernel qm_numeric uses for this block size: 1 = DMMA (mma.sync f64 tensor core),
- * 0 = generic FP64 SIMT (odd block sizes). */
+QM_API int qm_numeric(const qm_layout *layout, const double *a_blocks, int64_t nA,
+               const double *b_blocks, int64_t nB, const uint32_t *tri, const int64_t *c_tptr,
+               int64_t nC, double *c_blocks, double *c_sumsq, uint8_t *c_nonzero,
+               int64_t *zero_count, void *stream);
+/* Which numeric kernel qm_numeric uses for this block size: 2 = TMA + mbarrier warp-specialised
+ * DMMA (bs 32/64/128), 1 = cp.async DMMA (bs 16, or QM_NUMERIC=cpasync), 0 = FP64 SIMT (others). */
 QM_API int qm_numeric_path(int32_t block_size);
 
 /* ---- exact-zero compaction (replaces _put_leaf / _set_block dropping, ops.py:119-122) --------- */

@@ -77,7 +77,7 @@ _SIGS = {
                                        ctypes.POINTER(_I64), _P]),
     "qm_spgemm_fill_workspace_bytes": (_SZ, [_LP, _I64]),
     "qm_spgemm_fill": (ctypes.c_int, [_LP, _P, _I64, _P, _I64, _P, _SZ, _P, _SZ, _P, _P, _P, _P]),
-    "qm_numeric": (ctypes.c_int, [_LP, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P]),
+    "qm_numeric": (ctypes.c_int, [_LP, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P]),
     "qm_numeric_path": (ctypes.c_int, [_I32]),
     "qm_compact_workspace_bytes": (_SZ, [_I64]),
     "qm_compact": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),

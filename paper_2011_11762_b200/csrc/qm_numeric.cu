@@ -13,6 +13,8 @@
 // CTAs are persistent and walk C blocks in quadtree-key order (grid-stride), so concurrently
 // running CTAs touch neighbouring block rows/columns of A and B and reuse them from L2.
 #include <cuda_runtime.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "qm_common.cuh"
 
@@ -340,17 +342,29 @@ int launch_block_stats(int bs, int64_t n, const double *blocks, double *sumsq, u
 
 int numeric_sm_count() { return sm_count(); }
 
+int launch_numeric_tma(int bs, const double *A, int64_t nA, const double *B, int64_t nB,
+                       const uint32_t *tri, const int64_t *tptr, int64_t nC, double *C, double *csq,
+                       uint8_t *cnz, int64_t *zc, cudaStream_t st);
+
+// Numeric kernel selection: QM_NUMERIC=cpasync forces the v1 cp.async kernel (A/B comparisons).
+static int numeric_impl() {
+  const char *e = getenv("QM_NUMERIC");
+  return (e && strcmp(e, "cpasync") == 0) ? 1 : 2;
+}
+
 }  // namespace qm
 
 using namespace qm;
 
 extern "C" int qm_numeric_path(int32_t bs) {
+  if ((bs == 32 || bs == 64 || bs == 128) && numeric_impl() == 2) return 2;
   return (bs == 16 || bs == 32 || bs == 64 || bs == 128) ? 1 : 0;
 }
 
-extern "C" int qm_numeric(const qm_layout *layout, const double *a_blocks, const double *b_blocks,
-                          const uint32_t *tri, const int64_t *c_tptr, int64_t nC, double *c_blocks,
-                          double *c_sumsq, uint8_t *c_nonzero, int64_t *zero_count, void *stream) {
+extern "C" int qm_numeric(const qm_layout *layout, const double *a_blocks, int64_t nA,
+                          const double *b_blocks, int64_t nB, const uint32_t *tri,
+                          const int64_t *c_tptr, int64_t nC, double *c_blocks, double *c_sumsq,
+                          uint8_t *c_nonzero, int64_t *zero_count, void *stream) {
   Geometry g;
   int rc = make_geometry(layout, &g);
   if (rc != QM_OK) return rc;
@@ -361,6 +375,11 @@ extern "C" int qm_numeric(const qm_layout *layout, const double *a_blocks, const
   if (nC == 0) return QM_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const uint2 *t2 = (const uint2 *)tri;
+  if (numeric_impl() == 2) {
+    rc = launch_numeric_tma(g.bs, a_blocks, nA, b_blocks, nB, tri, c_tptr, nC, c_blocks, c_sumsq,
+                            c_nonzero, zero_count, st);
+    if (rc != QM_ERR_UNSUPPORTED) return rc;
+  }
   switch (g.bs) {
     case 16: return launch_dmma<Cfg16>(a_blocks, b_blocks, t2, c_tptr, nC, c_blocks, c_sumsq, c_nonzero, zero_count, st);
     case 32: return launch_dmma<Cfg32>(a_blocks, b_blocks, t2, c_tptr, nC, c_blocks, c_sumsq, c_nonzero, zero_count, st);

@@ -1,0 +1,372 @@
+// Numeric phase v2: warp-specialised TMA + mbarrier pipeline feeding FP64 DMMA.
+//
+// Same contract as k_numeric_dmma (qm_numeric.cu): each C block is owned by one CTA for its whole
+// k list, accumulated in registers in a fixed order, with the fused norm / exact-zero epilogue of
+// _set_block (block_sparse.py:37-41) -- the replacement of BlockSparseLeaf.multiply + add
+// (block_sparse.py:112-152). What changes is how operands reach the tensor cores:
+//
+//  * one producer warp per CTA walks the CTA's stage stream (C block -> triple -> k panel) and
+//    issues 2-D TMA loads (cp.async.bulk.tensor, SWIZZLE_128B, 16-double = 128-byte sub-panels)
+//    into a ring of shared-memory stages, signalling `full[s]` with complete_tx;
+//  * consumer warps wait on `full[s]`, run their DMMAs, and release the stage with one arrive on
+//    `empty[s]` per warp -- no CTA-wide barrier in the main loop, no LDGSTS or address math in the
+//    math warps;
+//  * the 4 k values of each m8n8k4 step are a permutation of the 16-double panel chosen so that the
+//    A fragment (8 rows x 4 k) and the B fragment (4 k x 8 columns) both hit 16 distinct 8-byte
+//    slots of the 128-byte swizzle row per half-warp: bank-conflict free without padding.
+//      lane t=0: k = 2j           t=1: k = 8 + 2((j+1)&3)
+//      lane t=2: k = 2((j+2)&3)+1 t=3: k = 9 + 2((j+3)&3)      (j = k step 0..3 in the panel)
+//    Each k in 0..15 is used exactly once per panel, so the sum is unchanged.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include "qm_common.cuh"
+
+namespace qm {
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// k index (0..15) inside a 16-double panel used by lane column t at k step j (see header).
+__host__ __device__ __forceinline__ int kperm(int t, int j) {
+  switch (t) {
+    case 0: return 2 * j;
+    case 1: return 8 + 2 * ((j + 1) & 3);
+    case 2: return 2 * ((j + 2) & 3) + 1;
+    default: return 9 + 2 * ((j + 3) & 3);
+  }
+}
+
+template <int BS_, int WARPS_M_, int WARPS_N_, int KP_, int STAGES_, int MINB_>
+struct TmaCfg {
+  static constexpr int BS = BS_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, KP = KP_, STAGES = STAGES_;
+  static constexpr int MINB = MINB_;
+  static constexpr int NCW = WARPS_M * WARPS_N;         // consumer warps
+  static constexpr int NTHR = 32 * (NCW + 1);           // + one producer warp
+  static constexpr int TM = BS / WARPS_M, TN = BS / WARPS_N;
+  static constexpr int MT = TM / 8, NT = TN / 8;
+  static constexpr int NP = BS / KP;                    // k panels per triple
+  static constexpr int KSP = KP / 16;                   // 16-wide k sub-panels per stage (A)
+  static constexpr int NSP = BS / 16;                   // 16-wide column sub-panels (B)
+  static constexpr int A_SP_BYTES = BS * 128;           // one A sub-panel: BS rows x 16 doubles
+  static constexpr int B_SP_BYTES = KP * 128;           // one B sub-panel: KP rows x 16 doubles
+  static constexpr int A_BYTES = KSP * A_SP_BYTES;
+  static constexpr int B_BYTES = NSP * B_SP_BYTES;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 2 * STAGES * 8 + 2 * 32 * 8;
+  static_assert(KP % 16 == 0 && BS % KP == 0 && BS % 16 == 0, "panels");
+  static_assert(TM % 8 == 0 && TN % 8 == 0, "warp tile");
+  static_assert(A_SP_BYTES % 1024 == 0 && B_SP_BYTES % 1024 == 0, "swizzle-128B atoms need 1 KB alignment");
+};
+
+struct Cur {
+  int64_t item, t, tend;
+  int p;
+};
+
+template <class Cfg>
+__device__ __forceinline__ void cur_start(Cur &c, int64_t item, int64_t nC, const int64_t *tptr) {
+  c.item = item;
+  c.p = 0;
+  if (item < nC) {
+    c.t = tptr[item];
+    c.tend = tptr[item + 1];
+  } else {
+    c.t = c.tend = 0;
+  }
+}
+
+template <class Cfg>
+__device__ __forceinline__ void cur_next(Cur &c, int64_t nC, const int64_t *tptr) {
+  if (++c.p == Cfg::NP) {
+    c.p = 0;
+    if (++c.t == c.tend) cur_start<Cfg>(c, c.item + gridDim.x, nC, tptr);
+  }
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
+    k_numeric_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const uint2 *__restrict__ tri, const int64_t *__restrict__ tptr, int64_t nC,
+                  double *__restrict__ C, double *__restrict__ csq, uint8_t *__restrict__ cnz,
+                  int64_t *__restrict__ zero_count) {
+  constexpr int BS = Cfg::BS, MT = Cfg::MT, NT = Cfg::NT, STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = (uint64_t *)(smem + (size_t)STAGES * Cfg::STAGE_BYTES);
+  uint64_t *empty = full + STAGES;
+  double *red = (double *)(empty + STAGES);  // [32] sums, [32] nonzero flags
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], Cfg::NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == Cfg::NCW) {
+    // ------------------------------ producer warp ------------------------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
+      Cur L;
+      cur_start<Cfg>(L, blockIdx.x, nC, tptr);
+      int s = 0;
+      uint32_t phase = 0;
+      while (L.item < nC) {
+        mbar_wait(&empty[s], phase ^ 1u);
+        const uint2 ab = tri[L.t];
+        uint8_t *st = smem + (size_t)s * Cfg::STAGE_BYTES;
+        mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
+#pragma unroll
+        for (int q = 0; q < Cfg::KSP; ++q)
+          tma_load_2d(st + q * Cfg::A_SP_BYTES, &tmA, L.p * Cfg::KP + q * 16, (int)(ab.x * BS), &full[s]);
+#pragma unroll
+        for (int q = 0; q < Cfg::NSP; ++q)
+          tma_load_2d(st + Cfg::A_BYTES + q * Cfg::B_SP_BYTES, &tmB, q * 16,
+                      (int)(ab.y * BS + L.p * Cfg::KP), &full[s]);
+        cur_next<Cfg>(L, nC, tptr);
+        if (++s == STAGES) {
+          s = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------ consumer warps ------------------------------
+  const int g = lane >> 2, tq = lane & 3;
+  const int wm0 = (warp / Cfg::WARPS_N) * Cfg::TM;
+  const int wn0 = (warp % Cfg::WARPS_N) * Cfg::TN;
+  // Per-lane swizzled byte offsets of the fragment elements (see kperm).
+  uint32_t aoff[4], boff[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int kk = kperm(tq, j);
+    aoff[j] = g * 128 + (((kk >> 1) ^ g) << 4) + (kk & 1) * 8;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c0 = h * 4;  // (n % 16) / 2 of the fragment's first column: 0 or 4
+      boff[j][h] = kk * 128 + (((c0 + (g >> 1)) ^ (kk & 7)) << 4) + (g & 1) * 8;
+    }
+  }
+
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  Cur Cc;
+  cur_start<Cfg>(Cc, blockIdx.x, nC, tptr);
+  int s = 0;
+  uint32_t phase = 0;
+  while (Cc.item < nC) {
+    mbar_wait(&full[s], phase);
+    const uint8_t *sa = smem + (size_t)s * Cfg::STAGE_BYTES;
+    const uint8_t *sb = sa + Cfg::A_BYTES;
+#pragma unroll
+    for (int kb = 0; kb < Cfg::KSP; ++kb) {
+      const uint8_t *pa = sa + kb * Cfg::A_SP_BYTES + wm0 * 128;
+      const uint8_t *pb = sb + kb * 16 * 128;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        double af[MT], bf[NT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) af[i] = *(const double *)(pa + i * 8 * 128 + aoff[j]);
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const int col = wn0 + n * 8;
+          bf[n] = *(const double *)(pb + (col >> 4) * Cfg::B_SP_BYTES + boff[j][(col & 15) >> 3]);
+        }
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int n = 0; n < NT; ++n) dmma(acc[i][n][0], acc[i][n][1], af[i], bf[n]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == STAGES) {
+      s = 0;
+      phase ^= 1u;
+    }
+
+    if (Cc.p == Cfg::NP - 1 && Cc.t + 1 == Cc.tend) {
+      const int64_t m = Cc.item;
+      double *cb = C + (size_t)m * (BS * BS);
+      double ss = 0.0;
+      bool nz = false;
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const double v0 = acc[i][n][0], v1 = acc[i][n][1];
+          *reinterpret_cast<double2 *>(cb + (size_t)(wm0 + i * 8 + g) * BS + wn0 + n * 8 + 2 * tq) =
+              make_double2(v0, v1);
+          ss = fma(v0, v0, ss);
+          ss = fma(v1, v1, ss);
+          nz |= (v0 != 0.0) | (v1 != 0.0);
+          acc[i][n][0] = acc[i][n][1] = 0.0;
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      const bool wnz = __any_sync(0xffffffffu, nz);
+      if (lane == 0) {
+        red[warp] = ss;
+        red[32 + warp] = wnz ? 1.0 : 0.0;
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::NCW * 32) : "memory");
+      if (threadIdx.x == 0) {
+        double tot = 0.0, anynz = 0.0;
+#pragma unroll
+        for (int w = 0; w < Cfg::NCW; ++w) {
+          tot += red[w];
+          anynz += red[32 + w];
+        }
+        csq[m] = tot;
+        cnz[m] = anynz != 0.0;
+        if (anynz == 0.0 && zero_count) atomicAdd((unsigned long long *)zero_count, 1ull);
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::NCW * 32) : "memory");
+    }
+    cur_next<Cfg>(Cc, nC, tptr);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+// 2-D view of a block pool: rows = nblocks * bs, cols = bs (row-major), box = 16 cols x box_rows.
+int make_map(CUtensorMap *m, const double *base, int64_t nblocks, int bs, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable from the driver");
+    return QM_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)bs, (cuuint64_t)nblocks * bs};
+  cuuint64_t strides[1] = {(cuuint64_t)bs * sizeof(double)};
+  cuuint32_t box[2] = {16u, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d) for %lld blocks of %d", (int)r, (long long)nblocks, bs);
+    return QM_ERR_CUDA;
+  }
+  return QM_OK;
+}
+
+int sm_count_tma() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <class Cfg>
+int launch_tma(const double *A, int64_t nA, const double *B, int64_t nB, const uint2 *tri,
+               const int64_t *tptr, int64_t nC, double *C, double *csq, uint8_t *cnz, int64_t *zc,
+               cudaStream_t st) {
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, A, nA, Cfg::BS, Cfg::BS);
+  if (rc != QM_OK) return rc;
+  rc = make_map(&mb, B, nB, Cfg::BS, Cfg::KP);
+  if (rc != QM_OK) return rc;
+  static bool configured = false;
+  if (!configured) {
+    QM_CUDA_TRY(cudaFuncSetAttribute(k_numeric_tma<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)Cfg::SMEM));
+    configured = true;
+  }
+  int per_sm = 0;
+  QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_numeric_tma<Cfg>, Cfg::NTHR, Cfg::SMEM));
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)sm_count_tma() * per_sm;
+  if (grid > nC) grid = nC;
+  k_numeric_tma<Cfg><<<(int)grid, Cfg::NTHR, Cfg::SMEM, st>>>(ma, mb, tri, tptr, nC, C, csq, cnz, zc);
+  QM_LAUNCHED("k_numeric_tma");
+  return QM_OK;
+}
+
+//                     BS  WM WN  KP STAGES MINB
+using Tma32 = TmaCfg<32, 1, 2, 32, 3, 4>;
+using Tma64 = TmaCfg<64, 2, 2, 32, 3, 2>;
+using Tma128 = TmaCfg<128, 2, 4, 16, 6, 1>;
+
+}  // namespace
+
+// Returns QM_ERR_UNSUPPORTED when no TMA variant exists for bs.
+int launch_numeric_tma(int bs, const double *A, int64_t nA, const double *B, int64_t nB,
+                       const uint32_t *tri, const int64_t *tptr, int64_t nC, double *C, double *csq,
+                       uint8_t *cnz, int64_t *zc, cudaStream_t st) {
+  const uint2 *t2 = (const uint2 *)tri;
+  switch (bs) {
+    case 32: return launch_tma<Tma32>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, st);
+    case 64: return launch_tma<Tma64>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, st);
+    case 128: return launch_tma<Tma128>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, st);
+    default: return QM_ERR_UNSUPPORTED;
+  }
+}
+
+}  // namespace qm

@@ -105,7 +105,7 @@ def numeric(layout, a: BlockSet, b: BlockSet, plan: SymbolicPlan, stream=None,
     nz = _alloc(nc, torch.uint8, dev)
     zc = torch.zeros(1, dtype=torch.int64, device=dev)
     _ffi.check(
-        lib.qm_numeric(ctypes.byref(layout), _ffi.ptr(a.blocks), _ffi.ptr(b.blocks),
+        lib.qm_numeric(ctypes.byref(layout), _ffi.ptr(a.blocks), a.n, _ffi.ptr(b.blocks), b.n,
                        _ffi.ptr(plan.tri), _ffi.ptr(plan.c_tptr), nc, _ffi.ptr(out.blocks),
                        _ffi.ptr(out.sumsq), _ffi.ptr(nz), _ffi.ptr(zc), _ffi.stream_handle(stream)),
         "qm_numeric",

@@ -36,7 +36,7 @@ def test_abi_version_and_host_queries():
     lay = _ffi.make_layout(MatrixParams.create(4096, 64), 64)
     assert lib.qm_spgemm_workspace_bytes(ctypes.byref(lay), 556, 556) > 0
     assert lib.qm_compact_workspace_bytes(1016) > 0
-    assert [lib.qm_numeric_path(b) for b in (16, 32, 64, 128, 8, 12)] == [1, 1, 1, 1, 0, 0]
+    assert [lib.qm_numeric_path(b) for b in (16, 32, 64, 128, 8, 12)] == [1, 2, 2, 2, 0, 0]
 
 
 def test_invalid_layout_is_reported_not_crashed():

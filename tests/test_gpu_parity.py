@@ -42,7 +42,7 @@ def test_native_library_is_the_path(ses):
     c = ses.multiply(a, a)
     assert lib.qm_launch_count() > before  # the product ran in libqmb200 kernels
     assert c.root.blockset.blocks.is_cuda
-    assert lib.qm_numeric_path(64) == 1 and lib.qm_numeric_path(12) == 0
+    assert lib.qm_numeric_path(64) == 2 and lib.qm_numeric_path(16) == 1 and lib.qm_numeric_path(12) == 0
 
 
 @pytest.mark.parametrize("ci", range(12))
@@ -215,3 +215,21 @@ def test_c2_131072_sampled_blocks_and_counts(ses):
     keys_all = c.root.blockset.keys.cpu().numpy()
     got = helpers.lookup(keys_all, c.root.blockset.blocks, kc)
     assert helpers.rel(got, bc) <= TOL
+
+
+@pytest.mark.parametrize("impl", ["tma", "cpasync"])
+@pytest.mark.parametrize("bs", [32, 64, 128])
+def test_both_numeric_kernels_match_oracle(ses, monkeypatch, impl, bs):
+    """The TMA/mbarrier kernel (default) and the cp.async kernel (QM_NUMERIC=cpasync) on the
+    same product: exact block set, values within TOL of the oracle."""
+    monkeypatch.setenv("QM_NUMERIC", impl)
+    lib = _ffi.load()
+    assert lib.qm_numeric_path(bs) == (2 if impl == "tma" else 1)
+    cfg = G.BaselineConfig("k", "banded", 24 * bs, bs, half_bw=3 * bs)
+    geom, (ka, ba), (kb, bb) = G.config_operands_host(cfg)
+    kc, bc, _ = O.multiply(O.Geom(cfg.n, bs, bs), ka, ba, kb, bb)
+    c = ses.multiply(ses.matrix_from_blocks(geom, ka, ba), ses.matrix_from_blocks(geom, kb, bb))
+    k2, b2, s2 = _host(c)
+    np.testing.assert_array_equal(k2, kc)
+    assert helpers.rel(b2, bc) <= TOL
+    np.testing.assert_allclose(s2, np.einsum("nij,nij->n", bc, bc), rtol=1e-12)
