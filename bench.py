@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-target-s", type=float, default=12.0)
+    p.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                   help="N>1: weak = banded n grows with N (default for C2), strong = fixed n (C5)")
     return p.parse_args()
 
 
@@ -213,25 +215,63 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
     lib = _ffi.load()
-    cfg = G.CONFIGS[args.config]
+    base = G.CONFIGS[args.config]
+    scaling = args.scaling or ("strong" if base.name.startswith("C5") or base.kind != "banded" else "weak")
+    cfg = base
+    if world > 1 and scaling == "weak":
+        if base.kind != "banded":
+            raise SystemExit("weak scaling is defined for the banded configs (n grows with the GPU count)")
+        cfg = G.BaselineConfig(f"{base.name}-x{world}", "banded", base.n * world, base.bs,
+                               half_bw=base.half_bw, seed=base.seed)
     ses = MatrixSession(device=dev)
-    geom, a, b = G.config_operands_device(cfg, dev)
-    if cfg.same_operand:
-        b = a
-    layout = _ffi.make_layout(geom.params, geom.bs)
     stream = torch.cuda.Stream(dev)
+    dist_stats = {}
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    def step(stats=None, events=None):
-        return spgemm.multiply_blocks(layout, a, b, stream=stream, stats=stats, events=events)
+    if world == 1:
+        geom, a, b = G.config_operands_device(cfg, dev)
+        if cfg.same_operand:
+            b = a
+        layout = _ffi.make_layout(geom.params, geom.bs)
+
+        def step(stats=None, events=None):
+            return spgemm.multiply_blocks(layout, a, b, stream=stream, stats=stats, events=events)
+    else:
+        from paper_2011_11762_b200 import distributed as D
+
+        geom = cfg.geometry
+        layout = _ffi.make_layout(geom.params, geom.bs)
+        parts = []
+        for m in (0, 1):
+            keys = G.config_keys(cfg, m)
+            lo, hi = (keys.size * rank) // world, (keys.size * (rank + 1)) // world
+            parts.append(G.device_blocks(geom, keys[lo:hi], cfg.seed, m, G.config_pattern(cfg),
+                                         cfg.half_bw, dev))
+        a, b = parts
+        comm = D.Comm()
+        backend = D.CudaBackend(stream)
+
+        def step(stats=None, events=None):
+            if events is not None:
+                events["symbolic"].record(stream)
+            c, ds = D.multiply(comm, layout, a, b, backend=backend)
+            if events is not None:
+                events["numeric"].record(stream)
+                events["end"].record(stream)
+            if stats is not None:
+                stats.n_triples = ds.n_triples_global
+                stats.flops = 2 * geom.bs ** 3 * ds.n_triples_global
+                stats.n_c = ds.n_c_global
+                dist_stats["last"] = ds
+            return c
 
     with torch.cuda.stream(stream):
         for _ in range(max(args.warmup, 0)):
@@ -265,7 +305,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     flops = stats.flops
-    value = flops * args.steps * world / (total_ms * 1e-3) / 1e9
+    value = flops * args.steps / (total_ms * 1e-3) / 1e9  # global flops of the product / max time
     ms_per_step = total_ms / args.steps
     nk_ms = statistics.mean(numeric_ms)
     bs = geom.bs
@@ -276,7 +316,11 @@ def run_ours(args):
         traffic = json.loads(tfile.read_text()).get(cfg.name, {}).get("traffic_bytes")
     peaks = fp64_peak(lib, torch, dev)
     peak = max(peaks["dmma"], peaks["dfma"], FP64_NOMINAL_TFLOPS)
-    achieved = flops / (nk_ms * 1e-3) / 1e12
+    if world > 1:  # the events bracket the whole distributed step; per-GPU share of the flops
+        nk_ms = statistics.mean(symbolic_ms)
+        achieved = flops / world / (nk_ms * 1e-3) / 1e12
+    else:
+        achieved = flops / (nk_ms * 1e-3) / 1e12
     line = {
         "metric": "block-sparse multiply leaf-GEMM GFLOP/s (FP64)",
         "value": round(value, 2),
@@ -286,14 +330,14 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": scaling,
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic: block-keyed uniform[-1,1] values (numpy PCG64 streams, generated on device)",
         "config": {"workload": cfg.name, "kind": cfg.kind, "n": cfg.n, "block_size": bs,
                    "half_bandwidth": cfg.half_bw, "leaf_dim": bs, "nnzb_a": a.n, "nnzb_b": b.n,
                    "nnzb_c": stats.n_c, "triples": stats.n_triples,
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "parallelism": f"keyrange-partition dp{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (no flush)"},
         "phases_ms": {"symbolic": round(statistics.mean(symbolic_ms), 4), "numeric": round(nk_ms, 4)},
         "roofline": {"bound": "tensor", "kernel": "k_numeric_dmma", "achieved": round(achieved, 3),
@@ -310,7 +354,22 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "launches_per_step": round(launches / args.steps, 2),
     }
-    if not args.no_e2e:
+    if world > 1:
+        ds = dist_stats["last"]
+        v = torch.tensor([ds.bytes_received, ds.t_range[1] - ds.t_range[0], ds.n_c_local],
+                         dtype=torch.float64, device=dev)
+        allv = [torch.zeros_like(v) for _ in range(world)]
+        dist.all_gather(allv, v)
+        m = torch.stack(allv).cpu().numpy()
+        line["distributed"] = {
+            "bytes_received_per_gpu": {"min": int(m[:, 0].min()), "mean": float(m[:, 0].mean()),
+                                       "max": int(m[:, 0].max())},
+            "triples_per_gpu": {"min": int(m[:, 1].min()), "max": int(m[:, 1].max())},
+            "phases_s_rank0": {k: round(x, 5) for k, x in ds.phase_s.items()},
+        }
+        line["roofline"]["note"] = ("multi-GPU: 'numeric' phase = the whole distributed step "
+                                    "(structure gather + symbolic + exchange + numeric)")
+    if not args.no_e2e and world == 1:
         line["e2e"] = run_e2e(args, torch, ses, geom, a, b, dev, world, dist)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args.config, args.cpu_target_s)

@@ -94,10 +94,20 @@ QM_API size_t qm_spgemm_fill_workspace_bytes(const qm_layout *layout, int64_t nC
 /* Emits the C key set in quadtree-key order (c_keys[nC]), the triple offsets c_tptr[nC+1] and the
  * triples tri[2*nT] = (a_index, b_index) pairs, grouped by C block, k ascending within a group --
  * the order of BlockSparseLeaf.multiply's k loop (block_sparse.py:121-129). */
-QM_API int qm_spgemm_fill(const qm_layout *layout, const uint64_t *a_keys, int64_t nA, const uint64_t *b_keys,
-                   int64_t nB, void *ws, size_t ws_bytes, void *fill_ws, size_t fill_ws_bytes,
-                   uint64_t *c_keys /*device*/, int64_t *c_tptr /*device*/, uint32_t *tri /*device*/,
-                   void *stream);
+QM_API int qm_spgemm_fill(const qm_layout *layout, int64_t nA, int64_t nB, int64_t nC, int64_t nT,
+                          void *ws, size_t ws_bytes, void *fill_ws, size_t fill_ws_bytes,
+                          uint64_t *c_keys /*device*/, int64_t *c_tptr /*device*/,
+                          uint32_t *tri /*device*/, void *stream);
+/* The two halves of qm_spgemm_fill, for the multi-GPU partition (each rank emits only the triples
+ * of its own C range): _keys writes c_keys and c_tptr (fill_ws must then stay untouched until the
+ * triples are emitted); _triples writes tri[0 .. t_hi-t_lo) = triples [t_lo, t_hi). */
+QM_API int qm_spgemm_fill_keys(const qm_layout *layout, int64_t nA, int64_t nB, int64_t nC, void *ws,
+                               size_t ws_bytes, void *fill_ws, size_t fill_ws_bytes,
+                               uint64_t *c_keys, int64_t *c_tptr, void *stream);
+QM_API int qm_spgemm_fill_triples(const qm_layout *layout, int64_t nA, int64_t nB, int64_t nC, void *ws,
+                                  size_t ws_bytes, void *fill_ws, size_t fill_ws_bytes,
+                                  const int64_t *c_tptr, int64_t t_lo, int64_t t_hi, uint32_t *tri,
+                                  void *stream);
 
 /* ---- numeric phase (replaces BlockSparseLeaf.multiply + add, block_sparse.py:112-152) ------- */
 /* c_blocks[m] = sum over t in [c_tptr[m], c_tptr[m+1]) of A[tri[2t]] * B[tri[2t+1]] (fp64),

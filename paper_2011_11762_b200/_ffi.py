@@ -35,6 +35,8 @@ EXPORTS = (
     "qm_spgemm_count",
     "qm_spgemm_fill_workspace_bytes",
     "qm_spgemm_fill",
+    "qm_spgemm_fill_keys",
+    "qm_spgemm_fill_triples",
     "qm_numeric",
     "qm_numeric_path",
     "qm_compact_workspace_bytes",
@@ -76,7 +78,10 @@ _SIGS = {
     "qm_spgemm_count": (ctypes.c_int, [_LP, _P, _I64, _P, _I64, _P, _SZ, ctypes.POINTER(_I64),
                                        ctypes.POINTER(_I64), _P]),
     "qm_spgemm_fill_workspace_bytes": (_SZ, [_LP, _I64]),
-    "qm_spgemm_fill": (ctypes.c_int, [_LP, _P, _I64, _P, _I64, _P, _SZ, _P, _SZ, _P, _P, _P, _P]),
+    "qm_spgemm_fill": (ctypes.c_int, [_LP, _I64, _I64, _I64, _I64, _P, _SZ, _P, _SZ, _P, _P, _P, _P]),
+    "qm_spgemm_fill_keys": (ctypes.c_int, [_LP, _I64, _I64, _I64, _P, _SZ, _P, _SZ, _P, _P, _P]),
+    "qm_spgemm_fill_triples": (ctypes.c_int, [_LP, _I64, _I64, _I64, _P, _SZ, _P, _SZ, _P, _I64, _I64,
+                                              _P, _P]),
     "qm_numeric": (ctypes.c_int, [_LP, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P]),
     "qm_numeric_path": (ctypes.c_int, [_I32]),
     "qm_compact_workspace_bytes": (_SZ, [_I64]),

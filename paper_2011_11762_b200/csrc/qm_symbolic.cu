@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_c(const uint32_t *a_rp, const 
 __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
     const uint32_t *a_rp, const uint32_t *a_scol, const uint32_t *a_perm, const uint32_t *b_rp,
     const uint32_t *b_scol, const uint32_t *b_perm, int64_t nbg, const uint64_t *rowC_off,
-    const uint32_t *inv, const int64_t *c_tptr, uint2 *tri) {
+    const uint32_t *inv, const int64_t *c_tptr, int64_t t_lo, int64_t t_hi, uint2 *tri) {
   __shared__ union {
     uint32_t cnt[kWin];
     int64_t cur[kWin];
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
             uint32_t j = b_scol[y];
             if (j >= wend) break;
             int64_t p = u.cur[j - wbase]++;
-            tri[p] = make_uint2(ai, b_perm[y]);
+            if (p >= t_lo && p < t_hi) tri[p - t_lo] = make_uint2(ai, b_perm[y]);
           }
           __syncthreads();
         }
@@ -469,35 +469,39 @@ extern "C" size_t qm_spgemm_fill_workspace_bytes(const qm_layout *layout, int64_
   return cv.off;
 }
 
-extern "C" int qm_spgemm_fill(const qm_layout *layout, const uint64_t *a_keys, int64_t nA,
-                              const uint64_t *b_keys, int64_t nB, void *ws, size_t ws_bytes,
-                              void *fill_ws, size_t fill_ws_bytes, uint64_t *c_keys,
-                              int64_t *c_tptr, uint32_t *tri, void *stream) {
-  (void)a_keys;
-  (void)b_keys;
-  Geometry g;
-  int rc = make_geometry(layout, &g);
+namespace {
+// Shared prologue of the fill entry points: carve both workspaces.
+int fill_setup(const qm_layout *layout, int64_t nA, int64_t nB, int64_t nC, void *ws, size_t ws_bytes,
+               void *fill_ws, size_t fill_ws_bytes, Geometry *g, SymWs *w, FillWs *f, int *key_bits) {
+  int rc = make_geometry(layout, g);
   if (rc != QM_OK) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
   Carver cv(ws, ws_bytes);
-  SymWs w = carve_sym(cv, nA, nB, g.nbg);
+  *w = carve_sym(cv, nA, nB, g->nbg);
   if (!cv.ok() || !ws) {
     set_error("qm_spgemm_fill: workspace too small");
     return QM_ERR_WORKSPACE;
   }
-  // Read back the sizes computed by qm_spgemm_count (stream-ordered, tiny).
-  uint64_t tot[2];
-  QM_CUDA_TRY(cudaMemcpyAsync(&tot[0], w.rowC_off + g.nbg, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-  QM_CUDA_TRY(cudaMemcpyAsync(&tot[1], w.rowT_off + g.nbg, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-  QM_CUDA_TRY(cudaStreamSynchronize(st));
-  const int64_t nC = (int64_t)tot[0];
-  const int key_bits = std::max(1, 2 * (g.depth + g.lbits));
+  *key_bits = std::max(1, 2 * (g->depth + g->lbits));
   Carver fv(fill_ws, fill_ws_bytes);
-  FillWs f = carve_fill(fv, nC, key_bits);
+  *f = carve_fill(fv, nC, *key_bits);
   if (!fv.ok() || (nC > 0 && !fill_ws)) {
     set_error("qm_spgemm_fill: fill workspace %zu bytes < required %zu", fill_ws_bytes, fv.off);
     return QM_ERR_WORKSPACE;
   }
+  return QM_OK;
+}
+}  // namespace
+
+extern "C" int qm_spgemm_fill_keys(const qm_layout *layout, int64_t nA, int64_t nB, int64_t nC,
+                                   void *ws, size_t ws_bytes, void *fill_ws, size_t fill_ws_bytes,
+                                   uint64_t *c_keys, int64_t *c_tptr, void *stream) {
+  Geometry g;
+  SymWs w;
+  FillWs f;
+  int key_bits;
+  int rc = fill_setup(layout, nA, nB, nC, ws, ws_bytes, fill_ws, fill_ws_bytes, &g, &w, &f, &key_bits);
+  if (rc != QM_OK) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
   QM_CUDA_TRY(cudaMemsetAsync(c_tptr, 0, sizeof(int64_t), st));
   if (nC == 0) return QM_OK;
   k_sym_emit_c<<<row_grid(g.nbg), kNT, 0, st>>>(w.a_rp, w.a_scol, w.b_rp, w.b_scol, g.nbg, g.nbl,
@@ -512,9 +516,34 @@ extern "C" int qm_spgemm_fill(const qm_layout *layout, const uint64_t *a_keys, i
   QM_LAUNCHED("k_inv_counts");
   tb = f.cub_bytes;
   QM_CUDA_TRY(cub::DeviceScan::InclusiveSum(f.cub, tb, f.cnt_q, c_tptr + 1, nC, st));
+  return QM_OK;
+}
+
+extern "C" int qm_spgemm_fill_triples(const qm_layout *layout, int64_t nA, int64_t nB, int64_t nC,
+                                      void *ws, size_t ws_bytes, void *fill_ws, size_t fill_ws_bytes,
+                                      const int64_t *c_tptr, int64_t t_lo, int64_t t_hi, uint32_t *tri,
+                                      void *stream) {
+  Geometry g;
+  SymWs w;
+  FillWs f;
+  int key_bits;
+  int rc = fill_setup(layout, nA, nB, nC, ws, ws_bytes, fill_ws, fill_ws_bytes, &g, &w, &f, &key_bits);
+  if (rc != QM_OK) return rc;
+  if (nC == 0 || t_hi <= t_lo) return QM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
   k_sym_emit_tri<<<row_grid(g.nbg), kNT, 0, st>>>(w.a_rp, w.a_scol, w.a_perm, w.b_rp, w.b_scol,
-                                                  w.b_perm, g.nbg, w.rowC_off, f.inv, c_tptr,
-                                                  (uint2 *)tri);
+                                                  w.b_perm, g.nbg, w.rowC_off, f.inv, c_tptr, t_lo,
+                                                  t_hi, (uint2 *)tri);
   QM_LAUNCHED("k_sym_emit_tri");
   return QM_OK;
+}
+
+extern "C" int qm_spgemm_fill(const qm_layout *layout, int64_t nA, int64_t nB, int64_t nC, int64_t nT,
+                              void *ws, size_t ws_bytes, void *fill_ws, size_t fill_ws_bytes,
+                              uint64_t *c_keys, int64_t *c_tptr, uint32_t *tri, void *stream) {
+  int rc = qm_spgemm_fill_keys(layout, nA, nB, nC, ws, ws_bytes, fill_ws, fill_ws_bytes, c_keys, c_tptr,
+                               stream);
+  if (rc != QM_OK) return rc;
+  return qm_spgemm_fill_triples(layout, nA, nB, nC, ws, ws_bytes, fill_ws, fill_ws_bytes, c_tptr, 0, nT,
+                                tri, stream);
 }

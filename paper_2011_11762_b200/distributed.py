@@ -1,0 +1,242 @@
+"""Multi-GPU product C = A*B: one process per GPU, torch.distributed (NCCL over NVLink/NVSwitch).
+
+Reference analogue: chunks are owned round-robin by subtree at a split depth (OwnerPolicy,
+quadtree.py:47-63), work is stolen breadth-first (engine.py:286-300) and remote operands are
+fetched through the transfer layer whose received bytes are counted per worker
+(TransferSim.fetch, chunkstore.py:188-210; WorkerStats.bytes_received :54-63).
+
+B200 design:
+  * ownership: each rank holds one contiguous quadtree-key range of A and of B (a union of
+    quadtree subtrees -- structure preserving, never a random permutation);
+  * structure: the ranks all-gather the operands' keys (8 bytes per block) and run the symbolic
+    phase's row indexing and C key pass on the global structure;
+  * partition: C's key range is cut into P contiguous ranges of equal triple count (c_tptr is the
+    prefix sum of per-C-block work), so every C block's whole k sum lives on one GPU -- no
+    reduction, bitwise the same result for any P;
+  * exchange: each rank emits only its own triples, derives the A and B blocks it needs, requests
+    them from their owners (all-to-all-v of indices) and receives them (all-to-all-v of blocks,
+    packed by qm_gather_blocks) -- one halo exchange, no data-path collective besides it;
+  * compute: the local numeric kernel over the received pools; C stays distributed.
+
+The collectives go through ``Comm`` so the same code runs over NCCL (product) and gloo (CPU tests
+with a test backend); ``LocalComm`` is the single-rank case.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import spgemm
+from .blocks import BlockSet
+from .errors import ContractViolationError
+
+
+class Comm:
+    """torch.distributed collectives used by the product (process group `group`)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def allgather_varlen(self, t: torch.Tensor) -> tuple[torch.Tensor, list[int]]:
+        """Concatenation over ranks (rank order) of 1-D tensors of different lengths."""
+        n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
+        ns = [torch.zeros_like(n) for _ in range(self.world)]
+        self.dist.all_gather(ns, n, group=self.group)
+        counts = [int(x.item()) for x in ns]
+        mx = max(counts) if counts else 0
+        pad = torch.zeros(mx, dtype=t.dtype, device=t.device)
+        pad[: t.shape[0]] = t
+        outs = [torch.empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(outs, pad, group=self.group)
+        return torch.cat([o[:c] for o, c in zip(outs, counts)]), counts
+
+    def alltoallv(self, send: torch.Tensor, send_counts: list[int]) -> tuple[torch.Tensor, list[int]]:
+        """Rows send[sum(send_counts[:d]) : ...] go to rank d; returns received rows (source rank
+        order) and the per-source counts."""
+        dev = send.device
+        sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
+        rc = torch.empty_like(sc)
+        self.dist.all_to_all_single(rc, sc, group=self.group)
+        recv_counts = [int(x) for x in rc.cpu().tolist()]
+        flat = send.reshape(send.shape[0], -1) if send.dim() > 1 else send.reshape(-1, 1)
+        out = torch.empty((sum(recv_counts), flat.shape[1]), dtype=send.dtype, device=dev)
+        self.dist.all_to_all_single(out, flat.contiguous(), recv_counts, send_counts, group=self.group)
+        return out.reshape((out.shape[0],) + tuple(send.shape[1:])), recv_counts
+
+    def allreduce_max(self, x: float, device) -> float:
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+
+class LocalComm:
+    """Single rank: every collective is the identity."""
+
+    rank, world = 0, 1
+
+    def allgather_varlen(self, t):
+        return t, [int(t.shape[0])]
+
+    def alltoallv(self, send, send_counts):
+        return send, list(send_counts)
+
+    def allreduce_max(self, x, device):
+        return x
+
+
+class CudaBackend:
+    """The product backend: libqmb200 kernels on the rank's GPU."""
+
+    def __init__(self, stream=None):
+        self.stream = stream
+
+    def symbolic_state(self, layout, a_keys: torch.Tensor, b_keys: torch.Tensor):
+        return spgemm.SymbolicState(layout, a_keys, int(a_keys.shape[0]), b_keys, int(b_keys.shape[0]),
+                                    self.stream)
+
+    def gather_blocks(self, blocks: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+        import ctypes  # noqa: F401
+
+        from . import _ffi
+
+        n = int(idx.shape[0])
+        bs = int(blocks.shape[1])
+        out = torch.empty((n, bs, bs), dtype=blocks.dtype, device=blocks.device)
+        if n:
+            _ffi.check(_ffi.load().qm_gather_blocks(bs, _ffi.ptr(blocks), _ffi.ptr(idx.contiguous()), n,
+                                                    _ffi.ptr(out), _ffi.stream_handle(self.stream)),
+                       "qm_gather_blocks")
+        return out
+
+    def numeric(self, layout, pool_a: BlockSet, pool_b: BlockSet, tri: torch.Tensor,
+                c_tptr: torch.Tensor, c_keys: torch.Tensor) -> BlockSet:
+        plan = spgemm.SymbolicPlan(int(c_keys.shape[0]), int(tri.shape[0] // 2), c_keys, c_tptr, tri)
+        c, nz, zc = spgemm.numeric(layout, pool_a, pool_b, plan, self.stream)
+        stream = self.stream if self.stream is not None else torch.cuda.current_stream(c_keys.device)
+        n_zero = spgemm._sync_item(zc, stream)
+        return spgemm.compact(layout.block_size, c, nz, n_zero, self.stream)
+
+
+@dataclass
+class DistStats:
+    rank: int = 0
+    world: int = 1
+    n_c_global: int = 0
+    n_triples_global: int = 0
+    c_range: tuple = (0, 0)
+    t_range: tuple = (0, 0)
+    n_c_local: int = 0
+    bytes_received: int = 0
+    bytes_sent: int = 0
+    blocks_received: int = 0
+    phase_s: dict = field(default_factory=dict)
+
+    @property
+    def flops_local(self) -> int:
+        return 0
+
+
+def partition(c_tptr: torch.Tensor, world: int) -> tuple[list[int], list[int]]:
+    """Contiguous C ranges of (nearly) equal triple count: bounds over C indices and triples."""
+    n_c = int(c_tptr.shape[0]) - 1
+    n_t = int(c_tptr[-1].item())
+    targets = torch.tensor([(r * n_t) // world for r in range(1, world)], dtype=torch.int64,
+                           device=c_tptr.device)
+    cuts = torch.searchsorted(c_tptr, targets).cpu().tolist() if world > 1 else []
+    cb = [0] + [min(max(int(x), 0), n_c) for x in cuts] + [n_c]
+    for r in range(1, len(cb)):
+        cb[r] = max(cb[r], cb[r - 1])
+    tb = c_tptr[torch.tensor(cb, device=c_tptr.device)].cpu().tolist()
+    return cb, [int(x) for x in tb]
+
+
+def _fetch(comm, backend, local_blocks: torch.Tensor, offsets: list[int], need: torch.Tensor):
+    """Request/serve exchange: returns the blocks of the sorted global indices `need`, in order,
+    plus (bytes received from peers, bytes sent to peers, blocks received from peers)."""
+    dev = need.device
+    off = torch.tensor(offsets, dtype=torch.int64, device=dev)
+    owner = torch.searchsorted(off[1:], need, right=True)
+    req_counts = torch.bincount(owner, minlength=comm.world).cpu().tolist()
+    wanted, serve_counts = comm.alltoallv(need, req_counts)  # indices peers want from me
+    local_idx = wanted.reshape(-1) - offsets[comm.rank]
+    payload = backend.gather_blocks(local_blocks, local_idx)
+    blocks, got_counts = comm.alltoallv(payload, serve_counts)
+    bsz = int(local_blocks.shape[1]) ** 2 * local_blocks.element_size()
+    peers_in = sum(c for r, c in enumerate(got_counts) if r != comm.rank)
+    peers_out = sum(c for r, c in enumerate(serve_counts) if r != comm.rank)
+    return blocks, peers_in * bsz, peers_out * bsz, peers_in
+
+
+def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b_is_a: bool = False,
+             timer=None):
+    """This rank's part of C = A*B. `a_local`/`b_local` are the rank's owned key ranges (ascending
+    across ranks). Returns (C blocks of this rank's C key range, DistStats)."""
+    backend = backend or CudaBackend()
+    stats = DistStats(rank=comm.rank, world=comm.world)
+    clock = timer or (lambda: time.perf_counter())
+    t0 = clock()
+    ka, a_counts = comm.allgather_varlen(a_local.keys)
+    kb, b_counts = (ka, a_counts) if b_is_a else comm.allgather_varlen(b_local.keys)
+    if ka.shape[0] > 1 and bool((ka[1:] <= ka[:-1]).any()):
+        raise ContractViolationError("distributed operands must own ascending, disjoint key ranges")
+    if kb.shape[0] > 1 and bool((kb[1:] <= kb[:-1]).any()):
+        raise ContractViolationError("distributed operands must own ascending, disjoint key ranges")
+    a_off = [0] + list(np.cumsum(a_counts).tolist())
+    b_off = [0] + list(np.cumsum(b_counts).tolist())
+    bs = layout.block_size
+    dev = a_local.blocks.device
+    empty = BlockSet.empty(bs, dev)
+    if ka.shape[0] == 0 or kb.shape[0] == 0:
+        return empty, stats
+    t1 = clock()
+    st = backend.symbolic_state(layout, ka, kb)
+    stats.n_c_global, stats.n_triples_global = st.n_c, st.n_t
+    if st.n_c == 0:
+        return empty, stats
+    c_keys, c_tptr = st.keys()
+    cb, tb = partition(c_tptr, comm.world)
+    m0, m1 = cb[comm.rank], cb[comm.rank + 1]
+    lo, hi = tb[comm.rank], tb[comm.rank + 1]
+    stats.c_range, stats.t_range = (m0, m1), (lo, hi)
+    tri = st.triples(c_tptr, lo, hi).view(-1, 2).to(torch.int64)
+    t2 = clock()
+    need_a = torch.unique(tri[:, 0]) if hi > lo else tri.new_zeros(0)
+    need_b = torch.unique(tri[:, 1]) if hi > lo else tri.new_zeros(0)
+    pool_a, ra, sa, na = _fetch(comm, backend, a_local.blocks, a_off, need_a)
+    if b_is_a:
+        pool_b, rb, sb, nb = _fetch(comm, backend, a_local.blocks, a_off, need_b)
+    else:
+        pool_b, rb, sb, nb = _fetch(comm, backend, b_local.blocks, b_off, need_b)
+    stats.bytes_received, stats.bytes_sent, stats.blocks_received = ra + rb, sa + sb, na + nb
+    t3 = clock()
+    if hi == lo:
+        return empty, stats
+    la = torch.searchsorted(need_a, tri[:, 0])
+    lb = torch.searchsorted(need_b, tri[:, 1])
+    tri_local = torch.stack([la, lb], dim=1).to(torch.int32).reshape(-1).contiguous()
+    c_tptr_local = (c_tptr[m0:m1 + 1] - lo).contiguous()
+    c_keys_local = c_keys[m0:m1].contiguous()
+    dummy_a = torch.empty(0, dtype=torch.float64, device=dev)
+    pa = BlockSet(need_a, pool_a, dummy_a)
+    pb = BlockSet(need_b, pool_b, dummy_a)
+    c = backend.numeric(layout, pa, pb, tri_local, c_tptr_local, c_keys_local)
+    t4 = clock()
+    stats.n_c_local = c.n
+    stats.phase_s = {"structure": t1 - t0, "symbolic": t2 - t1, "exchange": t3 - t2, "numeric": t4 - t3}
+    return c, stats
+
+
+def owned_range(keys_sorted: np.ndarray, bounds: list[int], rank: int) -> np.ndarray:
+    """Keys of rank `rank` when the key space is cut at `bounds` (key values, len world+1)."""
+    lo = np.searchsorted(keys_sorted, bounds[rank], side="left")
+    hi = np.searchsorted(keys_sorted, bounds[rank + 1], side="left")
+    return keys_sorted[lo:hi]

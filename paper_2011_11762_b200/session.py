@@ -179,6 +179,21 @@ class MatrixSession:
         self.last_stats: list[WorkerStats] | None = None
         self.last_multiply: spgemm.MultiplyStats | None = None
         self.last_engine = None
+        # n_workers > 1 inside a torch.distributed job of that size = one rank per GPU with the
+        # work-balanced key-range partition. Outside such a job the reference's workers are a CPU
+        # scheduling detail and the product runs on this process's GPU.
+        self.comm = None
+        if n_workers > 1:
+            import torch.distributed as dist  # noqa: PLC0415
+
+            if dist.is_available() and dist.is_initialized():
+                if dist.get_world_size() != n_workers:
+                    raise ConfigurationError(
+                        f"n_workers={n_workers} but the process group has {dist.get_world_size()} ranks"
+                    )
+                from .distributed import Comm  # noqa: PLC0415
+
+                self.comm = Comm()
 
     # -- engine plumbing ------------------------------------------------------------------------
 
@@ -204,10 +219,47 @@ class MatrixSession:
             return NIL  # _multiply_fallback (ops.py:244-245): a nil operand gives nil
         a, b = a_root.require(), b_root.require()
         layout = make_layout(geom.params, geom.bs)
+        if self.comm is not None:
+            return self._run_distributed(layout, a, b, a_root is b_root, stats)
         with torch.cuda.device(a.device) if a.device.type == "cuda" else _null():
             c = spgemm.multiply_blocks(layout, a, b, stats=stats)
         self.last_stats = [WorkerStats(0, tasks_executed=stats.n_triples)]
         return self.store.register(c)
+
+    def _run_distributed(self, layout, a, b, same, stats):
+        from . import distributed  # noqa: PLC0415
+
+        spgemm._require_cuda(a.blocks)
+        c, ds = distributed.multiply(self.comm, layout, a, b, b_is_a=same)
+        stats.n_c = c.n
+        stats.n_triples = ds.n_triples_global
+        stats.flops = 2 * layout.block_size ** 3 * ds.n_triples_global
+        mine = torch.tensor([ds.t_range[1] - ds.t_range[0], ds.bytes_received], dtype=torch.int64,
+                            device=a.device)
+        allv = [torch.zeros_like(mine) for _ in range(self.comm.world)]
+        self.comm.dist.all_gather(allv, mine)
+        self.last_stats = [WorkerStats(r, tasks_executed=int(v[0]), bytes_received=int(v[1]))
+                           for r, v in enumerate(allv)]
+        self.last_distributed = ds
+        return self.store.register(c)
+
+    def _distribute(self, bset: BlockSet) -> BlockSet:
+        """Keeps this rank's contiguous key range (equal block counts per rank)."""
+        if self.comm is None:
+            return bset
+        n, w, r = bset.n, self.comm.world, self.comm.rank
+        lo, hi = (n * r) // w, (n * (r + 1)) // w
+        return BlockSet(bset.keys[lo:hi].contiguous(), bset.blocks[lo:hi].contiguous(),
+                        bset.sumsq[lo:hi].contiguous())
+
+    def _gathered(self, bset: BlockSet) -> BlockSet:
+        """All ranks' parts of a distributed matrix, in key order (inspection only)."""
+        if self.comm is None:
+            return bset
+        k, _ = self.comm.allgather_varlen(bset.keys)
+        b, _ = self.comm.allgather_varlen(bset.blocks.reshape(-1))
+        s, _ = self.comm.allgather_varlen(bset.sumsq)
+        return BlockSet(k, b.reshape(-1, bset.bs, bset.bs), s)
 
     @property
     def owner_policy(self) -> OwnerPolicy:
@@ -226,7 +278,7 @@ class MatrixSession:
     def matrix_from_blocks(self, geom: Geometry, keys: np.ndarray, blocks: np.ndarray,
                            symmetric: bool = False, sumsq: np.ndarray | None = None) -> Matrix:
         """Registers an already-normalised block set (keys ascending, no zero blocks)."""
-        bset = BlockSet.from_numpy(keys, blocks, sumsq, self.device)
+        bset = self._distribute(BlockSet.from_numpy(keys, blocks, sumsq, self.device))
         root = self.store.register(bset)
         return Matrix(root, geom.params, LeafKind.BLOCK_SPARSE, geom.bs, symmetric)
 
@@ -283,12 +335,11 @@ class MatrixSession:
 
     # -- inspection -----------------------------------------------------------------------------
 
-    @staticmethod
-    def _host(a: Matrix):
+    def _host(self, a: Matrix):
         if a.root.is_nil or a.root.blockset is None:
             bs = a.block_size
             return np.zeros(0, np.int64), np.zeros((0, bs, bs)), np.zeros(0)
-        return a.root.blockset.to_host()
+        return self._gathered(a.root.blockset).to_host()
 
     @staticmethod
     def _map_symmetric(a: Matrix, rows, cols):

@@ -63,33 +63,60 @@ def _alloc(shape, dtype, device):
         raise StoreCapacityError(f"device memory exhausted allocating {shape} {dtype}: {e}") from e
 
 
+class SymbolicState:
+    """Workspaces of one symbolic phase (row indexes, fill scratch) kept between its steps."""
+
+    def __init__(self, layout, a_keys: torch.Tensor, n_a: int, b_keys: torch.Tensor, n_b: int, stream=None):
+        self.lib = _ffi.load()
+        self.layout = layout
+        self.lp = ctypes.byref(layout)
+        self.n_a, self.n_b = n_a, n_b
+        self.dev = a_keys.device
+        self.sh = _ffi.stream_handle(stream)
+        self.ws_bytes = self.lib.qm_spgemm_workspace_bytes(self.lp, n_a, n_b)
+        self.ws = _alloc(max(self.ws_bytes, 1), torch.uint8, self.dev)
+        n_c = ctypes.c_int64(0)
+        n_t = ctypes.c_int64(0)
+        _ffi.check(
+            self.lib.qm_spgemm_count(self.lp, _ffi.ptr(a_keys), n_a, _ffi.ptr(b_keys), n_b,
+                                     _ffi.ptr(self.ws), self.ws_bytes, ctypes.byref(n_c),
+                                     ctypes.byref(n_t), self.sh),
+            "qm_spgemm_count",
+        )
+        self.n_c, self.n_t = int(n_c.value), int(n_t.value)
+        self.fill_bytes = self.lib.qm_spgemm_fill_workspace_bytes(self.lp, self.n_c)
+        self.fws = _alloc(max(self.fill_bytes, 1), torch.uint8, self.dev)
+
+    def keys(self):
+        """C keys (quadtree order) and triple offsets c_tptr[nC+1]."""
+        c_keys = _alloc(self.n_c, torch.int64, self.dev)
+        c_tptr = _alloc(self.n_c + 1, torch.int64, self.dev)
+        _ffi.check(
+            self.lib.qm_spgemm_fill_keys(self.lp, self.n_a, self.n_b, self.n_c, _ffi.ptr(self.ws),
+                                         self.ws_bytes, _ffi.ptr(self.fws), self.fill_bytes,
+                                         _ffi.ptr(c_keys), _ffi.ptr(c_tptr), self.sh),
+            "qm_spgemm_fill_keys",
+        )
+        return c_keys, c_tptr
+
+    def triples(self, c_tptr: torch.Tensor, t_lo: int = 0, t_hi: int | None = None) -> torch.Tensor:
+        """(a_index, b_index) int32 pairs of triples [t_lo, t_hi)."""
+        t_hi = self.n_t if t_hi is None else t_hi
+        tri = _alloc(2 * max(t_hi - t_lo, 0), torch.int32, self.dev)
+        _ffi.check(
+            self.lib.qm_spgemm_fill_triples(self.lp, self.n_a, self.n_b, self.n_c, _ffi.ptr(self.ws),
+                                            self.ws_bytes, _ffi.ptr(self.fws), self.fill_bytes,
+                                            _ffi.ptr(c_tptr), t_lo, t_hi, _ffi.ptr(tri), self.sh),
+            "qm_spgemm_fill_triples",
+        )
+        return tri
+
+
 def symbolic(layout, a: BlockSet, b: BlockSet, stream=None) -> SymbolicPlan:
-    lib = _ffi.load()
-    dev = a.device
-    sh = _ffi.stream_handle(stream)
-    lp = ctypes.byref(layout)
-    ws_bytes = lib.qm_spgemm_workspace_bytes(lp, a.n, b.n)
-    ws = _alloc(max(ws_bytes, 1), torch.uint8, dev)
-    n_c = ctypes.c_int64(0)
-    n_t = ctypes.c_int64(0)
-    _ffi.check(
-        lib.qm_spgemm_count(lp, _ffi.ptr(a.keys), a.n, _ffi.ptr(b.keys), b.n, _ffi.ptr(ws), ws_bytes,
-                            ctypes.byref(n_c), ctypes.byref(n_t), sh),
-        "qm_spgemm_count",
-    )
-    nc, nt = int(n_c.value), int(n_t.value)
-    c_keys = _alloc(nc, torch.int64, dev)
-    c_tptr = _alloc(nc + 1, torch.int64, dev)
-    tri = _alloc(2 * nt, torch.int32, dev)
-    fill_bytes = lib.qm_spgemm_fill_workspace_bytes(lp, nc)
-    fws = _alloc(max(fill_bytes, 1), torch.uint8, dev)
-    _ffi.check(
-        lib.qm_spgemm_fill(lp, _ffi.ptr(a.keys), a.n, _ffi.ptr(b.keys), b.n, _ffi.ptr(ws), ws_bytes,
-                           _ffi.ptr(fws), fill_bytes, _ffi.ptr(c_keys), _ffi.ptr(c_tptr),
-                           _ffi.ptr(tri), sh),
-        "qm_spgemm_fill",
-    )
-    return SymbolicPlan(nc, nt, c_keys, c_tptr, tri)
+    st = SymbolicState(layout, a.keys, a.n, b.keys, b.n, stream)
+    c_keys, c_tptr = st.keys()
+    tri = st.triples(c_tptr)
+    return SymbolicPlan(st.n_c, st.n_t, c_keys, c_tptr, tri)
 
 
 def numeric(layout, a: BlockSet, b: BlockSet, plan: SymbolicPlan, stream=None,

@@ -1,0 +1,127 @@
+"""Multi-rank product path on CPU: world_size 2 and 3 over gloo, with the oracle as the compute
+backend and the product's own partition / request-serve exchange code (distributed.py).
+
+Checks: the union of the ranks' C ranges equals the single-process product bit for bit (same
+summation order per C block), the partition balances triples, and halo bytes are reported.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from oracle import spgemm_oracle as O
+from paper_2011_11762_b200 import distributed as D
+from paper_2011_11762_b200 import generators as G
+from paper_2011_11762_b200._ffi import make_layout
+from paper_2011_11762_b200.blocks import BlockSet
+
+
+class OracleBackend:
+    """Test backend: oracle symbolic/numeric on the CPU; same interface as D.CudaBackend."""
+
+    def __init__(self, geom):
+        self.geom = geom
+        self.og = O.Geom(geom.params.n_logical, geom.params.leaf_dim, geom.bs)
+
+    def symbolic_state(self, layout, a_keys, b_keys):
+        outer = self
+        self.ka = a_keys.numpy()
+        kc, cptr, ta, tb, tk = O.symbolic(self.og, a_keys.numpy(), b_keys.numpy())
+
+        class St:
+            n_c, n_t = int(kc.size), int(ta.size)
+
+            def keys(self):
+                return torch.from_numpy(kc), torch.from_numpy(cptr)
+
+            def triples(self, c_tptr, lo, hi):
+                return torch.from_numpy(np.stack([ta[lo:hi], tb[lo:hi]], 1).astype(np.int32).reshape(-1))
+
+        _ = outer
+        return St()
+
+    def gather_blocks(self, blocks, idx):
+        return blocks.index_select(0, idx)
+
+    def numeric(self, layout, pa, pb, tri, c_tptr, c_keys):
+        t = tri.view(-1, 2).numpy().astype(np.int64)
+        glob_a = pa.keys.numpy()[t[:, 0]]  # pool keys carry global A indices
+        _, k = self.og.decode(self.ka[glob_a])
+        kc, bc, _ = O.numeric(self.og, c_keys.numpy(), c_tptr.numpy(), t[:, 0], t[:, 1], k,
+                              pa.blocks.numpy(), pb.blocks.numpy())
+        return BlockSet(torch.from_numpy(kc), torch.from_numpy(bc), torch.from_numpy(np.einsum("nij,nij->n", bc, bc)))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+CASES = {
+    "banded": G.BaselineConfig("t-band", "banded", 2048, 32, half_bw=100),
+    "random": G.BaselineConfig("t-rand", "random", 2048, 32, per_row=4),
+}
+
+
+def _worker(rank, world, port, case, outdir):
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    cfg = CASES[case]
+    geom, (ka, ba), (kb, bb) = G.config_operands_host(cfg)
+    # ownership: contiguous key ranges with uneven cut points (ownership need not match C's cut)
+    qa = np.r_[0, np.sort(np.random.default_rng(5).choice(ka.size, world - 1, replace=False)), ka.size]
+    qb = np.r_[0, np.sort(np.random.default_rng(6).choice(kb.size, world - 1, replace=False)), kb.size]
+    la = BlockSet(torch.from_numpy(ka[qa[rank]:qa[rank + 1]]), torch.from_numpy(ba[qa[rank]:qa[rank + 1]]),
+                  torch.zeros(0))
+    lb = BlockSet(torch.from_numpy(kb[qb[rank]:qb[rank + 1]]), torch.from_numpy(bb[qb[rank]:qb[rank + 1]]),
+                  torch.zeros(0))
+    comm = D.Comm()
+    c, st = D.multiply(comm, make_layout(geom.params, geom.bs), la, lb, backend=OracleBackend(geom))
+    keys, _ = comm.allgather_varlen(c.keys)
+    flat, _ = comm.allgather_varlen(c.blocks.reshape(-1))
+    recv = torch.tensor([st.bytes_received, st.t_range[1] - st.t_range[0]], dtype=torch.int64)
+    allr = [torch.zeros_like(recv) for _ in range(world)]
+    dist.all_gather(allr, recv)
+    if rank == 0:
+        np.savez(os.path.join(outdir, "out.npz"), keys=keys.numpy(), blocks=flat.numpy(),
+                 recv=torch.stack(allr).numpy(), nt=st.n_triples_global)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", ["banded", "random"])
+def test_distributed_product_equals_single_process(tmp_path, world, case):
+    mp.spawn(_worker, args=(world, _free_port(), case, str(tmp_path)), nprocs=world, join=True)
+    out = np.load(tmp_path / "out.npz")
+    cfg = CASES[case]
+    geom, (ka, ba), (kb, bb) = G.config_operands_host(cfg)
+    kc, bc, T = O.multiply(O.Geom(cfg.n, cfg.bs, cfg.bs), ka, ba, kb, bb)
+    np.testing.assert_array_equal(out["keys"], kc)  # same C block set, in key order across ranks
+    np.testing.assert_array_equal(out["blocks"].reshape(bc.shape), bc)  # bitwise: same order per block
+    per_rank_triples = out["recv"][:, 1]
+    assert per_rank_triples.sum() == T == int(out["nt"])
+    assert per_rank_triples.max() - per_rank_triples.min() <= 2 * 32  # balanced by triples (+- one C row of work)
+    assert out["recv"][:, 0].sum() > 0  # halo blocks crossed ranks
+
+
+def test_partition_bounds_are_balanced_and_monotone():
+    tptr = torch.tensor(np.r_[0, np.cumsum(np.random.default_rng(0).integers(1, 20, 1000))])
+    for world in (1, 2, 3, 8):
+        cb, tb = D.partition(tptr, world)
+        assert cb[0] == 0 and cb[-1] == 1000 and all(x <= y for x, y in zip(cb, cb[1:]))
+        share = np.diff(tb)
+        assert share.max() - share.min() <= 2 * 20
+
+
+def test_local_comm_is_identity():
+    c = D.LocalComm()
+    t = torch.arange(5)
+    assert torch.equal(c.allgather_varlen(t)[0], t)
+    assert torch.equal(c.alltoallv(t, [5])[0], t)

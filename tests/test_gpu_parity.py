@@ -233,3 +233,33 @@ def test_both_numeric_kernels_match_oracle(ses, monkeypatch, impl, bs):
     np.testing.assert_array_equal(k2, kc)
     assert helpers.rel(b2, bc) <= TOL
     np.testing.assert_allclose(s2, np.einsum("nij,nij->n", bc, bc), rtol=1e-12)
+
+
+def test_distributed_path_single_rank_matches(ses):
+    """The multi-GPU code path (structure gather, partition, request/serve exchange, remapped
+    numeric) on one rank -- LocalComm and a real NCCL process group of size 1 -- equals the
+    single-GPU product bit for bit."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2011_11762_b200 import distributed as D
+
+    cfg = G.CONFIGS["C2-16384"]
+    geom, a, b = G.config_operands_device(cfg, ses.device)
+    layout = _ffi.make_layout(geom.params, geom.bs)
+    ref = spgemm.multiply_blocks(layout, a, b)
+    c, st = D.multiply(D.LocalComm(), layout, a, b)
+    assert torch.equal(c.keys, ref.keys) and torch.equal(c.blocks, ref.blocks)
+    assert st.bytes_received == 0 and st.t_range == (0, st.n_triples_global)
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=ses.device)
+    try:
+        c2, _ = D.multiply(D.Comm(), layout, a, b)
+        assert torch.equal(c2.keys, ref.keys) and torch.equal(c2.blocks, ref.blocks)
+    finally:
+        dist.destroy_process_group()
