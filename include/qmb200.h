@@ -113,11 +113,14 @@ QM_API int qm_spgemm_fill_triples(const qm_layout *layout, int64_t nA, int64_t n
 /* c_blocks[m] = sum over t in [c_tptr[m], c_tptr[m+1]) of A[tri[2t]] * B[tri[2t+1]] (fp64),
  * c_sumsq[m] = squared Frobenius norm of the block, c_nonzero[m] = any entry != 0
  * (the np.any test of _set_block, block_sparse.py:37-41). *zero_count (device, int64) is
- * incremented once per exactly-zero C block; the caller zeroes it first. */
+ * incremented once per exactly-zero C block; the caller zeroes it first. Block sizes above the
+ * 64x64 CTA tile (bs 128) are computed as (bs/64)^2 tiles whose partial norms go to the caller's
+ * workspace (qm_numeric_workspace_bytes, 0 for bs <= 64) and are combined in a fixed order. */
+QM_API size_t qm_numeric_workspace_bytes(int32_t block_size, int64_t nC);
 QM_API int qm_numeric(const qm_layout *layout, const double *a_blocks, int64_t nA,
                const double *b_blocks, int64_t nB, const uint32_t *tri, const int64_t *c_tptr,
                int64_t nC, double *c_blocks, double *c_sumsq, uint8_t *c_nonzero,
-               int64_t *zero_count, void *stream);
+               int64_t *zero_count, void *ws, size_t ws_bytes, void *stream);
 /* Which numeric kernel qm_numeric uses for this block size: 2 = TMA + mbarrier warp-specialised
  * DMMA (bs 32/64/128), 1 = cp.async DMMA (bs 16, or QM_NUMERIC=cpasync), 0 = FP64 SIMT (others). */
 QM_API int qm_numeric_path(int32_t block_size);

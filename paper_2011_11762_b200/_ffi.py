@@ -38,6 +38,7 @@ EXPORTS = (
     "qm_spgemm_fill_keys",
     "qm_spgemm_fill_triples",
     "qm_numeric",
+    "qm_numeric_workspace_bytes",
     "qm_numeric_path",
     "qm_compact_workspace_bytes",
     "qm_compact",
@@ -82,7 +83,8 @@ _SIGS = {
     "qm_spgemm_fill_keys": (ctypes.c_int, [_LP, _I64, _I64, _I64, _P, _SZ, _P, _SZ, _P, _P, _P]),
     "qm_spgemm_fill_triples": (ctypes.c_int, [_LP, _I64, _I64, _I64, _P, _SZ, _P, _SZ, _P, _I64, _I64,
                                               _P, _P]),
-    "qm_numeric": (ctypes.c_int, [_LP, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P]),
+    "qm_numeric": (ctypes.c_int, [_LP, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
+    "qm_numeric_workspace_bytes": (_SZ, [_I32, _I64]),
     "qm_numeric_path": (ctypes.c_int, [_I32]),
     "qm_compact_workspace_bytes": (_SZ, [_I64]),
     "qm_compact": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),

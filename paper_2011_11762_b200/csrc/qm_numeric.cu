@@ -344,7 +344,8 @@ int numeric_sm_count() { return sm_count(); }
 
 int launch_numeric_tma(int bs, const double *A, int64_t nA, const double *B, int64_t nB,
                        const uint32_t *tri, const int64_t *tptr, int64_t nC, double *C, double *csq,
-                       uint8_t *cnz, int64_t *zc, cudaStream_t st);
+                       uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes, cudaStream_t st);
+size_t numeric_tma_ws_bytes(int bs, int64_t nC);
 
 // Numeric kernel selection: QM_NUMERIC=cpasync forces the v1 cp.async kernel (A/B comparisons).
 static int numeric_impl() {
@@ -361,10 +362,15 @@ extern "C" int qm_numeric_path(int32_t bs) {
   return (bs == 16 || bs == 32 || bs == 64 || bs == 128) ? 1 : 0;
 }
 
+extern "C" size_t qm_numeric_workspace_bytes(int32_t block_size, int64_t nC) {
+  return numeric_impl() == 2 ? numeric_tma_ws_bytes(block_size, nC) : 0;
+}
+
 extern "C" int qm_numeric(const qm_layout *layout, const double *a_blocks, int64_t nA,
                           const double *b_blocks, int64_t nB, const uint32_t *tri,
                           const int64_t *c_tptr, int64_t nC, double *c_blocks, double *c_sumsq,
-                          uint8_t *c_nonzero, int64_t *zero_count, void *stream) {
+                          uint8_t *c_nonzero, int64_t *zero_count, void *ws, size_t ws_bytes,
+                          void *stream) {
   Geometry g;
   int rc = make_geometry(layout, &g);
   if (rc != QM_OK) return rc;
@@ -377,7 +383,7 @@ extern "C" int qm_numeric(const qm_layout *layout, const double *a_blocks, int64
   const uint2 *t2 = (const uint2 *)tri;
   if (numeric_impl() == 2) {
     rc = launch_numeric_tma(g.bs, a_blocks, nA, b_blocks, nB, tri, c_tptr, nC, c_blocks, c_sumsq,
-                            c_nonzero, zero_count, st);
+                            c_nonzero, zero_count, ws, ws_bytes, st);
     if (rc != QM_ERR_UNSUPPORTED) return rc;
   }
   switch (g.bs) {

@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "qm_common.cuh"
 
@@ -79,50 +80,55 @@ __host__ __device__ __forceinline__ int kperm(int t, int j) {
   }
 }
 
-template <int BS_, int WARPS_M_, int WARPS_N_, int KP_, int STAGES_, int MINB_>
+// A CTA computes one TILE x TILE tile of a C block (TILE = BS, or 64 for BS = 128: the block is
+// then NQ = (BS/TILE)^2 work units whose partial norms are combined in a fixed order afterwards).
+template <int BS_, int TILE_, int WARPS_M_, int WARPS_N_, int KP_, int STAGES_, int MINB_>
 struct TmaCfg {
-  static constexpr int BS = BS_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, KP = KP_, STAGES = STAGES_;
-  static constexpr int MINB = MINB_;
+  static constexpr int BS = BS_, TILE = TILE_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, KP = KP_;
+  static constexpr int STAGES = STAGES_, MINB = MINB_;
+  static constexpr int NQN = BS / TILE, NQ = NQN * NQN;  // tiles per C block
   static constexpr int NCW = WARPS_M * WARPS_N;         // consumer warps
   static constexpr int NTHR = 32 * (NCW + 1);           // + one producer warp
-  static constexpr int TM = BS / WARPS_M, TN = BS / WARPS_N;
+  static constexpr int TM = TILE / WARPS_M, TN = TILE / WARPS_N;
   static constexpr int MT = TM / 8, NT = TN / 8;
   static constexpr int NP = BS / KP;                    // k panels per triple
   static constexpr int KSP = KP / 16;                   // 16-wide k sub-panels per stage (A)
-  static constexpr int NSP = BS / 16;                   // 16-wide column sub-panels (B)
-  static constexpr int A_SP_BYTES = BS * 128;           // one A sub-panel: BS rows x 16 doubles
+  static constexpr int NSP = TILE / 16;                 // 16-wide column sub-panels (B)
+  static constexpr int A_SP_BYTES = TILE * 128;         // one A sub-panel: TILE rows x 16 doubles
   static constexpr int B_SP_BYTES = KP * 128;           // one B sub-panel: KP rows x 16 doubles
   static constexpr int A_BYTES = KSP * A_SP_BYTES;
   static constexpr int B_BYTES = NSP * B_SP_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 2 * STAGES * 8 + 2 * 32 * 8;
-  static_assert(KP % 16 == 0 && BS % KP == 0 && BS % 16 == 0, "panels");
+  static_assert(KP % 16 == 0 && BS % KP == 0 && TILE % 16 == 0 && BS % TILE == 0, "panels");
   static_assert(TM % 8 == 0 && TN % 8 == 0, "warp tile");
   static_assert(A_SP_BYTES % 1024 == 0 && B_SP_BYTES % 1024 == 0, "swizzle-128B atoms need 1 KB alignment");
 };
 
+// Stage cursor over work units u = m * NQ + q (C block m, tile q), triple t, k panel p.
 struct Cur {
-  int64_t item, t, tend;
+  int64_t unit, t, tend;
   int p;
 };
 
 template <class Cfg>
-__device__ __forceinline__ void cur_start(Cur &c, int64_t item, int64_t nC, const int64_t *tptr) {
-  c.item = item;
+__device__ __forceinline__ void cur_start(Cur &c, int64_t unit, int64_t nU, const int64_t *tptr) {
+  c.unit = unit;
   c.p = 0;
-  if (item < nC) {
-    c.t = tptr[item];
-    c.tend = tptr[item + 1];
+  if (unit < nU) {
+    const int64_t m = unit / Cfg::NQ;
+    c.t = tptr[m];
+    c.tend = tptr[m + 1];
   } else {
     c.t = c.tend = 0;
   }
 }
 
 template <class Cfg>
-__device__ __forceinline__ void cur_next(Cur &c, int64_t nC, const int64_t *tptr) {
+__device__ __forceinline__ void cur_next(Cur &c, int64_t nU, const int64_t *tptr) {
   if (++c.p == Cfg::NP) {
     c.p = 0;
-    if (++c.t == c.tend) cur_start<Cfg>(c, c.item + gridDim.x, nC, tptr);
+    if (++c.t == c.tend) cur_start<Cfg>(c, c.unit + gridDim.x, nU, tptr);
   }
 }
 
@@ -131,10 +137,15 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
     k_numeric_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const uint2 *__restrict__ tri, const int64_t *__restrict__ tptr, int64_t nC,
                   double *__restrict__ C, double *__restrict__ csq, uint8_t *__restrict__ cnz,
-                  int64_t *__restrict__ zero_count) {
+                  int64_t *__restrict__ zero_count, double *__restrict__ part_sq,
+                  uint8_t *__restrict__ part_nz, uint64_t zmask) {
   constexpr int BS = Cfg::BS, MT = Cfg::MT, NT = Cfg::NT, STAGES = Cfg::STAGES;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int64_t nU = nC * Cfg::NQ;
+  // Align to 1 KB (SWIZZLE_128B atoms) by offsetting the __shared__ array itself: the pointer keeps
+  // the shared address space, so fragment loads are LDS (not generic LD) and stay ordered before
+  // the stage-release mbarrier arrive.
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t *full = (uint64_t *)(smem + (size_t)STAGES * Cfg::STAGE_BYTES);
   uint64_t *empty = full + STAGES;
   double *red = (double *)(empty + STAGES);  // [32] sums, [32] nonzero flags
@@ -155,22 +166,25 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
       Cur L;
-      cur_start<Cfg>(L, blockIdx.x, nC, tptr);
+      cur_start<Cfg>(L, blockIdx.x, nU, tptr);
       int s = 0;
       uint32_t phase = 0;
-      while (L.item < nC) {
+      while (L.unit < nU) {
         mbar_wait(&empty[s], phase ^ 1u);
         const uint2 ab = tri[L.t];
+        const int qt = (int)(L.unit % Cfg::NQ);
+        const int row0 = (qt / Cfg::NQN) * Cfg::TILE, col0 = (qt % Cfg::NQN) * Cfg::TILE;
         uint8_t *st = smem + (size_t)s * Cfg::STAGE_BYTES;
         mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
 #pragma unroll
         for (int q = 0; q < Cfg::KSP; ++q)
-          tma_load_2d(st + q * Cfg::A_SP_BYTES, &tmA, L.p * Cfg::KP + q * 16, (int)(ab.x * BS), &full[s]);
+          tma_load_2d(st + q * Cfg::A_SP_BYTES, &tmA, L.p * Cfg::KP + q * 16, (int)(ab.x * BS + row0),
+                      &full[s]);
 #pragma unroll
         for (int q = 0; q < Cfg::NSP; ++q)
-          tma_load_2d(st + Cfg::A_BYTES + q * Cfg::B_SP_BYTES, &tmB, q * 16,
+          tma_load_2d(st + Cfg::A_BYTES + q * Cfg::B_SP_BYTES, &tmB, col0 + q * 16,
                       (int)(ab.y * BS + L.p * Cfg::KP), &full[s]);
-        cur_next<Cfg>(L, nC, tptr);
+        cur_next<Cfg>(L, nU, tptr);
         if (++s == STAGES) {
           s = 0;
           phase ^= 1u;
@@ -204,10 +218,10 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   Cur Cc;
-  cur_start<Cfg>(Cc, blockIdx.x, nC, tptr);
+  cur_start<Cfg>(Cc, blockIdx.x, nU, tptr);
   int s = 0;
   uint32_t phase = 0;
-  while (Cc.item < nC) {
+  while (Cc.unit < nU) {
     mbar_wait(&full[s], phase);
     const uint8_t *sa = smem + (size_t)s * Cfg::STAGE_BYTES;
     const uint8_t *sb = sa + Cfg::A_BYTES;
@@ -231,16 +245,28 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
           for (int n = 0; n < NT; ++n) dmma(acc[i][n][0], acc[i][n][1], af[i], bf[n]);
       }
     }
+    // Release the stage only after every DMMA of the stage has completed: the arrive's address
+    // carries a data dependency on all accumulators (masked by zmask, a runtime zero). Without it
+    // ptxas hoists the arrive above trailing DMMAs, and under DMMA-pipe contention (2 CTAs/SM) a
+    // queued DMMA was observed to pick up fragment registers already reloaded for the next stage.
+    uint64_t dep = 0;
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int n = 0; n < NT; ++n) dep |= (uint64_t)__double_as_longlong(acc[i][n][0]);
+    dep &= zmask;
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (lane == 0) mbar_arrive(&empty[s] + (uint32_t)dep);
     if (++s == STAGES) {
       s = 0;
       phase ^= 1u;
     }
 
     if (Cc.p == Cfg::NP - 1 && Cc.t + 1 == Cc.tend) {
-      const int64_t m = Cc.item;
-      double *cb = C + (size_t)m * (BS * BS);
+      const int64_t m = Cc.unit / Cfg::NQ;
+      const int qt = (int)(Cc.unit % Cfg::NQ);
+      double *cb = C + (size_t)m * (BS * BS) + (size_t)(qt / Cfg::NQN) * Cfg::TILE * BS +
+                   (qt % Cfg::NQN) * Cfg::TILE;
       double ss = 0.0;
       bool nz = false;
 #pragma unroll
@@ -270,13 +296,35 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
           tot += red[w];
           anynz += red[32 + w];
         }
-        csq[m] = tot;
-        cnz[m] = anynz != 0.0;
-        if (anynz == 0.0 && zero_count) atomicAdd((unsigned long long *)zero_count, 1ull);
+        if (Cfg::NQ == 1) {
+          csq[m] = tot;
+          cnz[m] = anynz != 0.0;
+          if (anynz == 0.0 && zero_count) atomicAdd((unsigned long long *)zero_count, 1ull);
+        } else {
+          part_sq[Cc.unit] = tot;
+          part_nz[Cc.unit] = anynz != 0.0;
+        }
       }
       asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::NCW * 32) : "memory");
     }
-    cur_next<Cfg>(Cc, nC, tptr);
+    cur_next<Cfg>(Cc, nU, tptr);
+  }
+}
+
+// Fixed-order combination of the per-tile partial norms / nonzero flags of NQ-tile C blocks.
+__global__ void k_combine_tiles(const double *part_sq, const uint8_t *part_nz, int nq, int64_t nC,
+                                double *csq, uint8_t *cnz, int64_t *zero_count) {
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < nC;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    int any = 0;
+    for (int q = 0; q < nq; ++q) {
+      s += part_sq[m * nq + q];
+      any |= part_nz[m * nq + q];
+    }
+    csq[m] = s;
+    cnz[m] = (uint8_t)(any != 0);
+    if (!any && zero_count) atomicAdd((unsigned long long *)zero_count, 1ull);
   }
 }
 
@@ -325,11 +373,26 @@ int sm_count_tma() {
 }
 
 template <class Cfg>
+size_t tma_ws_bytes(int64_t nC) {
+  return Cfg::NQ == 1 ? 0 : (size_t)nC * Cfg::NQ * (sizeof(double) + sizeof(uint8_t)) + 256;
+}
+
+template <class Cfg>
 int launch_tma(const double *A, int64_t nA, const double *B, int64_t nB, const uint2 *tri,
                const int64_t *tptr, int64_t nC, double *C, double *csq, uint8_t *cnz, int64_t *zc,
-               cudaStream_t st) {
+               void *ws, size_t ws_bytes, cudaStream_t st) {
+  double *part_sq = nullptr;
+  uint8_t *part_nz = nullptr;
+  if (Cfg::NQ > 1) {
+    if (!ws || ws_bytes < tma_ws_bytes<Cfg>(nC)) {
+      set_error("qm_numeric: workspace %zu < required %zu", ws_bytes, tma_ws_bytes<Cfg>(nC));
+      return QM_ERR_WORKSPACE;
+    }
+    part_sq = (double *)ws;
+    part_nz = (uint8_t *)(part_sq + nC * Cfg::NQ);
+  }
   CUtensorMap ma, mb;
-  int rc = make_map(&ma, A, nA, Cfg::BS, Cfg::BS);
+  int rc = make_map(&ma, A, nA, Cfg::BS, Cfg::TILE);
   if (rc != QM_OK) return rc;
   rc = make_map(&mb, B, nB, Cfg::BS, Cfg::KP);
   if (rc != QM_OK) return rc;
@@ -342,29 +405,55 @@ int launch_tma(const double *A, int64_t nA, const double *B, int64_t nB, const u
   int per_sm = 0;
   QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_numeric_tma<Cfg>, Cfg::NTHR, Cfg::SMEM));
   if (per_sm < 1) per_sm = 1;
+  const int64_t nU = nC * Cfg::NQ;
   int64_t grid = (int64_t)sm_count_tma() * per_sm;
-  if (grid > nC) grid = nC;
-  k_numeric_tma<Cfg><<<(int)grid, Cfg::NTHR, Cfg::SMEM, st>>>(ma, mb, tri, tptr, nC, C, csq, cnz, zc);
+  if (grid > nU) grid = nU;
+  k_numeric_tma<Cfg><<<(int)grid, Cfg::NTHR, Cfg::SMEM, st>>>(ma, mb, tri, tptr, nC, C, csq, cnz, zc,
+                                                              part_sq, part_nz, /*zmask=*/0ull);
   QM_LAUNCHED("k_numeric_tma");
+  if (Cfg::NQ > 1) {
+    int64_t g = std::min<int64_t>((nC + 255) / 256, (int64_t)sm_count_tma() * 8);
+    k_combine_tiles<<<(int)std::max<int64_t>(g, 1), 256, 0, st>>>(part_sq, part_nz, Cfg::NQ, nC, csq,
+                                                                   cnz, zc);
+    QM_LAUNCHED("k_combine_tiles");
+  }
   return QM_OK;
 }
 
-//                     BS  WM WN  KP STAGES MINB
-using Tma32 = TmaCfg<32, 1, 2, 32, 3, 4>;
-using Tma64 = TmaCfg<64, 2, 2, 32, 3, 2>;
-using Tma128 = TmaCfg<128, 2, 4, 16, 6, 1>;
+//                     BS TILE WM WN KP STAGES MINB
+using Tma32 = TmaCfg<32, 32, 1, 2, 32, 3, 4>;
+using Tma64 = TmaCfg<64, 64, 2, 2, 32, 3, 2>;
+using Tma128 = TmaCfg<128, 64, 2, 2, 32, 3, 2>;
+using Tma64x1 = TmaCfg<64, 64, 2, 2, 32, 6, 1>;  // diagnostic variant: 1 CTA/SM, 6 stages
+
+int tma_variant() {
+  const char *e = getenv("QM_TMA_VARIANT");
+  return e ? atoi(e) : 0;
+}
 
 }  // namespace
+
+size_t numeric_tma_ws_bytes(int bs, int64_t nC) {
+  switch (bs) {
+    case 32: return tma_ws_bytes<Tma32>(nC);
+    case 64: return tma_ws_bytes<Tma64>(nC);
+    case 128: return tma_ws_bytes<Tma128>(nC);
+    default: return 0;
+  }
+}
 
 // Returns QM_ERR_UNSUPPORTED when no TMA variant exists for bs.
 int launch_numeric_tma(int bs, const double *A, int64_t nA, const double *B, int64_t nB,
                        const uint32_t *tri, const int64_t *tptr, int64_t nC, double *C, double *csq,
-                       uint8_t *cnz, int64_t *zc, cudaStream_t st) {
+                       uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes, cudaStream_t st) {
   const uint2 *t2 = (const uint2 *)tri;
   switch (bs) {
-    case 32: return launch_tma<Tma32>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, st);
-    case 64: return launch_tma<Tma64>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, st);
-    case 128: return launch_tma<Tma128>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, st);
+    case 32: return launch_tma<Tma32>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
+    case 64:
+      if (tma_variant() == 1)
+        return launch_tma<Tma64x1>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
+      return launch_tma<Tma64>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
+    case 128: return launch_tma<Tma128>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
     default: return QM_ERR_UNSUPPORTED;
   }
 }

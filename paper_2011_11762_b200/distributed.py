@@ -35,6 +35,9 @@ from .blocks import BlockSet
 from .errors import ContractViolationError
 
 
+_DEBUG_SYNC = bool(int(__import__("os").environ.get("QM_DEBUG_SYNC", "0")))
+
+
 class Comm:
     """torch.distributed collectives used by the product (process group `group`)."""
 
@@ -217,6 +220,8 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     else:
         pool_b, rb, sb, nb = _fetch(comm, backend, b_local.blocks, b_off, need_b)
     stats.bytes_received, stats.bytes_sent, stats.blocks_received = ra + rb, sa + sb, na + nb
+    if _DEBUG_SYNC:
+        torch.cuda.synchronize(dev)
     t3 = clock()
     if hi == lo:
         return empty, stats

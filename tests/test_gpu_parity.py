@@ -263,3 +263,20 @@ def test_distributed_path_single_rank_matches(ses):
         assert torch.equal(c2.keys, ref.keys) and torch.equal(c2.blocks, ref.blocks)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("bs", [32, 64, 128])
+def test_numeric_kernel_is_deterministic_under_repetition(ses, bs):
+    """Regression test for a stage-release race: the fixed summation order
+    makes every repetition bitwise identical; 60 back-to-back launches must agree exactly."""
+    cfg = G.BaselineConfig("rep", "banded", 256 * bs, bs, half_bw=8 * bs)
+    geom, a, b = G.config_operands_device(cfg, ses.device)
+    layout = _ffi.make_layout(geom.params, bs)
+    plan = spgemm.symbolic(layout, a, b)
+    first, _, _ = spgemm.numeric(layout, a, b, plan)
+    bad = 0
+    for _ in range(60):
+        c, _, _ = spgemm.numeric(layout, a, b, plan)
+        bad += int(not torch.equal(c.blocks, first.blocks))
+    torch.cuda.synchronize()
+    assert bad == 0
