@@ -340,7 +340,7 @@ def run_ours(args):
                    "parallelism": f"keyrange-partition dp{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (no flush)"},
         "phases_ms": {"symbolic": round(statistics.mean(symbolic_ms), 4), "numeric": round(nk_ms, 4)},
-        "roofline": {"bound": "tensor", "kernel": "k_numeric_dmma", "achieved": round(achieved, 3),
+        "roofline": {"bound": "tensor", "kernel": "k_numeric_tma", "achieved": round(achieved, 3),
                      "peak": round(peak, 3), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
                      "peak_source": f"max(measured DMMA {peaks['dmma']:.2f}, measured DFMA "
                                     f"{peaks['dfma']:.2f}, nominal {FP64_NOMINAL_TFLOPS}) TFLOP/s; "
@@ -348,7 +348,7 @@ def run_ours(args):
                      "algorithmic_bytes": alg_bytes,
                      "hbm_gbs_at_alg_bytes": round(alg_bytes / (nk_ms * 1e-3) / 1e9, 1),
                      "traffic": traffic,
-                     "traffic_note": "dram read+write bytes of one k_numeric_dmma launch from a "
+                     "traffic_note": "dram read+write bytes of one k_numeric_tma launch from a "
                                      "committed ncu --set full capture (profiles/ncu_traffic.json)"},
         "clocks": clock,
         "gpu_launches": int(launches),
