@@ -81,6 +81,22 @@ QM_API int qm_encode_keys(const qm_layout *layout, const int32_t *bi /*device*/,
 QM_API int qm_decode_keys(const qm_layout *layout, const uint64_t *keys /*device*/, int64_t n,
                    int32_t *bi /*device*/, int32_t *bj /*device*/, void *stream);
 
+/* ---- construction (replaces build_from_triplets + BlockSparseLeaf.from_triplets,
+ *      quadtree.py:90-142, block_sparse.py:47-68) ---------------------------------------------- */
+QM_API size_t qm_build_workspace_bytes(const qm_layout *layout, int64_t n_entries);
+/* Sorts the entries by (block quadtree key, position in block), stably, and counts the distinct
+ * blocks touched. Entries outside [0, n_logical) are counted in *n_out_of_range (host) and nothing
+ * else is done (the caller raises OutOfRangeError). Synchronises `stream`. */
+QM_API int qm_build_count(const qm_layout *layout, const int64_t *rows /*device*/,
+                          const int64_t *cols /*device*/, int64_t n, void *ws, size_t ws_bytes,
+                          int64_t *n_blocks_out /*host*/, int64_t *n_out_of_range /*host*/, void *stream);
+/* Sums duplicate entries in input order starting from +0.0 (np.add.at), writes keys[n_blocks],
+ * blocks[n_blocks,bs,bs], sumsq, nonzero flags and counts exactly-zero blocks in *zero_count
+ * (device; the caller zeroes it first and compacts with qm_compact when it is nonzero). */
+QM_API int qm_build_fill(const qm_layout *layout, const double *vals /*device*/, int64_t n, void *ws,
+                         size_t ws_bytes, int64_t n_blocks, uint64_t *keys, double *blocks,
+                         double *sumsq, uint8_t *nonzero, int64_t *zero_count, void *stream);
+
 /* ---- symbolic phase (replaces the recursive task expansion, ops.py:197-245 + engine.py:196-326) */
 /* Persistent workspace for one product; valid from qm_spgemm_count until qm_spgemm_fill returns. */
 QM_API size_t qm_spgemm_workspace_bytes(const qm_layout *layout, int64_t nA, int64_t nB);

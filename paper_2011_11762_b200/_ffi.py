@@ -31,6 +31,9 @@ EXPORTS = (
     "qm_launch_count",
     "qm_encode_keys",
     "qm_decode_keys",
+    "qm_build_workspace_bytes",
+    "qm_build_count",
+    "qm_build_fill",
     "qm_spgemm_workspace_bytes",
     "qm_spgemm_count",
     "qm_spgemm_fill_workspace_bytes",
@@ -75,6 +78,10 @@ _SIGS = {
     "qm_launch_count": (ctypes.c_uint64, []),
     "qm_encode_keys": (ctypes.c_int, [_LP, _P, _P, _I64, _P, _P]),
     "qm_decode_keys": (ctypes.c_int, [_LP, _P, _I64, _P, _P, _P]),
+    "qm_build_workspace_bytes": (_SZ, [_LP, _I64]),
+    "qm_build_count": (ctypes.c_int, [_LP, _P, _P, _I64, _P, _SZ, ctypes.POINTER(_I64),
+                                      ctypes.POINTER(_I64), _P]),
+    "qm_build_fill": (ctypes.c_int, [_LP, _P, _I64, _P, _SZ, _I64, _P, _P, _P, _P, _P, _P]),
     "qm_spgemm_workspace_bytes": (_SZ, [_LP, _I64, _I64]),
     "qm_spgemm_count": (ctypes.c_int, [_LP, _P, _I64, _P, _I64, _P, _SZ, ctypes.POINTER(_I64),
                                        ctypes.POINTER(_I64), _P]),

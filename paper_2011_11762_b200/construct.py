@@ -105,3 +105,53 @@ def identity_triplets(n: int, c: float):
     """add_scaled_identity on a nil matrix (ops.py:253-270): c on the logical diagonal only."""
     d = np.arange(n, dtype=np.int64)
     return d, d, np.full(n, float(c))
+
+
+def blocks_from_triplets_device(geom: Geometry, rows, cols, vals, device, stream=None):
+    """Device build (libqmb200 qm_build_count / qm_build_fill / qm_compact): the same blocks as
+    ``blocks_from_triplets`` bit for bit, as a BlockSet on ``device``."""
+    import ctypes
+
+    import torch
+
+    from . import _ffi
+    from .blocks import BlockSet
+
+    lib = _ffi.load()
+    dev = torch.device(device)
+    bs = geom.bs
+    r = torch.as_tensor(np.ascontiguousarray(rows, dtype=np.int64).ravel()).to(dev)
+    c = torch.as_tensor(np.ascontiguousarray(cols, dtype=np.int64).ravel()).to(dev)
+    v = torch.as_tensor(np.ascontiguousarray(vals, dtype=np.float64).ravel()).to(dev)
+    n = int(r.shape[0])
+    if n == 0:
+        return BlockSet.empty(bs, dev)
+    layout = _ffi.make_layout(geom.params, bs)
+    lp = ctypes.byref(layout)
+    with torch.cuda.device(dev):
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        sh = _ffi.stream_handle(st)
+        wb = lib.qm_build_workspace_bytes(lp, n)
+        ws = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
+        nb = ctypes.c_int64(0)
+        bad = ctypes.c_int64(0)
+        _ffi.check(lib.qm_build_count(lp, _ffi.ptr(r), _ffi.ptr(c), n, _ffi.ptr(ws), wb,
+                                      ctypes.byref(nb), ctypes.byref(bad), sh), "qm_build_count")
+        if bad.value:
+            raise OutOfRangeError(f"entry index outside [0, {geom.params.n_logical})")
+        nblk = int(nb.value)
+        out = BlockSet(torch.empty(nblk, dtype=torch.int64, device=dev),
+                       torch.empty((nblk, bs, bs), dtype=torch.float64, device=dev),
+                       torch.empty(nblk, dtype=torch.float64, device=dev))
+        nz = torch.empty(nblk, dtype=torch.uint8, device=dev)
+        zc = torch.zeros(1, dtype=torch.int64, device=dev)
+        _ffi.check(lib.qm_build_fill(lp, _ffi.ptr(v), n, _ffi.ptr(ws), wb, nblk, _ffi.ptr(out.keys),
+                                     _ffi.ptr(out.blocks), _ffi.ptr(out.sumsq), _ffi.ptr(nz),
+                                     _ffi.ptr(zc), sh), "qm_build_fill")
+        st.synchronize()
+        n_zero = int(zc.item())
+        if n_zero:
+            from .spgemm import compact  # noqa: PLC0415
+
+            out = compact(bs, out, nz, n_zero, st)
+    return out

@@ -295,6 +295,10 @@ class MatrixSession:
         vals = np.asarray(vals, dtype=np.float64)
         if symmetric:
             rows, cols, vals = construct.mirror_symmetric(rows, cols, vals, leaf_dim)
+        if self.device.type == "cuda":  # device build (qm_build_*), bit-identical to the host one
+            bset = construct.blocks_from_triplets_device(geom, rows, cols, vals, self.device)
+            return Matrix(self.store.register(self._distribute(bset)), geom.params,
+                          LeafKind.BLOCK_SPARSE, geom.bs, symmetric)
         keys, blocks = construct.blocks_from_triplets(geom, rows, cols, vals)
         return self.matrix_from_blocks(geom, keys, blocks, symmetric)
 

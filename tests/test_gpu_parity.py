@@ -280,3 +280,39 @@ def test_numeric_kernel_is_deterministic_under_repetition(ses, bs):
         bad += int(not torch.equal(c.blocks, first.blocks))
     torch.cuda.synchronize()
     assert bad == 0
+
+
+@pytest.mark.parametrize("n,leaf,bs", [(13, 4, 2), (100, 16, 4), (37, 12, 4), (300, 64, 16), (1000, 64, 64), (777, 96, 32)])
+def test_device_construction_is_bit_identical_to_host(ses, n, leaf, bs):
+    """qm_build_* (GPU construction) == the host build == the reference's build:
+    duplicate sums in input order (np.add.at), -0.0 -> +0.0, exactly-cancelling blocks dropped."""
+    from paper_2011_11762_b200 import construct
+
+    rng = np.random.default_rng(n + bs)
+    m = max(4, n * n // 20)
+    r = rng.integers(0, n, m)
+    c = rng.integers(0, n, m)
+    v = rng.standard_normal(m)
+    # duplicates, a negative zero, and one block whose entries cancel exactly
+    r = np.concatenate([r, r[:50], [0], [n - 1, n - 1]])
+    c = np.concatenate([c, c[:50], [n - 1], [0, 0]])
+    v = np.concatenate([v, 0.5 * v[:50], [-0.0], [3.0, -3.0]])
+    geom = Geometry(MatrixParams.create(n, leaf), bs)
+    kh, bh = construct.blocks_from_triplets(geom, r, c, v)
+    dev = construct.blocks_from_triplets_device(geom, r, c, v, ses.device)
+    np.testing.assert_array_equal(dev.keys.cpu().numpy(), kh)
+    np.testing.assert_array_equal(dev.blocks.cpu().numpy(), bh)  # bitwise (incl. signs of zeros)
+    assert not np.any(np.signbit(dev.blocks.cpu().numpy()) & (dev.blocks.cpu().numpy() == 0))
+
+
+def test_device_construction_errors_and_empty(ses):
+    from paper_2011_11762_b200 import OutOfRangeError, construct
+
+    geom = Geometry(MatrixParams.create(64, 16), 8)
+    with pytest.raises(OutOfRangeError):
+        construct.blocks_from_triplets_device(geom, [0, 64], [0, 1], [1.0, 2.0], ses.device)
+    assert construct.blocks_from_triplets_device(geom, [], [], [], ses.device).n == 0
+    z = construct.blocks_from_triplets_device(geom, [1, 1], [2, 2], [1.5, -1.5], ses.device)
+    assert z.n == 0  # the only block sums to exactly zero and is dropped
+    m = ses.matrix_from_triplets(64, [1, 1], [2, 2], [1.5, -1.5], leaf_dim=16, block_size=8)
+    assert m.root.is_nil
