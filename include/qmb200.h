@@ -156,6 +156,11 @@ QM_API int qm_block_stats(int32_t block_size, int64_t n, const double *blocks, d
 QM_API int qm_gather_blocks(int32_t block_size, const double *src, const int64_t *idx, int64_t n,
                      double *dst, void *stream);
 
+/* dst[i] = src[i]^T per bs x bs block: the materialised form of the reference's virtual transpose
+ * (op_view, leaves/base.py:117-118; ta/tb/symmetric children, ops.py:100-116). */
+QM_API int qm_transpose_blocks(int32_t block_size, const double *src, int64_t n, double *dst,
+                               void *stream);
+
 /* ---- synthetic inputs (device side of the block-keyed generator) -------- */
 /* For each key, fills the block with numpy's default_rng([seed, matrix_id, bi, bj]).uniform(-1, 1,
  * (bs, bs)) -- bit-identical PCG64 + SeedSequence -- then zeroes entries outside the element

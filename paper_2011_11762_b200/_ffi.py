@@ -47,6 +47,7 @@ EXPORTS = (
     "qm_compact",
     "qm_block_stats",
     "qm_gather_blocks",
+    "qm_transpose_blocks",
     "qm_generate_blocks",
     "qm_fp64_peak_kernel",
 )
@@ -97,6 +98,7 @@ _SIGS = {
     "qm_compact": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "qm_block_stats": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P]),
     "qm_gather_blocks": (ctypes.c_int, [_I32, _P, _P, _I64, _P, _P]),
+    "qm_transpose_blocks": (ctypes.c_int, [_I32, _P, _I64, _P, _P]),
     "qm_generate_blocks": (ctypes.c_int, [_LP, _P, _I64, ctypes.c_uint64, ctypes.c_uint32, _I32,
                                           _I64, _P, _P, _P]),
     "qm_fp64_peak_kernel": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _I64, _P,

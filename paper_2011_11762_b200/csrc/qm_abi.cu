@@ -94,6 +94,27 @@ __global__ void __launch_bounds__(256) k_gather_blocks(int bs, const double *src
   }
 }
 
+// dst[i] = transpose(src[i]) for bs x bs blocks (32x33 smem tiles).
+__global__ void __launch_bounds__(256) k_transpose_blocks(int bs, const double *src, int64_t n, double *dst) {
+  __shared__ double tile[32][33];
+  const int nt = (bs + 31) / 32;
+  const int64_t work = n * nt * nt;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int64_t w = blockIdx.x; w < work; w += gridDim.x) {
+    const int64_t m = w / (nt * nt);
+    const int t = (int)(w % (nt * nt));
+    const int r0 = (t / nt) * 32, c0 = (t % nt) * 32;
+    const double *s = src + (size_t)m * bs * bs;
+    double *d = dst + (size_t)m * bs * bs;
+    for (int q = ty; q < 32; q += 8)
+      if (r0 + q < bs && c0 + tx < bs) tile[q][tx] = s[(size_t)(r0 + q) * bs + c0 + tx];
+    __syncthreads();
+    for (int q = ty; q < 32; q += 8)
+      if (c0 + q < bs && r0 + tx < bs) d[(size_t)(c0 + q) * bs + r0 + tx] = tile[tx][q];
+    __syncthreads();
+  }
+}
+
 size_t compact_cub_bytes(int64_t n) {
   size_t b = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t *)nullptr, (int64_t *)nullptr, n);
@@ -180,5 +201,19 @@ extern "C" int qm_gather_blocks(int32_t block_size, const double *src, const int
   int64_t grid = std::min<int64_t>(n, 148 * 16);
   k_gather_blocks<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(block_size, src, idx, n, dst);
   QM_LAUNCHED("k_gather_blocks");
+  return QM_OK;
+}
+
+extern "C" int qm_transpose_blocks(int32_t block_size, const double *src, int64_t n, double *dst,
+                                   void *stream) {
+  if (block_size < 1 || n < 0 || src == dst) {
+    set_error("qm_transpose_blocks: bad arguments (in-place is not supported)");
+    return QM_ERR_INVALID;
+  }
+  if (n == 0) return QM_OK;
+  const int nt = (block_size + 31) / 32;
+  int64_t grid = std::min<int64_t>(n * nt * nt, 148 * 16);
+  k_transpose_blocks<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(block_size, src, n, dst);
+  QM_LAUNCHED("k_transpose_blocks");
   return QM_OK;
 }

@@ -204,12 +204,13 @@ class MatrixSession:
                 f"task type {spec.task_type!r} is outside the B200 hot path (only 'multiply')"
             )
         args = spec.args
-        if args.get("tau", 0.0) > 0.0 or args.get("ta") or args.get("tb") or args.get("upper") \
-                or args.get("a_sym") or args.get("b_sym"):
+        if args.get("tau", 0.0) > 0.0:
             raise ConfigurationError(
-                "only the regular multiply variant runs on the B200 path "
-                "(symmetric / rank_k / approximate are listed as next in SURVEY.md 8(f))"
+                "the approximate (norm-pruned) variant is not on the B200 path yet "
+                "(SURVEY.md 8(f) #4); use tau=0"
             )
+        if args.get("ta"):
+            raise ConfigurationError("a transposed left operand is not a level-0 multiply spec")
         a_root, b_root = spec.inputs
         geom: Geometry = args["geometry"]
         stats = spgemm.MultiplyStats()
@@ -219,10 +220,27 @@ class MatrixSession:
             return NIL  # _multiply_fallback (ops.py:244-245): a nil operand gives nil
         a, b = a_root.require(), b_root.require()
         layout = make_layout(geom.params, geom.bs)
+        plain = not (args.get("tb") or args.get("upper") or args.get("a_sym") or args.get("b_sym"))
         if self.comm is not None:
+            if not plain:
+                raise ConfigurationError("multi-GPU products run the regular variant on general operands")
             return self._run_distributed(layout, a, b, a_root is b_root, stats)
-        with torch.cuda.device(a.device) if a.device.type == "cuda" else _null():
+        spgemm._require_cuda(a.blocks)
+        with torch.cuda.device(a.device):
+            if not plain:  # variants: materialise the reference's virtual transposes (variants.py)
+                from . import variants  # noqa: PLC0415
+
+                same = a_root is b_root
+                if args.get("a_sym"):
+                    a = variants.expand_symmetric(geom, a)
+                if args.get("b_sym"):
+                    b = a if (same and args.get("a_sym")) else variants.expand_symmetric(geom, b)
+                if args.get("tb"):
+                    b = variants.transpose(geom, b)
             c = spgemm.multiply_blocks(layout, a, b, stats=stats)
+            if args.get("upper"):
+                c = variants.upper_leaves(geom, c)
+                stats.n_c = c.n
         self.last_stats = [WorkerStats(0, tasks_executed=stats.n_triples)]
         return self.store.register(c)
 

@@ -1,0 +1,118 @@
+"""Multiply variants of the reference (ops.py:47-76, 582-608) on device block sets.
+
+The reference never materialises a transpose: tasks carry ta/tb flags and `_virtual_child`
+(ops.py:100-116) maps quadrants, and symmetric matrices store only the upper triangle at leaf
+granularity (SW quadrant of every diagonal-path node is nil and implied by NE^T; diagonal leaves
+hold full blocks, session.py:93-100). `upper` (symmetric_square, rank_k) makes every diagonal-path
+node skip its SW quadrant (ops.py:214-216) while leaf products stay full, so the result holds
+exactly the blocks of leaves (li, lj) with li <= lj.
+
+On the GPU the same algebra is expressed on flat block sets:
+  * transpose(X):        keys (bi,bj) -> (bj,bi) re-sorted, blocks transposed (qm_transpose_blocks);
+  * expand_symmetric(S): S plus transposed copies of the blocks of strictly-upper leaves;
+  * upper_leaves(C):     keep blocks of leaves with li <= lj.
+then the regular product runs unchanged:
+  regular/symmetric  C = expand(A) * expand(B)                      (a_sym / b_sym flags)
+  symmetric_square   C = upper(expand(A) * expand(A))               result symmetric
+  rank_k             C = upper(A * transpose(A))                    result symmetric
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _ffi
+from .blocks import BlockSet
+from .layout import Geometry
+
+
+def _decode(geom: Geometry, keys: torch.Tensor):
+    lib = _ffi.load()
+    n = int(keys.shape[0])
+    bi = torch.empty(n, dtype=torch.int32, device=keys.device)
+    bj = torch.empty(n, dtype=torch.int32, device=keys.device)
+    lay = _ffi.make_layout(geom.params, geom.bs)
+    import ctypes
+
+    _ffi.check(lib.qm_decode_keys(ctypes.byref(lay), _ffi.ptr(keys), n, _ffi.ptr(bi), _ffi.ptr(bj),
+                                  _ffi.stream_handle(torch.cuda.current_stream(keys.device))),
+               "qm_decode_keys")
+    return bi, bj
+
+
+def _encode(geom: Geometry, bi: torch.Tensor, bj: torch.Tensor) -> torch.Tensor:
+    import ctypes
+
+    lib = _ffi.load()
+    n = int(bi.shape[0])
+    keys = torch.empty(n, dtype=torch.int64, device=bi.device)
+    lay = _ffi.make_layout(geom.params, geom.bs)
+    _ffi.check(lib.qm_encode_keys(ctypes.byref(lay), _ffi.ptr(bi.contiguous()), _ffi.ptr(bj.contiguous()),
+                                  n, _ffi.ptr(keys), _ffi.stream_handle(torch.cuda.current_stream(bi.device))),
+               "qm_encode_keys")
+    return keys
+
+
+def _gather(bset_blocks: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+    lib = _ffi.load()
+    n = int(idx.shape[0])
+    bs = int(bset_blocks.shape[1])
+    out = torch.empty((n, bs, bs), dtype=torch.float64, device=bset_blocks.device)
+    if n:
+        _ffi.check(lib.qm_gather_blocks(bs, _ffi.ptr(bset_blocks), _ffi.ptr(idx.contiguous()), n, _ffi.ptr(out),
+                                        _ffi.stream_handle(torch.cuda.current_stream(idx.device))),
+                   "qm_gather_blocks")
+    return out
+
+
+def _transposed_blocks(blocks: torch.Tensor) -> torch.Tensor:
+    lib = _ffi.load()
+    n = int(blocks.shape[0])
+    bs = int(blocks.shape[1])
+    out = torch.empty_like(blocks)
+    if n:
+        _ffi.check(lib.qm_transpose_blocks(bs, _ffi.ptr(blocks), n, _ffi.ptr(out),
+                                           _ffi.stream_handle(torch.cuda.current_stream(blocks.device))),
+                   "qm_transpose_blocks")
+    return out
+
+
+def _sorted(keys: torch.Tensor, blocks: torch.Tensor, sumsq: torch.Tensor) -> BlockSet:
+    order = torch.argsort(keys, stable=True)
+    return BlockSet(keys[order].contiguous(), _gather(blocks, order), sumsq[order].contiguous())
+
+
+def transpose(geom: Geometry, x: BlockSet) -> BlockSet:
+    """X^T as a block set (the virtual transpose of op_view / tb=True, materialised)."""
+    if x.n == 0:
+        return x
+    bi, bj = _decode(geom, x.keys)
+    keys = _encode(geom, bj, bi)
+    return _sorted(keys, _transposed_blocks(x.blocks), x.sumsq)
+
+
+def expand_symmetric(geom: Geometry, s: BlockSet) -> BlockSet:
+    """Full matrix of an upper-stored symmetric block set: adds B(bj,bi) = B(bi,bj)^T for every
+    block of a strictly-upper leaf (diagonal leaves already hold both triangles)."""
+    if s.n == 0:
+        return s
+    bi, bj = _decode(geom, s.keys)
+    nbl = geom.nbl
+    off = (bi // nbl) < (bj // nbl)
+    idx = torch.nonzero(off).flatten()
+    if idx.numel() == 0:
+        return s
+    tb = _transposed_blocks(_gather(s.blocks, idx))
+    tk = _encode(geom, bj[idx], bi[idx])
+    return _sorted(torch.cat([s.keys, tk]), torch.cat([s.blocks, tb]), torch.cat([s.sumsq, s.sumsq[idx]]))
+
+
+def upper_leaves(geom: Geometry, c: BlockSet) -> BlockSet:
+    """Blocks of leaves (li, lj) with li <= lj (the `upper` result of ops.py:214-216)."""
+    if c.n == 0:
+        return c
+    bi, bj = _decode(geom, c.keys)
+    keep = torch.nonzero((bi // geom.nbl) <= (bj // geom.nbl)).flatten()
+    if keep.numel() == c.n:
+        return c
+    return BlockSet(c.keys[keep].contiguous(), _gather(c.blocks, keep), c.sumsq[keep].contiguous())

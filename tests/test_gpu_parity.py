@@ -316,3 +316,33 @@ def test_device_construction_errors_and_empty(ses):
     assert z.n == 0  # the only block sums to exactly zero and is dropped
     m = ses.matrix_from_triplets(64, [1, 1], [2, 2], [1.5, -1.5], leaf_dim=16, block_size=8)
     assert m.root.is_nil
+
+
+@pytest.mark.parametrize("ci", range(6))
+def test_multiply_variants_match_reference(ses, ci):
+    """symmetric / symmetric_square / rank_k (ops.py:582-608, virtual children ops.py:100-116):
+    same C block set as the reference, values within TOL, result symmetry flag, dense value."""
+    g = helpers.load("variants")
+    tag = str(g["tags"][ci])
+    _, n, leaf, bs, dens, seed = g["cases"][ci]
+    n, leaf, bs, seed = int(n), int(leaf), int(bs), int(seed)
+    m = helpers.random_sparse(n, float(dens), seed)
+    sym = np.triu(m + m.T)
+    rs, cs = np.nonzero(sym)
+    a_sym = ses.matrix_from_triplets(n, rs, cs, sym[rs, cs], leaf_dim=leaf, block_size=bs, symmetric=True)
+    a_gen = helpers.build(ses, m, leaf, bs)
+    if tag == "symmetric":
+        c = ses.multiply(a_sym, a_gen, variant="symmetric")
+        want = (m + m.T) @ m
+    elif tag == "symmetric_square":
+        c = ses.multiply(a_sym, variant="symmetric_square")
+        want = (m + m.T) @ (m + m.T)
+    else:
+        c = ses.multiply(a_gen, variant="rank_k")
+        want = m @ m.T
+    kc, bc, _ = _host(c)
+    np.testing.assert_array_equal(kc, g[f"c{ci}_keys"])
+    assert helpers.rel(bc, g[f"c{ci}_blocks"]) <= TOL
+    assert c.symmetric == bool(g[f"c{ci}_symmetric"][0])
+    assert helpers.rel(ses.to_dense(c), want) <= TOL
+    assert helpers.rel(ses.to_dense(c), g[f"c{ci}_dense"]) <= TOL
