@@ -204,11 +204,7 @@ class MatrixSession:
                 f"task type {spec.task_type!r} is outside the B200 hot path (only 'multiply')"
             )
         args = spec.args
-        if args.get("tau", 0.0) > 0.0:
-            raise ConfigurationError(
-                "the approximate (norm-pruned) variant is not on the B200 path yet "
-                "(SURVEY.md 8(f) #4); use tau=0"
-            )
+        tau = float(args.get("tau", 0.0))
         if args.get("ta"):
             raise ConfigurationError("a transposed left operand is not a level-0 multiply spec")
         a_root, b_root = spec.inputs
@@ -220,24 +216,36 @@ class MatrixSession:
             return NIL  # _multiply_fallback (ops.py:244-245): a nil operand gives nil
         a, b = a_root.require(), b_root.require()
         layout = make_layout(geom.params, geom.bs)
-        plain = not (args.get("tb") or args.get("upper") or args.get("a_sym") or args.get("b_sym"))
+        plain = not (args.get("tb") or args.get("upper") or args.get("a_sym") or args.get("b_sym")
+                     or tau > 0.0)
         if self.comm is not None:
             if not plain:
                 raise ConfigurationError("multi-GPU products run the regular variant on general operands")
             return self._run_distributed(layout, a, b, a_root is b_root, stats)
         spgemm._require_cuda(a.blocks)
         with torch.cuda.device(a.device):
+            plan_filter = None
             if not plain:  # variants: materialise the reference's virtual transposes (variants.py)
                 from . import variants  # noqa: PLC0415
 
                 same = a_root is b_root
+                a_stored, b_stored = a, b
                 if args.get("a_sym"):
                     a = variants.expand_symmetric(geom, a)
                 if args.get("b_sym"):
                     b = a if (same and args.get("a_sym")) else variants.expand_symmetric(geom, b)
                 if args.get("tb"):
                     b = variants.transpose(geom, b)
-            c = spgemm.multiply_blocks(layout, a, b, stats=stats)
+                if tau > 0.0:  # approximate: prune decisions on stored-chunk norms (approximate.py)
+                    from . import approximate  # noqa: PLC0415
+
+                    b_norms, b_sym = (b, False) if args.get("tb") else (b_stored, bool(args.get("b_sym")))
+                    pr = approximate.prune(geom, a_stored, b_norms, tau, a_sym=bool(args.get("a_sym")),
+                                           b_sym=b_sym, upper=bool(args.get("upper")))
+                    self.last_engine = _EngineInfo(pr.prune_log, pr.pairs_per_level)
+                    ax, bx = a, b
+                    plan_filter = lambda plan: approximate.filter_plan(geom, plan, ax, bx, pr)  # noqa: E731
+            c = spgemm.multiply_blocks(layout, a, b, stats=stats, plan_filter=plan_filter)
             if args.get("upper"):
                 c = variants.upper_leaves(geom, c)
                 stats.n_c = c.n
@@ -414,6 +422,15 @@ class MatrixSession:
         if not self.last_stats:
             return 0
         return sum(s.bytes_received for s in self.last_stats)
+
+
+@dataclass
+class _EngineInfo:
+    """What the reference's ``session.last_engine`` exposes for the approximate variant:
+    ``prune_log`` = bounds of the pruned subproducts (engine.py:156, 273-275)."""
+
+    prune_log: list
+    pairs_per_level: list
 
 
 class _null:

@@ -166,7 +166,8 @@ def compact(bs: int, c: BlockSet, nz: torch.Tensor, n_zero: int, stream=None) ->
 
 
 def multiply_blocks(layout, a: BlockSet, b: BlockSet, stream=None,
-                    stats: MultiplyStats | None = None, events: dict | None = None) -> BlockSet:
+                    stats: MultiplyStats | None = None, events: dict | None = None,
+                    plan_filter=None) -> BlockSet:
     """Full regular product of two conformant block sets on their CUDA device.
 
     ``events`` (optional): CUDA events recorded on the stream around the phases, keys
@@ -187,6 +188,8 @@ def multiply_blocks(layout, a: BlockSet, b: BlockSet, stream=None,
     if events is not None:
         events["symbolic"].record(stream)
     plan = symbolic(layout, a, b, stream)
+    if plan_filter is not None:  # e.g. the approximate variant's pruned triples (approximate.py)
+        plan = plan_filter(plan)
     if stats is not None:
         stats.n_a, stats.n_b = a.n, b.n
         stats.n_c_symbolic, stats.n_triples = plan.n_c, plan.n_triples

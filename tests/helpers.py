@@ -94,3 +94,12 @@ def lookup(keys_all: np.ndarray, blocks_dev, want: np.ndarray):
     assert np.all(pos < keys_all.size) and np.array_equal(keys_all[pos], want), "missing C blocks"
     idx = torch.from_numpy(pos).to(blocks_dev.device)
     return blocks_dev.index_select(0, idx).cpu().numpy()
+
+
+def decay_sparse(n: int, seed: int, width=None, scale: float = 4.0) -> np.ndarray:
+    """Banded support with decaying magnitudes (pkg/tests/oracles.py:122-132 recipe)."""
+    rng = np.random.default_rng(seed)
+    width = width or max(4, n // 4)
+    i = np.arange(n)
+    dist = np.abs(i[:, None] - i[None, :])
+    return np.exp(-dist / scale) * (dist <= width) * rng.standard_normal((n, n))

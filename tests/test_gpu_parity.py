@@ -346,3 +346,46 @@ def test_multiply_variants_match_reference(ses, ci):
     assert c.symmetric == bool(g[f"c{ci}_symmetric"][0])
     assert helpers.rel(ses.to_dense(c), want) <= TOL
     assert helpers.rel(ses.to_dense(c), g[f"c{ci}_dense"]) <= TOL
+
+
+@pytest.mark.parametrize("ci", range(16))
+def test_approximate_multiply_matches_reference(ses, ci):
+    """Norm-pruned multiply (ops.py:197-204, tau/8 per level): same surviving C blocks and the same
+    prune log as the reference; the error is bounded by the log and the log by tau
+    (test_acceptance.py:278-300)."""
+    g = helpers.load("approximate")
+    tag = str(g["tags"][ci])
+    n, leaf, bs, scale, sa, sb, tau = g["cases"][ci]
+    n, leaf, bs, sa, sb = int(n), int(leaf), int(bs), int(sa), int(sb)
+    da, db = helpers.decay_sparse(n, sa, scale=scale), helpers.decay_sparse(n, sb, scale=scale)
+    if tag == "approximate":
+        c = ses.multiply(helpers.build(ses, da, leaf, bs), helpers.build(ses, db, leaf, bs),
+                         variant="approximate", tau=tau)
+        exact = da @ db
+    elif tag == "symmetric_square":
+        sym = np.triu(da + da.T)
+        r, cc = np.nonzero(sym)
+        a = ses.matrix_from_triplets(n, r, cc, sym[r, cc], leaf_dim=leaf, block_size=bs, symmetric=True)
+        c = ses.multiply(a, variant="symmetric_square", tau=tau)
+        exact = (da + da.T) @ (da + da.T)
+    else:
+        c = ses.multiply(helpers.build(ses, da, leaf, bs), variant="rank_k", tau=tau)
+        exact = da @ da.T
+    kc, bc, _ = _host(c)
+    np.testing.assert_array_equal(kc, g[f"c{ci}_keys"])
+    if kc.size:
+        assert helpers.rel(bc, g[f"c{ci}_blocks"]) <= TOL
+    log = np.sort(np.array(ses.last_engine.prune_log))
+    ref_log = g[f"c{ci}_log"]
+    assert log.size == ref_log.size
+    np.testing.assert_allclose(log, ref_log, rtol=1e-12)
+    skipped = float(np.sum(log))
+    diff = np.linalg.norm(ses.to_dense(c) - exact)
+    assert diff <= skipped + 1e-12 and skipped <= tau + 1e-12
+
+
+def test_approximate_with_zero_tau_is_the_exact_product(ses):
+    """test_ops.py:190-197: tau = 0 gives the exact product bit for bit."""
+    da = helpers.decay_sparse(64, 77, scale=2.0)
+    a = helpers.build(ses, da, 16, 8)
+    assert ses.canonical(ses.multiply(a, a, variant="approximate", tau=0.0)) == ses.canonical(ses.multiply(a, a))
