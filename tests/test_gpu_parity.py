@@ -198,8 +198,10 @@ def test_conformance_errors(ses):
         ses.multiply(a, c)
     with pytest.raises(ContractViolationError):
         ses.multiply(a)
+    with pytest.raises(ContractViolationError):
+        ses.multiply(a, variant="symmetric_square")  # needs a symmetric operand (ops.py:590-591)
     with pytest.raises(ConfigurationError):
-        ses.multiply(a, a, variant="approximate", tau=0.5)
+        ses.multiply(a, a, variant="approximate", tau=-1.0)
 
 
 def test_c2_131072_sampled_blocks_and_counts(ses):
