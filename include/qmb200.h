@@ -161,6 +161,19 @@ QM_API int qm_gather_blocks(int32_t block_size, const double *src, const int64_t
 QM_API int qm_transpose_blocks(int32_t block_size, const double *src, int64_t n, double *dst,
                                void *stream);
 
+/* ---- add / scale / add_scaled_identity (the step after a product) ---------- */
+/* out[m] = alpha*A[ia[m]] + beta*B[ib[m]] per block, an operand absent when its index is -1;
+ * exact IEEE products and sum (BlockSparseLeaf.add / scale, block_sparse.py:134-160). */
+QM_API int qm_axpby_blocks(int32_t block_size, int64_t n, const int64_t *ia, const int64_t *ib,
+                           double alpha, double beta, const double *a_blocks, const double *b_blocks,
+                           double *out, void *stream);
+/* Diagonal blocks of A + c*I with the reference's two leaf cases (ops.py:253-345): mode 0 =
+ * A_blk + c*eye, mode 1 = A_blk + identity-from-triplets (logical diagonal only); ia = -1 when the
+ * A block is absent, bi = block row. */
+QM_API int qm_add_identity_blocks(int32_t block_size, int64_t n, const int64_t *ia, const int64_t *bi,
+                                  const int8_t *mode, double c, int64_t n_logical,
+                                  const double *a_blocks, double *out, void *stream);
+
 /* ---- synthetic inputs (device side of the block-keyed generator) -------- */
 /* For each key, fills the block with numpy's default_rng([seed, matrix_id, bi, bj]).uniform(-1, 1,
  * (bs, bs)) -- bit-identical PCG64 + SeedSequence -- then zeroes entries outside the element

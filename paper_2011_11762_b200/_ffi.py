@@ -48,6 +48,8 @@ EXPORTS = (
     "qm_block_stats",
     "qm_gather_blocks",
     "qm_transpose_blocks",
+    "qm_axpby_blocks",
+    "qm_add_identity_blocks",
     "qm_generate_blocks",
     "qm_fp64_peak_kernel",
 )
@@ -99,6 +101,8 @@ _SIGS = {
     "qm_block_stats": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P]),
     "qm_gather_blocks": (ctypes.c_int, [_I32, _P, _P, _I64, _P, _P]),
     "qm_transpose_blocks": (ctypes.c_int, [_I32, _P, _I64, _P, _P]),
+    "qm_axpby_blocks": (ctypes.c_int, [_I32, _I64, _P, _P, ctypes.c_double, ctypes.c_double, _P, _P, _P, _P]),
+    "qm_add_identity_blocks": (ctypes.c_int, [_I32, _I64, _P, _P, _P, ctypes.c_double, _I64, _P, _P, _P]),
     "qm_generate_blocks": (ctypes.c_int, [_LP, _P, _I64, ctypes.c_uint64, ctypes.c_uint32, _I32,
                                           _I64, _P, _P, _P]),
     "qm_fp64_peak_kernel": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _I64, _P,

@@ -115,6 +115,54 @@ __global__ void __launch_bounds__(256) k_transpose_blocks(int bs, const double *
   }
 }
 
+// out[m] = alpha*A[ia[m]] + beta*B[ib[m]] with an operand absent when its index is -1 (then
+// alpha*A or beta*B alone). Exact IEEE products and sum (no FMA contraction), like numpy's
+// `alpha * a + beta * b` in BlockSparseLeaf.add / scale (block_sparse.py:134-160).
+__global__ void __launch_bounds__(256) k_axpby(int64_t elems, int64_t n, const int64_t *ia,
+                                               const int64_t *ib, double alpha, double beta,
+                                               const double *A, const double *B, double *out) {
+  for (int64_t m = blockIdx.x; m < n; m += gridDim.x) {
+    const int64_t x = ia[m], y = ib[m];
+    const double *a = x >= 0 ? A + (size_t)x * elems : nullptr;
+    const double *b = y >= 0 ? B + (size_t)y * elems : nullptr;
+    double *o = out + (size_t)m * elems;
+    for (int64_t e = threadIdx.x; e < elems; e += blockDim.x) {
+      double v;
+      if (a && b) v = __dadd_rn(__dmul_rn(alpha, a[e]), __dmul_rn(beta, b[e]));
+      else if (a) v = __dmul_rn(alpha, a[e]);
+      else v = __dmul_rn(beta, b[e]);
+      o[e] = v;
+    }
+  }
+}
+
+// Diagonal blocks of A + c*I (ops.py:253-345, block_sparse.py:162-175). mode[m]:
+//   0  leaf of A present and inside n_logical: A_blk + c*eye (c*eye alone when A_blk absent)
+//   1  partial / absent leaf: identity block from triplets (c on the logical diagonal, +0.0
+//      elsewhere), added as 1.0*A + 1.0*I when A_blk is present.
+__global__ void __launch_bounds__(256) k_add_identity(int bs, int64_t n, const int64_t *ia,
+                                                      const int64_t *bi, const int8_t *mode, double c,
+                                                      int64_t n_logical, const double *A, double *out) {
+  const int64_t elems = (int64_t)bs * bs;
+  for (int64_t m = blockIdx.x; m < n; m += gridDim.x) {
+    const double *a = ia[m] >= 0 ? A + (size_t)ia[m] * elems : nullptr;
+    double *o = out + (size_t)m * elems;
+    const int64_t row0 = bi[m] * bs;
+    for (int64_t e = threadIdx.x; e < elems; e += blockDim.x) {
+      const int r = (int)(e / bs), col = (int)(e % bs);
+      double v;
+      if (mode[m] == 0) {
+        const double ce = __dmul_rn(c, r == col ? 1.0 : 0.0);
+        v = a ? __dadd_rn(a[e], ce) : ce;
+      } else {
+        const double id = (r == col && row0 + r < n_logical) ? c : 0.0;
+        v = a ? __dadd_rn(__dmul_rn(1.0, a[e]), __dmul_rn(1.0, id)) : id;
+      }
+      o[e] = v;
+    }
+  }
+}
+
 size_t compact_cub_bytes(int64_t n) {
   size_t b = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t *)nullptr, (int64_t *)nullptr, n);
@@ -215,5 +263,35 @@ extern "C" int qm_transpose_blocks(int32_t block_size, const double *src, int64_
   int64_t grid = std::min<int64_t>(n * nt * nt, 148 * 16);
   k_transpose_blocks<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(block_size, src, n, dst);
   QM_LAUNCHED("k_transpose_blocks");
+  return QM_OK;
+}
+
+extern "C" int qm_axpby_blocks(int32_t block_size, int64_t n, const int64_t *ia, const int64_t *ib,
+                               double alpha, double beta, const double *a_blocks,
+                               const double *b_blocks, double *out, void *stream) {
+  if (block_size < 1 || n < 0) {
+    set_error("qm_axpby_blocks: bad arguments");
+    return QM_ERR_INVALID;
+  }
+  if (n == 0) return QM_OK;
+  int64_t grid = std::min<int64_t>(n, 148 * 16);
+  k_axpby<<<(int)grid, 256, 0, (cudaStream_t)stream>>>((int64_t)block_size * block_size, n, ia, ib, alpha,
+                                                       beta, a_blocks, b_blocks, out);
+  QM_LAUNCHED("k_axpby");
+  return QM_OK;
+}
+
+extern "C" int qm_add_identity_blocks(int32_t block_size, int64_t n, const int64_t *ia,
+                                      const int64_t *bi, const int8_t *mode, double c, int64_t n_logical,
+                                      const double *a_blocks, double *out, void *stream) {
+  if (block_size < 1 || n < 0) {
+    set_error("qm_add_identity_blocks: bad arguments");
+    return QM_ERR_INVALID;
+  }
+  if (n == 0) return QM_OK;
+  int64_t grid = std::min<int64_t>(n, 148 * 16);
+  k_add_identity<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(block_size, n, ia, bi, mode, c, n_logical,
+                                                              a_blocks, out);
+  QM_LAUNCHED("k_add_identity");
   return QM_OK;
 }

@@ -26,7 +26,12 @@ import torch
 from . import bridge, construct, spgemm
 from ._ffi import make_layout
 from .blocks import NIL, BlockSet, DeviceStore, QuadChunk
-from .errors import ConfigurationError, ContractViolationError, DimensionMismatchError
+from .errors import (
+    ConfigurationError,
+    ContractViolationError,
+    DeviceUnavailableError,
+    DimensionMismatchError,
+)
 from .layout import Geometry, LeafKind, MatrixParams, OwnerPolicy, TreeStats, resolve_leaf_kind
 
 _MODES = ("gpu", "simulate", "threaded")
@@ -80,6 +85,20 @@ class MultiplyVariant:
     @classmethod
     def approximate(cls, tau: float):
         return cls("approximate", tau)
+
+
+@dataclass(frozen=True)
+class TruncationSpec:
+    """ops.py:79-88."""
+
+    tau: float
+    mode: str = "global_frobenius"
+
+    def __post_init__(self):
+        if self.tau < 0:
+            raise ConfigurationError("truncation needs tau >= 0")
+        if self.mode != "global_frobenius":
+            raise ConfigurationError(f"unknown truncation mode {self.mode!r}")
 
 
 @dataclass
@@ -362,6 +381,69 @@ class MatrixSession:
         spec, upper = multiply_spec(a, b, variant)
         root = self.run_spec(spec)
         return Matrix(root, a.params, a.leaf_kind, a.block_size, upper)
+
+    def _wrap(self, bset, like: Matrix, symmetric=None) -> Matrix:
+        sym = like.symmetric if symmetric is None else symmetric
+        return Matrix(self.store.register(bset), like.params, like.leaf_kind, like.block_size, sym)
+
+    def _local_only(self, what: str):
+        if self.comm is not None:
+            raise ConfigurationError(f"{what} runs on one GPU; multi-GPU sessions only multiply")
+
+    def add(self, a: Matrix, b: Matrix, alpha: float = 1.0, beta: float = 1.0) -> Matrix:
+        """session.py:148-150 / ops.add_spec + _add_body/_add_fallback (ops.py:147-169)."""
+        from . import algebra  # noqa: PLC0415
+
+        _check_conformant(a, b)
+        if a.symmetric != b.symmetric:
+            raise ContractViolationError("add needs both operands general or both symmetric")
+        self._local_only("add")
+        a_nil = a.root.is_nil or a.root.n_blocks == 0
+        b_nil = b.root.is_nil or b.root.n_blocks == 0
+        if a_nil and b_nil:
+            return Matrix(NIL, a.params, a.leaf_kind, a.block_size, a.symmetric)
+        if a_nil or b_nil:  # _add_fallback: the survivor, scaled by its coefficient
+            survivor, coeff = (b, beta) if a_nil else (a, alpha)
+            return self.scale(survivor, coeff)
+        return self._wrap(algebra.add(a.geometry, a.root.require(), b.root.require(), float(alpha),
+                                      float(beta)), a)
+
+    def scale(self, a: Matrix, alpha: float) -> Matrix:
+        """session.py:152-154 / _scale_body (ops.py:172-185): 1.0 shares the chunk, 0.0 is nil."""
+        from . import algebra  # noqa: PLC0415
+
+        if alpha == 1.0:
+            return a
+        if alpha == 0.0 or a.root.is_nil or a.root.n_blocks == 0:
+            return Matrix(NIL, a.params, a.leaf_kind, a.block_size, a.symmetric)
+        self._local_only("scale")
+        return self._wrap(algebra.scale(a.geometry, a.root.require(), float(alpha)), a)
+
+    def add_scaled_identity(self, a: Matrix, c: float) -> Matrix:
+        """session.py:156-158 / ops.py:253-345: A + c*I on the logical diagonal."""
+        from . import algebra  # noqa: PLC0415
+
+        if c == 0.0:
+            return a
+        self._local_only("add_scaled_identity")
+        if self.device.type != "cuda":
+            raise DeviceUnavailableError("add_scaled_identity runs on the CUDA path")
+        base = None if (a.root.is_nil or a.root.n_blocks == 0) else a.root.require()
+        return self._wrap(algebra.add_scaled_identity(a.geometry, base, float(c), self.device), a)
+
+    def truncate(self, a: Matrix, spec) -> tuple[Matrix, float]:
+        """session.py:173-185: global Frobenius truncation; returns (matrix, removed norm)."""
+        from . import algebra  # noqa: PLC0415
+
+        if not isinstance(spec, TruncationSpec):
+            spec = TruncationSpec(float(spec))
+        if a.root.is_nil or a.root.n_blocks == 0 or spec.tau == 0.0:
+            return a, 0.0
+        self._local_only("truncate")
+        out, removed = algebra.truncate(a.geometry, a.root.require(), spec.tau, a.symmetric)
+        if out is a.root.blockset:
+            return a, 0.0
+        return self._wrap(out, a), removed
 
     # -- inspection -----------------------------------------------------------------------------
 

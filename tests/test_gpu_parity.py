@@ -391,3 +391,48 @@ def test_approximate_with_zero_tau_is_the_exact_product(ses):
     da = helpers.decay_sparse(64, 77, scale=2.0)
     a = helpers.build(ses, da, 16, 8)
     assert ses.canonical(ses.multiply(a, a, variant="approximate", tau=0.0)) == ses.canonical(ses.multiply(a, a))
+
+
+@pytest.mark.parametrize("ci", range(15))
+def test_add_scale_identity_truncate_match_reference(ses, ci):
+    """SURVEY 8(f) #3 on the device: add / scale / add_scaled_identity are bit-identical to the
+    reference (canonical bytes); truncation drops the same blocks and removes the same norm."""
+    g = helpers.load("algebra")
+    op = str(g["ops"][ci])
+    n, leaf, bs, seed, p1, p2 = g["cases"][ci]
+    n, leaf, bs, seed = int(n), int(leaf), int(bs), int(seed)
+    da, db = helpers.random_sparse(n, 0.2, seed), helpers.random_sparse(n, 0.25, seed + 1000)
+    a, b = helpers.build(ses, da, leaf, bs), helpers.build(ses, db, leaf, bs)
+    removed = 0.0
+    if op == "add":
+        c = ses.add(a, b, p1, p2)
+    elif op == "cancel":
+        c = ses.add(a, a, p1, p2)
+    elif op == "scale":
+        c = ses.scale(a, p1)
+    elif op == "asi":
+        c = ses.add_scaled_identity(a, p1)
+    elif op == "asi_nil":
+        c = ses.add_scaled_identity(ses.zeros(n, leaf_dim=leaf, block_size=bs), p1)
+    elif op == "truncate":
+        c, removed = ses.truncate(a, p1 * np.linalg.norm(da))
+    else:
+        sym = np.triu(da + da.T)
+        r, cc = np.nonzero(sym)
+        s_ = ses.matrix_from_triplets(n, r, cc, sym[r, cc], leaf_dim=leaf, block_size=bs, symmetric=True)
+        c, removed = ses.truncate(s_, p1 * np.linalg.norm(da + da.T))
+    assert c.root.is_nil == bool(g[f"c{ci}_nil"][0])
+    assert helpers.sha(ses.canonical(c)) == bytes(g[f"c{ci}_sha"])
+    np.testing.assert_array_equal(ses.to_dense(c), g[f"c{ci}_dense"])
+    assert abs(removed - g[f"c{ci}_removed"][0]) <= 1e-12 * max(1.0, removed)
+
+
+def test_add_nil_fallbacks_share_the_survivor(ses):
+    """test_ops.py:41-52: adding nil returns the surviving chunk itself when its coefficient is 1."""
+    a = helpers.build(ses, helpers.random_sparse(16, 0.4, 3), 4, 2)
+    z = ses.zeros(16, leaf_dim=4, block_size=2)
+    assert ses.add(a, z).root == a.root
+    np.testing.assert_allclose(ses.to_dense(ses.add(z, a, alpha=1.0, beta=2.0)), 2.0 * ses.to_dense(a), atol=1e-15)
+    assert ses.add(z, z).root.is_nil
+    assert ses.scale(a, 1.0).root == a.root and ses.scale(a, 0.0).root.is_nil
+    assert ses.add_scaled_identity(a, 0.0).root == a.root
