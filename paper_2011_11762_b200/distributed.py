@@ -225,8 +225,8 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     t3 = clock()
     if hi == lo:
         return empty, stats
-    la = torch.searchsorted(need_a, tri[:, 0])
-    lb = torch.searchsorted(need_b, tri[:, 1])
+    la = torch.searchsorted(need_a, tri[:, 0].contiguous())
+    lb = torch.searchsorted(need_b, tri[:, 1].contiguous())
     tri_local = torch.stack([la, lb], dim=1).to(torch.int32).reshape(-1).contiguous()
     c_tptr_local = (c_tptr[m0:m1 + 1] - lo).contiguous()
     c_keys_local = c_keys[m0:m1].contiguous()
