@@ -99,7 +99,7 @@ struct TmaCfg {
   static constexpr int A_BYTES = KSP * A_SP_BYTES;
   static constexpr int B_BYTES = NSP * B_SP_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 2 * STAGES * 8 + 2 * 32 * 8;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 3 * STAGES * 8 + 2 * 32 * 8;
   static_assert(KP % 16 == 0 && BS % KP == 0 && TILE % 16 == 0 && BS % TILE == 0, "panels");
   static_assert(TM % 8 == 0 && TN % 8 == 0, "warp tile");
   static_assert(A_SP_BYTES % 1024 == 0 && B_SP_BYTES % 1024 == 0, "swizzle-128B atoms need 1 KB alignment");
@@ -124,11 +124,17 @@ __device__ __forceinline__ void cur_start(Cur &c, int64_t unit, int64_t nU, cons
   }
 }
 
+// Advances the producer's cursor; a finished unit is replaced by `next` (fetched ahead from the
+// global work counter) and a new `next` is claimed.
 template <class Cfg>
-__device__ __forceinline__ void cur_next(Cur &c, int64_t nU, const int64_t *tptr) {
+__device__ __forceinline__ void cur_next(Cur &c, int64_t nU, const int64_t *tptr, int64_t &next,
+                                         unsigned long long *counter) {
   if (++c.p == Cfg::NP) {
     c.p = 0;
-    if (++c.t == c.tend) cur_start<Cfg>(c, c.unit + gridDim.x, nU, tptr);
+    if (++c.t == c.tend) {
+      cur_start<Cfg>(c, next, nU, tptr);
+      if (next < nU) next = (int64_t)gridDim.x + (int64_t)atomicAdd(counter, 1ull);
+    }
   }
 }
 
@@ -138,7 +144,8 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
                   const uint2 *__restrict__ tri, const int64_t *__restrict__ tptr, int64_t nC,
                   double *__restrict__ C, double *__restrict__ csq, uint8_t *__restrict__ cnz,
                   int64_t *__restrict__ zero_count, double *__restrict__ part_sq,
-                  uint8_t *__restrict__ part_nz, uint64_t zmask) {
+                  uint8_t *__restrict__ part_nz, unsigned long long *__restrict__ counter,
+                  uint64_t zmask) {
   constexpr int BS = Cfg::BS, MT = Cfg::MT, NT = Cfg::NT, STAGES = Cfg::STAGES;
   const int64_t nU = nC * Cfg::NQ;
   // Align to 1 KB (SWIZZLE_128B atoms) by offsetting the __shared__ array itself: the pointer keeps
@@ -148,7 +155,8 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t *full = (uint64_t *)(smem + (size_t)STAGES * Cfg::STAGE_BYTES);
   uint64_t *empty = full + STAGES;
-  double *red = (double *)(empty + STAGES);  // [32] sums, [32] nonzero flags
+  volatile int64_t *meta = (volatile int64_t *)(empty + STAGES);  // per stage: unit*2 + last, -1 = end
+  double *red = (double *)(empty + 2 * STAGES);  // [32] sums, [32] nonzero flags
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -165,16 +173,26 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
+      // Dynamic work distribution: the first unit is blockIdx.x, later ones come from a global
+      // counter in key order (so concurrently running CTAs still share A/B rows/columns in L2)
+      // and no CTA is left with a long tail of heavy units.
       Cur L;
       cur_start<Cfg>(L, blockIdx.x, nU, tptr);
+      int64_t next = (int64_t)gridDim.x + (int64_t)atomicAdd(counter, 1ull);
       int s = 0;
       uint32_t phase = 0;
-      while (L.unit < nU) {
+      while (true) {
         mbar_wait(&empty[s], phase ^ 1u);
+        if (L.unit >= nU) {
+          meta[s] = -1;
+          mbar_arrive(&full[s]);  // tx-free completion: tells the consumers to stop
+          break;
+        }
         const uint2 ab = tri[L.t];
         const int qt = (int)(L.unit % Cfg::NQ);
         const int row0 = (qt / Cfg::NQN) * Cfg::TILE, col0 = (qt % Cfg::NQN) * Cfg::TILE;
         uint8_t *st = smem + (size_t)s * Cfg::STAGE_BYTES;
+        meta[s] = L.unit * 2 + ((L.p == Cfg::NP - 1 && L.t + 1 == L.tend) ? 1 : 0);
         mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
 #pragma unroll
         for (int q = 0; q < Cfg::KSP; ++q)
@@ -184,7 +202,7 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
         for (int q = 0; q < Cfg::NSP; ++q)
           tma_load_2d(st + Cfg::A_BYTES + q * Cfg::B_SP_BYTES, &tmB, col0 + q * 16,
                       (int)(ab.y * BS + L.p * Cfg::KP), &full[s]);
-        cur_next<Cfg>(L, nU, tptr);
+        cur_next<Cfg>(L, nU, tptr, next, counter);
         if (++s == STAGES) {
           s = 0;
           phase ^= 1u;
@@ -217,12 +235,12 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  Cur Cc;
-  cur_start<Cfg>(Cc, blockIdx.x, nU, tptr);
   int s = 0;
   uint32_t phase = 0;
-  while (Cc.unit < nU) {
+  while (true) {
     mbar_wait(&full[s], phase);
+    const int64_t mt = meta[s];
+    if (mt < 0) break;
     const uint8_t *sa = smem + (size_t)s * Cfg::STAGE_BYTES;
     const uint8_t *sb = sa + Cfg::A_BYTES;
 #pragma unroll
@@ -262,9 +280,10 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
       phase ^= 1u;
     }
 
-    if (Cc.p == Cfg::NP - 1 && Cc.t + 1 == Cc.tend) {
-      const int64_t m = Cc.unit / Cfg::NQ;
-      const int qt = (int)(Cc.unit % Cfg::NQ);
+    if (mt & 1) {
+      const int64_t unit = mt >> 1;
+      const int64_t m = unit / Cfg::NQ;
+      const int qt = (int)(unit % Cfg::NQ);
       double *cb = C + (size_t)m * (BS * BS) + (size_t)(qt / Cfg::NQN) * Cfg::TILE * BS +
                    (qt % Cfg::NQN) * Cfg::TILE;
       double ss = 0.0;
@@ -301,13 +320,12 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
           cnz[m] = anynz != 0.0;
           if (anynz == 0.0 && zero_count) atomicAdd((unsigned long long *)zero_count, 1ull);
         } else {
-          part_sq[Cc.unit] = tot;
-          part_nz[Cc.unit] = anynz != 0.0;
+          part_sq[unit] = tot;
+          part_nz[unit] = anynz != 0.0;
         }
       }
       asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::NCW * 32) : "memory");
     }
-    cur_next<Cfg>(Cc, nU, tptr);
   }
 }
 
@@ -372,9 +390,10 @@ int sm_count_tma() {
   return n;
 }
 
+// Workspace: the work counter (256 B), then the per-tile partial norms for NQ > 1.
 template <class Cfg>
 size_t tma_ws_bytes(int64_t nC) {
-  return Cfg::NQ == 1 ? 0 : (size_t)nC * Cfg::NQ * (sizeof(double) + sizeof(uint8_t)) + 256;
+  return 256 + (Cfg::NQ == 1 ? 0 : (size_t)nC * Cfg::NQ * (sizeof(double) + sizeof(uint8_t)) + 256);
 }
 
 template <class Cfg>
@@ -383,14 +402,16 @@ int launch_tma(const double *A, int64_t nA, const double *B, int64_t nB, const u
                void *ws, size_t ws_bytes, cudaStream_t st) {
   double *part_sq = nullptr;
   uint8_t *part_nz = nullptr;
+  if (!ws || ws_bytes < tma_ws_bytes<Cfg>(nC)) {
+    set_error("qm_numeric: workspace %zu < required %zu", ws_bytes, tma_ws_bytes<Cfg>(nC));
+    return QM_ERR_WORKSPACE;
+  }
+  unsigned long long *counter = (unsigned long long *)ws;
   if (Cfg::NQ > 1) {
-    if (!ws || ws_bytes < tma_ws_bytes<Cfg>(nC)) {
-      set_error("qm_numeric: workspace %zu < required %zu", ws_bytes, tma_ws_bytes<Cfg>(nC));
-      return QM_ERR_WORKSPACE;
-    }
-    part_sq = (double *)ws;
+    part_sq = (double *)((char *)ws + 256);
     part_nz = (uint8_t *)(part_sq + nC * Cfg::NQ);
   }
+  QM_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
   CUtensorMap ma, mb;
   int rc = make_map(&ma, A, nA, Cfg::BS, Cfg::TILE);
   if (rc != QM_OK) return rc;
@@ -409,7 +430,7 @@ int launch_tma(const double *A, int64_t nA, const double *B, int64_t nB, const u
   int64_t grid = (int64_t)sm_count_tma() * per_sm;
   if (grid > nU) grid = nU;
   k_numeric_tma<Cfg><<<(int)grid, Cfg::NTHR, Cfg::SMEM, st>>>(ma, mb, tri, tptr, nC, C, csq, cnz, zc,
-                                                              part_sq, part_nz, /*zmask=*/0ull);
+                                                              part_sq, part_nz, counter, /*zmask=*/0ull);
   QM_LAUNCHED("k_numeric_tma");
   if (Cfg::NQ > 1) {
     int64_t g = std::min<int64_t>((nC + 255) / 256, (int64_t)sm_count_tma() * 8);
