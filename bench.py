@@ -371,6 +371,8 @@ def run_ours(args):
                                     "(structure gather + symbolic + exchange + numeric)")
     if not args.no_e2e and world == 1:
         line["e2e"] = run_e2e(args, torch, ses, geom, a, b, dev, world, dist)
+    elif not args.no_e2e:
+        line["e2e"] = run_e2e_distributed(args, torch, geom, a, b, dev, world, dist)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args.config, args.cpu_target_s)
     if rank == 0:
@@ -467,6 +469,47 @@ def run_e2e(args, torch, ses, geom, a, b, dev, world, dist):
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps,
             "ms_per_step": round(ms / steps, 3), "api": "MatrixSession.multiply",
             "pipelining": "H2D(k+1) | product(k) | D2H(k) on separate streams, double-buffered inputs"}
+
+
+def run_e2e_distributed(args, torch, geom, a, b, dev, world, dist):
+    """N > 1: MatrixSession(n_workers=N).multiply on each rank's host-resident key range of A and
+    B (pinned H2D inside the timed region), the distributed product, D2H of the rank's C range."""
+    from paper_2011_11762_b200 import MatrixSession
+    from paper_2011_11762_b200.blocks import BlockSet
+
+    ses = MatrixSession(n_workers=world, device=dev)
+    pin = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t)  # noqa: E731
+    ha = [pin(t) for t in (a.keys, a.blocks, a.sumsq)]
+    hb = [pin(t) for t in (b.keys, b.blocks, b.sumsq)]
+    h2d = sum(t.numel() * t.element_size() for t in ha + hb)
+
+    def step():
+        da = BlockSet(*[t.to(dev, non_blocking=True) for t in ha])
+        db = BlockSet(*[t.to(dev, non_blocking=True) for t in hb])
+        c = ses.multiply(ses.matrix_from_blockset(geom, da), ses.matrix_from_blockset(geom, db))
+        cs = c.root.blockset if not c.root.is_nil else BlockSet.empty(geom.bs, dev)
+        outs = [t.to("cpu", non_blocking=True) for t in (cs.keys, cs.blocks, cs.sumsq)]
+        return sum(t.numel() * t.element_size() for t in outs)
+
+    steps = max(1, min(args.steps, 3))
+    step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    d2h = 0
+    for _ in range(steps):
+        d2h = step()
+    e.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([s.elapsed_time(e)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    flops = ses.last_multiply.flops
+    return {"value": round(flops * steps / (ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "ms_per_step": round(ms / steps, 3), "api": "MatrixSession(n_workers=N).multiply",
+            "note": "per-rank bytes (rank 0); each rank copies its own key range in and its C range out"}
 
 
 # ---------------------------------------------------------------------------------------------
