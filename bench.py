@@ -215,10 +215,16 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    backend = os.environ.get("QM_DIST_BACKEND", "nccl")  # gloo: host-staged (tests, 1 GPU)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    cdev = dev if backend == "nccl" else torch.device("cpu")  # where timing collectives run
     lib = _ffi.load()
     base = G.CONFIGS[args.config]
     scaling = args.scaling or ("strong" if base.name.startswith("C5") or base.kind != "banded" else "weak")
@@ -301,7 +307,7 @@ def run_ours(args):
     numeric_ms = [e["numeric"].elapsed_time(e["end"]) for e in evs]
     symbolic_ms = [e["symbolic"].elapsed_time(e["numeric"]) for e in evs]
     if world > 1:
-        t = torch.tensor([total_ms], device=dev)
+        t = torch.tensor([total_ms], device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     flops = stats.flops
@@ -357,7 +363,7 @@ def run_ours(args):
     if world > 1:
         ds = dist_stats["last"]
         v = torch.tensor([ds.bytes_received, ds.t_range[1] - ds.t_range[0], ds.n_c_local],
-                         dtype=torch.float64, device=dev)
+                         dtype=torch.float64, device=cdev)
         allv = [torch.zeros_like(v) for _ in range(world)]
         dist.all_gather(allv, v)
         m = torch.stack(allv).cpu().numpy()
@@ -372,7 +378,7 @@ def run_ours(args):
     if not args.no_e2e and world == 1:
         line["e2e"] = run_e2e(args, torch, ses, geom, a, b, dev, world, dist)
     elif not args.no_e2e:
-        line["e2e"] = run_e2e_distributed(args, torch, geom, a, b, dev, world, dist)
+        line["e2e"] = run_e2e_distributed(args, torch, geom, a, b, dev, world, dist, cdev)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args.config, args.cpu_target_s)
     if rank == 0:
@@ -471,7 +477,7 @@ def run_e2e(args, torch, ses, geom, a, b, dev, world, dist):
             "pipelining": "H2D(k+1) | product(k) | D2H(k) on separate streams, double-buffered inputs"}
 
 
-def run_e2e_distributed(args, torch, geom, a, b, dev, world, dist):
+def run_e2e_distributed(args, torch, geom, a, b, dev, world, dist, cdev):
     """N > 1: MatrixSession(n_workers=N).multiply on each rank's host-resident key range of A and
     B (pinned H2D inside the timed region), the distributed product, D2H of the rank's C range."""
     from paper_2011_11762_b200 import MatrixSession
@@ -502,7 +508,7 @@ def run_e2e_distributed(args, torch, geom, a, b, dev, world, dist):
         d2h = step()
     e.record()
     torch.cuda.synchronize()
-    t = torch.tensor([s.elapsed_time(e)], device=dev)
+    t = torch.tensor([s.elapsed_time(e)], device=cdev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     flops = ses.last_multiply.flops

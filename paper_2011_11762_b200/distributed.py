@@ -48,9 +48,20 @@ class Comm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        # gloo moves host memory only: device tensors are staged through the host (tests run the
+        # CUDA backend with several ranks on one GPU this way, with no cross-rank GPU waits)
+        self.stage = dist.get_backend(group) == "gloo"
+
+    def _in(self, t: torch.Tensor) -> torch.Tensor:
+        return t.cpu() if self.stage else t
+
+    def _out(self, t: torch.Tensor, device) -> torch.Tensor:
+        return t.to(device) if self.stage else t
 
     def allgather_varlen(self, t: torch.Tensor) -> tuple[torch.Tensor, list[int]]:
         """Concatenation over ranks (rank order) of 1-D tensors of different lengths."""
+        dev = t.device
+        t = self._in(t)
         n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
         ns = [torch.zeros_like(n) for _ in range(self.world)]
         self.dist.all_gather(ns, n, group=self.group)
@@ -60,11 +71,13 @@ class Comm:
         pad[: t.shape[0]] = t
         outs = [torch.empty_like(pad) for _ in range(self.world)]
         self.dist.all_gather(outs, pad, group=self.group)
-        return torch.cat([o[:c] for o, c in zip(outs, counts)]), counts
+        return self._out(torch.cat([o[:c] for o, c in zip(outs, counts)]), dev), counts
 
     def alltoallv(self, send: torch.Tensor, send_counts: list[int]) -> tuple[torch.Tensor, list[int]]:
         """Rows send[sum(send_counts[:d]) : ...] go to rank d; returns received rows (source rank
         order) and the per-source counts."""
+        dev0 = send.device
+        send = self._in(send)
         dev = send.device
         sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
         rc = torch.empty_like(sc)
@@ -73,10 +86,10 @@ class Comm:
         flat = send.reshape(send.shape[0], -1) if send.dim() > 1 else send.reshape(-1, 1)
         out = torch.empty((sum(recv_counts), flat.shape[1]), dtype=send.dtype, device=dev)
         self.dist.all_to_all_single(out, flat.contiguous(), recv_counts, send_counts, group=self.group)
-        return out.reshape((out.shape[0],) + tuple(send.shape[1:])), recv_counts
+        return self._out(out.reshape((out.shape[0],) + tuple(send.shape[1:])), dev0), recv_counts
 
     def allreduce_max(self, x: float, device) -> float:
-        t = torch.tensor([x], dtype=torch.float64, device=device)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if self.stage else device)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return float(t.item())
 

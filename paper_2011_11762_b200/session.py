@@ -280,7 +280,7 @@ class MatrixSession:
         stats.n_triples = ds.n_triples_global
         stats.flops = 2 * layout.block_size ** 3 * ds.n_triples_global
         mine = torch.tensor([ds.t_range[1] - ds.t_range[0], ds.bytes_received], dtype=torch.int64,
-                            device=a.device)
+                            device="cpu" if self.comm.stage else a.device)
         allv = [torch.zeros_like(mine) for _ in range(self.comm.world)]
         self.comm.dist.all_gather(allv, mine)
         self.last_stats = [WorkerStats(r, tasks_executed=int(v[0]), bytes_received=int(v[1]))
