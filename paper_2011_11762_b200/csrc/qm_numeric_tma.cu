@@ -156,7 +156,6 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
   uint64_t *full = (uint64_t *)(smem + (size_t)STAGES * Cfg::STAGE_BYTES);
   uint64_t *empty = full + STAGES;
   volatile int64_t *meta = (volatile int64_t *)(empty + STAGES);  // per stage: unit*2 + last, -1 = end
-  double *red = (double *)(empty + 2 * STAGES);  // [32] sums, [32] nonzero flags
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -286,7 +285,10 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
       const int qt = (int)(unit % Cfg::NQ);
       double *cb = C + (size_t)m * (BS * BS) + (size_t)(qt / Cfg::NQN) * Cfg::TILE * BS +
                    (qt % Cfg::NQN) * Cfg::TILE;
-      double ss = 0.0;
+      // Barrier-free epilogue: each warp stores its tile fragment and writes its partial squared
+      // norm / nonzero flag for the unit; k_combine_tiles sums the NQ*NCW partials of a block in a
+      // fixed order afterwards (deterministic, no named barrier between the consumer warps).
+      double ss0 = 0.0, ss1 = 0.0;
       bool nz = false;
 #pragma unroll
       for (int i = 0; i < MT; ++i)
@@ -295,36 +297,19 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
           const double v0 = acc[i][n][0], v1 = acc[i][n][1];
           *reinterpret_cast<double2 *>(cb + (size_t)(wm0 + i * 8 + g) * BS + wn0 + n * 8 + 2 * tq) =
               make_double2(v0, v1);
-          ss = fma(v0, v0, ss);
-          ss = fma(v1, v1, ss);
+          ss0 = fma(v0, v0, ss0);
+          ss1 = fma(v1, v1, ss1);
           nz |= (v0 != 0.0) | (v1 != 0.0);
           acc[i][n][0] = acc[i][n][1] = 0.0;
         }
+      double ss = ss0 + ss1;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
       const bool wnz = __any_sync(0xffffffffu, nz);
       if (lane == 0) {
-        red[warp] = ss;
-        red[32 + warp] = wnz ? 1.0 : 0.0;
+        part_sq[unit * Cfg::NCW + warp] = ss;
+        part_nz[unit * Cfg::NCW + warp] = wnz;
       }
-      asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::NCW * 32) : "memory");
-      if (threadIdx.x == 0) {
-        double tot = 0.0, anynz = 0.0;
-#pragma unroll
-        for (int w = 0; w < Cfg::NCW; ++w) {
-          tot += red[w];
-          anynz += red[32 + w];
-        }
-        if (Cfg::NQ == 1) {
-          csq[m] = tot;
-          cnz[m] = anynz != 0.0;
-          if (anynz == 0.0 && zero_count) atomicAdd((unsigned long long *)zero_count, 1ull);
-        } else {
-          part_sq[unit] = tot;
-          part_nz[unit] = anynz != 0.0;
-        }
-      }
-      asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::NCW * 32) : "memory");
     }
   }
 }
@@ -390,10 +375,10 @@ int sm_count_tma() {
   return n;
 }
 
-// Workspace: the work counter (256 B), then the per-tile partial norms for NQ > 1.
+// Workspace: the work counter (256 B), then per-warp partial norms / nonzero flags of every tile.
 template <class Cfg>
 size_t tma_ws_bytes(int64_t nC) {
-  return 256 + (Cfg::NQ == 1 ? 0 : (size_t)nC * Cfg::NQ * (sizeof(double) + sizeof(uint8_t)) + 256);
+  return 256 + (size_t)nC * Cfg::NQ * Cfg::NCW * (sizeof(double) + sizeof(uint8_t)) + 256;
 }
 
 template <class Cfg>
@@ -407,10 +392,8 @@ int launch_tma(const double *A, int64_t nA, const double *B, int64_t nB, const u
     return QM_ERR_WORKSPACE;
   }
   unsigned long long *counter = (unsigned long long *)ws;
-  if (Cfg::NQ > 1) {
-    part_sq = (double *)((char *)ws + 256);
-    part_nz = (uint8_t *)(part_sq + nC * Cfg::NQ);
-  }
+  part_sq = (double *)((char *)ws + 256);
+  part_nz = (uint8_t *)(part_sq + nC * Cfg::NQ * Cfg::NCW);
   QM_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
   CUtensorMap ma, mb;
   int rc = make_map(&ma, A, nA, Cfg::BS, Cfg::TILE);
@@ -432,10 +415,10 @@ int launch_tma(const double *A, int64_t nA, const double *B, int64_t nB, const u
   k_numeric_tma<Cfg><<<(int)grid, Cfg::NTHR, Cfg::SMEM, st>>>(ma, mb, tri, tptr, nC, C, csq, cnz, zc,
                                                               part_sq, part_nz, counter, /*zmask=*/0ull);
   QM_LAUNCHED("k_numeric_tma");
-  if (Cfg::NQ > 1) {
+  {
     int64_t g = std::min<int64_t>((nC + 255) / 256, (int64_t)sm_count_tma() * 8);
-    k_combine_tiles<<<(int)std::max<int64_t>(g, 1), 256, 0, st>>>(part_sq, part_nz, Cfg::NQ, nC, csq,
-                                                                   cnz, zc);
+    k_combine_tiles<<<(int)std::max<int64_t>(g, 1), 256, 0, st>>>(part_sq, part_nz, Cfg::NQ * Cfg::NCW,
+                                                                   nC, csq, cnz, zc);
     QM_LAUNCHED("k_combine_tiles");
   }
   return QM_OK;
@@ -445,7 +428,7 @@ int launch_tma(const double *A, int64_t nA, const double *B, int64_t nB, const u
 using Tma32 = TmaCfg<32, 32, 1, 2, 32, 3, 4>;
 using Tma64 = TmaCfg<64, 64, 2, 2, 32, 3, 2>;
 using Tma128 = TmaCfg<128, 64, 2, 2, 32, 3, 2>;
-using Tma64x1 = TmaCfg<64, 64, 2, 2, 32, 6, 1>;  // diagnostic variant: 1 CTA/SM, 6 stages
+using Tma64x1 = TmaCfg<64, 64, 2, 2, 16, 6, 2>;  // QM_TMA_VARIANT=1: 16-deep panels, 6 stages (slower)
 
 int tma_variant() {
   const char *e = getenv("QM_TMA_VARIANT");
