@@ -111,6 +111,26 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def bind_to_gpu_numa(index: int):
+    """Restricts this process to the CPUs local to GPU `index` (NVML CPU affinity), so pinned host
+    buffers are first-touched on the GPU's NUMA node. Returns the previous affinity (or None)."""
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, 16)
+        cpus = {w * 64 + b for w, word in enumerate(words) for b in range(64) if (word >> b) & 1}
+        prev = os.sched_getaffinity(0)
+        cpus &= prev
+        if cpus and cpus != prev:
+            os.sched_setaffinity(0, cpus)
+            return prev
+    except Exception:  # noqa: BLE001 -- best effort (no NVML, containers without affinity rights)
+        return None
+    return None
+
+
 # ---------------------------------------------------------------------------------------------
 # CPU side: oracle port on a bounded sample
 # ---------------------------------------------------------------------------------------------
@@ -216,6 +236,7 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     local = local % torch.cuda.device_count()
+    prev_affinity = bind_to_gpu_numa(local)  # before any pinned allocation (e2e host buffers)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     backend = os.environ.get("QM_DIST_BACKEND", "nccl")  # gloo: host-staged (tests, 1 GPU)
@@ -379,6 +400,9 @@ def run_ours(args):
         line["e2e"] = run_e2e(args, torch, ses, geom, a, b, dev, world, dist)
     elif not args.no_e2e:
         line["e2e"] = run_e2e_distributed(args, torch, geom, a, b, dev, world, dist, cdev)
+    if prev_affinity is not None:
+        line.setdefault("e2e", {})["numa_bound"] = True
+        os.sched_setaffinity(0, prev_affinity)  # the CPU baseline uses every host core
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args.config, args.cpu_target_s)
     if rank == 0:

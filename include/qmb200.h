@@ -72,6 +72,12 @@ QM_API const char *qm_last_error(void);
 /* Number of kernels this library has launched in this process (relaxed counter; for bench). */
 QM_API uint64_t qm_launch_count(void);
 
+/* Reads n (1..8) int64 values from device memory to host memory through a mapped pinned buffer
+ * written by a kernel on `stream` (no copy engine, so it never queues behind large in-flight
+ * copies), then synchronises `stream`. Used for the small counts the host needs. */
+QM_API int qm_read_i64(const int64_t *dev_src /*device*/, int32_t n, int64_t *host_out /*host*/,
+                       void *stream);
+
 /* ---- quadtree keys ---------------------------------------------------------------------------- */
 /* Replaces the quadrant recursion of build_from_triplets (quadtree.py:112-142) for block placement:
  * keys[i] = qkey(bi[i], bj[i]) on the device. */

@@ -29,6 +29,7 @@ EXPORTS = (
     "qm_abi_version",
     "qm_last_error",
     "qm_launch_count",
+    "qm_read_i64",
     "qm_encode_keys",
     "qm_decode_keys",
     "qm_build_workspace_bytes",
@@ -79,6 +80,7 @@ _SIGS = {
     "qm_abi_version": (ctypes.c_int, []),
     "qm_last_error": (ctypes.c_char_p, []),
     "qm_launch_count": (ctypes.c_uint64, []),
+    "qm_read_i64": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_I64), _P]),
     "qm_encode_keys": (ctypes.c_int, [_LP, _P, _P, _I64, _P, _P]),
     "qm_decode_keys": (ctypes.c_int, [_LP, _P, _I64, _P, _P, _P]),
     "qm_build_workspace_bytes": (_SZ, [_LP, _I64]),
@@ -160,3 +162,13 @@ def ptr(t) -> int:
 
 def stream_handle(stream) -> int:
     return 0 if stream is None else int(stream.cuda_stream)
+
+
+def read_i64(t, stream=None) -> int:
+    """One int64 device value to the host without a copy engine (qm_read_i64)."""
+    import torch  # noqa: PLC0415
+
+    out = ctypes.c_int64(0)
+    st = stream if stream is not None else torch.cuda.current_stream(t.device)
+    check(load().qm_read_i64(ptr(t), 1, ctypes.byref(out), stream_handle(st)), "qm_read_i64")
+    return int(out.value)

@@ -37,7 +37,7 @@ def _drop_zero_blocks(bs: int, c: BlockSet) -> BlockSet:
     nz = torch.empty(c.n, dtype=torch.uint8, device=c.device)
     _ffi.check(lib.qm_block_stats(bs, c.n, _ffi.ptr(c.blocks), _ffi.ptr(c.sumsq), _ffi.ptr(nz),
                                   _stream(c.device)), "qm_block_stats")
-    n_zero = int(c.n - int(nz.sum().item()))
+    n_zero = _ffi.read_i64((nz == 0).sum().reshape(1).to(torch.int64))
     return compact(bs, c, nz, n_zero)
 
 

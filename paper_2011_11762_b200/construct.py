@@ -148,8 +148,7 @@ def blocks_from_triplets_device(geom: Geometry, rows, cols, vals, device, stream
         _ffi.check(lib.qm_build_fill(lp, _ffi.ptr(v), n, _ffi.ptr(ws), wb, nblk, _ffi.ptr(out.keys),
                                      _ffi.ptr(out.blocks), _ffi.ptr(out.sumsq), _ffi.ptr(nz),
                                      _ffi.ptr(zc), sh), "qm_build_fill")
-        st.synchronize()
-        n_zero = int(zc.item())
+        n_zero = _ffi.read_i64(zc, st)
         if n_zero:
             from .spgemm import compact  # noqa: PLC0415
 

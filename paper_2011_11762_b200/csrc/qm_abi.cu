@@ -22,6 +22,34 @@ void set_error(const char *fmt, ...) {
 
 void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
+__global__ void k_read_i64(const int64_t *src, int n, volatile int64_t *dst) {
+  if (threadIdx.x < n) dst[threadIdx.x] = src[threadIdx.x];
+}
+
+int read_device_i64(const void *dev_src, int n, int64_t *host_out, cudaStream_t stream) {
+  struct Mapped {
+    int64_t *host = nullptr, *dev = nullptr;
+    int device = -1;
+  };
+  static thread_local Mapped m;
+  int device = 0;
+  QM_CUDA_TRY(cudaGetDevice(&device));
+  if (m.host == nullptr || m.device != device) {
+    QM_CUDA_TRY(cudaHostAlloc((void **)&m.host, 8 * sizeof(int64_t), cudaHostAllocMapped));
+    QM_CUDA_TRY(cudaHostGetDevicePointer((void **)&m.dev, m.host, 0));
+    m.device = device;
+  }
+  if (n < 1 || n > 8) {
+    set_error("read_device_i64: n=%d out of range", n);
+    return QM_ERR_INVALID;
+  }
+  k_read_i64<<<1, 32, 0, stream>>>((const int64_t *)dev_src, n, m.dev);
+  QM_LAUNCHED("k_read_i64");
+  QM_CUDA_TRY(cudaStreamSynchronize(stream));
+  for (int i = 0; i < n; ++i) host_out[i] = ((volatile int64_t *)m.host)[i];
+  return QM_OK;
+}
+
 int launch_block_stats(int bs, int64_t n, const double *blocks, double *sumsq, uint8_t *nonzero,
                        int64_t *zero_count, cudaStream_t st);
 
@@ -294,4 +322,8 @@ extern "C" int qm_add_identity_blocks(int32_t block_size, int64_t n, const int64
                                                               a_blocks, out);
   QM_LAUNCHED("k_add_identity");
   return QM_OK;
+}
+
+extern "C" int qm_read_i64(const int64_t *dev_src, int32_t n, int64_t *host_out, void *stream) {
+  return read_device_i64(dev_src, n, host_out, (cudaStream_t)stream);
 }

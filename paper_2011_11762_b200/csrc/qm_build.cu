@@ -164,9 +164,9 @@ extern "C" int qm_build_count(const qm_layout *layout, const int64_t *rows, cons
   k_entry_keys<<<grid_for(n), 256, 0, st>>>(rows, cols, n, layout->n_logical, g.bs, g.nbl, g.lbits,
                                             pbits, w.key, w.iota, w.bad);
   QM_LAUNCHED("k_entry_keys");
-  unsigned long long bad = 0;
-  QM_CUDA_TRY(cudaMemcpyAsync(&bad, w.bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
-  QM_CUDA_TRY(cudaStreamSynchronize(st));
+  int64_t bad = 0;
+  rc = read_device_i64(w.bad, 1, &bad, st);
+  if (rc != QM_OK) return rc;
   if (bad) {
     *n_out_of_range = (int64_t)bad;
     return QM_OK;
@@ -177,10 +177,12 @@ extern "C" int qm_build_count(const qm_layout *layout, const int64_t *rows, cons
   QM_LAUNCHED("k_heads");
   tb = w.cub_bytes;
   QM_CUDA_TRY(cub::DeviceScan::InclusiveSum(w.cub, tb, w.blk_head, w.blk_incl, n, st));
-  uint32_t nb = 0;
-  QM_CUDA_TRY(cudaMemcpyAsync(&nb, w.blk_incl + (n - 1), sizeof(nb), cudaMemcpyDeviceToHost, st));
-  QM_CUDA_TRY(cudaStreamSynchronize(st));
-  *n_blocks_out = nb;
+  // blk_incl is uint32: read the aligned 8-byte word holding the last entry
+  const int64_t last = n - 1;
+  int64_t word = 0;
+  rc = read_device_i64(w.blk_incl + (last & ~1ll), 1, &word, st);
+  if (rc != QM_OK) return rc;
+  *n_blocks_out = (last & 1) ? (int64_t)((uint64_t)word >> 32) : (int64_t)(uint32_t)word;
   return QM_OK;
 }
 

@@ -10,6 +10,10 @@ namespace qm {
 
 // Thread-local last-error message (qm_last_error).
 void set_error(const char *fmt, ...);
+// Reads n (<= 8) int64 values from device memory into host memory without a copy engine: a tiny
+// kernel writes them into a mapped pinned buffer, then `stream` is synchronised. (A D2H
+// cudaMemcpyAsync would queue behind large in-flight copies of earlier steps on the copy engine.)
+int read_device_i64(const void *dev_src, int n, int64_t *host_out, cudaStream_t stream);
 // Counts one kernel launch (qm_launch_count).
 void note_launch(int n = 1);
 

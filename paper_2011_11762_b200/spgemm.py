@@ -211,5 +211,6 @@ def multiply_blocks(layout, a: BlockSet, b: BlockSet, stream=None,
 
 
 def _sync_item(t: torch.Tensor, stream) -> int:
-    stream.synchronize()
-    return int(t.item())
+    """Device int64 -> host via a mapped buffer (qm_read_i64): unlike .item(), it does not queue
+    behind large D2H copies of earlier products on the copy engine."""
+    return _ffi.read_i64(t, stream)
