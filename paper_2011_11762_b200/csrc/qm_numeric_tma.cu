@@ -428,12 +428,6 @@ int launch_tma(const double *A, int64_t nA, const double *B, int64_t nB, const u
 using Tma32 = TmaCfg<32, 32, 1, 2, 32, 3, 4>;
 using Tma64 = TmaCfg<64, 64, 2, 2, 32, 3, 2>;
 using Tma128 = TmaCfg<128, 64, 2, 2, 32, 3, 2>;
-using Tma64x1 = TmaCfg<64, 64, 2, 2, 16, 6, 2>;  // QM_TMA_VARIANT=1: 16-deep panels, 6 stages (slower)
-
-int tma_variant() {
-  const char *e = getenv("QM_TMA_VARIANT");
-  return e ? atoi(e) : 0;
-}
 
 }  // namespace
 
@@ -453,10 +447,7 @@ int launch_numeric_tma(int bs, const double *A, int64_t nA, const double *B, int
   const uint2 *t2 = (const uint2 *)tri;
   switch (bs) {
     case 32: return launch_tma<Tma32>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
-    case 64:
-      if (tma_variant() == 1)
-        return launch_tma<Tma64x1>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
-      return launch_tma<Tma64>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
+    case 64: return launch_tma<Tma64>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
     case 128: return launch_tma<Tma128>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
     default: return QM_ERR_UNSUPPORTED;
   }

@@ -35,9 +35,6 @@ from .blocks import BlockSet
 from .errors import ContractViolationError
 
 
-_DEBUG_SYNC = bool(int(__import__("os").environ.get("QM_DEBUG_SYNC", "0")))
-
-
 class Comm:
     """torch.distributed collectives used by the product (process group `group`)."""
 
@@ -156,10 +153,6 @@ class DistStats:
     blocks_received: int = 0
     phase_s: dict = field(default_factory=dict)
 
-    @property
-    def flops_local(self) -> int:
-        return 0
-
 
 def partition(c_tptr: torch.Tensor, world: int) -> tuple[list[int], list[int]]:
     """Contiguous C ranges of (nearly) equal triple count: bounds over C indices and triples."""
@@ -233,8 +226,6 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     else:
         pool_b, rb, sb, nb = _fetch(comm, backend, b_local.blocks, b_off, need_b)
     stats.bytes_received, stats.bytes_sent, stats.blocks_received = ra + rb, sa + sb, na + nb
-    if _DEBUG_SYNC:
-        torch.cuda.synchronize(dev)
     t3 = clock()
     if hi == lo:
         return empty, stats

@@ -515,14 +515,6 @@ class _EngineInfo:
     pairs_per_level: list
 
 
-class _null:
-    def __enter__(self):
-        return self
-
-    def __exit__(self, *exc):
-        return False
-
-
 def _read_coordinate_text(path):
     """quadtree.read_coordinate_text (quadtree.py:379-402)."""
     rows, cols, vals = [], [], []

@@ -47,3 +47,23 @@ def test_invalid_layout_is_reported_not_crashed():
     assert b"divide" in lib.qm_last_error()
     with pytest.raises(Exception):
         _ffi.check(rc, "qm_encode_keys")
+
+
+def test_workspace_and_argument_errors_before_any_device_work():
+    """Status codes of the C ABI for caller mistakes (no GPU needed: they return before launching)."""
+    lib = _ffi.load()
+    lay = _ffi.make_layout(MatrixParams.create(4096, 64), 64)
+    nc, nt = ctypes.c_int64(-1), ctypes.c_int64(-1)
+    rc = lib.qm_spgemm_count(ctypes.byref(lay), None, 10, None, 10, None, 0, ctypes.byref(nc),
+                             ctypes.byref(nt), None)
+    assert rc == _ffi.QM_ERR_WORKSPACE and b"workspace" in lib.qm_last_error()
+    rc = lib.qm_spgemm_count(ctypes.byref(lay), None, -1, None, 10, None, 0, ctypes.byref(nc),
+                             ctypes.byref(nt), None)
+    assert rc == _ffi.QM_ERR_INVALID
+    assert lib.qm_numeric(ctypes.byref(lay), None, 0, None, 0, None, None, 0, None, None, None, None,
+                          None, 0, None) == _ffi.QM_OK  # nC == 0 is a no-op
+    assert lib.qm_compact(64, -1, None, None, None, None, None, None, None, None, 0, None) == _ffi.QM_ERR_INVALID
+    assert lib.qm_transpose_blocks(64, None, 4, None, None) == _ffi.QM_ERR_INVALID  # in place
+    too_deep = _ffi.QmLayout(1 << 40, 1, 40, 1, 0)
+    assert lib.qm_spgemm_workspace_bytes(ctypes.byref(too_deep), 1, 1) == 0
+    assert lib.qm_encode_keys(ctypes.byref(too_deep), None, None, 1, None, None) == _ffi.QM_ERR_UNSUPPORTED

@@ -436,3 +436,28 @@ def test_add_nil_fallbacks_share_the_survivor(ses):
     assert ses.add(z, z).root.is_nil
     assert ses.scale(a, 1.0).root == a.root and ses.scale(a, 0.0).root.is_nil
     assert ses.add_scaled_identity(a, 0.0).root == a.root
+
+
+@pytest.mark.parametrize("n,leaf,bs", [(1, 1, 1), (2, 1, 1), (3, 2, 1), (5, 4, 1), (9, 4, 4), (64, 64, 64), (1000, 2, 1)])
+def test_tiny_and_degenerate_shapes(ses, n, leaf, bs):
+    """n = 1, bs = 1 (generic SIMT path), one-leaf trees, deep trees of tiny leaves."""
+    da, db = helpers.random_sparse(n, 0.5, n), helpers.random_sparse(n, 0.5, n + 7)
+    c = ses.multiply(helpers.build(ses, da, leaf, bs), helpers.build(ses, db, leaf, bs))
+    assert helpers.rel(ses.to_dense(c), da @ db) <= TOL
+
+
+def test_products_without_matching_inner_indices_are_nil(ses):
+    """No k with A(i,k) and B(k,j): the symbolic phase finds no triple and C is nil."""
+    n, bs = 256, 64
+    da = np.zeros((n, n))
+    db = np.zeros((n, n))
+    da[:bs, :bs] = 1.0        # A only touches k in block 0
+    db[bs:2 * bs, :bs] = 2.0  # B only has k in block 1
+    c = ses.multiply(helpers.build(ses, da, bs, bs), helpers.build(ses, db, bs, bs))
+    assert c.root.is_nil and ses.last_multiply.n_triples == 0
+
+
+def test_very_sparse_with_empty_rows(ses):
+    da, db = helpers.random_sparse(777, 0.0005, 1), helpers.random_sparse(777, 0.0005, 2)
+    c = ses.multiply(helpers.build(ses, da, 16, 8), helpers.build(ses, db, 16, 8))
+    assert helpers.rel(ses.to_dense(c), da @ db) <= TOL
