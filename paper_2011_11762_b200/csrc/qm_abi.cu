@@ -22,11 +22,13 @@ void set_error(const char *fmt, ...) {
 
 void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
-__global__ void k_read_i64(const int64_t *src, int n, volatile int64_t *dst) {
+__global__ void k_read_i64(const int64_t *src, int n, const int64_t *src2, volatile int64_t *dst) {
   if (threadIdx.x < n) dst[threadIdx.x] = src[threadIdx.x];
+  if (src2 && threadIdx.x == 0) dst[n] = *src2;
 }
 
-int read_device_i64(const void *dev_src, int n, int64_t *host_out, cudaStream_t stream) {
+int read_device_i64(const void *dev_src, int n, int64_t *host_out, cudaStream_t stream,
+                    const void *dev_src2) {
   struct Mapped {
     int64_t *host = nullptr, *dev = nullptr;
     int device = -1;
@@ -43,10 +45,15 @@ int read_device_i64(const void *dev_src, int n, int64_t *host_out, cudaStream_t 
     set_error("read_device_i64: n=%d out of range", n);
     return QM_ERR_INVALID;
   }
-  k_read_i64<<<1, 32, 0, stream>>>((const int64_t *)dev_src, n, m.dev);
+  if (dev_src2 && n > 7) {
+    set_error("read_device_i64: n=%d too large with a second source", n);
+    return QM_ERR_INVALID;
+  }
+  k_read_i64<<<1, 32, 0, stream>>>((const int64_t *)dev_src, n, (const int64_t *)dev_src2, m.dev);
   QM_LAUNCHED("k_read_i64");
   QM_CUDA_TRY(cudaStreamSynchronize(stream));
-  for (int i = 0; i < n; ++i) host_out[i] = ((volatile int64_t *)m.host)[i];
+  const int total = n + (dev_src2 ? 1 : 0);
+  for (int i = 0; i < total; ++i) host_out[i] = ((volatile int64_t *)m.host)[i];
   return QM_OK;
 }
 

@@ -13,7 +13,9 @@ void set_error(const char *fmt, ...);
 // Reads n (<= 8) int64 values from device memory into host memory without a copy engine: a tiny
 // kernel writes them into a mapped pinned buffer, then `stream` is synchronised. (A D2H
 // cudaMemcpyAsync would queue behind large in-flight copies of earlier steps on the copy engine.)
-int read_device_i64(const void *dev_src, int n, int64_t *host_out, cudaStream_t stream);
+// An optional second source appends one more value (two scattered counts, one synchronisation).
+int read_device_i64(const void *dev_src, int n, int64_t *host_out, cudaStream_t stream,
+                    const void *dev_src2 = nullptr);
 // Counts one kernel launch (qm_launch_count).
 void note_launch(int n = 1);
 

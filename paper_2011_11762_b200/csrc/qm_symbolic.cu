@@ -449,9 +449,7 @@ extern "C" int qm_spgemm_count(const qm_layout *layout, const uint64_t *a_keys, 
   tb = w.cub_bytes;
   QM_CUDA_TRY(cub::DeviceScan::InclusiveSum(w.cub, tb, w.rowT, w.rowT_off + 1, g.nbg, st));
   uint64_t tot[2];
-  rc = read_device_i64(w.rowC_off + g.nbg, 1, (int64_t *)&tot[0], st);
-  if (rc != QM_OK) return rc;
-  rc = read_device_i64(w.rowT_off + g.nbg, 1, (int64_t *)&tot[1], st);
+  rc = read_device_i64(w.rowC_off + g.nbg, 1, (int64_t *)tot, st, w.rowT_off + g.nbg);
   if (rc != QM_OK) return rc;
   if (tot[0] >= (1ull << 32)) {
     set_error("product has %llu C blocks; this build indexes C with 32 bits", (unsigned long long)tot[0]);
