@@ -143,6 +143,23 @@ QM_API int qm_numeric(const qm_layout *layout, const double *a_blocks, int64_t n
                const double *b_blocks, int64_t nB, const uint32_t *tri, const int64_t *c_tptr,
                int64_t nC, double *c_blocks, double *c_sumsq, uint8_t *c_nonzero,
                int64_t *zero_count, void *ws, size_t ws_bytes, void *stream);
+/* The numeric phase of a multi-GPU product fused with its halo exchange: operand blocks live in
+ * up to 8 pools per operand -- this rank's and the other ranks' block pools mapped into this GPU's
+ * address space (CUDA IPC / peer access over NVLink). a_pools / b_pools / a_counts / b_counts are
+ * HOST arrays of device pointers and block counts; triple indices are packed
+ * (owner << 28) | local_index. The TMA producer reads each block straight from its owner's memory,
+ * overlapped with the DMMAs of earlier stages (no separate exchange). bs 32/64/128 only. */
+QM_API int qm_numeric_pools(const qm_layout *layout, const double *const *a_pools, const int64_t *a_counts,
+                            int32_t n_a_pools, const double *const *b_pools, const int64_t *b_counts,
+                            int32_t n_b_pools, const uint32_t *tri, const int64_t *c_tptr, int64_t nC,
+                            double *c_blocks, double *c_sumsq, uint8_t *c_nonzero, int64_t *zero_count,
+                            void *ws, size_t ws_bytes, void *stream);
+/* CUDA IPC of block pools for qm_numeric_pools (same-node ranks): export writes the 64-byte
+ * cudaIpcMemHandle of the allocation containing `ptr` and ptr's byte offset in it; open maps a peer
+ * handle (once per handle and process) and returns the allocation base; close unmaps it. */
+QM_API int qm_ipc_export(const void *ptr, void *handle_out, int64_t *offset_out);
+QM_API int qm_ipc_open(const void *handle, void **base_out);
+QM_API int qm_ipc_close(void *base);
 /* Which numeric kernel qm_numeric uses for this block size: 2 = TMA + mbarrier warp-specialised
  * DMMA (bs 32/64/128), 1 = cp.async DMMA (bs 16, or QM_NUMERIC=cpasync), 0 = FP64 SIMT (others). */
 QM_API int qm_numeric_path(int32_t block_size);

@@ -43,6 +43,10 @@ EXPORTS = (
     "qm_spgemm_fill_triples",
     "qm_numeric",
     "qm_numeric_workspace_bytes",
+    "qm_numeric_pools",
+    "qm_ipc_export",
+    "qm_ipc_open",
+    "qm_ipc_close",
     "qm_numeric_path",
     "qm_compact_workspace_bytes",
     "qm_compact",
@@ -97,6 +101,11 @@ _SIGS = {
                                               _P, _P]),
     "qm_numeric": (ctypes.c_int, [_LP, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "qm_numeric_workspace_bytes": (_SZ, [_I32, _I64]),
+    "qm_ipc_export": (ctypes.c_int, [_P, _P, ctypes.POINTER(_I64)]),
+    "qm_ipc_open": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
+    "qm_ipc_close": (ctypes.c_int, [_P]),
+    "qm_numeric_pools": (ctypes.c_int, [_LP, _P, _P, _I32, _P, _P, _I32, _P, _P, _I64, _P, _P, _P, _P, _P,
+                                        _SZ, _P]),
     "qm_numeric_path": (ctypes.c_int, [_I32]),
     "qm_compact_workspace_bytes": (_SZ, [_I64]),
     "qm_compact": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),

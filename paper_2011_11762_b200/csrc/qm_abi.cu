@@ -3,8 +3,12 @@
 #include <cub/cub.cuh>
 #include <stdarg.h>
 #include <stdio.h>
+#include <string.h>
 
 #include <atomic>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "qm_common.cuh"
 
@@ -333,4 +337,43 @@ extern "C" int qm_add_identity_blocks(int32_t block_size, int64_t n, const int64
 
 extern "C" int qm_read_i64(const int64_t *dev_src, int32_t n, int64_t *host_out, void *stream) {
   return read_device_i64(dev_src, n, host_out, (cudaStream_t)stream);
+}
+
+// ---- CUDA IPC for the fused multi-GPU product: a block pool is exported as the IPC handle of its
+// ---- allocation plus the pool's byte offset inside it (torch's caching allocator sub-allocates).
+extern "C" int qm_ipc_export(const void *ptr, void *handle_out /*64 bytes*/, int64_t *offset_out) {
+  static PFN_cuMemGetAddressRange_v3020 get_range = nullptr;
+  if (!get_range) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      set_error("qm_ipc_export: cuMemGetAddressRange unavailable");
+      return QM_ERR_CUDA;
+    }
+    get_range = (PFN_cuMemGetAddressRange_v3020)fn;
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS) {
+    set_error("qm_ipc_export: pointer %p is not a device allocation", ptr);
+    return QM_ERR_INVALID;
+  }
+  cudaIpcMemHandle_t h;
+  QM_CUDA_TRY(cudaIpcGetMemHandle(&h, (void *)base));
+  memcpy(handle_out, &h, sizeof(h));
+  *offset_out = (int64_t)((CUdeviceptr)ptr - base);
+  return QM_OK;
+}
+
+extern "C" int qm_ipc_open(const void *handle /*64 bytes*/, void **base_out) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  QM_CUDA_TRY(cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return QM_OK;
+}
+
+extern "C" int qm_ipc_close(void *base) {
+  QM_CUDA_TRY(cudaIpcCloseMemHandle(base));
+  return QM_OK;
 }

@@ -21,6 +21,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "qm_common.cuh"
 
@@ -105,6 +106,21 @@ struct TmaCfg {
   static_assert(A_SP_BYTES % 1024 == 0 && B_SP_BYTES % 1024 == 0, "swizzle-128B atoms need 1 KB alignment");
 };
 
+// Tensor maps of the operand block pools. NPOOL = 1: one local pool per operand. NPOOL > 1: the
+// pools of every rank of a multi-GPU product, mapped into this GPU's address space (CUDA IPC /
+// peer access); a triple index then packs (owner << kOwnerShift) | local index, and the producer's
+// TMA reads the block straight from its owner's HBM over NVLink -- the halo exchange fused into the
+// numeric kernel, overlapped with the DMMAs of earlier stages.
+constexpr int kOwnerShift = 28;
+constexpr uint32_t kLocalMask = (1u << kOwnerShift) - 1u;
+constexpr int kMaxPools = 8;
+
+template <int NPOOL>
+struct __align__(64) TmaMaps {
+  CUtensorMap a[NPOOL];
+  CUtensorMap b[NPOOL];
+};
+
 // Stage cursor over work units u = m * NQ + q (C block m, tile q), triple t, k panel p.
 struct Cur {
   int64_t unit, t, tend;
@@ -138,9 +154,9 @@ __device__ __forceinline__ void cur_next(Cur &c, int64_t nU, const int64_t *tptr
   }
 }
 
-template <class Cfg>
+template <class Cfg, int NPOOL>
 __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
-    k_numeric_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+    k_numeric_tma(const __grid_constant__ TmaMaps<NPOOL> maps,
                   const uint2 *__restrict__ tri, const int64_t *__restrict__ tptr, int64_t nC,
                   double *__restrict__ C, double *__restrict__ csq, uint8_t *__restrict__ cnz,
                   int64_t *__restrict__ zero_count, double *__restrict__ part_sq,
@@ -170,8 +186,11 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
   if (warp == Cfg::NCW) {
     // ------------------------------ producer warp ------------------------------
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
-      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
+#pragma unroll
+      for (int i = 0; i < NPOOL; ++i) {
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(&maps.a[i]) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(&maps.b[i]) : "memory");
+      }
       // Dynamic work distribution: the first unit is blockIdx.x, later ones come from a global
       // counter in key order (so concurrently running CTAs still share A/B rows/columns in L2)
       // and no CTA is left with a long tail of heavy units.
@@ -188,6 +207,8 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
           break;
         }
         const uint2 ab = tri[L.t];
+        const uint32_t ao = NPOOL > 1 ? ab.x >> kOwnerShift : 0u, al = NPOOL > 1 ? ab.x & kLocalMask : ab.x;
+        const uint32_t bo = NPOOL > 1 ? ab.y >> kOwnerShift : 0u, bl = NPOOL > 1 ? ab.y & kLocalMask : ab.y;
         const int qt = (int)(L.unit % Cfg::NQ);
         const int row0 = (qt / Cfg::NQN) * Cfg::TILE, col0 = (qt % Cfg::NQN) * Cfg::TILE;
         uint8_t *st = smem + (size_t)s * Cfg::STAGE_BYTES;
@@ -195,12 +216,12 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
         mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
 #pragma unroll
         for (int q = 0; q < Cfg::KSP; ++q)
-          tma_load_2d(st + q * Cfg::A_SP_BYTES, &tmA, L.p * Cfg::KP + q * 16, (int)(ab.x * BS + row0),
+          tma_load_2d(st + q * Cfg::A_SP_BYTES, &maps.a[ao], L.p * Cfg::KP + q * 16, (int)(al * BS + row0),
                       &full[s]);
 #pragma unroll
         for (int q = 0; q < Cfg::NSP; ++q)
-          tma_load_2d(st + Cfg::A_BYTES + q * Cfg::B_SP_BYTES, &tmB, col0 + q * 16,
-                      (int)(ab.y * BS + L.p * Cfg::KP), &full[s]);
+          tma_load_2d(st + Cfg::A_BYTES + q * Cfg::B_SP_BYTES, &maps.b[bo], col0 + q * 16,
+                      (int)(bl * BS + L.p * Cfg::KP), &full[s]);
         cur_next<Cfg>(L, nU, tptr, next, counter);
         if (++s == STAGES) {
           s = 0;
@@ -381,39 +402,46 @@ size_t tma_ws_bytes(int64_t nC) {
   return 256 + (size_t)nC * Cfg::NQ * Cfg::NCW * (sizeof(double) + sizeof(uint8_t)) + 256;
 }
 
-template <class Cfg>
-int launch_tma(const double *A, int64_t nA, const double *B, int64_t nB, const uint2 *tri,
-               const int64_t *tptr, int64_t nC, double *C, double *csq, uint8_t *cnz, int64_t *zc,
-               void *ws, size_t ws_bytes, cudaStream_t st) {
-  double *part_sq = nullptr;
-  uint8_t *part_nz = nullptr;
+template <class Cfg, int NPOOL>
+int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const double *const *B,
+                     const int64_t *nB, int nb, const uint2 *tri, const int64_t *tptr, int64_t nC,
+                     double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes,
+                     cudaStream_t st) {
+  if (na < 1 || nb < 1 || na > NPOOL || nb > NPOOL) {
+    set_error("qm_numeric: %d / %d operand pools (at most %d)", na, nb, NPOOL);
+    return QM_ERR_INVALID;
+  }
   if (!ws || ws_bytes < tma_ws_bytes<Cfg>(nC)) {
     set_error("qm_numeric: workspace %zu < required %zu", ws_bytes, tma_ws_bytes<Cfg>(nC));
     return QM_ERR_WORKSPACE;
   }
   unsigned long long *counter = (unsigned long long *)ws;
-  part_sq = (double *)((char *)ws + 256);
-  part_nz = (uint8_t *)(part_sq + nC * Cfg::NQ * Cfg::NCW);
+  double *part_sq = (double *)((char *)ws + 256);
+  uint8_t *part_nz = (uint8_t *)(part_sq + nC * Cfg::NQ * Cfg::NCW);
   QM_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
-  CUtensorMap ma, mb;
-  int rc = make_map(&ma, A, nA, Cfg::BS, Cfg::TILE);
-  if (rc != QM_OK) return rc;
-  rc = make_map(&mb, B, nB, Cfg::BS, Cfg::KP);
-  if (rc != QM_OK) return rc;
+  TmaMaps<NPOOL> maps;
+  memset(&maps, 0, sizeof(maps));
+  for (int i = 0; i < NPOOL; ++i) {  // unused slots repeat pool 0 (never indexed)
+    int rc = make_map(&maps.a[i], A[i < na ? i : 0], nA[i < na ? i : 0], Cfg::BS, Cfg::TILE);
+    if (rc != QM_OK) return rc;
+    rc = make_map(&maps.b[i], B[i < nb ? i : 0], nB[i < nb ? i : 0], Cfg::BS, Cfg::KP);
+    if (rc != QM_OK) return rc;
+  }
   static bool configured = false;
   if (!configured) {
-    QM_CUDA_TRY(cudaFuncSetAttribute(k_numeric_tma<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    QM_CUDA_TRY(cudaFuncSetAttribute(k_numeric_tma<Cfg, NPOOL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)Cfg::SMEM));
     configured = true;
   }
   int per_sm = 0;
-  QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_numeric_tma<Cfg>, Cfg::NTHR, Cfg::SMEM));
+  QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_numeric_tma<Cfg, NPOOL>, Cfg::NTHR,
+                                                            Cfg::SMEM));
   if (per_sm < 1) per_sm = 1;
   const int64_t nU = nC * Cfg::NQ;
   int64_t grid = (int64_t)sm_count_tma() * per_sm;
   if (grid > nU) grid = nU;
-  k_numeric_tma<Cfg><<<(int)grid, Cfg::NTHR, Cfg::SMEM, st>>>(ma, mb, tri, tptr, nC, C, csq, cnz, zc,
-                                                              part_sq, part_nz, counter, /*zmask=*/0ull);
+  k_numeric_tma<Cfg, NPOOL><<<(int)grid, Cfg::NTHR, Cfg::SMEM, st>>>(
+      maps, tri, tptr, nC, C, csq, cnz, zc, part_sq, part_nz, counter, /*zmask=*/0ull);
   QM_LAUNCHED("k_numeric_tma");
   {
     int64_t g = std::min<int64_t>((nC + 255) / 256, (int64_t)sm_count_tma() * 8);
@@ -422,6 +450,16 @@ int launch_tma(const double *A, int64_t nA, const double *B, int64_t nB, const u
     QM_LAUNCHED("k_combine_tiles");
   }
   return QM_OK;
+}
+
+template <class Cfg>
+int launch_tma(const double *const *A, const int64_t *nA, int na, const double *const *B,
+               const int64_t *nB, int nb, const uint2 *tri, const int64_t *tptr, int64_t nC, double *C,
+               double *csq, uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes, cudaStream_t st) {
+  if (na == 1 && nb == 1)
+    return launch_tma_pools<Cfg, 1>(A, nA, na, B, nB, nb, tri, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
+  return launch_tma_pools<Cfg, kMaxPools>(A, nA, na, B, nB, nb, tri, tptr, nC, C, csq, cnz, zc, ws, ws_bytes,
+                                          st);
 }
 
 //                     BS TILE WM WN KP STAGES MINB
@@ -440,15 +478,17 @@ size_t numeric_tma_ws_bytes(int bs, int64_t nC) {
   }
 }
 
-// Returns QM_ERR_UNSUPPORTED when no TMA variant exists for bs.
-int launch_numeric_tma(int bs, const double *A, int64_t nA, const double *B, int64_t nB,
-                       const uint32_t *tri, const int64_t *tptr, int64_t nC, double *C, double *csq,
-                       uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes, cudaStream_t st) {
+// Returns QM_ERR_UNSUPPORTED when no TMA variant exists for bs. `na` / `nb` operand pools (1 =
+// local; > 1 = every rank's pool, triple indices packed as owner << 28 | local).
+int launch_numeric_tma(int bs, const double *const *A, const int64_t *nA, int na, const double *const *B,
+                       const int64_t *nB, int nb, const uint32_t *tri, const int64_t *tptr, int64_t nC,
+                       double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes,
+                       cudaStream_t st) {
   const uint2 *t2 = (const uint2 *)tri;
   switch (bs) {
-    case 32: return launch_tma<Tma32>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
-    case 64: return launch_tma<Tma64>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
-    case 128: return launch_tma<Tma128>(A, nA, B, nB, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
+    case 32: return launch_tma<Tma32>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
+    case 64: return launch_tma<Tma64>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
+    case 128: return launch_tma<Tma128>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
     default: return QM_ERR_UNSUPPORTED;
   }
 }

@@ -85,6 +85,9 @@ class Comm:
         self.dist.all_to_all_single(out, flat.contiguous(), recv_counts, send_counts, group=self.group)
         return self._out(out.reshape((out.shape[0],) + tuple(send.shape[1:])), dev0), recv_counts
 
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
     def allreduce_max(self, x: float, device) -> float:
         t = torch.tensor([x], dtype=torch.float64, device="cpu" if self.stage else device)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
@@ -102,12 +105,41 @@ class LocalComm:
     def alltoallv(self, send, send_counts):
         return send, list(send_counts)
 
+    def barrier(self):
+        pass
+
     def allreduce_max(self, x, device):
         return x
 
 
 class CudaBackend:
     """The product backend: libqmb200 kernels on the rank's GPU."""
+
+    def numeric_pools(self, layout, pa: list, na: list, pb: list, nb: list, tri: torch.Tensor,
+                      c_tptr: torch.Tensor, c_keys: torch.Tensor) -> BlockSet:
+        import ctypes
+
+        from . import _ffi
+
+        lib = _ffi.load()
+        bs = layout.block_size
+        dev = c_keys.device
+        nc = int(c_keys.shape[0])
+        arr_p = lambda v: (ctypes.c_void_p * len(v))(*v)  # noqa: E731
+        arr_n = lambda v: (ctypes.c_int64 * len(v))(*v)  # noqa: E731
+        out = BlockSet(c_keys, torch.empty((nc, bs, bs), dtype=torch.float64, device=dev),
+                       torch.empty(nc, dtype=torch.float64, device=dev))
+        nz = torch.empty(nc, dtype=torch.uint8, device=dev)
+        zc = torch.zeros(1, dtype=torch.int64, device=dev)
+        wb = lib.qm_numeric_workspace_bytes(bs, nc)
+        ws = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
+        stream = self.stream if self.stream is not None else torch.cuda.current_stream(dev)
+        _ffi.check(lib.qm_numeric_pools(ctypes.byref(layout), arr_p(pa), arr_n(na), len(pa), arr_p(pb),
+                                        arr_n(nb), len(pb), _ffi.ptr(tri), _ffi.ptr(c_tptr), nc,
+                                        _ffi.ptr(out.blocks), _ffi.ptr(out.sumsq), _ffi.ptr(nz), _ffi.ptr(zc),
+                                        _ffi.ptr(ws), wb, _ffi.stream_handle(stream)), "qm_numeric_pools")
+        n_zero = spgemm._sync_item(zc, stream)
+        return spgemm.compact(bs, out, nz, n_zero, self.stream)
 
     def __init__(self, stream=None):
         self.stream = stream
@@ -151,6 +183,7 @@ class DistStats:
     bytes_received: int = 0
     bytes_sent: int = 0
     blocks_received: int = 0
+    mode: str = "exchange"
     phase_s: dict = field(default_factory=dict)
 
 
@@ -166,6 +199,71 @@ def partition(c_tptr: torch.Tensor, world: int) -> tuple[list[int], list[int]]:
         cb[r] = max(cb[r], cb[r - 1])
     tb = c_tptr[torch.tensor(cb, device=c_tptr.device)].cpu().tolist()
     return cb, [int(x) for x in tb]
+
+
+class PeerPools:
+    """Block pools of every rank, mapped into this GPU's address space for the fused kernel.
+
+    Each rank exports (qm_ipc_export) the CUDA IPC handle of the allocation holding its pool and
+    the pool's offset in it; the handles are all-gathered through the process group and every
+    peer handle is opened once (qm_ipc_open, peer access over NVLink on a multi-GPU node; on a
+    single GPU the "peers" are other processes sharing it). ``close`` unmaps before the caller's
+    barrier, so no rank frees a pool another rank still maps."""
+
+    def __init__(self, comm, pools):
+        import ctypes
+
+        from . import _ffi
+
+        lib = _ffi.load()
+        self.lib, self.rank = lib, comm.rank
+        mine = []
+        for t in pools:
+            if t.numel() == 0:
+                mine.append(None)
+                continue
+            h = ctypes.create_string_buffer(64)
+            off = ctypes.c_int64(0)
+            _ffi.check(lib.qm_ipc_export(_ffi.ptr(t), h, ctypes.byref(off)), "qm_ipc_export")
+            mine.append((h.raw, int(off.value), int(t.shape[0])))
+        every = [None] * comm.world
+        comm.dist.all_gather_object(every, mine, group=comm.group)
+        self._opened = {}
+        self.ptrs = [[0] * comm.world for _ in pools]
+        self.counts = [[0] * comm.world for _ in pools]
+        bs = int(pools[0].shape[1])
+        self._dummy = torch.zeros((1, bs, bs), dtype=torch.float64, device=pools[0].device)
+        for r, entries in enumerate(every):
+            for p_i, e in enumerate(entries):
+                if r == comm.rank:
+                    t = pools[p_i]
+                    self.ptrs[p_i][r] = _ffi.ptr(t) if t.numel() else _ffi.ptr(self._dummy)
+                    self.counts[p_i][r] = max(int(t.shape[0]), 1)
+                    continue
+                if e is None:
+                    self.ptrs[p_i][r], self.counts[p_i][r] = _ffi.ptr(self._dummy), 1
+                    continue
+                handle, off, n = e
+                if handle not in self._opened:
+                    base = ctypes.c_void_p(0)
+                    _ffi.check(lib.qm_ipc_open(handle, ctypes.byref(base)), "qm_ipc_open")
+                    self._opened[handle] = int(base.value)
+                self.ptrs[p_i][r] = self._opened[handle] + off
+                self.counts[p_i][r] = n
+
+    def close(self):
+        from . import _ffi
+
+        for base in self._opened.values():
+            _ffi.check(self.lib.qm_ipc_close(base), "qm_ipc_close")
+        self._opened = {}
+
+
+def _pack_owner(idx: torch.Tensor, offsets: torch.Tensor):
+    """Global block index -> (owner << 28) | local index, and the owner."""
+    owner = torch.searchsorted(offsets[1:], idx, right=True)
+    local = idx - offsets[owner]
+    return (owner << 28) | local, owner
 
 
 def _fetch(comm, backend, local_blocks: torch.Tensor, offsets: list[int], need: torch.Tensor):
@@ -185,10 +283,23 @@ def _fetch(comm, backend, local_blocks: torch.Tensor, offsets: list[int], need: 
     return blocks, peers_in * bsz, peers_out * bsz, peers_in
 
 
+NVLINK_GBS = 770.0   # measured peer copy bandwidth per direction (B200_PROFILING.md)
+FP64_TFLOPS = 35.0   # sustained numeric-kernel rate used by the mode heuristic
+
+
 def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b_is_a: bool = False,
-             timer=None):
+             timer=None, mode: str = "auto"):
     """This rank's part of C = A*B. `a_local`/`b_local` are the rank's owned key ranges (ascending
-    across ranks). Returns (C blocks of this rank's C key range, DistStats)."""
+    across ranks). Returns (C blocks of this rank's C key range, DistStats).
+
+    mode "exchange": request/serve halo exchange, then the local numeric kernel.
+    mode "fused":    no exchange; the numeric kernel's TMA producer reads remote blocks directly
+                     from their owners' pools (PeerPools, CUDA IPC over NVLink), overlapped with
+                     the math (qm_numeric_pools).
+    mode "auto":     fused when its estimated NVLink time (every remote block reference is a
+                     remote read: peer loads bypass the local L2) stays under a quarter of the
+                     estimated compute time, else exchange (heavy reuse of remote blocks, e.g.
+                     random patterns)."""
     backend = backend or CudaBackend()
     stats = DistStats(rank=comm.rank, world=comm.world)
     clock = timer or (lambda: time.perf_counter())
@@ -218,6 +329,37 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     stats.c_range, stats.t_range = (m0, m1), (lo, hi)
     tri = st.triples(c_tptr, lo, hi).view(-1, 2).to(torch.int64)
     t2 = clock()
+    fused_ok = (comm.world > 1 and mode != "exchange" and hasattr(backend, "numeric_pools")
+                and layout.block_size in (32, 64, 128) and comm.world <= 8)
+    if fused_ok and hi > lo:
+        offa = torch.tensor(a_off, dtype=torch.int64, device=dev)
+        offb = offa if b_is_a else torch.tensor(b_off, dtype=torch.int64, device=dev)
+        pa_idx, own_a = _pack_owner(tri[:, 0].contiguous(), offa)
+        pb_idx, own_b = _pack_owner(tri[:, 1].contiguous(), offb)
+        blk_bytes = bs * bs * 8
+        remote_refs = int(((own_a != comm.rank).sum() + (own_b != comm.rank).sum()).item())
+        fused_s = remote_refs * blk_bytes / (NVLINK_GBS * 1e9)
+        compute_s = 2.0 * bs ** 3 * (hi - lo) / (FP64_TFLOPS * 1e12)
+        if mode == "fused" or fused_s <= 0.25 * compute_s:
+            comm.barrier()  # pools are complete on every rank before anyone maps them
+            pools = PeerPools(comm, [a_local.blocks] if b_is_a else [a_local.blocks, b_local.blocks])
+            tri_packed = torch.stack([pa_idx, pb_idx], dim=1).to(torch.int32).reshape(-1).contiguous()
+            c_tptr_local = (c_tptr[m0:m1 + 1] - lo).contiguous()
+            try:
+                c = backend.numeric_pools(layout, pools.ptrs[0], pools.counts[0], pools.ptrs[-1],
+                                          pools.counts[-1], tri_packed, c_tptr_local,
+                                          c_keys[m0:m1].contiguous())
+                torch.cuda.synchronize(dev)
+            finally:
+                pools.close()
+            comm.barrier()  # every rank has finished reading and unmapping the others' pools
+            t4 = clock()
+            stats.n_c_local = c.n
+            stats.mode = "fused"
+            stats.bytes_received = remote_refs * blk_bytes  # NVLink reads of the fused kernel
+            stats.phase_s = {"structure": t1 - t0, "symbolic": t2 - t1, "exchange": 0.0,
+                             "numeric": t4 - t2}
+            return c, stats
     need_a = torch.unique(tri[:, 0]) if hi > lo else tri.new_zeros(0)
     need_b = torch.unique(tri[:, 1]) if hi > lo else tri.new_zeros(0)
     pool_a, ra, sa, na = _fetch(comm, backend, a_local.blocks, a_off, need_a)
@@ -240,6 +382,7 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     c = backend.numeric(layout, pa, pb, tri_local, c_tptr_local, c_keys_local)
     t4 = clock()
     stats.n_c_local = c.n
+    stats.mode = "exchange"
     stats.phase_s = {"structure": t1 - t0, "symbolic": t2 - t1, "exchange": t3 - t2, "numeric": t4 - t3}
     return c, stats
 

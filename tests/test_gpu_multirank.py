@@ -20,7 +20,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, cfg_name, outdir):
+def _worker(rank, world, port, cfg_name, outdir, mode="exchange"):
     import sys
 
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -43,7 +43,8 @@ def _worker(rank, world, port, cfg_name, outdir):
                                      cfg.half_bw, dev))
     layout = _ffi.make_layout(geom.params, geom.bs)
     comm = D.Comm()
-    c, st = D.multiply(comm, layout, parts[0], parts[1])
+    c, st = D.multiply(comm, layout, parts[0], parts[1], mode=mode)
+    assert st.mode == mode
     keys, _ = comm.allgather_varlen(c.keys)
     blocks, _ = comm.allgather_varlen(c.blocks.reshape(-1))
     info = torch.tensor([st.bytes_received, st.t_range[1] - st.t_range[0]], dtype=torch.int64)
@@ -57,13 +58,17 @@ def _worker(rank, world, port, cfg_name, outdir):
                  same_keys=torch.equal(keys, ref.keys), same_blocks=torch.equal(blocks.view(ref.blocks.shape), ref.blocks)
                  if blocks.numel() == ref.blocks.numel() else False,
                  info=torch.stack(allinfo).numpy())
+    torch.cuda.synchronize()
     dist.barrier()
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("mode", ["exchange", "fused"])
 @pytest.mark.parametrize("world,cfg", [(2, "C1"), (3, "C2-16384"), (2, "random")])
-def test_multirank_cuda_backend_equals_single_gpu(tmp_path, world, cfg):
-    mp.spawn(_worker, args=(world, _free_port(), cfg, str(tmp_path)), nprocs=world, join=True)
+def test_multirank_cuda_backend_equals_single_gpu(tmp_path, world, cfg, mode):
+    """mode "fused": the numeric kernel reads remote blocks through CUDA-IPC-mapped peer pools
+    (qm_numeric_pools) instead of an exchange -- here the peers share the one GPU."""
+    mp.spawn(_worker, args=(world, _free_port(), cfg, str(tmp_path), mode), nprocs=world, join=True)
     out = np.load(tmp_path / "out.npz")
     assert bool(out["same_keys"]) and bool(out["same_blocks"])
     info = out["info"]
