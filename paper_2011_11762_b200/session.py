@@ -365,6 +365,11 @@ class MatrixSession:
         m = self.matrix_from_triplets(n, r, cc, v, leaf_dim, leaf_kind, block_size)
         return Matrix(m.root, m.params, m.leaf_kind, m.block_size, symmetric)
 
+    def assign_from_triplets(self, n, rows, cols, vals, leaf_dim: int = 128,
+                             leaf_kind="block_sparse", block_size: int = 16) -> Matrix:
+        """session.py:191-198 (the task-built variant of matrix_from_triplets; same result)."""
+        return self.matrix_from_triplets(n, rows, cols, vals, leaf_dim, leaf_kind, block_size)
+
     def load_coordinate(self, path, leaf_dim: int = 128, leaf_kind="block_sparse",
                         block_size: int = 16, symmetric: bool = False) -> Matrix:
         """session.py:139-144 (1-based coordinate text)."""

@@ -461,3 +461,44 @@ def test_very_sparse_with_empty_rows(ses):
     da, db = helpers.random_sparse(777, 0.0005, 1), helpers.random_sparse(777, 0.0005, 2)
     c = ses.multiply(helpers.build(ses, da, 16, 8), helpers.build(ses, db, 16, 8))
     assert helpers.rel(ses.to_dense(c), da @ db) <= TOL
+
+
+@pytest.mark.parametrize("name,counts", [
+    ("C5-64", (1063904, 17827216)), ("C5-128", (270064, 2365448)), ("C5-32", (4222912, 138330400))])
+def test_c5_full_size_sampled_rows(ses, name, counts):
+    """BASELINE configs[4] at full size (N = 2^20, up to 70 GB on the device): C block and triple
+    counts equal SURVEY.md 8(d), sampled C block rows equal the oracle on regenerated blocks, and
+    the fused norms match the blocks."""
+    cfg = G.CONFIGS[name]
+    geom, a, b = G.config_operands_device(cfg, ses.device)
+    layout = _ffi.make_layout(geom.params, geom.bs)
+    st = spgemm.MultiplyStats()
+    c = spgemm.multiply_blocks(layout, a, b, stats=st)
+    del a, b
+    assert (st.n_c, st.n_triples) == counts
+    rows = np.r_[0, np.random.default_rng(1).choice(geom.nbg, 6, replace=False), geom.nbg - 1]
+    kc, bc = helpers.oracle_rows(cfg, rows)
+    keys_all = c.keys.cpu().numpy()
+    got = helpers.lookup(keys_all, c.blocks, kc)
+    assert helpers.rel(got, bc) <= TOL
+    pos = torch.from_numpy(np.searchsorted(keys_all, kc)).to(c.sumsq.device)
+    np.testing.assert_allclose(c.sumsq.index_select(0, pos).cpu().numpy(), np.einsum("nij,nij->n", bc, bc),
+                               rtol=1e-12)
+    del c
+    torch.cuda.empty_cache()
+
+
+def test_c4_full_size_sampled_rows(ses):
+    """BASELINE configs[3] (decay, C = A*A) at full size: sampled C block rows vs the oracle."""
+    cfg = G.CONFIGS["C4"]
+    geom, (ka, ba), _ = G.config_operands_host(cfg)
+    c = ses.multiply(*(2 * [ses.matrix_from_blocks(geom, ka, ba)]))
+    assert ses.last_multiply.n_triples == 735716
+    ai, ak = geom.decode(ka)
+    rows = np.r_[0, np.random.default_rng(2).choice(geom.nbg, 6, replace=False), geom.nbg - 1]
+    sel = np.isin(ai, rows)
+    need_k = np.unique(ak[sel])
+    sel_b = np.isin(ai, need_k)  # B = A: rows k of A
+    kc, bc, _ = O.multiply(O.Geom(cfg.n, cfg.bs, cfg.bs), ka[sel], ba[sel], ka[sel_b], ba[sel_b])
+    got = helpers.lookup(c.root.blockset.keys.cpu().numpy(), c.root.blockset.blocks, kc)
+    assert helpers.rel(got, bc) <= TOL
