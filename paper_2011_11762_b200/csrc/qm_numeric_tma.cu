@@ -419,6 +419,16 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
   double *part_sq = (double *)((char *)ws + 256);
   uint8_t *part_nz = (uint8_t *)(part_sq + nC * Cfg::NQ * Cfg::NCW);
   QM_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
+  for (int i = 0; i < na; ++i)
+    if (nA[i] * (int64_t)Cfg::BS >= ((int64_t)1 << 31)) {
+      set_error("qm_numeric: pool of %lld blocks exceeds TMA's int32 row coordinate", (long long)nA[i]);
+      return QM_ERR_UNSUPPORTED;
+    }
+  for (int i = 0; i < nb; ++i)
+    if (nB[i] * (int64_t)Cfg::BS >= ((int64_t)1 << 31)) {
+      set_error("qm_numeric: pool of %lld blocks exceeds TMA's int32 row coordinate", (long long)nB[i]);
+      return QM_ERR_UNSUPPORTED;
+    }
   TmaMaps<NPOOL> maps;
   memset(&maps, 0, sizeof(maps));
   for (int i = 0; i < NPOOL; ++i) {  // unused slots repeat pool 0 (never indexed)
