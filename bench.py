@@ -79,6 +79,10 @@ class ClockSampler:
             return
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
+        # nvidia-smi's own start-up (NVML init) must not overlap the timed region
+        t0 = time.time()
+        while not self.rows and time.time() - t0 < 3.0:
+            time.sleep(0.01)
 
     def _read(self):
         for line in self.proc.stdout:

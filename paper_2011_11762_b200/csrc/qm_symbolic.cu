@@ -6,7 +6,7 @@
 // multiply tasks are exactly the block triples (i,k,j) with A(i,k) and B(k,j) stored, and the C
 // block set is the set of (i,j) reached. Here that set is computed per C block-row with a windowed
 // dense accumulator in shared memory:
-//   1. block-row indexes of A and B (stable radix sort by row; quadtree keys are monotone in the
+//   1. one block-row index of A and B (stable radix sort by row; quadtree keys are monotone in the
 //      column for a fixed row, so each row comes out k-ascending),
 //   2. k_sym_count:    per row i -> #distinct j, #triples,
 //   3. k_sym_emit_c:   per row i -> C keys in j order + per-C triple counts,
@@ -24,35 +24,43 @@ constexpr int kWin = 4096;   // j-window of the per-row accumulator (slots)
 constexpr int kNT = 256;     // threads per row CTA
 constexpr int kPer = kWin / kNT;
 
-__global__ void k_decode_rows(const uint64_t *keys, int64_t n, int nbl, int lbits, uint32_t *row,
-                              uint32_t *col, uint32_t *iota) {
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+// Row keys of both operands in one array: A entry t -> row(t), B entry t -> nbg + row(t); the
+// value carried through the sort is the entry's index within its own operand.
+__global__ void k_decode_rows(const uint64_t *a_keys, int64_t nA, const uint64_t *b_keys, int64_t nB,
+                              int64_t nbg, int nbl, int lbits, uint32_t *rowkey, uint32_t *val) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nA + nB;
        x += (int64_t)gridDim.x * blockDim.x) {
+    const bool is_b = x >= nA;
+    const int64_t t = is_b ? x - nA : x;
     uint32_t bi, bj;
-    qkey_decode(keys[x], nbl, lbits, &bi, &bj);
-    row[x] = bi;
-    col[x] = bj;
-    iota[x] = (uint32_t)x;
+    qkey_decode(is_b ? b_keys[t] : a_keys[t], nbl, lbits, &bi, &bj);
+    rowkey[x] = bi + (is_b ? (uint32_t)nbg : 0u);
+    val[x] = (uint32_t)t;
   }
 }
 
-// rp[r] = first position in the sorted row array with row >= r, r in [0, nbg].
-__global__ void k_row_ptr(const uint32_t *srow, int64_t n, int64_t nbg, uint32_t *rp) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= nbg;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    int64_t lo = 0, hi = n;
-    while (lo < hi) {
-      int64_t mid = (lo + hi) >> 1;
-      if ((int64_t)srow[mid] < r) lo = mid + 1; else hi = mid;
+// After the stable sort by row key: column of every sorted entry (x < n), and the row pointers
+// rp[r] = first sorted position with row key >= r, r in [0, 2*nbg] (A rows, then B rows).
+__global__ void k_cols_rowptr(const uint64_t *a_keys, const uint64_t *b_keys, const uint32_t *srow,
+                              const uint32_t *perm, int64_t n, int64_t nbg, int nbl, int lbits,
+                              uint32_t *scol, uint32_t *rp) {
+  const int64_t span = n > 2 * nbg + 1 ? n : 2 * nbg + 1;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < span;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    if (x < n) {
+      uint32_t bi, bj;
+      qkey_decode(((int64_t)srow[x] < nbg ? a_keys : b_keys)[perm[x]], nbl, lbits, &bi, &bj);
+      scol[x] = bj;
     }
-    rp[r] = (uint32_t)lo;
+    if (x <= 2 * nbg) {
+      int64_t lo = 0, hi = n;
+      while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)srow[mid] < x) lo = mid + 1; else hi = mid;
+      }
+      rp[x] = (uint32_t)lo;
+    }
   }
-}
-
-__global__ void k_gather_u32(const uint32_t *src, const uint32_t *idx, int64_t n, uint32_t *dst) {
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
-       x += (int64_t)gridDim.x * blockDim.x)
-    dst[x] = src[idx[x]];
 }
 
 // ---- block-level reductions / scans (deterministic, fixed order) ------------------------------
@@ -152,10 +160,11 @@ __device__ void for_window_pairs(const RowSpan &s, uint32_t wbase, bool multi, c
 
 __global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const uint32_t *a_scol,
                                                    const uint32_t *b_rp, const uint32_t *b_scol,
-                                                   int64_t nbg, uint32_t *rowC, uint64_t *rowT) {
+                                                   int64_t nbg, uint64_t *cnt) {
   __shared__ uint32_t bm[kWin / 32];
   __shared__ uint64_t red64[32];
   __shared__ uint32_t red32[32];
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt[2 * nbg] = 0;  // exclusive-scan tail
   for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
     RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
     uint32_t total = 0;
@@ -176,8 +185,8 @@ __global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const u
       }
     }
     if (threadIdx.x == 0) {
-      rowC[i] = total;
-      rowT[i] = s.nt;
+      cnt[i] = total;
+      cnt[nbg + i] = s.nt;
     }
     __syncthreads();
   }
@@ -187,7 +196,7 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_c(const uint32_t *a_rp, const 
                                                     const uint32_t *b_rp, const uint32_t *b_scol,
                                                     int64_t nbg, int nbl, int lbits,
                                                     const uint64_t *rowC_off, uint64_t *rm_key,
-                                                    uint32_t *rm_cnt) {
+                                                    uint32_t *rm_cnt, uint32_t *rm_iota) {
   __shared__ uint32_t cnt[kWin];
   __shared__ uint64_t red64[32];
   __shared__ uint32_t red32[32];
@@ -215,6 +224,7 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_c(const uint32_t *a_rp, const 
           if (c) {
             rm_key[out + pos] = qkey((uint32_t)i, wbase + s0 + q, nbl, lbits);
             rm_cnt[out + pos] = c;
+            rm_iota[out + pos] = (uint32_t)(out + pos);
             ++pos;
           }
         }
@@ -289,18 +299,13 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
 
 __global__ void k_inv_counts(const uint32_t *perm, const uint32_t *rm_cnt, int64_t nC, uint32_t *inv,
                              int64_t *cnt_q) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt_q[nC] = 0;  // exclusive-scan tail
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nC;
        p += (int64_t)gridDim.x * blockDim.x) {
     uint32_t c = perm[p];
     inv[c] = (uint32_t)p;
     cnt_q[p] = rm_cnt[c];
   }
-}
-
-__global__ void k_iota(uint32_t *v, int64_t n) {
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
-       x += (int64_t)gridDim.x * blockDim.x)
-    v[x] = (uint32_t)x;
 }
 
 inline int grid_for(int64_t n, int threads = 256) {
@@ -316,37 +321,35 @@ inline int bits_for(uint64_t maxval) {
   return b;
 }
 
-// Workspace of the count phase (persists into the fill phase).
+// Workspace of the count phase (persists into the fill phase). Both operands share one row index:
+// sorted entries [0, nA) are A's rows, [nA, nA+nB) B's; rp has 2*nbg+1 entries (a_rp = rp,
+// b_rp = rp + nbg); positions index scol/perm of either operand directly.
 struct SymWs {
-  uint32_t *a_row, *a_col, *a_iota, *a_srow, *a_perm, *a_scol, *a_rp;
-  uint32_t *b_row, *b_col, *b_iota, *b_srow, *b_perm, *b_scol, *b_rp;
-  uint32_t *rowC;
-  uint64_t *rowT, *rowC_off, *rowT_off;
+  uint32_t *rowkey, *val, *srow, *perm, *scol, *rp;
+  uint64_t *cnt;   // [2*nbg+1]: C blocks per row, triples per row, 0
+  uint64_t *off;   // exclusive scan of cnt: rowC_off = off, nC = off[nbg], nT = off[2nbg] - off[nbg]
   void *cub;
   size_t cub_bytes;
 };
 
-size_t cub_bytes_count(int64_t nmax, int64_t nbg) {
+size_t cub_bytes_count(int64_t n, int64_t nbg) {
   size_t a = 0, b = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, a, (uint32_t *)nullptr, (uint32_t *)nullptr,
-                                  (uint32_t *)nullptr, (uint32_t *)nullptr, (int64_t)nmax, 0, 32);
-  cub::DeviceScan::InclusiveSum(nullptr, b, (uint64_t *)nullptr, (uint64_t *)nullptr, (int64_t)nbg);
+                                  (uint32_t *)nullptr, (uint32_t *)nullptr, (int64_t)n, 0, 32);
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (uint64_t *)nullptr, (uint64_t *)nullptr,
+                                (int64_t)(2 * nbg + 1));
   return std::max(a, b);
 }
 
 SymWs carve_sym(Carver &cv, int64_t nA, int64_t nB, int64_t nbg) {
   SymWs w;
-  w.a_row = cv.take<uint32_t>(nA); w.a_col = cv.take<uint32_t>(nA); w.a_iota = cv.take<uint32_t>(nA);
-  w.a_srow = cv.take<uint32_t>(nA); w.a_perm = cv.take<uint32_t>(nA); w.a_scol = cv.take<uint32_t>(nA);
-  w.a_rp = cv.take<uint32_t>(nbg + 1);
-  w.b_row = cv.take<uint32_t>(nB); w.b_col = cv.take<uint32_t>(nB); w.b_iota = cv.take<uint32_t>(nB);
-  w.b_srow = cv.take<uint32_t>(nB); w.b_perm = cv.take<uint32_t>(nB); w.b_scol = cv.take<uint32_t>(nB);
-  w.b_rp = cv.take<uint32_t>(nbg + 1);
-  w.rowC = cv.take<uint32_t>(nbg);
-  w.rowT = cv.take<uint64_t>(nbg);
-  w.rowC_off = cv.take<uint64_t>(nbg + 1);
-  w.rowT_off = cv.take<uint64_t>(nbg + 1);
-  w.cub_bytes = cub_bytes_count(std::max(nA, nB), nbg);
+  const int64_t n = nA + nB;
+  w.rowkey = cv.take<uint32_t>(n); w.val = cv.take<uint32_t>(n); w.srow = cv.take<uint32_t>(n);
+  w.perm = cv.take<uint32_t>(n); w.scol = cv.take<uint32_t>(n);
+  w.rp = cv.take<uint32_t>(2 * nbg + 1);
+  w.cnt = cv.take<uint64_t>(2 * nbg + 1);
+  w.off = cv.take<uint64_t>(2 * nbg + 1);
+  w.cub_bytes = cub_bytes_count(n, nbg);
   w.cub = cv.take<char>(w.cub_bytes);
   return w;
 }
@@ -366,32 +369,33 @@ FillWs carve_fill(Carver &cv, int64_t nC, int key_bits) {
   w.rm_iota = cv.take<uint32_t>(nC);
   w.perm = cv.take<uint32_t>(nC);
   w.inv = cv.take<uint32_t>(nC);
-  w.cnt_q = cv.take<int64_t>(nC);
+  w.cnt_q = cv.take<int64_t>(nC + 1);
   size_t a = 0, b = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, a, (uint64_t *)nullptr, (uint64_t *)nullptr,
                                   (uint32_t *)nullptr, (uint32_t *)nullptr, (int64_t)nC, 0, key_bits);
-  cub::DeviceScan::InclusiveSum(nullptr, b, (int64_t *)nullptr, (int64_t *)nullptr, (int64_t)nC);
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t *)nullptr, (int64_t *)nullptr, (int64_t)nC + 1);
   w.cub_bytes = std::max(a, b);
   w.cub = cv.take<char>(w.cub_bytes);
   return w;
 }
 
-// Block-row index of one operand: rows sorted stably, columns gathered, row pointers.
-int build_rows(const uint64_t *keys, int64_t n, const Geometry &g, uint32_t *row, uint32_t *col,
-               uint32_t *iota, uint32_t *srow, uint32_t *perm, uint32_t *scol, uint32_t *rp,
-               void *cub, size_t cub_bytes, cudaStream_t st) {
+// Block-row index of both operands: one stable radix sort by row key (quadtree keys are monotone
+// in the column for a fixed row, so every row comes out k-ascending), columns, row pointers.
+int build_rows(const uint64_t *a_keys, int64_t nA, const uint64_t *b_keys, int64_t nB,
+               const Geometry &g, const SymWs &w, cudaStream_t st) {
+  const int64_t n = nA + nB;
   if (n > 0) {
-    k_decode_rows<<<grid_for(n), 256, 0, st>>>(keys, n, g.nbl, g.lbits, row, col, iota);
+    k_decode_rows<<<grid_for(n), 256, 0, st>>>(a_keys, nA, b_keys, nB, g.nbg, g.nbl, g.lbits,
+                                                w.rowkey, w.val);
     QM_LAUNCHED("k_decode_rows");
-    size_t tb = cub_bytes;
-    QM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub, tb, row, srow, iota, perm, n, 0,
-                                                bits_for((uint64_t)(g.nbg - 1)), st));
+    size_t tb = w.cub_bytes;
+    QM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.cub, tb, w.rowkey, w.srow, w.val, w.perm, n, 0,
+                                                bits_for((uint64_t)(2 * g.nbg - 1)), st));
     QM_CUDA_TRY(cudaGetLastError());
-    k_gather_u32<<<grid_for(n), 256, 0, st>>>(col, perm, n, scol);
-    QM_LAUNCHED("k_gather_u32");
   }
-  k_row_ptr<<<grid_for(g.nbg + 1), 256, 0, st>>>(srow, n, g.nbg, rp);
-  QM_LAUNCHED("k_row_ptr");
+  k_cols_rowptr<<<grid_for(std::max<int64_t>(n, 2 * g.nbg + 1)), 256, 0, st>>>(
+      a_keys, b_keys, w.srow, w.perm, n, g.nbg, g.nbl, g.lbits, w.scol, w.rp);
+  QM_LAUNCHED("k_cols_rowptr");
   return QM_OK;
 }
 
@@ -420,7 +424,7 @@ extern "C" int qm_spgemm_count(const qm_layout *layout, const uint64_t *a_keys, 
   Geometry g;
   int rc = make_geometry(layout, &g);
   if (rc != QM_OK) return rc;
-  if (nA < 0 || nB < 0 || nA >= (int64_t)1 << 32 || nB >= (int64_t)1 << 32 || !n_c_out || !n_triples_out) {
+  if (nA < 0 || nB < 0 || nA + nB >= (int64_t)1 << 32 || !n_c_out || !n_triples_out) {
     set_error("qm_spgemm_count: bad sizes or output pointers");
     return QM_ERR_INVALID;
   }
@@ -433,24 +437,17 @@ extern "C" int qm_spgemm_count(const qm_layout *layout, const uint64_t *a_keys, 
   }
   *n_c_out = 0;
   *n_triples_out = 0;
-  rc = build_rows(a_keys, nA, g, w.a_row, w.a_col, w.a_iota, w.a_srow, w.a_perm, w.a_scol, w.a_rp,
-                  w.cub, w.cub_bytes, st);
+  rc = build_rows(a_keys, nA, b_keys, nB, g, w, st);
   if (rc != QM_OK) return rc;
-  rc = build_rows(b_keys, nB, g, w.b_row, w.b_col, w.b_iota, w.b_srow, w.b_perm, w.b_scol, w.b_rp,
-                  w.cub, w.cub_bytes, st);
-  if (rc != QM_OK) return rc;
-  k_sym_count<<<row_grid(g.nbg), kNT, 0, st>>>(w.a_rp, w.a_scol, w.b_rp, w.b_scol, g.nbg, w.rowC,
-                                               w.rowT);
+  const uint32_t *a_rp = w.rp, *b_rp = w.rp + g.nbg;
+  k_sym_count<<<row_grid(g.nbg), kNT, 0, st>>>(a_rp, w.scol, b_rp, w.scol, g.nbg, w.cnt);
   QM_LAUNCHED("k_sym_count");
-  QM_CUDA_TRY(cudaMemsetAsync(w.rowC_off, 0, sizeof(uint64_t), st));
-  QM_CUDA_TRY(cudaMemsetAsync(w.rowT_off, 0, sizeof(uint64_t), st));
   size_t tb = w.cub_bytes;
-  QM_CUDA_TRY(cub::DeviceScan::InclusiveSum(w.cub, tb, w.rowC, w.rowC_off + 1, g.nbg, st));
-  tb = w.cub_bytes;
-  QM_CUDA_TRY(cub::DeviceScan::InclusiveSum(w.cub, tb, w.rowT, w.rowT_off + 1, g.nbg, st));
+  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(w.cub, tb, w.cnt, w.off, 2 * g.nbg + 1, st));
   uint64_t tot[2];
-  rc = read_device_i64(w.rowC_off + g.nbg, 1, (int64_t *)tot, st, w.rowT_off + g.nbg);
+  rc = read_device_i64(w.off + g.nbg, 1, (int64_t *)tot, st, w.off + 2 * g.nbg);
   if (rc != QM_OK) return rc;
+  tot[1] -= tot[0];
   if (tot[0] >= (1ull << 32)) {
     set_error("product has %llu C blocks; this build indexes C with 32 bits", (unsigned long long)tot[0]);
     return QM_ERR_UNSUPPORTED;
@@ -501,20 +498,17 @@ extern "C" int qm_spgemm_fill_keys(const qm_layout *layout, int64_t nA, int64_t 
   int rc = fill_setup(layout, nA, nB, nC, ws, ws_bytes, fill_ws, fill_ws_bytes, &g, &w, &f, &key_bits);
   if (rc != QM_OK) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  QM_CUDA_TRY(cudaMemsetAsync(c_tptr, 0, sizeof(int64_t), st));
-  if (nC == 0) return QM_OK;
-  k_sym_emit_c<<<row_grid(g.nbg), kNT, 0, st>>>(w.a_rp, w.a_scol, w.b_rp, w.b_scol, g.nbg, g.nbl,
-                                                g.lbits, w.rowC_off, f.rm_key, f.rm_cnt);
+  if (nC == 0) return cudaMemsetAsync(c_tptr, 0, sizeof(int64_t), st) == cudaSuccess ? QM_OK : QM_ERR_CUDA;
+  k_sym_emit_c<<<row_grid(g.nbg), kNT, 0, st>>>(w.rp, w.scol, w.rp + g.nbg, w.scol, g.nbg, g.nbl,
+                                                g.lbits, w.off, f.rm_key, f.rm_cnt, f.rm_iota);
   QM_LAUNCHED("k_sym_emit_c");
-  k_iota<<<grid_for(nC), 256, 0, st>>>(f.rm_iota, nC);
-  QM_LAUNCHED("k_iota");
   size_t tb = f.cub_bytes;
   QM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(f.cub, tb, f.rm_key, c_keys, f.rm_iota, f.perm, nC, 0,
                                               key_bits, st));
   k_inv_counts<<<grid_for(nC), 256, 0, st>>>(f.perm, f.rm_cnt, nC, f.inv, f.cnt_q);
   QM_LAUNCHED("k_inv_counts");
   tb = f.cub_bytes;
-  QM_CUDA_TRY(cub::DeviceScan::InclusiveSum(f.cub, tb, f.cnt_q, c_tptr + 1, nC, st));
+  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(f.cub, tb, f.cnt_q, c_tptr, nC + 1, st));
   return QM_OK;
 }
 
@@ -530,8 +524,8 @@ extern "C" int qm_spgemm_fill_triples(const qm_layout *layout, int64_t nA, int64
   if (rc != QM_OK) return rc;
   if (nC == 0 || t_hi <= t_lo) return QM_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  k_sym_emit_tri<<<row_grid(g.nbg), kNT, 0, st>>>(w.a_rp, w.a_scol, w.a_perm, w.b_rp, w.b_scol,
-                                                  w.b_perm, g.nbg, w.rowC_off, f.inv, c_tptr, t_lo,
+  k_sym_emit_tri<<<row_grid(g.nbg), kNT, 0, st>>>(w.rp, w.scol, w.perm, w.rp + g.nbg, w.scol,
+                                                  w.perm, g.nbg, w.off, f.inv, c_tptr, t_lo,
                                                   t_hi, (uint2 *)tri);
   QM_LAUNCHED("k_sym_emit_tri");
   return QM_OK;
