@@ -13,4 +13,5 @@ for _ in range(2):
         with torch.cuda.stream(s1): d.copy_(h, non_blocking=True)
         with torch.cuda.stream(s2): h2.copy_(d2, non_blocking=True)
     c = timed(both)
-print(f"H2D {16/a:.1f} GB/s  D2H {16/b:.1f} GB/s  concurrent {32/c:.1f} GB/s total")
+gb = n * 8 / 1e9
+print(f"H2D {gb/a:.1f} GB/s  D2H {gb/b:.1f} GB/s  concurrent {2*gb/c:.1f} GB/s total")
