@@ -97,6 +97,29 @@ __global__ void k_flags_to_i64(const uint8_t *f, int64_t n, int64_t *out) {
     out[x] = f[x] ? 1 : 0;
 }
 
+// One CTA copies one block: 16-byte vectors, four loads in flight per thread (streaming loads --
+// the source is read once).
+__device__ __forceinline__ void copy_block(const double *__restrict__ s, double *__restrict__ o,
+                                           int64_t elems) {
+  if ((elems & 1) == 0) {
+    const double2 *s2 = reinterpret_cast<const double2 *>(s);
+    double2 *o2 = reinterpret_cast<double2 *>(o);
+    const int64_t n2 = elems / 2, st = blockDim.x;
+    int64_t e = threadIdx.x;
+    for (; e + 3 * st < n2; e += 4 * st) {
+      const double2 v0 = __ldcs(s2 + e), v1 = __ldcs(s2 + e + st), v2 = __ldcs(s2 + e + 2 * st),
+                    v3 = __ldcs(s2 + e + 3 * st);
+      o2[e] = v0;
+      o2[e + st] = v1;
+      o2[e + 2 * st] = v2;
+      o2[e + 3 * st] = v3;
+    }
+    for (; e < n2; e += st) o2[e] = __ldcs(s2 + e);
+  } else {
+    for (int64_t e = threadIdx.x; e < elems; e += blockDim.x) o[e] = s[e];
+  }
+}
+
 // One CTA per block: copies the kept blocks to their compacted slot.
 __global__ void __launch_bounds__(256) k_compact(int bs, int64_t n, const uint8_t *flags,
                                                  const int64_t *pos, const uint64_t *keys_in,
@@ -111,9 +134,7 @@ __global__ void __launch_bounds__(256) k_compact(int bs, int64_t n, const uint8_
       keys_out[d] = keys_in[m];
       if (sumsq_out) sumsq_out[d] = sumsq_in[m];
     }
-    const double *s = blocks_in + (size_t)m * elems;
-    double *o = blocks_out + (size_t)d * elems;
-    for (int64_t e = threadIdx.x; e < elems; e += blockDim.x) o[e] = s[e];
+    copy_block(blocks_in + (size_t)m * elems, blocks_out + (size_t)d * elems, elems);
   }
 }
 
@@ -121,15 +142,7 @@ __global__ void __launch_bounds__(256) k_gather_blocks(int bs, const double *src
                                                        int64_t n, double *dst) {
   const int64_t elems = (int64_t)bs * bs;
   for (int64_t m = blockIdx.x; m < n; m += gridDim.x) {
-    const double *s = src + (size_t)idx[m] * elems;
-    double *o = dst + (size_t)m * elems;
-    if ((elems & 1) == 0) {
-      const double2 *s2 = reinterpret_cast<const double2 *>(s);
-      double2 *o2 = reinterpret_cast<double2 *>(o);
-      for (int64_t e = threadIdx.x; e < elems / 2; e += blockDim.x) o2[e] = s2[e];
-    } else {
-      for (int64_t e = threadIdx.x; e < elems; e += blockDim.x) o[e] = s[e];
-    }
+    copy_block(src + (size_t)idx[m] * elems, dst + (size_t)m * elems, elems);
   }
 }
 

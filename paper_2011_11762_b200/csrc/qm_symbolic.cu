@@ -236,61 +236,89 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_c(const uint32_t *a_rp, const 
   }
 }
 
+// Triples of C row i at their final positions. A entries are taken 32 at a time (a group): every
+// pair (A entry x, B entry y) of the group sets bit x-x0 of its C column's slot mask, so the rank of
+// a pair among the C block's triples is the cursor plus the set bits below its own -- k order is
+// kept without serialising over the A entries.
+constexpr int kWinT = 2048;
+constexpr int kPerT = kWinT / kNT;  // 8 slots per thread: a byte of one bitmap word
+static_assert(kPerT == 8, "slot ownership assumes 8 slots per thread");
+
 __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
     const uint32_t *a_rp, const uint32_t *a_scol, const uint32_t *a_perm, const uint32_t *b_rp,
     const uint32_t *b_scol, const uint32_t *b_perm, int64_t nbg, const uint64_t *rowC_off,
     const uint32_t *inv, const int64_t *c_tptr, int64_t t_lo, int64_t t_hi, uint2 *tri) {
-  __shared__ union {
-    uint32_t cnt[kWin];
-    int64_t cur[kWin];
-  } u;
+  __shared__ uint32_t mask[kWinT];
+  __shared__ int64_t cur[kWinT];
+  __shared__ uint32_t bm[kWinT / 32];
   __shared__ uint64_t red64[32];
   __shared__ uint32_t red32[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kNT >> 5;
+  const int s0 = threadIdx.x * kPerT;
   for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
     RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
     if (s.nt > 0) {
       uint64_t out = rowC_off[i];
-      const bool multi = (s.jmax - s.jmin) >= (uint32_t)kWin;
-      for (uint64_t wb = s.jmin; wb <= s.jmax; wb += kWin) {
+      const bool multi = (s.jmax - s.jmin) >= (uint32_t)kWinT;
+      for (uint64_t wb = s.jmin; wb <= s.jmax; wb += kWinT) {
         const uint32_t wbase = (uint32_t)wb;
-        const uint32_t wend = wbase + kWin;
-        for (int w = threadIdx.x; w < kWin; w += blockDim.x) u.cnt[w] = 0u;
+        const uint32_t wend = wbase + kWinT;
+        if (threadIdx.x < kWinT / 32) bm[threadIdx.x] = 0u;
         __syncthreads();
-        for_window_pairs(s, wbase, multi, a_scol, b_rp, b_scol,
-                         [&](uint32_t, uint32_t, uint32_t j) { atomicAdd(&u.cnt[j - wbase], 1u); });
-        __syncthreads();
-        const int s0 = threadIdx.x * kPer;
-        uint32_t flags = 0, mine = 0;
-#pragma unroll
-        for (int q = 0; q < kPer; ++q)
-          if (u.cnt[s0 + q]) { flags |= 1u << q; ++mine; }
-        uint32_t total;
-        uint32_t pos = block_exclusive_scan(mine, &total, red32);  // contains __syncthreads
-        __syncthreads();  // every thread has read its cnt slots; the union now becomes cursors
-#pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-          if (flags & (1u << q)) {
-            u.cur[s0 + q] = c_tptr[inv[out + pos]];
-            ++pos;
-          }
-        }
-        __syncthreads();
-        // k ascending: A row entries one at a time; within one entry every column j is distinct,
-        // so each cursor slot is bumped by at most one thread per step.
-        for (uint32_t x = s.a0; x < s.a1; ++x) {
-          const uint32_t k = a_scol[x];
-          const uint32_t ai = a_perm[x];
+        // occupied C columns of the window
+        for (uint32_t x = s.a0 + warp; x < s.a1; x += nw) {
+          uint32_t k = a_scol[x];
           uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
           if (multi) b0 = lower_bound_col(b_scol, b0, b1, wbase);
-          for (uint32_t y = b0 + threadIdx.x; y < b1; y += blockDim.x) {
+          for (uint32_t y = b0 + lane; y < b1; y += 32) {
             uint32_t j = b_scol[y];
             if (j >= wend) break;
-            int64_t p = u.cur[j - wbase]++;
-            if (p >= t_lo && p < t_hi) tri[p - t_lo] = make_uint2(ai, b_perm[y]);
+            atomicOr(&bm[(j - wbase) >> 5], 1u << ((j - wbase) & 31));
+          }
+        }
+        __syncthreads();
+        const uint32_t occ = (bm[s0 >> 5] >> (s0 & 31)) & 0xffu;
+        uint32_t total;
+        uint32_t pos = block_exclusive_scan((uint32_t)__popc(occ), &total, red32);
+#pragma unroll
+        for (int q = 0; q < kPerT; ++q)
+          if (occ & (1u << q)) cur[s0 + q] = c_tptr[inv[out + pos++]];
+        for (uint32_t x0 = s.a0; x0 < s.a1; x0 += 32) {
+          const uint32_t xe = min(x0 + 32u, s.a1);
+#pragma unroll
+          for (int q = 0; q < kPerT; ++q) mask[s0 + q] = 0u;
+          __syncthreads();
+          for (uint32_t x = x0 + warp; x < xe; x += nw) {
+            uint32_t k = a_scol[x];
+            uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
+            if (multi) b0 = lower_bound_col(b_scol, b0, b1, wbase);
+            for (uint32_t y = b0 + lane; y < b1; y += 32) {
+              uint32_t j = b_scol[y];
+              if (j >= wend) break;
+              atomicOr(&mask[j - wbase], 1u << (x - x0));
+            }
           }
           __syncthreads();
+          for (uint32_t x = x0 + warp; x < xe; x += nw) {
+            const uint32_t k = a_scol[x];
+            const uint32_t ai = a_perm[x];
+            const uint32_t below = (1u << (x - x0)) - 1u;
+            uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
+            if (multi) b0 = lower_bound_col(b_scol, b0, b1, wbase);
+            for (uint32_t y = b0 + lane; y < b1; y += 32) {
+              uint32_t j = b_scol[y];
+              if (j >= wend) break;
+              const int64_t p = cur[j - wbase] + __popc(mask[j - wbase] & below);
+              if (p >= t_lo && p < t_hi) tri[p - t_lo] = make_uint2(ai, b_perm[y]);
+            }
+          }
+          __syncthreads();
+#pragma unroll
+          for (int q = 0; q < kPerT; ++q)
+            if (occ & (1u << q)) cur[s0 + q] += __popc(mask[s0 + q]);
         }
         out += total;
+        __syncthreads();
       }
     }
     __syncthreads();
