@@ -263,6 +263,7 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
     if (mt < 0) break;
     const uint8_t *sa = smem + (size_t)s * Cfg::STAGE_BYTES;
     const uint8_t *sb = sa + Cfg::A_BYTES;
+    uint64_t dep = 0;
 #pragma unroll
     for (int kb = 0; kb < Cfg::KSP; ++kb) {
       const uint8_t *pa = sa + kb * Cfg::A_SP_BYTES + wm0 * 128;
@@ -277,21 +278,23 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
           const int col = wn0 + n * 8;
           bf[n] = *(const double *)(pb + (col >> 4) * Cfg::B_SP_BYTES + boff[j][(col & 15) >> 3]);
         }
+        if (kb == Cfg::KSP - 1 && j == 3) {
+          // The stage's last fragment loads: the release below depends on their values.
+#pragma unroll
+          for (int i = 0; i < MT; ++i) dep |= (uint64_t)__double_as_longlong(af[i]);
+#pragma unroll
+          for (int n = 0; n < NT; ++n) dep |= (uint64_t)__double_as_longlong(bf[n]);
+        }
 #pragma unroll
         for (int i = 0; i < MT; ++i)
 #pragma unroll
           for (int n = 0; n < NT; ++n) dmma(acc[i][n][0], acc[i][n][1], af[i], bf[n]);
       }
     }
-    // Release the stage only after every DMMA of the stage has completed: the arrive's address
-    // carries a data dependency on all accumulators (masked by zmask, a runtime zero). Without it
-    // ptxas hoists the arrive above trailing DMMAs, and under DMMA-pipe contention (2 CTAs/SM) a
-    // queued DMMA was observed to pick up fragment registers already reloaded for the next stage.
-    uint64_t dep = 0;
-#pragma unroll
-    for (int i = 0; i < MT; ++i)
-#pragma unroll
-      for (int n = 0; n < NT; ++n) dep |= (uint64_t)__double_as_longlong(acc[i][n][0]);
+    // Release the stage once every fragment of it is in registers: the arrive's address carries a
+    // data dependency on the stage's last shared-memory loads (masked by zmask, a runtime zero), so
+    // it cannot be hoisted above them; the DMMAs themselves read registers only, so the warp does
+    // not drain its DMMA queue before releasing.
     dep &= zmask;
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s] + (uint32_t)dep);
