@@ -147,6 +147,11 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         return lib
 
 
+def last_error() -> str:
+    """The calling thread's last libqmb200 error message."""
+    return (load().qm_last_error() or b"").decode(errors="replace")
+
+
 def check(rc: int, what: str) -> None:
     """Map a qm_status onto the reference's exception types."""
     if rc == QM_OK:

@@ -24,7 +24,9 @@ with a test backend); ``LocalComm`` is the single-rank case.
 
 from __future__ import annotations
 
+import os
 import time
+import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -32,7 +34,7 @@ import torch
 
 from . import spgemm
 from .blocks import BlockSet
-from .errors import ContractViolationError
+from .errors import ConfigurationError, ContractViolationError
 
 
 class Comm:
@@ -208,7 +210,11 @@ class PeerPools:
     the pool's offset in it; the handles are all-gathered through the process group and every
     peer handle is opened once (qm_ipc_open, peer access over NVLink on a multi-GPU node; on a
     single GPU the "peers" are other processes sharing it). ``close`` unmaps before the caller's
-    barrier, so no rank frees a pool another rank still maps."""
+    barrier, so no rank frees a pool another rank still maps.
+
+    Failures to export or map (no peer access between two GPUs, IPC unsupported) do not raise:
+    they leave ``ok`` False, and ``multiply`` agrees on the mode across ranks before any kernel
+    runs (every rank falls back to the exchange when one cannot map its peers)."""
 
     def __init__(self, comm, pools):
         import ctypes
@@ -217,6 +223,8 @@ class PeerPools:
 
         lib = _ffi.load()
         self.lib, self.rank = lib, comm.rank
+        self.ok, self.error = True, ""
+        self._opened = {}
         mine = []
         for t in pools:
             if t.numel() == 0:
@@ -224,11 +232,13 @@ class PeerPools:
                 continue
             h = ctypes.create_string_buffer(64)
             off = ctypes.c_int64(0)
-            _ffi.check(lib.qm_ipc_export(_ffi.ptr(t), h, ctypes.byref(off)), "qm_ipc_export")
+            if lib.qm_ipc_export(_ffi.ptr(t), h, ctypes.byref(off)) != 0:
+                self.ok, self.error = False, _ffi.last_error()
+                mine.append(None)
+                continue
             mine.append((h.raw, int(off.value), int(t.shape[0])))
         every = [None] * comm.world
         comm.dist.all_gather_object(every, mine, group=comm.group)
-        self._opened = {}
         self.ptrs = [[0] * comm.world for _ in pools]
         self.counts = [[0] * comm.world for _ in pools]
         bs = int(pools[0].shape[1])
@@ -246,7 +256,10 @@ class PeerPools:
                 handle, off, n = e
                 if handle not in self._opened:
                     base = ctypes.c_void_p(0)
-                    _ffi.check(lib.qm_ipc_open(handle, ctypes.byref(base)), "qm_ipc_open")
+                    if lib.qm_ipc_open(handle, ctypes.byref(base)) != 0:
+                        self.ok, self.error = False, _ffi.last_error()
+                        self.ptrs[p_i][r], self.counts[p_i][r] = _ffi.ptr(self._dummy), 1
+                        continue
                     self._opened[handle] = int(base.value)
                 self.ptrs[p_i][r] = self._opened[handle] + off
                 self.counts[p_i][r] = n
@@ -288,7 +301,7 @@ FP64_TFLOPS = 35.0   # sustained numeric-kernel rate used by the mode heuristic
 
 
 def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b_is_a: bool = False,
-             timer=None, mode: str = "auto"):
+             timer=None, mode: str | None = None):
     """This rank's part of C = A*B. `a_local`/`b_local` are the rank's owned key ranges (ascending
     across ranks). Returns (C blocks of this rank's C key range, DistStats).
 
@@ -296,11 +309,15 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     mode "fused":    no exchange; the numeric kernel's TMA producer reads remote blocks directly
                      from their owners' pools (PeerPools, CUDA IPC over NVLink), overlapped with
                      the math (qm_numeric_pools).
+    mode None:       $QM_DIST_MODE, default "auto".
     mode "auto":     fused when its estimated NVLink time (every remote block reference is a
                      remote read: peer loads bypass the local L2) stays under a quarter of the
                      estimated compute time, else exchange (heavy reuse of remote blocks, e.g.
                      random patterns)."""
     backend = backend or CudaBackend()
+    mode = mode or os.environ.get("QM_DIST_MODE", "auto")
+    if mode not in ("auto", "exchange", "fused"):
+        raise ConfigurationError(f"unknown distributed mode {mode!r} (auto, exchange, fused)")
     stats = DistStats(rank=comm.rank, world=comm.world)
     clock = timer or (lambda: time.perf_counter())
     t0 = clock()
@@ -340,9 +357,19 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
         remote_refs = int(((own_a != comm.rank).sum() + (own_b != comm.rank).sum()).item())
         fused_s = remote_refs * blk_bytes / (NVLINK_GBS * 1e9)
         compute_s = 2.0 * bs ** 3 * (hi - lo) / (FP64_TFLOPS * 1e12)
+        pools = None
         if mode == "fused" or fused_s <= 0.25 * compute_s:
             comm.barrier()  # pools are complete on every rank before anyone maps them
             pools = PeerPools(comm, [a_local.blocks] if b_is_a else [a_local.blocks, b_local.blocks])
+            if comm.allreduce_max(0.0 if pools.ok else 1.0, dev) > 0.0:
+                # some rank cannot map its peers' pools: every rank takes the exchange path
+                if not pools.ok:
+                    warnings.warn(f"rank {comm.rank}: fused mode unavailable ({pools.error}); "
+                                  "using the halo exchange", RuntimeWarning, stacklevel=2)
+                pools.close()
+                comm.barrier()
+                pools = None
+        if pools is not None:
             tri_packed = torch.stack([pa_idx, pb_idx], dim=1).to(torch.int32).reshape(-1).contiguous()
             c_tptr_local = (c_tptr[m0:m1 + 1] - lo).contiguous()
             try:

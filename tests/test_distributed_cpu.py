@@ -68,7 +68,15 @@ CASES = {
 }
 
 
-def _worker(rank, world, port, case, outdir):
+class NoPoolsBackend(OracleBackend):
+    """Offers the fused path, which must not run: on a host without peer-mappable device memory
+    PeerPools cannot export, and every rank has to agree on the exchange instead."""
+
+    def numeric_pools(self, *args, **kwargs):
+        raise AssertionError("fused kernel launched although a rank could not map its peers")
+
+
+def _worker(rank, world, port, case, outdir, mode="auto"):
     import torch.distributed as dist
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
@@ -82,7 +90,17 @@ def _worker(rank, world, port, case, outdir):
     lb = BlockSet(torch.from_numpy(kb[qb[rank]:qb[rank + 1]]), torch.from_numpy(bb[qb[rank]:qb[rank + 1]]),
                   torch.zeros(0))
     comm = D.Comm()
-    c, st = D.multiply(comm, make_layout(geom.params, geom.bs), la, lb, backend=OracleBackend(geom))
+    backend = NoPoolsBackend(geom) if mode == "fused" else OracleBackend(geom)
+    if mode == "fused":
+        import warnings
+
+        with warnings.catch_warnings(record=True) as w:
+            warnings.simplefilter("always")
+            c, st = D.multiply(comm, make_layout(geom.params, geom.bs), la, lb, backend=backend, mode=mode)
+        assert st.mode == "exchange"
+        assert any("fused mode unavailable" in str(x.message) for x in w)
+    else:
+        c, st = D.multiply(comm, make_layout(geom.params, geom.bs), la, lb, backend=backend)
     keys, _ = comm.allgather_varlen(c.keys)
     flat, _ = comm.allgather_varlen(c.blocks.reshape(-1))
     recv = torch.tensor([st.bytes_received, st.t_range[1] - st.t_range[0]], dtype=torch.int64)
@@ -109,6 +127,16 @@ def test_distributed_product_equals_single_process(tmp_path, world, case):
     assert per_rank_triples.sum() == T == int(out["nt"])
     assert per_rank_triples.max() - per_rank_triples.min() <= 2 * 32  # balanced by triples (+- one C row of work)
     assert out["recv"][:, 0].sum() > 0  # halo blocks crossed ranks
+
+
+def test_fused_mode_falls_back_on_every_rank_when_pools_cannot_be_mapped(tmp_path):
+    mp.spawn(_worker, args=(2, _free_port(), "banded", str(tmp_path), "fused"), nprocs=2, join=True)
+    out = np.load(tmp_path / "out.npz")
+    cfg = CASES["banded"]
+    geom, (ka, ba), (kb, bb) = G.config_operands_host(cfg)
+    kc, bc, _ = O.multiply(O.Geom(cfg.n, cfg.bs, cfg.bs), ka, ba, kb, bb)
+    np.testing.assert_array_equal(out["keys"], kc)
+    np.testing.assert_array_equal(out["blocks"].reshape(bc.shape), bc)
 
 
 def test_partition_bounds_are_balanced_and_monotone():
