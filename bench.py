@@ -412,6 +412,10 @@ def run_ours(args):
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
+        from paper_2011_11762_b200 import distributed as D
+
+        D.release_peer_mappings()
+        dist.barrier()
         dist.destroy_process_group()
 
 

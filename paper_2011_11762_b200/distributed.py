@@ -24,6 +24,7 @@ with a test backend); ``LocalComm`` is the single-rank case.
 
 from __future__ import annotations
 
+import atexit
 import os
 import time
 import warnings
@@ -72,6 +73,14 @@ class Comm:
         self.dist.all_gather(outs, pad, group=self.group)
         return self._out(torch.cat([o[:c] for o, c in zip(outs, counts)]), dev), counts
 
+    def allgather_fixed(self, t: torch.Tensor) -> torch.Tensor:
+        """[world, *t.shape]: every rank's tensor of the same shape, in rank order."""
+        dev = t.device
+        t = self._in(t)
+        outs = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(outs, t, group=self.group)
+        return self._out(torch.stack(outs), dev)
+
     def alltoallv(self, send: torch.Tensor, send_counts: list[int]) -> tuple[torch.Tensor, list[int]]:
         """Rows send[sum(send_counts[:d]) : ...] go to rank d; returns received rows (source rank
         order) and the per-source counts."""
@@ -103,6 +112,9 @@ class LocalComm:
 
     def allgather_varlen(self, t):
         return t, [int(t.shape[0])]
+
+    def allgather_fixed(self, t):
+        return t.unsqueeze(0)
 
     def alltoallv(self, send, send_counts):
         return send, list(send_counts)
@@ -203,14 +215,39 @@ def partition(c_tptr: torch.Tensor, world: int) -> tuple[list[int], list[int]]:
     return cb, [int(x) for x in tb]
 
 
+# CUDA IPC mappings of peer pools, kept across products (opening a handle costs far more than a
+# product's bookkeeping): handle bytes -> mapped base address in this process, plus the handles
+# each (process group, peer rank) used last, so mappings a peer no longer exports are closed.
+_IPC_MAPPED: dict[bytes, int] = {}
+_IPC_BY_PEER: dict[tuple, set] = {}
+_REC = 88  # per pool record: 64-byte handle, int64 offset, int64 block count, valid flag (+pad)
+
+
+def release_peer_mappings():
+    """Closes every cached peer-pool mapping of this process (call before tearing down the
+    process group; also registered atexit)."""
+    from . import _ffi
+
+    if not _IPC_MAPPED:
+        return
+    lib = _ffi.load()
+    for base in _IPC_MAPPED.values():
+        lib.qm_ipc_close(base)
+    _IPC_MAPPED.clear()
+    _IPC_BY_PEER.clear()
+
+
+atexit.register(release_peer_mappings)
+
+
 class PeerPools:
     """Block pools of every rank, mapped into this GPU's address space for the fused kernel.
 
     Each rank exports (qm_ipc_export) the CUDA IPC handle of the allocation holding its pool and
-    the pool's offset in it; the handles are all-gathered through the process group and every
-    peer handle is opened once (qm_ipc_open, peer access over NVLink on a multi-GPU node; on a
-    single GPU the "peers" are other processes sharing it). ``close`` unmaps before the caller's
-    barrier, so no rank frees a pool another rank still maps.
+    the pool's offset in it; the fixed-size records are all-gathered in one collective and every
+    peer handle is opened once per process (qm_ipc_open, peer access over NVLink on a multi-GPU
+    node; on a single GPU the "peers" are other processes sharing it) and cached: repeated products
+    on the same pools map nothing new. A cached mapping is closed when its peer stops exporting it.
 
     Failures to export or map (no peer access between two GPUs, IPC unsupported) do not raise:
     they leave ``ok`` False, and ``multiply`` agrees on the mode across ranks before any kernel
@@ -224,52 +261,58 @@ class PeerPools:
         lib = _ffi.load()
         self.lib, self.rank = lib, comm.rank
         self.ok, self.error = True, ""
-        self._opened = {}
-        mine = []
-        for t in pools:
+        dev = pools[0].device
+        rec = np.zeros((len(pools), _REC), dtype=np.uint8)
+        for p_i, t in enumerate(pools):
             if t.numel() == 0:
-                mine.append(None)
                 continue
             h = ctypes.create_string_buffer(64)
             off = ctypes.c_int64(0)
             if lib.qm_ipc_export(_ffi.ptr(t), h, ctypes.byref(off)) != 0:
                 self.ok, self.error = False, _ffi.last_error()
-                mine.append(None)
                 continue
-            mine.append((h.raw, int(off.value), int(t.shape[0])))
-        every = [None] * comm.world
-        comm.dist.all_gather_object(every, mine, group=comm.group)
+            rec[p_i, :64] = np.frombuffer(h.raw, dtype=np.uint8)
+            rec[p_i, 64:80] = np.array([off.value, t.shape[0]], dtype=np.int64).view(np.uint8)
+            rec[p_i, 80] = 1
+        every = comm.allgather_fixed(torch.from_numpy(rec.reshape(-1)).to(dev))
+        every = every.cpu().numpy().reshape(comm.world, len(pools), _REC)
         self.ptrs = [[0] * comm.world for _ in pools]
         self.counts = [[0] * comm.world for _ in pools]
         bs = int(pools[0].shape[1])
-        self._dummy = torch.zeros((1, bs, bs), dtype=torch.float64, device=pools[0].device)
-        for r, entries in enumerate(every):
-            for p_i, e in enumerate(entries):
+        self._dummy = torch.zeros((1, bs, bs), dtype=torch.float64, device=dev)
+        gkey = id(comm.group)
+        for r in range(comm.world):
+            used = set()
+            for p_i in range(len(pools)):
                 if r == comm.rank:
                     t = pools[p_i]
                     self.ptrs[p_i][r] = _ffi.ptr(t) if t.numel() else _ffi.ptr(self._dummy)
                     self.counts[p_i][r] = max(int(t.shape[0]), 1)
                     continue
-                if e is None:
-                    self.ptrs[p_i][r], self.counts[p_i][r] = _ffi.ptr(self._dummy), 1
+                e = every[r, p_i]
+                self.ptrs[p_i][r], self.counts[p_i][r] = _ffi.ptr(self._dummy), 1
+                if not e[80]:
                     continue
-                handle, off, n = e
-                if handle not in self._opened:
-                    base = ctypes.c_void_p(0)
-                    if lib.qm_ipc_open(handle, ctypes.byref(base)) != 0:
+                handle = e[:64].tobytes()
+                off, n = (int(x) for x in e[64:80].view(np.int64))
+                base = _IPC_MAPPED.get(handle)
+                if base is None:
+                    out = ctypes.c_void_p(0)
+                    if lib.qm_ipc_open(handle, ctypes.byref(out)) != 0:
                         self.ok, self.error = False, _ffi.last_error()
-                        self.ptrs[p_i][r], self.counts[p_i][r] = _ffi.ptr(self._dummy), 1
                         continue
-                    self._opened[handle] = int(base.value)
-                self.ptrs[p_i][r] = self._opened[handle] + off
-                self.counts[p_i][r] = n
+                    base = _IPC_MAPPED[handle] = int(out.value)
+                used.add(handle)
+                self.ptrs[p_i][r], self.counts[p_i][r] = base + off, n
+            if r != comm.rank:
+                for h in _IPC_BY_PEER.get((gkey, r), set()) - used:
+                    base = _IPC_MAPPED.pop(h, None)
+                    if base is not None:
+                        lib.qm_ipc_close(base)
+                _IPC_BY_PEER[(gkey, r)] = used
 
     def close(self):
-        from . import _ffi
-
-        for base in self._opened.values():
-            _ffi.check(self.lib.qm_ipc_close(base), "qm_ipc_close")
-        self._opened = {}
+        """Mappings stay cached for the next product (release_peer_mappings closes them)."""
 
 
 def _pack_owner(idx: torch.Tensor, offsets: torch.Tensor):
@@ -359,7 +402,9 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
         compute_s = 2.0 * bs ** 3 * (hi - lo) / (FP64_TFLOPS * 1e12)
         pools = None
         if mode == "fused" or fused_s <= 0.25 * compute_s:
-            comm.barrier()  # pools are complete on every rank before anyone maps them
+            if dev.type == "cuda":
+                torch.cuda.synchronize(dev)  # this rank's pools are written (any stream) ...
+            comm.barrier()  # ... on every rank, before anyone reads them
             pools = PeerPools(comm, [a_local.blocks] if b_is_a else [a_local.blocks, b_local.blocks])
             if comm.allreduce_max(0.0 if pools.ok else 1.0, dev) > 0.0:
                 # some rank cannot map its peers' pools: every rank takes the exchange path
@@ -379,7 +424,7 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
                 torch.cuda.synchronize(dev)
             finally:
                 pools.close()
-            comm.barrier()  # every rank has finished reading and unmapping the others' pools
+            comm.barrier()  # every rank has finished reading the others' pools
             t4 = clock()
             stats.n_c_local = c.n
             stats.mode = "fused"

@@ -45,6 +45,11 @@ def _worker(rank, world, port, cfg_name, outdir, mode="exchange"):
     comm = D.Comm()
     c, st = D.multiply(comm, layout, parts[0], parts[1], mode=mode)
     assert st.mode == mode
+    if mode == "fused":  # a repeated product reuses the cached peer mappings and is bitwise equal
+        mapped = dict(D._IPC_MAPPED)
+        c2, st2 = D.multiply(comm, layout, parts[0], parts[1], mode=mode)
+        assert st2.mode == "fused" and D._IPC_MAPPED == mapped
+        assert torch.equal(c2.keys, c.keys) and torch.equal(c2.blocks, c.blocks)
     keys, _ = comm.allgather_varlen(c.keys)
     blocks, _ = comm.allgather_varlen(c.blocks.reshape(-1))
     info = torch.tensor([st.bytes_received, st.t_range[1] - st.t_range[0]], dtype=torch.int64)
@@ -59,6 +64,7 @@ def _worker(rank, world, port, cfg_name, outdir, mode="exchange"):
                  if blocks.numel() == ref.blocks.numel() else False,
                  info=torch.stack(allinfo).numpy())
     torch.cuda.synchronize()
+    D.release_peer_mappings()
     dist.barrier()
     dist.destroy_process_group()
 
