@@ -14,8 +14,12 @@ ses = MatrixSession(device="cuda:0")
 for leaf, bs in ((128, 16), (128, 32), (128, 64), (64, 64)):
     a = ses.matrix_from_triplets(n, rows, cols, vals, leaf_dim=leaf, block_size=bs)
     for _ in range(2): ses.multiply(a, a)
-    torch.cuda.synchronize(); t = time.perf_counter()
-    for _ in range(5): c = ses.multiply(a, a)
-    torch.cuda.synchronize(); dt = (time.perf_counter() - t) / 5
+    ts = []
+    for _ in range(8):
+        torch.cuda.synchronize(); t = time.perf_counter()
+        c = ses.multiply(a, a)
+        torch.cuda.synchronize(); ts.append(time.perf_counter() - t)
+    dt = sorted(ts)[len(ts) // 2]
+    print("  per call ms:", " ".join(f"{x*1e3:.2f}" for x in ts))
     f = ses.last_multiply.flops
     print(f"leaf {leaf} bs {bs}: triples {ses.last_multiply.n_triples} {dt*1e3:.2f} ms  {f/dt/1e12:.2f} TFLOP/s")
