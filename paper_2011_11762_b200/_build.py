@@ -60,6 +60,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
     nvcc = nvcc_path()
     OBJ_DIR.mkdir(parents=True, exist_ok=True)
     extra = ["-Xptxas", "-v"] if ptxas_info else []
+    extra += os.environ.get("QM_NVCC_EXTRA", "").split()  # experiments only (e.g. -DQM_EXP_...)
 
     def compile_one(src: Path) -> tuple[Path, str]:
         obj = OBJ_DIR / (src.stem + ".o")
