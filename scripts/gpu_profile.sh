@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 timeout 900 python bench.py > gpurun_out/bench_default_$TAG.log 2>&1; echo "bench default rc=$?"; tail -1 gpurun_out/bench_default_$TAG.log | cut -c1-300
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference_$TAG.log 2>&1; echo "bench reference rc=$?"; tail -1 gpurun_out/bench_reference_$TAG.log | cut -c1-200
 for C in C1 C2-16384 C2-32768 C2-65536 C2-131072 C3 C4 C5-32 C5-64 C5-128; do
-  timeout 600 python bench.py --config $C --steps 5 --warmup 2 --no-e2e --no-cpu > gpurun_out/bench_${TAG}_$C.log 2>&1; echo "bench $C rc=$?"
+  timeout 600 python bench.py --config $C --steps 10 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench_${TAG}_$C.log 2>&1; echo "bench $C rc=$?"
 done
 CMD="python bench.py --config C2-131072 --steps 2 --warmup 1 --no-e2e --no-cpu"
 $CMD > gpurun_out/ncu_plain_$TAG.log 2>&1 && \

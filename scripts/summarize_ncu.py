@@ -16,7 +16,7 @@ from collections import defaultdict
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
-STEP_KERNELS = ("k_decode_rows", "k_row_ptr", "k_gather_u32", "k_sym_", "k_inv_counts", "k_iota",
+STEP_KERNELS = ("k_decode_rows", "k_row_ptr", "k_gather_u32", "k_cols_rowptr", "k_sym_", "k_combine", "k_inv_counts", "k_iota",
                 "k_numeric", "k_block_stats", "k_flags", "k_compact", "DeviceRadixSort", "DeviceScan",
                 "Onesweep", "Histogram", "ExclusiveSum", "cub::", "vectorized_elementwise",
                 "elementwise")
