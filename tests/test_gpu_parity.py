@@ -112,10 +112,12 @@ def test_device_generator_matches_numpy_streams(bs, n, pattern):
 
 
 @pytest.mark.parametrize("kind,n,bs,per_row", [
-    ("banded", 4096, 64, 0), ("random", 8192, 64, 8), ("random", 1 << 17, 16, 8), ("banded", 3000, 8, 0)])
+    ("banded", 4096, 64, 0), ("random", 8192, 64, 8), ("random", 1 << 17, 16, 8), ("banded", 3000, 8, 0),
+    ("random", 1 << 17, 16, 64)])
 def test_symbolic_phase_matches_oracle_exactly(ses, kind, n, bs, per_row):
     """Triples, their grouping and k order (block_sparse.py:121-129) equal the oracle's; the
-    random 8192-wide grid exercises the multi-window accumulator (window 4096 columns)."""
+    random 8192-wide grid exercises the multi-window accumulator (window 4096 columns), rows with
+    more than 32 A entries the grouped triple emission (32 A entries per group)."""
     cfg = G.BaselineConfig("t", kind, n, bs, half_bw=300, per_row=per_row)
     geom = cfg.geometry
     ka, kb = G.config_keys(cfg, 0), G.config_keys(cfg, 1)
@@ -132,6 +134,35 @@ def test_symbolic_phase_matches_oracle_exactly(ses, kind, n, bs, per_row):
     tri = plan.tri.cpu().numpy().view(np.uint32).reshape(-1, 2).astype(np.int64)
     np.testing.assert_array_equal(tri[:, 0], ta)
     np.testing.assert_array_equal(tri[:, 1], tb)
+
+
+@pytest.mark.parametrize("case", ["a_empty", "b_empty", "no_match"])
+def test_symbolic_c_abi_degenerate_operands(ses, case):
+    """qm_spgemm_count straight through the C ABI: an empty operand, or operands whose inner
+    indices never meet, give nC = nT = 0 (the nil product, ops.py:244-245)."""
+    import ctypes
+
+    lib = _ffi.load()
+    geom = Geometry(MatrixParams.create(4096, 64), 64)
+    layout = _ffi.make_layout(geom.params, 64)
+    enc = lambda bi, bj: torch.from_numpy(geom.qkey(np.array(list(bi)), np.array(list(bj))))
+    if case == "no_match":  # A uses inner columns 0..3, B only inner rows 10..13
+        ka, kb = enc(range(4), range(4)), enc(range(10, 14), range(4))
+    else:
+        ka, kb = enc(range(8), range(8)), enc(range(8), range(8))
+        if case == "a_empty":
+            ka = ka[:0]
+        else:
+            kb = kb[:0]
+    ka, kb = ka.sort().values.to(ses.device), kb.sort().values.to(ses.device)
+    ws_n = lib.qm_spgemm_workspace_bytes(ctypes.byref(layout), ka.numel(), kb.numel())
+    ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device=ses.device)
+    nc, nt = ctypes.c_int64(-1), ctypes.c_int64(-1)
+    st = torch.cuda.current_stream().cuda_stream
+    rc = lib.qm_spgemm_count(ctypes.byref(layout), ka.data_ptr(), ka.numel(), kb.data_ptr(), kb.numel(),
+                             ws.data_ptr(), ws_n, ctypes.byref(nc), ctypes.byref(nt), st)
+    assert rc == 0, _ffi.last_error()
+    assert nc.value == 0 and nt.value == 0
 
 
 def test_identity_multiply_is_bit_exact(ses):
