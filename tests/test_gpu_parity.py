@@ -68,6 +68,24 @@ def test_integer_product_is_bit_exact(ses):
     assert c.root.blockset.blocks.sum().item() == G.flop_count_exact(case) // 2
 
 
+@pytest.mark.parametrize("case,leaf,bs", [
+    (("banded", 3000, 37, 0, 0, 0), 64, 16),
+    (("growing_block", 2048, 20, 300, 0, 0), 128, 32),
+    (("random_blocks", 4096, 16, 200, 6, 3), 128, 64),
+    (("random_blocks", 1500, 8, 100, 4, 9), 96, 32),
+])
+def test_generated_families_sum_to_half_the_flop_count(ses, case, leaf, bs):
+    """Known-answer test (generators.py:134-138, oracles.py:106-109): on the
+    reference's value-1.0 families, every C entry counts scalar products, so sum(C) is exactly
+    flop_count_exact / 2 and every C value is an integer."""
+    c_ = G.ExperimentCase(*case)
+    a = G.generate(ses.store, c_, leaf, "block_sparse", bs)
+    c = ses.multiply(a, a)
+    blocks = c.root.blockset.blocks
+    assert blocks.sum().item() == G.flop_count_exact(c_) // 2
+    assert torch.equal(blocks, blocks.round())
+
+
 @pytest.mark.parametrize("name", ["C1", "C3s", "C4s", "C2-16384"])
 def test_configs_match_reference(ses, name):
     g = helpers.load(name)
