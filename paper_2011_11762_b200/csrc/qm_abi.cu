@@ -355,16 +355,17 @@ extern "C" int qm_read_i64(const int64_t *dev_src, int32_t n, int64_t *host_out,
 // ---- CUDA IPC for the fused multi-GPU product: a block pool is exported as the IPC handle of its
 // ---- allocation plus the pool's byte offset inside it (torch's caching allocator sub-allocates).
 extern "C" int qm_ipc_export(const void *ptr, void *handle_out /*64 bytes*/, int64_t *offset_out) {
-  static PFN_cuMemGetAddressRange_v3020 get_range = nullptr;
-  if (!get_range) {
+  static const PFN_cuMemGetAddressRange_v3020 get_range = [] {  // thread-safe one-time lookup
     void *fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !fn) {
-      set_error("qm_ipc_export: cuMemGetAddressRange unavailable");
-      return QM_ERR_CUDA;
-    }
-    get_range = (PFN_cuMemGetAddressRange_v3020)fn;
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return (PFN_cuMemGetAddressRange_v3020)fn;
+  }();
+  if (!get_range) {
+    set_error("qm_ipc_export: cuMemGetAddressRange unavailable");
+    return QM_ERR_CUDA;
   }
   CUdeviceptr base = 0;
   size_t size = 0;

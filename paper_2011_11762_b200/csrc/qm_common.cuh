@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/qmb200.h"
 
 namespace qm {
@@ -39,6 +41,36 @@ void note_launch(int n = 1);
       return QM_ERR_CUDA;                                                                   \
     }                                                                                       \
   } while (0)
+
+// Once-per-device initialisation (cudaFuncSetAttribute applies to the current device only, so a
+// process driving several GPUs must configure each). f() returns a qm_status; a failure is retried
+// on the next call. Devices are tracked in a 64-bit mask (ordinal & 63).
+struct PerDeviceOnce {
+  std::atomic<uint64_t> done{0};
+  template <class F>
+  int run(F f) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return 0;
+    const int rc = f();
+    if (rc == 0) done.fetch_or(bit, std::memory_order_acq_rel);
+    return rc;
+  }
+};
+
+// SM count of the current device (cached per device).
+inline int device_sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  int n = cache[dev & 63].load(std::memory_order_relaxed);
+  if (n <= 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev & 63].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
 
 // Derived geometry of a qm_layout.
 struct Geometry {

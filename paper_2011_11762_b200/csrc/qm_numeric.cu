@@ -291,27 +291,20 @@ __global__ void __launch_bounds__(256) k_block_stats(const double *__restrict__ 
   }
 }
 
-int g_sm_count = 0;
 
-int sm_count() {
-  if (g_sm_count == 0) {
-    int dev = 0, n = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    g_sm_count = n > 0 ? n : 148;
-  }
-  return g_sm_count;
-}
+
+int sm_count() { return device_sm_count(); }
 
 template <class Cfg>
 int launch_dmma(const double *A, const double *B, const uint2 *tri, const int64_t *tptr, int64_t nC,
                 double *C, double *csq, uint8_t *cnz, int64_t *zc, cudaStream_t st) {
-  static bool configured = false;  // benign race: idempotent attribute set
-  if (!configured) {
+  static PerDeviceOnce once;
+  int rc = once.run([]() -> int {
     QM_CUDA_TRY(cudaFuncSetAttribute(k_numeric_dmma<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)Cfg::SMEM));
-    configured = true;
-  }
+    return (int)QM_OK;
+  });
+  if (rc != QM_OK) return rc;
   int per_sm = 0;
   QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_numeric_dmma<Cfg>, Cfg::NTHR,
                                                             Cfg::SMEM));

@@ -356,14 +356,14 @@ __global__ void k_combine_tiles(const double *part_sq, const uint8_t *part_nz, i
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {  // thread-safe one-time lookup
     void *p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
-  }
+      return (PFN_cuTensorMapEncodeTiled_v12000)p;
+    return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+  }();
   return fn;
 }
 
@@ -388,16 +388,7 @@ int make_map(CUtensorMap *m, const double *base, int64_t nblocks, int bs, int bo
   return QM_OK;
 }
 
-int sm_count_tma() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int sm_count_tma() { return device_sm_count(); }
 
 // Workspace: the work counter (256 B), then per-warp partial norms / nonzero flags of every tile.
 template <class Cfg>
@@ -440,12 +431,13 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
     rc = make_map(&maps.b[i], B[i < nb ? i : 0], nB[i < nb ? i : 0], Cfg::BS, Cfg::KP);
     if (rc != QM_OK) return rc;
   }
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce once;
+  int rc = once.run([]() -> int {
     QM_CUDA_TRY(cudaFuncSetAttribute(k_numeric_tma<Cfg, NPOOL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)Cfg::SMEM));
-    configured = true;
-  }
+    return (int)QM_OK;
+  });
+  if (rc != QM_OK) return rc;
   int per_sm = 0;
   QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_numeric_tma<Cfg, NPOOL>, Cfg::NTHR,
                                                             Cfg::SMEM));
