@@ -228,7 +228,11 @@ def numeric(geom: Geom, c_keys, c_ptr, tri_a, tri_b, tri_k, a_blocks, b_blocks,
         return keys_out, blocks_out
 
     if threads > 1:
-        with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        # one BLAS thread per worker: the workers already use every core, and nested BLAS
+        # threading only oversubscribes them (measured ~2x slower)
+        from threadpoolctl import threadpool_limits
+
+        with threadpool_limits(limits=1, user_api="blas"), cf.ThreadPoolExecutor(max_workers=threads) as ex:
             parts = list(ex.map(run, bounds))
     else:
         parts = [run(b) for b in bounds]
