@@ -186,16 +186,43 @@ QM_API int qm_transpose_blocks(int32_t block_size, const double *src, int64_t n,
 
 /* ---- add / scale / add_scaled_identity (the step after a product) ---------- */
 /* out[m] = alpha*A[ia[m]] + beta*B[ib[m]] per block, an operand absent when its index is -1;
- * exact IEEE products and sum (BlockSparseLeaf.add / scale, block_sparse.py:134-160). */
+ * exact IEEE products and sum (BlockSparseLeaf.add / scale, block_sparse.py:134-160). Optional
+ * (NULL = skip) fused statistics of each output block, bit-identical to qm_block_stats on `out`:
+ * sum of squares, nonzero flag, and the count of exactly-zero blocks added to *zero_count. */
 QM_API int qm_axpby_blocks(int32_t block_size, int64_t n, const int64_t *ia, const int64_t *ib,
                            double alpha, double beta, const double *a_blocks, const double *b_blocks,
-                           double *out, void *stream);
+                           double *out, double *out_sumsq, uint8_t *out_nonzero, int64_t *zero_count,
+                           void *stream);
 /* Diagonal blocks of A + c*I with the reference's two leaf cases (ops.py:253-345): mode 0 =
  * A_blk + c*eye, mode 1 = A_blk + identity-from-triplets (logical diagonal only); ia = -1 when the
  * A block is absent, bi = block row. */
 QM_API int qm_add_identity_blocks(int32_t block_size, int64_t n, const int64_t *ia, const int64_t *bi,
                                   const int8_t *mode, double c, int64_t n_logical,
                                   const double *a_blocks, double *out, void *stream);
+
+/* ---- approximate multiply: the reference's norm-based pruning ------------- */
+/* Node norms of every quadtree level of one operand (the store's id-carried norms,
+ * quadtree.py:138-140, block_sparse.py:91-92): level L (0 = root .. depth) occupies
+ * codes/norms[L*n, L*n + counts[L]) (caller arrays of (depth+1)*n entries; counts on the host),
+ * codes = Morton node codes ascending. Synchronises the stream once per level. */
+QM_API size_t qm_node_norms_workspace_bytes(int64_t n);
+QM_API int qm_node_norms(const qm_layout *layout, const uint64_t *keys, const double *sumsq, int64_t n,
+                         uint64_t *codes, double *norms, int64_t *counts, void *ws, size_t ws_bytes,
+                         void *stream);
+/* One level of the pruned task recursion (ops.py:197-241 with tau, ops.py:232): the 8 child pairs
+ * of every parent pair (packed I<<42 | K<<21 | J; level 0: the root pair, parents unused), kept
+ * when both operand nodes exist (a_sym/b_sym: lower nodes read their stored upper mirror;
+ * b_transposed: B node (K,J) is stored node (J,K); upper: I <= J). Pairs with
+ * norm(A node)*norm(B node) < tau_l are pruned: their bounds go to pruned_out (the prune log,
+ * engine.py:273-275); the others to alive_out. Outputs hold up to 8*n_parents entries; counts are
+ * returned on the host (synchronises the stream). */
+QM_API size_t qm_prune_level_workspace_bytes(int64_t n_parents);
+QM_API int qm_prune_level(const qm_layout *layout, int32_t level, double tau_l, const uint64_t *parents,
+                          int64_t n_parents, const uint64_t *a_codes, const double *a_norms, int64_t a_count,
+                          int32_t a_sym, const uint64_t *b_codes, const double *b_norms, int64_t b_count,
+                          int32_t b_sym, int32_t b_transposed, int32_t upper, uint64_t *alive_out,
+                          double *pruned_out, int64_t *n_alive, int64_t *n_pruned, void *ws,
+                          size_t ws_bytes, void *stream);
 
 /* ---- synthetic inputs (device side of the block-keyed generator) -------- */
 /* For each key, fills the block with numpy's default_rng([seed, matrix_id, bi, bj]).uniform(-1, 1,

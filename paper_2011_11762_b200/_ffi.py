@@ -55,6 +55,10 @@ EXPORTS = (
     "qm_transpose_blocks",
     "qm_axpby_blocks",
     "qm_add_identity_blocks",
+    "qm_node_norms_workspace_bytes",
+    "qm_node_norms",
+    "qm_prune_level_workspace_bytes",
+    "qm_prune_level",
     "qm_generate_blocks",
     "qm_fp64_peak_kernel",
 )
@@ -112,8 +116,15 @@ _SIGS = {
     "qm_block_stats": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P]),
     "qm_gather_blocks": (ctypes.c_int, [_I32, _P, _P, _I64, _P, _P]),
     "qm_transpose_blocks": (ctypes.c_int, [_I32, _P, _I64, _P, _P]),
-    "qm_axpby_blocks": (ctypes.c_int, [_I32, _I64, _P, _P, ctypes.c_double, ctypes.c_double, _P, _P, _P, _P]),
+    "qm_axpby_blocks": (ctypes.c_int, [_I32, _I64, _P, _P, ctypes.c_double, ctypes.c_double, _P, _P, _P, _P,
+                                       _P, _P, _P]),
     "qm_add_identity_blocks": (ctypes.c_int, [_I32, _I64, _P, _P, _P, ctypes.c_double, _I64, _P, _P, _P]),
+    "qm_node_norms_workspace_bytes": (_SZ, [_I64]),
+    "qm_node_norms": (ctypes.c_int, [_LP, _P, _P, _I64, _P, _P, ctypes.POINTER(_I64), _P, _SZ, _P]),
+    "qm_prune_level_workspace_bytes": (_SZ, [_I64]),
+    "qm_prune_level": (ctypes.c_int, [_LP, _I32, ctypes.c_double, _P, _I64, _P, _P, _I64, _I32, _P, _P, _I64,
+                                      _I32, _I32, _I32, _P, _P, ctypes.POINTER(_I64), ctypes.POINTER(_I64),
+                                      _P, _SZ, _P]),
     "qm_generate_blocks": (ctypes.c_int, [_LP, _P, _I64, ctypes.c_uint64, ctypes.c_uint32, _I32,
                                           _I64, _P, _P, _P]),
     "qm_fp64_peak_kernel": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _I64, _P,

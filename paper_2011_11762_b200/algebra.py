@@ -28,16 +28,21 @@ def _stream(dev):
     return _ffi.stream_handle(torch.cuda.current_stream(dev))
 
 
-def _drop_zero_blocks(bs: int, c: BlockSet) -> BlockSet:
+def _drop_zero_blocks(bs: int, c: BlockSet, nz: torch.Tensor | None = None,
+                      zero_count: torch.Tensor | None = None) -> BlockSet:
+    """Drops exactly-zero blocks (_set_block). `nz`/`zero_count` come fused from qm_axpby_blocks;
+    otherwise qm_block_stats computes them (and c.sumsq)."""
     from .spgemm import compact
 
     if c.n == 0:
         return c
     lib = _ffi.load()
-    nz = torch.empty(c.n, dtype=torch.uint8, device=c.device)
-    _ffi.check(lib.qm_block_stats(bs, c.n, _ffi.ptr(c.blocks), _ffi.ptr(c.sumsq), _ffi.ptr(nz),
-                                  _stream(c.device)), "qm_block_stats")
-    n_zero = _ffi.read_i64((nz == 0).sum().reshape(1).to(torch.int64))
+    if nz is None:
+        nz = torch.empty(c.n, dtype=torch.uint8, device=c.device)
+        _ffi.check(lib.qm_block_stats(bs, c.n, _ffi.ptr(c.blocks), _ffi.ptr(c.sumsq), _ffi.ptr(nz),
+                                      _stream(c.device)), "qm_block_stats")
+        zero_count = (nz == 0).sum().reshape(1).to(torch.int64)
+    n_zero = _ffi.read_i64(zero_count)
     return compact(bs, c, nz, n_zero)
 
 
@@ -53,14 +58,20 @@ def _member(sorted_vals: torch.Tensor, q: torch.Tensor) -> torch.Tensor:
 
 
 def _axpby(bs, ia, ib, alpha, beta, A, B, out_keys) -> BlockSet:
+    """alpha*A[ia] + beta*B[ib] with the output's norms and zero flags fused; exact-zero blocks
+    dropped."""
     lib = _ffi.load()
     n = int(ia.shape[0])
     dev = out_keys.device
     out = torch.empty((n, bs, bs), dtype=torch.float64, device=dev)
+    sumsq = torch.empty(n, dtype=torch.float64, device=dev)
+    nz = torch.empty(n, dtype=torch.uint8, device=dev)
+    zc = torch.zeros(1, dtype=torch.int64, device=dev)
     _ffi.check(lib.qm_axpby_blocks(bs, n, _ffi.ptr(ia.contiguous()), _ffi.ptr(ib.contiguous()), alpha,
-                                   beta, _ffi.ptr(A), _ffi.ptr(B), _ffi.ptr(out), _stream(dev)),
+                                   beta, _ffi.ptr(A), _ffi.ptr(B), _ffi.ptr(out), _ffi.ptr(sumsq),
+                                   _ffi.ptr(nz), _ffi.ptr(zc), _stream(dev)),
                "qm_axpby_blocks")
-    return BlockSet(out_keys.contiguous(), out, torch.empty(n, dtype=torch.float64, device=dev))
+    return _drop_zero_blocks(bs, BlockSet(out_keys.contiguous(), out, sumsq), nz, zc)
 
 
 def add(geom: Geometry, a: BlockSet, b: BlockSet, alpha: float, beta: float) -> BlockSet:
@@ -86,15 +97,14 @@ def add(geom: Geometry, a: BlockSet, b: BlockSet, alpha: float, beta: float) -> 
         if beta == 0.0:
             keep &= ~(_member(lb, lk) & ~_member(la, lk))
         keys, ia, ib = keys[keep], ia[keep], ib[keep]
-    out = _axpby(bs, ia, ib, alpha, beta, a.blocks, b.blocks, keys)
-    return _drop_zero_blocks(bs, out)
+    return _axpby(bs, ia, ib, alpha, beta, a.blocks, b.blocks, keys)
 
 
 def scale(geom: Geometry, a: BlockSet, alpha: float) -> BlockSet:
     """alpha*A (alpha not in {0, 1}; those are identity / nil at the caller, ops.py:172-185)."""
     ia = torch.arange(a.n, device=a.device)
     ib = torch.full_like(ia, -1)
-    return _drop_zero_blocks(geom.bs, _axpby(geom.bs, ia, ib, alpha, 0.0, a.blocks, a.blocks, a.keys))
+    return _axpby(geom.bs, ia, ib, alpha, 0.0, a.blocks, a.blocks, a.keys)
 
 
 def add_scaled_identity(geom: Geometry, a: BlockSet | None, c: float, device) -> BlockSet:

@@ -8,12 +8,14 @@ skipped. Node norms are the store's id-carried Frobenius norms (quadtree.py:138-
 symmetric operand they are the norms of the *stored* (upper) chunks, and virtual SW children reuse
 the NE chunk (ops.py:100-116).
 
-B200 form: the prune decisions are made level by level on the compressed node structure (torch
-on the device): level-l node norms are segment sums of the per-block squared norms over the
-quadtree-key order (every node is a contiguous key range); the pairs reached at level l are the
-unpruned pairs of level l-1 expanded to their 8 child pairs where both child nodes exist; pruned
-pairs go to the log. The surviving leaf pairs then filter the regular symbolic phase's triples,
-and the numeric kernel runs unchanged on the kept triples (k order preserved).
+B200 form (csrc/qm_prune.cu): qm_node_norms builds every level's node table of an operand
+bottom-up from the block sums of squares (nodes are runs of equal Morton codes in quadtree-key
+order; sqrt of the compensated sum of the children's squared norms, like the reference's
+sqrt(fsum(...))); qm_prune_level expands the surviving pairs of level l-1 to their 8 child pairs,
+looks both operand nodes up (a symmetric operand's lower nodes read their stored upper mirror),
+classifies each pair dead / pruned / alive and compacts the alive pairs and the pruned bounds (the
+log). The surviving leaf pairs then filter the regular symbolic phase's triples, and the numeric
+kernel runs unchanged on the kept triples (k order preserved).
 """
 
 from __future__ import annotations
@@ -22,6 +24,7 @@ from dataclasses import dataclass, field
 
 import torch
 
+from . import _ffi
 from .blocks import BlockSet
 from .layout import Geometry
 
@@ -40,80 +43,70 @@ def _coords(geom: Geometry, keys: torch.Tensor):
     return bi.to(torch.int64), bj.to(torch.int64)
 
 
-class _Nodes:
-    """Nodes of one operand at one level: sorted codes r*W + c and norms (stored-chunk norms)."""
+def _node_tables(geom: Geometry, s: BlockSet, lay):
+    """Every level's (Morton codes, norms, count) of one operand (qm_node_norms)."""
+    import ctypes
 
-    def __init__(self, r, c, sumsq, width, sym: bool):
-        code = r * width + c
-        order = torch.argsort(code, stable=True)
-        code, sq = code[order], sumsq[order]
-        uniq, inv = torch.unique_consecutive(code, return_inverse=True)
-        acc = torch.zeros(uniq.shape[0], dtype=torch.float64, device=code.device)
-        acc.index_add_(0, inv, sq)
-        self.width, self.sym = width, sym
-        if sym:  # add the virtual lower nodes (r > c) as mirrors of the stored upper ones
-            ur, uc = uniq // width, uniq % width
-            up = ur < uc
-            mcode = uc[up] * width + ur[up]
-            allc = torch.cat([uniq, mcode])
-            alln = torch.cat([acc, acc[up]])
-            o = torch.argsort(allc)
-            uniq, acc = allc[o], alln[o]
-        self.code = uniq
-        self.norm = torch.sqrt(acc)
-
-    def lookup(self, r, c):
-        """(exists mask, norms) for node coordinates."""
-        q = r * self.width + c
-        pos = torch.searchsorted(self.code, q).clamp(max=max(self.code.shape[0] - 1, 0))
-        hit = self.code[pos] == q if self.code.shape[0] else torch.zeros_like(q, dtype=torch.bool)
-        return hit, torch.where(hit, self.norm[pos], torch.zeros_like(self.norm[pos]))
+    lib = _ffi.load()
+    n = s.n
+    L = geom.params.depth + 1
+    dev = s.keys.device
+    codes = torch.empty(max(L * n, 1), dtype=torch.int64, device=dev)
+    norms = torch.empty(max(L * n, 1), dtype=torch.float64, device=dev)
+    counts = (ctypes.c_int64 * L)()
+    wb = lib.qm_node_norms_workspace_bytes(n)
+    ws = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
+    _ffi.check(lib.qm_node_norms(ctypes.byref(lay), _ffi.ptr(s.keys), _ffi.ptr(s.sumsq), n, _ffi.ptr(codes),
+                                 _ffi.ptr(norms), counts, _ffi.ptr(ws), wb,
+                                 _ffi.stream_handle(torch.cuda.current_stream(dev))), "qm_node_norms")
+    return [(codes[l * n:], norms[l * n:], int(counts[l])) for l in range(L)]
 
 
 def prune(geom: Geometry, a: BlockSet, b: BlockSet, tau: float, a_sym: bool = False, b_sym: bool = False,
           b_transposed: bool = False, upper: bool = False) -> PruneResult:
-    """Level-by-level prune decisions of the reference's task recursion (regular algebra on the
-    logical operands op(A) = A or expand(A), op(B) = B, expand(B) or B^T)."""
-    depth = geom.params.depth
-    nbl = geom.nbl
-    ar, ac = _coords(geom, a.keys)
-    br, bc = _coords(geom, b.keys)
-    if b_transposed:  # logical B = stored B^T: node (K, J) of B^T is node (J, K) of B
-        br, bc = bc, br
+    """Level-by-level prune decisions of the reference's task recursion on the device
+    (qm_node_norms + qm_prune_level) for the logical operands op(A) = A or expand(A),
+    op(B) = B, expand(B) or B^T; node norms are those of the stored chunks."""
+    import ctypes
+
     res = PruneResult()
+    if a.n == 0 or b.n == 0:
+        return res
+    lib = _ffi.load()
+    depth = geom.params.depth
     dev = a.keys.device
-    surv = None  # (I, K, J) at the previous level
+    lay = _ffi.make_layout(geom.params, geom.bs)
+    ta, tb = _node_tables(geom, a, lay), _node_tables(geom, b, lay)
+    sh = _ffi.stream_handle(torch.cuda.current_stream(dev))
+    parents = torch.zeros(1, dtype=torch.int64, device=dev)
+    n_par = 0
+    logs = []
     for lev in range(depth + 1):
-        shift_blocks = nbl << (depth - lev)  # blocks per node side at this level
-        width = 1 << lev
-        na = _Nodes(ar // shift_blocks, ac // shift_blocks, a.sumsq, width, a_sym)
-        nb = _Nodes(br // shift_blocks, bc // shift_blocks, b.sumsq, width, b_sym)
-        if lev == 0:
-            if na.code.numel() == 0 or nb.code.numel() == 0:
-                return res
-            I = K = J = torch.zeros(1, dtype=torch.int64, device=dev)
-        else:
-            d = torch.arange(8, device=dev)
-            I = (2 * surv[0][:, None] + (d >> 2)).reshape(-1)
-            K = (2 * surv[1][:, None] + ((d >> 1) & 1)).reshape(-1)
-            J = (2 * surv[2][:, None] + (d & 1)).reshape(-1)
-        ha, nA = na.lookup(I, K)
-        hb, nB = nb.lookup(K, J)
-        live = ha & hb
-        if upper:
-            live &= I <= J
-        I, K, J, nA, nB = I[live], K[live], J[live], nA[live], nB[live]
-        bound = nA * nB
-        tau_l = tau / (8.0 ** lev)
-        pruned = bound < tau_l
-        res.prune_log.extend(bound[pruned].tolist())
-        keep = ~pruned
-        surv = (I[keep], K[keep], J[keep])
-        res.pairs_per_level.append(int(live.sum().item()))
-        if surv[0].numel() == 0:
-            return res
-    w = 1 << depth
-    res.leaf_pairs = torch.sort((surv[0] * w + surv[1]) * w + surv[2]).values
+        n_cand = 1 if lev == 0 else 8 * n_par
+        alive = torch.empty(n_cand, dtype=torch.int64, device=dev)
+        pruned = torch.empty(n_cand, dtype=torch.float64, device=dev)
+        wb = lib.qm_prune_level_workspace_bytes(max(n_par, 1))
+        ws = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
+        na, npr = ctypes.c_int64(0), ctypes.c_int64(0)
+        (ac, an, acnt), (bc, bn, bcnt) = ta[lev], tb[lev]
+        _ffi.check(lib.qm_prune_level(ctypes.byref(lay), lev, tau / (8.0 ** lev), _ffi.ptr(parents), n_par,
+                                      _ffi.ptr(ac), _ffi.ptr(an), acnt, int(a_sym), _ffi.ptr(bc), _ffi.ptr(bn),
+                                      bcnt, int(b_sym), int(b_transposed), int(upper), _ffi.ptr(alive),
+                                      _ffi.ptr(pruned), ctypes.byref(na), ctypes.byref(npr), _ffi.ptr(ws), wb,
+                                      sh), "qm_prune_level")
+        res.pairs_per_level.append(int(na.value + npr.value))
+        if npr.value:
+            logs.append(pruned[:npr.value])
+        parents, n_par = alive[:na.value], int(na.value)
+        if n_par == 0:
+            break
+    if logs:
+        res.prune_log = torch.cat(logs).tolist()
+    if n_par and len(res.pairs_per_level) == depth + 1:
+        w = 1 << depth
+        mask = (1 << 21) - 1
+        I, K, J = parents >> 42, (parents >> 21) & mask, parents & mask
+        res.leaf_pairs = torch.sort((I * w + K) * w + J).values
     return res
 
 

@@ -170,21 +170,74 @@ __global__ void __launch_bounds__(256) k_transpose_blocks(int bs, const double *
 // out[m] = alpha*A[ia[m]] + beta*B[ib[m]] with an operand absent when its index is -1 (then
 // alpha*A or beta*B alone). Exact IEEE products and sum (no FMA contraction), like numpy's
 // `alpha * a + beta * b` in BlockSparseLeaf.add / scale (block_sparse.py:134-160).
+__device__ __forceinline__ double axpby1(bool ha, bool hb, double alpha, double beta, double a, double b) {
+  if (ha && hb) return __dadd_rn(__dmul_rn(alpha, a), __dmul_rn(beta, b));
+  return ha ? __dmul_rn(alpha, a) : __dmul_rn(beta, b);
+}
+
+// One CTA (256 threads) per output block; thread t handles elements t, t+256, ... with four
+// loads per operand in flight (no FMA contraction: alpha*a + beta*b rounds like numpy's two
+// products and one sum). Optionally fuses the output block's statistics in exactly
+// k_block_stats's order (per-thread fma chain over its elements, warp xor tree, warps in order),
+// so the sum of squares is bit-identical to a separate qm_block_stats pass over the output.
 __global__ void __launch_bounds__(256) k_axpby(int64_t elems, int64_t n, const int64_t *ia,
                                                const int64_t *ib, double alpha, double beta,
-                                               const double *A, const double *B, double *out) {
+                                               const double *A, const double *B, double *out,
+                                               double *sumsq, uint8_t *nonzero, int64_t *zero_count) {
+  __shared__ double red[8];
+  __shared__ int rnz[8];
+  const bool stats = sumsq || nonzero || zero_count;
   for (int64_t m = blockIdx.x; m < n; m += gridDim.x) {
     const int64_t x = ia[m], y = ib[m];
-    const double *a = x >= 0 ? A + (size_t)x * elems : nullptr;
-    const double *b = y >= 0 ? B + (size_t)y * elems : nullptr;
+    const bool ha = x >= 0, hb = y >= 0;
+    const double *a = ha ? A + (size_t)x * elems : nullptr;
+    const double *b = hb ? B + (size_t)y * elems : nullptr;
     double *o = out + (size_t)m * elems;
-    for (int64_t e = threadIdx.x; e < elems; e += blockDim.x) {
-      double v;
-      if (a && b) v = __dadd_rn(__dmul_rn(alpha, a[e]), __dmul_rn(beta, b[e]));
-      else if (a) v = __dmul_rn(alpha, a[e]);
-      else v = __dmul_rn(beta, b[e]);
-      o[e] = v;
+    const int64_t st = blockDim.x;
+    double ss = 0.0;
+    bool nz = false;
+    int64_t e = threadIdx.x;
+    for (; e + 3 * st < elems; e += 4 * st) {
+      double va[4], vb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        va[u] = ha ? a[e + u * st] : 0.0;
+        vb[u] = hb ? b[e + u * st] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double v = axpby1(ha, hb, alpha, beta, va[u], vb[u]);
+        o[e + u * st] = v;
+        ss = fma(v, v, ss);
+        nz |= v != 0.0;
+      }
     }
+    for (; e < elems; e += st) {
+      const double v = axpby1(ha, hb, alpha, beta, ha ? a[e] : 0.0, hb ? b[e] : 0.0);
+      o[e] = v;
+      ss = fma(v, v, ss);
+      nz |= v != 0.0;
+    }
+    if (!stats) continue;
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    const bool wnz = __any_sync(0xffffffffu, nz);
+    if ((threadIdx.x & 31) == 0) {
+      red[threadIdx.x >> 5] = ss;
+      rnz[threadIdx.x >> 5] = wnz;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      int any = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        tot += red[w];
+        any |= rnz[w];
+      }
+      if (sumsq) sumsq[m] = tot;
+      if (nonzero) nonzero[m] = (uint8_t)any;
+      if (!any && zero_count) atomicAdd((unsigned long long *)zero_count, 1ull);
+    }
+    __syncthreads();
   }
 }
 
@@ -320,7 +373,8 @@ extern "C" int qm_transpose_blocks(int32_t block_size, const double *src, int64_
 
 extern "C" int qm_axpby_blocks(int32_t block_size, int64_t n, const int64_t *ia, const int64_t *ib,
                                double alpha, double beta, const double *a_blocks,
-                               const double *b_blocks, double *out, void *stream) {
+                               const double *b_blocks, double *out, double *out_sumsq,
+                               uint8_t *out_nonzero, int64_t *zero_count, void *stream) {
   if (block_size < 1 || n < 0) {
     set_error("qm_axpby_blocks: bad arguments");
     return QM_ERR_INVALID;
@@ -328,7 +382,8 @@ extern "C" int qm_axpby_blocks(int32_t block_size, int64_t n, const int64_t *ia,
   if (n == 0) return QM_OK;
   int64_t grid = std::min<int64_t>(n, 148 * 16);
   k_axpby<<<(int)grid, 256, 0, (cudaStream_t)stream>>>((int64_t)block_size * block_size, n, ia, ib, alpha,
-                                                       beta, a_blocks, b_blocks, out);
+                                                       beta, a_blocks, b_blocks, out, out_sumsq,
+                                                       out_nonzero, zero_count);
   QM_LAUNCHED("k_axpby");
   return QM_OK;
 }

@@ -1,0 +1,269 @@
+// Approximate (norm-pruned) multiply: the reference's prune decisions, level by level, on device.
+//
+// Reference: every multiply task at quadtree level l whose operand nodes X (rows I, cols K) and
+// Y (rows K, cols J) are both non-nil first tests norm(X) * norm(Y) < tau_l (ops.py:199-204) with
+// tau_0 = tau and tau_{l+1} = tau_l / 8 (ops.py:232); a pruned task logs its bound
+// (ctx.log_prune, engine.py:273-275) and returns nil, otherwise it spawns its 8 child products.
+// Node norms are the store's id-carried Frobenius norms: a leaf's is sqrt(fsum(block_norm^2))
+// (block_sparse.py:91-92), a branch's sqrt(fsum(child_norm^2)) (quadtree.py:138-140).
+//
+// B200 form:
+//   qm_node_norms  -- every level's node table of one operand (Morton node code, norm), built
+//                     bottom-up from the block sums of squares: runs of equal codes in quadtree-key
+//                     order are the nodes, summed with compensated (Neumaier) summation in order,
+//                     which rounds like fsum for these short runs of positive terms;
+//   qm_prune_level -- one level of the task recursion: the 8 children of every surviving pair of
+//                     the previous level (or the root pair), node lookups by binary search in the
+//                     tables (stored-chunk norms: a symmetric operand's lower nodes read their
+//                     upper mirror, a transposed operand swaps the coordinates), classification
+//                     dead / pruned / alive, and stream compaction of the alive pairs (packed
+//                     I<<42 | K<<21 | J) and of the pruned bounds (the prune log).
+#include <cub/cub.cuh>
+
+#include "qm_common.cuh"
+
+namespace qm {
+namespace {
+
+constexpr int kPairBits = 21;  // node coordinates of up to 2^21 per side per level
+constexpr uint64_t kPairMask = (1ull << kPairBits) - 1ull;
+
+inline int grid_for(int64_t n, int threads = 256) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)g;
+}
+
+__device__ __forceinline__ void neumaier_add(double &s, double &c, double x) {
+  const double t = s + x;
+  if (fabs(s) >= fabs(x)) c += (s - t) + x;
+  else c += (x - t) + s;
+  s = t;
+}
+
+// head[i] = 1 when code(i) = in[i] >> shift starts a run; head[n] = 0 (exclusive-scan tail).
+__global__ void k_run_heads(const uint64_t *in, int64_t n, int shift, int64_t *head) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x)
+    head[i] = (i < n && (i == 0 || (in[i] >> shift) != (in[i - 1] >> shift))) ? 1 : 0;
+}
+
+__global__ void k_run_starts(const uint64_t *in, int64_t n, int shift, const int64_t *head,
+                             const int64_t *pos, uint64_t *out_code, int64_t *start) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (head[i]) {
+      out_code[pos[i]] = in[i] >> shift;
+      start[pos[i]] = i;
+    }
+}
+
+// norm of run j = sqrt(sum over its members of v^2), v = sqrt(sumsq) for blocks (from_sumsq)
+// or the member's norm for nodes; members summed in key order.
+__global__ void k_run_norms(const double *vals, int from_sumsq, int64_t n_in, const int64_t *start,
+                            int64_t n_runs, double *out_norm) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_runs;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = j + 1 < n_runs ? start[j + 1] : n_in;
+    double s = 0.0, c = 0.0;
+    for (int64_t i = start[j]; i < e; ++i) {
+      const double v = from_sumsq ? sqrt(vals[i]) : vals[i];
+      neumaier_add(s, c, v * v);
+    }
+    out_norm[j] = sqrt(s + c);
+  }
+}
+
+struct Table {
+  const uint64_t *code;
+  const double *norm;
+  int64_t n;
+};
+
+// Norm of node (r, c) (0 when absent). sym: a lower node reads its stored upper mirror.
+__device__ __forceinline__ bool lookup(const Table &t, uint32_t r, uint32_t c, bool sym, double *norm) {
+  if (sym && r > c) {
+    const uint32_t x = r;
+    r = c;
+    c = x;
+  }
+  const uint64_t q = (spread_bits(r) << 1) | spread_bits(c);
+  int64_t lo = 0, hi = t.n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (t.code[mid] < q) lo = mid + 1; else hi = mid;
+  }
+  if (lo < t.n && t.code[lo] == q) {
+    *norm = t.norm[lo];
+    return true;
+  }
+  return false;
+}
+
+// Candidate x: child (x % 8) of parent x / 8 (or the root pair). status: 0 dead, 1 pruned, 2 alive.
+__global__ void k_prune_expand(const uint64_t *parents, int64_t n_cand, int root, Table ta, int a_sym,
+                               Table tb, int b_sym, int b_transposed, int upper, double tau_l,
+                               uint64_t *cand, double *bound, uint8_t *alive, uint8_t *pruned) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n_cand;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t I = 0, K = 0, J = 0;
+    if (!root) {
+      const uint64_t p = parents[x >> 3];
+      const uint32_t d = (uint32_t)(x & 7);
+      I = 2 * (uint32_t)(p >> (2 * kPairBits)) + (d >> 2);
+      K = 2 * (uint32_t)((p >> kPairBits) & kPairMask) + ((d >> 1) & 1u);
+      J = 2 * (uint32_t)(p & kPairMask) + (d & 1u);
+    }
+    double na = 0.0, nb = 0.0;
+    bool live = lookup(ta, I, K, a_sym, &na);
+    if (live) live = b_transposed ? lookup(tb, J, K, b_sym, &nb) : lookup(tb, K, J, b_sym, &nb);
+    if (upper && I > J) live = false;
+    const double bd = na * nb;
+    const bool pr = live && bd < tau_l;
+    cand[x] = ((uint64_t)I << (2 * kPairBits)) | ((uint64_t)K << kPairBits) | J;
+    bound[x] = bd;
+    alive[x] = (uint8_t)(live && !pr);
+    pruned[x] = (uint8_t)pr;
+  }
+}
+
+size_t select_bytes(int64_t n) {
+  size_t a = 0, b = 0;
+  cub::DeviceSelect::Flagged(nullptr, a, (uint64_t *)nullptr, (uint8_t *)nullptr, (uint64_t *)nullptr,
+                             (int64_t *)nullptr, n);
+  cub::DeviceSelect::Flagged(nullptr, b, (double *)nullptr, (uint8_t *)nullptr, (double *)nullptr,
+                             (int64_t *)nullptr, n);
+  return std::max(a, b);
+}
+
+size_t scan_bytes(int64_t n) {
+  size_t b = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t *)nullptr, (int64_t *)nullptr, n);
+  return b;
+}
+
+}  // namespace
+}  // namespace qm
+
+using namespace qm;
+
+extern "C" size_t qm_node_norms_workspace_bytes(int64_t n) {
+  Carver cv(nullptr, 0);
+  cv.take<int64_t>(n + 1);  // head
+  cv.take<int64_t>(n + 1);  // pos
+  cv.take<int64_t>(n + 1);  // start
+  cv.take<char>(scan_bytes(n + 1));
+  return cv.off;
+}
+
+extern "C" int qm_node_norms(const qm_layout *layout, const uint64_t *keys, const double *sumsq, int64_t n,
+                             uint64_t *codes, double *norms, int64_t *counts, void *ws, size_t ws_bytes,
+                             void *stream) {
+  Geometry g;
+  int rc = make_geometry(layout, &g);
+  if (rc != QM_OK) return rc;
+  if (n < 0 || !counts || (n > 0 && (!keys || !sumsq || !codes || !norms))) {
+    set_error("qm_node_norms: bad arguments");
+    return QM_ERR_INVALID;
+  }
+  if (g.depth >= kPairBits) {
+    set_error("qm_node_norms: depth %d exceeds %d", g.depth, kPairBits - 1);
+    return QM_ERR_UNSUPPORTED;
+  }
+  Carver cv(ws, ws_bytes);
+  int64_t *head = cv.take<int64_t>(n + 1), *pos = cv.take<int64_t>(n + 1), *start = cv.take<int64_t>(n + 1);
+  const size_t sb = scan_bytes(n + 1);
+  void *cub = cv.take<char>(sb);
+  if (!cv.ok() || !ws) {
+    set_error("qm_node_norms: workspace %zu < required %zu", ws_bytes, cv.off);
+    return QM_ERR_WORKSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  // Level L (root 0 .. depth) occupies codes/norms [L*n, L*n + counts[L]); built bottom-up: the
+  // leaves from the blocks (code = key >> 2*lbits), every level above from the one below (>> 2).
+  const uint64_t *in = keys;
+  const double *vals = sumsq;
+  int64_t n_in = n;
+  int shift = 2 * g.lbits, from_sumsq = 1;
+  for (int L = g.depth; L >= 0; --L) {
+    if (n_in == 0) {
+      counts[L] = 0;
+      continue;
+    }
+    uint64_t *oc = codes + (size_t)L * n;
+    double *on = norms + (size_t)L * n;
+    k_run_heads<<<grid_for(n_in + 1), 256, 0, st>>>(in, n_in, shift, head);
+    QM_LAUNCHED("k_run_heads");
+    size_t tb = sb;
+    QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub, tb, head, pos, n_in + 1, st));
+    k_run_starts<<<grid_for(n_in), 256, 0, st>>>(in, n_in, shift, head, pos, oc, start);
+    QM_LAUNCHED("k_run_starts");
+    int64_t runs = 0;
+    rc = read_device_i64(pos + n_in, 1, &runs, st);
+    if (rc != QM_OK) return rc;
+    k_run_norms<<<grid_for(runs), 256, 0, st>>>(vals, from_sumsq, n_in, start, runs, on);
+    QM_LAUNCHED("k_run_norms");
+    counts[L] = runs;
+    in = oc;
+    vals = on;
+    n_in = runs;
+    shift = 2;
+    from_sumsq = 0;
+  }
+  return QM_OK;
+}
+
+extern "C" size_t qm_prune_level_workspace_bytes(int64_t n_parents) {
+  const int64_t n = std::max<int64_t>(n_parents * 8, 1);
+  Carver cv(nullptr, 0);
+  cv.take<uint64_t>(n);  // candidates
+  cv.take<double>(n);    // bounds
+  cv.take<uint8_t>(n);   // alive
+  cv.take<uint8_t>(n);   // pruned
+  cv.take<int64_t>(2);   // selected counts
+  cv.take<char>(select_bytes(n));
+  return cv.off;
+}
+
+extern "C" int qm_prune_level(const qm_layout *layout, int32_t level, double tau_l, const uint64_t *parents,
+                              int64_t n_parents, const uint64_t *a_codes, const double *a_norms,
+                              int64_t a_count, int32_t a_sym, const uint64_t *b_codes, const double *b_norms,
+                              int64_t b_count, int32_t b_sym, int32_t b_transposed, int32_t upper,
+                              uint64_t *alive_out, double *pruned_out, int64_t *n_alive, int64_t *n_pruned,
+                              void *ws, size_t ws_bytes, void *stream) {
+  Geometry g;
+  int rc = make_geometry(layout, &g);
+  if (rc != QM_OK) return rc;
+  if (level < 0 || level > g.depth || n_parents < 0 || !n_alive || !n_pruned || (level > 0 && n_parents == 0)) {
+    set_error("qm_prune_level: bad arguments");
+    return QM_ERR_INVALID;
+  }
+  const int root = level == 0;
+  const int64_t n_cand = root ? 1 : n_parents * 8;
+  Carver cv(ws, ws_bytes);
+  const int64_t cap = std::max<int64_t>(n_cand, 1);
+  uint64_t *cand = cv.take<uint64_t>(cap);
+  double *bound = cv.take<double>(cap);
+  uint8_t *alive = cv.take<uint8_t>(cap), *pruned = cv.take<uint8_t>(cap);
+  int64_t *sel = cv.take<int64_t>(2);
+  const size_t sb = select_bytes(cap);
+  void *cub = cv.take<char>(sb);
+  if (!cv.ok() || !ws) {
+    set_error("qm_prune_level: workspace %zu < required %zu", ws_bytes, cv.off);
+    return QM_ERR_WORKSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  Table ta{a_codes, a_norms, a_count}, tb{b_codes, b_norms, b_count};
+  k_prune_expand<<<grid_for(n_cand), 256, 0, st>>>(parents, n_cand, root, ta, a_sym, tb, b_sym, b_transposed,
+                                                   upper, tau_l, cand, bound, alive, pruned);
+  QM_LAUNCHED("k_prune_expand");
+  size_t t1 = sb;
+  QM_CUDA_TRY(cub::DeviceSelect::Flagged(cub, t1, cand, alive, alive_out, sel, n_cand, st));
+  size_t t2 = sb;
+  QM_CUDA_TRY(cub::DeviceSelect::Flagged(cub, t2, bound, pruned, pruned_out, sel + 1, n_cand, st));
+  int64_t cnt[2];
+  rc = read_device_i64(sel, 2, cnt, st);
+  if (rc != QM_OK) return rc;
+  *n_alive = cnt[0];
+  *n_pruned = cnt[1];
+  return QM_OK;
+}
