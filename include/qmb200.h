@@ -224,6 +224,18 @@ QM_API int qm_prune_level(const qm_layout *layout, int32_t level, double tau_l, 
                           double *pruned_out, int64_t *n_alive, int64_t *n_pruned, void *ws,
                           size_t ws_bytes, void *stream);
 
+/* Keeps the triples of a symbolic plan whose leaf pair (li, lk, lj) is in the sorted
+ * leaf_pairs codes ((li*w + lk)*w + lj, w = 2^depth): the products of pruned subtrees vanish; C
+ * blocks left without triples vanish too (an all-pruned subtree is nil). Order is preserved.
+ * Outputs have the input capacities (nT pairs, nC+1 offsets, nC keys); counts returned on the
+ * host (synchronises the stream). */
+QM_API size_t qm_filter_triples_workspace_bytes(int64_t nC, int64_t nT);
+QM_API int qm_filter_triples(const qm_layout *layout, const uint64_t *a_keys, const uint64_t *b_keys,
+                             int32_t b_transposed, const uint32_t *tri, const int64_t *c_tptr,
+                             const uint64_t *c_keys, int64_t nC, int64_t nT, const uint64_t *leaf_pairs,
+                             int64_t n_pairs, uint32_t *tri_out, int64_t *c_tptr_out, uint64_t *c_keys_out,
+                             int64_t *nC_out, int64_t *nT_out, void *ws, size_t ws_bytes, void *stream);
+
 /* ---- synthetic inputs (device side of the block-keyed generator) -------- */
 /* For each key, fills the block with numpy's default_rng([seed, matrix_id, bi, bj]).uniform(-1, 1,
  * (bs, bs)) -- bit-identical PCG64 + SeedSequence -- then zeroes entries outside the element

@@ -59,6 +59,8 @@ EXPORTS = (
     "qm_node_norms",
     "qm_prune_level_workspace_bytes",
     "qm_prune_level",
+    "qm_filter_triples_workspace_bytes",
+    "qm_filter_triples",
     "qm_generate_blocks",
     "qm_fp64_peak_kernel",
 )
@@ -125,6 +127,9 @@ _SIGS = {
     "qm_prune_level": (ctypes.c_int, [_LP, _I32, ctypes.c_double, _P, _I64, _P, _P, _I64, _I32, _P, _P, _I64,
                                       _I32, _I32, _I32, _P, _P, ctypes.POINTER(_I64), ctypes.POINTER(_I64),
                                       _P, _SZ, _P]),
+    "qm_filter_triples_workspace_bytes": (_SZ, [_I64, _I64]),
+    "qm_filter_triples": (ctypes.c_int, [_LP, _P, _P, _I32, _P, _P, _P, _I64, _I64, _P, _I64, _P, _P, _P,
+                                         ctypes.POINTER(_I64), ctypes.POINTER(_I64), _P, _SZ, _P]),
     "qm_generate_blocks": (ctypes.c_int, [_LP, _P, _I64, ctypes.c_uint64, ctypes.c_uint32, _I32,
                                           _I64, _P, _P, _P]),
     "qm_fp64_peak_kernel": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _I64, _P,

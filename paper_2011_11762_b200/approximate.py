@@ -36,13 +36,6 @@ class PruneResult:
     pairs_per_level: list = field(default_factory=list)
 
 
-def _coords(geom: Geometry, keys: torch.Tensor):
-    from .variants import _decode
-
-    bi, bj = _decode(geom, keys)
-    return bi.to(torch.int64), bj.to(torch.int64)
-
-
 def _node_tables(geom: Geometry, s: BlockSet, lay):
     """Every level's (Morton codes, norms, count) of one operand (qm_node_norms)."""
     import ctypes
@@ -111,8 +104,10 @@ def prune(geom: Geometry, a: BlockSet, b: BlockSet, tau: float, a_sym: bool = Fa
 
 
 def filter_plan(geom: Geometry, plan, a: BlockSet, b: BlockSet, pr: PruneResult, b_transposed=False):
-    """Keeps the triples whose leaf pair survived; rebuilds c_keys / c_tptr (C blocks left with no
-    triple vanish, like an all-pruned subtree)."""
+    """Keeps the triples whose leaf pair survived and rebuilds c_keys / c_tptr (qm_filter_triples:
+    C blocks left with no triple vanish, like an all-pruned subtree)."""
+    import ctypes
+
     from .spgemm import SymbolicPlan
 
     dev = plan.c_keys.device
@@ -120,22 +115,20 @@ def filter_plan(geom: Geometry, plan, a: BlockSet, b: BlockSet, pr: PruneResult,
         z = torch.zeros(0, dtype=torch.int64, device=dev)
         return SymbolicPlan(0, 0, z, torch.zeros(1, dtype=torch.int64, device=dev),
                             torch.zeros(0, dtype=torch.int32, device=dev))
-    nbl, w = geom.nbl, 1 << geom.params.depth
-    tri = plan.tri.view(-1, 2).to(torch.int64)
-    ar, ac = _coords(geom, a.keys)
-    br, bc = _coords(geom, b.keys)
-    li, lk = ar[tri[:, 0]] // nbl, ac[tri[:, 0]] // nbl
-    lj = (bc[tri[:, 1]] if not b_transposed else br[tri[:, 1]]) // nbl
-    code = (li * w + lk) * w + lj
-    pos = torch.searchsorted(pr.leaf_pairs, code).clamp(max=pr.leaf_pairs.shape[0] - 1)
-    keep = pr.leaf_pairs[pos] == code
-    counts = torch.zeros(plan.n_c, dtype=torch.int64, device=dev)
-    grp = torch.repeat_interleave(torch.arange(plan.n_c, device=dev), torch.diff(plan.c_tptr))
-    counts.index_add_(0, grp, keep.to(torch.int64))
-    alive = counts > 0
-    c_keys = plan.c_keys[alive].contiguous()
-    cnt = counts[alive]
-    c_tptr = torch.zeros(cnt.shape[0] + 1, dtype=torch.int64, device=dev)
-    c_tptr[1:] = torch.cumsum(cnt, 0)
-    tri_k = plan.tri.view(-1, 2)[keep].reshape(-1).contiguous()
-    return SymbolicPlan(int(c_keys.shape[0]), int(tri_k.shape[0] // 2), c_keys, c_tptr, tri_k)
+    lib = _ffi.load()
+    lay = _ffi.make_layout(geom.params, geom.bs)
+    nc, nt = plan.n_c, plan.n_triples
+    tri = torch.empty(2 * nt, dtype=torch.int32, device=dev)
+    c_tptr = torch.empty(nc + 1, dtype=torch.int64, device=dev)
+    c_keys = torch.empty(nc, dtype=torch.int64, device=dev)
+    wb = lib.qm_filter_triples_workspace_bytes(nc, nt)
+    ws = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
+    nc2, nt2 = ctypes.c_int64(0), ctypes.c_int64(0)
+    pairs = pr.leaf_pairs.contiguous()
+    _ffi.check(lib.qm_filter_triples(ctypes.byref(lay), _ffi.ptr(a.keys), _ffi.ptr(b.keys), int(b_transposed),
+                                     _ffi.ptr(plan.tri), _ffi.ptr(plan.c_tptr), _ffi.ptr(plan.c_keys), nc, nt,
+                                     _ffi.ptr(pairs), int(pairs.shape[0]), _ffi.ptr(tri), _ffi.ptr(c_tptr),
+                                     _ffi.ptr(c_keys), ctypes.byref(nc2), ctypes.byref(nt2), _ffi.ptr(ws), wb,
+                                     _ffi.stream_handle(torch.cuda.current_stream(dev))), "qm_filter_triples")
+    n_c, n_t = int(nc2.value), int(nt2.value)
+    return SymbolicPlan(n_c, n_t, c_keys[:n_c], c_tptr[:n_c + 1], tri[:2 * n_t])

@@ -267,3 +267,128 @@ extern "C" int qm_prune_level(const qm_layout *layout, int32_t level, double tau
   *n_pruned = cnt[1];
   return QM_OK;
 }
+
+// ---- filter of the symbolic plan by the surviving leaf pairs -----------------------------------
+
+namespace qm {
+namespace {
+
+// keep[t] = leaf pair (li, lk, lj) of triple t survived; code = (li*w + lk)*w + lj.
+__global__ void k_filter_keep(const uint2 *tri, int64_t nT, const uint64_t *a_keys, const uint64_t *b_keys,
+                              int b_transposed, int nbl, int lbits, int depth, const uint64_t *pairs,
+                              int64_t n_pairs, int64_t *keep) {
+  const uint64_t w = 1ull << depth;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= nT; t += (int64_t)gridDim.x * blockDim.x) {
+    if (t == nT) {
+      keep[t] = 0;  // exclusive-scan tail
+      continue;
+    }
+    uint32_t ai, ak, bk, bj;
+    qkey_decode(a_keys[tri[t].x], nbl, lbits, &ai, &ak);
+    qkey_decode(b_keys[tri[t].y], nbl, lbits, &bk, &bj);
+    if (b_transposed) bj = bk;
+    const uint64_t code = ((uint64_t)(ai / nbl) * w + ak / nbl) * w + bj / nbl;
+    int64_t lo = 0, hi = n_pairs;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (pairs[mid] < code) lo = mid + 1; else hi = mid;
+    }
+    keep[t] = (lo < n_pairs && pairs[lo] == code) ? 1 : 0;
+  }
+}
+
+// cnt[c] = kept triples of C block c; alive[c] = cnt[c] > 0; tails 0.
+__global__ void k_filter_count(const int64_t *tptr, int64_t nC, const int64_t *keep, int64_t *cnt,
+                               int64_t *alive) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= nC; c += (int64_t)gridDim.x * blockDim.x) {
+    if (c == nC) {
+      cnt[c] = 0;
+      alive[c] = 0;
+      continue;
+    }
+    int64_t s = 0;
+    for (int64_t t = tptr[c]; t < tptr[c + 1]; ++t) s += keep[t];
+    cnt[c] = s;
+    alive[c] = s > 0 ? 1 : 0;
+  }
+}
+
+__global__ void k_filter_scatter_tri(const uint2 *tri, int64_t nT, const int64_t *keep, const int64_t *kpos,
+                                     uint2 *tri_out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nT; t += (int64_t)gridDim.x * blockDim.x)
+    if (keep[t]) tri_out[kpos[t]] = tri[t];
+}
+
+__global__ void k_filter_scatter_c(const uint64_t *c_keys, int64_t nC, const int64_t *alive, const int64_t *apos,
+                                   const int64_t *cpos, uint64_t *keys_out, int64_t *tptr_out) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= nC; c += (int64_t)gridDim.x * blockDim.x) {
+    if (c == nC) {
+      tptr_out[apos[nC]] = cpos[nC];
+    } else if (alive[c]) {
+      keys_out[apos[c]] = c_keys[c];
+      tptr_out[apos[c]] = cpos[c];
+    }
+  }
+}
+
+}  // namespace
+}  // namespace qm
+
+extern "C" size_t qm_filter_triples_workspace_bytes(int64_t nC, int64_t nT) {
+  Carver cv(nullptr, 0);
+  cv.take<int64_t>(nT + 1);  // keep
+  cv.take<int64_t>(nT + 1);  // kpos
+  cv.take<int64_t>(nC + 1);  // cnt
+  cv.take<int64_t>(nC + 1);  // alive
+  cv.take<int64_t>(nC + 1);  // cpos
+  cv.take<int64_t>(nC + 1);  // apos
+  cv.take<char>(std::max(scan_bytes(nT + 1), scan_bytes(nC + 1)));
+  return cv.off;
+}
+
+extern "C" int qm_filter_triples(const qm_layout *layout, const uint64_t *a_keys, const uint64_t *b_keys,
+                                 int32_t b_transposed, const uint32_t *tri, const int64_t *c_tptr,
+                                 const uint64_t *c_keys, int64_t nC, int64_t nT, const uint64_t *leaf_pairs,
+                                 int64_t n_pairs, uint32_t *tri_out, int64_t *c_tptr_out, uint64_t *c_keys_out,
+                                 int64_t *nC_out, int64_t *nT_out, void *ws, size_t ws_bytes, void *stream) {
+  Geometry g;
+  int rc = make_geometry(layout, &g);
+  if (rc != QM_OK) return rc;
+  if (nC < 0 || nT < 0 || n_pairs < 0 || !nC_out || !nT_out) {
+    set_error("qm_filter_triples: bad arguments");
+    return QM_ERR_INVALID;
+  }
+  Carver cv(ws, ws_bytes);
+  int64_t *keep = cv.take<int64_t>(nT + 1), *kpos = cv.take<int64_t>(nT + 1);
+  int64_t *cnt = cv.take<int64_t>(nC + 1), *alive = cv.take<int64_t>(nC + 1);
+  int64_t *cpos = cv.take<int64_t>(nC + 1), *apos = cv.take<int64_t>(nC + 1);
+  const size_t sb = std::max(scan_bytes(nT + 1), scan_bytes(nC + 1));
+  void *cub = cv.take<char>(sb);
+  if (!cv.ok() || !ws) {
+    set_error("qm_filter_triples: workspace %zu < required %zu", ws_bytes, cv.off);
+    return QM_ERR_WORKSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint2 *t2 = (const uint2 *)tri;
+  k_filter_keep<<<grid_for(nT + 1), 256, 0, st>>>(t2, nT, a_keys, b_keys, b_transposed, g.nbl, g.lbits, g.depth,
+                                                  leaf_pairs, n_pairs, keep);
+  QM_LAUNCHED("k_filter_keep");
+  k_filter_count<<<grid_for(nC + 1), 256, 0, st>>>(c_tptr, nC, keep, cnt, alive);
+  QM_LAUNCHED("k_filter_count");
+  size_t tb = sb;
+  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub, tb, keep, kpos, nT + 1, st));
+  tb = sb;
+  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub, tb, cnt, cpos, nC + 1, st));
+  tb = sb;
+  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub, tb, alive, apos, nC + 1, st));
+  k_filter_scatter_tri<<<grid_for(nT), 256, 0, st>>>(t2, nT, keep, kpos, (uint2 *)tri_out);
+  QM_LAUNCHED("k_filter_scatter_tri");
+  k_filter_scatter_c<<<grid_for(nC + 1), 256, 0, st>>>(c_keys, nC, alive, apos, cpos, c_keys_out, c_tptr_out);
+  QM_LAUNCHED("k_filter_scatter_c");
+  int64_t counts[2];
+  rc = read_device_i64(apos + nC, 1, counts, st, kpos + nT);
+  if (rc != QM_OK) return rc;
+  *nC_out = counts[0];
+  *nT_out = counts[1];
+  return QM_OK;
+}
