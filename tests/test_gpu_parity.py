@@ -435,6 +435,37 @@ def test_approximate_multiply_matches_reference(ses, ci):
     assert diff <= skipped + 1e-12 and skipped <= tau + 1e-12
 
 
+@pytest.mark.parametrize("n,leaf,bs", [(512, 64, 16), (1000, 32, 32), (4096, 256, 64)])
+def test_node_norms_follow_the_reference_recursion(ses, n, leaf, bs):
+    """qm_node_norms: every level's nodes are the non-nil quadtree nodes, and each norm is
+    sqrt(fsum(child_norm^2)) of the level below, down to sqrt(fsum(block_norm^2)) per leaf
+    (quadtree.py:138-140, block_sparse.py:91-92) -- here with math.fsum on the host."""
+    import math
+
+    from paper_2011_11762_b200 import approximate
+
+    da = helpers.random_sparse(n, 0.01, 7)
+    m = helpers.build(ses, da, leaf, bs)
+    s = m.root.require()
+    geom = m.geometry
+    lay = _ffi.make_layout(geom.params, bs)
+    tables = approximate._node_tables(geom, s, lay)
+    keys = s.keys.cpu().numpy().astype(np.uint64)
+    vals = np.sqrt(s.sumsq.cpu().numpy())
+    codes = keys >> np.uint64(2 * geom.lbits)
+    depth = geom.params.depth
+    for lev in range(depth, -1, -1):
+        uniq, start = np.unique(codes, return_index=True)
+        bounds = list(start) + [codes.size]
+        want = np.array([math.sqrt(math.fsum(float(v) * float(v) for v in vals[bounds[i]:bounds[i + 1]]))
+                         for i in range(uniq.size)])
+        c, nrm, cnt = tables[lev]
+        assert cnt == uniq.size
+        np.testing.assert_array_equal(c[:cnt].cpu().numpy().astype(np.uint64), uniq)
+        np.testing.assert_allclose(nrm[:cnt].cpu().numpy(), want, rtol=2e-16, atol=0)
+        codes, vals = uniq >> np.uint64(2), want
+
+
 def test_approximate_with_zero_tau_is_the_exact_product(ses):
     """test_ops.py:190-197: tau = 0 gives the exact product bit for bit."""
     da = helpers.decay_sparse(64, 77, scale=2.0)
