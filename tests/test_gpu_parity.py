@@ -582,3 +582,21 @@ def test_c4_full_size_sampled_rows(ses):
     kc, bc, _ = O.multiply(O.Geom(cfg.n, cfg.bs, cfg.bs), ka[sel], ba[sel], ka[sel_b], ba[sel_b])
     got = helpers.lookup(c.root.blockset.keys.cpu().numpy(), c.root.blockset.blocks, kc)
     assert helpers.rel(got, bc) <= TOL
+
+
+def test_c3_full_size_sampled_rows_and_block_set(ses):
+    """BASELINE configs[2] (random, no locality) at full size: the exact C block set (host
+    symbolic of the oracle) and sampled C block rows against the oracle."""
+    cfg = G.CONFIGS["C3"]
+    geom, (ka, ba), (kb, bb) = G.config_operands_host(cfg)
+    c = ses.multiply(ses.matrix_from_blocks(geom, ka, ba), ses.matrix_from_blocks(geom, kb, bb))
+    assert ses.last_multiply.n_triples == 65536  # 1024 block rows x 8 x 8
+    kc_all, _, _, _, _ = O.symbolic(O.Geom(cfg.n, cfg.bs, cfg.bs), ka, kb)
+    keys = c.root.blockset.keys.cpu().numpy()
+    np.testing.assert_array_equal(keys, kc_all)  # no exact-zero products with random values
+    ai, _ = geom.decode(ka)
+    rows = np.r_[0, np.random.default_rng(3).choice(geom.nbg, 10, replace=False), geom.nbg - 1]
+    sel = np.isin(ai, rows)
+    kc, bc, _ = O.multiply(O.Geom(cfg.n, cfg.bs, cfg.bs), ka[sel], ba[sel], kb, bb)
+    got = helpers.lookup(keys, c.root.blockset.blocks, kc)
+    assert helpers.rel(got, bc) <= TOL
