@@ -255,7 +255,22 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
   __shared__ uint32_t red32[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kNT >> 5;
   const int s0 = threadIdx.x * kPerT;
+  const bool ranged = t_lo > 0 || t_hi < c_tptr[rowC_off[nbg]];
   for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
+    if (ranged) {
+      // A multi-GPU rank emits one triple range: skip rows none of whose C blocks reach it
+      // (their triples are [c_tptr[q], c_tptr[q+1]) for q = inv[row-major index]).
+      int64_t lo = INT64_MAX, hi = -1;
+      for (uint64_t x = rowC_off[i] + threadIdx.x; x < rowC_off[i + 1]; x += blockDim.x) {
+        const uint32_t q = inv[x];
+        lo = min(lo, c_tptr[q]);
+        hi = max(hi, c_tptr[q + 1]);
+      }
+      lo = (int64_t)block_reduce((uint64_t)lo, [](uint64_t a, uint64_t b) { return a < b ? a : b; }, red64);
+      hi = (int64_t)block_reduce((uint64_t)(hi + 1), [](uint64_t a, uint64_t b) { return a > b ? a : b; },
+                                 red64) - 1;
+      if (hi <= t_lo || lo >= t_hi) continue;
+    }
     RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
     if (s.nt > 0) {
       uint64_t out = rowC_off[i];
