@@ -576,7 +576,7 @@ def run_reference(args):
     from oracle import spgemm_oracle as O
 
     threads = O.default_threads()
-    target = max(2.0, min(args.cpu_target_s, 150.0 / max(1, args.steps + args.warmup)))
+    target = max(1.0, min(args.cpu_target_s, 100.0 / max(1, args.steps + args.warmup)))  # whole run ~3 min
     cfg, s, run, rows = cpu_sample(args.config, target, threads)
     for _ in range(max(args.warmup, 0)):
         run(s)
