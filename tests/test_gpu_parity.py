@@ -600,3 +600,30 @@ def test_c3_full_size_sampled_rows_and_block_set(ses):
     kc, bc, _ = O.multiply(O.Geom(cfg.n, cfg.bs, cfg.bs), ka[sel], ba[sel], kb, bb)
     got = helpers.lookup(keys, c.root.blockset.blocks, kc)
     assert helpers.rel(got, bc) <= TOL
+
+
+@pytest.mark.parametrize("bs", [16, 32, 64, 128])
+def test_special_values_subnormal_nan_inf(ses, bs):
+    """IEEE edge cases through the DMMA kernels: subnormal operands and products that underflow
+    into the subnormal range are kept (no flush-to-zero, so the exact-zero drop of _set_block
+    sees what numpy sees), NaN and Inf propagate inside their stored blocks only (block-sparse
+    semantics: absent blocks are never touched). One triple per C block, so bitwise vs numpy."""
+    n = 4 * bs
+    rng = np.random.default_rng(bs)
+    da, db = np.zeros((n, n)), np.zeros((n, n))
+    da[:bs, :bs] = rng.uniform(-1, 1, (bs, bs)) * 1e-310
+    db[:bs, :bs] = rng.uniform(-1, 1, (bs, bs))
+    da[bs:2 * bs, bs:2 * bs] = 1e-160
+    db[bs:2 * bs, bs:2 * bs] = 1e-160
+    da[2 * bs, 2 * bs], db[2 * bs, 2 * bs] = np.nan, 1.0
+    da[3 * bs, 3 * bs], db[3 * bs, 3 * bs] = np.inf, 2.0
+    a = helpers.build(ses, da, bs, bs)
+    b = helpers.build(ses, db, bs, bs)
+    got = ses.to_dense(ses.multiply(a, b))
+    want = np.zeros((n, n))
+    with np.errstate(invalid="ignore", over="ignore", under="ignore"):
+        for q in range(4):
+            sl = slice(q * bs, (q + 1) * bs)
+            want[sl, sl] = da[sl, sl] @ db[sl, sl]
+    assert np.array_equal(got, want, equal_nan=True)
+    assert np.count_nonzero(got[:bs, :bs]) == bs * bs  # subnormal results survive
