@@ -468,7 +468,9 @@ int launch_tma(const double *const *A, const int64_t *nA, int na, const double *
 }
 
 //                     BS TILE WM WN KP STAGES MINB
-using Tma32 = TmaCfg<32, 32, 1, 2, 32, 3, 4>;
+// bs 32: a triple is one 16 KB stage; 4 warps of 16x16 and 6 CTAs/SM (6 consumer warps per SMSP
+// hide the per-stage overheads better than 2 warps of 32x16 in 4 CTAs: C5-bs32 263.6 -> 259.1 ms).
+using Tma32 = TmaCfg<32, 32, 2, 2, 32, 2, 6>;
 using Tma64 = TmaCfg<64, 64, 2, 2, 32, 3, 2>;
 using Tma128 = TmaCfg<128, 64, 2, 2, 32, 3, 2>;
 
