@@ -137,11 +137,13 @@ QM_API int qm_spgemm_fill_triples(const qm_layout *layout, int64_t nA, int64_t n
  * (the np.any test of _set_block, block_sparse.py:37-41). *zero_count (device, int64) is
  * incremented once per exactly-zero C block; the caller zeroes it first. Block sizes above the
  * 64x64 CTA tile (bs 128) are computed as (bs/64)^2 tiles whose partial norms go to the caller's
- * workspace (qm_numeric_workspace_bytes, 0 for bs <= 64) and are combined in a fixed order. */
+ * workspace (qm_numeric_workspace_bytes) and are combined in a fixed order. nT = c_tptr[nC] (the
+ * triple count, known to the caller from qm_spgemm_count) selects the kernel variant: few triples
+ * per C block favour deeper prefetch, many favour more resident CTAs. */
 QM_API size_t qm_numeric_workspace_bytes(int32_t block_size, int64_t nC);
 QM_API int qm_numeric(const qm_layout *layout, const double *a_blocks, int64_t nA,
                const double *b_blocks, int64_t nB, const uint32_t *tri, const int64_t *c_tptr,
-               int64_t nC, double *c_blocks, double *c_sumsq, uint8_t *c_nonzero,
+               int64_t nC, int64_t nT, double *c_blocks, double *c_sumsq, uint8_t *c_nonzero,
                int64_t *zero_count, void *ws, size_t ws_bytes, void *stream);
 /* The numeric phase of a multi-GPU product fused with its halo exchange: operand blocks live in
  * up to 8 pools per operand -- this rank's and the other ranks' block pools mapped into this GPU's
@@ -152,8 +154,8 @@ QM_API int qm_numeric(const qm_layout *layout, const double *a_blocks, int64_t n
 QM_API int qm_numeric_pools(const qm_layout *layout, const double *const *a_pools, const int64_t *a_counts,
                             int32_t n_a_pools, const double *const *b_pools, const int64_t *b_counts,
                             int32_t n_b_pools, const uint32_t *tri, const int64_t *c_tptr, int64_t nC,
-                            double *c_blocks, double *c_sumsq, uint8_t *c_nonzero, int64_t *zero_count,
-                            void *ws, size_t ws_bytes, void *stream);
+                            int64_t nT, double *c_blocks, double *c_sumsq, uint8_t *c_nonzero,
+                            int64_t *zero_count, void *ws, size_t ws_bytes, void *stream);
 /* CUDA IPC of block pools for qm_numeric_pools (same-node ranks): export writes the 64-byte
  * cudaIpcMemHandle of the allocation containing `ptr` and ptr's byte offset in it; open maps a peer
  * handle (once per handle and process) and returns the allocation base; close unmaps it. */

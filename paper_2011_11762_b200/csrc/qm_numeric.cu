@@ -337,8 +337,8 @@ int numeric_sm_count() { return sm_count(); }
 
 int launch_numeric_tma(int bs, const double *const *A, const int64_t *nA, int na, const double *const *B,
                        const int64_t *nB, int nb, const uint32_t *tri, const int64_t *tptr, int64_t nC,
-                       double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes,
-                       cudaStream_t st);
+                       int64_t nT, double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws,
+                       size_t ws_bytes, cudaStream_t st);
 size_t numeric_tma_ws_bytes(int bs, int64_t nC);
 
 // Numeric kernel selection: QM_NUMERIC=cpasync forces the v1 cp.async kernel (A/B comparisons).
@@ -362,9 +362,9 @@ extern "C" size_t qm_numeric_workspace_bytes(int32_t block_size, int64_t nC) {
 
 extern "C" int qm_numeric(const qm_layout *layout, const double *a_blocks, int64_t nA,
                           const double *b_blocks, int64_t nB, const uint32_t *tri,
-                          const int64_t *c_tptr, int64_t nC, double *c_blocks, double *c_sumsq,
-                          uint8_t *c_nonzero, int64_t *zero_count, void *ws, size_t ws_bytes,
-                          void *stream) {
+                          const int64_t *c_tptr, int64_t nC, int64_t nT, double *c_blocks,
+                          double *c_sumsq, uint8_t *c_nonzero, int64_t *zero_count, void *ws,
+                          size_t ws_bytes, void *stream) {
   Geometry g;
   int rc = make_geometry(layout, &g);
   if (rc != QM_OK) return rc;
@@ -376,7 +376,7 @@ extern "C" int qm_numeric(const qm_layout *layout, const double *a_blocks, int64
   cudaStream_t st = (cudaStream_t)stream;
   const uint2 *t2 = (const uint2 *)tri;
   if (numeric_impl() == 2) {
-    rc = launch_numeric_tma(g.bs, &a_blocks, &nA, 1, &b_blocks, &nB, 1, tri, c_tptr, nC, c_blocks,
+    rc = launch_numeric_tma(g.bs, &a_blocks, &nA, 1, &b_blocks, &nB, 1, tri, c_tptr, nC, nT, c_blocks,
                             c_sumsq, c_nonzero, zero_count, ws, ws_bytes, st);
     if (rc != QM_ERR_UNSUPPORTED) return rc;
   }
@@ -407,8 +407,8 @@ extern "C" int qm_block_stats(int32_t block_size, int64_t n, const double *block
 extern "C" int qm_numeric_pools(const qm_layout *layout, const double *const *a_pools, const int64_t *a_counts,
                                 int32_t n_a_pools, const double *const *b_pools, const int64_t *b_counts,
                                 int32_t n_b_pools, const uint32_t *tri, const int64_t *c_tptr, int64_t nC,
-                                double *c_blocks, double *c_sumsq, uint8_t *c_nonzero, int64_t *zero_count,
-                                void *ws, size_t ws_bytes, void *stream) {
+                                int64_t nT, double *c_blocks, double *c_sumsq, uint8_t *c_nonzero,
+                                int64_t *zero_count, void *ws, size_t ws_bytes, void *stream) {
   Geometry g;
   int rc = make_geometry(layout, &g);
   if (rc != QM_OK) return rc;
@@ -418,5 +418,6 @@ extern "C" int qm_numeric_pools(const qm_layout *layout, const double *const *a_
     return QM_ERR_INVALID;
   }
   return launch_numeric_tma(g.bs, a_pools, a_counts, n_a_pools, b_pools, b_counts, n_b_pools, tri, c_tptr,
-                            nC, c_blocks, c_sumsq, c_nonzero, zero_count, ws, ws_bytes, (cudaStream_t)stream);
+                            nC, nT, c_blocks, c_sumsq, c_nonzero, zero_count, ws, ws_bytes,
+                            (cudaStream_t)stream);
 }

@@ -17,6 +17,8 @@
 //      lane t=0: k = 2j           t=1: k = 8 + 2((j+1)&3)
 //      lane t=2: k = 2((j+2)&3)+1 t=3: k = 9 + 2((j+3)&3)      (j = k step 0..3 in the panel)
 //    Each k in 0..15 is used exactly once per panel, so the sum is unchanged.
+#include <algorithm>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -472,15 +474,29 @@ int launch_tma(const double *const *A, const int64_t *nA, int na, const double *
 // hide the per-stage overheads better than 2 warps of 32x16 in 4 CTAs: C5-bs32 263.6 -> 259.1 ms).
 using Tma32 = TmaCfg<32, 32, 2, 2, 32, 2, 6>;
 using Tma64 = TmaCfg<64, 64, 2, 2, 32, 3, 2>;
+// Many triples per C block: 3 CTAs/SM with 2 stages (more resident warps hide the per-stage
+// overheads; C2-131072 -0.7%, C4 -0.9%); about one triple per block (random patterns, C3): 2 CTAs
+// with 3 stages (deeper prefetch of DRAM-resident operands; C3 -1.4% against the 3-CTA variant).
+using Tma64m = TmaCfg<64, 64, 2, 2, 32, 2, 3>;
+constexpr int64_t kManyTriplesPerBlock = 2;
+
+// Variant choice for bs 64/128: QM_TMA_VARIANT=deep|wide forces one (A/B measurements).
+bool use_wide(int64_t nC, int64_t nT) {
+  const char *e = getenv("QM_TMA_VARIANT");
+  if (e && strcmp(e, "deep") == 0) return false;
+  if (e && strcmp(e, "wide") == 0) return true;
+  return nT >= kManyTriplesPerBlock * nC;
+}
 using Tma128 = TmaCfg<128, 64, 2, 2, 32, 3, 2>;
+using Tma128m = TmaCfg<128, 64, 2, 2, 32, 2, 3>;
 
 }  // namespace
 
 size_t numeric_tma_ws_bytes(int bs, int64_t nC) {
   switch (bs) {
     case 32: return tma_ws_bytes<Tma32>(nC);
-    case 64: return tma_ws_bytes<Tma64>(nC);
-    case 128: return tma_ws_bytes<Tma128>(nC);
+    case 64: return std::max(tma_ws_bytes<Tma64>(nC), tma_ws_bytes<Tma64m>(nC));
+    case 128: return std::max(tma_ws_bytes<Tma128>(nC), tma_ws_bytes<Tma128m>(nC));
     default: return 0;
   }
 }
@@ -489,13 +505,19 @@ size_t numeric_tma_ws_bytes(int bs, int64_t nC) {
 // local; > 1 = every rank's pool, triple indices packed as owner << 28 | local).
 int launch_numeric_tma(int bs, const double *const *A, const int64_t *nA, int na, const double *const *B,
                        const int64_t *nB, int nb, const uint32_t *tri, const int64_t *tptr, int64_t nC,
-                       double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes,
-                       cudaStream_t st) {
+                       int64_t nT, double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws,
+                       size_t ws_bytes, cudaStream_t st) {
   const uint2 *t2 = (const uint2 *)tri;
   switch (bs) {
     case 32: return launch_tma<Tma32>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
-    case 64: return launch_tma<Tma64>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
-    case 128: return launch_tma<Tma128>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
+    case 64:
+      if (use_wide(nC, nT))
+        return launch_tma<Tma64m>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
+      return launch_tma<Tma64>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
+    case 128:
+      if (use_wide(nC, nT))
+        return launch_tma<Tma128m>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
+      return launch_tma<Tma128>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
     default: return QM_ERR_UNSUPPORTED;
   }
 }

@@ -150,6 +150,7 @@ class CudaBackend:
         stream = self.stream if self.stream is not None else torch.cuda.current_stream(dev)
         _ffi.check(lib.qm_numeric_pools(ctypes.byref(layout), arr_p(pa), arr_n(na), len(pa), arr_p(pb),
                                         arr_n(nb), len(pb), _ffi.ptr(tri), _ffi.ptr(c_tptr), nc,
+                                        int(tri.numel()) // 2,
                                         _ffi.ptr(out.blocks), _ffi.ptr(out.sumsq), _ffi.ptr(nz), _ffi.ptr(zc),
                                         _ffi.ptr(ws), wb, _ffi.stream_handle(stream)), "qm_numeric_pools")
         n_zero = spgemm._sync_item(zc, stream)

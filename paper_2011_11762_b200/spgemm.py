@@ -135,7 +135,7 @@ def numeric(layout, a: BlockSet, b: BlockSet, plan: SymbolicPlan, stream=None,
     ws = _alloc(wb, torch.uint8, dev) if wb else None
     _ffi.check(
         lib.qm_numeric(ctypes.byref(layout), _ffi.ptr(a.blocks), a.n, _ffi.ptr(b.blocks), b.n,
-                       _ffi.ptr(plan.tri), _ffi.ptr(plan.c_tptr), nc, _ffi.ptr(out.blocks),
+                       _ffi.ptr(plan.tri), _ffi.ptr(plan.c_tptr), nc, plan.n_triples, _ffi.ptr(out.blocks),
                        _ffi.ptr(out.sumsq), _ffi.ptr(nz), _ffi.ptr(zc), _ffi.ptr(ws), wb,
                        _ffi.stream_handle(stream)),
         "qm_numeric",

@@ -60,7 +60,7 @@ def test_workspace_and_argument_errors_before_any_device_work():
     rc = lib.qm_spgemm_count(ctypes.byref(lay), None, -1, None, 10, None, 0, ctypes.byref(nc),
                              ctypes.byref(nt), None)
     assert rc == _ffi.QM_ERR_INVALID
-    assert lib.qm_numeric(ctypes.byref(lay), None, 0, None, 0, None, None, 0, None, None, None, None,
+    assert lib.qm_numeric(ctypes.byref(lay), None, 0, None, 0, None, None, 0, 0, None, None, None, None,
                           None, 0, None) == _ffi.QM_OK  # nC == 0 is a no-op
     assert lib.qm_compact(64, -1, None, None, None, None, None, None, None, None, 0, None) == _ffi.QM_ERR_INVALID
     assert lib.qm_transpose_blocks(64, None, 4, None, None) == _ffi.QM_ERR_INVALID  # in place
