@@ -67,6 +67,19 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
       : "memory");
 }
 
+// C is written once and read by nobody in this kernel: its lines are marked evict-first in L2 so
+// they do not push out the A/B blocks that neighbouring work units are about to reuse.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ void st_evict_first(double *p, double a, double b, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(a), "d"(b), "l"(pol)
+               : "memory");
+}
+
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
@@ -142,17 +155,15 @@ __device__ __forceinline__ void cur_start(Cur &c, int64_t unit, int64_t nU, cons
   }
 }
 
-// Advances the producer's cursor; a finished unit is replaced by `next` (fetched ahead from the
-// global work counter) and a new `next` is claimed.
+// Advances the producer's cursor; a finished unit is replaced by the next one claimed from the
+// global work counter just in time (claiming a unit ahead widened the window of units in flight
+// and raised DRAM re-reads of A/B by 2x with 3 CTAs/SM).
 template <class Cfg>
-__device__ __forceinline__ void cur_next(Cur &c, int64_t nU, const int64_t *tptr, int64_t &next,
+__device__ __forceinline__ void cur_next(Cur &c, int64_t nU, const int64_t *tptr,
                                          unsigned long long *counter) {
   if (++c.p == Cfg::NP) {
     c.p = 0;
-    if (++c.t == c.tend) {
-      cur_start<Cfg>(c, next, nU, tptr);
-      if (next < nU) next = (int64_t)gridDim.x + (int64_t)atomicAdd(counter, 1ull);
-    }
+    if (++c.t == c.tend) cur_start<Cfg>(c, (int64_t)gridDim.x + (int64_t)atomicAdd(counter, 1ull), nU, tptr);
   }
 }
 
@@ -198,7 +209,6 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
       // and no CTA is left with a long tail of heavy units.
       Cur L;
       cur_start<Cfg>(L, blockIdx.x, nU, tptr);
-      int64_t next = (int64_t)gridDim.x + (int64_t)atomicAdd(counter, 1ull);
       int s = 0;
       uint32_t phase = 0;
       while (true) {
@@ -224,7 +234,7 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
         for (int q = 0; q < Cfg::NSP; ++q)
           tma_load_2d(st + Cfg::A_BYTES + q * Cfg::B_SP_BYTES, &maps.b[bo], col0 + q * 16,
                       (int)(bl * BS + L.p * Cfg::KP), &full[s]);
-        cur_next<Cfg>(L, nU, tptr, next, counter);
+        cur_next<Cfg>(L, nU, tptr, counter);
         if (++s == STAGES) {
           s = 0;
           phase ^= 1u;
@@ -236,6 +246,7 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
 
   // ------------------------------ consumer warps ------------------------------
   const int g = lane >> 2, tq = lane & 3;
+  const uint64_t c_policy = l2_evict_first_policy();
   const int wm0 = (warp / Cfg::WARPS_N) * Cfg::TM;
   const int wn0 = (warp % Cfg::WARPS_N) * Cfg::TN;
   // Per-lane swizzled byte offsets of the fragment elements (see kperm).
@@ -321,8 +332,7 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
           const double v0 = acc[i][n][0], v1 = acc[i][n][1];
-          *reinterpret_cast<double2 *>(cb + (size_t)(wm0 + i * 8 + g) * BS + wn0 + n * 8 + 2 * tq) =
-              make_double2(v0, v1);
+          st_evict_first(cb + (size_t)(wm0 + i * 8 + g) * BS + wn0 + n * 8 + 2 * tq, v0, v1, c_policy);
           ss0 = fma(v0, v0, ss0);
           ss1 = fma(v1, v1, ss1);
           nz |= (v0 != 0.0) | (v1 != 0.0);
