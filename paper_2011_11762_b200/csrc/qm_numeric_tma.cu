@@ -490,13 +490,18 @@ using Tma64 = TmaCfg<64, 64, 2, 2, 32, 3, 2>;
 using Tma64m = TmaCfg<64, 64, 2, 2, 32, 2, 3>;
 constexpr int64_t kManyTriplesPerBlock = 2;
 
-// Variant choice for bs 64/128: QM_TMA_VARIANT=deep|wide forces one (A/B measurements).
-bool use_wide(int64_t nC, int64_t nT) {
+// Variant choice for bs 64/128 (nU work units = C blocks x tiles per block): the 3-CTA variant needs
+// >= 2 triples per C block and enough units that its shorter per-CTA queue does not lengthen the
+// tail (>= 24 units per resident CTA: C2-16384 with 18 stays on 2 CTAs, C2-32768 with 37 moves).
+// QM_TMA_VARIANT=deep|wide forces one (A/B measurements).
+constexpr int64_t kWideUnitsPerCta = 24;
+bool use_wide(int64_t nU, int64_t nC, int64_t nT) {
   const char *e = getenv("QM_TMA_VARIANT");
   if (e && strcmp(e, "deep") == 0) return false;
   if (e && strcmp(e, "wide") == 0) return true;
-  return nT >= kManyTriplesPerBlock * nC;
+  return nT >= kManyTriplesPerBlock * nC && nU >= kWideUnitsPerCta * 3 * (int64_t)device_sm_count();
 }
+
 using Tma128 = TmaCfg<128, 64, 2, 2, 32, 3, 2>;
 using Tma128m = TmaCfg<128, 64, 2, 2, 32, 2, 3>;
 
@@ -521,11 +526,11 @@ int launch_numeric_tma(int bs, const double *const *A, const int64_t *nA, int na
   switch (bs) {
     case 32: return launch_tma<Tma32>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
     case 64:
-      if (use_wide(nC, nT))
+      if (use_wide(nC, nC, nT))
         return launch_tma<Tma64m>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
       return launch_tma<Tma64>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
     case 128:
-      if (use_wide(nC, nT))
+      if (use_wide(nC * Tma128::NQ, nC, nT))
         return launch_tma<Tma128m>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
       return launch_tma<Tma128>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
     default: return QM_ERR_UNSUPPORTED;
