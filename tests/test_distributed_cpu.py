@@ -153,3 +153,39 @@ def test_local_comm_is_identity():
     t = torch.arange(5)
     assert torch.equal(c.allgather_varlen(t)[0], t)
     assert torch.equal(c.alltoallv(t, [5])[0], t)
+
+
+def _locality_worker(rank, world, port, outdir):
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    cfg = G.BaselineConfig(f"loc{world}", "banded", 1024 * world, 64, half_bw=64)
+    geom, (ka, ba), (kb, bb) = G.config_operands_host(cfg)
+    qa = (np.arange(world + 1) * ka.size) // world
+    qb = (np.arange(world + 1) * kb.size) // world
+    la = BlockSet(torch.from_numpy(ka[qa[rank]:qa[rank + 1]]), torch.from_numpy(ba[qa[rank]:qa[rank + 1]]),
+                  torch.zeros(0))
+    lb = BlockSet(torch.from_numpy(kb[qb[rank]:qb[rank + 1]]), torch.from_numpy(bb[qb[rank]:qb[rank + 1]]),
+                  torch.zeros(0))
+    _, st = D.multiply(D.Comm(), make_layout(geom.params, geom.bs), la, lb, backend=OracleBackend(geom),
+                       mode="exchange")
+    got = torch.tensor([st.bytes_received], dtype=torch.int64)
+    allv = [torch.zeros_like(got) for _ in range(world)]
+    dist.all_gather(allv, got)
+    if rank == 0:
+        np.save(os.path.join(outdir, f"bytes_{world}.npy"), torch.cat(allv).numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_weak_scaling_locality(tmp_path):
+    """Mirror of the reference's test_weak_scaling_locality (test_acceptance.py:333-347): banded
+    matrices with n growing with the rank count; doubling the ranks may grow the mean bytes each
+    rank receives by at most 1.5x (the key-range partition keeps the halo to the band)."""
+    means = {}
+    for world in (2, 4, 8):
+        mp.spawn(_locality_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+        means[world] = float(np.load(tmp_path / f"bytes_{world}.npy").mean())
+    assert means[2] > 0
+    for low, high in ((2, 4), (4, 8)):
+        assert means[high] / means[low] <= 1.5, (low, high, means)
