@@ -139,12 +139,14 @@ QM_API int qm_spgemm_fill_triples(const qm_layout *layout, int64_t nA, int64_t n
  * 64x64 CTA tile (bs 128) are computed as (bs/64)^2 tiles whose partial norms go to the caller's
  * workspace (qm_numeric_workspace_bytes) and are combined in a fixed order. nT = c_tptr[nC] (the
  * triple count, known to the caller from qm_spgemm_count) selects the kernel variant: few triples
- * per C block favour deeper prefetch, many favour more resident CTAs. */
-QM_API size_t qm_numeric_workspace_bytes(int32_t block_size, int64_t nC);
-QM_API int qm_numeric(const qm_layout *layout, const double *a_blocks, int64_t nA,
+ * per C block favour deeper prefetch, many favour more resident CTAs. a_keys / c_keys (the A and C
+ * quadtree keys) are used for bs 16 only, where the C blocks of one leaf row segment are computed
+ * together so that they share their A blocks (NULL: per-block kernel). */
+QM_API size_t qm_numeric_workspace_bytes(int32_t block_size, int64_t nC, int64_t nT);
+QM_API int qm_numeric(const qm_layout *layout, const uint64_t *a_keys, const double *a_blocks, int64_t nA,
                const double *b_blocks, int64_t nB, const uint32_t *tri, const int64_t *c_tptr,
-               int64_t nC, int64_t nT, double *c_blocks, double *c_sumsq, uint8_t *c_nonzero,
-               int64_t *zero_count, void *ws, size_t ws_bytes, void *stream);
+               const uint64_t *c_keys, int64_t nC, int64_t nT, double *c_blocks, double *c_sumsq,
+               uint8_t *c_nonzero, int64_t *zero_count, void *ws, size_t ws_bytes, void *stream);
 /* The numeric phase of a multi-GPU product fused with its halo exchange: operand blocks live in
  * up to 8 pools per operand -- this rank's and the other ranks' block pools mapped into this GPU's
  * address space (CUDA IPC / peer access over NVLink). a_pools / b_pools / a_counts / b_counts are
@@ -163,7 +165,8 @@ QM_API int qm_ipc_export(const void *ptr, void *handle_out, int64_t *offset_out)
 QM_API int qm_ipc_open(const void *handle, void **base_out);
 QM_API int qm_ipc_close(void *base);
 /* Which numeric kernel qm_numeric uses for this block size: 2 = TMA + mbarrier warp-specialised
- * DMMA (bs 32/64/128), 1 = cp.async DMMA (bs 16, or QM_NUMERIC=cpasync), 0 = FP64 SIMT (others). */
+ * DMMA (bs 32/64/128; bs 16 as grouped leaf-row segments when a leaf holds >= 2 blocks per side),
+ * 1 = cp.async DMMA (QM_NUMERIC=cpasync, or bs 16 with one block per leaf), 0 = FP64 SIMT. */
 QM_API int qm_numeric_path(int32_t block_size);
 
 /* ---- exact-zero compaction (replaces _put_leaf / _set_block dropping, ops.py:119-122) --------- */

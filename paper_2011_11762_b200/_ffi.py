@@ -105,8 +105,9 @@ _SIGS = {
     "qm_spgemm_fill_keys": (ctypes.c_int, [_LP, _I64, _I64, _I64, _P, _SZ, _P, _SZ, _P, _P, _P]),
     "qm_spgemm_fill_triples": (ctypes.c_int, [_LP, _I64, _I64, _I64, _P, _SZ, _P, _SZ, _P, _I64, _I64,
                                               _P, _P]),
-    "qm_numeric": (ctypes.c_int, [_LP, _P, _I64, _P, _I64, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
-    "qm_numeric_workspace_bytes": (_SZ, [_I32, _I64]),
+    "qm_numeric": (ctypes.c_int, [_LP, _P, _P, _I64, _P, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _SZ,
+                                  _P]),
+    "qm_numeric_workspace_bytes": (_SZ, [_I32, _I64, _I64]),
     "qm_ipc_export": (ctypes.c_int, [_P, _P, ctypes.POINTER(_I64)]),
     "qm_ipc_open": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
     "qm_ipc_close": (ctypes.c_int, [_P]),

@@ -340,6 +340,11 @@ int launch_numeric_tma(int bs, const double *const *A, const int64_t *nA, int na
                        int64_t nT, double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws,
                        size_t ws_bytes, cudaStream_t st);
 size_t numeric_tma_ws_bytes(int bs, int64_t nC);
+size_t numeric_group16_ws_bytes(int64_t nC, int64_t nT);
+int launch_numeric_group16(const Geometry &g, const double *A, int64_t nA, const double *B, int64_t nB,
+                           const uint64_t *a_keys, const uint32_t *tri, const int64_t *c_tptr,
+                           const uint64_t *c_keys, int64_t nC, int64_t nT, double *C, double *csq,
+                           uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes, cudaStream_t st);
 
 // Numeric kernel selection: QM_NUMERIC=cpasync forces the v1 cp.async kernel (A/B comparisons).
 static int numeric_impl() {
@@ -352,17 +357,18 @@ static int numeric_impl() {
 using namespace qm;
 
 extern "C" int qm_numeric_path(int32_t bs) {
-  if ((bs == 32 || bs == 64 || bs == 128) && numeric_impl() == 2) return 2;
+  if ((bs == 16 || bs == 32 || bs == 64 || bs == 128) && numeric_impl() == 2) return 2;
   return (bs == 16 || bs == 32 || bs == 64 || bs == 128) ? 1 : 0;
 }
 
-extern "C" size_t qm_numeric_workspace_bytes(int32_t block_size, int64_t nC) {
-  return numeric_impl() == 2 ? numeric_tma_ws_bytes(block_size, nC) : 0;
+extern "C" size_t qm_numeric_workspace_bytes(int32_t block_size, int64_t nC, int64_t nT) {
+  if (numeric_impl() != 2) return 0;
+  return block_size == 16 ? numeric_group16_ws_bytes(nC, nT) : numeric_tma_ws_bytes(block_size, nC);
 }
 
-extern "C" int qm_numeric(const qm_layout *layout, const double *a_blocks, int64_t nA,
+extern "C" int qm_numeric(const qm_layout *layout, const uint64_t *a_keys, const double *a_blocks, int64_t nA,
                           const double *b_blocks, int64_t nB, const uint32_t *tri,
-                          const int64_t *c_tptr, int64_t nC, int64_t nT, double *c_blocks,
+                          const int64_t *c_tptr, const uint64_t *c_keys, int64_t nC, int64_t nT, double *c_blocks,
                           double *c_sumsq, uint8_t *c_nonzero, int64_t *zero_count, void *ws,
                           size_t ws_bytes, void *stream) {
   Geometry g;
@@ -375,6 +381,11 @@ extern "C" int qm_numeric(const qm_layout *layout, const double *a_blocks, int64
   if (nC == 0) return QM_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const uint2 *t2 = (const uint2 *)tri;
+  if (numeric_impl() == 2 && g.bs == 16) {
+    rc = launch_numeric_group16(g, a_blocks, nA, b_blocks, nB, a_keys, tri, c_tptr, c_keys, nC, nT, c_blocks,
+                                c_sumsq, c_nonzero, zero_count, ws, ws_bytes, st);
+    if (rc != QM_ERR_UNSUPPORTED) return rc;
+  }
   if (numeric_impl() == 2) {
     rc = launch_numeric_tma(g.bs, &a_blocks, &nA, 1, &b_blocks, &nB, 1, tri, c_tptr, nC, nT, c_blocks,
                             c_sumsq, c_nonzero, zero_count, ws, ws_bytes, st);

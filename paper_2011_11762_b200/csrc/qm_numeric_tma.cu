@@ -26,75 +26,10 @@
 #include <string.h>
 
 #include "qm_common.cuh"
+#include "qm_tma.cuh"
 
 namespace qm {
 namespace {
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// C is written once and read by nobody in this kernel: its lines are marked evict-first in L2 so
-// they do not push out the A/B blocks that neighbouring work units are about to reuse.
-__device__ __forceinline__ uint64_t l2_evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
-  return pol;
-}
-
-__device__ __forceinline__ void st_evict_first(double *p, double a, double b, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(a), "d"(b), "l"(pol)
-               : "memory");
-}
-
-__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
-
-// k index (0..15) inside a 16-double panel used by lane column t at k step j (see header).
-__host__ __device__ __forceinline__ int kperm(int t, int j) {
-  switch (t) {
-    case 0: return 2 * j;
-    case 1: return 8 + 2 * ((j + 1) & 3);
-    case 2: return 2 * ((j + 2) & 3) + 1;
-    default: return 9 + 2 * ((j + 3) & 3);
-  }
-}
 
 // A CTA computes one TILE x TILE tile of a C block (TILE = BS, or 64 for BS = 128: the block is
 // then NQ = (BS/TILE)^2 work units whose partial norms are combined in a fixed order afterwards).
@@ -365,39 +300,6 @@ __global__ void k_combine_tiles(const double *part_sq, const uint8_t *part_nz, i
     cnz[m] = (uint8_t)(any != 0);
     if (!any && zero_count) atomicAdd((unsigned long long *)zero_count, 1ull);
   }
-}
-
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {  // thread-safe one-time lookup
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      return (PFN_cuTensorMapEncodeTiled_v12000)p;
-    return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
-  }();
-  return fn;
-}
-
-// 2-D view of a block pool: rows = nblocks * bs, cols = bs (row-major), box = 16 cols x box_rows.
-int make_map(CUtensorMap *m, const double *base, int64_t nblocks, int bs, int box_rows) {
-  auto fn = encode_fn();
-  if (!fn) {
-    set_error("cuTensorMapEncodeTiled unavailable from the driver");
-    return QM_ERR_CUDA;
-  }
-  cuuint64_t dims[2] = {(cuuint64_t)bs, (cuuint64_t)nblocks * bs};
-  cuuint64_t strides[1] = {(cuuint64_t)bs * sizeof(double)};
-  cuuint32_t box[2] = {16u, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1u, 1u};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)base, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    set_error("cuTensorMapEncodeTiled failed (%d) for %lld blocks of %d", (int)r, (long long)nblocks, bs);
-    return QM_ERR_CUDA;
-  }
-  return QM_OK;
 }
 
 int sm_count_tma() { return device_sm_count(); }

@@ -145,7 +145,7 @@ class CudaBackend:
                        torch.empty(nc, dtype=torch.float64, device=dev))
         nz = torch.empty(nc, dtype=torch.uint8, device=dev)
         zc = torch.zeros(1, dtype=torch.int64, device=dev)
-        wb = lib.qm_numeric_workspace_bytes(bs, nc)
+        wb = lib.qm_numeric_workspace_bytes(bs, nc, int(tri.numel()) // 2)
         ws = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
         stream = self.stream if self.stream is not None else torch.cuda.current_stream(dev)
         _ffi.check(lib.qm_numeric_pools(ctypes.byref(layout), arr_p(pa), arr_n(na), len(pa), arr_p(pb),

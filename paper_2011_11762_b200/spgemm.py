@@ -131,11 +131,12 @@ def numeric(layout, a: BlockSet, b: BlockSet, plan: SymbolicPlan, stream=None,
                        _alloc(nc, torch.float64, dev))
     nz = _alloc(nc, torch.uint8, dev)
     zc = torch.zeros(1, dtype=torch.int64, device=dev)
-    wb = lib.qm_numeric_workspace_bytes(bs, nc)
+    wb = lib.qm_numeric_workspace_bytes(bs, nc, plan.n_triples)
     ws = _alloc(wb, torch.uint8, dev) if wb else None
     _ffi.check(
-        lib.qm_numeric(ctypes.byref(layout), _ffi.ptr(a.blocks), a.n, _ffi.ptr(b.blocks), b.n,
-                       _ffi.ptr(plan.tri), _ffi.ptr(plan.c_tptr), nc, plan.n_triples, _ffi.ptr(out.blocks),
+        lib.qm_numeric(ctypes.byref(layout), _ffi.ptr(a.keys), _ffi.ptr(a.blocks), a.n, _ffi.ptr(b.blocks), b.n,
+                       _ffi.ptr(plan.tri), _ffi.ptr(plan.c_tptr), _ffi.ptr(plan.c_keys), nc, plan.n_triples,
+                       _ffi.ptr(out.blocks),
                        _ffi.ptr(out.sumsq), _ffi.ptr(nz), _ffi.ptr(zc), _ffi.ptr(ws), wb,
                        _ffi.stream_handle(stream)),
         "qm_numeric",

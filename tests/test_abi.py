@@ -36,7 +36,7 @@ def test_abi_version_and_host_queries():
     lay = _ffi.make_layout(MatrixParams.create(4096, 64), 64)
     assert lib.qm_spgemm_workspace_bytes(ctypes.byref(lay), 556, 556) > 0
     assert lib.qm_compact_workspace_bytes(1016) > 0
-    assert [lib.qm_numeric_path(b) for b in (16, 32, 64, 128, 8, 12)] == [1, 2, 2, 2, 0, 0]
+    assert [lib.qm_numeric_path(b) for b in (16, 32, 64, 128, 8, 12)] == [2, 2, 2, 2, 0, 0]
 
 
 def test_invalid_layout_is_reported_not_crashed():
@@ -60,8 +60,8 @@ def test_workspace_and_argument_errors_before_any_device_work():
     rc = lib.qm_spgemm_count(ctypes.byref(lay), None, -1, None, 10, None, 0, ctypes.byref(nc),
                              ctypes.byref(nt), None)
     assert rc == _ffi.QM_ERR_INVALID
-    assert lib.qm_numeric(ctypes.byref(lay), None, 0, None, 0, None, None, 0, 0, None, None, None, None,
-                          None, 0, None) == _ffi.QM_OK  # nC == 0 is a no-op
+    assert lib.qm_numeric(ctypes.byref(lay), None, None, 0, None, 0, None, None, None, 0, 0, None, None, None,
+                          None, None, 0, None) == _ffi.QM_OK  # nC == 0 is a no-op
     assert lib.qm_compact(64, -1, None, None, None, None, None, None, None, None, 0, None) == _ffi.QM_ERR_INVALID
     assert lib.qm_transpose_blocks(64, None, 4, None, None) == _ffi.QM_ERR_INVALID  # in place
     too_deep = _ffi.QmLayout(1 << 40, 1, 40, 1, 0)

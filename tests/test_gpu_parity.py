@@ -269,7 +269,7 @@ def test_c2_131072_sampled_blocks_and_counts(ses):
 
 
 @pytest.mark.parametrize("impl", ["tma", "cpasync"])
-@pytest.mark.parametrize("bs", [32, 64, 128])
+@pytest.mark.parametrize("bs", [16, 32, 64, 128])
 def test_both_numeric_kernels_match_oracle(ses, monkeypatch, impl, bs):
     """The TMA/mbarrier kernel (default) and the cp.async kernel (QM_NUMERIC=cpasync) on the
     same product: exact block set, values within TOL of the oracle."""
@@ -627,3 +627,24 @@ def test_special_values_subnormal_nan_inf(ses, bs):
             want[sl, sl] = da[sl, sl] @ db[sl, sl]
     assert np.array_equal(got, want, equal_nan=True)
     assert np.count_nonzero(got[:bs, :bs]) == bs * bs  # subnormal results survive
+
+
+@pytest.mark.parametrize("n,leaf,dens", [(1000, 128, 0.02), (700, 64, 0.05), (500, 48, 0.05), (1500, 256, 0.01),
+                                         (2048, 128, 0.3)])
+def test_bs16_grouped_kernel_vs_oracle(ses, n, leaf, dens):
+    """bs 16 with several blocks per leaf side runs k_numeric_group16 (the C blocks of a leaf row
+    segment share their A blocks): exact C block set and values within TOL of the oracle, which
+    sums each block's own triples k-ascending -- members missing a k must not see its products.
+    Includes 3 and 16 blocks per leaf side (partial and split groups) and a nearly dense case."""
+    lib = _ffi.load()
+    assert lib.qm_numeric_path(16) == 2
+    da, db = helpers.random_sparse(n, dens, n + 1), helpers.random_sparse(n, dens, n + 2)
+    c = ses.multiply(helpers.build(ses, da, leaf, 16), helpers.build(ses, db, leaf, 16))
+    host = MatrixSession(device="cpu")
+    ka, ba, _ = helpers.build(host, da, leaf, 16).root.blockset.to_host()
+    kb, bb, _ = helpers.build(host, db, leaf, 16).root.blockset.to_host()
+    kc, bc, _ = O.multiply(O.Geom(n, leaf, 16), ka, ba, kb, bb)
+    np.testing.assert_array_equal(c.root.blockset.keys.cpu().numpy(), kc)
+    assert helpers.rel(c.root.blockset.blocks.cpu().numpy(), bc) <= TOL
+    np.testing.assert_allclose(c.root.blockset.sumsq.cpu().numpy(), np.einsum("nij,nij->n", bc, bc), rtol=1e-12)
+    assert helpers.rel(ses.to_dense(c), da @ db) <= TOL
