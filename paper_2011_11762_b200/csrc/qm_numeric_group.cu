@@ -8,9 +8,9 @@
 // pipeline stage carries one A block and the B blocks B(k, j) of the members that have that k:
 // up to 8 products for 18 KB, 3.6 flop/byte.
 //
-//   k_group_merge<count|fill>: one warp per group merges the members' k-ascending triple lists
-//     into the group's union of k (one entry per k: the A index and up to 8 B indices, absent =
-//     0xffffffff);
+//   k_group_merge: one warp per group merges the members' k-ascending triple lists into the
+//     group's union of k (one entry per k: the A index and up to 8 B indices, absent =
+//     0xffffffff), stored in the group's own triple range;
 //   k_numeric_group16: warp-specialised like k_numeric_tma (one TMA producer warp, mbarrier ring),
 //     8 consumer warps, warp w owns member w: a 16x16 accumulator fed only by the entries that
 //     contain its k (so each C block sums exactly its own triples, k ascending -- the order of
@@ -61,19 +61,17 @@ __global__ void k_triple_k(const uint2 *tri, int64_t nT, const uint64_t *a_keys,
 
 // One warp per group (at its head C block): lane s owns the member in slot s (if any) and walks
 // its k-ascending triple list; each step takes the smallest head k over the lanes (warp min) and
-// every lane holding it contributes its B index to the entry. Count pass: entries per group;
-// fill pass: the entries, 9 words written by 9 lanes.
-template <bool FILL>
+// every lane holding it contributes its B index to the entry (9 words written by 9 lanes). The
+// group's entries go to its own triple range [c_tptr[first], ...): the union of the members' k
+// is never longer than their triple lists together, so no count pass is needed.
 __global__ void k_group_merge(const uint64_t *c_keys, const int64_t *c_tptr, const uint2 *tri, const uint32_t *tk,
                               int64_t nC, int mbits, const int64_t *head, const int64_t *gidx, int64_t *ucount,
-                              const int64_t *uoff, int64_t *gfirst, uint32_t *gmask, Entry *entries,
-                              int64_t *n_groups) {
+                              int64_t *gfirst, uint32_t *gmask, Entry *entries, int64_t *n_groups) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t c0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c0 < nC; c0 += warps) {
     if (!head[c0]) continue;  // warp-uniform
     const int64_t g = gidx[c0];
-    // members: C blocks c0 .. c0+nm-1 (nm <= 8), slot = low key bits
     int nm = 1;
     while (nm < kG && c0 + nm < nC && !head[c0 + nm]) ++nm;
     int64_t pos = 0, end = 0;
@@ -86,24 +84,23 @@ __global__ void k_group_merge(const uint64_t *c_keys, const int64_t *c_tptr, con
         end = c_tptr[c0 + m + 1];
       }
     }
-    int64_t out = FILL ? uoff[g] : 0, cnt = 0;
+    Entry *out = entries + c_tptr[c0];
+    int64_t cnt = 0;
     while (true) {
       const uint32_t myk = (lane < kG && pos < end) ? tk[pos] : 0xffffffffu;
       const uint32_t kmin = __reduce_min_sync(0xffffffffu, myk);
       if (kmin == 0xffffffffu) break;
       const bool hit = myk == kmin;
-      if (FILL) {
-        const unsigned hits = __ballot_sync(0xffffffffu, hit);
-        const uint32_t my_a = hit ? tri[pos].x : 0u;
-        const uint32_t a = __shfl_sync(0xffffffffu, my_a, __ffs(hits) - 1);
-        uint32_t *ew = reinterpret_cast<uint32_t *>(entries + out + cnt);
-        if (lane == kG) ew[0] = a;  // Entry::a
-        if (lane < kG) ew[1 + lane] = hit ? tri[pos].y : kAbsent;
-      }
+      const unsigned hits = __ballot_sync(0xffffffffu, hit);
+      const uint32_t my_a = hit ? tri[pos].x : 0u;
+      const uint32_t a = __shfl_sync(0xffffffffu, my_a, __ffs(hits) - 1);
+      uint32_t *ew = reinterpret_cast<uint32_t *>(out + cnt);
+      if (lane == kG) ew[0] = a;  // Entry::a
+      if (lane < kG) ew[1 + lane] = hit ? tri[pos].y : kAbsent;
       if (hit) ++pos;
       ++cnt;
     }
-    if (!FILL && lane == 0) {
+    if (lane == 0) {
       ucount[g] = cnt;
       gfirst[g] = c0;
       gmask[g] = mask;
@@ -112,15 +109,10 @@ __global__ void k_group_merge(const uint64_t *c_keys, const int64_t *c_tptr, con
   }
 }
 
-__global__ void k_zero_tail(int64_t *ucount, int64_t nC) {
-  // groups beyond the real count keep a zero entry count (the scans run over nC + 1 slots)
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x <= nC; x += (int64_t)gridDim.x * blockDim.x)
-    ucount[x] = 0;
-}
-
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     k_numeric_group16(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                      const Entry *__restrict__ entries, const int64_t *__restrict__ uoff,
+                      const Entry *__restrict__ entries, const int64_t *__restrict__ c_tptr,
+                      const int64_t *__restrict__ ucount,
                       const int64_t *__restrict__ gfirst, const uint32_t *__restrict__ gmask,
                       const int64_t *__restrict__ n_groups_dev, double *__restrict__ C, double *__restrict__ csq,
                       uint8_t *__restrict__ cnz, int64_t *__restrict__ zero_count,
@@ -155,8 +147,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     int64_t unit = blockIdx.x, e = 0, e1 = 0;
     uint32_t cur = kAbsent;
     if (unit < nG) {
-      e = uoff[unit];
-      e1 = uoff[unit + 1];
+      e = c_tptr[gfirst[unit]];
+      e1 = e + ucount[unit];
       if (lane <= kG) cur = ew[e * (1 + kG) + word];
     }
     int s = 0;
@@ -170,8 +162,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
           if (lane == 0) got = atomicAdd(counter, 1ull);
           nunit = (int64_t)gridDim.x + (int64_t)__shfl_sync(0xffffffffu, got, 0);
           if (nunit < nG) {
-            ne = uoff[nunit];
-            ne1 = uoff[nunit + 1];
+            ne = c_tptr[gfirst[nunit]];
+            ne1 = ne + ucount[nunit];
           }
         }
         if (nunit < nG && lane <= kG) nxt = ew[ne * (1 + kG) + word];
@@ -330,7 +322,7 @@ size_t scan_bytes(int64_t n) {
 }
 
 struct GroupWs {
-  int64_t *head, *gidx, *ucount, *uoff, *gfirst, *n_groups;
+  int64_t *head, *gidx, *ucount, *gfirst, *n_groups;
   uint32_t *gmask;
   unsigned long long *counter;
   Entry *entries;
@@ -344,7 +336,6 @@ GroupWs carve_group(Carver &cv, int64_t nC, int64_t nT) {
   w.head = cv.take<int64_t>(nC + 1);
   w.gidx = cv.take<int64_t>(nC + 1);
   w.ucount = cv.take<int64_t>(nC + 1);
-  w.uoff = cv.take<int64_t>(nC + 1);
   w.gfirst = cv.take<int64_t>(nC + 1);
   w.n_groups = cv.take<int64_t>(1);
   w.gmask = cv.take<uint32_t>(nC + 1);
@@ -386,19 +377,12 @@ int launch_numeric_group16(const Geometry &g, const double *A, int64_t nA, const
   QM_LAUNCHED("k_group_heads");
   size_t tb = w.cub_bytes;
   QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(w.cub, tb, w.head, w.gidx, nC + 1, st));
-  k_zero_tail<<<grid_for(nC + 1), 256, 0, st>>>(w.ucount, nC);
-  QM_LAUNCHED("k_zero_tail");
   k_triple_k<<<grid_for(nT), 256, 0, st>>>(t2, nT, a_keys, g.nbl, g.lbits, w.tk);
   QM_LAUNCHED("k_triple_k");
   const int merge_grid = (int)std::min<int64_t>((nC + 7) / 8, 148 * 64);
-  k_group_merge<false><<<merge_grid, 256, 0, st>>>(c_keys, c_tptr, t2, w.tk, nC, mbits, w.head, w.gidx, w.ucount,
-                                                   nullptr, w.gfirst, w.gmask, nullptr, w.n_groups);
-  QM_LAUNCHED("k_group_merge<count>");
-  tb = w.cub_bytes;
-  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(w.cub, tb, w.ucount, w.uoff, nC + 1, st));
-  k_group_merge<true><<<merge_grid, 256, 0, st>>>(c_keys, c_tptr, t2, w.tk, nC, mbits, w.head, w.gidx, nullptr,
-                                                  w.uoff, nullptr, nullptr, w.entries, nullptr);
-  QM_LAUNCHED("k_group_merge<fill>");
+  k_group_merge<<<merge_grid, 256, 0, st>>>(c_keys, c_tptr, t2, w.tk, nC, mbits, w.head, w.gidx, w.ucount,
+                                            w.gfirst, w.gmask, w.entries, w.n_groups);
+  QM_LAUNCHED("k_group_merge");
   CUtensorMap ma, mb;
   int rc = make_map(&ma, A, nA, kBlk, kBlk);
   if (rc != QM_OK) return rc;
@@ -416,7 +400,8 @@ int launch_numeric_group16(const Geometry &g, const double *A, int64_t nA, const
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)device_sm_count() * per_sm;
   if (grid > nC) grid = nC;  // groups <= C blocks
-  k_numeric_group16<<<(int)grid, kThreads, kSmem, st>>>(ma, mb, w.entries, w.uoff, w.gfirst, w.gmask, w.n_groups,
+  k_numeric_group16<<<(int)grid, kThreads, kSmem, st>>>(ma, mb, w.entries, c_tptr, w.ucount, w.gfirst, w.gmask,
+                                                         w.n_groups,
                                                          C, csq, cnz, zc, w.counter, /*zmask=*/0ull);
   QM_LAUNCHED("k_numeric_group16");
   return QM_OK;
