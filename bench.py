@@ -416,6 +416,7 @@ def run_ours(args):
                                     "(structure gather + symbolic + exchange + numeric)")
     if not args.no_e2e and world == 1:
         line["e2e"] = run_e2e(args, torch, ses, geom, a, b, dev, world, dist)
+        line["e2e"]["pcie"] = pcie_floor(torch, dev, line["e2e"])
     elif not args.no_e2e:
         line["e2e"] = run_e2e_distributed(args, torch, geom, a, b, dev, world, dist, cdev)
     if prev_affinity is not None:
@@ -521,6 +522,49 @@ def run_e2e(args, torch, ses, geom, a, b, dev, world, dist):
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps,
             "ms_per_step": round(ms / steps, 3), "api": "MatrixSession.multiply",
             "pipelining": "H2D(k+1) | product(k) | D2H(k) on separate streams, double-buffered inputs"}
+
+
+def pcie_floor(torch, dev, e2e, mib=1024):
+    """Pinned copy bandwidth of this box measured right after the e2e run (outside its timed
+    region): H2D alone, D2H alone, both directions at once. The e2e step moves its H2D and D2H
+    bytes concurrently, so its floor is (h2d + d2h bytes) / bidirectional bandwidth."""
+    n = mib * 2**20 // 8
+    h_in = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    h_out = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    d_in = torch.empty(n, dtype=torch.float64, device=dev)
+    d_out = torch.empty(n, dtype=torch.float64, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def timed(h2d, d2h):
+        best = float("inf")
+        for _ in range(3):
+            torch.cuda.synchronize(dev)
+            e = [ev(), ev(), ev(), ev()]
+            e[0].record(s1)
+            s2.wait_event(e[0])
+            if h2d:
+                with torch.cuda.stream(s1):
+                    d_in.copy_(h_in, non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(s2):
+                    h_out.copy_(d_out, non_blocking=True)
+            e[1].record(s1)
+            e[2].record(s2)
+            s1.wait_event(e[2])
+            e[3].record(s1)
+            torch.cuda.synchronize(dev)
+            best = min(best, e[0].elapsed_time(e[3]))
+        return (h2d + d2h) * n * 8 / (best * 1e-3) / 1e9
+
+    bw = {"h2d_gbs": round(timed(1, 0), 1), "d2h_gbs": round(timed(0, 1), 1),
+          "bidir_gbs": round(timed(1, 1), 1)}
+    floor = (e2e["h2d_bytes_per_step"] + e2e["d2h_bytes_per_step"]) / (bw["bidir_gbs"] * 1e9) * 1e3
+    bw["floor_ms_per_step"] = round(floor, 3)
+    bw["frac_of_floor"] = round(floor / e2e["ms_per_step"], 3)
+    bw["note"] = f"{mib} MiB pinned buffers, best of 3, measured after the e2e loop"
+    del h_in, h_out, d_in, d_out
+    return bw
 
 
 def run_e2e_distributed(args, torch, geom, a, b, dev, world, dist, cdev):

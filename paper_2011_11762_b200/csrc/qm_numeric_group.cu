@@ -2,20 +2,26 @@
 //
 // A 16x16 triple is 8 KFLOP for 4 KB of operands, 2 flop/byte: with one C block per work unit the
 // kernel streams every A and B block from L2 once per triple and is bound by L2->SM bandwidth
-// (the cp.async kernel reaches ~50% of the DMMA peak). Here a work unit is a *group*: the up to 8
-// C blocks of one leaf row segment (same block row i, consecutive in quadtree-key order, since a
-// leaf stores its blocks row-major -- BlockSparseLeaf.encode). They share the A blocks A(i,k), so a
-// pipeline stage carries one A block and the B blocks B(k, j) of the members that have that k:
-// up to 8 products for 18 KB, 3.6 flop/byte.
+// (the cp.async kernel reaches ~50% of the DMMA peak). Here a work unit is a *group*: the C blocks
+// of R block rows (R = 2 when a leaf has <= 8 blocks per side, else 1) x up to 8 aligned block
+// columns of one leaf -- consecutive in quadtree-key order, since a leaf stores its blocks
+// row-major (BlockSparseLeaf.encode). A triple (r,k,c) exists iff A(r,k) and B(k,c) do, so one
+// pipeline stage per k carries the group's A(r,k) and B(k,c) blocks and feeds every member
+// product at that k: up to 16 products for 20 KB (R = 2; 6.6 flop/byte) -- each B block serves
+// both rows and each A block all 8 columns.
 //
 //   k_group_merge: one warp per group merges the members' k-ascending triple lists into the
-//     group's union of k (one entry per k: the A index and up to 8 B indices, absent =
-//     0xffffffff), stored in the group's own triple range;
+//     group's union of k (one entry per k: R A indices and 8 B indices, absent = 0xffffffff),
+//     stored in the group's own triple range;
 //   k_numeric_group16: warp-specialised like k_numeric_tma (one TMA producer warp, mbarrier ring),
-//     8 consumer warps, warp w owns member w: a 16x16 accumulator fed only by the entries that
-//     contain its k (so each C block sums exactly its own triples, k ascending -- the order of
-//     BlockSparseLeaf.multiply, block_sparse.py:121-129), and writes the block, its sum of squares
-//     and exact-zero flag (_set_block, block_sparse.py:37-41) when the group ends.
+//     4 consumer warps, warp w owns columns 2w, 2w+1 of every group row: R x 2 accumulators of
+//     16x16 fed only by the entries where both its A row and B column are present (so each C
+//     block sums exactly its own triples, k ascending -- the order of BlockSparseLeaf.multiply,
+//     block_sparse.py:121-129), and writes the blocks, their sums of squares and exact-zero flags
+//     (_set_block, block_sparse.py:37-41) when the group ends.
+#include <stdlib.h>
+#include <string.h>
+
 #include <cub/cub.cuh>
 
 #include "qm_common.cuh"
@@ -24,109 +30,211 @@
 namespace qm {
 namespace {
 
-constexpr int kG = 8;                         // members per group
+constexpr int kG = 8;                         // block columns per group
 constexpr int kBlk = 16;                      // block size
 constexpr int kBlkBytes = kBlk * kBlk * 8;    // 2 KB
-constexpr int kMPW = 2;                       // members per consumer warp (16x32 warp tile)
-constexpr int kCW = kG / kMPW;                // consumer warps
-constexpr int kStages = 3;
-constexpr int kStageBytes = (1 + kG) * kBlkBytes;
-constexpr int kThreads = 32 * (kCW + 1);
-constexpr int kMinBlocks = 4;
-constexpr size_t kSmem = 1024 + (size_t)kStages * kStageBytes + 4 * kStages * 8 + 64;
+constexpr int kCW = 4;                        // consumer warps: warp w owns columns 2w, 2w+1
 constexpr uint32_t kAbsent = 0xffffffffu;
 
-struct Entry {
-  uint32_t a;
-  uint32_t b[kG];
+// R = block rows per group (1, or 2 when a leaf row pair is contiguous in key order: <= 8 blocks per
+// leaf side). A group is R x 8 member slots, slot = r * 8 + c, in key order.
+template <int R>
+struct GCfg {
+  static constexpr int M = R * kG;                       // member slots
+  static constexpr int EW = R + kG;                      // words per entry: a[R], b[8]
+#ifndef QM_G16_STAGES2
+#define QM_G16_STAGES2 3
+#endif
+#ifndef QM_G16_MINB2
+#define QM_G16_MINB2 3
+#endif
+  static constexpr int STAGES = R == 1 ? 3 : QM_G16_STAGES2;
+  static constexpr int STAGE_BYTES = (R + kG) * kBlkBytes;
+  static constexpr int THREADS = 32 * (kCW + 1);
+  static constexpr int MINB = R == 1 ? 4 : QM_G16_MINB2;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 4 * STAGES * 8 + 64;
 };
 
-// Group of C block c: its key without the low member bits (same leaf, same block row, aligned runs
-// of up to 8 block columns); member slot = those low bits.
-__device__ __forceinline__ uint64_t group_code(uint64_t key, int mbits) { return key >> mbits; }
-
-__global__ void k_group_heads(const uint64_t *c_keys, int64_t nC, int mbits, int64_t *head) {
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= nC; c += (int64_t)gridDim.x * blockDim.x)
-    head[c] = (c < nC && (c == 0 || group_code(c_keys[c], mbits) != group_code(c_keys[c - 1], mbits))) ? 1 : 0;
+// Group of a C block: its key without the member bits (same leaf; same block row, or the same
+// aligned pair of block rows for R = 2; aligned runs of up to 8 block columns).
+template <int R>
+__device__ __forceinline__ uint64_t group_code(uint64_t key, int lbits, int mbits) {
+  return R == 2 ? key >> (lbits + 1) : key >> mbits;
+}
+template <int R>
+__device__ __forceinline__ int member_slot(uint64_t key, int lbits, int mbits) {
+  if (R == 2) return (int)((((key >> lbits) & 1ull) << 3) | (key & ((1ull << lbits) - 1ull)));
+  return (int)(key & ((1ull << mbits) - 1ull));
 }
 
-// k (block column of the A block) of every triple.
-__global__ void k_triple_k(const uint2 *tri, int64_t nT, const uint64_t *a_keys, int nbl, int lbits, uint32_t *tk) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nT; t += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t bi, bj;
-    qkey_decode(a_keys[tri[t].x], nbl, lbits, &bi, &bj);
-    tk[t] = bj;
+template <int R>
+__global__ void k_group_heads(const uint64_t *c_keys, int64_t nC, int lbits, int mbits, int64_t *head) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= nC; c += (int64_t)gridDim.x * blockDim.x)
+    head[c] = (c < nC && (c == 0 || group_code<R>(c_keys[c], lbits, mbits) !=
+                                        group_code<R>(c_keys[c - 1], lbits, mbits))) ? 1 : 0;
+}
+
+// First C block of every group (a scatter of the heads through their exclusive scan) and the
+// group count.
+__global__ void k_group_first(const int64_t *head, const int64_t *gidx, int64_t nC, int64_t *gfirst,
+                              int64_t *n_groups) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= nC; c += (int64_t)gridDim.x * blockDim.x) {
+    if (c < nC && head[c]) gfirst[gidx[c]] = c;
+    if (c == nC) *n_groups = gidx[nC];
   }
 }
 
-// One warp per group (at its head C block): lane s owns the member in slot s (if any) and walks
-// its k-ascending triple list; each step takes the smallest head k over the lanes (warp min) and
-// every lane holding it contributes its B index to the entry (9 words written by 9 lanes). The
-// group's entries go to its own triple range [c_tptr[first], ...): the union of the members' k
-// is never longer than their triple lists together, so no count pass is needed.
-__global__ void k_group_merge(const uint64_t *c_keys, const int64_t *c_tptr, const uint2 *tri, const uint32_t *tk,
-                              int64_t nC, int mbits, const int64_t *head, const int64_t *gidx, int64_t *ucount,
-                              int64_t *gfirst, uint32_t *gmask, Entry *entries, int64_t *n_groups) {
+// One warp per group (grid-stride over the groups, so every warp of the launch has work): lane s owns the member in slot s (if any) and walks
+// its k-ascending triple list; each step takes the smallest head k over the lanes (warp min), and
+// the lanes holding it supply the entry's A index of their row and B index of their column (a
+// triple (r,k,c) exists iff A(r,k) and B(k,c) do, so one entry per k describes every member's
+// product at that k). The group's entries go to its own triple range [c_tptr[first], ...): the
+// union of the members' k is never longer than their triple lists together, so no count pass.
+template <int R>
+__global__ void k_group_merge(const uint64_t *c_keys, const int64_t *c_tptr, const uint2 *tri, const uint64_t *a_keys,
+                              int64_t nC, int nbl, int lbits, int mbits, const int64_t *gfirst,
+                              const int64_t *n_groups, int64_t *ucount, uint32_t *gmask, uint32_t *entries) {
+  constexpr int M = GCfg<R>::M, EW = GCfg<R>::EW;
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t c0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c0 < nC; c0 += warps) {
-    if (!head[c0]) continue;  // warp-uniform
-    const int64_t g = gidx[c0];
-    int nm = 1;
-    while (nm < kG && c0 + nm < nC && !head[c0 + nm]) ++nm;
+  // writer lanes: [0, R) the A index of row `lane`, [R, R+8) the B index of column lane-R
+  const int wr = lane < R ? lane : 0;
+  const int wc = (lane >= R && lane < EW) ? lane - R : 0;
+  const uint32_t rowsel = 0xffu << (8 * wr);
+  const uint32_t colsel = R == 2 ? (0x101u << wc) : (1u << wc);
+  const int64_t nG = *n_groups;
+  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < nG; g += warps) {
+    const int64_t c0 = gfirst[g];
+    const int nm = (int)((g + 1 < nG ? gfirst[g + 1] : nC) - c0);
     int64_t pos = 0, end = 0;
     uint32_t mask = 0;
     for (int m = 0; m < nm; ++m) {
-      const int sl = (int)(c_keys[c0 + m] & ((1ull << mbits) - 1ull));
+      const int sl = member_slot<R>(c_keys[c0 + m], lbits, mbits);
       mask |= 1u << sl;
       if (lane == sl) {
         pos = c_tptr[c0 + m];
         end = c_tptr[c0 + m + 1];
       }
     }
-    Entry *out = entries + c_tptr[c0];
+    uint32_t *out = entries + (size_t)c_tptr[c0] * EW;
     int64_t cnt = 0;
+    // The lane's next kD triples and their k (block column of the A block), prefetched kD deep so
+    // the dependent tri -> a_keys loads of a lane overlap the merge steps in between.
+    constexpr int kD = 4;
+    uint2 t[kD];
+    uint32_t kq[kD];
+#pragma unroll
+    for (int d = 0; d < kD; ++d) {
+      kq[d] = 0xffffffffu;
+      t[d] = make_uint2(0u, 0u);
+      if (lane < M && pos + d < end) {
+        uint32_t bi;
+        t[d] = tri[pos + d];
+        qkey_decode(a_keys[t[d].x], nbl, lbits, &bi, &kq[d]);
+      }
+    }
     while (true) {
-      const uint32_t myk = (lane < kG && pos < end) ? tk[pos] : 0xffffffffu;
-      const uint32_t kmin = __reduce_min_sync(0xffffffffu, myk);
+      const uint32_t kmin = __reduce_min_sync(0xffffffffu, kq[0]);
       if (kmin == 0xffffffffu) break;
-      const bool hit = myk == kmin;
-      const unsigned hits = __ballot_sync(0xffffffffu, hit);
-      const uint32_t my_a = hit ? tri[pos].x : 0u;
-      const uint32_t a = __shfl_sync(0xffffffffu, my_a, __ffs(hits) - 1);
-      uint32_t *ew = reinterpret_cast<uint32_t *>(out + cnt);
-      if (lane == kG) ew[0] = a;  // Entry::a
-      if (lane < kG) ew[1 + lane] = hit ? tri[pos].y : kAbsent;
-      if (hit) ++pos;
+      const bool hit = kq[0] == kmin;
+      const uint32_t hits = __ballot_sync(0xffffffffu, hit);
+      const uint32_t sa = hits & rowsel, sb = hits & colsel;
+      const uint32_t a = __shfl_sync(0xffffffffu, t[0].x, sa ? __ffs(sa) - 1 : 0);
+      const uint32_t b = __shfl_sync(0xffffffffu, t[0].y, sb ? __ffs(sb) - 1 : 0);
+      if (lane < R) out[cnt * EW + lane] = sa ? a : kAbsent;
+      else if (lane < EW) out[cnt * EW + lane] = sb ? b : kAbsent;
+      if (hit) {
+#pragma unroll
+        for (int d = 0; d + 1 < kD; ++d) {
+          t[d] = t[d + 1];
+          kq[d] = kq[d + 1];
+        }
+        kq[kD - 1] = 0xffffffffu;
+        if (++pos + kD - 1 < end) {
+          uint32_t bi;
+          t[kD - 1] = tri[pos + kD - 1];
+          qkey_decode(a_keys[t[kD - 1].x], nbl, lbits, &bi, &kq[kD - 1]);
+        }
+      }
       ++cnt;
     }
     if (lane == 0) {
       ucount[g] = cnt;
-      gfirst[g] = c0;
       gmask[g] = mask;
-      if (c0 + nm == nC) *n_groups = g + 1;
     }
   }
 }
 
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
+// One stage of a consumer warp: the products of its columns 2w, 2w+1 with every present A row.
+// ALL = every A row and both B columns present (no per-product guards, so loads of the next k step
+// can be scheduled under the DMMAs of this one). Returns the OR of the stage's last fragments (the
+// stage-release dependency, see k_numeric_tma).
+template <int R, bool ALL>
+__device__ __forceinline__ uint64_t group_stage(const uint8_t *sa, int warp, uint32_t ona, uint32_t onb,
+                                                const uint32_t (&aoff)[4], const uint32_t (&boff)[4][2],
+                                                double (&acc)[R][2][2][2][2]) {
+  uint64_t dep = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    double af[R][2], bf[2][2];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (ALL || (ona & (1u << r)))
+#pragma unroll
+        for (int i = 0; i < 2; ++i) af[r][i] = *(const double *)(sa + r * kBlkBytes + i * 8 * 128 + aoff[j]);
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (ALL || (onb & (1u << q))) {
+        const uint8_t *sb = sa + (R + 2 * warp + q) * kBlkBytes;
+#pragma unroll
+        for (int n = 0; n < 2; ++n) bf[q][n] = *(const double *)(sb + boff[j][n]);
+      }
+    if (j == 3) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (ALL || (ona & (1u << r)))
+#pragma unroll
+          for (int i = 0; i < 2; ++i) dep |= (uint64_t)__double_as_longlong(af[r][i]);
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (ALL || (onb & (1u << q)))
+#pragma unroll
+          for (int n = 0; n < 2; ++n) dep |= (uint64_t)__double_as_longlong(bf[q][n]);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (ALL || ((ona & (1u << r)) && (onb & (1u << q))))
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int n = 0; n < 2; ++n) dmma(acc[r][q][i][n][0], acc[r][q][i][n][1], af[r][i], bf[q][n]);
+  }
+  return dep;
+}
+
+template <int R>
+__global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
     k_numeric_group16(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                      const Entry *__restrict__ entries, const int64_t *__restrict__ c_tptr,
+                      const uint32_t *__restrict__ entries, const int64_t *__restrict__ c_tptr,
                       const int64_t *__restrict__ ucount,
                       const int64_t *__restrict__ gfirst, const uint32_t *__restrict__ gmask,
                       const int64_t *__restrict__ n_groups_dev, double *__restrict__ C, double *__restrict__ csq,
                       uint8_t *__restrict__ cnz, int64_t *__restrict__ zero_count,
                       unsigned long long *__restrict__ counter, uint64_t zmask) {
+  using Cfg = GCfg<R>;
+  constexpr int STAGES = Cfg::STAGES, EW = Cfg::EW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t *full = (uint64_t *)(smem + (size_t)kStages * kStageBytes);
-  uint64_t *empty = full + kStages;
-  volatile int64_t *meta = (volatile int64_t *)(empty + kStages);       // unit*2 + last, -1 = end
-  volatile uint32_t *pmask = (volatile uint32_t *)(meta + kStages);     // members present in the entry
+  uint64_t *full = (uint64_t *)(smem + (size_t)STAGES * Cfg::STAGE_BYTES);
+  uint64_t *empty = full + STAGES;
+  volatile int64_t *meta = (volatile int64_t *)(empty + STAGES);       // unit*2 + last, -1 = end
+  volatile uint32_t *pmask = (volatile uint32_t *)(meta + STAGES);     // bits 0-7 B columns, 8.. A rows
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nG = *n_groups_dev;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kCW);
     }
@@ -135,21 +243,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   __syncthreads();
 
   if (warp == kCW) {
-    // ---------------- producer warp: one stage per entry; lane m < 8 loads member m's B block,
-    // lane 8 the A block, so the up to 9 TMA loads of a stage issue together. The entry of the
-    // next stage (and the next claimed group) is loaded one stage ahead.
+    // ---------------- producer warp: one stage per entry; lane c < 8 loads column c's B block,
+    // lane 8 + r row r's A block, so the up to 8 + R TMA loads of a stage issue together. The entry
+    // of the next stage (and the next claimed group) is loaded one stage ahead.
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&map_a) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&map_b) : "memory");
     }
-    const uint32_t *ew = reinterpret_cast<const uint32_t *>(entries);
-    const int word = lane < kG ? 1 + lane : 0;  // Entry layout: a, b[0..7]
+    const bool loader = lane < kG + R;
+    const int word = lane < kG ? R + lane : lane - kG;  // Entry layout: a[R], b[8]
+    // smem slot of this lane's block: A rows first, then the 8 B columns
+    const int slot = lane < kG ? R + lane : lane - kG;
     int64_t unit = blockIdx.x, e = 0, e1 = 0;
     uint32_t cur = kAbsent;
     if (unit < nG) {
       e = c_tptr[gfirst[unit]];
       e1 = e + ucount[unit];
-      if (lane <= kG) cur = ew[e * (1 + kG) + word];
+      if (loader) cur = entries[e * EW + word];
     }
     int s = 0;
     uint32_t phase = 0;
@@ -166,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
             ne1 = ne + ucount[nunit];
           }
         }
-        if (nunit < nG && lane <= kG) nxt = ew[ne * (1 + kG) + word];
+        if (nunit < nG && loader) nxt = entries[ne * EW + word];
       }
       if (lane == 0) mbar_wait(&empty[s], phase ^ 1u);
       __syncwarp();
@@ -177,22 +287,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
         }
         break;
       }
-      const uint32_t pm = __ballot_sync(0xffffffffu, lane < kG && cur != kAbsent);
-      uint8_t *st = smem + (size_t)s * kStageBytes;
+      const uint32_t pm = __ballot_sync(0xffffffffu, loader && cur != kAbsent);
+      uint8_t *st = smem + (size_t)s * Cfg::STAGE_BYTES;
       if (lane == 0) {
         meta[s] = unit * 2 + (e + 1 == e1 ? 1 : 0);
         pmask[s] = pm;
-        mbar_expect_tx(&full[s], (uint32_t)(1 + __popc(pm)) * kBlkBytes);
+        mbar_expect_tx(&full[s], (uint32_t)__popc(pm) * kBlkBytes);
       }
       __syncwarp();
-      if (lane == kG) tma_load_2d(st, &map_a, 0, (int)(cur * kBlk), &full[s]);
-      else if (lane < kG && cur != kAbsent)
-        tma_load_2d(st + (1 + lane) * kBlkBytes, &map_b, 0, (int)(cur * kBlk), &full[s]);
+      if (loader && cur != kAbsent)
+        tma_load_2d(st + slot * kBlkBytes, lane < kG ? &map_b : &map_a, 0, (int)(cur * kBlk), &full[s]);
       unit = nunit;
       e = ne;
       e1 = ne1;
       cur = nxt;
-      if (++s == kStages) {
+      if (++s == STAGES) {
         s = 0;
         phase ^= 1u;
       }
@@ -200,7 +309,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     return;
   }
 
-  // -------- consumers: warp w = members 2w, 2w+1 (16x32: the A fragments serve both) --------
+  // -------- consumers: warp w = columns 2w, 2w+1 of every group row (R*16 x 32: each A fragment
+  // serves both columns, each B fragment every row) --------
   const int g = lane >> 2, tq = lane & 3;
   uint32_t aoff[4], boff[4][2];
 #pragma unroll
@@ -211,99 +321,84 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     for (int h = 0; h < 2; ++h) boff[j][h] = kk * 128 + ((((h * 4) + (g >> 1)) ^ (kk & 7)) << 4) + (g & 1) * 8;
   }
   const uint64_t c_policy = l2_evict_first_policy();
-  double acc[kMPW][2][2][2];
+  double acc[R][2][2][2][2];  // [row][column of the pair][i][n][2]
 #pragma unroll
-  for (int q = 0; q < kMPW; ++q)
+  for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int q = 0; q < 2; ++q)
 #pragma unroll
-      for (int n = 0; n < 2; ++n) acc[q][i][n][0] = acc[q][i][n][1] = 0.0;
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int n = 0; n < 2; ++n) acc[r][q][i][n][0] = acc[r][q][i][n][1] = 0.0;
   int s = 0;
   uint32_t phase = 0;
+  int64_t cur_unit = -1, c_first = 0;
+  uint32_t gm = 0;
   while (true) {
     mbar_wait(&full[s], phase);
     const int64_t mt = meta[s];
     if (mt < 0) break;
-    const uint32_t on = (pmask[s] >> (kMPW * warp)) & ((1u << kMPW) - 1u);
-    uint64_t dep = 0;
-    if (on) {
-      const uint8_t *sa = smem + (size_t)s * kStageBytes;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        double af[2], bf[kMPW][2];
-#pragma unroll
-        for (int i = 0; i < 2; ++i) af[i] = *(const double *)(sa + i * 8 * 128 + aoff[j]);
-#pragma unroll
-        for (int q = 0; q < kMPW; ++q)
-          if (on & (1u << q)) {
-            const uint8_t *sb = sa + (1 + kMPW * warp + q) * kBlkBytes;
-#pragma unroll
-            for (int n = 0; n < 2; ++n) bf[q][n] = *(const double *)(sb + boff[j][n]);
-          }
-        if (j == 3) {
-#pragma unroll
-          for (int i = 0; i < 2; ++i) dep |= (uint64_t)__double_as_longlong(af[i]);
-#pragma unroll
-          for (int q = 0; q < kMPW; ++q)
-            if (on & (1u << q))
-#pragma unroll
-              for (int n = 0; n < 2; ++n) dep |= (uint64_t)__double_as_longlong(bf[q][n]);
-        }
-#pragma unroll
-        for (int q = 0; q < kMPW; ++q)
-          if (on & (1u << q))
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-#pragma unroll
-              for (int n = 0; n < 2; ++n) dmma(acc[q][i][n][0], acc[q][i][n][1], af[i], bf[q][n]);
-      }
+    if ((mt >> 1) != cur_unit) {  // a group's first stage: fetch its epilogue metadata now, so the
+      cur_unit = mt >> 1;         // loads complete under the group's DMMAs
+      gm = gmask[cur_unit];
+      c_first = gfirst[cur_unit];
     }
+    const uint32_t pm = pmask[s];
+    const uint32_t onb = (pm >> (2 * warp)) & 3u;
+    const uint32_t ona = (pm >> kG) & ((1u << R) - 1u);
+    uint64_t dep = 0;
+    if (onb == 3u && ona == (1u << R) - 1u)  // every product of the warp present: no guards
+      dep = group_stage<R, true>(smem + (size_t)s * Cfg::STAGE_BYTES, warp, ona, onb, aoff, boff, acc);
+    else if (onb)
+      dep = group_stage<R, false>(smem + (size_t)s * Cfg::STAGE_BYTES, warp, ona, onb, aoff, boff, acc);
     // release once this warp's fragments are in registers (see k_numeric_tma)
     dep &= zmask;
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s] + (uint32_t)dep);
-    if (++s == kStages) {
+    if (++s == STAGES) {
       s = 0;
       phase ^= 1u;
     }
     if (mt & 1) {
-      const int64_t unit = mt >> 1;
-      const uint32_t gm = gmask[unit];
 #pragma unroll
-      for (int q = 0; q < kMPW; ++q) {
-        const int mb = kMPW * warp + q;
-        if ((gm >> mb) & 1u) {
-          const int64_t c = gfirst[unit] + __popc(gm & ((1u << mb) - 1u));
-          double *cb = C + (size_t)c * (kBlk * kBlk);
-          double ss0 = 0.0, ss1 = 0.0;
-          bool nz = false;
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int mb = r * kG + 2 * warp + q;
+          if ((gm >> mb) & 1u) {
+            const int64_t c = c_first + __popc(gm & ((1u << mb) - 1u));
+            double *cb = C + (size_t)c * (kBlk * kBlk);
+            double ss0 = 0.0, ss1 = 0.0;
+            bool nz = false;
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+              for (int n = 0; n < 2; ++n) {
+                const double v0 = acc[r][q][i][n][0], v1 = acc[r][q][i][n][1];
+                st_evict_first(cb + (size_t)(i * 8 + g) * kBlk + n * 8 + 2 * tq, v0, v1, c_policy);
+                ss0 = fma(v0, v0, ss0);
+                ss1 = fma(v1, v1, ss1);
+                nz |= (v0 != 0.0) | (v1 != 0.0);
+              }
+            double ss = ss0 + ss1;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+            const bool wnz = __any_sync(0xffffffffu, nz);
+            if (lane == 0) {
+              csq[c] = ss;
+              cnz[c] = (uint8_t)wnz;
+              if (!wnz && zero_count) atomicAdd((unsigned long long *)zero_count, 1ull);
+            }
+          }
+        }
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
 #pragma unroll
           for (int i = 0; i < 2; ++i)
 #pragma unroll
-            for (int n = 0; n < 2; ++n) {
-              const double v0 = acc[q][i][n][0], v1 = acc[q][i][n][1];
-              st_evict_first(cb + (size_t)(i * 8 + g) * kBlk + n * 8 + 2 * tq, v0, v1, c_policy);
-              ss0 = fma(v0, v0, ss0);
-              ss1 = fma(v1, v1, ss1);
-              nz |= (v0 != 0.0) | (v1 != 0.0);
-            }
-          double ss = ss0 + ss1;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-          const bool wnz = __any_sync(0xffffffffu, nz);
-          if (lane == 0) {
-            csq[c] = ss;
-            cnz[c] = (uint8_t)wnz;
-            if (!wnz && zero_count) atomicAdd((unsigned long long *)zero_count, 1ull);
-          }
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < kMPW; ++q)
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-          for (int n = 0; n < 2; ++n) acc[q][i][n][0] = acc[q][i][n][1] = 0.0;
+            for (int n = 0; n < 2; ++n) acc[r][q][i][n][0] = acc[r][q][i][n][1] = 0.0;
     }
   }
 }
@@ -325,12 +420,12 @@ struct GroupWs {
   int64_t *head, *gidx, *ucount, *gfirst, *n_groups;
   uint32_t *gmask;
   unsigned long long *counter;
-  Entry *entries;
-  uint32_t *tk;
+  uint32_t *entries;
   void *cub;
   size_t cub_bytes;
 };
 
+// Entries are sized for the widest layout (R = 2: 10 words), one per triple at most.
 GroupWs carve_group(Carver &cv, int64_t nC, int64_t nT) {
   GroupWs w;
   w.head = cv.take<int64_t>(nC + 1);
@@ -340,11 +435,61 @@ GroupWs carve_group(Carver &cv, int64_t nC, int64_t nT) {
   w.n_groups = cv.take<int64_t>(1);
   w.gmask = cv.take<uint32_t>(nC + 1);
   w.counter = cv.take<unsigned long long>(1);
-  w.entries = cv.take<Entry>(std::max<int64_t>(nT, 1));  // one entry per distinct k: <= triples
-  w.tk = cv.take<uint32_t>(std::max<int64_t>(nT, 1));
+  w.entries = cv.take<uint32_t>(std::max<int64_t>(nT, 1) * GCfg<2>::EW);  // <= one entry per triple
   w.cub_bytes = scan_bytes(nC + 1);
   w.cub = cv.take<char>(w.cub_bytes);
   return w;
+}
+
+// Rows per group: 2 when a leaf has <= 8 blocks per side (a leaf row pair is then contiguous in
+// key order), else 1. QM_GROUP_ROWS=1 forces single-row groups (A/B measurements).
+int group_rows(const Geometry &g) {
+  const char *e = getenv("QM_GROUP_ROWS");
+  if (e && strcmp(e, "1") == 0) return 1;
+  return g.lbits <= 3 ? 2 : 1;
+}
+
+template <int R>
+int launch_group(const Geometry &g, const double *A, int64_t nA, const double *B, int64_t nB,
+                 const uint64_t *a_keys, const uint2 *t2, const int64_t *c_tptr, const uint64_t *c_keys,
+                 int64_t nC, int64_t nT, double *C, double *csq, uint8_t *cnz, int64_t *zc, const GroupWs &w,
+                 cudaStream_t st) {
+  using Cfg = GCfg<R>;
+  const int mbits = std::min(g.lbits, 3);
+  k_group_heads<R><<<grid_for(nC + 1), 256, 0, st>>>(c_keys, nC, g.lbits, mbits, w.head);
+  QM_LAUNCHED("k_group_heads");
+  size_t tb = w.cub_bytes;
+  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(w.cub, tb, w.head, w.gidx, nC + 1, st));
+  k_group_first<<<grid_for(nC + 1), 256, 0, st>>>(w.head, w.gidx, nC, w.gfirst, w.n_groups);
+  QM_LAUNCHED("k_group_first");
+  const int merge_grid = (int)std::min<int64_t>((nC + 7) / 8, (int64_t)device_sm_count() * 8);
+  k_group_merge<R><<<merge_grid, 256, 0, st>>>(c_keys, c_tptr, t2, a_keys, nC, g.nbl, g.lbits, mbits, w.gfirst,
+                                               w.n_groups, w.ucount, w.gmask, w.entries);
+  QM_LAUNCHED("k_group_merge");
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, A, nA, kBlk, kBlk);
+  if (rc != QM_OK) return rc;
+  rc = make_map(&mb, B, nB, kBlk, kBlk);
+  if (rc != QM_OK) return rc;
+  static PerDeviceOnce once;
+  rc = once.run([]() -> int {
+    QM_CUDA_TRY(cudaFuncSetAttribute(k_numeric_group16<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)Cfg::SMEM));
+    return (int)QM_OK;
+  });
+  if (rc != QM_OK) return rc;
+  QM_CUDA_TRY(cudaMemsetAsync(w.counter, 0, sizeof(unsigned long long), st));
+  int per_sm = 0;
+  QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_numeric_group16<R>, Cfg::THREADS,
+                                                            Cfg::SMEM));
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)device_sm_count() * per_sm;
+  if (grid > nC) grid = nC;  // groups <= C blocks
+  k_numeric_group16<R><<<(int)grid, Cfg::THREADS, Cfg::SMEM, st>>>(
+      ma, mb, w.entries, c_tptr, w.ucount, w.gfirst, w.gmask, w.n_groups, C, csq, cnz, zc, w.counter,
+      /*zmask=*/0ull);
+  QM_LAUNCHED("k_numeric_group16");
+  return QM_OK;
 }
 
 }  // namespace
@@ -371,40 +516,10 @@ int launch_numeric_group16(const Geometry &g, const double *A, int64_t nA, const
     set_error("qm_numeric: pool exceeds TMA's int32 row coordinate");
     return QM_ERR_UNSUPPORTED;
   }
-  const int mbits = std::min(g.lbits, 3);
   const uint2 *t2 = (const uint2 *)tri;
-  k_group_heads<<<grid_for(nC + 1), 256, 0, st>>>(c_keys, nC, mbits, w.head);
-  QM_LAUNCHED("k_group_heads");
-  size_t tb = w.cub_bytes;
-  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(w.cub, tb, w.head, w.gidx, nC + 1, st));
-  k_triple_k<<<grid_for(nT), 256, 0, st>>>(t2, nT, a_keys, g.nbl, g.lbits, w.tk);
-  QM_LAUNCHED("k_triple_k");
-  const int merge_grid = (int)std::min<int64_t>((nC + 7) / 8, 148 * 64);
-  k_group_merge<<<merge_grid, 256, 0, st>>>(c_keys, c_tptr, t2, w.tk, nC, mbits, w.head, w.gidx, w.ucount,
-                                            w.gfirst, w.gmask, w.entries, w.n_groups);
-  QM_LAUNCHED("k_group_merge");
-  CUtensorMap ma, mb;
-  int rc = make_map(&ma, A, nA, kBlk, kBlk);
-  if (rc != QM_OK) return rc;
-  rc = make_map(&mb, B, nB, kBlk, kBlk);
-  if (rc != QM_OK) return rc;
-  static PerDeviceOnce once;
-  rc = once.run([]() -> int {
-    QM_CUDA_TRY(cudaFuncSetAttribute(k_numeric_group16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
-    return (int)QM_OK;
-  });
-  if (rc != QM_OK) return rc;
-  QM_CUDA_TRY(cudaMemsetAsync(w.counter, 0, sizeof(unsigned long long), st));
-  int per_sm = 0;
-  QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_numeric_group16, kThreads, kSmem));
-  if (per_sm < 1) per_sm = 1;
-  int64_t grid = (int64_t)device_sm_count() * per_sm;
-  if (grid > nC) grid = nC;  // groups <= C blocks
-  k_numeric_group16<<<(int)grid, kThreads, kSmem, st>>>(ma, mb, w.entries, c_tptr, w.ucount, w.gfirst, w.gmask,
-                                                         w.n_groups,
-                                                         C, csq, cnz, zc, w.counter, /*zmask=*/0ull);
-  QM_LAUNCHED("k_numeric_group16");
-  return QM_OK;
+  if (group_rows(g) == 2)
+    return launch_group<2>(g, A, nA, B, nB, a_keys, t2, c_tptr, c_keys, nC, nT, C, csq, cnz, zc, w, st);
+  return launch_group<1>(g, A, nA, B, nB, a_keys, t2, c_tptr, c_keys, nC, nT, C, csq, cnz, zc, w, st);
 }
 
 }  // namespace qm

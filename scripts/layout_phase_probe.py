@@ -1,5 +1,6 @@
 """Per-phase device time of the product for the reference's default-style layouts (leaf 128 with
-bs 16/32/64), TMA vs cp.async numeric kernel (QM_NUMERIC)."""
+bs 16/32/64), TMA vs cp.async numeric kernel (QM_NUMERIC); bs 16 also with single-row groups
+(QM_GROUP_ROWS=1)."""
 import os
 import sys
 
@@ -23,8 +24,9 @@ for leaf, bs in ((128, 16), (128, 32), (32, 32), (128, 64)):
     a = ses.matrix_from_triplets(n, rows, cols, vals, leaf_dim=leaf, block_size=bs)
     layout = _ffi.make_layout(a.params, bs)
     bsx = a.root.require()
-    for impl in ("tma", "cpasync"):
-        os.environ["QM_NUMERIC"] = impl
+    for impl in (("tma", "tma-rows1", "cpasync") if bs == 16 else ("tma", "cpasync")):
+        os.environ["QM_NUMERIC"] = impl.split("-")[0]
+        os.environ["QM_GROUP_ROWS"] = "1" if impl.endswith("rows1") else "2"
         res = []
         for it in range(6):
             ev = {k: E() for k in ("symbolic", "numeric", "end")}
@@ -34,5 +36,5 @@ for leaf, bs in ((128, 16), (128, 32), (32, 32), (128, 64)):
             if it >= 2:
                 res.append((ev["symbolic"].elapsed_time(ev["numeric"]), ev["numeric"].elapsed_time(ev["end"])))
         sym, num = np.median(np.array(res), axis=0)
-        print(f"leaf {leaf} bs {bs} {impl:8s}: T={st.n_triples} nC={st.n_c_symbolic} symbolic {sym:.3f} ms "
+        print(f"leaf {leaf} bs {bs} {impl:10s}: T={st.n_triples} nC={st.n_c_symbolic} symbolic {sym:.3f} ms "
               f"numeric {num:.3f} ms = {st.flops / num / 1e9:.2f} TFLOP/s")

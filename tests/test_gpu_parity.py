@@ -650,3 +650,18 @@ def test_bs16_grouped_kernel_vs_oracle(ses, n, leaf, dens):
     assert helpers.rel(c.root.blockset.blocks.cpu().numpy(), bc) <= TOL
     np.testing.assert_allclose(c.root.blockset.sumsq.cpu().numpy(), np.einsum("nij,nij->n", bc, bc), rtol=1e-12)
     assert helpers.rel(ses.to_dense(c), da @ db) <= TOL
+
+
+@pytest.mark.parametrize("n,leaf,dens", [(1000, 128, 0.02), (500, 48, 0.05), (2048, 128, 0.3), (600, 32, 0.1)])
+def test_bs16_row_pair_groups_bitwise_equal_single_row(ses, monkeypatch, n, leaf, dens):
+    """Leaf row pairs (R = 2 groups: each B block feeds both rows) change only which products share
+    a pipeline stage; every C block still sums its own triples k-ascending with the same fragment
+    order, so the result is bitwise the single-row grouping's (QM_GROUP_ROWS=1)."""
+    da, db = helpers.random_sparse(n, dens, n + 5), helpers.random_sparse(n, dens, n + 6)
+    a, b = helpers.build(ses, da, leaf, 16), helpers.build(ses, db, leaf, 16)
+    c2 = ses.multiply(a, b).root.blockset
+    monkeypatch.setenv("QM_GROUP_ROWS", "1")
+    c1 = ses.multiply(a, b).root.blockset
+    assert torch.equal(c1.keys, c2.keys)
+    assert torch.equal(c1.blocks, c2.blocks) and torch.equal(c1.sumsq, c2.sumsq)
+    assert helpers.rel(ses.to_dense(ses.multiply(a, b)), da @ db) <= TOL
