@@ -140,8 +140,9 @@ QM_API int qm_spgemm_fill_triples(const qm_layout *layout, int64_t nA, int64_t n
  * workspace (qm_numeric_workspace_bytes) and are combined in a fixed order. nT = c_tptr[nC] (the
  * triple count, known to the caller from qm_spgemm_count) selects the kernel variant: few triples
  * per C block favour deeper prefetch, many favour more resident CTAs. a_keys / c_keys (the A and C
- * quadtree keys) are used for bs 16 only, where the C blocks of one leaf row segment are computed
- * together so that they share their A blocks (NULL: per-block kernel). */
+ * quadtree keys) are used for bs 16, where the C blocks of one leaf row (pair) segment are computed
+ * together so that they share their A and B blocks (NULL: per-block kernel), and by the optional
+ * claim orders of the bs 32/64/128 kernel (QM_UNIT_ORDER=k|lpt; default quadtree-key order). */
 QM_API size_t qm_numeric_workspace_bytes(int32_t block_size, int64_t nC, int64_t nT);
 QM_API int qm_numeric(const qm_layout *layout, const uint64_t *a_keys, const double *a_blocks, int64_t nA,
                const double *b_blocks, int64_t nB, const uint32_t *tri, const int64_t *c_tptr,

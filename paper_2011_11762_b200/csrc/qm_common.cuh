@@ -81,6 +81,14 @@ struct Geometry {
   int64_t nbg;    // blocks per matrix side = nbl << depth
 };
 
+// What the numeric kernel needs to choose a claim order other than quadtree-key order (the A keys
+// and the layout; a_keys = NULL keeps key order).
+struct OrderInfo {
+  const uint64_t *a_keys = nullptr;
+  int32_t nbl = 1, lbits = 0;
+  int64_t nbg = 1;
+};
+
 inline int make_geometry(const qm_layout *l, Geometry *g) {
   if (!l) { set_error("layout is NULL"); return QM_ERR_INVALID; }
   if (l->block_size < 1 || l->leaf_dim < 1 || l->depth < 0 || l->n_logical < 1) {

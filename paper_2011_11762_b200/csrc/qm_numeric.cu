@@ -337,8 +337,8 @@ int numeric_sm_count() { return sm_count(); }
 
 int launch_numeric_tma(int bs, const double *const *A, const int64_t *nA, int na, const double *const *B,
                        const int64_t *nB, int nb, const uint32_t *tri, const int64_t *tptr, int64_t nC,
-                       int64_t nT, double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws,
-                       size_t ws_bytes, cudaStream_t st);
+                       int64_t nT, const OrderInfo &oi, double *C, double *csq, uint8_t *cnz, int64_t *zc,
+                       void *ws, size_t ws_bytes, cudaStream_t st);
 size_t numeric_tma_ws_bytes(int bs, int64_t nC);
 size_t numeric_group16_ws_bytes(int64_t nC, int64_t nT);
 int launch_numeric_group16(const Geometry &g, const double *A, int64_t nA, const double *B, int64_t nB,
@@ -387,7 +387,12 @@ extern "C" int qm_numeric(const qm_layout *layout, const uint64_t *a_keys, const
     if (rc != QM_ERR_UNSUPPORTED) return rc;
   }
   if (numeric_impl() == 2) {
-    rc = launch_numeric_tma(g.bs, &a_blocks, &nA, 1, &b_blocks, &nB, 1, tri, c_tptr, nC, nT, c_blocks,
+    OrderInfo oi;
+    oi.a_keys = a_keys;
+    oi.nbl = g.nbl;
+    oi.lbits = g.lbits;
+    oi.nbg = g.nbg;
+    rc = launch_numeric_tma(g.bs, &a_blocks, &nA, 1, &b_blocks, &nB, 1, tri, c_tptr, nC, nT, oi, c_blocks,
                             c_sumsq, c_nonzero, zero_count, ws, ws_bytes, st);
     if (rc != QM_ERR_UNSUPPORTED) return rc;
   }
@@ -429,6 +434,6 @@ extern "C" int qm_numeric_pools(const qm_layout *layout, const double *const *a_
     return QM_ERR_INVALID;
   }
   return launch_numeric_tma(g.bs, a_pools, a_counts, n_a_pools, b_pools, b_counts, n_b_pools, tri, c_tptr,
-                            nC, nT, c_blocks, c_sumsq, c_nonzero, zero_count, ws, ws_bytes,
+                            nC, nT, OrderInfo(), c_blocks, c_sumsq, c_nonzero, zero_count, ws, ws_bytes,
                             (cudaStream_t)stream);
 }

@@ -19,6 +19,8 @@
 //    Each k in 0..15 is used exactly once per panel, so the sum is unchanged.
 #include <algorithm>
 
+#include <cub/cub.cuh>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -72,21 +74,25 @@ struct __align__(64) TmaMaps {
 };
 
 // Stage cursor over work units u = m * NQ + q (C block m, tile q), triple t, k panel p.
+// `unit` is the claim index; `mu` the work unit it maps to (C block order[unit / NQ], tile unit % NQ;
+// order = NULL: the identity, quadtree-key order).
 struct Cur {
-  int64_t unit, t, tend;
+  int64_t unit, mu, t, tend;
   int p;
 };
 
 template <class Cfg>
-__device__ __forceinline__ void cur_start(Cur &c, int64_t unit, int64_t nU, const int64_t *tptr) {
+__device__ __forceinline__ void cur_start(Cur &c, int64_t unit, int64_t nU, const int64_t *tptr,
+                                          const uint32_t *order) {
   c.unit = unit;
   c.p = 0;
   if (unit < nU) {
-    const int64_t m = unit / Cfg::NQ;
+    const int64_t m = order ? (int64_t)order[unit / Cfg::NQ] : unit / Cfg::NQ;
+    c.mu = m * Cfg::NQ + unit % Cfg::NQ;
     c.t = tptr[m];
     c.tend = tptr[m + 1];
   } else {
-    c.t = c.tend = 0;
+    c.mu = c.t = c.tend = 0;
   }
 }
 
@@ -94,11 +100,12 @@ __device__ __forceinline__ void cur_start(Cur &c, int64_t unit, int64_t nU, cons
 // global work counter just in time (claiming a unit ahead widened the window of units in flight
 // and raised DRAM re-reads of A/B by 2x with 3 CTAs/SM).
 template <class Cfg>
-__device__ __forceinline__ void cur_next(Cur &c, int64_t nU, const int64_t *tptr,
+__device__ __forceinline__ void cur_next(Cur &c, int64_t nU, const int64_t *tptr, const uint32_t *order,
                                          unsigned long long *counter) {
   if (++c.p == Cfg::NP) {
     c.p = 0;
-    if (++c.t == c.tend) cur_start<Cfg>(c, (int64_t)gridDim.x + (int64_t)atomicAdd(counter, 1ull), nU, tptr);
+    if (++c.t == c.tend)
+      cur_start<Cfg>(c, (int64_t)gridDim.x + (int64_t)atomicAdd(counter, 1ull), nU, tptr, order);
   }
 }
 
@@ -109,7 +116,7 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
                   double *__restrict__ C, double *__restrict__ csq, uint8_t *__restrict__ cnz,
                   int64_t *__restrict__ zero_count, double *__restrict__ part_sq,
                   uint8_t *__restrict__ part_nz, unsigned long long *__restrict__ counter,
-                  uint64_t zmask) {
+                  const uint32_t *__restrict__ order, uint64_t zmask) {
   constexpr int BS = Cfg::BS, MT = Cfg::MT, NT = Cfg::NT, STAGES = Cfg::STAGES;
   const int64_t nU = nC * Cfg::NQ;
   // Align to 1 KB (SWIZZLE_128B atoms) by offsetting the __shared__ array itself: the pointer keeps
@@ -143,7 +150,7 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
       // counter in key order (so concurrently running CTAs still share A/B rows/columns in L2)
       // and no CTA is left with a long tail of heavy units.
       Cur L;
-      cur_start<Cfg>(L, blockIdx.x, nU, tptr);
+      cur_start<Cfg>(L, blockIdx.x, nU, tptr, order);
       int s = 0;
       uint32_t phase = 0;
       while (true) {
@@ -156,10 +163,10 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
         const uint2 ab = tri[L.t];
         const uint32_t ao = NPOOL > 1 ? ab.x >> kOwnerShift : 0u, al = NPOOL > 1 ? ab.x & kLocalMask : ab.x;
         const uint32_t bo = NPOOL > 1 ? ab.y >> kOwnerShift : 0u, bl = NPOOL > 1 ? ab.y & kLocalMask : ab.y;
-        const int qt = (int)(L.unit % Cfg::NQ);
+        const int qt = (int)(L.mu % Cfg::NQ);
         const int row0 = (qt / Cfg::NQN) * Cfg::TILE, col0 = (qt % Cfg::NQN) * Cfg::TILE;
         uint8_t *st = smem + (size_t)s * Cfg::STAGE_BYTES;
-        meta[s] = L.unit * 2 + ((L.p == Cfg::NP - 1 && L.t + 1 == L.tend) ? 1 : 0);
+        meta[s] = L.mu * 2 + ((L.p == Cfg::NP - 1 && L.t + 1 == L.tend) ? 1 : 0);
         mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
 #pragma unroll
         for (int q = 0; q < Cfg::KSP; ++q)
@@ -169,7 +176,7 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
         for (int q = 0; q < Cfg::NSP; ++q)
           tma_load_2d(st + Cfg::A_BYTES + q * Cfg::B_SP_BYTES, &maps.b[bo], col0 + q * 16,
                       (int)(bl * BS + L.p * Cfg::KP), &full[s]);
-        cur_next<Cfg>(L, nU, tptr, counter);
+        cur_next<Cfg>(L, nU, tptr, order, counter);
         if (++s == STAGES) {
           s = 0;
           phase ^= 1u;
@@ -302,19 +309,84 @@ __global__ void k_combine_tiles(const double *part_sq, const uint8_t *part_nz, i
   }
 }
 
+// Claim-order key of each C block: lpt = 0: the k (block column of the A block) of its first
+// triple; lpt = 1: the complement of its triple count (longest k list first).
+__global__ void k_order_key(const uint2 *tri, const int64_t *tptr, const uint64_t *a_keys, int64_t nC, int nbl,
+                            int lbits, int lpt, uint32_t *key, uint32_t *iota) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nC; c += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t bi, bj = 0;
+    const int64_t t = tptr[c], n = tptr[c + 1] - t;
+    if (lpt) bj = ~(uint32_t)(n < 0xffffffffll ? n : 0xffffffffll);
+    else if (n > 0) qkey_decode(a_keys[tri[t].x], nbl, lbits, &bi, &bj);
+    key[c] = bj;
+    iota[c] = (uint32_t)c;
+  }
+}
+
 int sm_count_tma() { return device_sm_count(); }
 
-// Workspace: the work counter (256 B), then per-warp partial norms / nonzero flags of every tile.
+// Claim order of the C blocks. Quadtree-key order is the default: neighbouring block rows and
+// columns of A/B stay in L2 when C blocks have several triples (banded, decay). Two alternatives,
+// measured and kept as options (QM_UNIT_ORDER=k|lpt):
+//  * k: by the k of each C block's first triple, so the blocks sharing A(., k) and B(k, .) run
+//    together -- for about one triple per C block and no locality (random patterns, C3). On C3
+//    (ncu, r45) DRAM reads fall 2.39 -> 0.65 GB per launch at the same kernel time (1.082 ms, DMMA
+//    pipe 88%): the kernel is not DRAM-bound there, and the ordering sort costs ~20 us.
+//  * lpt: longest k list first, against a tail of CTAs that claimed long lists last. On C1 (1,016
+//    C blocks, 296 CTAs, L2-resident) the numeric phase went 0.138 -> 0.141 ms (r48).
+// Processing order never changes a C block's own summation order: results are bitwise the same.
+enum { kOrderKey = 0, kOrderK = 1, kOrderLpt = 2 };
+int claim_order() {
+  const char *e = getenv("QM_UNIT_ORDER");
+  if (e && strcmp(e, "k") == 0) return kOrderK;
+  if (e && strcmp(e, "lpt") == 0) return kOrderLpt;
+  return kOrderKey;
+}
+
+size_t order_cub_bytes(int64_t nC) {
+  size_t b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, b, (uint32_t *)nullptr, (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                  (uint32_t *)nullptr, (int64_t)std::max<int64_t>(nC, 1), 0, 32);
+  return b;
+}
+
+// Workspace: the work counter (256 B), per-warp partial norms / nonzero flags of every tile, then
+// the claim-order arrays (4 x nC uint32 + radix-sort scratch).
+template <class Cfg>
+size_t tma_ws_base(int64_t nC) {
+  return align_up(256 + (size_t)nC * Cfg::NQ * Cfg::NCW * (sizeof(double) + sizeof(uint8_t)) + 256);
+}
 template <class Cfg>
 size_t tma_ws_bytes(int64_t nC) {
-  return 256 + (size_t)nC * Cfg::NQ * Cfg::NCW * (sizeof(double) + sizeof(uint8_t)) + 256;
+  return tma_ws_base<Cfg>(nC) + align_up(4 * sizeof(uint32_t) * (size_t)nC) + align_up(order_cub_bytes(nC));
+}
+
+// Fills the claim order (k of each C block's first triple, stable radix sort) into the workspace
+// tail; returns the order array.
+template <class Cfg>
+int make_order(int kind, const uint2 *tri, const int64_t *tptr, const uint64_t *a_keys, int nbl, int lbits,
+               int64_t nbg, int64_t nC, void *ws, uint32_t **order_out, cudaStream_t st) {
+  char *base = (char *)ws + tma_ws_base<Cfg>(nC);
+  uint32_t *key = (uint32_t *)base, *iota = key + nC, *skey = iota + nC, *order = skey + nC;
+  void *cub_tmp = base + align_up(4 * sizeof(uint32_t) * (size_t)nC);
+  size_t tb = order_cub_bytes(nC);
+  const int grid = (int)std::min<int64_t>((nC + 255) / 256, (int64_t)sm_count_tma() * 8);
+  k_order_key<<<std::max(grid, 1), 256, 0, st>>>(tri, tptr, a_keys, nC, nbl, lbits, kind == kOrderLpt, key,
+                                                  iota);
+  QM_LAUNCHED("k_order_key");
+  int bits = 32;
+  if (kind == kOrderK)
+    for (bits = 1; bits < 32 && ((uint64_t)(nbg - 1) >> bits) != 0;) ++bits;
+  QM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, key, skey, iota, order, nC, 0, bits, st));
+  *order_out = order;
+  return QM_OK;
 }
 
 template <class Cfg, int NPOOL>
 int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const double *const *B,
-                     const int64_t *nB, int nb, const uint2 *tri, const int64_t *tptr, int64_t nC,
-                     double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes,
-                     cudaStream_t st) {
+                     const int64_t *nB, int nb, const uint2 *tri, const int64_t *tptr, int64_t nC, int64_t nT,
+                     const OrderInfo &oi, double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws,
+                     size_t ws_bytes, cudaStream_t st) {
   if (na < 1 || nb < 1 || na > NPOOL || nb > NPOOL) {
     set_error("qm_numeric: %d / %d operand pools (at most %d)", na, nb, NPOOL);
     return QM_ERR_INVALID;
@@ -359,8 +431,16 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
   const int64_t nU = nC * Cfg::NQ;
   int64_t grid = (int64_t)sm_count_tma() * per_sm;
   if (grid > nU) grid = nU;
+  uint32_t *order = nullptr;
+  if (oi.a_keys && na == 1 && nb == 1) {
+    const int kind = claim_order();
+    if (kind != kOrderKey) {
+      rc = make_order<Cfg>(kind, tri, tptr, oi.a_keys, oi.nbl, oi.lbits, oi.nbg, nC, ws, &order, st);
+      if (rc != QM_OK) return rc;
+    }
+  }
   k_numeric_tma<Cfg, NPOOL><<<(int)grid, Cfg::NTHR, Cfg::SMEM, st>>>(
-      maps, tri, tptr, nC, C, csq, cnz, zc, part_sq, part_nz, counter, /*zmask=*/0ull);
+      maps, tri, tptr, nC, C, csq, cnz, zc, part_sq, part_nz, counter, order, /*zmask=*/0ull);
   QM_LAUNCHED("k_numeric_tma");
   {
     int64_t g = std::min<int64_t>((nC + 255) / 256, (int64_t)sm_count_tma() * 8);
@@ -373,12 +453,14 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
 
 template <class Cfg>
 int launch_tma(const double *const *A, const int64_t *nA, int na, const double *const *B,
-               const int64_t *nB, int nb, const uint2 *tri, const int64_t *tptr, int64_t nC, double *C,
-               double *csq, uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes, cudaStream_t st) {
+               const int64_t *nB, int nb, const uint2 *tri, const int64_t *tptr, int64_t nC, int64_t nT,
+               const OrderInfo &oi, double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes,
+               cudaStream_t st) {
   if (na == 1 && nb == 1)
-    return launch_tma_pools<Cfg, 1>(A, nA, na, B, nB, nb, tri, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
-  return launch_tma_pools<Cfg, kMaxPools>(A, nA, na, B, nB, nb, tri, tptr, nC, C, csq, cnz, zc, ws, ws_bytes,
-                                          st);
+    return launch_tma_pools<Cfg, 1>(A, nA, na, B, nB, nb, tri, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes,
+                                    st);
+  return launch_tma_pools<Cfg, kMaxPools>(A, nA, na, B, nB, nb, tri, tptr, nC, nT, oi, C, csq, cnz, zc, ws,
+                                          ws_bytes, st);
 }
 
 //                     BS TILE WM WN KP STAGES MINB
@@ -422,19 +504,20 @@ size_t numeric_tma_ws_bytes(int bs, int64_t nC) {
 // local; > 1 = every rank's pool, triple indices packed as owner << 28 | local).
 int launch_numeric_tma(int bs, const double *const *A, const int64_t *nA, int na, const double *const *B,
                        const int64_t *nB, int nb, const uint32_t *tri, const int64_t *tptr, int64_t nC,
-                       int64_t nT, double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws,
-                       size_t ws_bytes, cudaStream_t st) {
+                       int64_t nT, const OrderInfo &oi, double *C, double *csq, uint8_t *cnz, int64_t *zc,
+                       void *ws, size_t ws_bytes, cudaStream_t st) {
   const uint2 *t2 = (const uint2 *)tri;
   switch (bs) {
-    case 32: return launch_tma<Tma32>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
+    case 32:
+      return launch_tma<Tma32>(A, nA, na, B, nB, nb, t2, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes, st);
     case 64:
       if (use_wide(nC, nC, nT))
-        return launch_tma<Tma64m>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
-      return launch_tma<Tma64>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
+        return launch_tma<Tma64m>(A, nA, na, B, nB, nb, t2, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes, st);
+      return launch_tma<Tma64>(A, nA, na, B, nB, nb, t2, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes, st);
     case 128:
       if (use_wide(nC * Tma128::NQ, nC, nT))
-        return launch_tma<Tma128m>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
-      return launch_tma<Tma128>(A, nA, na, B, nB, nb, t2, tptr, nC, C, csq, cnz, zc, ws, ws_bytes, st);
+        return launch_tma<Tma128m>(A, nA, na, B, nB, nb, t2, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes, st);
+      return launch_tma<Tma128>(A, nA, na, B, nB, nb, t2, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes, st);
     default: return QM_ERR_UNSUPPORTED;
   }
 }

@@ -665,3 +665,30 @@ def test_bs16_row_pair_groups_bitwise_equal_single_row(ses, monkeypatch, n, leaf
     assert torch.equal(c1.keys, c2.keys)
     assert torch.equal(c1.blocks, c2.blocks) and torch.equal(c1.sumsq, c2.sumsq)
     assert helpers.rel(ses.to_dense(ses.multiply(a, b)), da @ db) <= TOL
+
+
+@pytest.mark.parametrize("bs,n", [(64, 65536), (32, 16384), (128, 32768), (64, 8192)])
+def test_claim_order_is_bitwise_neutral(ses, monkeypatch, bs, n):
+    """Claim orders of the numeric kernel: QM_UNIT_ORDER=k (by the k of each C block's first triple:
+    A(., k) and B(k, .) reused from L2 on random patterns, C3's shape) and lpt (longest k list first),
+    at bs 32/64 and bs 128's 4-tile
+    blocks. Only the processing order changes: the result is bitwise the key-order product's, and
+    the C3-sized case also matches the oracle on sampled block rows."""
+    cfg = G.BaselineConfig("t", "random", n, bs, per_row=8)
+    geom, a, b = G.config_operands_device(cfg, ses.device)
+    ma, mb = ses.matrix_from_blockset(geom, a), ses.matrix_from_blockset(geom, b)
+    monkeypatch.setenv("QM_UNIT_ORDER", "key")
+    c0 = ses.multiply(ma, mb).root.blockset
+    for kind in ("k", "lpt"):
+        monkeypatch.setenv("QM_UNIT_ORDER", kind)
+        c1 = ses.multiply(ma, mb).root.blockset
+        assert torch.equal(c0.keys, c1.keys)
+        assert torch.equal(c0.blocks, c1.blocks) and torch.equal(c0.sumsq, c1.sumsq)
+    if n == 65536:
+        _, (ka, ba), (kb, bb) = G.config_operands_host(cfg)
+        ai, _ = geom.decode(ka)
+        rows = np.r_[0, np.random.default_rng(5).choice(geom.nbg, 6, replace=False), geom.nbg - 1]
+        sel = np.isin(ai, rows)
+        kc, bc, _ = O.multiply(O.Geom(cfg.n, cfg.bs, cfg.bs), ka[sel], ba[sel], kb, bb)
+        got = helpers.lookup(c1.keys.cpu().numpy(), c1.blocks, kc)
+        assert helpers.rel(got, bc) <= TOL
