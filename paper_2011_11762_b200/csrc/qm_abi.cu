@@ -31,8 +31,7 @@ __global__ void k_read_i64(const int64_t *src, int n, const int64_t *src2, volat
   if (src2 && threadIdx.x == 0) dst[n] = *src2;
 }
 
-int read_device_i64(const void *dev_src, int n, int64_t *host_out, cudaStream_t stream,
-                    const void *dev_src2) {
+int mapped_i64(int64_t **host, int64_t **dev) {
   struct Mapped {
     int64_t *host = nullptr, *dev = nullptr;
     int device = -1;
@@ -45,6 +44,18 @@ int read_device_i64(const void *dev_src, int n, int64_t *host_out, cudaStream_t 
     QM_CUDA_TRY(cudaHostGetDevicePointer((void **)&m.dev, m.host, 0));
     m.device = device;
   }
+  *host = m.host;
+  *dev = m.dev;
+  return QM_OK;
+}
+
+int read_device_i64(const void *dev_src, int n, int64_t *host_out, cudaStream_t stream,
+                    const void *dev_src2) {
+  struct {
+    int64_t *host = nullptr, *dev = nullptr;
+  } m;
+  int rc = mapped_i64(&m.host, &m.dev);
+  if (rc != QM_OK) return rc;
   if (n < 1 || n > 8) {
     set_error("read_device_i64: n=%d out of range", n);
     return QM_ERR_INVALID;

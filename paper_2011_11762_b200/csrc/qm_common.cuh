@@ -18,6 +18,9 @@ void set_error(const char *fmt, ...);
 // An optional second source appends one more value (two scattered counts, one synchronisation).
 int read_device_i64(const void *dev_src, int n, int64_t *host_out, cudaStream_t stream,
                     const void *dev_src2 = nullptr);
+// The calling thread's mapped pinned buffer (8 int64) used by read_device_i64: a kernel may write
+// values there itself (device pointer `dev`) and the host read them after synchronising the stream.
+int mapped_i64(int64_t **host, int64_t **dev);
 // Counts one kernel launch (qm_launch_count).
 void note_launch(int n = 1);
 

@@ -27,7 +27,9 @@ constexpr int kPer = kWin / kNT;
 // Row keys of both operands in one array: A entry t -> row(t), B entry t -> nbg + row(t); the
 // value carried through the sort is the entry's index within its own operand.
 __global__ void k_decode_rows(const uint64_t *a_keys, int64_t nA, const uint64_t *b_keys, int64_t nB,
-                              int64_t nbg, int nbl, int lbits, uint32_t *rowkey, uint32_t *val) {
+                              int64_t nbg, int nbl, int lbits, uint32_t *rowkey, uint32_t *val,
+                              unsigned int *done) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *done = 0u;  // k_sym_count's completion ticket
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nA + nB;
        x += (int64_t)gridDim.x * blockDim.x) {
     const bool is_b = x >= nA;
@@ -99,6 +101,43 @@ __device__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *total, uint32_t *
   return before + inc - v;
 }
 
+// Exclusive scan of one uint64 per thread (block-wide); returns the prefix and the block total.
+__device__ uint64_t block_exclusive_scan64(uint64_t v, uint64_t *total, uint64_t *wsum /* smem[32] */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint64_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  __syncthreads();
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  uint64_t before = 0, tot = 0;
+  for (int w = 0; w < nw; ++w) {
+    if (w < warp) before += wsum[w];
+    tot += wsum[w];
+  }
+  *total = tot;
+  return before + inc - v;
+}
+
+// Exclusive scan of x[0, n) into y by one CTA (contiguous chunk per thread, in index order).
+__device__ void cta_exclusive_scan64(const uint64_t *x, uint64_t *y, int64_t n, uint64_t *wsum) {
+  const int64_t per = (n + blockDim.x - 1) / blockDim.x;
+  const int64_t lo0 = (int64_t)threadIdx.x * per;
+  const int64_t lo = lo0 < n ? lo0 : n, hi = lo + per < n ? lo + per : n;
+  uint64_t part = 0;
+  for (int64_t q = lo; q < hi; ++q) part += x[q];
+  uint64_t total;
+  uint64_t run = block_exclusive_scan64(part, &total, wsum);
+  for (int64_t q = lo; q < hi; ++q) {
+    const uint64_t v = x[q];
+    y[q] = run;
+    run += v;
+  }
+}
+
 struct RowSpan {
   uint32_t a0, a1;     // A row entries
   uint64_t nt;         // triples of the row
@@ -158,12 +197,18 @@ __device__ void for_window_pairs(const RowSpan &s, uint32_t wbase, bool multi, c
   }
 }
 
+// Per row i: cnt[i] = C blocks, cnt[nbg + i] = triples. The last CTA to finish (ticket on `done`,
+// zeroed by k_decode_rows) scans cnt into off (C-row offsets, then triple-row offsets) and writes
+// the totals (nC, nT) into the caller's mapped host buffer -- one launch instead of count + scan +
+// read-back.
 __global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const uint32_t *a_scol,
                                                    const uint32_t *b_rp, const uint32_t *b_scol,
-                                                   int64_t nbg, uint64_t *cnt) {
+                                                   int64_t nbg, uint64_t *cnt, uint64_t *off,
+                                                   unsigned int *done, volatile int64_t *host_tot) {
   __shared__ uint32_t bm[kWin / 32];
   __shared__ uint64_t red64[32];
   __shared__ uint32_t red32[32];
+  __shared__ bool last;
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt[2 * nbg] = 0;  // exclusive-scan tail
   for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
     RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
@@ -189,6 +234,19 @@ __global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const u
       cnt[nbg + i] = s.nt;
     }
     __syncthreads();
+  }
+  __threadfence();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  cta_exclusive_scan64((const uint64_t *)cnt, off, 2 * nbg + 1, red64);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint64_t n_c = ((volatile uint64_t *)off)[nbg], tail = ((volatile uint64_t *)off)[2 * nbg];
+    host_tot[0] = (int64_t)n_c;
+    host_tot[1] = (int64_t)(tail - n_c);
+    __threadfence_system();
   }
 }
 
@@ -371,6 +429,7 @@ struct SymWs {
   uint32_t *rowkey, *val, *srow, *perm, *scol, *rp;
   uint64_t *cnt;   // [2*nbg+1]: C blocks per row, triples per row, 0
   uint64_t *off;   // exclusive scan of cnt: rowC_off = off, nC = off[nbg], nT = off[2nbg] - off[nbg]
+  unsigned int *done;  // k_sym_count's completion ticket
   void *cub;
   size_t cub_bytes;
 };
@@ -392,6 +451,7 @@ SymWs carve_sym(Carver &cv, int64_t nA, int64_t nB, int64_t nbg) {
   w.rp = cv.take<uint32_t>(2 * nbg + 1);
   w.cnt = cv.take<uint64_t>(2 * nbg + 1);
   w.off = cv.take<uint64_t>(2 * nbg + 1);
+  w.done = cv.take<unsigned int>(1);
   w.cub_bytes = cub_bytes_count(n, nbg);
   w.cub = cv.take<char>(w.cub_bytes);
   return w;
@@ -429,7 +489,7 @@ int build_rows(const uint64_t *a_keys, int64_t nA, const uint64_t *b_keys, int64
   const int64_t n = nA + nB;
   if (n > 0) {
     k_decode_rows<<<grid_for(n), 256, 0, st>>>(a_keys, nA, b_keys, nB, g.nbg, g.nbl, g.lbits,
-                                                w.rowkey, w.val);
+                                                w.rowkey, w.val, w.done);
     QM_LAUNCHED("k_decode_rows");
     size_t tb = w.cub_bytes;
     QM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.cub, tb, w.rowkey, w.srow, w.val, w.perm, n, 0,
@@ -483,14 +543,15 @@ extern "C" int qm_spgemm_count(const qm_layout *layout, const uint64_t *a_keys, 
   rc = build_rows(a_keys, nA, b_keys, nB, g, w, st);
   if (rc != QM_OK) return rc;
   const uint32_t *a_rp = w.rp, *b_rp = w.rp + g.nbg;
-  k_sym_count<<<row_grid(g.nbg), kNT, 0, st>>>(a_rp, w.scol, b_rp, w.scol, g.nbg, w.cnt);
-  QM_LAUNCHED("k_sym_count");
-  size_t tb = w.cub_bytes;
-  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(w.cub, tb, w.cnt, w.off, 2 * g.nbg + 1, st));
-  uint64_t tot[2];
-  rc = read_device_i64(w.off + g.nbg, 1, (int64_t *)tot, st, w.off + 2 * g.nbg);
+  if (nA + nB == 0) QM_CUDA_TRY(cudaMemsetAsync(w.done, 0, sizeof(unsigned int), st));  // no k_decode_rows
+  int64_t *host_tot = nullptr, *dev_tot = nullptr;
+  rc = mapped_i64(&host_tot, &dev_tot);
   if (rc != QM_OK) return rc;
-  tot[1] -= tot[0];
+  k_sym_count<<<row_grid(g.nbg), kNT, 0, st>>>(a_rp, w.scol, b_rp, w.scol, g.nbg, w.cnt, w.off, w.done,
+                                               dev_tot);
+  QM_LAUNCHED("k_sym_count");
+  QM_CUDA_TRY(cudaStreamSynchronize(st));
+  uint64_t tot[2] = {(uint64_t)((volatile int64_t *)host_tot)[0], (uint64_t)((volatile int64_t *)host_tot)[1]};
   if (tot[0] >= (1ull << 32)) {
     set_error("product has %llu C blocks; this build indexes C with 32 bits", (unsigned long long)tot[0]);
     return QM_ERR_UNSUPPORTED;
