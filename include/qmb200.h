@@ -134,8 +134,8 @@ QM_API int qm_spgemm_fill_triples(const qm_layout *layout, int64_t nA, int64_t n
 /* ---- numeric phase (replaces BlockSparseLeaf.multiply + add, block_sparse.py:112-152) ------- */
 /* c_blocks[m] = sum over t in [c_tptr[m], c_tptr[m+1]) of A[tri[2t]] * B[tri[2t+1]] (fp64),
  * c_sumsq[m] = squared Frobenius norm of the block, c_nonzero[m] = any entry != 0
- * (the np.any test of _set_block, block_sparse.py:37-41). *zero_count (device, int64) is
- * incremented once per exactly-zero C block; the caller zeroes it first. Block sizes above the
+ * (the np.any test of _set_block, block_sparse.py:37-41). *zero_count (device, int64) is set
+ * to the number of exactly-zero C blocks (zeroed on the stream first). Block sizes above the
  * 64x64 CTA tile (bs 128) are computed as (bs/64)^2 tiles whose partial norms go to the caller's
  * workspace (qm_numeric_workspace_bytes) and are combined in a fixed order. nT = c_tptr[nC] (the
  * triple count, known to the caller from qm_spgemm_count) selects the kernel variant: few triples

@@ -62,6 +62,27 @@ struct PerDeviceOnce {
   }
 };
 
+// An int computed once per device (e.g. a kernel's occupancy: it never changes for a device).
+struct PerDeviceInt {
+  std::atomic<int> v[64];
+  PerDeviceInt() {
+    for (auto &x : v) x.store(-1, std::memory_order_relaxed);
+  }
+  template <class F>
+  int get(int *out, F f) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    int x = v[dev & 63].load(std::memory_order_relaxed);
+    if (x < 0) {
+      const int rc = f(&x);
+      if (rc != 0) return rc;
+      v[dev & 63].store(x, std::memory_order_relaxed);
+    }
+    *out = x;
+    return 0;
+  }
+};
+
 // SM count of the current device (cached per device).
 inline int device_sm_count() {
   static std::atomic<int> cache[64];

@@ -378,8 +378,9 @@ extern "C" int qm_numeric(const qm_layout *layout, const uint64_t *a_keys, const
     set_error("qm_numeric: negative nC");
     return QM_ERR_INVALID;
   }
-  if (nC == 0) return QM_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  if (zero_count) QM_CUDA_TRY(cudaMemsetAsync(zero_count, 0, sizeof(int64_t), st));
+  if (nC == 0) return QM_OK;
   const uint2 *t2 = (const uint2 *)tri;
   if (numeric_impl() == 2 && g.bs == 16) {
     rc = launch_numeric_group16(g, a_blocks, nA, b_blocks, nB, a_keys, tri, c_tptr, c_keys, nC, nT, c_blocks,
@@ -428,6 +429,7 @@ extern "C" int qm_numeric_pools(const qm_layout *layout, const double *const *a_
   Geometry g;
   int rc = make_geometry(layout, &g);
   if (rc != QM_OK) return rc;
+  if (zero_count) QM_CUDA_TRY(cudaMemsetAsync(zero_count, 0, sizeof(int64_t), (cudaStream_t)stream));
   if (nC <= 0) return nC < 0 ? QM_ERR_INVALID : QM_OK;
   if (!a_pools || !b_pools || !a_counts || !b_counts) {
     set_error("qm_numeric_pools: NULL pool arrays");

@@ -480,8 +480,12 @@ int launch_group(const Geometry &g, const double *A, int64_t nA, const double *B
   if (rc != QM_OK) return rc;
   QM_CUDA_TRY(cudaMemsetAsync(w.counter, 0, sizeof(unsigned long long), st));
   int per_sm = 0;
-  QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_numeric_group16<R>, Cfg::THREADS,
-                                                            Cfg::SMEM));
+  static PerDeviceInt occupancy;  // cudaOccupancy* costs microseconds of host time per call
+  rc = occupancy.get(&per_sm, [](int *x) -> int {
+    QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(x, k_numeric_group16<R>, Cfg::THREADS, Cfg::SMEM));
+    return (int)QM_OK;
+  });
+  if (rc != QM_OK) return rc;
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)device_sm_count() * per_sm;
   if (grid > nC) grid = nC;  // groups <= C blocks

@@ -425,8 +425,12 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
   });
   if (rc != QM_OK) return rc;
   int per_sm = 0;
-  QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_numeric_tma<Cfg, NPOOL>, Cfg::NTHR,
-                                                            Cfg::SMEM));
+  static PerDeviceInt occupancy;  // cudaOccupancy* costs microseconds of host time per call
+  rc = occupancy.get(&per_sm, [](int *x) -> int {
+    QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(x, k_numeric_tma<Cfg, NPOOL>, Cfg::NTHR, Cfg::SMEM));
+    return (int)QM_OK;
+  });
+  if (rc != QM_OK) return rc;
   if (per_sm < 1) per_sm = 1;
   const int64_t nU = nC * Cfg::NQ;
   int64_t grid = (int64_t)sm_count_tma() * per_sm;

@@ -254,10 +254,11 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_c(const uint32_t *a_rp, const 
                                                     const uint32_t *b_rp, const uint32_t *b_scol,
                                                     int64_t nbg, int nbl, int lbits,
                                                     const uint64_t *rowC_off, uint64_t *rm_key,
-                                                    uint32_t *rm_cnt, uint32_t *rm_iota) {
+                                                    uint32_t *rm_cnt, uint32_t *rm_iota, unsigned int *done) {
   __shared__ uint32_t cnt[kWin];
   __shared__ uint64_t red64[32];
   __shared__ uint32_t red32[32];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *done = 0u;  // k_inv_counts' completion ticket
   for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
     RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
     if (s.nt > 0) {
@@ -398,8 +399,13 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
   }
 }
 
+// Inverse of the C-key sort permutation and the per-C-block triple counts in quadtree order. For
+// small products (scan_tptr) the last CTA to finish also scans the counts into c_tptr (one launch
+// instead of this kernel + a CUB scan); `done` is zeroed by k_sym_emit_c.
 __global__ void k_inv_counts(const uint32_t *perm, const uint32_t *rm_cnt, int64_t nC, uint32_t *inv,
-                             int64_t *cnt_q) {
+                             int64_t *cnt_q, int64_t *c_tptr, unsigned int *done) {
+  __shared__ uint64_t wsum[32];
+  __shared__ bool last;
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt_q[nC] = 0;  // exclusive-scan tail
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nC;
        p += (int64_t)gridDim.x * blockDim.x) {
@@ -407,6 +413,14 @@ __global__ void k_inv_counts(const uint32_t *perm, const uint32_t *rm_cnt, int64
     inv[c] = (uint32_t)p;
     cnt_q[p] = rm_cnt[c];
   }
+  if (!c_tptr) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  cta_exclusive_scan64((const uint64_t *)cnt_q, (uint64_t *)c_tptr, nC + 1, wsum);
 }
 
 inline int grid_for(int64_t n, int threads = 256) {
@@ -461,9 +475,13 @@ struct FillWs {
   uint64_t *rm_key;
   uint32_t *rm_cnt, *rm_iota, *perm, *inv;
   int64_t *cnt_q;
+  unsigned int *done;
   void *cub;
   size_t cub_bytes;
 };
+
+// Products with at most this many C blocks scan c_tptr inside k_inv_counts (one CTA).
+constexpr int64_t kFusedTptrScanMax = 32768;
 
 FillWs carve_fill(Carver &cv, int64_t nC, int key_bits) {
   FillWs w;
@@ -473,6 +491,7 @@ FillWs carve_fill(Carver &cv, int64_t nC, int key_bits) {
   w.perm = cv.take<uint32_t>(nC);
   w.inv = cv.take<uint32_t>(nC);
   w.cnt_q = cv.take<int64_t>(nC + 1);
+  w.done = cv.take<unsigned int>(1);
   size_t a = 0, b = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, a, (uint64_t *)nullptr, (uint64_t *)nullptr,
                                   (uint32_t *)nullptr, (uint32_t *)nullptr, (int64_t)nC, 0, key_bits);
@@ -604,15 +623,19 @@ extern "C" int qm_spgemm_fill_keys(const qm_layout *layout, int64_t nA, int64_t 
   cudaStream_t st = (cudaStream_t)stream;
   if (nC == 0) return cudaMemsetAsync(c_tptr, 0, sizeof(int64_t), st) == cudaSuccess ? QM_OK : QM_ERR_CUDA;
   k_sym_emit_c<<<row_grid(g.nbg), kNT, 0, st>>>(w.rp, w.scol, w.rp + g.nbg, w.scol, g.nbg, g.nbl,
-                                                g.lbits, w.off, f.rm_key, f.rm_cnt, f.rm_iota);
+                                                g.lbits, w.off, f.rm_key, f.rm_cnt, f.rm_iota, f.done);
   QM_LAUNCHED("k_sym_emit_c");
   size_t tb = f.cub_bytes;
   QM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(f.cub, tb, f.rm_key, c_keys, f.rm_iota, f.perm, nC, 0,
                                               key_bits, st));
-  k_inv_counts<<<grid_for(nC), 256, 0, st>>>(f.perm, f.rm_cnt, nC, f.inv, f.cnt_q);
+  const bool fused = nC <= kFusedTptrScanMax;
+  k_inv_counts<<<grid_for(nC), 256, 0, st>>>(f.perm, f.rm_cnt, nC, f.inv, f.cnt_q, fused ? c_tptr : nullptr,
+                                             f.done);
   QM_LAUNCHED("k_inv_counts");
-  tb = f.cub_bytes;
-  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(f.cub, tb, f.cnt_q, c_tptr, nC + 1, st));
+  if (!fused) {
+    tb = f.cub_bytes;
+    QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(f.cub, tb, f.cnt_q, c_tptr, nC + 1, st));
+  }
   return QM_OK;
 }
 

@@ -114,8 +114,15 @@ class SymbolicState:
 
 def symbolic(layout, a: BlockSet, b: BlockSet, stream=None) -> SymbolicPlan:
     st = SymbolicState(layout, a.keys, a.n, b.keys, b.n, stream)
-    c_keys, c_tptr = st.keys()
-    tri = st.triples(c_tptr)
+    c_keys = _alloc(st.n_c, torch.int64, st.dev)
+    c_tptr = _alloc(st.n_c + 1, torch.int64, st.dev)
+    tri = _alloc(2 * st.n_t, torch.int32, st.dev)
+    _ffi.check(  # C keys, c_tptr and every triple in one call (keys() + triples() of SymbolicState)
+        st.lib.qm_spgemm_fill(st.lp, st.n_a, st.n_b, st.n_c, st.n_t, _ffi.ptr(st.ws), st.ws_bytes,
+                              _ffi.ptr(st.fws), st.fill_bytes, _ffi.ptr(c_keys), _ffi.ptr(c_tptr),
+                              _ffi.ptr(tri), st.sh),
+        "qm_spgemm_fill",
+    )
     return SymbolicPlan(st.n_c, st.n_t, c_keys, c_tptr, tri)
 
 
@@ -130,7 +137,7 @@ def numeric(layout, a: BlockSet, b: BlockSet, plan: SymbolicPlan, stream=None,
         out = BlockSet(plan.c_keys, _alloc((nc, bs, bs), torch.float64, dev),
                        _alloc(nc, torch.float64, dev))
     nz = _alloc(nc, torch.uint8, dev)
-    zc = torch.zeros(1, dtype=torch.int64, device=dev)
+    zc = _alloc(1, torch.int64, dev)  # qm_numeric zeroes it on the stream
     wb = lib.qm_numeric_workspace_bytes(bs, nc, plan.n_triples)
     ws = _alloc(wb, torch.uint8, dev) if wb else None
     _ffi.check(
