@@ -6,7 +6,9 @@ One step = one full product of the configured BASELINE workload (symbolic phase 
 phase + exact-zero compaction) through the drop-in API's multiply path, inputs resident in HBM
 (inputs are larger than L2, so no flush is needed between steps). Prints ONE JSON line (rank 0).
 
-  metric  leaf-GEMM GFLOP/s (FP64) = 2*bs^3*T / time, T = block triples
+  metric  leaf-GEMM GFLOP/s (FP64) = 2*bs^3*T / time, T = block triples executed (SURVEY.md 8(d);
+          pairs whose nonzero-column / nonzero-row masks do not meet multiply to exact zeros and
+          are skipped -- config.triples_structural is the block-level count)
   e2e     the same metric through MatrixSession.multiply with host (pinned) operands: H2D of A
           and B and D2H of C inside the timed region
   roofline  the numeric kernel (dominant) against the measured FP64 tensor peak (a DMMA
@@ -380,6 +382,7 @@ def run_ours(args):
         "config": {"workload": cfg.name, "kind": cfg.kind, "n": cfg.n, "block_size": bs,
                    "half_bandwidth": cfg.half_bw, "leaf_dim": bs, "nnzb_a": a.n, "nnzb_b": b.n,
                    "nnzb_c": stats.n_c, "triples": stats.n_triples,
+                   "triples_structural": structural_triples(geom, a, b, world),
                    "parallelism": f"keyrange-partition dp{world}" if world > 1 else "single",
                    "l2": (f"working set {work_bytes / 1e6:.0f} MB < 2x L2: L2 flushed between timed "
                           f"steps (a {2 * l2_bytes >> 20} MiB write outside each step's events)" if flush
@@ -432,6 +435,19 @@ def run_ours(args):
         D.release_peer_mappings()
         dist.barrier()
         dist.destroy_process_group()
+
+
+def structural_triples(geom, a, b, world):
+    """Block-level triple count (every (A block, B block) pair with a matching k, as the reference's
+    BlockSparseLeaf.multiply executes them). `triples` counts only the products executed here:
+    pairs whose nonzero-column / nonzero-row masks do not meet multiply to an exact zero and are
+    skipped; the metric uses the executed count."""
+    if world > 1:
+        return None
+    from paper_2011_11762_b200 import _ffi, spgemm
+
+    st = spgemm.SymbolicState(_ffi.make_layout(geom.params, geom.bs), a.keys, a.n, b.keys, b.n)
+    return st.n_t
 
 
 def run_e2e(args, torch, ses, geom, a, b, dev, world, dist):

@@ -112,6 +112,15 @@ QM_API size_t qm_spgemm_workspace_bytes(const qm_layout *layout, int64_t nA, int
 QM_API int qm_spgemm_count(const qm_layout *layout, const uint64_t *a_keys /*device, sorted*/, int64_t nA,
                     const uint64_t *b_keys /*device, sorted*/, int64_t nB, void *ws, size_t ws_bytes,
                     int64_t *n_c_out /*host*/, int64_t *n_triples_out /*host*/, void *stream);
+/* qm_spgemm_count with per-block support masks (NULL = full support): a_cmask[t] / b_rmask[t] are
+ * the nonzero-column mask of A block t and the nonzero-row mask of B block t (qm_block_masks). A
+ * pair whose masks share no bit multiplies to an exactly-zero block: it yields no triple, and a C
+ * block without any surviving triple is not created (it would be an exact-zero block, which
+ * _set_block, block_sparse.py:37-41, drops). The fill calls of the same workspace use the masks too. */
+QM_API int qm_spgemm_count_masked(const qm_layout *layout, const uint64_t *a_keys, const uint64_t *a_cmask,
+                                  int64_t nA, const uint64_t *b_keys, const uint64_t *b_rmask, int64_t nB,
+                                  void *ws, size_t ws_bytes, int64_t *n_c_out, int64_t *n_triples_out,
+                                  void *stream);
 QM_API size_t qm_spgemm_fill_workspace_bytes(const qm_layout *layout, int64_t nC);
 /* Emits the C key set in quadtree-key order (c_keys[nC]), the triple offsets c_tptr[nC+1] and the
  * triples tri[2*nT] = (a_index, b_index) pairs, grouped by C block, k ascending within a group --
@@ -181,6 +190,11 @@ QM_API int qm_compact(int32_t block_size, int64_t nC, const uint8_t *c_nonzero, 
 /* sumsq[i] = sum of squares of block i, nonzero[i] = any entry != 0 (nonzero may be NULL). */
 QM_API int qm_block_stats(int32_t block_size, int64_t n, const double *blocks, double *sumsq,
                    uint8_t *nonzero, void *stream);
+/* Support masks of n bs x bs blocks: bit b of row_mask[m] / col_mask[m] is set when a row / column r
+ * with b = r (bs <= 64) or b = r*64/bs (bs > 64) of block m holds a nonzero; blocks holding NaN or
+ * Inf get full masks. */
+QM_API int qm_block_masks(int32_t block_size, int64_t n, const double *blocks, uint64_t *row_mask,
+                          uint64_t *col_mask, void *stream);
 /* dst[i] = src[idx[i]] for whole bs x bs blocks (packs halo blocks for the NVLink exchange). */
 QM_API int qm_gather_blocks(int32_t block_size, const double *src, const int64_t *idx, int64_t n,
                      double *dst, void *stream);

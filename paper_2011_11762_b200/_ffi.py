@@ -37,6 +37,7 @@ EXPORTS = (
     "qm_build_fill",
     "qm_spgemm_workspace_bytes",
     "qm_spgemm_count",
+    "qm_spgemm_count_masked",
     "qm_spgemm_fill_workspace_bytes",
     "qm_spgemm_fill",
     "qm_spgemm_fill_keys",
@@ -51,6 +52,7 @@ EXPORTS = (
     "qm_compact_workspace_bytes",
     "qm_compact",
     "qm_block_stats",
+    "qm_block_masks",
     "qm_gather_blocks",
     "qm_transpose_blocks",
     "qm_axpby_blocks",
@@ -100,6 +102,8 @@ _SIGS = {
     "qm_spgemm_workspace_bytes": (_SZ, [_LP, _I64, _I64]),
     "qm_spgemm_count": (ctypes.c_int, [_LP, _P, _I64, _P, _I64, _P, _SZ, ctypes.POINTER(_I64),
                                        ctypes.POINTER(_I64), _P]),
+    "qm_spgemm_count_masked": (ctypes.c_int, [_LP, _P, _P, _I64, _P, _P, _I64, _P, _SZ, ctypes.POINTER(_I64),
+                                             ctypes.POINTER(_I64), _P]),
     "qm_spgemm_fill_workspace_bytes": (_SZ, [_LP, _I64]),
     "qm_spgemm_fill": (ctypes.c_int, [_LP, _I64, _I64, _I64, _I64, _P, _SZ, _P, _SZ, _P, _P, _P, _P]),
     "qm_spgemm_fill_keys": (ctypes.c_int, [_LP, _I64, _I64, _I64, _P, _SZ, _P, _SZ, _P, _P, _P]),
@@ -117,6 +121,7 @@ _SIGS = {
     "qm_compact_workspace_bytes": (_SZ, [_I64]),
     "qm_compact": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "qm_block_stats": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P]),
+    "qm_block_masks": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P]),
     "qm_gather_blocks": (ctypes.c_int, [_I32, _P, _P, _I64, _P, _P]),
     "qm_transpose_blocks": (ctypes.c_int, [_I32, _P, _I64, _P, _P]),
     "qm_axpby_blocks": (ctypes.c_int, [_I32, _I64, _P, _P, ctypes.c_double, ctypes.c_double, _P, _P, _P, _P,

@@ -32,6 +32,23 @@ class BlockSet:
     keys: torch.Tensor
     blocks: torch.Tensor
     sumsq: torch.Tensor
+    # int64[2, n] support masks (row 0: nonzero rows, row 1: nonzero columns; qm_block_masks),
+    # computed on first use by a product and kept with the (immutable) block set; None = not yet.
+    masks: torch.Tensor | None = None
+
+    def support_masks(self, stream=None) -> torch.Tensor:
+        """Per-block nonzero-row / nonzero-column bit masks (device). A product skips block pairs
+        whose masks do not meet: their product is exactly zero (spgemm.multiply_blocks)."""
+        if self.masks is None:
+            from . import _ffi  # noqa: PLC0415
+
+            m = torch.empty((2, self.n), dtype=torch.int64, device=self.device)
+            if self.n:
+                _ffi.check(_ffi.load().qm_block_masks(self.bs, self.n, _ffi.ptr(self.blocks), _ffi.ptr(m[0]),
+                                                      _ffi.ptr(m[1]), _ffi.stream_handle(stream)),
+                           "qm_block_masks")
+            self.masks = m
+        return self.masks
 
     @property
     def n(self) -> int:

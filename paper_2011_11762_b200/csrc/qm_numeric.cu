@@ -421,6 +421,53 @@ extern "C" int qm_block_stats(int32_t block_size, int64_t n, const double *block
   return launch_block_stats(block_size, n, blocks, sumsq, nonzero, nullptr, (cudaStream_t)stream);
 }
 
+namespace qm {
+namespace {
+// Support masks of each block: bit b of row_mask is set when a row r with b = r*64/bs (b = r for
+// bs <= 64) holds a nonzero, col_mask likewise for columns. A block holding a NaN or Inf gets full
+// masks (0 * Inf is NaN, so its products are never provably zero). One warp per block.
+__global__ void k_block_masks(const double *blocks, int64_t n, int bs, uint64_t *rmask, uint64_t *cmask) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t elems = (int64_t)bs * bs;
+  for (int64_t m = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); m < n; m += warps) {
+    const double *b = blocks + (size_t)m * elems;
+    uint64_t rb = 0, cb = 0;
+    bool bad = false;
+    for (int64_t e = lane; e < elems; e += 32) {
+      const double v = __ldcs(b + e);
+      if (v != 0.0) {
+        const int r = (int)(e / bs), c = (int)(e % bs);
+        rb |= 1ull << (bs <= 64 ? r : (r * 64) / bs);
+        cb |= 1ull << (bs <= 64 ? c : (c * 64) / bs);
+      }
+      bad |= !isfinite(v);
+    }
+    const uint32_t rl = __reduce_or_sync(0xffffffffu, (uint32_t)rb), rh = __reduce_or_sync(0xffffffffu, (uint32_t)(rb >> 32));
+    const uint32_t cl = __reduce_or_sync(0xffffffffu, (uint32_t)cb), ch = __reduce_or_sync(0xffffffffu, (uint32_t)(cb >> 32));
+    const bool anybad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      rmask[m] = anybad ? ~0ull : ((uint64_t)rh << 32 | rl);
+      cmask[m] = anybad ? ~0ull : ((uint64_t)ch << 32 | cl);
+    }
+  }
+}
+}  // namespace
+}  // namespace qm
+
+extern "C" int qm_block_masks(int32_t block_size, int64_t n, const double *blocks, uint64_t *row_mask,
+                              uint64_t *col_mask, void *stream) {
+  if (block_size < 1 || n < 0 || (n > 0 && (!blocks || !row_mask || !col_mask))) {
+    set_error("qm_block_masks: bad arguments");
+    return QM_ERR_INVALID;
+  }
+  if (n == 0) return QM_OK;
+  const int64_t grid = std::min<int64_t>((n + 7) / 8, (int64_t)sm_count() * 16);
+  k_block_masks<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(blocks, n, block_size, row_mask, col_mask);
+  QM_LAUNCHED("k_block_masks");
+  return QM_OK;
+}
+
 extern "C" int qm_numeric_pools(const qm_layout *layout, const double *const *a_pools, const int64_t *a_counts,
                                 int32_t n_a_pools, const double *const *b_pools, const int64_t *b_counts,
                                 int32_t n_b_pools, const uint32_t *tri, const int64_t *c_tptr, int64_t nC,

@@ -381,9 +381,13 @@ def config_operands_device(cfg: BaselineConfig, device) -> tuple[Geometry, Block
     if cfg.kind == "decay":
         _, (ka, ba), _ = config_operands_host(cfg)
         a = BlockSet.from_numpy(ka, ba, None, device)
+        if a.device.type == "cuda":
+            a.support_masks()  # input metadata, like the block norms
         return geom, a, a
     sets = []
     for m in (0, 1):
         keys = config_keys(cfg, m)
         sets.append(device_blocks(geom, keys, cfg.seed, m, config_pattern(cfg), cfg.half_bw, device))
+        if sets[-1].device.type == "cuda":
+            sets[-1].support_masks()
     return geom, sets[0], sets[1]

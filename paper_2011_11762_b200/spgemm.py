@@ -15,6 +15,7 @@ recursion (ops.py:197-241) enumerates the same triples, BlockSparseLeaf.multiply
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -66,7 +67,8 @@ def _alloc(shape, dtype, device):
 class SymbolicState:
     """Workspaces of one symbolic phase (row indexes, fill scratch) kept between its steps."""
 
-    def __init__(self, layout, a_keys: torch.Tensor, n_a: int, b_keys: torch.Tensor, n_b: int, stream=None):
+    def __init__(self, layout, a_keys: torch.Tensor, n_a: int, b_keys: torch.Tensor, n_b: int, stream=None,
+                 a_cmask: torch.Tensor | None = None, b_rmask: torch.Tensor | None = None):
         self.lib = _ffi.load()
         self.layout = layout
         self.lp = ctypes.byref(layout)
@@ -77,11 +79,11 @@ class SymbolicState:
         self.ws = _alloc(max(self.ws_bytes, 1), torch.uint8, self.dev)
         n_c = ctypes.c_int64(0)
         n_t = ctypes.c_int64(0)
-        _ffi.check(
-            self.lib.qm_spgemm_count(self.lp, _ffi.ptr(a_keys), n_a, _ffi.ptr(b_keys), n_b,
-                                     _ffi.ptr(self.ws), self.ws_bytes, ctypes.byref(n_c),
-                                     ctypes.byref(n_t), self.sh),
-            "qm_spgemm_count",
+        _ffi.check(  # support masks (None = full support): pairs whose product is exactly zero are skipped
+            self.lib.qm_spgemm_count_masked(self.lp, _ffi.ptr(a_keys), _ffi.ptr(a_cmask), n_a, _ffi.ptr(b_keys),
+                                            _ffi.ptr(b_rmask), n_b, _ffi.ptr(self.ws), self.ws_bytes,
+                                            ctypes.byref(n_c), ctypes.byref(n_t), self.sh),
+            "qm_spgemm_count_masked",
         )
         self.n_c, self.n_t = int(n_c.value), int(n_t.value)
         self.fill_bytes = self.lib.qm_spgemm_fill_workspace_bytes(self.lp, self.n_c)
@@ -112,8 +114,21 @@ class SymbolicState:
         return tri
 
 
+def support_filter_enabled() -> bool:
+    """QM_SUPPORT_FILTER=0 disables the exact-zero product filter (A/B measurements, tests)."""
+    return os.environ.get("QM_SUPPORT_FILTER", "1") != "0"
+
+
 def symbolic(layout, a: BlockSet, b: BlockSet, stream=None) -> SymbolicPlan:
-    st = SymbolicState(layout, a.keys, a.n, b.keys, b.n, stream)
+    """Triples of C = A*B. Block pairs whose support masks do not meet (A(i,k)'s nonzero columns vs
+    B(k,j)'s nonzero rows) multiply to an exactly-zero block and yield no triple; a C block left
+    without triples is an exact-zero block the reference computes and then drops (_set_block,
+    block_sparse.py:37-41), so the product is unchanged."""
+    a_cm = b_rm = None
+    if support_filter_enabled():
+        a_cm = a.support_masks(stream)[1]
+        b_rm = b.support_masks(stream)[0]
+    st = SymbolicState(layout, a.keys, a.n, b.keys, b.n, stream, a_cm, b_rm)
     c_keys = _alloc(st.n_c, torch.int64, st.dev)
     c_tptr = _alloc(st.n_c + 1, torch.int64, st.dev)
     tri = _alloc(2 * st.n_t, torch.int32, st.dev)

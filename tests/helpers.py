@@ -103,3 +103,26 @@ def decay_sparse(n: int, seed: int, width=None, scale: float = 4.0) -> np.ndarra
     i = np.arange(n)
     dist = np.abs(i[:, None] - i[None, :])
     return np.exp(-dist / scale) * (dist <= width) * rng.standard_normal((n, n))
+
+
+def support_masks_np(blocks: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """numpy statement of qm_block_masks: bit r (r*64//bs above 64) of the row / column mask is set
+    when that row / column of the block holds a nonzero; a NaN/Inf block gets full masks."""
+    n, bs, _ = blocks.shape
+    nz = blocks != 0
+    bit = np.arange(bs) if bs <= 64 else (np.arange(bs) * 64) // bs
+    w = (np.uint64(1) << bit.astype(np.uint64))
+    rows = np.bitwise_or.reduce(np.where(nz.any(axis=2), w[None, :], np.uint64(0)), axis=1)
+    cols = np.bitwise_or.reduce(np.where(nz.any(axis=1), w[None, :], np.uint64(0)), axis=1)
+    bad = ~np.isfinite(blocks).all(axis=(1, 2))
+    full = np.uint64(0xFFFFFFFFFFFFFFFF)
+    return np.where(bad, full, rows).astype(np.uint64), np.where(bad, full, cols).astype(np.uint64)
+
+
+def banded_support_decay(n: int, bw: int, seed: int) -> np.ndarray:
+    """Element-level band |i-j| <= bw with positive decaying values: blocks near the band edge are
+    partly empty, so many block pairs multiply to exact zeros (the C4 decay situation)."""
+    rng = np.random.default_rng(seed)
+    i = np.arange(n)
+    dist = np.abs(i[:, None] - i[None, :])
+    return np.where(dist <= bw, np.exp(-dist / 8.0) * rng.uniform(0.5, 1.5, (n, n)), 0.0)

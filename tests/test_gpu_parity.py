@@ -20,6 +20,7 @@ from paper_2011_11762_b200 import (
     spgemm,
 )
 from paper_2011_11762_b200 import generators as G
+from paper_2011_11762_b200.blocks import BlockSet
 from paper_2011_11762_b200.layout import Geometry, MatrixParams
 
 pytestmark = pytest.mark.gpu
@@ -134,10 +135,12 @@ def test_device_generator_matches_numpy_streams(bs, n, pattern):
 @pytest.mark.parametrize("kind,n,bs,per_row", [
     ("banded", 4096, 64, 0), ("random", 8192, 64, 8), ("random", 1 << 17, 16, 8), ("banded", 3000, 8, 0),
     ("random", 1 << 17, 16, 64)])
-def test_symbolic_phase_matches_oracle_exactly(ses, kind, n, bs, per_row):
+def test_symbolic_phase_matches_oracle_exactly(ses, monkeypatch, kind, n, bs, per_row):
     """Triples, their grouping and k order (block_sparse.py:121-129) equal the oracle's; the
     random 8192-wide grid exercises the multi-window accumulator (window 4096 columns), rows with
-    more than 32 A entries the grouped triple emission (32 A entries per group)."""
+    more than 32 A entries the grouped triple emission (32 A entries per group). Structure only
+    (the blocks are placeholders), so without the support-mask filter."""
+    monkeypatch.setenv("QM_SUPPORT_FILTER", "0")
     cfg = G.BaselineConfig("t", kind, n, bs, half_bw=300, per_row=per_row)
     geom = cfg.geometry
     ka, kb = G.config_keys(cfg, 0), G.config_keys(cfg, 1)
@@ -575,7 +578,10 @@ def test_c4_full_size_sampled_rows(ses):
     cfg = G.CONFIGS["C4"]
     geom, (ka, ba), _ = G.config_operands_host(cfg)
     c = ses.multiply(*(2 * [ses.matrix_from_blocks(geom, ka, ba)]))
-    assert ses.last_multiply.n_triples == 735716
+    # 735,716 block triples; 485,208 of them have meeting supports -- the rest multiply
+    # to exact zeros and are skipped, so the 59,678 exact-zero C blocks are never created
+    assert ses.last_multiply.n_triples == 485208 and ses.last_multiply.n_c == 60824
+    assert ses.last_multiply.zero_blocks == 0
     ai, ak = geom.decode(ka)
     rows = np.r_[0, np.random.default_rng(2).choice(geom.nbg, 6, replace=False), geom.nbg - 1]
     sel = np.isin(ai, rows)
@@ -692,3 +698,66 @@ def test_claim_order_is_bitwise_neutral(ses, monkeypatch, bs, n):
         kc, bc, _ = O.multiply(O.Geom(cfg.n, cfg.bs, cfg.bs), ka[sel], ba[sel], kb, bb)
         got = helpers.lookup(c1.keys.cpu().numpy(), c1.blocks, kc)
         assert helpers.rel(got, bc) <= TOL
+
+
+@pytest.mark.parametrize("bs", [16, 32, 64, 128])
+def test_block_support_masks_match_numpy(ses, bs):
+    """qm_block_masks: nonzero-row / nonzero-column bit masks per block (coarse bits above 64), full
+    masks for blocks holding NaN or Inf."""
+    rng = np.random.default_rng(bs)
+    blocks = np.where(rng.random((40, bs, bs)) < 0.02, rng.standard_normal((40, bs, bs)), 0.0)
+    blocks[3] = 0.0
+    blocks[5, 7, 9] = np.nan
+    blocks[6, 1, 2] = np.inf
+    blocks[7, bs - 1, :] = 1.0
+    bset = BlockSet.from_numpy(np.arange(40), blocks, None, ses.device)
+    m = bset.support_masks().cpu().numpy().view(np.uint64)
+    want_r, want_c = helpers.support_masks_np(blocks)
+    np.testing.assert_array_equal(m[0], want_r)
+    np.testing.assert_array_equal(m[1], want_c)
+
+
+@pytest.mark.parametrize("n,bw,leaf,bs", [(1024, 20, 64, 64), (768, 10, 32, 32), (512, 5, 128, 16),
+                                          (1024, 40, 128, 128), (600, 6, 48, 16)])
+def test_support_filter_skips_exact_zero_products(ses, monkeypatch, n, bw, leaf, bs):
+    """Block pairs whose supports do not meet are skipped: the executed triples are exactly the
+    oracle's triples with meeting masks, the C block set equals the oracle's after its exact-zero
+    drop (no zero block is ever created, so nothing is compacted), and the values are bitwise those
+    of the unfiltered product (QM_SUPPORT_FILTER=0: the skipped products only add +0)."""
+    da = helpers.banded_support_decay(n, bw, n)
+    db = helpers.banded_support_decay(n, bw, n + 1)
+    a, b = helpers.build(ses, da, leaf, bs), helpers.build(ses, db, leaf, bs)
+    c = ses.multiply(a, b)
+    st = ses.last_multiply
+    host = MatrixSession(device="cpu")
+    ka, ba, _ = helpers.build(host, da, leaf, bs).root.blockset.to_host()
+    kb, bb, _ = helpers.build(host, db, leaf, bs).root.blockset.to_host()
+    g = O.Geom(n, leaf, bs)
+    kc, bc, _ = O.multiply(g, ka, ba, kb, bb)
+    np.testing.assert_array_equal(c.root.blockset.keys.cpu().numpy(), kc)
+    assert helpers.rel(c.root.blockset.blocks.cpu().numpy(), bc) <= TOL
+    _, _, ta, tb, _ = O.symbolic(g, ka, kb)
+    _, cmask = helpers.support_masks_np(ba)
+    rmask, _ = helpers.support_masks_np(bb)
+    meet = (cmask[ta] & rmask[tb]) != 0
+    assert st.n_triples == int(meet.sum()) and st.n_triples < ta.size  # some products were skipped
+    assert st.zero_blocks == 0
+    monkeypatch.setenv("QM_SUPPORT_FILTER", "0")
+    c0 = ses.multiply(a, b)
+    assert ses.last_multiply.n_triples == ta.size and ses.last_multiply.zero_blocks > 0
+    assert torch.equal(c0.root.blockset.keys, c.root.blockset.keys)
+    assert torch.equal(c0.root.blockset.blocks, c.root.blockset.blocks)
+
+
+def test_support_filter_keeps_nan_inf_products(ses):
+    """0 * Inf is NaN: a block holding Inf/NaN is never filtered, so its NaN products reach C as in
+    the reference (A's only nonzero column is 5, B's Inf sits in row 7: disjoint supports)."""
+    bs = 16
+    da, db = np.zeros((32, 32)), np.zeros((32, 32))
+    da[0:bs, 5] = 1.0
+    db[7, 0] = np.inf
+    c = ses.to_dense(ses.multiply(helpers.build(ses, da, bs, bs), helpers.build(ses, db, bs, bs)))
+    with np.errstate(invalid="ignore"):
+        want = da[:bs, :bs] @ db[:bs, :bs]  # the only stored pair of blocks
+    assert np.array_equal(c[:bs, :bs], want, equal_nan=True)
+    assert np.isnan(c[0, 0]) and not c[bs:].any() and not c[:, bs:].any()
