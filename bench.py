@@ -6,9 +6,10 @@ One step = one full product of the configured BASELINE workload (symbolic phase 
 phase + exact-zero compaction) through the drop-in API's multiply path, inputs resident in HBM
 (inputs are larger than L2, so no flush is needed between steps). Prints ONE JSON line (rank 0).
 
-  metric  leaf-GEMM GFLOP/s (FP64) = 2*bs^3*T / time, T = block triples executed (SURVEY.md 8(d);
-          pairs whose nonzero-column / nonzero-row masks do not meet multiply to exact zeros and
-          are skipped -- config.triples_structural is the block-level count)
+  metric  leaf-GEMM GFLOP/s (FP64) = executed flops / time: 2*bs^3 per block triple (SURVEY.md
+          8(d)), i.e. 2*bs^2*32 per 32-deep k panel; block pairs (and k panels of a pair) whose
+          nonzero-column / nonzero-row masks do not meet multiply to exact zeros and are skipped,
+          so only the executed ones count (config.triples_structural is the block-level count)
   e2e     the same metric through MatrixSession.multiply with host (pinned) operands: H2D of A
           and B and D2H of C inside the timed region
   roofline  the numeric kernel (dominant) against the measured FP64 tensor peak (a DMMA

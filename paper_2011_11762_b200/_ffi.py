@@ -43,6 +43,7 @@ EXPORTS = (
     "qm_spgemm_fill_keys",
     "qm_spgemm_fill_triples",
     "qm_numeric",
+    "qm_numeric_masked",
     "qm_numeric_workspace_bytes",
     "qm_numeric_pools",
     "qm_ipc_export",
@@ -111,6 +112,8 @@ _SIGS = {
                                               _P, _P]),
     "qm_numeric": (ctypes.c_int, [_LP, _P, _P, _I64, _P, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _SZ,
                                   _P]),
+    "qm_numeric_masked": (ctypes.c_int, [_LP, _P, _P, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P,
+                                         _P, _P, _P, _SZ, _P]),
     "qm_numeric_workspace_bytes": (_SZ, [_I32, _I64, _I64]),
     "qm_ipc_export": (ctypes.c_int, [_P, _P, ctypes.POINTER(_I64)]),
     "qm_ipc_open": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
@@ -198,6 +201,16 @@ def ptr(t) -> int:
 
 def stream_handle(stream) -> int:
     return 0 if stream is None else int(stream.cuda_stream)
+
+
+def read_i64s(t, n: int, stream=None) -> list[int]:
+    """The first n (<= 8) int64 values of a device tensor, one synchronisation (qm_read_i64)."""
+    import torch  # noqa: PLC0415
+
+    out = (ctypes.c_int64 * n)()
+    st = stream if stream is not None else torch.cuda.current_stream(t.device)
+    check(load().qm_read_i64(ptr(t), n, out, stream_handle(st)), "qm_read_i64")
+    return [int(x) for x in out]
 
 
 def read_i64(t, stream=None) -> int:

@@ -35,6 +35,8 @@ class BlockSet:
     # int64[2, n] support masks (row 0: nonzero rows, row 1: nonzero columns; qm_block_masks),
     # computed on first use by a product and kept with the (immutable) block set; None = not yet.
     masks: torch.Tensor | None = None
+    # (every block has all rows nonzero, every block has all columns nonzero): set with `masks`
+    masks_full: tuple[bool, bool] = (False, False)
 
     def support_masks(self, stream=None) -> torch.Tensor:
         """Per-block nonzero-row / nonzero-column bit masks (device). A product skips block pairs
@@ -47,6 +49,11 @@ class BlockSet:
                 _ffi.check(_ffi.load().qm_block_masks(self.bs, self.n, _ffi.ptr(self.blocks), _ffi.ptr(m[0]),
                                                       _ffi.ptr(m[1]), _ffi.stream_handle(stream)),
                            "qm_block_masks")
+                full = -1 if self.bs >= 64 else (1 << self.bs) - 1
+                f = (m == full).all(dim=1).tolist()  # one synchronisation, once per block set
+                self.masks_full = (bool(f[0]), bool(f[1]))
+            else:
+                self.masks_full = (True, True)
             self.masks = m
         return self.masks
 

@@ -105,12 +105,16 @@ struct Geometry {
   int64_t nbg;    // blocks per matrix side = nbl << depth
 };
 
-// What the numeric kernel needs to choose a claim order other than quadtree-key order (the A keys
-// and the layout; a_keys = NULL keeps key order).
-struct OrderInfo {
+// Optional inputs of the numeric kernel beyond the triples: the A keys and layout (for claim
+// orders other than quadtree-key order; a_keys = NULL keeps key order), the operands' support masks
+// (A's nonzero columns, B's nonzero rows: k panels where they do not meet are skipped; NULL = all
+// panels), and where to count the k panels executed (device int64, NULL = not counted).
+struct NumericAux {
   const uint64_t *a_keys = nullptr;
   int32_t nbl = 1, lbits = 0;
   int64_t nbg = 1;
+  const uint64_t *a_cmask = nullptr, *b_rmask = nullptr;
+  int64_t *panel_count = nullptr;
 };
 
 inline int make_geometry(const qm_layout *l, Geometry *g) {

@@ -337,9 +337,9 @@ int numeric_sm_count() { return sm_count(); }
 
 int launch_numeric_tma(int bs, const double *const *A, const int64_t *nA, int na, const double *const *B,
                        const int64_t *nB, int nb, const uint32_t *tri, const int64_t *tptr, int64_t nC,
-                       int64_t nT, const OrderInfo &oi, double *C, double *csq, uint8_t *cnz, int64_t *zc,
+                       int64_t nT, const NumericAux &oi, double *C, double *csq, uint8_t *cnz, int64_t *zc,
                        void *ws, size_t ws_bytes, cudaStream_t st);
-size_t numeric_tma_ws_bytes(int bs, int64_t nC);
+size_t numeric_tma_ws_bytes(int bs, int64_t nC, int64_t nT);
 size_t numeric_group16_ws_bytes(int64_t nC, int64_t nT);
 int launch_numeric_group16(const Geometry &g, const double *A, int64_t nA, const double *B, int64_t nB,
                            const uint64_t *a_keys, const uint32_t *tri, const int64_t *c_tptr,
@@ -363,14 +363,15 @@ extern "C" int qm_numeric_path(int32_t bs) {
 
 extern "C" size_t qm_numeric_workspace_bytes(int32_t block_size, int64_t nC, int64_t nT) {
   if (numeric_impl() != 2) return 0;
-  return block_size == 16 ? numeric_group16_ws_bytes(nC, nT) : numeric_tma_ws_bytes(block_size, nC);
+  return block_size == 16 ? numeric_group16_ws_bytes(nC, nT) : numeric_tma_ws_bytes(block_size, nC, nT);
 }
 
-extern "C" int qm_numeric(const qm_layout *layout, const uint64_t *a_keys, const double *a_blocks, int64_t nA,
-                          const double *b_blocks, int64_t nB, const uint32_t *tri,
-                          const int64_t *c_tptr, const uint64_t *c_keys, int64_t nC, int64_t nT, double *c_blocks,
-                          double *c_sumsq, uint8_t *c_nonzero, int64_t *zero_count, void *ws,
-                          size_t ws_bytes, void *stream) {
+extern "C" int qm_numeric_masked(const qm_layout *layout, const uint64_t *a_keys, const double *a_blocks,
+                                 const uint64_t *a_cmask, int64_t nA, const double *b_blocks,
+                                 const uint64_t *b_rmask, int64_t nB, const uint32_t *tri, const int64_t *c_tptr,
+                                 const uint64_t *c_keys, int64_t nC, int64_t nT, double *c_blocks, double *c_sumsq,
+                                 uint8_t *c_nonzero, int64_t *zero_count, int64_t *panel_count, void *ws,
+                                 size_t ws_bytes, void *stream) {
   Geometry g;
   int rc = make_geometry(layout, &g);
   if (rc != QM_OK) return rc;
@@ -380,6 +381,7 @@ extern "C" int qm_numeric(const qm_layout *layout, const uint64_t *a_keys, const
   }
   cudaStream_t st = (cudaStream_t)stream;
   if (zero_count) QM_CUDA_TRY(cudaMemsetAsync(zero_count, 0, sizeof(int64_t), st));
+  if (panel_count) QM_CUDA_TRY(cudaMemsetAsync(panel_count, nC == 0 ? 0 : 0xff, sizeof(int64_t), st));  // -1: not counted
   if (nC == 0) return QM_OK;
   const uint2 *t2 = (const uint2 *)tri;
   if (numeric_impl() == 2 && g.bs == 16) {
@@ -388,11 +390,14 @@ extern "C" int qm_numeric(const qm_layout *layout, const uint64_t *a_keys, const
     if (rc != QM_ERR_UNSUPPORTED) return rc;
   }
   if (numeric_impl() == 2) {
-    OrderInfo oi;
+    NumericAux oi;
     oi.a_keys = a_keys;
     oi.nbl = g.nbl;
     oi.lbits = g.lbits;
     oi.nbg = g.nbg;
+    oi.a_cmask = a_cmask;
+    oi.b_rmask = b_rmask;
+    oi.panel_count = panel_count;
     rc = launch_numeric_tma(g.bs, &a_blocks, &nA, 1, &b_blocks, &nB, 1, tri, c_tptr, nC, nT, oi, c_blocks,
                             c_sumsq, c_nonzero, zero_count, ws, ws_bytes, st);
     if (rc != QM_ERR_UNSUPPORTED) return rc;
@@ -410,6 +415,15 @@ extern "C" int qm_numeric(const qm_layout *layout, const uint64_t *a_keys, const
   k_numeric_generic<<<(int)grid, 256, 0, st>>>(a_blocks, b_blocks, t2, c_tptr, nC, g.bs, c_blocks);
   QM_LAUNCHED("k_numeric_generic");
   return launch_block_stats(g.bs, nC, c_blocks, c_sumsq, c_nonzero, zero_count, st);
+}
+
+extern "C" int qm_numeric(const qm_layout *layout, const uint64_t *a_keys, const double *a_blocks, int64_t nA,
+                          const double *b_blocks, int64_t nB, const uint32_t *tri,
+                          const int64_t *c_tptr, const uint64_t *c_keys, int64_t nC, int64_t nT, double *c_blocks,
+                          double *c_sumsq, uint8_t *c_nonzero, int64_t *zero_count, void *ws,
+                          size_t ws_bytes, void *stream) {
+  return qm_numeric_masked(layout, a_keys, a_blocks, nullptr, nA, b_blocks, nullptr, nB, tri, c_tptr, c_keys, nC,
+                           nT, c_blocks, c_sumsq, c_nonzero, zero_count, nullptr, ws, ws_bytes, stream);
 }
 
 extern "C" int qm_block_stats(int32_t block_size, int64_t n, const double *blocks, double *sumsq,
@@ -483,6 +497,6 @@ extern "C" int qm_numeric_pools(const qm_layout *layout, const double *const *a_
     return QM_ERR_INVALID;
   }
   return launch_numeric_tma(g.bs, a_pools, a_counts, n_a_pools, b_pools, b_counts, n_b_pools, tri, c_tptr,
-                            nC, nT, OrderInfo(), c_blocks, c_sumsq, c_nonzero, zero_count, ws, ws_bytes,
+                            nC, nT, NumericAux(), c_blocks, c_sumsq, c_nonzero, zero_count, ws, ws_bytes,
                             (cudaStream_t)stream);
 }

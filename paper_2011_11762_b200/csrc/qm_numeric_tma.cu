@@ -75,25 +75,41 @@ struct __align__(64) TmaMaps {
 
 // Stage cursor over work units u = m * NQ + q (C block m, tile q), triple t, k panel p.
 // `unit` is the claim index; `mu` the work unit it maps to (C block order[unit / NQ], tile unit % NQ;
-// order = NULL: the identity, quadtree-key order).
+// order = NULL: the identity, quadtree-key order). `sm` = the k panels of triple t that can
+// contribute (tri_sm[t], from the operands' support masks; all NP panels when tri_sm is NULL):
+// a panel where A's columns or B's rows are all zero adds exactly zero and is skipped.
 struct Cur {
   int64_t unit, mu, t, tend;
   int p;
+  uint32_t sm;
 };
 
 template <class Cfg>
+__device__ __forceinline__ uint32_t triple_panels(const uint8_t *tri_sm, int64_t t) {
+  return tri_sm ? (uint32_t)tri_sm[t] : (1u << Cfg::NP) - 1u;
+}
+
+template <class Cfg>
 __device__ __forceinline__ void cur_start(Cur &c, int64_t unit, int64_t nU, const int64_t *tptr,
-                                          const uint32_t *order) {
+                                          const uint32_t *order, const uint8_t *tri_sm) {
   c.unit = unit;
-  c.p = 0;
   if (unit < nU) {
     const int64_t m = order ? (int64_t)order[unit / Cfg::NQ] : unit / Cfg::NQ;
     c.mu = m * Cfg::NQ + unit % Cfg::NQ;
     c.t = tptr[m];
     c.tend = tptr[m + 1];
+    c.sm = triple_panels<Cfg>(tri_sm, c.t);
   } else {
     c.mu = c.t = c.tend = 0;
+    c.sm = 1u;
   }
+  c.p = __ffs(c.sm) - 1;
+}
+
+// True when the cursor's stage is the unit's last (no later panel of this triple, no later triple:
+// every triple has at least one panel).
+__device__ __forceinline__ bool cur_last(const Cur &c) {
+  return (c.sm & ~((2u << c.p) - 1u)) == 0u && c.t + 1 == c.tend;
 }
 
 // Advances the producer's cursor; a finished unit is replaced by the next one claimed from the
@@ -101,11 +117,15 @@ __device__ __forceinline__ void cur_start(Cur &c, int64_t unit, int64_t nU, cons
 // and raised DRAM re-reads of A/B by 2x with 3 CTAs/SM).
 template <class Cfg>
 __device__ __forceinline__ void cur_next(Cur &c, int64_t nU, const int64_t *tptr, const uint32_t *order,
-                                         unsigned long long *counter) {
-  if (++c.p == Cfg::NP) {
-    c.p = 0;
-    if (++c.t == c.tend)
-      cur_start<Cfg>(c, (int64_t)gridDim.x + (int64_t)atomicAdd(counter, 1ull), nU, tptr, order);
+                                         const uint8_t *tri_sm, unsigned long long *counter) {
+  const uint32_t rest = c.sm & ~((2u << c.p) - 1u);
+  if (rest) {
+    c.p = __ffs(rest) - 1;
+  } else if (++c.t == c.tend) {
+    cur_start<Cfg>(c, (int64_t)gridDim.x + (int64_t)atomicAdd(counter, 1ull), nU, tptr, order, tri_sm);
+  } else {
+    c.sm = triple_panels<Cfg>(tri_sm, c.t);
+    c.p = __ffs(c.sm) - 1;
   }
 }
 
@@ -116,7 +136,7 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
                   double *__restrict__ C, double *__restrict__ csq, uint8_t *__restrict__ cnz,
                   int64_t *__restrict__ zero_count, double *__restrict__ part_sq,
                   uint8_t *__restrict__ part_nz, unsigned long long *__restrict__ counter,
-                  const uint32_t *__restrict__ order, uint64_t zmask) {
+                  const uint32_t *__restrict__ order, const uint8_t *__restrict__ tri_sm, uint64_t zmask) {
   constexpr int BS = Cfg::BS, MT = Cfg::MT, NT = Cfg::NT, STAGES = Cfg::STAGES;
   const int64_t nU = nC * Cfg::NQ;
   // Align to 1 KB (SWIZZLE_128B atoms) by offsetting the __shared__ array itself: the pointer keeps
@@ -150,7 +170,7 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
       // counter in key order (so concurrently running CTAs still share A/B rows/columns in L2)
       // and no CTA is left with a long tail of heavy units.
       Cur L;
-      cur_start<Cfg>(L, blockIdx.x, nU, tptr, order);
+      cur_start<Cfg>(L, blockIdx.x, nU, tptr, order, tri_sm);
       int s = 0;
       uint32_t phase = 0;
       while (true) {
@@ -166,7 +186,7 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
         const int qt = (int)(L.mu % Cfg::NQ);
         const int row0 = (qt / Cfg::NQN) * Cfg::TILE, col0 = (qt % Cfg::NQN) * Cfg::TILE;
         uint8_t *st = smem + (size_t)s * Cfg::STAGE_BYTES;
-        meta[s] = L.mu * 2 + ((L.p == Cfg::NP - 1 && L.t + 1 == L.tend) ? 1 : 0);
+        meta[s] = L.mu * 2 + (cur_last(L) ? 1 : 0);
         mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
 #pragma unroll
         for (int q = 0; q < Cfg::KSP; ++q)
@@ -176,7 +196,7 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
         for (int q = 0; q < Cfg::NSP; ++q)
           tma_load_2d(st + Cfg::A_BYTES + q * Cfg::B_SP_BYTES, &maps.b[bo], col0 + q * 16,
                       (int)(bl * BS + L.p * Cfg::KP), &full[s]);
-        cur_next<Cfg>(L, nU, tptr, order, counter);
+        cur_next<Cfg>(L, nU, tptr, order, tri_sm, counter);
         if (++s == STAGES) {
           s = 0;
           phase ^= 1u;
@@ -294,7 +314,9 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
 
 // Fixed-order combination of the per-tile partial norms / nonzero flags of NQ-tile C blocks.
 __global__ void k_combine_tiles(const double *part_sq, const uint8_t *part_nz, int nq, int64_t nC,
-                                double *csq, uint8_t *cnz, int64_t *zero_count) {
+                                double *csq, uint8_t *cnz, int64_t *zero_count, int64_t *panel_count,
+                                int64_t panel_fill) {
+  if (panel_count && panel_fill >= 0 && blockIdx.x == 0 && threadIdx.x == 0) *panel_count = panel_fill;
   for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < nC;
        m += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
@@ -321,6 +343,33 @@ __global__ void k_order_key(const uint2 *tri, const int64_t *tptr, const uint64_
     key[c] = bj;
     iota[c] = (uint32_t)c;
   }
+}
+
+// k panels of each triple that can contribute: panel p covers rows [p*KP, (p+1)*KP) of B and the
+// same columns of A, i.e. mask bits [p*W, (p+1)*W) with W = 64*KP/max(BS, 64) (mask bit b = row b
+// for BS <= 64, rows 2b, 2b+1 for BS = 128). A panel where A's columns and B's rows share no bit
+// adds exactly zero. Disjoint supports overall (not filtered by the symbolic phase) keep one panel.
+// Also counts the panels to execute (block partials, one atomic per CTA).
+template <class Cfg>
+__global__ void k_triple_panels(const uint2 *tri, int64_t nT, const uint64_t *a_cmask, const uint64_t *b_rmask,
+                                uint8_t *sm, unsigned long long *panels) {
+  constexpr int W = 64 * Cfg::KP / (Cfg::BS > 64 ? Cfg::BS : 64);
+  constexpr uint64_t kW = W >= 64 ? ~0ull : ((1ull << W) - 1ull);
+  uint32_t cnt = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nT; t += (int64_t)gridDim.x * blockDim.x) {
+    const uint2 ab = tri[t];
+    const uint64_t ov = a_cmask[ab.x] & b_rmask[ab.y];
+    uint32_t m = 0;
+#pragma unroll
+    for (int p = 0; p < Cfg::NP; ++p)
+      if ((ov >> (p * W)) & kW) m |= 1u << p;
+    if (!m) m = 1u;
+    sm[t] = (uint8_t)m;
+    cnt += __popc(m);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(panels, (unsigned long long)cnt);
 }
 
 int sm_count_tma() { return device_sm_count(); }
@@ -350,15 +399,19 @@ size_t order_cub_bytes(int64_t nC) {
   return b;
 }
 
-// Workspace: the work counter (256 B), per-warp partial norms / nonzero flags of every tile, then
-// the claim-order arrays (4 x nC uint32 + radix-sort scratch).
+// Workspace: the work counter (256 B), per-warp partial norms / nonzero flags of every tile, the
+// claim-order arrays (4 x nC uint32 + radix-sort scratch), then the per-triple panel masks (nT bytes).
 template <class Cfg>
 size_t tma_ws_base(int64_t nC) {
   return align_up(256 + (size_t)nC * Cfg::NQ * Cfg::NCW * (sizeof(double) + sizeof(uint8_t)) + 256);
 }
 template <class Cfg>
-size_t tma_ws_bytes(int64_t nC) {
+size_t tma_ws_panels_offset(int64_t nC) {
   return tma_ws_base<Cfg>(nC) + align_up(4 * sizeof(uint32_t) * (size_t)nC) + align_up(order_cub_bytes(nC));
+}
+template <class Cfg>
+size_t tma_ws_bytes(int64_t nC, int64_t nT) {
+  return tma_ws_panels_offset<Cfg>(nC) + align_up((size_t)std::max<int64_t>(nT, 1));
 }
 
 // Fills the claim order (k of each C block's first triple, stable radix sort) into the workspace
@@ -385,14 +438,14 @@ int make_order(int kind, const uint2 *tri, const int64_t *tptr, const uint64_t *
 template <class Cfg, int NPOOL>
 int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const double *const *B,
                      const int64_t *nB, int nb, const uint2 *tri, const int64_t *tptr, int64_t nC, int64_t nT,
-                     const OrderInfo &oi, double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws,
+                     const NumericAux &oi, double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws,
                      size_t ws_bytes, cudaStream_t st) {
   if (na < 1 || nb < 1 || na > NPOOL || nb > NPOOL) {
     set_error("qm_numeric: %d / %d operand pools (at most %d)", na, nb, NPOOL);
     return QM_ERR_INVALID;
   }
-  if (!ws || ws_bytes < tma_ws_bytes<Cfg>(nC)) {
-    set_error("qm_numeric: workspace %zu < required %zu", ws_bytes, tma_ws_bytes<Cfg>(nC));
+  if (!ws || ws_bytes < tma_ws_bytes<Cfg>(nC, nT)) {
+    set_error("qm_numeric: workspace %zu < required %zu", ws_bytes, tma_ws_bytes<Cfg>(nC, nT));
     return QM_ERR_WORKSPACE;
   }
   unsigned long long *counter = (unsigned long long *)ws;
@@ -443,13 +496,24 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
       if (rc != QM_OK) return rc;
     }
   }
+  uint8_t *tri_sm = nullptr;
+  int64_t panel_fill = Cfg::NP * nT;  // every panel of every triple
+  if (oi.a_cmask && oi.b_rmask && na == 1 && nb == 1 && Cfg::NP > 1 && nT > 0) {
+    tri_sm = (uint8_t *)ws + tma_ws_panels_offset<Cfg>(nC);
+    if (oi.panel_count) QM_CUDA_TRY(cudaMemsetAsync(oi.panel_count, 0, sizeof(int64_t), st));
+    const int g = (int)std::min<int64_t>((nT + 255) / 256, (int64_t)sm_count_tma() * 16);
+    k_triple_panels<Cfg><<<g, 256, 0, st>>>(tri, nT, oi.a_cmask, oi.b_rmask, tri_sm,
+                                            (unsigned long long *)oi.panel_count);
+    QM_LAUNCHED("k_triple_panels");
+    panel_fill = -1;  // counted by k_triple_panels
+  }
   k_numeric_tma<Cfg, NPOOL><<<(int)grid, Cfg::NTHR, Cfg::SMEM, st>>>(
-      maps, tri, tptr, nC, C, csq, cnz, zc, part_sq, part_nz, counter, order, /*zmask=*/0ull);
+      maps, tri, tptr, nC, C, csq, cnz, zc, part_sq, part_nz, counter, order, tri_sm, /*zmask=*/0ull);
   QM_LAUNCHED("k_numeric_tma");
   {
     int64_t g = std::min<int64_t>((nC + 255) / 256, (int64_t)sm_count_tma() * 8);
     k_combine_tiles<<<(int)std::max<int64_t>(g, 1), 256, 0, st>>>(part_sq, part_nz, Cfg::NQ * Cfg::NCW,
-                                                                   nC, csq, cnz, zc);
+                                                                   nC, csq, cnz, zc, oi.panel_count, panel_fill);
     QM_LAUNCHED("k_combine_tiles");
   }
   return QM_OK;
@@ -458,7 +522,7 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
 template <class Cfg>
 int launch_tma(const double *const *A, const int64_t *nA, int na, const double *const *B,
                const int64_t *nB, int nb, const uint2 *tri, const int64_t *tptr, int64_t nC, int64_t nT,
-               const OrderInfo &oi, double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes,
+               const NumericAux &oi, double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes,
                cudaStream_t st) {
   if (na == 1 && nb == 1)
     return launch_tma_pools<Cfg, 1>(A, nA, na, B, nB, nb, tri, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes,
@@ -495,11 +559,11 @@ using Tma128m = TmaCfg<128, 64, 2, 2, 32, 2, 3>;
 
 }  // namespace
 
-size_t numeric_tma_ws_bytes(int bs, int64_t nC) {
+size_t numeric_tma_ws_bytes(int bs, int64_t nC, int64_t nT) {
   switch (bs) {
-    case 32: return tma_ws_bytes<Tma32>(nC);
-    case 64: return std::max(tma_ws_bytes<Tma64>(nC), tma_ws_bytes<Tma64m>(nC));
-    case 128: return std::max(tma_ws_bytes<Tma128>(nC), tma_ws_bytes<Tma128m>(nC));
+    case 32: return tma_ws_bytes<Tma32>(nC, nT);
+    case 64: return std::max(tma_ws_bytes<Tma64>(nC, nT), tma_ws_bytes<Tma64m>(nC, nT));
+    case 128: return std::max(tma_ws_bytes<Tma128>(nC, nT), tma_ws_bytes<Tma128m>(nC, nT));
     default: return 0;
   }
 }
@@ -508,7 +572,7 @@ size_t numeric_tma_ws_bytes(int bs, int64_t nC) {
 // local; > 1 = every rank's pool, triple indices packed as owner << 28 | local).
 int launch_numeric_tma(int bs, const double *const *A, const int64_t *nA, int na, const double *const *B,
                        const int64_t *nB, int nb, const uint32_t *tri, const int64_t *tptr, int64_t nC,
-                       int64_t nT, const OrderInfo &oi, double *C, double *csq, uint8_t *cnz, int64_t *zc,
+                       int64_t nT, const NumericAux &oi, double *C, double *csq, uint8_t *cnz, int64_t *zc,
                        void *ws, size_t ws_bytes, cudaStream_t st) {
   const uint2 *t2 = (const uint2 *)tri;
   switch (bs) {

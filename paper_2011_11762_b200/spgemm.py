@@ -119,15 +119,24 @@ def support_filter_enabled() -> bool:
     return os.environ.get("QM_SUPPORT_FILTER", "1") != "0"
 
 
+def _use_masks(a: BlockSet, b: BlockSet, stream=None) -> bool:
+    """Support masks matter unless A's blocks all have full column support or B's all have full row
+    support (dense blocks: every pair and every k panel contributes, so filtering is skipped)."""
+    if not support_filter_enabled():
+        return False
+    a.support_masks(stream)
+    b.support_masks(stream)
+    return not (a.masks_full[1] or b.masks_full[0])
+
+
 def symbolic(layout, a: BlockSet, b: BlockSet, stream=None) -> SymbolicPlan:
     """Triples of C = A*B. Block pairs whose support masks do not meet (A(i,k)'s nonzero columns vs
     B(k,j)'s nonzero rows) multiply to an exactly-zero block and yield no triple; a C block left
     without triples is an exact-zero block the reference computes and then drops (_set_block,
     block_sparse.py:37-41), so the product is unchanged."""
     a_cm = b_rm = None
-    if support_filter_enabled():
-        a_cm = a.support_masks(stream)[1]
-        b_rm = b.support_masks(stream)[0]
+    if _use_masks(a, b, stream):
+        a_cm, b_rm = a.masks[1], b.masks[0]
     st = SymbolicState(layout, a.keys, a.n, b.keys, b.n, stream, a_cm, b_rm)
     c_keys = _alloc(st.n_c, torch.int64, st.dev)
     c_tptr = _alloc(st.n_c + 1, torch.int64, st.dev)
@@ -152,16 +161,19 @@ def numeric(layout, a: BlockSet, b: BlockSet, plan: SymbolicPlan, stream=None,
         out = BlockSet(plan.c_keys, _alloc((nc, bs, bs), torch.float64, dev),
                        _alloc(nc, torch.float64, dev))
     nz = _alloc(nc, torch.uint8, dev)
-    zc = _alloc(1, torch.int64, dev)  # qm_numeric zeroes it on the stream
+    zc = _alloc(2, torch.int64, dev)  # [exact-zero C blocks, k panels executed]: set by the library
     wb = lib.qm_numeric_workspace_bytes(bs, nc, plan.n_triples)
     ws = _alloc(wb, torch.uint8, dev) if wb else None
+    a_cm = b_rm = None
+    if _use_masks(a, b, stream):
+        a_cm, b_rm = a.masks[1], b.masks[0]
     _ffi.check(
-        lib.qm_numeric(ctypes.byref(layout), _ffi.ptr(a.keys), _ffi.ptr(a.blocks), a.n, _ffi.ptr(b.blocks), b.n,
-                       _ffi.ptr(plan.tri), _ffi.ptr(plan.c_tptr), _ffi.ptr(plan.c_keys), nc, plan.n_triples,
-                       _ffi.ptr(out.blocks),
-                       _ffi.ptr(out.sumsq), _ffi.ptr(nz), _ffi.ptr(zc), _ffi.ptr(ws), wb,
-                       _ffi.stream_handle(stream)),
-        "qm_numeric",
+        lib.qm_numeric_masked(ctypes.byref(layout), _ffi.ptr(a.keys), _ffi.ptr(a.blocks), _ffi.ptr(a_cm), a.n,
+                              _ffi.ptr(b.blocks), _ffi.ptr(b_rm), b.n, _ffi.ptr(plan.tri), _ffi.ptr(plan.c_tptr),
+                              _ffi.ptr(plan.c_keys), nc, plan.n_triples, _ffi.ptr(out.blocks),
+                              _ffi.ptr(out.sumsq), _ffi.ptr(nz), _ffi.ptr(zc), _ffi.ptr(zc[1:]), _ffi.ptr(ws), wb,
+                              _ffi.stream_handle(stream)),
+        "qm_numeric_masked",
     )
     return out, nz, zc
 
@@ -224,10 +236,13 @@ def multiply_blocks(layout, a: BlockSet, b: BlockSet, stream=None,
     c, nz, zc = numeric(layout, a, b, plan, stream)
     if events is not None:
         events["end"].record(stream)
-    n_zero = _sync_item(zc, stream)
+    n_zero, panels = _ffi.read_i64s(zc, 2, stream)
     c = compact(bs, c, nz, n_zero, stream)
     if stats is not None:
         stats.zero_blocks = n_zero
+        if panels >= 0:  # 32-deep k panels executed (panels where the supports miss are skipped)
+            stats.extra["k_panels"] = panels
+            stats.flops = 2 * bs * bs * 32 * panels
         stats.n_c = c.n
         stats.launches = int(lib.qm_launch_count() - l0)
     return c
