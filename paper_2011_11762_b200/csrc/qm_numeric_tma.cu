@@ -349,7 +349,7 @@ __global__ void k_order_key(const uint2 *tri, const int64_t *tptr, const uint64_
 // same columns of A, i.e. mask bits [p*W, (p+1)*W) with W = 64*KP/max(BS, 64) (mask bit b = row b
 // for BS <= 64, rows 2b, 2b+1 for BS = 128). A panel where A's columns and B's rows share no bit
 // adds exactly zero. Disjoint supports overall (not filtered by the symbolic phase) keep one panel.
-// Also counts the panels to execute (block partials, one atomic per CTA).
+// Also counts the k rows to execute (KP per panel; warp partials, one atomic per warp).
 template <class Cfg>
 __global__ void k_triple_panels(const uint2 *tri, int64_t nT, const uint64_t *a_cmask, const uint64_t *b_rmask,
                                 uint8_t *sm, unsigned long long *panels) {
@@ -365,7 +365,7 @@ __global__ void k_triple_panels(const uint2 *tri, int64_t nT, const uint64_t *a_
       if ((ov >> (p * W)) & kW) m |= 1u << p;
     if (!m) m = 1u;
     sm[t] = (uint8_t)m;
-    cnt += __popc(m);
+    cnt += __popc(m) * Cfg::KP;  // k rows executed
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
@@ -497,7 +497,7 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
     }
   }
   uint8_t *tri_sm = nullptr;
-  int64_t panel_fill = Cfg::NP * nT;  // every panel of every triple
+  int64_t panel_fill = (int64_t)Cfg::BS * nT;  // every k row of every triple
   if (oi.a_cmask && oi.b_rmask && na == 1 && nb == 1 && Cfg::NP > 1 && nT > 0) {
     tri_sm = (uint8_t *)ws + tma_ws_panels_offset<Cfg>(nC);
     if (oi.panel_count) QM_CUDA_TRY(cudaMemsetAsync(oi.panel_count, 0, sizeof(int64_t), st));
@@ -554,6 +554,14 @@ bool use_wide(int64_t nU, int64_t nC, int64_t nT) {
   return nT >= kManyTriplesPerBlock * nC && nU >= kWideUnitsPerCta * 3 * (int64_t)device_sm_count();
 }
 
+// Masked products (operands with partial block supports): 16-deep k panels, so the panel skip of
+// k_triple_panels works at half the granularity; 4 stages of 16 KB, 3 CTAs/SM.
+using Tma64k16 = TmaCfg<64, 64, 2, 2, 16, 4, 3>;
+bool use_k16(const NumericAux &oi) {
+  const char *e = getenv("QM_PANEL16");
+  return oi.a_cmask && oi.b_rmask && !(e && strcmp(e, "0") == 0);
+}
+
 using Tma128 = TmaCfg<128, 64, 2, 2, 32, 3, 2>;
 using Tma128m = TmaCfg<128, 64, 2, 2, 32, 2, 3>;
 
@@ -562,7 +570,9 @@ using Tma128m = TmaCfg<128, 64, 2, 2, 32, 2, 3>;
 size_t numeric_tma_ws_bytes(int bs, int64_t nC, int64_t nT) {
   switch (bs) {
     case 32: return tma_ws_bytes<Tma32>(nC, nT);
-    case 64: return std::max(tma_ws_bytes<Tma64>(nC, nT), tma_ws_bytes<Tma64m>(nC, nT));
+    case 64:
+      return std::max(std::max(tma_ws_bytes<Tma64>(nC, nT), tma_ws_bytes<Tma64m>(nC, nT)),
+                      tma_ws_bytes<Tma64k16>(nC, nT));
     case 128: return std::max(tma_ws_bytes<Tma128>(nC, nT), tma_ws_bytes<Tma128m>(nC, nT));
     default: return 0;
   }
@@ -579,6 +589,8 @@ int launch_numeric_tma(int bs, const double *const *A, const int64_t *nA, int na
     case 32:
       return launch_tma<Tma32>(A, nA, na, B, nB, nb, t2, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes, st);
     case 64:
+      if (use_k16(oi))
+        return launch_tma<Tma64k16>(A, nA, na, B, nB, nb, t2, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes, st);
       if (use_wide(nC, nC, nT))
         return launch_tma<Tma64m>(A, nA, na, B, nB, nb, t2, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes, st);
       return launch_tma<Tma64>(A, nA, na, B, nB, nb, t2, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes, st);

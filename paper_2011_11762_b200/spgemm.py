@@ -240,9 +240,9 @@ def multiply_blocks(layout, a: BlockSet, b: BlockSet, stream=None,
     c = compact(bs, c, nz, n_zero, stream)
     if stats is not None:
         stats.zero_blocks = n_zero
-        if panels >= 0:  # 32-deep k panels executed (panels where the supports miss are skipped)
-            stats.extra["k_panels"] = panels
-            stats.flops = 2 * bs * bs * 32 * panels
+        if panels >= 0:  # k depth executed over all triples (k panels where the supports miss are skipped)
+            stats.extra["k_rows"] = panels
+            stats.flops = 2 * bs * bs * panels
         stats.n_c = c.n
         stats.launches = int(lib.qm_launch_count() - l0)
     return c

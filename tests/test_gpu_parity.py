@@ -742,12 +742,13 @@ def test_support_filter_skips_exact_zero_products(ses, monkeypatch, n, bw, leaf,
     meet = (cmask[ta] & rmask[tb]) != 0
     assert st.n_triples == int(meet.sum()) and st.n_triples < ta.size  # some products were skipped
     assert st.zero_blocks == 0
-    if bs >= 32:  # 32-deep k panels of the surviving triples where the supports meet
-        npan, w = bs // 32, 64 * 32 // max(bs, 64)
+    if bs >= 32:  # k panels (16 deep at bs 64, 32 deep at bs 128) of the surviving triples where the supports meet
+        kp = 16 if bs == 64 else 32
+        npan, w = bs // kp, 64 * kp // max(bs, 64)
         ov = (cmask[ta] & rmask[tb])[meet]
-        live = sum(((ov >> np.uint64(p * w)) & np.uint64((1 << w) - 1 if w < 64 else ~0)) != 0 for p in range(npan))
-        want_panels = int(np.maximum(live, 1).sum()) if npan > 1 else int(meet.sum())
-        assert st.extra["k_panels"] == want_panels and st.flops == 2 * bs * bs * 32 * want_panels
+        live = sum(((ov >> np.uint64(p * w)) & np.uint64((1 << w) - 1)) != 0 for p in range(npan))
+        want_rows = kp * int(np.maximum(live, 1).sum()) if npan > 1 else bs * int(meet.sum())
+        assert st.extra["k_rows"] == want_rows and st.flops == 2 * bs * bs * want_rows
     monkeypatch.setenv("QM_SUPPORT_FILTER", "0")
     c0 = ses.multiply(a, b)
     assert ses.last_multiply.n_triples == ta.size and ses.last_multiply.zero_blocks > 0
