@@ -159,9 +159,9 @@ class CudaBackend:
     def __init__(self, stream=None):
         self.stream = stream
 
-    def symbolic_state(self, layout, a_keys: torch.Tensor, b_keys: torch.Tensor):
+    def symbolic_state(self, layout, a_keys: torch.Tensor, b_keys: torch.Tensor, a_cmask=None, b_rmask=None):
         return spgemm.SymbolicState(layout, a_keys, int(a_keys.shape[0]), b_keys, int(b_keys.shape[0]),
-                                    self.stream)
+                                    self.stream, a_cmask, b_rmask)
 
     def gather_blocks(self, blocks: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
         import ctypes  # noqa: F401
@@ -378,8 +378,20 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     empty = BlockSet.empty(bs, dev)
     if ka.shape[0] == 0 or kb.shape[0] == 0:
         return empty, stats
+    # Support masks (spgemm.symbolic): gathered with the keys when some rank's blocks have partial
+    # supports, so every rank skips the same exactly-zero block pairs and k panels.
+    ma = mb = None
+    if spgemm.support_filter_enabled() and a_local.blocks.is_cuda:
+        a_local.support_masks()
+        if not b_is_a:
+            b_local.support_masks()
+        partial = not (a_local.masks_full[1] or (a_local if b_is_a else b_local).masks_full[0])
+        if comm.allreduce_max(1.0 if partial else 0.0, dev) > 0.0:
+            ma, _ = comm.allgather_varlen(a_local.masks[1].contiguous())
+            mb, _ = comm.allgather_varlen((a_local if b_is_a else b_local).masks[0].contiguous())
     t1 = clock()
-    st = backend.symbolic_state(layout, ka, kb)
+    st = (backend.symbolic_state(layout, ka, kb, a_cmask=ma, b_rmask=mb) if ma is not None
+          else backend.symbolic_state(layout, ka, kb))
     stats.n_c_global, stats.n_triples_global = st.n_c, st.n_t
     if st.n_c == 0:
         return empty, stats
@@ -450,8 +462,15 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     c_tptr_local = (c_tptr[m0:m1 + 1] - lo).contiguous()
     c_keys_local = c_keys[m0:m1].contiguous()
     dummy_a = torch.empty(0, dtype=torch.float64, device=dev)
-    pa = BlockSet(need_a, pool_a, dummy_a)
-    pb = BlockSet(need_b, pool_b, dummy_a)
+    if ma is not None:  # the pools' masks are the gathered ones (A columns, B rows), not recomputed
+        none_a = torch.full((need_a.shape[0],), -1, dtype=torch.int64, device=dev)
+        none_b = torch.full((need_b.shape[0],), -1, dtype=torch.int64, device=dev)
+        pa = BlockSet(need_a, pool_a, dummy_a, torch.stack([none_a, ma[need_a]]), (False, False))
+        pb = BlockSet(need_b, pool_b, dummy_a, torch.stack([mb[need_b], none_b]), (False, False))
+    else:  # full supports (or filter off): nothing to skip, and no per-product mask pass
+        pa = BlockSet(need_a, pool_a, dummy_a, masks_full=(True, True))
+        pb = BlockSet(need_b, pool_b, dummy_a, masks_full=(True, True))
+        pa.masks = pb.masks = torch.empty((2, 0), dtype=torch.int64, device=dev)
     c = backend.numeric(layout, pa, pb, tri_local, c_tptr_local, c_keys_local)
     t4 = clock()
     stats.n_c_local = c.n

@@ -33,14 +33,33 @@ def _worker(rank, world, port, cfg_name, outdir, mode="exchange"):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
-    cfg = G.CONFIGS[cfg_name] if cfg_name in G.CONFIGS else G.BaselineConfig("r", "random", 8192, 64, per_row=8)
-    geom = cfg.geometry
-    parts = []
-    for m in (0, 1):
-        keys = G.config_keys(cfg, m)
-        cut = np.r_[0, np.sort(np.random.default_rng(m).choice(keys.size, world - 1, replace=False)), keys.size]
-        parts.append(G.device_blocks(geom, keys[cut[rank]:cut[rank + 1]], cfg.seed, m, G.config_pattern(cfg),
-                                     cfg.half_bw, dev))
+    full = None
+    if cfg_name == "masked":  # partial block supports: the support-mask filter runs distributed
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        import helpers
+
+        from paper_2011_11762_b200 import MatrixSession
+        from paper_2011_11762_b200.blocks import BlockSet
+
+        ses = MatrixSession(device=dev)
+        mats = [helpers.build(ses, helpers.banded_support_decay(2048, 20, 7 + m), 64, 64) for m in (0, 1)]
+        geom = mats[0].geometry
+        full = [m.root.blockset for m in mats]
+        parts = []
+        for m in (0, 1):
+            n = full[m].n
+            cut = np.r_[0, np.sort(np.random.default_rng(m).choice(n, world - 1, replace=False)), n]
+            sl = slice(int(cut[rank]), int(cut[rank + 1]))
+            parts.append(BlockSet(full[m].keys[sl].clone(), full[m].blocks[sl].clone(), full[m].sumsq[sl].clone()))
+    else:
+        cfg = G.CONFIGS[cfg_name] if cfg_name in G.CONFIGS else G.BaselineConfig("r", "random", 8192, 64, per_row=8)
+        geom = cfg.geometry
+        parts = []
+        for m in (0, 1):
+            keys = G.config_keys(cfg, m)
+            cut = np.r_[0, np.sort(np.random.default_rng(m).choice(keys.size, world - 1, replace=False)), keys.size]
+            parts.append(G.device_blocks(geom, keys[cut[rank]:cut[rank + 1]], cfg.seed, m, G.config_pattern(cfg),
+                                         cfg.half_bw, dev))
     layout = _ffi.make_layout(geom.params, geom.bs)
     comm = D.Comm()
     c, st = D.multiply(comm, layout, parts[0], parts[1], mode=mode)
@@ -56,8 +75,9 @@ def _worker(rank, world, port, cfg_name, outdir, mode="exchange"):
     allinfo = [torch.zeros_like(info) for _ in range(world)]
     dist.all_gather(allinfo, info)
     if rank == 0:
-        full = [G.device_blocks(geom, G.config_keys(cfg, m), cfg.seed, m, G.config_pattern(cfg), cfg.half_bw, dev)
-                for m in (0, 1)]
+        if full is None:
+            full = [G.device_blocks(geom, G.config_keys(cfg, m), cfg.seed, m, G.config_pattern(cfg), cfg.half_bw,
+                                    dev) for m in (0, 1)]
         ref = spgemm.multiply_blocks(layout, full[0], full[1])
         np.savez(os.path.join(outdir, "out.npz"),
                  same_keys=torch.equal(keys, ref.keys), same_blocks=torch.equal(blocks.view(ref.blocks.shape), ref.blocks)
@@ -70,7 +90,7 @@ def _worker(rank, world, port, cfg_name, outdir, mode="exchange"):
 
 
 @pytest.mark.parametrize("mode", ["exchange", "fused"])
-@pytest.mark.parametrize("world,cfg", [(2, "C1"), (3, "C2-16384"), (2, "random")])
+@pytest.mark.parametrize("world,cfg", [(2, "C1"), (3, "C2-16384"), (2, "random"), (3, "masked")])
 def test_multirank_cuda_backend_equals_single_gpu(tmp_path, world, cfg, mode):
     """mode "fused": the numeric kernel reads remote blocks through CUDA-IPC-mapped peer pools
     (qm_numeric_pools) instead of an exchange -- here the peers share the one GPU."""
