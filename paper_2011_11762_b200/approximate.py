@@ -31,14 +31,19 @@ from .layout import Geometry
 
 @dataclass
 class PruneResult:
-    prune_log: list = field(default_factory=list)   # bounds of the pruned tasks (engine.prune_log)
+    prune_log: list | torch.Tensor = field(default_factory=list)  # pruned tasks' bounds (engine.prune_log)
     leaf_pairs: torch.Tensor | None = None           # sorted codes of surviving (li, lk, lj)
     pairs_per_level: list = field(default_factory=list)
 
 
 def _node_tables(geom: Geometry, s: BlockSet, lay):
-    """Every level's (Morton codes, norms, count) of one operand (qm_node_norms)."""
+    """Every level's (Morton codes, norms, count) of one operand (qm_node_norms) -- the quadtree's
+    node norms, fixed for an (immutable) block set, so kept with it after the first product."""
     import ctypes
+
+    cached = getattr(s, "_node_tables", None)
+    if cached is not None and cached[0] == (geom.params.depth, geom.nbl):
+        return cached[1]
 
     lib = _ffi.load()
     n = s.n
@@ -52,7 +57,9 @@ def _node_tables(geom: Geometry, s: BlockSet, lay):
     _ffi.check(lib.qm_node_norms(ctypes.byref(lay), _ffi.ptr(s.keys), _ffi.ptr(s.sumsq), n, _ffi.ptr(codes),
                                  _ffi.ptr(norms), counts, _ffi.ptr(ws), wb,
                                  _ffi.stream_handle(torch.cuda.current_stream(dev))), "qm_node_norms")
-    return [(codes[l * n:], norms[l * n:], int(counts[l])) for l in range(L)]
+    tables = [(codes[l * n:], norms[l * n:], int(counts[l])) for l in range(L)]
+    s._node_tables = ((geom.params.depth, geom.nbl), tables)
+    return tables
 
 
 def prune(geom: Geometry, a: BlockSet, b: BlockSet, tau: float, a_sym: bool = False, b_sym: bool = False,
@@ -69,7 +76,8 @@ def prune(geom: Geometry, a: BlockSet, b: BlockSet, tau: float, a_sym: bool = Fa
     depth = geom.params.depth
     dev = a.keys.device
     lay = _ffi.make_layout(geom.params, geom.bs)
-    ta, tb = _node_tables(geom, a, lay), _node_tables(geom, b, lay)
+    ta = _node_tables(geom, a, lay)
+    tb = ta if b is a else _node_tables(geom, b, lay)
     sh = _ffi.stream_handle(torch.cuda.current_stream(dev))
     parents = torch.zeros(1, dtype=torch.int64, device=dev)
     n_par = 0
@@ -94,7 +102,7 @@ def prune(geom: Geometry, a: BlockSet, b: BlockSet, tau: float, a_sym: bool = Fa
         if n_par == 0:
             break
     if logs:
-        res.prune_log = torch.cat(logs).tolist()
+        res.prune_log = torch.cat(logs)  # device; _EngineInfo converts on first read
     if n_par and len(res.pairs_per_level) == depth + 1:
         w = 1 << depth
         mask = (1 << 21) - 1

@@ -511,13 +511,21 @@ class MatrixSession:
         return sum(s.bytes_received for s in self.last_stats)
 
 
-@dataclass
 class _EngineInfo:
     """What the reference's ``session.last_engine`` exposes for the approximate variant:
-    ``prune_log`` = bounds of the pruned subproducts (engine.py:156, 273-275)."""
+    ``prune_log`` = bounds of the pruned subproducts (engine.py:156, 273-275). The bounds stay on
+    the device until first read (a product can prune ~10^5 tasks; the list is built on access)."""
 
-    prune_log: list
-    pairs_per_level: list
+    def __init__(self, prune_log, pairs_per_level: list):
+        self._log = prune_log
+        self._list = None if isinstance(prune_log, torch.Tensor) else list(prune_log)
+        self.pairs_per_level = pairs_per_level
+
+    @property
+    def prune_log(self) -> list:
+        if self._list is None:
+            self._list = self._log.tolist()
+        return self._list
 
 
 def _read_coordinate_text(path):
