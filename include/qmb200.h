@@ -157,8 +157,8 @@ QM_API int qm_numeric(const qm_layout *layout, const uint64_t *a_keys, const dou
                const double *b_blocks, int64_t nB, const uint32_t *tri, const int64_t *c_tptr,
                const uint64_t *c_keys, int64_t nC, int64_t nT, double *c_blocks, double *c_sumsq,
                uint8_t *c_nonzero, int64_t *zero_count, void *ws, size_t ws_bytes, void *stream);
-/* qm_numeric with the operands' support masks (qm_block_masks; NULL = full support): for bs 64/128
- * the TMA kernel skips the k panels (16 deep for bs 64, 32 for bs 128) of a triple where A's nonzero
+/* qm_numeric with the operands' support masks (qm_block_masks; NULL = full support): for bs 32-128
+ * the TMA kernel skips the k panels (16 deep for bs 32/64, 32 for bs 128) of a triple where A's nonzero
  * columns and B's nonzero rows do not meet (they add exactly zero). *panel_count (device int64, may
  * be NULL) receives the k depth executed by the bs 32/64/128 kernel, summed over triples (bs per
  * triple without skipping; -1 for other kernels): the executed flops are 2*bs*bs*count. */

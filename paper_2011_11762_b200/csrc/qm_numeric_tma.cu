@@ -557,6 +557,7 @@ bool use_wide(int64_t nU, int64_t nC, int64_t nT) {
 // Masked products (operands with partial block supports): 16-deep k panels, so the panel skip of
 // k_triple_panels works at half the granularity; 4 stages of 16 KB, 3 CTAs/SM.
 using Tma64k16 = TmaCfg<64, 64, 2, 2, 16, 4, 3>;
+using Tma32k16 = TmaCfg<32, 32, 2, 2, 16, 4, 6>;  // same for bs 32: 4 stages of 8 KB, 6 CTAs/SM
 bool use_k16(const NumericAux &oi) {
   const char *e = getenv("QM_PANEL16");
   return oi.a_cmask && oi.b_rmask && !(e && strcmp(e, "0") == 0);
@@ -569,7 +570,7 @@ using Tma128m = TmaCfg<128, 64, 2, 2, 32, 2, 3>;
 
 size_t numeric_tma_ws_bytes(int bs, int64_t nC, int64_t nT) {
   switch (bs) {
-    case 32: return tma_ws_bytes<Tma32>(nC, nT);
+    case 32: return std::max(tma_ws_bytes<Tma32>(nC, nT), tma_ws_bytes<Tma32k16>(nC, nT));
     case 64:
       return std::max(std::max(tma_ws_bytes<Tma64>(nC, nT), tma_ws_bytes<Tma64m>(nC, nT)),
                       tma_ws_bytes<Tma64k16>(nC, nT));
@@ -587,6 +588,8 @@ int launch_numeric_tma(int bs, const double *const *A, const int64_t *nA, int na
   const uint2 *t2 = (const uint2 *)tri;
   switch (bs) {
     case 32:
+      if (use_k16(oi))
+        return launch_tma<Tma32k16>(A, nA, na, B, nB, nb, t2, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes, st);
       return launch_tma<Tma32>(A, nA, na, B, nB, nb, t2, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes, st);
     case 64:
       if (use_k16(oi))

@@ -742,8 +742,8 @@ def test_support_filter_skips_exact_zero_products(ses, monkeypatch, n, bw, leaf,
     meet = (cmask[ta] & rmask[tb]) != 0
     assert st.n_triples == int(meet.sum()) and st.n_triples < ta.size  # some products were skipped
     assert st.zero_blocks == 0
-    if bs >= 32:  # k panels (16 deep at bs 64, 32 deep at bs 128) of the surviving triples where the supports meet
-        kp = 16 if bs == 64 else 32
+    if bs >= 32:  # k panels (16 deep at bs 32/64, 32 deep at bs 128) of the surviving triples where the supports meet
+        kp = 16 if bs <= 64 else 32
         npan, w = bs // kp, 64 * kp // max(bs, 64)
         ov = (cmask[ta] & rmask[tb])[meet]
         live = sum(((ov >> np.uint64(p * w)) & np.uint64((1 << w) - 1)) != 0 for p in range(npan))
