@@ -48,8 +48,9 @@ __global__ void k_decode_rows(const uint64_t *a_keys, int64_t nA, const uint64_t
 __global__ void k_cols_rowptr(const uint64_t *a_keys, const uint64_t *b_keys, const uint32_t *srow,
                               const uint32_t *perm, int64_t n, int64_t nbg, int nbl, int lbits,
                               const uint64_t *a_cmask, const uint64_t *b_rmask, uint32_t *scol,
-                              uint32_t *rp, uint64_t *smask) {
+                              uint32_t *rp, uint64_t *smask, int *masked) {
   const int64_t span = n > 2 * nbg + 1 ? n : 2 * nbg + 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *masked = (a_cmask || b_rmask) ? 1 : 0;
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < span;
        x += (int64_t)gridDim.x * blockDim.x) {
     if (x < n) {
@@ -58,7 +59,7 @@ __global__ void k_cols_rowptr(const uint64_t *a_keys, const uint64_t *b_keys, co
       qkey_decode((is_a ? a_keys : b_keys)[perm[x]], nbl, lbits, &bi, &bj);
       scol[x] = bj;
       const uint64_t *m = is_a ? a_cmask : b_rmask;
-      smask[x] = m ? m[perm[x]] : ~0ull;
+      if (a_cmask || b_rmask) smask[x] = m ? m[perm[x]] : ~0ull;
     }
     if (x <= 2 * nbg) {
       int64_t lo = 0, hi = n;
@@ -192,18 +193,19 @@ __device__ __forceinline__ uint32_t lower_bound_col(const uint32_t *b_scol, uint
 // dropped by _set_block anyway).
 template <class F>
 __device__ void for_window_pairs(const RowSpan &s, uint32_t wbase, bool multi, const uint32_t *a_scol,
-                                 const uint32_t *b_rp, const uint32_t *b_scol, const uint64_t *smask, F f) {
+                                 const uint32_t *b_rp, const uint32_t *b_scol, const uint64_t *smask, bool masked,
+                                 F f) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint32_t wend = wbase + kWin;
   for (uint32_t x = s.a0 + warp; x < s.a1; x += nw) {
     uint32_t k = a_scol[x];
-    const uint64_t am = smask[x];
+    const uint64_t am = masked ? smask[x] : ~0ull;
     uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
     if (multi) b0 = lower_bound_col(b_scol, b0, b1, wbase);
     for (uint32_t y = b0 + lane; y < b1; y += 32) {
       uint32_t j = b_scol[y];
       if (j >= wend) break;
-      if (am & smask[y]) f(x, y, j);
+      if (!masked || (am & smask[y])) f(x, y, j);
     }
   }
 }
@@ -214,13 +216,14 @@ __device__ void for_window_pairs(const RowSpan &s, uint32_t wbase, bool multi, c
 // read-back.
 __global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const uint32_t *a_scol,
                                                    const uint32_t *b_rp, const uint32_t *b_scol,
-                                                   const uint64_t *smask, int64_t nbg, uint64_t *cnt,
-                                                   uint64_t *off, unsigned int *done,
+                                                   const uint64_t *smask, const int *masked_flag, int64_t nbg,
+                                                   uint64_t *cnt, uint64_t *off, unsigned int *done,
                                                    volatile int64_t *host_tot) {
   __shared__ uint32_t bm[kWin / 32];
   __shared__ uint64_t red64[32];
   __shared__ uint32_t red32[32];
   __shared__ bool last;
+  const bool masked = *masked_flag != 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt[2 * nbg] = 0;  // exclusive-scan tail
   for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
     RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
@@ -233,7 +236,7 @@ __global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const u
         for (int w = threadIdx.x; w < kWin / 32; w += blockDim.x) bm[w] = 0u;
         __syncthreads();
         uint64_t mine = 0;
-        for_window_pairs(s, wbase, multi, a_scol, b_rp, b_scol, smask, [&](uint32_t, uint32_t, uint32_t j) {
+        for_window_pairs(s, wbase, multi, a_scol, b_rp, b_scol, smask, masked, [&](uint32_t, uint32_t, uint32_t j) {
           uint32_t o = j - wbase;
           atomicOr(&bm[o >> 5], 1u << (o & 31));
           ++mine;
@@ -268,13 +271,15 @@ __global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const u
 
 __global__ void __launch_bounds__(kNT) k_sym_emit_c(const uint32_t *a_rp, const uint32_t *a_scol,
                                                     const uint32_t *b_rp, const uint32_t *b_scol,
-                                                    const uint64_t *smask, int64_t nbg, int nbl, int lbits,
+                                                    const uint64_t *smask, const int *masked_flag, int64_t nbg,
+                                                    int nbl, int lbits,
                                                     const uint64_t *rowC_off, uint64_t *rm_key,
                                                     uint32_t *rm_cnt, uint32_t *rm_iota, unsigned int *done) {
   __shared__ uint32_t cnt[kWin];
   __shared__ uint64_t red64[32];
   __shared__ uint32_t red32[32];
   if (blockIdx.x == 0 && threadIdx.x == 0) *done = 0u;  // k_inv_counts' completion ticket
+  const bool masked = *masked_flag != 0;
   for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
     RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
     if (s.nt > 0) {
@@ -284,7 +289,7 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_c(const uint32_t *a_rp, const 
         const uint32_t wbase = (uint32_t)wb;
         for (int w = threadIdx.x; w < kWin; w += blockDim.x) cnt[w] = 0u;
         __syncthreads();
-        for_window_pairs(s, wbase, multi, a_scol, b_rp, b_scol, smask,
+        for_window_pairs(s, wbase, multi, a_scol, b_rp, b_scol, smask, masked,
                          [&](uint32_t, uint32_t, uint32_t j) { atomicAdd(&cnt[j - wbase], 1u); });
         __syncthreads();
         const int s0 = threadIdx.x * kPer;
@@ -321,7 +326,8 @@ static_assert(kPerT == 8, "slot ownership assumes 8 slots per thread");
 
 __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
     const uint32_t *a_rp, const uint32_t *a_scol, const uint32_t *a_perm, const uint32_t *b_rp,
-    const uint32_t *b_scol, const uint32_t *b_perm, const uint64_t *smask, int64_t nbg, const uint64_t *rowC_off,
+    const uint32_t *b_scol, const uint32_t *b_perm, const uint64_t *smask, const int *masked_flag, int64_t nbg,
+    const uint64_t *rowC_off,
     const uint32_t *inv, const int64_t *c_tptr, int64_t t_lo, int64_t t_hi, uint2 *tri) {
   __shared__ uint32_t mask[kWinT];
   __shared__ int64_t cur[kWinT];
@@ -331,6 +337,7 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kNT >> 5;
   const int s0 = threadIdx.x * kPerT;
   const bool ranged = t_lo > 0 || t_hi < c_tptr[rowC_off[nbg]];
+  const bool masked = *masked_flag != 0;
   for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
     if (ranged) {
       // A multi-GPU rank emits one triple range: skip rows none of whose C blocks reach it
@@ -358,13 +365,13 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
         // occupied C columns of the window
         for (uint32_t x = s.a0 + warp; x < s.a1; x += nw) {
           uint32_t k = a_scol[x];
-          const uint64_t am = smask[x];
+          const uint64_t am = masked ? smask[x] : ~0ull;
           uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
           if (multi) b0 = lower_bound_col(b_scol, b0, b1, wbase);
           for (uint32_t y = b0 + lane; y < b1; y += 32) {
             uint32_t j = b_scol[y];
             if (j >= wend) break;
-            if (am & smask[y]) atomicOr(&bm[(j - wbase) >> 5], 1u << ((j - wbase) & 31));
+            if (!masked || (am & smask[y])) atomicOr(&bm[(j - wbase) >> 5], 1u << ((j - wbase) & 31));
           }
         }
         __syncthreads();
@@ -381,27 +388,27 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
           __syncthreads();
           for (uint32_t x = x0 + warp; x < xe; x += nw) {
             uint32_t k = a_scol[x];
-            const uint64_t am = smask[x];
+            const uint64_t am = masked ? smask[x] : ~0ull;
             uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
             if (multi) b0 = lower_bound_col(b_scol, b0, b1, wbase);
             for (uint32_t y = b0 + lane; y < b1; y += 32) {
               uint32_t j = b_scol[y];
               if (j >= wend) break;
-              if (am & smask[y]) atomicOr(&mask[j - wbase], 1u << (x - x0));
+              if (!masked || (am & smask[y])) atomicOr(&mask[j - wbase], 1u << (x - x0));
             }
           }
           __syncthreads();
           for (uint32_t x = x0 + warp; x < xe; x += nw) {
             const uint32_t k = a_scol[x];
             const uint32_t ai = a_perm[x];
-            const uint64_t am = smask[x];
+            const uint64_t am = masked ? smask[x] : ~0ull;
             const uint32_t below = (1u << (x - x0)) - 1u;
             uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
             if (multi) b0 = lower_bound_col(b_scol, b0, b1, wbase);
             for (uint32_t y = b0 + lane; y < b1; y += 32) {
               uint32_t j = b_scol[y];
               if (j >= wend) break;
-              if (!(am & smask[y])) continue;
+              if (masked && !(am & smask[y])) continue;
               const int64_t p = cur[j - wbase] + __popc(mask[j - wbase] & below);
               if (p >= t_lo && p < t_hi) tri[p - t_lo] = make_uint2(ai, b_perm[y]);
             }
@@ -462,6 +469,7 @@ inline int bits_for(uint64_t maxval) {
 struct SymWs {
   uint32_t *rowkey, *val, *srow, *perm, *scol, *rp;
   uint64_t *smask;  // support mask of every sorted entry (see k_cols_rowptr)
+  int *masked;      // 1 when the count phase was given support masks
   uint64_t *cnt;   // [2*nbg+1]: C blocks per row, triples per row, 0
   uint64_t *off;   // exclusive scan of cnt: rowC_off = off, nC = off[nbg], nT = off[2nbg] - off[nbg]
   unsigned int *done;  // k_sym_count's completion ticket
@@ -484,6 +492,7 @@ SymWs carve_sym(Carver &cv, int64_t nA, int64_t nB, int64_t nbg) {
   w.rowkey = cv.take<uint32_t>(n); w.val = cv.take<uint32_t>(n); w.srow = cv.take<uint32_t>(n);
   w.perm = cv.take<uint32_t>(n); w.scol = cv.take<uint32_t>(n);
   w.smask = cv.take<uint64_t>(n);
+  w.masked = cv.take<int>(1);
   w.rp = cv.take<uint32_t>(2 * nbg + 1);
   w.cnt = cv.take<uint64_t>(2 * nbg + 1);
   w.off = cv.take<uint64_t>(2 * nbg + 1);
@@ -538,7 +547,7 @@ int build_rows(const uint64_t *a_keys, const uint64_t *a_cmask, int64_t nA, cons
     QM_CUDA_TRY(cudaGetLastError());
   }
   k_cols_rowptr<<<grid_for(std::max<int64_t>(n, 2 * g.nbg + 1)), 256, 0, st>>>(
-      a_keys, b_keys, w.srow, w.perm, n, g.nbg, g.nbl, g.lbits, a_cmask, b_rmask, w.scol, w.rp, w.smask);
+      a_keys, b_keys, w.srow, w.perm, n, g.nbg, g.nbl, g.lbits, a_cmask, b_rmask, w.scol, w.rp, w.smask, w.masked);
   QM_LAUNCHED("k_cols_rowptr");
   return QM_OK;
 }
@@ -589,8 +598,8 @@ extern "C" int qm_spgemm_count_masked(const qm_layout *layout, const uint64_t *a
   int64_t *host_tot = nullptr, *dev_tot = nullptr;
   rc = mapped_i64(&host_tot, &dev_tot);
   if (rc != QM_OK) return rc;
-  k_sym_count<<<row_grid(g.nbg), kNT, 0, st>>>(a_rp, w.scol, b_rp, w.scol, w.smask, g.nbg, w.cnt, w.off,
-                                               w.done, dev_tot);
+  k_sym_count<<<row_grid(g.nbg), kNT, 0, st>>>(a_rp, w.scol, b_rp, w.scol, w.smask, w.masked, g.nbg, w.cnt,
+                                               w.off, w.done, dev_tot);
   QM_LAUNCHED("k_sym_count");
   QM_CUDA_TRY(cudaStreamSynchronize(st));
   uint64_t tot[2] = {(uint64_t)((volatile int64_t *)host_tot)[0], (uint64_t)((volatile int64_t *)host_tot)[1]};
@@ -652,7 +661,7 @@ extern "C" int qm_spgemm_fill_keys(const qm_layout *layout, int64_t nA, int64_t 
   if (rc != QM_OK) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   if (nC == 0) return cudaMemsetAsync(c_tptr, 0, sizeof(int64_t), st) == cudaSuccess ? QM_OK : QM_ERR_CUDA;
-  k_sym_emit_c<<<row_grid(g.nbg), kNT, 0, st>>>(w.rp, w.scol, w.rp + g.nbg, w.scol, w.smask, g.nbg, g.nbl,
+  k_sym_emit_c<<<row_grid(g.nbg), kNT, 0, st>>>(w.rp, w.scol, w.rp + g.nbg, w.scol, w.smask, w.masked, g.nbg, g.nbl,
                                                 g.lbits, w.off, f.rm_key, f.rm_cnt, f.rm_iota, f.done);
   QM_LAUNCHED("k_sym_emit_c");
   size_t tb = f.cub_bytes;
@@ -682,7 +691,7 @@ extern "C" int qm_spgemm_fill_triples(const qm_layout *layout, int64_t nA, int64
   if (nC == 0 || t_hi <= t_lo) return QM_OK;
   cudaStream_t st = (cudaStream_t)stream;
   k_sym_emit_tri<<<row_grid(g.nbg), kNT, 0, st>>>(w.rp, w.scol, w.perm, w.rp + g.nbg, w.scol,
-                                                  w.perm, w.smask, g.nbg, w.off, f.inv, c_tptr, t_lo,
+                                                  w.perm, w.smask, w.masked, g.nbg, w.off, f.inv, c_tptr, t_lo,
                                                   t_hi, (uint2 *)tri);
   QM_LAUNCHED("k_sym_emit_tri");
   return QM_OK;
