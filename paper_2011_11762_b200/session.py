@@ -249,6 +249,9 @@ class MatrixSession:
 
                 same = a_root is b_root
                 a_stored, b_stored = a, b
+                if spgemm.support_filter_enabled():  # on the stored sets (kept), carried through
+                    a.support_masks()                # the transposes / expansions below
+                    b.support_masks()
                 if args.get("a_sym"):
                     a = variants.expand_symmetric(geom, a)
                 if args.get("b_sym"):
@@ -264,6 +267,10 @@ class MatrixSession:
                     self.last_engine = _EngineInfo(pr.prune_log, pr.pairs_per_level)
                     ax, bx = a, b
                     plan_filter = lambda plan: approximate.filter_plan(geom, plan, ax, bx, pr)  # noqa: E731
+                if args.get("upper"):  # compute only the kept (upper-leaf) C blocks
+                    inner = plan_filter
+                    plan_filter = lambda plan: variants.upper_plan(  # noqa: E731
+                        geom, inner(plan) if inner is not None else plan)
             c = spgemm.multiply_blocks(layout, a, b, stats=stats, plan_filter=plan_filter)
             if args.get("upper"):
                 c = variants.upper_leaves(geom, c)

@@ -77,9 +77,13 @@ def _transposed_blocks(blocks: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def _sorted(keys: torch.Tensor, blocks: torch.Tensor, sumsq: torch.Tensor) -> BlockSet:
+def _sorted(keys: torch.Tensor, blocks: torch.Tensor, sumsq: torch.Tensor, masks=None,
+            masks_full=(False, False)) -> BlockSet:
     order = torch.argsort(keys, stable=True)
-    return BlockSet(keys[order].contiguous(), _gather(blocks, order), sumsq[order].contiguous())
+    out = BlockSet(keys[order].contiguous(), _gather(blocks, order), sumsq[order].contiguous())
+    if masks is not None:  # support masks follow their blocks (no mask pass on the derived set)
+        out.masks, out.masks_full = masks[:, order].contiguous(), masks_full
+    return out
 
 
 def transpose(geom: Geometry, x: BlockSet) -> BlockSet:
@@ -88,7 +92,8 @@ def transpose(geom: Geometry, x: BlockSet) -> BlockSet:
         return x
     bi, bj = _decode(geom, x.keys)
     keys = _encode(geom, bj, bi)
-    return _sorted(keys, _transposed_blocks(x.blocks), x.sumsq)
+    m = x.masks[[1, 0]] if x.masks is not None else None  # a transposed block swaps row / column supports
+    return _sorted(keys, _transposed_blocks(x.blocks), x.sumsq, m, (x.masks_full[1], x.masks_full[0]))
 
 
 def expand_symmetric(geom: Geometry, s: BlockSet) -> BlockSet:
@@ -104,7 +109,13 @@ def expand_symmetric(geom: Geometry, s: BlockSet) -> BlockSet:
         return s
     tb = _transposed_blocks(_gather(s.blocks, idx))
     tk = _encode(geom, bj[idx], bi[idx])
-    return _sorted(torch.cat([s.keys, tk]), torch.cat([s.blocks, tb]), torch.cat([s.sumsq, s.sumsq[idx]]))
+    m = full = None
+    if s.masks is not None:
+        m = torch.cat([s.masks, s.masks[[1, 0]][:, idx]], dim=1)
+        both = s.masks_full[0] and s.masks_full[1]
+        full = (both, both)
+    return _sorted(torch.cat([s.keys, tk]), torch.cat([s.blocks, tb]), torch.cat([s.sumsq, s.sumsq[idx]]), m,
+                   full if full is not None else (False, False))
 
 
 def upper_leaves(geom: Geometry, c: BlockSet) -> BlockSet:
@@ -115,4 +126,31 @@ def upper_leaves(geom: Geometry, c: BlockSet) -> BlockSet:
     keep = torch.nonzero((bi // geom.nbl) <= (bj // geom.nbl)).flatten()
     if keep.numel() == c.n:
         return c
-    return BlockSet(c.keys[keep].contiguous(), _gather(c.blocks, keep), c.sumsq[keep].contiguous())
+    out = BlockSet(c.keys[keep].contiguous(), _gather(c.blocks, keep), c.sumsq[keep].contiguous())
+    if c.masks is not None:
+        out.masks, out.masks_full = c.masks[:, keep].contiguous(), c.masks_full
+    return out
+
+
+def upper_plan(geom: Geometry, plan):
+    """Restricts a symbolic plan to the C blocks of leaves (li, lj) with li <= lj before the numeric
+    phase, so the `upper` variants (symmetric_square, rank_k) compute only the blocks they keep --
+    the reference's diagonal-path tasks never spawn their SW products (ops.py:214-216). Triples keep
+    their order (k ascending per C block)."""
+    from .spgemm import SymbolicPlan  # noqa: PLC0415
+
+    if plan.n_c == 0:
+        return plan
+    bi, bj = _decode(geom, plan.c_keys)
+    keep = torch.nonzero((bi // geom.nbl) <= (bj // geom.nbl)).flatten()
+    if keep.numel() == plan.n_c:
+        return plan
+    cnt = (plan.c_tptr[1:] - plan.c_tptr[:-1])[keep]
+    tptr = torch.zeros(keep.numel() + 1, dtype=torch.int64, device=cnt.device)
+    torch.cumsum(cnt, 0, out=tptr[1:])
+    nt = int(tptr[-1])
+    src = torch.repeat_interleave(plan.c_tptr[:-1][keep] - tptr[:-1], cnt, output_size=nt)
+    src += torch.arange(nt, dtype=torch.int64, device=cnt.device)
+    tri = plan.tri.view(-1, 2)[src].reshape(-1).contiguous()
+    return SymbolicPlan(int(keep.numel()), nt, plan.c_keys[keep].contiguous(), tptr, tri)
+
