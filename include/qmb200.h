@@ -116,11 +116,15 @@ QM_API int qm_spgemm_count(const qm_layout *layout, const uint64_t *a_keys /*dev
  * the nonzero-column mask of A block t and the nonzero-row mask of B block t (qm_block_masks). A
  * pair whose masks share no bit multiplies to an exactly-zero block: it yields no triple, and a C
  * block without any surviving triple is not created (it would be an exact-zero block, which
- * _set_block, block_sparse.py:37-41, drops). The fill calls of the same workspace use the masks too. */
+ * _set_block, block_sparse.py:37-41, drops). The fill calls of the same workspace use the masks too.
+ * flags & QM_SPGEMM_UPPER: only the C blocks of leaves (li, lj) with li <= lj are enumerated -- the
+ * reference's symmetric_square / rank_k never spawn the SW products of diagonal-path nodes
+ * (ops.py:214-216). */
+#define QM_SPGEMM_UPPER 1 /* flags: only C blocks of leaves (li, lj) with li <= lj (the `upper` variants) */
 QM_API int qm_spgemm_count_masked(const qm_layout *layout, const uint64_t *a_keys, const uint64_t *a_cmask,
                                   int64_t nA, const uint64_t *b_keys, const uint64_t *b_rmask, int64_t nB,
-                                  void *ws, size_t ws_bytes, int64_t *n_c_out, int64_t *n_triples_out,
-                                  void *stream);
+                                  int32_t flags, void *ws, size_t ws_bytes, int64_t *n_c_out,
+                                  int64_t *n_triples_out, void *stream);
 QM_API size_t qm_spgemm_fill_workspace_bytes(const qm_layout *layout, int64_t nC);
 /* Emits the C key set in quadtree-key order (c_keys[nC]), the triple offsets c_tptr[nC+1] and the
  * triples tri[2*nT] = (a_index, b_index) pairs, grouped by C block, k ascending within a group --
@@ -213,6 +217,11 @@ QM_API int qm_gather_blocks(int32_t block_size, const double *src, const int64_t
  * (op_view, leaves/base.py:117-118; ta/tb/symmetric children, ops.py:100-116). */
 QM_API int qm_transpose_blocks(int32_t block_size, const double *src, int64_t n, double *dst,
                                void *stream);
+/* dst[m] = src[idx[m]], transposed where transpose[m] != 0 (transpose may be NULL): a symmetric
+ * operand's full block set from its stored upper triangle in one pass (ops.py:100-116's virtual
+ * transposes, materialised). */
+QM_API int qm_gather_blocks_t(int32_t block_size, const double *src, const int64_t *idx,
+                              const uint8_t *transpose, int64_t n, double *dst, void *stream);
 
 /* ---- add / scale / add_scaled_identity (the step after a product) ---------- */
 /* out[m] = alpha*A[ia[m]] + beta*B[ib[m]] per block, an operand absent when its index is -1;

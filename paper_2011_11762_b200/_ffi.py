@@ -55,6 +55,7 @@ EXPORTS = (
     "qm_block_stats",
     "qm_block_masks",
     "qm_gather_blocks",
+    "qm_gather_blocks_t",
     "qm_transpose_blocks",
     "qm_axpby_blocks",
     "qm_add_identity_blocks",
@@ -103,8 +104,8 @@ _SIGS = {
     "qm_spgemm_workspace_bytes": (_SZ, [_LP, _I64, _I64]),
     "qm_spgemm_count": (ctypes.c_int, [_LP, _P, _I64, _P, _I64, _P, _SZ, ctypes.POINTER(_I64),
                                        ctypes.POINTER(_I64), _P]),
-    "qm_spgemm_count_masked": (ctypes.c_int, [_LP, _P, _P, _I64, _P, _P, _I64, _P, _SZ, ctypes.POINTER(_I64),
-                                             ctypes.POINTER(_I64), _P]),
+    "qm_spgemm_count_masked": (ctypes.c_int, [_LP, _P, _P, _I64, _P, _P, _I64, _I32, _P, _SZ,
+                                             ctypes.POINTER(_I64), ctypes.POINTER(_I64), _P]),
     "qm_spgemm_fill_workspace_bytes": (_SZ, [_LP, _I64]),
     "qm_spgemm_fill": (ctypes.c_int, [_LP, _I64, _I64, _I64, _I64, _P, _SZ, _P, _SZ, _P, _P, _P, _P]),
     "qm_spgemm_fill_keys": (ctypes.c_int, [_LP, _I64, _I64, _I64, _P, _SZ, _P, _SZ, _P, _P, _P]),
@@ -126,6 +127,7 @@ _SIGS = {
     "qm_block_stats": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P]),
     "qm_block_masks": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P]),
     "qm_gather_blocks": (ctypes.c_int, [_I32, _P, _P, _I64, _P, _P]),
+    "qm_gather_blocks_t": (ctypes.c_int, [_I32, _P, _P, _P, _I64, _P, _P]),
     "qm_transpose_blocks": (ctypes.c_int, [_I32, _P, _I64, _P, _P]),
     "qm_axpby_blocks": (ctypes.c_int, [_I32, _I64, _P, _P, ctypes.c_double, ctypes.c_double, _P, _P, _P, _P,
                                        _P, _P, _P]),

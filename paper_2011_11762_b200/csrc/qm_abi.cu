@@ -178,6 +178,35 @@ __global__ void __launch_bounds__(256) k_transpose_blocks(int bs, const double *
   }
 }
 
+// dst[m] = src[idx[m]], transposed when tflag[m] != 0 (32x33 smem tiles): the expansion of a
+// symmetric operand's stored upper triangle in one pass (variants.expand_symmetric).
+__global__ void __launch_bounds__(256) k_gather_blocks_t(int bs, const double *src, const int64_t *idx,
+                                                         const uint8_t *tflag, int64_t n, double *dst) {
+  __shared__ double tile[32][33];
+  const int nt = (bs + 31) / 32;
+  const int64_t work = n * nt * nt;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int64_t w = blockIdx.x; w < work; w += gridDim.x) {
+    const int64_t m = w / (nt * nt);
+    const int t = (int)(w % (nt * nt));
+    const int r0 = (t / nt) * 32, c0 = (t % nt) * 32;
+    const double *sb = src + (size_t)idx[m] * bs * bs;
+    double *d = dst + (size_t)m * bs * bs;
+    const bool tr = tflag && tflag[m];
+    for (int q = ty; q < 32; q += 8)
+      if (r0 + q < bs && c0 + tx < bs) tile[q][tx] = __ldcs(sb + (size_t)(r0 + q) * bs + c0 + tx);
+    __syncthreads();
+    for (int q = ty; q < 32; q += 8) {
+      if (tr) {
+        if (c0 + q < bs && r0 + tx < bs) d[(size_t)(c0 + q) * bs + r0 + tx] = tile[tx][q];
+      } else if (r0 + q < bs && c0 + tx < bs) {
+        d[(size_t)(r0 + q) * bs + c0 + tx] = tile[q][tx];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // out[m] = alpha*A[ia[m]] + beta*B[ib[m]] with an operand absent when its index is -1 (then
 // alpha*A or beta*B alone). Exact IEEE products and sum (no FMA contraction), like numpy's
 // `alpha * a + beta * b` in BlockSparseLeaf.add / scale (block_sparse.py:134-160).
@@ -379,6 +408,20 @@ extern "C" int qm_transpose_blocks(int32_t block_size, const double *src, int64_
   int64_t grid = std::min<int64_t>(n * nt * nt, 148 * 16);
   k_transpose_blocks<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(block_size, src, n, dst);
   QM_LAUNCHED("k_transpose_blocks");
+  return QM_OK;
+}
+
+extern "C" int qm_gather_blocks_t(int32_t block_size, const double *src, const int64_t *idx,
+                                  const uint8_t *transpose, int64_t n, double *dst, void *stream) {
+  if (block_size < 1 || n < 0 || (n > 0 && (!src || !idx || !dst))) {
+    set_error("qm_gather_blocks_t: bad arguments");
+    return QM_ERR_INVALID;
+  }
+  if (n == 0) return QM_OK;
+  const int nt = (block_size + 31) / 32;
+  int64_t grid = std::min<int64_t>(n * nt * nt, 148 * 32);
+  k_gather_blocks_t<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(block_size, src, idx, transpose, n, dst);
+  QM_LAUNCHED("k_gather_blocks_t");
   return QM_OK;
 }
 

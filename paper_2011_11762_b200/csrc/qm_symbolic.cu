@@ -47,10 +47,10 @@ __global__ void k_decode_rows(const uint64_t *a_keys, int64_t nA, const uint64_t
 // nonzero-row mask; all ones when the operand has no masks).
 __global__ void k_cols_rowptr(const uint64_t *a_keys, const uint64_t *b_keys, const uint32_t *srow,
                               const uint32_t *perm, int64_t n, int64_t nbg, int nbl, int lbits,
-                              const uint64_t *a_cmask, const uint64_t *b_rmask, uint32_t *scol,
+                              const uint64_t *a_cmask, const uint64_t *b_rmask, int upper, uint32_t *scol,
                               uint32_t *rp, uint64_t *smask, int *masked) {
   const int64_t span = n > 2 * nbg + 1 ? n : 2 * nbg + 1;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *masked = (a_cmask || b_rmask) ? 1 : 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *masked = ((a_cmask || b_rmask) ? 1 : 0) | (upper ? 2 : 0);
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < span;
        x += (int64_t)gridDim.x * blockDim.x) {
     if (x < n) {
@@ -217,16 +217,18 @@ __device__ void for_window_pairs(const RowSpan &s, uint32_t wbase, bool multi, c
 __global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const uint32_t *a_scol,
                                                    const uint32_t *b_rp, const uint32_t *b_scol,
                                                    const uint64_t *smask, const int *masked_flag, int64_t nbg,
-                                                   uint64_t *cnt, uint64_t *off, unsigned int *done,
+                                                   int nbl, uint64_t *cnt, uint64_t *off, unsigned int *done,
                                                    volatile int64_t *host_tot) {
   __shared__ uint32_t bm[kWin / 32];
   __shared__ uint64_t red64[32];
   __shared__ uint32_t red32[32];
   __shared__ bool last;
-  const bool masked = *masked_flag != 0;
+  const bool masked = (*masked_flag & 1) != 0;
+  const bool upper = (*masked_flag & 2) != 0;  // only C blocks of leaves (li, lj) with li <= lj
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt[2 * nbg] = 0;  // exclusive-scan tail
   for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
     RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
+    if (upper) s.jmin = max(s.jmin, (uint32_t)((i / nbl) * nbl));
     uint32_t total = 0;
     uint64_t ntri = 0;  // surviving triples of the row (<= s.nt, the structural count)
     if (s.nt > 0) {
@@ -236,7 +238,7 @@ __global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const u
         for (int w = threadIdx.x; w < kWin / 32; w += blockDim.x) bm[w] = 0u;
         __syncthreads();
         uint64_t mine = 0;
-        for_window_pairs(s, wbase, multi, a_scol, b_rp, b_scol, smask, masked, [&](uint32_t, uint32_t, uint32_t j) {
+        for_window_pairs(s, wbase, multi || upper, a_scol, b_rp, b_scol, smask, masked, [&](uint32_t, uint32_t, uint32_t j) {
           uint32_t o = j - wbase;
           atomicOr(&bm[o >> 5], 1u << (o & 31));
           ++mine;
@@ -279,9 +281,11 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_c(const uint32_t *a_rp, const 
   __shared__ uint64_t red64[32];
   __shared__ uint32_t red32[32];
   if (blockIdx.x == 0 && threadIdx.x == 0) *done = 0u;  // k_inv_counts' completion ticket
-  const bool masked = *masked_flag != 0;
+  const bool masked = (*masked_flag & 1) != 0;
+  const bool upper = (*masked_flag & 2) != 0;  // only C blocks of leaves (li, lj) with li <= lj
   for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
     RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
+    if (upper) s.jmin = max(s.jmin, (uint32_t)((i / nbl) * nbl));
     if (s.nt > 0) {
       uint64_t out = rowC_off[i];
       const bool multi = (s.jmax - s.jmin) >= (uint32_t)kWin;
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_c(const uint32_t *a_rp, const 
         const uint32_t wbase = (uint32_t)wb;
         for (int w = threadIdx.x; w < kWin; w += blockDim.x) cnt[w] = 0u;
         __syncthreads();
-        for_window_pairs(s, wbase, multi, a_scol, b_rp, b_scol, smask, masked,
+        for_window_pairs(s, wbase, multi || upper, a_scol, b_rp, b_scol, smask, masked,
                          [&](uint32_t, uint32_t, uint32_t j) { atomicAdd(&cnt[j - wbase], 1u); });
         __syncthreads();
         const int s0 = threadIdx.x * kPer;
@@ -327,7 +331,7 @@ static_assert(kPerT == 8, "slot ownership assumes 8 slots per thread");
 __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
     const uint32_t *a_rp, const uint32_t *a_scol, const uint32_t *a_perm, const uint32_t *b_rp,
     const uint32_t *b_scol, const uint32_t *b_perm, const uint64_t *smask, const int *masked_flag, int64_t nbg,
-    const uint64_t *rowC_off,
+    int nbl, const uint64_t *rowC_off,
     const uint32_t *inv, const int64_t *c_tptr, int64_t t_lo, int64_t t_hi, uint2 *tri) {
   __shared__ uint32_t mask[kWinT];
   __shared__ int64_t cur[kWinT];
@@ -337,7 +341,8 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kNT >> 5;
   const int s0 = threadIdx.x * kPerT;
   const bool ranged = t_lo > 0 || t_hi < c_tptr[rowC_off[nbg]];
-  const bool masked = *masked_flag != 0;
+  const bool masked = (*masked_flag & 1) != 0;
+  const bool upper = (*masked_flag & 2) != 0;  // only C blocks of leaves (li, lj) with li <= lj
   for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
     if (ranged) {
       // A multi-GPU rank emits one triple range: skip rows none of whose C blocks reach it
@@ -354,6 +359,7 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
       if (hi <= t_lo || lo >= t_hi) continue;
     }
     RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
+    if (upper) s.jmin = max(s.jmin, (uint32_t)((i / nbl) * nbl));
     if (s.nt > 0) {
       uint64_t out = rowC_off[i];
       const bool multi = (s.jmax - s.jmin) >= (uint32_t)kWinT;
@@ -367,7 +373,7 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
           uint32_t k = a_scol[x];
           const uint64_t am = masked ? smask[x] : ~0ull;
           uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
-          if (multi) b0 = lower_bound_col(b_scol, b0, b1, wbase);
+          if (multi || upper) b0 = lower_bound_col(b_scol, b0, b1, wbase);
           for (uint32_t y = b0 + lane; y < b1; y += 32) {
             uint32_t j = b_scol[y];
             if (j >= wend) break;
@@ -390,7 +396,7 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
             uint32_t k = a_scol[x];
             const uint64_t am = masked ? smask[x] : ~0ull;
             uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
-            if (multi) b0 = lower_bound_col(b_scol, b0, b1, wbase);
+            if (multi || upper) b0 = lower_bound_col(b_scol, b0, b1, wbase);
             for (uint32_t y = b0 + lane; y < b1; y += 32) {
               uint32_t j = b_scol[y];
               if (j >= wend) break;
@@ -404,7 +410,7 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
             const uint64_t am = masked ? smask[x] : ~0ull;
             const uint32_t below = (1u << (x - x0)) - 1u;
             uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
-            if (multi) b0 = lower_bound_col(b_scol, b0, b1, wbase);
+            if (multi || upper) b0 = lower_bound_col(b_scol, b0, b1, wbase);
             for (uint32_t y = b0 + lane; y < b1; y += 32) {
               uint32_t j = b_scol[y];
               if (j >= wend) break;
@@ -535,7 +541,7 @@ FillWs carve_fill(Carver &cv, int64_t nC, int key_bits) {
 // Block-row index of both operands: one stable radix sort by row key (quadtree keys are monotone
 // in the column for a fixed row, so every row comes out k-ascending), columns, row pointers.
 int build_rows(const uint64_t *a_keys, const uint64_t *a_cmask, int64_t nA, const uint64_t *b_keys,
-               const uint64_t *b_rmask, int64_t nB, const Geometry &g, const SymWs &w, cudaStream_t st) {
+               const uint64_t *b_rmask, int64_t nB, int upper, const Geometry &g, const SymWs &w, cudaStream_t st) {
   const int64_t n = nA + nB;
   if (n > 0) {
     k_decode_rows<<<grid_for(n), 256, 0, st>>>(a_keys, nA, b_keys, nB, g.nbg, g.nbl, g.lbits,
@@ -547,7 +553,8 @@ int build_rows(const uint64_t *a_keys, const uint64_t *a_cmask, int64_t nA, cons
     QM_CUDA_TRY(cudaGetLastError());
   }
   k_cols_rowptr<<<grid_for(std::max<int64_t>(n, 2 * g.nbg + 1)), 256, 0, st>>>(
-      a_keys, b_keys, w.srow, w.perm, n, g.nbg, g.nbl, g.lbits, a_cmask, b_rmask, w.scol, w.rp, w.smask, w.masked);
+      a_keys, b_keys, w.srow, w.perm, n, g.nbg, g.nbl, g.lbits, a_cmask, b_rmask, upper, w.scol, w.rp, w.smask,
+      w.masked);
   QM_LAUNCHED("k_cols_rowptr");
   return QM_OK;
 }
@@ -573,8 +580,8 @@ extern "C" size_t qm_spgemm_workspace_bytes(const qm_layout *layout, int64_t nA,
 
 extern "C" int qm_spgemm_count_masked(const qm_layout *layout, const uint64_t *a_keys, const uint64_t *a_cmask,
                                       int64_t nA, const uint64_t *b_keys, const uint64_t *b_rmask, int64_t nB,
-                                      void *ws, size_t ws_bytes, int64_t *n_c_out, int64_t *n_triples_out,
-                                      void *stream) {
+                                      int32_t flags, void *ws, size_t ws_bytes, int64_t *n_c_out,
+                                      int64_t *n_triples_out, void *stream) {
   Geometry g;
   int rc = make_geometry(layout, &g);
   if (rc != QM_OK) return rc;
@@ -591,15 +598,15 @@ extern "C" int qm_spgemm_count_masked(const qm_layout *layout, const uint64_t *a
   }
   *n_c_out = 0;
   *n_triples_out = 0;
-  rc = build_rows(a_keys, a_cmask, nA, b_keys, b_rmask, nB, g, w, st);
+  rc = build_rows(a_keys, a_cmask, nA, b_keys, b_rmask, nB, (flags & QM_SPGEMM_UPPER) ? 1 : 0, g, w, st);
   if (rc != QM_OK) return rc;
   const uint32_t *a_rp = w.rp, *b_rp = w.rp + g.nbg;
   if (nA + nB == 0) QM_CUDA_TRY(cudaMemsetAsync(w.done, 0, sizeof(unsigned int), st));  // no k_decode_rows
   int64_t *host_tot = nullptr, *dev_tot = nullptr;
   rc = mapped_i64(&host_tot, &dev_tot);
   if (rc != QM_OK) return rc;
-  k_sym_count<<<row_grid(g.nbg), kNT, 0, st>>>(a_rp, w.scol, b_rp, w.scol, w.smask, w.masked, g.nbg, w.cnt,
-                                               w.off, w.done, dev_tot);
+  k_sym_count<<<row_grid(g.nbg), kNT, 0, st>>>(a_rp, w.scol, b_rp, w.scol, w.smask, w.masked, g.nbg, g.nbl,
+                                               w.cnt, w.off, w.done, dev_tot);
   QM_LAUNCHED("k_sym_count");
   QM_CUDA_TRY(cudaStreamSynchronize(st));
   uint64_t tot[2] = {(uint64_t)((volatile int64_t *)host_tot)[0], (uint64_t)((volatile int64_t *)host_tot)[1]};
@@ -615,7 +622,7 @@ extern "C" int qm_spgemm_count_masked(const qm_layout *layout, const uint64_t *a
 extern "C" int qm_spgemm_count(const qm_layout *layout, const uint64_t *a_keys, int64_t nA,
                                const uint64_t *b_keys, int64_t nB, void *ws, size_t ws_bytes,
                                int64_t *n_c_out, int64_t *n_triples_out, void *stream) {
-  return qm_spgemm_count_masked(layout, a_keys, nullptr, nA, b_keys, nullptr, nB, ws, ws_bytes, n_c_out,
+  return qm_spgemm_count_masked(layout, a_keys, nullptr, nA, b_keys, nullptr, nB, 0, ws, ws_bytes, n_c_out,
                                 n_triples_out, stream);
 }
 
@@ -691,7 +698,7 @@ extern "C" int qm_spgemm_fill_triples(const qm_layout *layout, int64_t nA, int64
   if (nC == 0 || t_hi <= t_lo) return QM_OK;
   cudaStream_t st = (cudaStream_t)stream;
   k_sym_emit_tri<<<row_grid(g.nbg), kNT, 0, st>>>(w.rp, w.scol, w.perm, w.rp + g.nbg, w.scol,
-                                                  w.perm, w.smask, w.masked, g.nbg, w.off, f.inv, c_tptr, t_lo,
+                                                  w.perm, w.smask, w.masked, g.nbg, g.nbl, w.off, f.inv, c_tptr, t_lo,
                                                   t_hi, (uint2 *)tri);
   QM_LAUNCHED("k_sym_emit_tri");
   return QM_OK;

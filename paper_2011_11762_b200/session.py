@@ -267,14 +267,9 @@ class MatrixSession:
                     self.last_engine = _EngineInfo(pr.prune_log, pr.pairs_per_level)
                     ax, bx = a, b
                     plan_filter = lambda plan: approximate.filter_plan(geom, plan, ax, bx, pr)  # noqa: E731
-                if args.get("upper"):  # compute only the kept (upper-leaf) C blocks
-                    inner = plan_filter
-                    plan_filter = lambda plan: variants.upper_plan(  # noqa: E731
-                        geom, inner(plan) if inner is not None else plan)
-            c = spgemm.multiply_blocks(layout, a, b, stats=stats, plan_filter=plan_filter)
-            if args.get("upper"):
-                c = variants.upper_leaves(geom, c)
-                stats.n_c = c.n
+            # upper variants: the symbolic phase enumerates only the kept (upper-leaf) C blocks
+            c = spgemm.multiply_blocks(layout, a, b, stats=stats, plan_filter=plan_filter,
+                                       upper=bool(args.get("upper")))
         self.last_stats = [WorkerStats(0, tasks_executed=stats.n_triples)]
         return self.store.register(c)
 

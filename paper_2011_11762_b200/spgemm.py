@@ -68,7 +68,7 @@ class SymbolicState:
     """Workspaces of one symbolic phase (row indexes, fill scratch) kept between its steps."""
 
     def __init__(self, layout, a_keys: torch.Tensor, n_a: int, b_keys: torch.Tensor, n_b: int, stream=None,
-                 a_cmask: torch.Tensor | None = None, b_rmask: torch.Tensor | None = None):
+                 a_cmask: torch.Tensor | None = None, b_rmask: torch.Tensor | None = None, upper: bool = False):
         self.lib = _ffi.load()
         self.layout = layout
         self.lp = ctypes.byref(layout)
@@ -81,8 +81,8 @@ class SymbolicState:
         n_t = ctypes.c_int64(0)
         _ffi.check(  # support masks (None = full support): pairs whose product is exactly zero are skipped
             self.lib.qm_spgemm_count_masked(self.lp, _ffi.ptr(a_keys), _ffi.ptr(a_cmask), n_a, _ffi.ptr(b_keys),
-                                            _ffi.ptr(b_rmask), n_b, _ffi.ptr(self.ws), self.ws_bytes,
-                                            ctypes.byref(n_c), ctypes.byref(n_t), self.sh),
+                                            _ffi.ptr(b_rmask), n_b, 1 if upper else 0, _ffi.ptr(self.ws),
+                                            self.ws_bytes, ctypes.byref(n_c), ctypes.byref(n_t), self.sh),
             "qm_spgemm_count_masked",
         )
         self.n_c, self.n_t = int(n_c.value), int(n_t.value)
@@ -129,7 +129,7 @@ def _use_masks(a: BlockSet, b: BlockSet, stream=None) -> bool:
     return not (a.masks_full[1] or b.masks_full[0])
 
 
-def symbolic(layout, a: BlockSet, b: BlockSet, stream=None) -> SymbolicPlan:
+def symbolic(layout, a: BlockSet, b: BlockSet, stream=None, upper: bool = False) -> SymbolicPlan:
     """Triples of C = A*B. Block pairs whose support masks do not meet (A(i,k)'s nonzero columns vs
     B(k,j)'s nonzero rows) multiply to an exactly-zero block and yield no triple; a C block left
     without triples is an exact-zero block the reference computes and then drops (_set_block,
@@ -137,7 +137,7 @@ def symbolic(layout, a: BlockSet, b: BlockSet, stream=None) -> SymbolicPlan:
     a_cm = b_rm = None
     if _use_masks(a, b, stream):
         a_cm, b_rm = a.masks[1], b.masks[0]
-    st = SymbolicState(layout, a.keys, a.n, b.keys, b.n, stream, a_cm, b_rm)
+    st = SymbolicState(layout, a.keys, a.n, b.keys, b.n, stream, a_cm, b_rm, upper)
     c_keys = _alloc(st.n_c, torch.int64, st.dev)
     c_tptr = _alloc(st.n_c + 1, torch.int64, st.dev)
     tri = _alloc(2 * st.n_t, torch.int32, st.dev)
@@ -202,7 +202,7 @@ def compact(bs: int, c: BlockSet, nz: torch.Tensor, n_zero: int, stream=None) ->
 
 def multiply_blocks(layout, a: BlockSet, b: BlockSet, stream=None,
                     stats: MultiplyStats | None = None, events: dict | None = None,
-                    plan_filter=None) -> BlockSet:
+                    plan_filter=None, upper: bool = False) -> BlockSet:
     """Full regular product of two conformant block sets on their CUDA device.
 
     ``events`` (optional): CUDA events recorded on the stream around the phases, keys
@@ -222,7 +222,7 @@ def multiply_blocks(layout, a: BlockSet, b: BlockSet, stream=None,
         return BlockSet.empty(bs, a.device)
     if events is not None:
         events["symbolic"].record(stream)
-    plan = symbolic(layout, a, b, stream)
+    plan = symbolic(layout, a, b, stream, upper)  # upper: only C blocks of leaves li <= lj
     if plan_filter is not None:  # e.g. the approximate variant's pruned triples (approximate.py)
         plan = plan_filter(plan)
     if stats is not None:

@@ -15,6 +15,8 @@ then the regular product runs unchanged:
   regular/symmetric  C = expand(A) * expand(B)                      (a_sym / b_sym flags)
   symmetric_square   C = upper(expand(A) * expand(A))               result symmetric
   rank_k             C = upper(A * transpose(A))                    result symmetric
+where upper(.) is not a filter on the result: the symbolic phase enumerates only the C blocks of
+upper leaves (qm_spgemm_count_masked with QM_SPGEMM_UPPER), so the dropped half is never computed.
 """
 
 from __future__ import annotations
@@ -107,15 +109,23 @@ def expand_symmetric(geom: Geometry, s: BlockSet) -> BlockSet:
     idx = torch.nonzero(off).flatten()
     if idx.numel() == 0:
         return s
-    tb = _transposed_blocks(_gather(s.blocks, idx))
     tk = _encode(geom, bj[idx], bi[idx])
-    m = full = None
-    if s.masks is not None:
+    keys = torch.cat([s.keys, tk])
+    order = torch.argsort(keys, stable=True)
+    src = torch.cat([torch.arange(s.n, dtype=torch.int64, device=keys.device), idx])[order].contiguous()
+    tflag = (order >= s.n).to(torch.uint8)  # the appended entries are the transposed copies
+    n = int(order.shape[0])
+    blocks = torch.empty((n, s.bs, s.bs), dtype=torch.float64, device=keys.device)
+    _ffi.check(_ffi.load().qm_gather_blocks_t(s.bs, _ffi.ptr(s.blocks), _ffi.ptr(src), _ffi.ptr(tflag), n,
+                                              _ffi.ptr(blocks),
+                                              _ffi.stream_handle(torch.cuda.current_stream(keys.device))),
+               "qm_gather_blocks_t")
+    out = BlockSet(keys[order].contiguous(), blocks, s.sumsq[src].contiguous())
+    if s.masks is not None:  # copies swap row / column supports
         m = torch.cat([s.masks, s.masks[[1, 0]][:, idx]], dim=1)
         both = s.masks_full[0] and s.masks_full[1]
-        full = (both, both)
-    return _sorted(torch.cat([s.keys, tk]), torch.cat([s.blocks, tb]), torch.cat([s.sumsq, s.sumsq[idx]]), m,
-                   full if full is not None else (False, False))
+        out.masks, out.masks_full = m[:, order].contiguous(), (both, both)
+    return out
 
 
 def upper_leaves(geom: Geometry, c: BlockSet) -> BlockSet:
@@ -130,27 +140,4 @@ def upper_leaves(geom: Geometry, c: BlockSet) -> BlockSet:
     if c.masks is not None:
         out.masks, out.masks_full = c.masks[:, keep].contiguous(), c.masks_full
     return out
-
-
-def upper_plan(geom: Geometry, plan):
-    """Restricts a symbolic plan to the C blocks of leaves (li, lj) with li <= lj before the numeric
-    phase, so the `upper` variants (symmetric_square, rank_k) compute only the blocks they keep --
-    the reference's diagonal-path tasks never spawn their SW products (ops.py:214-216). Triples keep
-    their order (k ascending per C block)."""
-    from .spgemm import SymbolicPlan  # noqa: PLC0415
-
-    if plan.n_c == 0:
-        return plan
-    bi, bj = _decode(geom, plan.c_keys)
-    keep = torch.nonzero((bi // geom.nbl) <= (bj // geom.nbl)).flatten()
-    if keep.numel() == plan.n_c:
-        return plan
-    cnt = (plan.c_tptr[1:] - plan.c_tptr[:-1])[keep]
-    tptr = torch.zeros(keep.numel() + 1, dtype=torch.int64, device=cnt.device)
-    torch.cumsum(cnt, 0, out=tptr[1:])
-    nt = int(tptr[-1])
-    src = torch.repeat_interleave(plan.c_tptr[:-1][keep] - tptr[:-1], cnt, output_size=nt)
-    src += torch.arange(nt, dtype=torch.int64, device=cnt.device)
-    tri = plan.tri.view(-1, 2)[src].reshape(-1).contiguous()
-    return SymbolicPlan(int(keep.numel()), nt, plan.c_keys[keep].contiguous(), tptr, tri)
 
