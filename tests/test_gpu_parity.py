@@ -749,6 +749,9 @@ def test_support_filter_skips_exact_zero_products(ses, monkeypatch, n, bw, leaf,
         live = sum(((ov >> np.uint64(p * w)) & np.uint64((1 << w) - 1)) != 0 for p in range(npan))
         want_rows = kp * int(np.maximum(live, 1).sum()) if npan > 1 else bs * int(meet.sum())
         assert st.extra["k_rows"] == want_rows and st.flops == 2 * bs * bs * want_rows
+    c2 = ses.multiply(c, c)  # chained product: C's masks computed on first use
+    assert c.root.blockset.masks is not None
+    assert helpers.rel(ses.to_dense(c2), ses.to_dense(c) @ ses.to_dense(c)) <= TOL
     monkeypatch.setenv("QM_SUPPORT_FILTER", "0")
     c0 = ses.multiply(a, b)
     assert ses.last_multiply.n_triples == ta.size and ses.last_multiply.zero_blocks > 0
