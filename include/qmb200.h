@@ -161,16 +161,23 @@ QM_API int qm_numeric(const qm_layout *layout, const uint64_t *a_keys, const dou
                const double *b_blocks, int64_t nB, const uint32_t *tri, const int64_t *c_tptr,
                const uint64_t *c_keys, int64_t nC, int64_t nT, double *c_blocks, double *c_sumsq,
                uint8_t *c_nonzero, int64_t *zero_count, void *ws, size_t ws_bytes, void *stream);
-/* qm_numeric with the operands' support masks (qm_block_masks; NULL = full support): for bs 32-128
- * the TMA kernel skips the k panels (16 deep for bs 32/64, 32 for bs 128) of a triple where A's nonzero
- * columns and B's nonzero rows do not meet (they add exactly zero). *panel_count (device int64, may
- * be NULL) receives the k depth executed by the bs 32/64/128 kernel, summed over triples (bs per
- * triple without skipping; -1 for other kernels): the executed flops are 2*bs*bs*count. */
+/* qm_numeric with the operands' support masks and virtual transposes. a_masks / b_masks: device
+ * uint64[2*n] (row masks, then column masks; qm_block_masks) or NULL = full support: for bs 32-128
+ * the TMA kernel skips the k panels (16 deep for bs 32/64, 32 for bs 128) of a triple where A's
+ * nonzero columns and B's nonzero rows do not meet (they add exactly zero). flags &
+ * QM_NUMERIC_TRANSPOSED_REFS: a triple index with bit 31 set names a stored block used transposed
+ * -- the reference's virtual transposes (`_virtual_child` / ta / tb, ops.py:100-116) as a TMA box
+ * and shared-memory addressing choice, no materialised transpose (bs 32/64/128 only).
+ * *panel_count (device int64, may be NULL) receives the k depth executed by the bs 32/64/128
+ * kernel, summed over triples (bs per triple without skipping; -1 for other kernels): the executed
+ * flops are 2*bs*bs*count. */
+#define QM_NUMERIC_TRANSPOSED_REFS 1
 QM_API int qm_numeric_masked(const qm_layout *layout, const uint64_t *a_keys, const double *a_blocks,
-                             const uint64_t *a_cmask, int64_t nA, const double *b_blocks, const uint64_t *b_rmask,
-                             int64_t nB, const uint32_t *tri, const int64_t *c_tptr, const uint64_t *c_keys,
-                             int64_t nC, int64_t nT, double *c_blocks, double *c_sumsq, uint8_t *c_nonzero,
-                             int64_t *zero_count, int64_t *panel_count, void *ws, size_t ws_bytes, void *stream);
+                             const uint64_t *a_masks, int64_t nA, const double *b_blocks, const uint64_t *b_masks,
+                             int64_t nB, int32_t flags, const uint32_t *tri, const int64_t *c_tptr,
+                             const uint64_t *c_keys, int64_t nC, int64_t nT, double *c_blocks, double *c_sumsq,
+                             uint8_t *c_nonzero, int64_t *zero_count, int64_t *panel_count, void *ws,
+                             size_t ws_bytes, void *stream);
 /* The numeric phase of a multi-GPU product fused with its halo exchange: operand blocks live in
  * up to 8 pools per operand -- this rank's and the other ranks' block pools mapped into this GPU's
  * address space (CUDA IPC / peer access over NVLink). a_pools / b_pools / a_counts / b_counts are

@@ -113,8 +113,8 @@ _SIGS = {
                                               _P, _P]),
     "qm_numeric": (ctypes.c_int, [_LP, _P, _P, _I64, _P, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _SZ,
                                   _P]),
-    "qm_numeric_masked": (ctypes.c_int, [_LP, _P, _P, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P,
-                                         _P, _P, _P, _SZ, _P]),
+    "qm_numeric_masked": (ctypes.c_int, [_LP, _P, _P, _P, _I64, _P, _P, _I64, _I32, _P, _P, _P, _I64, _I64, _P, _P,
+                                         _P, _P, _P, _P, _SZ, _P]),
     "qm_numeric_workspace_bytes": (_SZ, [_I32, _I64, _I64]),
     "qm_ipc_export": (ctypes.c_int, [_P, _P, ctypes.POINTER(_I64)]),
     "qm_ipc_open": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),

@@ -107,13 +107,14 @@ struct Geometry {
 
 // Optional inputs of the numeric kernel beyond the triples: the A keys and layout (for claim
 // orders other than quadtree-key order; a_keys = NULL keeps key order), the operands' support masks
-// (A's nonzero columns, B's nonzero rows: k panels where they do not meet are skipped; NULL = all
-// panels), and where to count the k panels executed (device int64, NULL = not counted).
+// (k panels where A's nonzero columns and B's nonzero rows do not meet are skipped; NULL = all
+// panels), whether triple indices carry transpose flags, and where to count the k depth executed.
 struct NumericAux {
   const uint64_t *a_keys = nullptr;
   int32_t nbl = 1, lbits = 0;
   int64_t nbg = 1;
-  const uint64_t *a_cmask = nullptr, *b_rmask = nullptr;
+  const uint64_t *a_masks = nullptr, *b_masks = nullptr;  // [2, n]: row masks, then column masks
+  bool transpose_bits = false;  // triple indices carry a transpose flag in bit 31 (virtual transposes)
   int64_t *panel_count = nullptr;
 };
 

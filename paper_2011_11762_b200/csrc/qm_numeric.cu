@@ -367,8 +367,9 @@ extern "C" size_t qm_numeric_workspace_bytes(int32_t block_size, int64_t nC, int
 }
 
 extern "C" int qm_numeric_masked(const qm_layout *layout, const uint64_t *a_keys, const double *a_blocks,
-                                 const uint64_t *a_cmask, int64_t nA, const double *b_blocks,
-                                 const uint64_t *b_rmask, int64_t nB, const uint32_t *tri, const int64_t *c_tptr,
+                                 const uint64_t *a_masks, int64_t nA, const double *b_blocks,
+                                 const uint64_t *b_masks, int64_t nB, int32_t flags, const uint32_t *tri,
+                                 const int64_t *c_tptr,
                                  const uint64_t *c_keys, int64_t nC, int64_t nT, double *c_blocks, double *c_sumsq,
                                  uint8_t *c_nonzero, int64_t *zero_count, int64_t *panel_count, void *ws,
                                  size_t ws_bytes, void *stream) {
@@ -384,6 +385,11 @@ extern "C" int qm_numeric_masked(const qm_layout *layout, const uint64_t *a_keys
   if (panel_count) QM_CUDA_TRY(cudaMemsetAsync(panel_count, nC == 0 ? 0 : 0xff, sizeof(int64_t), st));  // -1: not counted
   if (nC == 0) return QM_OK;
   const uint2 *t2 = (const uint2 *)tri;
+  const bool tbits = (flags & QM_NUMERIC_TRANSPOSED_REFS) != 0;
+  if (tbits && !(numeric_impl() == 2 && (g.bs == 32 || g.bs == 64 || g.bs == 128))) {
+    set_error("qm_numeric: transposed block references need the bs 32/64/128 TMA kernel");
+    return QM_ERR_UNSUPPORTED;
+  }
   if (numeric_impl() == 2 && g.bs == 16) {
     rc = launch_numeric_group16(g, a_blocks, nA, b_blocks, nB, a_keys, tri, c_tptr, c_keys, nC, nT, c_blocks,
                                 c_sumsq, c_nonzero, zero_count, ws, ws_bytes, st);
@@ -395,8 +401,9 @@ extern "C" int qm_numeric_masked(const qm_layout *layout, const uint64_t *a_keys
     oi.nbl = g.nbl;
     oi.lbits = g.lbits;
     oi.nbg = g.nbg;
-    oi.a_cmask = a_cmask;
-    oi.b_rmask = b_rmask;
+    oi.a_masks = a_masks;
+    oi.b_masks = b_masks;
+    oi.transpose_bits = tbits;
     oi.panel_count = panel_count;
     rc = launch_numeric_tma(g.bs, &a_blocks, &nA, 1, &b_blocks, &nB, 1, tri, c_tptr, nC, nT, oi, c_blocks,
                             c_sumsq, c_nonzero, zero_count, ws, ws_bytes, st);
@@ -422,7 +429,7 @@ extern "C" int qm_numeric(const qm_layout *layout, const uint64_t *a_keys, const
                           const int64_t *c_tptr, const uint64_t *c_keys, int64_t nC, int64_t nT, double *c_blocks,
                           double *c_sumsq, uint8_t *c_nonzero, int64_t *zero_count, void *ws,
                           size_t ws_bytes, void *stream) {
-  return qm_numeric_masked(layout, a_keys, a_blocks, nullptr, nA, b_blocks, nullptr, nB, tri, c_tptr, c_keys, nC,
+  return qm_numeric_masked(layout, a_keys, a_blocks, nullptr, nA, b_blocks, nullptr, nB, 0, tri, c_tptr, c_keys, nC,
                            nT, c_blocks, c_sumsq, c_nonzero, zero_count, nullptr, ws, ws_bytes, stream);
 }
 

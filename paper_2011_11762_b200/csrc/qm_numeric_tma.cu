@@ -67,11 +67,21 @@ constexpr int kOwnerShift = 28;
 constexpr uint32_t kLocalMask = (1u << kOwnerShift) - 1u;
 constexpr int kMaxPools = 8;
 
-template <int NPOOL>
+template <int NPOOL, bool TR = false>
 struct __align__(64) TmaMaps {
   CUtensorMap a[NPOOL];
   CUtensorMap b[NPOOL];
 };
+// TR: triple indices may carry a transpose flag (bit 31): the stored block is used transposed, the
+// reference's virtual transposes (ops.py:100-116) as TMA box / shared-memory addressing choices.
+// `at` views the A pool with the B box (KP rows x 16 columns), `bt` the B pool with the A box.
+template <int NPOOL>
+struct __align__(64) TmaMaps<NPOOL, true> {
+  CUtensorMap a[NPOOL];
+  CUtensorMap b[NPOOL];
+  CUtensorMap at, bt;
+};
+constexpr uint32_t kTransposed = 1u << 31;
 
 // Stage cursor over work units u = m * NQ + q (C block m, tile q), triple t, k panel p.
 // `unit` is the claim index; `mu` the work unit it maps to (C block order[unit / NQ], tile unit % NQ;
@@ -129,9 +139,9 @@ __device__ __forceinline__ void cur_next(Cur &c, int64_t nU, const int64_t *tptr
   }
 }
 
-template <class Cfg, int NPOOL>
+template <class Cfg, int NPOOL, bool TR>
 __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
-    k_numeric_tma(const __grid_constant__ TmaMaps<NPOOL> maps,
+    k_numeric_tma(const __grid_constant__ TmaMaps<NPOOL, TR> maps,
                   const uint2 *__restrict__ tri, const int64_t *__restrict__ tptr, int64_t nC,
                   double *__restrict__ C, double *__restrict__ csq, uint8_t *__restrict__ cnz,
                   int64_t *__restrict__ zero_count, double *__restrict__ part_sq,
@@ -181,21 +191,50 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
           break;
         }
         const uint2 ab = tri[L.t];
-        const uint32_t ao = NPOOL > 1 ? ab.x >> kOwnerShift : 0u, al = NPOOL > 1 ? ab.x & kLocalMask : ab.x;
-        const uint32_t bo = NPOOL > 1 ? ab.y >> kOwnerShift : 0u, bl = NPOOL > 1 ? ab.y & kLocalMask : ab.y;
+        const uint32_t ao = NPOOL > 1 ? ab.x >> kOwnerShift : 0u;
+        const uint32_t bo = NPOOL > 1 ? ab.y >> kOwnerShift : 0u;
+        uint32_t al = NPOOL > 1 ? ab.x & kLocalMask : ab.x, bl = NPOOL > 1 ? ab.y & kLocalMask : ab.y;
+        uint32_t ta = 0, tb = 0;
+        if constexpr (TR) {
+          ta = al >> 31;
+          tb = bl >> 31;
+          al &= ~kTransposed;
+          bl &= ~kTransposed;
+        }
         const int qt = (int)(L.mu % Cfg::NQ);
         const int row0 = (qt / Cfg::NQN) * Cfg::TILE, col0 = (qt % Cfg::NQN) * Cfg::TILE;
         uint8_t *st = smem + (size_t)s * Cfg::STAGE_BYTES;
-        meta[s] = L.mu * 2 + (cur_last(L) ? 1 : 0);
+        if constexpr (TR)
+          meta[s] = ((L.mu * 2 + (cur_last(L) ? 1 : 0)) << 2) | (ta << 1) | tb;
+        else
+          meta[s] = L.mu * 2 + (cur_last(L) ? 1 : 0);
         mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
+        if (TR && ta) {  // A(i,k) = S^T: S's rows k of the panel, columns = the tile's rows (B box)
+          if constexpr (TR) {
 #pragma unroll
-        for (int q = 0; q < Cfg::KSP; ++q)
-          tma_load_2d(st + q * Cfg::A_SP_BYTES, &maps.a[ao], L.p * Cfg::KP + q * 16, (int)(al * BS + row0),
-                      &full[s]);
+            for (int q = 0; q < Cfg::TILE / 16; ++q)
+              tma_load_2d(st + q * Cfg::B_SP_BYTES, &maps.at, row0 + q * 16, (int)(al * BS + L.p * Cfg::KP),
+                          &full[s]);
+          }
+        } else {
 #pragma unroll
-        for (int q = 0; q < Cfg::NSP; ++q)
-          tma_load_2d(st + Cfg::A_BYTES + q * Cfg::B_SP_BYTES, &maps.b[bo], col0 + q * 16,
-                      (int)(bl * BS + L.p * Cfg::KP), &full[s]);
+          for (int q = 0; q < Cfg::KSP; ++q)
+            tma_load_2d(st + q * Cfg::A_SP_BYTES, &maps.a[ao], L.p * Cfg::KP + q * 16, (int)(al * BS + row0),
+                        &full[s]);
+        }
+        if (TR && tb) {  // B(k,j) = S^T: S's rows = the tile's columns, columns k of the panel (A box)
+          if constexpr (TR) {
+#pragma unroll
+            for (int q = 0; q < Cfg::KSP; ++q)
+              tma_load_2d(st + Cfg::A_BYTES + q * Cfg::A_SP_BYTES, &maps.bt, L.p * Cfg::KP + q * 16,
+                          (int)(bl * BS + col0), &full[s]);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < Cfg::NSP; ++q)
+            tma_load_2d(st + Cfg::A_BYTES + q * Cfg::B_SP_BYTES, &maps.b[bo], col0 + q * 16,
+                        (int)(bl * BS + L.p * Cfg::KP), &full[s]);
+        }
         cur_next<Cfg>(L, nU, tptr, order, tri_sm, counter);
         if (++s == STAGES) {
           s = 0;
@@ -234,8 +273,14 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
   uint32_t phase = 0;
   while (true) {
     mbar_wait(&full[s], phase);
-    const int64_t mt = meta[s];
+    int64_t mt = meta[s];
     if (mt < 0) break;
+    bool ta = false, tb = false;
+    if constexpr (TR) {
+      ta = (mt >> 1) & 1;
+      tb = mt & 1;
+      mt >>= 2;
+    }
     const uint8_t *sa = smem + (size_t)s * Cfg::STAGE_BYTES;
     const uint8_t *sb = sa + Cfg::A_BYTES;
     uint64_t dep = 0;
@@ -246,12 +291,25 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         double af[MT], bf[NT];
+        // A transposed (TR): the stage holds S^T's panel in the B layout, so A's fragment is read
+        // with B's addressing (same lane <-> (row, k) map: g indexes rows / columns, tq the k);
+        // B transposed: the A layout, read with A's addressing.
 #pragma unroll
-        for (int i = 0; i < MT; ++i) af[i] = *(const double *)(pa + i * 8 * 128 + aoff[j]);
+        for (int i = 0; i < MT; ++i) {
+          if (TR && ta) {
+            const int row = wm0 + i * 8;
+            af[i] = *(const double *)(sa + (row >> 4) * Cfg::B_SP_BYTES + kb * 16 * 128 + boff[j][(row & 15) >> 3]);
+          } else {
+            af[i] = *(const double *)(pa + i * 8 * 128 + aoff[j]);
+          }
+        }
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
           const int col = wn0 + n * 8;
-          bf[n] = *(const double *)(pb + (col >> 4) * Cfg::B_SP_BYTES + boff[j][(col & 15) >> 3]);
+          if (TR && tb)
+            bf[n] = *(const double *)(sb + kb * Cfg::A_SP_BYTES + col * 128 + aoff[j]);
+          else
+            bf[n] = *(const double *)(pb + (col >> 4) * Cfg::B_SP_BYTES + boff[j][(col & 15) >> 3]);
         }
         if (kb == Cfg::KSP - 1 && j == 3) {
           // The stage's last fragment loads: the release below depends on their values.
@@ -351,14 +409,18 @@ __global__ void k_order_key(const uint2 *tri, const int64_t *tptr, const uint64_
 // adds exactly zero. Disjoint supports overall (not filtered by the symbolic phase) keep one panel.
 // Also counts the k rows to execute (KP per panel; warp partials, one atomic per warp).
 template <class Cfg>
-__global__ void k_triple_panels(const uint2 *tri, int64_t nT, const uint64_t *a_cmask, const uint64_t *b_rmask,
-                                uint8_t *sm, unsigned long long *panels) {
+__global__ void k_triple_panels(const uint2 *tri, int64_t nT, const uint64_t *a_masks, int64_t nA,
+                                const uint64_t *b_masks, int64_t nB, uint8_t *sm, unsigned long long *panels) {
   constexpr int W = 64 * Cfg::KP / (Cfg::BS > 64 ? Cfg::BS : 64);
   constexpr uint64_t kW = W >= 64 ? ~0ull : ((1ull << W) - 1ull);
   uint32_t cnt = 0;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nT; t += (int64_t)gridDim.x * blockDim.x) {
     const uint2 ab = tri[t];
-    const uint64_t ov = a_cmask[ab.x] & b_rmask[ab.y];
+    // A's columns are the stored block's rows when it is used transposed (bit 31), B's rows its columns
+    const uint32_t a = ab.x & ~kTransposed, b = ab.y & ~kTransposed;
+    const uint64_t ac = (ab.x & kTransposed) ? a_masks[a] : a_masks[nA + a];
+    const uint64_t br = (ab.y & kTransposed) ? b_masks[nB + b] : b_masks[b];
+    const uint64_t ov = ac & br;
     uint32_t m = 0;
 #pragma unroll
     for (int p = 0; p < Cfg::NP; ++p)
@@ -435,7 +497,7 @@ int make_order(int kind, const uint2 *tri, const int64_t *tptr, const uint64_t *
   return QM_OK;
 }
 
-template <class Cfg, int NPOOL>
+template <class Cfg, int NPOOL, bool TR>
 int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const double *const *B,
                      const int64_t *nB, int nb, const uint2 *tri, const int64_t *tptr, int64_t nC, int64_t nT,
                      const NumericAux &oi, double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws,
@@ -462,7 +524,7 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
       set_error("qm_numeric: pool of %lld blocks exceeds TMA's int32 row coordinate", (long long)nB[i]);
       return QM_ERR_UNSUPPORTED;
     }
-  TmaMaps<NPOOL> maps;
+  TmaMaps<NPOOL, TR> maps;
   memset(&maps, 0, sizeof(maps));
   for (int i = 0; i < NPOOL; ++i) {  // unused slots repeat pool 0 (never indexed)
     int rc = make_map(&maps.a[i], A[i < na ? i : 0], nA[i < na ? i : 0], Cfg::BS, Cfg::TILE);
@@ -470,9 +532,15 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
     rc = make_map(&maps.b[i], B[i < nb ? i : 0], nB[i < nb ? i : 0], Cfg::BS, Cfg::KP);
     if (rc != QM_OK) return rc;
   }
+  if constexpr (TR) {
+    int rc = make_map(&maps.at, A[0], nA[0], Cfg::BS, Cfg::KP);
+    if (rc != QM_OK) return rc;
+    rc = make_map(&maps.bt, B[0], nB[0], Cfg::BS, Cfg::TILE);
+    if (rc != QM_OK) return rc;
+  }
   static PerDeviceOnce once;
   int rc = once.run([]() -> int {
-    QM_CUDA_TRY(cudaFuncSetAttribute(k_numeric_tma<Cfg, NPOOL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    QM_CUDA_TRY(cudaFuncSetAttribute(k_numeric_tma<Cfg, NPOOL, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)Cfg::SMEM));
     return (int)QM_OK;
   });
@@ -480,7 +548,8 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
   int per_sm = 0;
   static PerDeviceInt occupancy;  // cudaOccupancy* costs microseconds of host time per call
   rc = occupancy.get(&per_sm, [](int *x) -> int {
-    QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(x, k_numeric_tma<Cfg, NPOOL>, Cfg::NTHR, Cfg::SMEM));
+    QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(x, k_numeric_tma<Cfg, NPOOL, TR>, Cfg::NTHR,
+                                                              Cfg::SMEM));
     return (int)QM_OK;
   });
   if (rc != QM_OK) return rc;
@@ -498,16 +567,16 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
   }
   uint8_t *tri_sm = nullptr;
   int64_t panel_fill = (int64_t)Cfg::BS * nT;  // every k row of every triple
-  if (oi.a_cmask && oi.b_rmask && na == 1 && nb == 1 && Cfg::NP > 1 && nT > 0) {
+  if (oi.a_masks && oi.b_masks && na == 1 && nb == 1 && Cfg::NP > 1 && nT > 0) {
     tri_sm = (uint8_t *)ws + tma_ws_panels_offset<Cfg>(nC);
     if (oi.panel_count) QM_CUDA_TRY(cudaMemsetAsync(oi.panel_count, 0, sizeof(int64_t), st));
     const int g = (int)std::min<int64_t>((nT + 255) / 256, (int64_t)sm_count_tma() * 16);
-    k_triple_panels<Cfg><<<g, 256, 0, st>>>(tri, nT, oi.a_cmask, oi.b_rmask, tri_sm,
+    k_triple_panels<Cfg><<<g, 256, 0, st>>>(tri, nT, oi.a_masks, nA[0], oi.b_masks, nB[0], tri_sm,
                                             (unsigned long long *)oi.panel_count);
     QM_LAUNCHED("k_triple_panels");
     panel_fill = -1;  // counted by k_triple_panels
   }
-  k_numeric_tma<Cfg, NPOOL><<<(int)grid, Cfg::NTHR, Cfg::SMEM, st>>>(
+  k_numeric_tma<Cfg, NPOOL, TR><<<(int)grid, Cfg::NTHR, Cfg::SMEM, st>>>(
       maps, tri, tptr, nC, C, csq, cnz, zc, part_sq, part_nz, counter, order, tri_sm, /*zmask=*/0ull);
   QM_LAUNCHED("k_numeric_tma");
   {
@@ -524,11 +593,19 @@ int launch_tma(const double *const *A, const int64_t *nA, int na, const double *
                const int64_t *nB, int nb, const uint2 *tri, const int64_t *tptr, int64_t nC, int64_t nT,
                const NumericAux &oi, double *C, double *csq, uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes,
                cudaStream_t st) {
-  if (na == 1 && nb == 1)
-    return launch_tma_pools<Cfg, 1>(A, nA, na, B, nB, nb, tri, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes,
-                                    st);
-  return launch_tma_pools<Cfg, kMaxPools>(A, nA, na, B, nB, nb, tri, tptr, nC, nT, oi, C, csq, cnz, zc, ws,
-                                          ws_bytes, st);
+  if (na == 1 && nb == 1) {
+    if (oi.transpose_bits)
+      return launch_tma_pools<Cfg, 1, true>(A, nA, na, B, nB, nb, tri, tptr, nC, nT, oi, C, csq, cnz, zc, ws,
+                                            ws_bytes, st);
+    return launch_tma_pools<Cfg, 1, false>(A, nA, na, B, nB, nb, tri, tptr, nC, nT, oi, C, csq, cnz, zc, ws,
+                                           ws_bytes, st);
+  }
+  if (oi.transpose_bits) {
+    set_error("qm_numeric: transposed block references need a single pool per operand");
+    return QM_ERR_INVALID;
+  }
+  return launch_tma_pools<Cfg, kMaxPools, false>(A, nA, na, B, nB, nb, tri, tptr, nC, nT, oi, C, csq, cnz, zc,
+                                                 ws, ws_bytes, st);
 }
 
 //                     BS TILE WM WN KP STAGES MINB
@@ -560,7 +637,7 @@ using Tma64k16 = TmaCfg<64, 64, 2, 2, 16, 4, 3>;
 using Tma32k16 = TmaCfg<32, 32, 2, 2, 16, 4, 6>;  // same for bs 32: 4 stages of 8 KB, 6 CTAs/SM
 bool use_k16(const NumericAux &oi) {
   const char *e = getenv("QM_PANEL16");
-  return oi.a_cmask && oi.b_rmask && !(e && strcmp(e, "0") == 0);
+  return oi.a_masks && oi.b_masks && !(e && strcmp(e, "0") == 0);
 }
 
 using Tma128 = TmaCfg<128, 64, 2, 2, 32, 3, 2>;

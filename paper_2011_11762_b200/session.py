@@ -252,12 +252,14 @@ class MatrixSession:
                 if spgemm.support_filter_enabled():  # on the stored sets (kept), carried through
                     a.support_masks()                # the transposes / expansions below
                     b.support_masks()
+                virt = variants.virtual_ok(geom.bs)  # transposes as TMA / fragment addressing
+                expand = variants.expand_symmetric_view if virt else variants.expand_symmetric
                 if args.get("a_sym"):
-                    a = variants.expand_symmetric(geom, a)
+                    a = expand(geom, a)
                 if args.get("b_sym"):
-                    b = a if (same and args.get("a_sym")) else variants.expand_symmetric(geom, b)
+                    b = a if (same and args.get("a_sym")) else expand(geom, b)
                 if args.get("tb"):
-                    b = variants.transpose(geom, b)
+                    b = (variants.transpose_view if virt else variants.transpose)(geom, b)
                 if tau > 0.0:  # approximate: prune decisions on stored-chunk norms (approximate.py)
                     from . import approximate  # noqa: PLC0415
 

@@ -164,12 +164,20 @@ def numeric(layout, a: BlockSet, b: BlockSet, plan: SymbolicPlan, stream=None,
     zc = _alloc(2, torch.int64, dev)  # [exact-zero C blocks, k panels executed]: set by the library
     wb = lib.qm_numeric_workspace_bytes(bs, nc, plan.n_triples)
     ws = _alloc(wb, torch.uint8, dev) if wb else None
-    a_cm = b_rm = None
-    if _use_masks(a, b, stream):
-        a_cm, b_rm = a.masks[1], b.masks[0]
+    use_masks = _use_masks(a, b, stream)
+    tri, flags = plan.tri, 0
+    pa, pb = getattr(a, "pool", None), getattr(b, "pool", None)
+    if pa is not None or pb is not None:  # virtual transposes: view indices -> stored block | bit 31
+        t2 = plan.tri.view(-1, 2)
+        tri = torch.stack([a.src[t2[:, 0].long()] if pa is not None else t2[:, 0],
+                           b.src[t2[:, 1].long()] if pb is not None else t2[:, 1]], dim=1).reshape(-1).contiguous()
+        flags = 1  # QM_NUMERIC_TRANSPOSED_REFS
+    sa, sb = pa if pa is not None else a, pb if pb is not None else b  # the stored pools
+    am = sa.support_masks(stream) if use_masks else None
+    bm = sb.support_masks(stream) if use_masks else None
     _ffi.check(
-        lib.qm_numeric_masked(ctypes.byref(layout), _ffi.ptr(a.keys), _ffi.ptr(a.blocks), _ffi.ptr(a_cm), a.n,
-                              _ffi.ptr(b.blocks), _ffi.ptr(b_rm), b.n, _ffi.ptr(plan.tri), _ffi.ptr(plan.c_tptr),
+        lib.qm_numeric_masked(ctypes.byref(layout), _ffi.ptr(a.keys), _ffi.ptr(sa.blocks), _ffi.ptr(am), sa.n,
+                              _ffi.ptr(sb.blocks), _ffi.ptr(bm), sb.n, flags, _ffi.ptr(tri), _ffi.ptr(plan.c_tptr),
                               _ffi.ptr(plan.c_keys), nc, plan.n_triples, _ffi.ptr(out.blocks),
                               _ffi.ptr(out.sumsq), _ffi.ptr(nz), _ffi.ptr(zc), _ffi.ptr(zc[1:]), _ffi.ptr(ws), wb,
                               _ffi.stream_handle(stream)),

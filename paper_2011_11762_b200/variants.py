@@ -88,6 +88,77 @@ def _sorted(keys: torch.Tensor, blocks: torch.Tensor, sumsq: torch.Tensor, masks
     return out
 
 
+class BlockView(BlockSet):
+    """A virtual block set over a stored pool: entry m is the pool's block src[m] & 0x7fffffff,
+    transposed when bit 31 of src[m] is set (src: int32). Keys, norms and support masks are the
+    view's own; `blocks` is the pool's tensor (never indexed by view position on the host). The
+    numeric kernel reads transposed entries through a transposed TMA box / fragment addressing
+    (qm_numeric_masked with QM_NUMERIC_TRANSPOSED_REFS) -- the reference's virtual transposes
+    (`_virtual_child`, ops.py:100-116), never materialised."""
+
+    def __init__(self, keys, pool: BlockSet, src: torch.Tensor, sumsq: torch.Tensor, tsel: torch.Tensor):
+        super().__init__(keys, pool.blocks, sumsq)
+        self.pool, self.src, self._tsel = pool, src, tsel  # tsel: bool[n], entry is transposed
+
+    def support_masks(self, stream=None) -> torch.Tensor:
+        if self.masks is None:
+            pm = self.pool.support_masks(stream)
+            idx = (self.src.long() & 0x7FFFFFFF)
+            rows, cols = pm[0][idx], pm[1][idx]
+            self.masks = torch.stack([torch.where(self._tsel, cols, rows), torch.where(self._tsel, rows, cols)])
+            fr, fc = self.pool.masks_full
+            both = fr and fc
+            self.masks_full = (both, both) if bool(self._tsel.any()) else (fr, fc)
+        return self.masks
+
+
+def _src32(idx: torch.Tensor, tsel: torch.Tensor) -> torch.Tensor:
+    """int32 view entries: stored index, bit 31 set for a transposed use (two's complement)."""
+    return torch.where(tsel, idx - (1 << 31), idx).to(torch.int32)
+
+
+def virtual_ok(bs: int) -> bool:
+    """Transposes stay virtual when the bs 32/64/128 TMA kernel runs the product
+    (QM_VIRTUAL_TRANSPOSE=0 materialises them, for A/B comparisons)."""
+    import os  # noqa: PLC0415
+
+    return bs in (32, 64, 128) and _ffi.load().qm_numeric_path(bs) == 2 and \
+        os.environ.get("QM_VIRTUAL_TRANSPOSE", "1") != "0"
+
+
+def transpose_view(geom: Geometry, x: BlockSet) -> BlockSet:
+    """X^T as a view of X's blocks (keys swapped and re-sorted, every entry's transpose flag
+    toggled; X may itself be a view)."""
+    if x.n == 0:
+        return x
+    bi, bj = _decode(geom, x.keys)
+    keys = _encode(geom, bj, bi)
+    order = torch.argsort(keys, stable=True)
+    if isinstance(x, BlockView):
+        pool, idx, tsel = x.pool, (x.src.long() & 0x7FFFFFFF)[order], ~x._tsel[order]
+    else:
+        pool, idx, tsel = x, order, torch.ones(x.n, dtype=torch.bool, device=keys.device)
+    return BlockView(keys[order].contiguous(), pool, _src32(idx, tsel), x.sumsq[order].contiguous(), tsel)
+
+
+def expand_symmetric_view(geom: Geometry, s: BlockSet) -> BlockSet:
+    """expand_symmetric as a view: the stored blocks plus transposed references for the blocks of
+    strictly-upper leaves, no block copied."""
+    if s.n == 0:
+        return s
+    bi, bj = _decode(geom, s.keys)
+    off = (bi // geom.nbl) < (bj // geom.nbl)
+    idx = torch.nonzero(off).flatten()
+    if idx.numel() == 0:
+        return s
+    tk = _encode(geom, bj[idx], bi[idx])
+    keys = torch.cat([s.keys, tk])
+    order = torch.argsort(keys, stable=True)
+    src = torch.cat([torch.arange(s.n, dtype=torch.int64, device=keys.device), idx])[order]
+    tsel = order >= s.n
+    return BlockView(keys[order].contiguous(), s, _src32(src, tsel), s.sumsq[src].contiguous(), tsel)
+
+
 def transpose(geom: Geometry, x: BlockSet) -> BlockSet:
     """X^T as a block set (the virtual transpose of op_view / tb=True, materialised)."""
     if x.n == 0:

@@ -771,3 +771,29 @@ def test_support_filter_keeps_nan_inf_products(ses):
         want = da[:bs, :bs] @ db[:bs, :bs]  # the only stored pair of blocks
     assert np.array_equal(c[:bs, :bs], want, equal_nan=True)
     assert np.isnan(c[0, 0]) and not c[bs:].any() and not c[:, bs:].any()
+
+
+@pytest.mark.parametrize("bs,leaf", [(64, 64), (32, 64), (128, 128), (64, 128)])
+def test_virtual_transposes_bitwise_equal_materialised(ses, monkeypatch, bs, leaf):
+    """symmetric_square / rank_k / symmetric products read stored blocks transposed inside the
+    numeric kernel (QM_NUMERIC_TRANSPOSED_REFS: transposed TMA box + fragment addressing) instead of
+    materialising the transposes: the result is bitwise the materialised path's
+    (QM_VIRTUAL_TRANSPOSE=0) -- the same products summed in the same order -- and matches dense."""
+    n = 6 * leaf
+    rng = np.random.default_rng(bs + leaf)
+    d = np.where(rng.random((n, n)) < 0.15, rng.standard_normal((n, n)), 0.0)
+    d = d + d.T
+    a = helpers.build(ses, d, leaf, bs)
+    up = ses.matrix_from_triplets(n, *helpers.triplets_of(np.triu(d)), leaf_dim=leaf,
+                                  block_size=bs, symmetric=True)
+    e = helpers.build(ses, rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.2), leaf, bs)
+    cases = [("rank_k", lambda: ses.multiply(e, None, "rank_k")),
+             ("symmetric_square", lambda: ses.multiply(up, None, "symmetric_square")),
+             ("symmetric", lambda: ses.multiply(up, a, "symmetric"))]
+    for name, run in cases:
+        monkeypatch.setenv("QM_VIRTUAL_TRANSPOSE", "1")
+        cv = run().root.blockset
+        monkeypatch.setenv("QM_VIRTUAL_TRANSPOSE", "0")
+        cm = run().root.blockset
+        assert torch.equal(cv.keys, cm.keys), name
+        assert torch.equal(cv.blocks, cm.blocks), name
