@@ -44,14 +44,19 @@ class BlockSet:
         if self.masks is None:
             from . import _ffi  # noqa: PLC0415
 
+            st = stream if stream is not None else torch.cuda.current_stream(self.device)
             m = torch.empty((2, self.n), dtype=torch.int64, device=self.device)
             if self.n:
                 _ffi.check(_ffi.load().qm_block_masks(self.bs, self.n, _ffi.ptr(self.blocks), _ffi.ptr(m[0]),
-                                                      _ffi.ptr(m[1]), _ffi.stream_handle(stream)),
+                                                      _ffi.ptr(m[1]), _ffi.stream_handle(st)),
                            "qm_block_masks")
                 full = -1 if self.bs >= 64 else (1 << self.bs) - 1
-                f = (m == full).all(dim=1).tolist()  # one synchronisation, once per block set
-                self.masks_full = (bool(f[0]), bool(f[1]))
+                with torch.cuda.stream(st):
+                    f = (m == full).all(dim=1).to(torch.int64)
+                # one read per block set, through mapped memory (a copy-engine read would queue
+                # behind bulk D2H copies in flight, e.g. a pipelined serving loop's result copies)
+                f0, f1 = _ffi.read_i64s(f, 2, st)
+                self.masks_full = (bool(f0), bool(f1))
             else:
                 self.masks_full = (True, True)
             self.masks = m
