@@ -99,6 +99,7 @@ class BlockView(BlockSet):
     def __init__(self, keys, pool: BlockSet, src: torch.Tensor, sumsq: torch.Tensor, tsel: torch.Tensor):
         super().__init__(keys, pool.blocks, sumsq)
         self.pool, self.src, self._tsel = pool, src, tsel  # tsel: bool[n], entry is transposed
+        self._any_t = True  # some entry is transposed (every view built here has one)
 
     def support_masks(self, stream=None) -> torch.Tensor:
         if self.masks is None:
@@ -108,7 +109,7 @@ class BlockView(BlockSet):
             self.masks = torch.stack([torch.where(self._tsel, cols, rows), torch.where(self._tsel, rows, cols)])
             fr, fc = self.pool.masks_full
             both = fr and fc
-            self.masks_full = (both, both) if bool(self._tsel.any()) else (fr, fc)
+            self.masks_full = (both, both) if self._any_t else (fr, fc)
         return self.masks
 
 
@@ -148,15 +149,19 @@ def expand_symmetric_view(geom: Geometry, s: BlockSet) -> BlockSet:
         return s
     bi, bj = _decode(geom, s.keys)
     off = (bi // geom.nbl) < (bj // geom.nbl)
-    idx = torch.nonzero(off).flatten()
-    if idx.numel() == 0:
+    # the count through mapped memory (torch.nonzero's own read-back would use a copy engine)
+    n_off = _ffi.read_i64s(off.sum().reshape(1).to(torch.int64), 1)[0]
+    if n_off == 0:
         return s
+    idx = torch.nonzero_static(off, size=n_off).flatten()
     tk = _encode(geom, bj[idx], bi[idx])
     keys = torch.cat([s.keys, tk])
     order = torch.argsort(keys, stable=True)
     src = torch.cat([torch.arange(s.n, dtype=torch.int64, device=keys.device), idx])[order]
     tsel = order >= s.n
-    return BlockView(keys[order].contiguous(), s, _src32(src, tsel), s.sumsq[src].contiguous(), tsel)
+    view = BlockView(keys[order].contiguous(), s, _src32(src, tsel), s.sumsq[src].contiguous(), tsel)
+    view._any_t = True
+    return view
 
 
 def transpose(geom: Geometry, x: BlockSet) -> BlockSet:
