@@ -10,7 +10,7 @@ exactly the blocks of leaves (li, lj) with li <= lj.
 On the GPU the same algebra is expressed on flat block sets:
   * transpose(X):        keys (bi,bj) -> (bj,bi) re-sorted, blocks transposed (qm_transpose_blocks);
   * expand_symmetric(S): S plus transposed copies of the blocks of strictly-upper leaves;
-  * upper_leaves(C):     keep blocks of leaves with li <= lj.
+  * upper(C):            only the blocks of leaves with li <= lj.
 then the regular product runs unchanged:
   regular/symmetric  C = expand(A) * expand(B)                      (a_sym / b_sym flags)
   symmetric_square   C = upper(expand(A) * expand(A))               result symmetric
@@ -201,19 +201,5 @@ def expand_symmetric(geom: Geometry, s: BlockSet) -> BlockSet:
         m = torch.cat([s.masks, s.masks[[1, 0]][:, idx]], dim=1)
         both = s.masks_full[0] and s.masks_full[1]
         out.masks, out.masks_full = m[:, order].contiguous(), (both, both)
-    return out
-
-
-def upper_leaves(geom: Geometry, c: BlockSet) -> BlockSet:
-    """Blocks of leaves (li, lj) with li <= lj (the `upper` result of ops.py:214-216)."""
-    if c.n == 0:
-        return c
-    bi, bj = _decode(geom, c.keys)
-    keep = torch.nonzero((bi // geom.nbl) <= (bj // geom.nbl)).flatten()
-    if keep.numel() == c.n:
-        return c
-    out = BlockSet(c.keys[keep].contiguous(), _gather(c.blocks, keep), c.sumsq[keep].contiguous())
-    if c.masks is not None:
-        out.masks, out.masks_full = c.masks[:, keep].contiguous(), c.masks_full
     return out
 
