@@ -126,6 +126,96 @@ __global__ void k_prune_expand(const uint64_t *parents, int64_t n_cand, int root
   }
 }
 
+// Classification of candidate x (shared by the two level kernels).
+__device__ __forceinline__ void prune_classify(const uint64_t *parents, int64_t x, int root, const Table &ta,
+                                               int a_sym, const Table &tb, int b_sym, int b_transposed, int upper,
+                                               double tau_l, uint64_t *code, double *bd, bool *live, bool *pr) {
+  uint32_t I = 0, K = 0, J = 0;
+  if (!root) {
+    const uint64_t p = parents[x >> 3];
+    const uint32_t d = (uint32_t)(x & 7);
+    I = 2 * (uint32_t)(p >> (2 * kPairBits)) + (d >> 2);
+    K = 2 * (uint32_t)((p >> kPairBits) & kPairMask) + ((d >> 1) & 1u);
+    J = 2 * (uint32_t)(p & kPairMask) + (d & 1u);
+  }
+  double na = 0.0, nb = 0.0;
+  bool lv = lookup(ta, I, K, a_sym, &na);
+  if (lv) lv = b_transposed ? lookup(tb, J, K, b_sym, &nb) : lookup(tb, K, J, b_sym, &nb);
+  if (upper && I > J) lv = false;
+  *bd = na * nb;
+  *pr = lv && *bd < tau_l;
+  *live = lv && !*pr;
+  *code = ((uint64_t)I << (2 * kPairBits)) | ((uint64_t)K << kPairBits) | J;
+}
+
+// Small levels in one CTA (one launch instead of expand + two stream compactions): each thread
+// classifies up to kSmallPer consecutive candidates (kept in registers), a block-wide exclusive scan
+// orders the survivors exactly as the stable compaction of the multi-kernel path does, and the two
+// counts go straight to the caller's mapped host buffer.
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallPer = 4;
+constexpr int64_t kSmallLevelMax = (int64_t)kSmallThreads * kSmallPer;
+__global__ void __launch_bounds__(kSmallThreads) k_prune_small(const uint64_t *parents, int64_t n_cand, int root,
+                                                             Table ta, int a_sym, Table tb, int b_sym,
+                                                             int b_transposed, int upper, double tau_l,
+                                                             uint64_t *alive_out, double *pruned_out,
+                                                             volatile int64_t *host_cnt) {
+  __shared__ uint32_t wsa[32], wsp[32];
+  const int t = threadIdx.x;
+  uint64_t code[kSmallPer];
+  double bd[kSmallPer];
+  uint32_t live = 0, pr = 0, na = 0, np = 0;
+#pragma unroll
+  for (int q = 0; q < kSmallPer; ++q) {
+    const int64_t x = (int64_t)t * kSmallPer + q;
+    if (x < n_cand) {
+      bool lv, p;
+      prune_classify(parents, x, root, ta, a_sym, tb, b_sym, b_transposed, upper, tau_l, &code[q], &bd[q], &lv, &p);
+      live |= (uint32_t)lv << q;
+      pr |= (uint32_t)p << q;
+    }
+  }
+  na = __popc(live);
+  np = __popc(pr);
+  const int lane = t & 31, warp = t >> 5;
+  uint32_t ia = na, ip = np;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t xa = __shfl_up_sync(0xffffffffu, ia, o), xp = __shfl_up_sync(0xffffffffu, ip, o);
+    if (lane >= o) {
+      ia += xa;
+      ip += xp;
+    }
+  }
+  if (lane == 31) {
+    wsa[warp] = ia;
+    wsp[warp] = ip;
+  }
+  __syncthreads();
+  uint32_t ba = 0, bp = 0, tot_a = 0, tot_p = 0;
+  for (int w = 0; w < kSmallThreads / 32; ++w) {
+    if (w < warp) {
+      ba += wsa[w];
+      bp += wsp[w];
+    }
+    tot_a += wsa[w];
+    tot_p += wsp[w];
+  }
+  uint32_t oa = ba + ia - na, op = bp + ip - np;
+#pragma unroll
+  for (int q = 0; q < kSmallPer; ++q) {
+    if (live & (1u << q)) alive_out[oa++] = code[q];
+    if (pr & (1u << q)) pruned_out[op++] = bd[q];
+  }
+  __syncthreads();
+  if (t == 0) {
+    __threadfence();
+    host_cnt[0] = tot_a;
+    host_cnt[1] = tot_p;
+    __threadfence_system();
+  }
+}
+
 size_t select_bytes(int64_t n) {
   size_t a = 0, b = 0;
   cub::DeviceSelect::Flagged(nullptr, a, (uint64_t *)nullptr, (uint8_t *)nullptr, (uint64_t *)nullptr,
@@ -239,6 +329,20 @@ extern "C" int qm_prune_level(const qm_layout *layout, int32_t level, double tau
   }
   const int root = level == 0;
   const int64_t n_cand = root ? 1 : n_parents * 8;
+  if (n_cand <= kSmallLevelMax) {  // one launch, counts through mapped memory
+    int64_t *host_cnt = nullptr, *dev_cnt = nullptr;
+    rc = mapped_i64(&host_cnt, &dev_cnt);
+    if (rc != QM_OK) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    Table ta{a_codes, a_norms, a_count}, tb{b_codes, b_norms, b_count};
+    k_prune_small<<<1, kSmallThreads, 0, st>>>(parents, n_cand, root, ta, a_sym, tb, b_sym, b_transposed, upper,
+                                                tau_l, alive_out, pruned_out, dev_cnt);
+    QM_LAUNCHED("k_prune_small");
+    QM_CUDA_TRY(cudaStreamSynchronize(st));
+    *n_alive = ((volatile int64_t *)host_cnt)[0];
+    *n_pruned = ((volatile int64_t *)host_cnt)[1];
+    return QM_OK;
+  }
   Carver cv(ws, ws_bytes);
   const int64_t cap = std::max<int64_t>(n_cand, 1);
   uint64_t *cand = cv.take<uint64_t>(cap);
