@@ -39,4 +39,7 @@ def test_gpu_arm_contract():
     assert set(line["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
     assert line["gpu_launches"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
+    p = line["e2e"]["pcie"]  # the box's pinned-copy floor next to the e2e number
+    assert p["bidir_gbs"] > 0 and 0 < p["frac_of_floor"] <= 1.2
+    assert line["config"]["triples"] == line["config"]["triples_structural"]  # dense blocks: nothing skipped
     assert line["cpu_baseline"]["value"] > 0 and line["cpu_baseline"]["kind"] == "port"
