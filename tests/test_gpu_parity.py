@@ -812,3 +812,38 @@ def test_masked_and_transposed_kernels_deterministic_under_repetition(ses, bs):
         first = run().root.blockset.blocks.clone()
         bad = sum(int(not torch.equal(run().root.blockset.blocks, first)) for _ in range(30))
         assert bad == 0
+
+
+def test_support_filter_multi_window_rows(ses):
+    """The support filter in the windowed accumulator: rows spanning more than one 4096-column window
+    (8192 block columns, bs 4), blocks with partial supports. Executed triples equal the oracle's
+    triples with meeting masks, the C block set equals the oracle's after its exact-zero drop."""
+    bs, nbg = 4, 8192
+    n = bs * nbg
+    rng = np.random.default_rng(11)
+    rows, cols, vals = [], [], []
+    for bi in range(0, nbg, 37):  # a few block rows reaching across the whole width
+        for bj in rng.choice(nbg, 24, replace=False):
+            r = bi * bs + rng.integers(0, bs, 2)
+            c = bj * bs + rng.integers(0, bs, 2)
+            rows += list(r)
+            cols += list(c)
+            vals += list(rng.uniform(0.5, 1.5, 2))
+    for bk in range(nbg):  # B-side rows: one partial block per block row
+        bj = rng.integers(0, nbg)
+        rows.append(bk * bs + int(rng.integers(0, bs)))
+        cols.append(int(bj) * bs + int(rng.integers(0, bs)))
+        vals.append(1.0)
+    rows, cols, vals = np.array(rows), np.array(cols), np.array(vals)
+    a = ses.matrix_from_triplets(n, rows, cols, vals, leaf_dim=bs, block_size=bs)
+    c = ses.multiply(a, a)
+    st = ses.last_multiply
+    host = MatrixSession(device="cpu")
+    ka, ba, _ = host.matrix_from_triplets(n, rows, cols, vals, leaf_dim=bs, block_size=bs).root.blockset.to_host()
+    g = O.Geom(n, bs, bs)
+    kc, bc, _ = O.multiply(g, ka, ba, ka, ba)
+    np.testing.assert_array_equal(c.root.blockset.keys.cpu().numpy(), kc)
+    assert helpers.rel(c.root.blockset.blocks.cpu().numpy(), bc) <= TOL
+    _, _, ta, tb, _ = O.symbolic(g, ka, ka)
+    rm, cm = helpers.support_masks_np(ba)
+    assert st.n_triples == int(((cm[ta] & rm[tb]) != 0).sum()) < ta.size
