@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define QM_ABI_VERSION 1
+#define QM_ABI_VERSION 2 /* 2: support masks are uint64[3*n] (rows, columns, flags) */
 
 enum qm_status {
   QM_OK = 0,
@@ -102,6 +102,13 @@ QM_API int qm_build_count(const qm_layout *layout, const int64_t *rows /*device*
 QM_API int qm_build_fill(const qm_layout *layout, const double *vals /*device*/, int64_t n, void *ws,
                          size_t ws_bytes, int64_t n_blocks, uint64_t *keys, double *blocks,
                          double *sumsq, uint8_t *nonzero, int64_t *zero_count, void *stream);
+/* qm_build_fill that also writes the blocks' support masks (uint64[3*n_blocks], qm_block_meta's
+ * layout; NULL = none) and OR-accumulates the not-full flags into not_full[2] (device, zeroed by
+ * the caller; NULL = none) in the same pass over the filled blocks that computes the norms. */
+QM_API int qm_build_fill_meta(const qm_layout *layout, const double *vals /*device*/, int64_t n, void *ws,
+                              size_t ws_bytes, int64_t n_blocks, uint64_t *keys, double *blocks,
+                              double *sumsq, uint8_t *nonzero, int64_t *zero_count, uint64_t *masks,
+                              int64_t *not_full, void *stream);
 
 /* ---- symbolic phase (replaces the recursive task expansion, ops.py:197-245 + engine.py:196-326) */
 /* Persistent workspace for one product; valid from qm_spgemm_count until qm_spgemm_fill returns. */
@@ -162,9 +169,10 @@ QM_API int qm_numeric(const qm_layout *layout, const uint64_t *a_keys, const dou
                const uint64_t *c_keys, int64_t nC, int64_t nT, double *c_blocks, double *c_sumsq,
                uint8_t *c_nonzero, int64_t *zero_count, void *ws, size_t ws_bytes, void *stream);
 /* qm_numeric with the operands' support masks and virtual transposes. a_masks / b_masks: device
- * uint64[2*n] (row masks, then column masks; qm_block_masks) or NULL = full support: for bs 32-128
+ * uint64[3*n] (row masks, column masks, flags; qm_block_meta) or NULL = full support: for bs 32-128
  * the TMA kernel skips the k panels (16 deep for bs 32/64, 32 for bs 128) of a triple where A's
- * nonzero columns and B's nonzero rows do not meet (they add exactly zero). flags &
+ * nonzero columns and B's nonzero rows do not meet (they add exactly zero), except when either
+ * block's flags mark a NaN/Inf (then every panel runs: 0*Inf is NaN). flags &
  * QM_NUMERIC_TRANSPOSED_REFS: a triple index with bit 31 set names a stored block used transposed
  * -- the reference's virtual transposes (`_virtual_child` / ta / tb, ops.py:100-116) as a TMA box
  * and shared-memory addressing choice, no materialised transpose (bs 32/64/128 only).
@@ -216,6 +224,16 @@ QM_API int qm_block_stats(int32_t block_size, int64_t n, const double *blocks, d
  * Inf get full masks. */
 QM_API int qm_block_masks(int32_t block_size, int64_t n, const double *blocks, uint64_t *row_mask,
                           uint64_t *col_mask, void *stream);
+/* All per-block metadata of n blocks in ONE read of the blocks (each output may be NULL):
+ * sumsq[i] / nonzero[i] as qm_block_stats (bit-identical sums), *zero_count += exactly-zero blocks,
+ * masks = uint64[3*n]: row masks, column masks (as qm_block_masks), flags (bit 0: the block holds a
+ * NaN or Inf -- its masks are full and the numeric kernel executes all of its k panels, so 0*Inf
+ * still yields the reference's NaN), and not_full[0] / not_full[1] (device int64, zeroed by the
+ * caller) become nonzero when some block's row / column mask is not full (all-full operands skip
+ * the exact-zero filters entirely). The reference keeps block norms with the leaf
+ * (block_sparse.py:41, BlockSparseLeaf.block_norms); masks are the same kind of input metadata. */
+QM_API int qm_block_meta(int32_t block_size, int64_t n, const double *blocks, double *sumsq, uint8_t *nonzero,
+                         int64_t *zero_count, uint64_t *masks, int64_t *not_full, void *stream);
 /* dst[i] = src[idx[i]] for whole bs x bs blocks (packs halo blocks for the NVLink exchange). */
 QM_API int qm_gather_blocks(int32_t block_size, const double *src, const int64_t *idx, int64_t n,
                      double *dst, void *stream);

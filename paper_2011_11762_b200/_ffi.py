@@ -22,6 +22,8 @@ from .errors import (
 
 LIB_PATH = Path(__file__).resolve().parent / "libqmb200.so"
 
+ABI_VERSION = 2  # include/qmb200.h QM_ABI_VERSION
+
 QM_OK, QM_ERR_INVALID, QM_ERR_CUDA, QM_ERR_WORKSPACE, QM_ERR_UNSUPPORTED = 0, -1, -2, -3, -4
 
 # Every symbol include/qmb200.h declares (tests check the .so exports all of them).
@@ -35,6 +37,7 @@ EXPORTS = (
     "qm_build_workspace_bytes",
     "qm_build_count",
     "qm_build_fill",
+    "qm_build_fill_meta",
     "qm_spgemm_workspace_bytes",
     "qm_spgemm_count",
     "qm_spgemm_count_masked",
@@ -54,6 +57,7 @@ EXPORTS = (
     "qm_compact",
     "qm_block_stats",
     "qm_block_masks",
+    "qm_block_meta",
     "qm_gather_blocks",
     "qm_gather_blocks_t",
     "qm_transpose_blocks",
@@ -101,6 +105,7 @@ _SIGS = {
     "qm_build_count": (ctypes.c_int, [_LP, _P, _P, _I64, _P, _SZ, ctypes.POINTER(_I64),
                                       ctypes.POINTER(_I64), _P]),
     "qm_build_fill": (ctypes.c_int, [_LP, _P, _I64, _P, _SZ, _I64, _P, _P, _P, _P, _P, _P]),
+    "qm_build_fill_meta": (ctypes.c_int, [_LP, _P, _I64, _P, _SZ, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "qm_spgemm_workspace_bytes": (_SZ, [_LP, _I64, _I64]),
     "qm_spgemm_count": (ctypes.c_int, [_LP, _P, _I64, _P, _I64, _P, _SZ, ctypes.POINTER(_I64),
                                        ctypes.POINTER(_I64), _P]),
@@ -126,6 +131,7 @@ _SIGS = {
     "qm_compact": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "qm_block_stats": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P]),
     "qm_block_masks": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P]),
+    "qm_block_meta": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "qm_gather_blocks": (ctypes.c_int, [_I32, _P, _P, _I64, _P, _P]),
     "qm_gather_blocks_t": (ctypes.c_int, [_I32, _P, _P, _P, _I64, _P, _P]),
     "qm_transpose_blocks": (ctypes.c_int, [_I32, _P, _I64, _P, _P]),
@@ -167,8 +173,9 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.qm_abi_version() != 1:
-            raise ConfigurationError(f"libqmb200 ABI {lib.qm_abi_version()} != 1")
+        if lib.qm_abi_version() != ABI_VERSION:
+            raise ConfigurationError(f"libqmb200 ABI {lib.qm_abi_version()} != {ABI_VERSION} (rebuild: "
+                                     "paper_2011_11762_b200._build.build())")
         if path is None:
             _lib = lib
         return lib

@@ -32,8 +32,9 @@ class BlockSet:
     keys: torch.Tensor
     blocks: torch.Tensor
     sumsq: torch.Tensor
-    # int64[2, n] support masks (row 0: nonzero rows, row 1: nonzero columns; qm_block_masks),
-    # computed on first use by a product and kept with the (immutable) block set; None = not yet.
+    # int64[3, n] support masks (row 0: nonzero rows, row 1: nonzero columns, row 2: flags, bit 0 =
+    # the block holds a NaN/Inf; qm_block_meta), computed with the norms by the block set's producer
+    # (device generator / builder) or on first use by a product, and kept with the (immutable) set.
     masks: torch.Tensor | None = None
     # (every block has all rows nonzero, every block has all columns nonzero): set with `masks`
     masks_full: tuple[bool, bool] = (False, False)
@@ -42,25 +43,29 @@ class BlockSet:
         """Per-block nonzero-row / nonzero-column bit masks (device). A product skips block pairs
         whose masks do not meet: their product is exactly zero (spgemm.multiply_blocks)."""
         if self.masks is None:
-            from . import _ffi  # noqa: PLC0415
-
-            st = stream if stream is not None else torch.cuda.current_stream(self.device)
-            m = torch.empty((2, self.n), dtype=torch.int64, device=self.device)
-            if self.n:
-                _ffi.check(_ffi.load().qm_block_masks(self.bs, self.n, _ffi.ptr(self.blocks), _ffi.ptr(m[0]),
-                                                      _ffi.ptr(m[1]), _ffi.stream_handle(st)),
-                           "qm_block_masks")
-                full = -1 if self.bs >= 64 else (1 << self.bs) - 1
-                with torch.cuda.stream(st):
-                    f = (m == full).all(dim=1).to(torch.int64)
-                # one read per block set, through mapped memory (a copy-engine read would queue
-                # behind bulk D2H copies in flight, e.g. a pipelined serving loop's result copies)
-                f0, f1 = _ffi.read_i64s(f, 2, st)
-                self.masks_full = (bool(f0), bool(f1))
-            else:
-                self.masks_full = (True, True)
-            self.masks = m
+            self.compute_meta(stream, sumsq=False)
         return self.masks
+
+    def compute_meta(self, stream=None, sumsq: bool = True) -> "BlockSet":
+        """Norms (sumsq) and support masks of every block in one read of the blocks (qm_block_meta);
+        the all-full flags are read back through mapped memory (a copy-engine read would queue behind
+        bulk D2H copies in flight, e.g. a pipelined serving loop's result copies)."""
+        from . import _ffi  # noqa: PLC0415
+
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        m = torch.empty((3, self.n), dtype=torch.int64, device=self.device)
+        if self.n:
+            nf = torch.zeros(2, dtype=torch.int64, device=self.device)
+            _ffi.check(_ffi.load().qm_block_meta(self.bs, self.n, _ffi.ptr(self.blocks),
+                                                 _ffi.ptr(self.sumsq) if sumsq else 0, 0, 0, _ffi.ptr(m),
+                                                 _ffi.ptr(nf), _ffi.stream_handle(st)),
+                       "qm_block_meta")
+            f0, f1 = _ffi.read_i64s(nf, 2, st)
+            self.masks_full = (f0 == 0, f1 == 0)
+        else:
+            self.masks_full = (True, True)
+        self.masks = m
+        return self
 
     @property
     def n(self) -> int:

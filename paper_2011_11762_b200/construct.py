@@ -144,13 +144,18 @@ def blocks_from_triplets_device(geom: Geometry, rows, cols, vals, device, stream
                        torch.empty((nblk, bs, bs), dtype=torch.float64, device=dev),
                        torch.empty(nblk, dtype=torch.float64, device=dev))
         nz = torch.empty(nblk, dtype=torch.uint8, device=dev)
-        zc = torch.zeros(1, dtype=torch.int64, device=dev)
-        _ffi.check(lib.qm_build_fill(lp, _ffi.ptr(v), n, _ffi.ptr(ws), wb, nblk, _ffi.ptr(out.keys),
-                                     _ffi.ptr(out.blocks), _ffi.ptr(out.sumsq), _ffi.ptr(nz),
-                                     _ffi.ptr(zc), sh), "qm_build_fill")
-        n_zero = _ffi.read_i64(zc, st)
+        zc = torch.zeros(3, dtype=torch.int64, device=dev)  # [exact-zero blocks, rows not full, cols not full]
+        masks = torch.empty((3, nblk), dtype=torch.int64, device=dev)
+        # norms, nonzero flags and support masks in one pass over the filled blocks
+        _ffi.check(lib.qm_build_fill_meta(lp, _ffi.ptr(v), n, _ffi.ptr(ws), wb, nblk, _ffi.ptr(out.keys),
+                                          _ffi.ptr(out.blocks), _ffi.ptr(out.sumsq), _ffi.ptr(nz),
+                                          _ffi.ptr(zc), _ffi.ptr(masks), _ffi.ptr(zc[1:]), sh),
+                   "qm_build_fill_meta")
+        n_zero, nf_r, nf_c = _ffi.read_i64s(zc, 3, st)
         if n_zero:
             from .spgemm import compact  # noqa: PLC0415
 
-            out = compact(bs, out, nz, n_zero, st)
+            out = compact(bs, out, nz, n_zero, st)  # masks are recomputed on first use
+        else:
+            out.masks, out.masks_full = masks, (nf_r == 0, nf_c == 0)
     return out

@@ -32,20 +32,23 @@ __global__ void k_read_i64(const int64_t *src, int n, const int64_t *src2, volat
 }
 
 int mapped_i64(int64_t **host, int64_t **dev) {
+  // One mapped buffer per (thread, device): a thread that alternates GPUs reuses each device's
+  // buffer instead of allocating (and leaking) a new one on every switch. (Not freed at thread
+  // exit: the CUDA runtime may already be unloading then; it is 64 bytes per thread and device.)
   struct Mapped {
-    int64_t *host = nullptr, *dev = nullptr;
-    int device = -1;
+    int64_t *host[64] = {};
+    int64_t *dev[64] = {};
   };
   static thread_local Mapped m;
   int device = 0;
   QM_CUDA_TRY(cudaGetDevice(&device));
-  if (m.host == nullptr || m.device != device) {
-    QM_CUDA_TRY(cudaHostAlloc((void **)&m.host, 8 * sizeof(int64_t), cudaHostAllocMapped));
-    QM_CUDA_TRY(cudaHostGetDevicePointer((void **)&m.dev, m.host, 0));
-    m.device = device;
+  const int d = device & 63;
+  if (m.host[d] == nullptr) {
+    QM_CUDA_TRY(cudaHostAlloc((void **)&m.host[d], 8 * sizeof(int64_t), cudaHostAllocMapped | cudaHostAllocPortable));
+    QM_CUDA_TRY(cudaHostGetDevicePointer((void **)&m.dev[d], m.host[d], 0));
   }
-  *host = m.host;
-  *dev = m.dev;
+  *host = m.host[d];
+  *dev = m.dev[d];
   return QM_OK;
 }
 

@@ -186,9 +186,10 @@ extern "C" int qm_build_count(const qm_layout *layout, const int64_t *rows, cons
   return QM_OK;
 }
 
-extern "C" int qm_build_fill(const qm_layout *layout, const double *vals, int64_t n, void *ws,
-                             size_t ws_bytes, int64_t n_blocks, uint64_t *keys, double *blocks,
-                             double *sumsq, uint8_t *nonzero, int64_t *zero_count, void *stream) {
+extern "C" int qm_build_fill_meta(const qm_layout *layout, const double *vals, int64_t n, void *ws,
+                                  size_t ws_bytes, int64_t n_blocks, uint64_t *keys, double *blocks,
+                                  double *sumsq, uint8_t *nonzero, int64_t *zero_count, uint64_t *masks,
+                                  int64_t *not_full, void *stream) {
   Geometry g;
   int rc = make_geometry(layout, &g);
   if (rc != QM_OK) return rc;
@@ -207,5 +208,14 @@ extern "C" int qm_build_fill(const qm_layout *layout, const double *vals, int64_
   k_elements<<<grid_for(n), 256, 0, st>>>(w.skey, w.perm, vals, n, pbits, g.bs, w.elem_head, w.blk_head,
                                           w.blk_incl, blocks, keys);
   QM_LAUNCHED("k_elements");
-  return launch_block_stats(g.bs, n_blocks, blocks, sumsq, nonzero, zero_count, st);
+  // norms, nonzero flags and (optionally) support masks in one read of the filled blocks
+  return launch_block_meta(g.bs, n_blocks, blocks, sumsq, nonzero, zero_count, masks,
+                           masks ? masks + n_blocks : nullptr, masks ? masks + 2 * n_blocks : nullptr, not_full, st);
+}
+
+extern "C" int qm_build_fill(const qm_layout *layout, const double *vals, int64_t n, void *ws,
+                             size_t ws_bytes, int64_t n_blocks, uint64_t *keys, double *blocks,
+                             double *sumsq, uint8_t *nonzero, int64_t *zero_count, void *stream) {
+  return qm_build_fill_meta(layout, vals, n, ws, ws_bytes, n_blocks, keys, blocks, sumsq, nonzero, zero_count,
+                            nullptr, nullptr, stream);
 }

@@ -23,6 +23,11 @@ int read_device_i64(const void *dev_src, int n, int64_t *host_out, cudaStream_t 
 int mapped_i64(int64_t **host, int64_t **dev);
 // Counts one kernel launch (qm_launch_count).
 void note_launch(int n = 1);
+// Per-block metadata in one read (k_block_meta, qm_numeric.cu): sums of squares, nonzero flags,
+// exact-zero count, support masks (rmask/cmask/flags may be NULL) and the not-full OR flags.
+int launch_block_meta(int bs, int64_t n, const double *blocks, double *sumsq, uint8_t *nonzero,
+                      int64_t *zero_count, uint64_t *rmask, uint64_t *cmask, uint64_t *flags,
+                      int64_t *not_full, cudaStream_t st);
 
 #define QM_CUDA_TRY(expr)                                                                   \
   do {                                                                                      \
@@ -113,7 +118,7 @@ struct NumericAux {
   const uint64_t *a_keys = nullptr;
   int32_t nbl = 1, lbits = 0;
   int64_t nbg = 1;
-  const uint64_t *a_masks = nullptr, *b_masks = nullptr;  // [2, n]: row masks, then column masks
+  const uint64_t *a_masks = nullptr, *b_masks = nullptr;  // [3, n]: row masks, column masks, flags (bit 0: NaN/Inf)
   bool transpose_bits = false;  // triple indices carry a transpose flag in bit 31 (virtual transposes)
   int64_t *panel_count = nullptr;
 };

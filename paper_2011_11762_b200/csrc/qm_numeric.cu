@@ -254,42 +254,117 @@ __global__ void __launch_bounds__(256) k_numeric_generic(const double *__restric
   }
 }
 
-__global__ void __launch_bounds__(256) k_block_stats(const double *__restrict__ blocks, int64_t n,
-                                                     int bs, double *sumsq, uint8_t *nonzero,
-                                                     int64_t *zero_count) {
+// Per-block metadata in one read of the blocks (the reference stores a leaf's block norms with
+// it, block_sparse.py:41; the support masks and non-finite flag are the same kind of input
+// metadata): squared Frobenius norm, any-nonzero flag (_set_block's np.any, block_sparse.py:37-41),
+// and optionally the support masks -- bit b of rmask / cmask is set when a row / column r with
+// b = r (bs <= 64) or b = r*64/bs (bs > 64) holds a nonzero -- plus flags bit 0 = the block holds a
+// NaN or Inf (its masks are then full: 0 * Inf is NaN, so none of its products is provably zero,
+// and the numeric kernel must not skip any of its k panels). not_full[0] / [1] (OR-accumulated,
+// one atomic per CTA) become nonzero when some block's row / column mask is not full.
+// One CTA of 256 threads per block (grid-stride): thread t sums elements t, t+256, ... in an fma
+// chain, warp xor tree, warps in order -- the order every fused statistics pass of the library
+// (k_axpby, the numeric epilogues' tile partials aside) reproduces bit for bit.
+template <int BS>
+__global__ void __launch_bounds__(256) k_block_meta(const double *__restrict__ blocks, int64_t n, int bs_rt,
+                                                    double *sumsq, uint8_t *nonzero, int64_t *zero_count,
+                                                    uint64_t *rmask, uint64_t *cmask, uint64_t *flags,
+                                                    unsigned long long *not_full) {
   __shared__ double red[8];
   __shared__ int rnz[8];
+  __shared__ uint64_t rrm[8], rcm[8];
+  __shared__ int rbad[8];
+  const int bs = BS ? BS : bs_rt;
   const int64_t elems = (int64_t)bs * bs;
+  const bool want_masks = rmask != nullptr;
+  const uint64_t full = bs >= 64 ? ~0ull : ((1ull << bs) - 1ull);
+  unsigned long long nf_rows = 0, nf_cols = 0;  // this CTA saw a block with a partial row / column mask
   for (int64_t m = blockIdx.x; m < n; m += gridDim.x) {
     const double *b = blocks + (size_t)m * elems;
     double ss = 0.0;
-    bool nz = false;
-    for (int64_t e = threadIdx.x; e < elems; e += blockDim.x) {
-      const double v = b[e];
-      ss = fma(v, v, ss);
-      nz |= v != 0.0;
+    bool nz = false, bad = false;
+    uint64_t rb = 0, cb = 0;
+    if (BS) {
+#pragma unroll
+      for (int j = 0; j < (BS * BS + 255) / 256; ++j) {
+        const int e = threadIdx.x + 256 * j;
+        if (BS * BS % 256 == 0 || e < BS * BS) {
+          const double v = b[e];
+          ss = fma(v, v, ss);
+          nz |= v != 0.0;
+          if (want_masks) {
+            const int r = e / BS, c = e % BS;
+            const uint64_t on = v != 0.0 ? 1ull : 0ull;
+            rb |= on << (BS <= 64 ? r : r * 64 / BS);
+            cb |= on << (BS <= 64 ? c : c * 64 / BS);
+            bad |= !isfinite(v);
+          }
+        }
+      }
+    } else {
+      for (int64_t e = threadIdx.x; e < elems; e += blockDim.x) {
+        const double v = b[e];
+        ss = fma(v, v, ss);
+        nz |= v != 0.0;
+        if (want_masks && v != 0.0) {
+          const int r = (int)(e / bs), c = (int)(e % bs);
+          rb |= 1ull << (bs <= 64 ? r : (r * 64) / bs);
+          cb |= 1ull << (bs <= 64 ? c : (c * 64) / bs);
+        }
+        bad |= !isfinite(v);
+      }
     }
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
     const bool wnz = __any_sync(0xffffffffu, nz);
+    const int w = threadIdx.x >> 5;
+    if (want_masks) {
+      const uint32_t rl = __reduce_or_sync(0xffffffffu, (uint32_t)rb), rh = __reduce_or_sync(0xffffffffu, (uint32_t)(rb >> 32));
+      const uint32_t cl = __reduce_or_sync(0xffffffffu, (uint32_t)cb), ch = __reduce_or_sync(0xffffffffu, (uint32_t)(cb >> 32));
+      const bool wbad = __any_sync(0xffffffffu, bad);
+      if ((threadIdx.x & 31) == 0) {
+        rrm[w] = (uint64_t)rh << 32 | rl;
+        rcm[w] = (uint64_t)ch << 32 | cl;
+        rbad[w] = wbad;
+      }
+    }
     if ((threadIdx.x & 31) == 0) {
-      red[threadIdx.x >> 5] = ss;
-      rnz[threadIdx.x >> 5] = wnz;
+      red[w] = ss;
+      rnz[w] = wnz;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       double tot = 0.0;
-      int any = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-        tot += red[w];
-        any |= rnz[w];
+      int any = 0, nonfinite = 0;
+      uint64_t r = 0, c = 0;
+      for (int x = 0; x < (int)(blockDim.x >> 5); ++x) {
+        tot += red[x];
+        any |= rnz[x];
+        if (want_masks) {
+          r |= rrm[x];
+          c |= rcm[x];
+          nonfinite |= rbad[x];
+        }
       }
       if (sumsq) sumsq[m] = tot;
       if (nonzero) nonzero[m] = (uint8_t)any;
       if (!any && zero_count) atomicAdd((unsigned long long *)zero_count, 1ull);
+      if (want_masks) {
+        if (nonfinite) r = c = full;
+        rmask[m] = r;
+        cmask[m] = c;
+        if (flags) flags[m] = nonfinite ? 1ull : 0ull;
+        nf_rows |= r != full;
+        nf_cols |= c != full;
+      }
     }
     __syncthreads();
   }
+  if (not_full && threadIdx.x == 0) {
+    if (nf_rows) atomicOr(&not_full[0], 1ull);
+    if (nf_cols) atomicOr(&not_full[1], 1ull);
+  }
 }
+
 
 
 
@@ -324,13 +399,34 @@ using Cfg128 = DmmaCfg<128, 2, 4, 16, 4, 1>;
 
 }  // namespace
 
+int launch_block_meta(int bs, int64_t n, const double *blocks, double *sumsq, uint8_t *nonzero,
+                      int64_t *zero_count, uint64_t *rmask, uint64_t *cmask, uint64_t *flags,
+                      int64_t *not_full, cudaStream_t st) {
+  if (n <= 0) return QM_OK;
+  // 8 CTAs of 256 threads per SM, several waves' worth of blocks in flight (each thread has all of
+  // its bs*bs/256 loads of a block outstanding at once)
+  const int64_t grid = std::min<int64_t>(n, (int64_t)sm_count() * 16);
+  unsigned long long *nf = (unsigned long long *)not_full;
+  switch (bs) {
+#define QM_META_CASE(B)                                                                                   \
+  case B:                                                                                                 \
+    k_block_meta<B><<<(int)grid, 256, 0, st>>>(blocks, n, bs, sumsq, nonzero, zero_count, rmask, cmask, flags, nf); \
+    break;
+    QM_META_CASE(16)
+    QM_META_CASE(32)
+    QM_META_CASE(64)
+    QM_META_CASE(128)
+#undef QM_META_CASE
+    default:
+      k_block_meta<0><<<(int)grid, 256, 0, st>>>(blocks, n, bs, sumsq, nonzero, zero_count, rmask, cmask, flags, nf);
+  }
+  QM_LAUNCHED("k_block_meta");
+  return QM_OK;
+}
+
 int launch_block_stats(int bs, int64_t n, const double *blocks, double *sumsq, uint8_t *nonzero,
                        int64_t *zero_count, cudaStream_t st) {
-  if (n <= 0) return QM_OK;
-  int64_t grid = std::min<int64_t>(n, (int64_t)sm_count() * 16);
-  k_block_stats<<<(int)grid, 256, 0, st>>>(blocks, n, bs, sumsq, nonzero, zero_count);
-  QM_LAUNCHED("k_block_stats");
-  return QM_OK;
+  return launch_block_meta(bs, n, blocks, sumsq, nonzero, zero_count, nullptr, nullptr, nullptr, nullptr, st);
 }
 
 int numeric_sm_count() { return sm_count(); }
@@ -442,51 +538,24 @@ extern "C" int qm_block_stats(int32_t block_size, int64_t n, const double *block
   return launch_block_stats(block_size, n, blocks, sumsq, nonzero, nullptr, (cudaStream_t)stream);
 }
 
-namespace qm {
-namespace {
-// Support masks of each block: bit b of row_mask is set when a row r with b = r*64/bs (b = r for
-// bs <= 64) holds a nonzero, col_mask likewise for columns. A block holding a NaN or Inf gets full
-// masks (0 * Inf is NaN, so its products are never provably zero). One warp per block.
-__global__ void k_block_masks(const double *blocks, int64_t n, int bs, uint64_t *rmask, uint64_t *cmask) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t elems = (int64_t)bs * bs;
-  for (int64_t m = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); m < n; m += warps) {
-    const double *b = blocks + (size_t)m * elems;
-    uint64_t rb = 0, cb = 0;
-    bool bad = false;
-    for (int64_t e = lane; e < elems; e += 32) {
-      const double v = __ldcs(b + e);
-      if (v != 0.0) {
-        const int r = (int)(e / bs), c = (int)(e % bs);
-        rb |= 1ull << (bs <= 64 ? r : (r * 64) / bs);
-        cb |= 1ull << (bs <= 64 ? c : (c * 64) / bs);
-      }
-      bad |= !isfinite(v);
-    }
-    const uint32_t rl = __reduce_or_sync(0xffffffffu, (uint32_t)rb), rh = __reduce_or_sync(0xffffffffu, (uint32_t)(rb >> 32));
-    const uint32_t cl = __reduce_or_sync(0xffffffffu, (uint32_t)cb), ch = __reduce_or_sync(0xffffffffu, (uint32_t)(cb >> 32));
-    const bool anybad = __any_sync(0xffffffffu, bad);
-    if (lane == 0) {
-      rmask[m] = anybad ? ~0ull : ((uint64_t)rh << 32 | rl);
-      cmask[m] = anybad ? ~0ull : ((uint64_t)ch << 32 | cl);
-    }
-  }
-}
-}  // namespace
-}  // namespace qm
-
 extern "C" int qm_block_masks(int32_t block_size, int64_t n, const double *blocks, uint64_t *row_mask,
                               uint64_t *col_mask, void *stream) {
   if (block_size < 1 || n < 0 || (n > 0 && (!blocks || !row_mask || !col_mask))) {
     set_error("qm_block_masks: bad arguments");
     return QM_ERR_INVALID;
   }
-  if (n == 0) return QM_OK;
-  const int64_t grid = std::min<int64_t>((n + 7) / 8, (int64_t)sm_count() * 16);
-  k_block_masks<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(blocks, n, block_size, row_mask, col_mask);
-  QM_LAUNCHED("k_block_masks");
-  return QM_OK;
+  return launch_block_meta(block_size, n, blocks, nullptr, nullptr, nullptr, row_mask, col_mask, nullptr, nullptr,
+                           (cudaStream_t)stream);
+}
+
+extern "C" int qm_block_meta(int32_t block_size, int64_t n, const double *blocks, double *sumsq, uint8_t *nonzero,
+                             int64_t *zero_count, uint64_t *masks, int64_t *not_full, void *stream) {
+  if (block_size < 1 || n < 0 || (n > 0 && !blocks)) {
+    set_error("qm_block_meta: bad arguments");
+    return QM_ERR_INVALID;
+  }
+  return launch_block_meta(block_size, n, blocks, sumsq, nonzero, zero_count, masks, masks ? masks + n : nullptr,
+                           masks ? masks + 2 * n : nullptr, not_full, (cudaStream_t)stream);
 }
 
 extern "C" int qm_numeric_pools(const qm_layout *layout, const double *const *a_pools, const int64_t *a_counts,

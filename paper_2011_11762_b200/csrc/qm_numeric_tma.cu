@@ -406,7 +406,9 @@ __global__ void k_order_key(const uint2 *tri, const int64_t *tptr, const uint64_
 // k panels of each triple that can contribute: panel p covers rows [p*KP, (p+1)*KP) of B and the
 // same columns of A, i.e. mask bits [p*W, (p+1)*W) with W = 64*KP/max(BS, 64) (mask bit b = row b
 // for BS <= 64, rows 2b, 2b+1 for BS = 128). A panel where A's columns and B's rows share no bit
-// adds exactly zero. Disjoint supports overall (not filtered by the symbolic phase) keep one panel.
+// adds exactly zero -- unless either block holds a NaN or Inf (masks' flags row), where 0 * Inf = NaN
+// must be formed as numpy's dgemm does. Disjoint supports overall (not filtered by the symbolic
+// phase) keep one panel.
 // Also counts the k rows to execute (KP per panel; warp partials, one atomic per warp).
 template <class Cfg>
 __global__ void k_triple_panels(const uint2 *tri, int64_t nT, const uint64_t *a_masks, int64_t nA,
@@ -426,6 +428,8 @@ __global__ void k_triple_panels(const uint2 *tri, int64_t nT, const uint64_t *a_
     for (int p = 0; p < Cfg::NP; ++p)
       if ((ov >> (p * W)) & kW) m |= 1u << p;
     if (!m) m = 1u;
+    // a block holding NaN/Inf (flags row, bit 0): every panel runs, so 0 * Inf still yields NaN
+    if ((a_masks[2 * nA + a] | b_masks[2 * nB + b]) & 1ull) m = (1u << Cfg::NP) - 1u;
     sm[t] = (uint8_t)m;
     cnt += __popc(m) * Cfg::KP;  // k rows executed
   }
@@ -558,7 +562,8 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
   int64_t grid = (int64_t)sm_count_tma() * per_sm;
   if (grid > nU) grid = nU;
   uint32_t *order = nullptr;
-  if (oi.a_keys && na == 1 && nb == 1) {
+  // (not with transposed references: their triple indices name stored blocks, not view entries)
+  if (oi.a_keys && na == 1 && nb == 1 && !TR) {
     const int kind = claim_order();
     if (kind != kOrderKey) {
       rc = make_order<Cfg>(kind, tri, tptr, oi.a_keys, oi.nbl, oi.lbits, oi.nbg, nC, ws, &order, st);

@@ -380,15 +380,21 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
         return empty, stats
     # Support masks (spgemm.symbolic): gathered with the keys when some rank's blocks have partial
     # supports, so every rank skips the same exactly-zero block pairs and k panels.
-    ma = mb = None
+    ma = mb = fa = fb = None
     if spgemm.support_filter_enabled() and a_local.blocks.is_cuda:
         a_local.support_masks()
         if not b_is_a:
             b_local.support_masks()
-        partial = not (a_local.masks_full[1] or (a_local if b_is_a else b_local).masks_full[0])
-        if comm.allreduce_max(1.0 if partial else 0.0, dev) > 0.0:
+        # the filter is needed unless ALL of A's blocks have full column supports or ALL of B's
+        # full row supports (a max-reduction of "not full" per operand, then the global test)
+        bl = a_local if b_is_a else b_local
+        a_part = comm.allreduce_max(0.0 if a_local.masks_full[1] else 1.0, dev) > 0.0
+        b_part = comm.allreduce_max(0.0 if bl.masks_full[0] else 1.0, dev) > 0.0
+        if a_part and b_part:
             ma, _ = comm.allgather_varlen(a_local.masks[1].contiguous())
-            mb, _ = comm.allgather_varlen((a_local if b_is_a else b_local).masks[0].contiguous())
+            mb, _ = comm.allgather_varlen(bl.masks[0].contiguous())
+            fa, _ = comm.allgather_varlen(a_local.masks[2].contiguous())  # NaN/Inf flags
+            fb = fa if b_is_a else comm.allgather_varlen(bl.masks[2].contiguous())[0]
     t1 = clock()
     st = (backend.symbolic_state(layout, ka, kb, a_cmask=ma, b_rmask=mb) if ma is not None
           else backend.symbolic_state(layout, ka, kb))
@@ -462,15 +468,17 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     c_tptr_local = (c_tptr[m0:m1 + 1] - lo).contiguous()
     c_keys_local = c_keys[m0:m1].contiguous()
     dummy_a = torch.empty(0, dtype=torch.float64, device=dev)
-    if ma is not None:  # the pools' masks are the gathered ones (A columns, B rows), not recomputed
+    # pool keys are the blocks' quadtree keys (the bs-16 grouping and claim orders decode them)
+    pk_a, pk_b = ka[need_a], kb[need_b]
+    if ma is not None:  # the pools' masks are the gathered ones (A columns, B rows, flags), not recomputed
         none_a = torch.full((need_a.shape[0],), -1, dtype=torch.int64, device=dev)
         none_b = torch.full((need_b.shape[0],), -1, dtype=torch.int64, device=dev)
-        pa = BlockSet(need_a, pool_a, dummy_a, torch.stack([none_a, ma[need_a]]), (False, False))
-        pb = BlockSet(need_b, pool_b, dummy_a, torch.stack([mb[need_b], none_b]), (False, False))
+        pa = BlockSet(pk_a, pool_a, dummy_a, torch.stack([none_a, ma[need_a], fa[need_a]]), (False, False))
+        pb = BlockSet(pk_b, pool_b, dummy_a, torch.stack([mb[need_b], none_b, fb[need_b]]), (False, False))
     else:  # full supports (or filter off): nothing to skip, and no per-product mask pass
-        pa = BlockSet(need_a, pool_a, dummy_a, masks_full=(True, True))
-        pb = BlockSet(need_b, pool_b, dummy_a, masks_full=(True, True))
-        pa.masks = pb.masks = torch.empty((2, 0), dtype=torch.int64, device=dev)
+        pa = BlockSet(pk_a, pool_a, dummy_a, masks_full=(True, True))
+        pb = BlockSet(pk_b, pool_b, dummy_a, masks_full=(True, True))
+        pa.masks = pb.masks = torch.empty((3, 0), dtype=torch.int64, device=dev)
     c = backend.numeric(layout, pa, pb, tri_local, c_tptr_local, c_keys_local)
     t4 = clock()
     stats.n_c_local = c.n

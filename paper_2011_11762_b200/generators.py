@@ -264,10 +264,10 @@ def device_blocks(geom: Geometry, keys: np.ndarray | torch.Tensor, seed: int, ma
     with torch.cuda.device(dev):
         st = stream if stream is not None else torch.cuda.current_stream(dev)
         _ffi.check(lib.qm_generate_blocks(ctypes.byref(layout), _ffi.ptr(k), n, seed, matrix_id,
-                                          pattern, half_bw, _ffi.ptr(blocks), _ffi.ptr(sumsq),
-                                          _ffi.stream_handle(st)),
+                                          pattern, half_bw, _ffi.ptr(blocks), 0, _ffi.stream_handle(st)),
                    "qm_generate_blocks")
-    return BlockSet(k, blocks, sumsq)
+        # operand metadata (norms + support masks + NaN/Inf flags) in one read of the new blocks
+        return BlockSet(k, blocks, sumsq).compute_meta(st)
 
 
 # ---- C4: decay matrix ---------------------------------------------------------------------------
@@ -382,12 +382,34 @@ def config_operands_device(cfg: BaselineConfig, device) -> tuple[Geometry, Block
         _, (ka, ba), _ = config_operands_host(cfg)
         a = BlockSet.from_numpy(ka, ba, None, device)
         if a.device.type == "cuda":
-            a.support_masks()  # input metadata, like the block norms
+            a.compute_meta()  # input metadata, like the block norms (one pass: norms + masks)
         return geom, a, a
     sets = []
     for m in (0, 1):
         keys = config_keys(cfg, m)
         sets.append(device_blocks(geom, keys, cfg.seed, m, config_pattern(cfg), cfg.half_bw, device))
-        if sets[-1].device.type == "cuda":
-            sets[-1].support_masks()
     return geom, sets[0], sets[1]
+
+
+def structure_counts(cfg: BaselineConfig) -> dict:
+    """Block-level structure of a configuration's product, on the host (numpy/scipy, no device):
+    nnzb(A), nnzb(B), the structural C block count and triple count T (every (A block, B block)
+    pair with a matching k, as BlockSparseLeaf.multiply enumerates them). Both
+    bench arms report these as the workload definition."""
+    import scipy.sparse as sp  # noqa: PLC0415
+
+    geom = cfg.geometry
+    if cfg.kind == "decay":
+        _, (ka, _), (kb, _) = config_operands_host(cfg)
+    else:
+        ka, kb = config_keys(cfg, 0), config_keys(cfg, 1)
+    nb = geom.nbg
+
+    def occ(keys):
+        bi, bj = geom.decode(keys)
+        return sp.csr_matrix((np.ones(keys.size, dtype=np.int64), (bi, bj)), shape=(nb, nb))
+
+    pa, pb = occ(ka), occ(kb)
+    c = pa @ pb
+    return {"nnzb_a": int(ka.size), "nnzb_b": int(kb.size), "nnzb_c_structural": int(c.nnz),
+            "triples_structural": int(c.sum())}

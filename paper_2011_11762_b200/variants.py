@@ -106,7 +106,8 @@ class BlockView(BlockSet):
             pm = self.pool.support_masks(stream)
             idx = (self.src.long() & 0x7FFFFFFF)
             rows, cols = pm[0][idx], pm[1][idx]
-            self.masks = torch.stack([torch.where(self._tsel, cols, rows), torch.where(self._tsel, rows, cols)])
+            self.masks = torch.stack([torch.where(self._tsel, cols, rows), torch.where(self._tsel, rows, cols),
+                                      pm[2][idx]])
             fr, fc = self.pool.masks_full
             both = fr and fc
             self.masks_full = (both, both) if self._any_t else (fr, fc)
@@ -170,7 +171,7 @@ def transpose(geom: Geometry, x: BlockSet) -> BlockSet:
         return x
     bi, bj = _decode(geom, x.keys)
     keys = _encode(geom, bj, bi)
-    m = x.masks[[1, 0]] if x.masks is not None else None  # a transposed block swaps row / column supports
+    m = x.masks[[1, 0, 2]] if x.masks is not None else None  # a transposed block swaps row / column supports
     return _sorted(keys, _transposed_blocks(x.blocks), x.sumsq, m, (x.masks_full[1], x.masks_full[0]))
 
 
@@ -198,7 +199,7 @@ def expand_symmetric(geom: Geometry, s: BlockSet) -> BlockSet:
                "qm_gather_blocks_t")
     out = BlockSet(keys[order].contiguous(), blocks, s.sumsq[src].contiguous())
     if s.masks is not None:  # copies swap row / column supports
-        m = torch.cat([s.masks, s.masks[[1, 0]][:, idx]], dim=1)
+        m = torch.cat([s.masks, s.masks[[1, 0, 2]][:, idx]], dim=1)
         both = s.masks_full[0] and s.masks_full[1]
         out.masks, out.masks_full = m[:, order].contiguous(), (both, both)
     return out

@@ -105,9 +105,10 @@ def decay_sparse(n: int, seed: int, width=None, scale: float = 4.0) -> np.ndarra
     return np.exp(-dist / scale) * (dist <= width) * rng.standard_normal((n, n))
 
 
-def support_masks_np(blocks: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
-    """numpy statement of qm_block_masks: bit r (r*64//bs above 64) of the row / column mask is set
-    when that row / column of the block holds a nonzero; a NaN/Inf block gets full masks."""
+def support_masks_np(blocks: np.ndarray, with_flags: bool = False):
+    """numpy statement of qm_block_meta's masks: bit r (r*64//bs above 64) of the row / column mask
+    is set when that row / column of the block holds a nonzero; a NaN/Inf block gets full masks
+    (bs bits, or all 64 from bs 64 up) and flag bit 0."""
     n, bs, _ = blocks.shape
     nz = blocks != 0
     bit = np.arange(bs) if bs <= 64 else (np.arange(bs) * 64) // bs
@@ -115,8 +116,12 @@ def support_masks_np(blocks: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
     rows = np.bitwise_or.reduce(np.where(nz.any(axis=2), w[None, :], np.uint64(0)), axis=1)
     cols = np.bitwise_or.reduce(np.where(nz.any(axis=1), w[None, :], np.uint64(0)), axis=1)
     bad = ~np.isfinite(blocks).all(axis=(1, 2))
-    full = np.uint64(0xFFFFFFFFFFFFFFFF)
-    return np.where(bad, full, rows).astype(np.uint64), np.where(bad, full, cols).astype(np.uint64)
+    full = np.uint64(0xFFFFFFFFFFFFFFFF if bs >= 64 else (1 << bs) - 1)
+    r = np.where(bad, full, rows).astype(np.uint64)
+    c = np.where(bad, full, cols).astype(np.uint64)
+    if with_flags:
+        return r, c, bad.astype(np.uint64)
+    return r, c
 
 
 def banded_support_decay(n: int, bw: int, seed: int) -> np.ndarray:

@@ -32,7 +32,7 @@ def test_exports_every_header_symbol():
 
 def test_abi_version_and_host_queries():
     lib = _ffi.load()
-    assert lib.qm_abi_version() == 1
+    assert lib.qm_abi_version() == _ffi.ABI_VERSION == 2
     lay = _ffi.make_layout(MatrixParams.create(4096, 64), 64)
     assert lib.qm_spgemm_workspace_bytes(ctypes.byref(lay), 556, 556) > 0
     assert lib.qm_compact_workspace_bytes(1016) > 0

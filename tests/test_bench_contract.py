@@ -27,6 +27,16 @@ def test_reference_arm_contract():
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["value"] > 0
     assert line["config"]["workload"] == "C1"
+    assert line["config"]["triples_structural"] == 4884 and line["config"]["nnzb_c_structural"] == 1016
+    assert line["sampling"]["c_block_rows"] >= 1
+
+
+def test_default_workload_is_the_largest_single_gpu_config():
+    """The driver's N=1 line is quoted on C5-64 (BASELINE configs[4]: the largest configuration that
+    fits one B200), and N > 1 runs strong-scale it."""
+    import bench
+
+    assert bench.DEFAULT_CONFIG == "C5-64"
 
 
 @pytest.mark.gpu
@@ -41,5 +51,9 @@ def test_gpu_arm_contract():
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
     p = line["e2e"]["pcie"]  # the box's pinned-copy floor next to the e2e number
     assert p["bidir_gbs"] > 0 and 0 < p["frac_of_floor"] <= 1.2
-    assert line["config"]["triples"] == line["config"]["triples_structural"]  # dense blocks: nothing skipped
+    assert line["result"]["triples_executed"] == line["config"]["triples_structural"]  # dense blocks: nothing skipped
+    assert line["operand_metadata"]["kernel"] == "k_block_meta"
+    ref = _run(["--impl", "reference", "--config", "C2-16384", "--steps", "1", "--warmup", "0",
+                "--cpu-target-s", "1"])
+    assert ref["config"] == line["config"]  # both arms print the same workload definition
     assert line["cpu_baseline"]["value"] > 0 and line["cpu_baseline"]["kind"] == "port"

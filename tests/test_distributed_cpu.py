@@ -49,8 +49,7 @@ class OracleBackend:
 
     def numeric(self, layout, pa, pb, tri, c_tptr, c_keys):
         t = tri.view(-1, 2).numpy().astype(np.int64)
-        glob_a = pa.keys.numpy()[t[:, 0]]  # pool keys carry global A indices
-        _, k = self.og.decode(self.ka[glob_a])
+        _, k = self.og.decode(pa.keys.numpy()[t[:, 0]])  # pool keys are the blocks' quadtree keys
         kc, bc, _ = O.numeric(self.og, c_keys.numpy(), c_tptr.numpy(), t[:, 0], t[:, 1], k,
                               pa.blocks.numpy(), pb.blocks.numpy())
         return BlockSet(torch.from_numpy(kc), torch.from_numpy(bc), torch.from_numpy(np.einsum("nij,nij->n", bc, bc)))

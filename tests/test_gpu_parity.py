@@ -711,10 +711,30 @@ def test_block_support_masks_match_numpy(ses, bs):
     blocks[6, 1, 2] = np.inf
     blocks[7, bs - 1, :] = 1.0
     bset = BlockSet.from_numpy(np.arange(40), blocks, None, ses.device)
+    sumsq_stats = bset.sumsq.clone()
     m = bset.support_masks().cpu().numpy().view(np.uint64)
-    want_r, want_c = helpers.support_masks_np(blocks)
+    want_r, want_c, want_f = helpers.support_masks_np(blocks, with_flags=True)
     np.testing.assert_array_equal(m[0], want_r)
     np.testing.assert_array_equal(m[1], want_c)
+    np.testing.assert_array_equal(m[2], want_f)
+    assert bset.masks_full == (False, False)
+    # qm_block_meta: norms + masks in one pass; its sums of squares are bit-identical to
+    # qm_block_stats' (the order every fused statistics pass reproduces)
+    lib = _ffi.load()
+    st = torch.empty(40, dtype=torch.float64, device=ses.device)
+    ref = torch.empty(40, dtype=torch.float64, device=ses.device)
+    mm = torch.empty((3, 40), dtype=torch.int64, device=ses.device)
+    nf = torch.zeros(2, dtype=torch.int64, device=ses.device)
+    _ffi.check(lib.qm_block_meta(bs, 40, _ffi.ptr(bset.blocks), _ffi.ptr(st), 0, 0, _ffi.ptr(mm), _ffi.ptr(nf), 0),
+               "qm_block_meta")
+    _ffi.check(lib.qm_block_stats(bs, 40, _ffi.ptr(bset.blocks), _ffi.ptr(ref), 0, 0), "qm_block_stats")
+    torch.cuda.synchronize()
+    assert torch.equal(mm, bset.masks)
+    assert torch.equal(st.view(torch.int64), ref.view(torch.int64))
+    assert nf.cpu().tolist() == [1, 1]
+    dense = np.ones((4, bs, bs))
+    full = BlockSet.from_numpy(np.arange(4), dense, None, ses.device).compute_meta()
+    assert full.masks_full == (True, True)
 
 
 @pytest.mark.parametrize("n,bw,leaf,bs", [(1024, 20, 64, 64), (768, 10, 32, 32), (512, 5, 128, 16),
@@ -771,6 +791,31 @@ def test_support_filter_keeps_nan_inf_products(ses):
         want = da[:bs, :bs] @ db[:bs, :bs]  # the only stored pair of blocks
     assert np.array_equal(c[:bs, :bs], want, equal_nan=True)
     assert np.isnan(c[0, 0]) and not c[bs:].any() and not c[:, bs:].any()
+
+
+@pytest.mark.parametrize("bs", [32, 64, 128])
+def test_panel_skip_keeps_nan_inf_products(ses, bs):
+    """The masked TMA kernels (Tma32k16 / Tma64k16 / Tma128) skip k panels where A's columns and B's
+    rows do not meet -- but never for a block holding NaN/Inf (masks' flags row): A(0,0)'s only
+    nonzero column is 5 (first panel), B(0,0)'s row 5 is nonzero and its Inf sits in row bs-7, the
+    last panel, where A(0,0) is zero: 0 * Inf = NaN must reach C like numpy's dgemm.
+    Other blocks have partial supports, so the filters are active."""
+    n = 2 * bs
+    da, db = np.zeros((n, n)), np.zeros((n, n))
+    da[:bs, 5] = 1.0
+    da[:bs, bs + 3] = 2.0                   # A(0,1): column 3 only
+    da[bs + 1, bs:] = 1.0                   # A(1,1): row 1 only
+    db[5, :bs] = 1.0
+    db[bs - 7, 0] = np.inf                  # B(0,0)
+    db[bs + 3, 2] = 3.0                     # B(1,0): row 3 only
+    db[bs + 9, bs + 4] = -1.0               # B(1,1): row 9 only (A(0,1)'s column 3 misses it)
+    a, b = helpers.build(ses, da, bs, bs), helpers.build(ses, db, bs, bs)
+    c = ses.to_dense(ses.multiply(a, b))
+    assert ses.last_multiply.n_triples == 4  # of 5 structural: A(0,1)*B(1,1) filtered, masks in use
+    with np.errstate(invalid="ignore"):
+        want = da @ db
+    assert np.array_equal(c, want, equal_nan=True)
+    assert np.isnan(c[:bs, 0]).all()
 
 
 @pytest.mark.parametrize("bs,leaf", [(64, 64), (32, 64), (128, 128), (64, 128)])
