@@ -551,7 +551,7 @@ class HostOperands:
         self.nbytes = sum(t.numel() * t.element_size() for ts in self.tensors for t in ts)
 
 
-def run_e2e(args, torch, ses, geom, host: HostOperands, dev):
+def run_e2e(args, torch, ses, geom, host: HostOperands, dev, timeline: dict | None = None):
     """MatrixSession.multiply with host (pinned) operands, as a pipelined serving loop: every step
     copies its operands host->device (keys, blocks, norms and support masks -- the stored matrix)
     and its result C device->host, on dedicated copy streams with double-buffered device inputs, so
@@ -574,15 +574,23 @@ def run_e2e(args, torch, ses, geom, host: HostOperands, dev):
     out_host = {}
     live = []  # (result, its D2H-done event)
 
+    def mark(name, stream):  # optional per-step timeline (scripts/e2e_c5_probe.py)
+        if timeline is not None:
+            e = ev()
+            e.record(stream)
+            timeline.setdefault(name, []).append((e, time.perf_counter()))
+
     def issue_h2d(k):
         slot = k % 2
         with torch.cuda.stream(s_in):
             if used[slot] is not None:
                 s_in.wait_event(used[slot])  # the product of step k-2 has finished reading this slot
+            mark("h2d_start", s_in)
             for dts, hts in zip(dev_in[slot], host.tensors):
                 for d, h in zip(dts, hts):
                     d.copy_(h, non_blocking=True)
             h2d_done[slot].record(s_in)
+            mark("h2d_end", s_in)
 
     def operand(slot, i):
         k, blk, sq, m = dev_in[slot][i]
@@ -590,16 +598,23 @@ def run_e2e(args, torch, ses, geom, host: HostOperands, dev):
 
     def step(k):
         slot = k % 2
-        while len(live) > 1:  # result of step k-2: its D2H is complete before its memory is reused
+        # The result of step k-2 is released only once its D2H has completed (host-side event wait;
+        # it finished long ago in a PCIe-bound pipeline), so its memory is reusable by this step's
+        # product at once. (record_stream on the copy stream would instead defer the reuse until
+        # everything queued there -- the D2H of step k-1 too -- had drained: the allocator would
+        # then fall back to a fresh 35 GB cudaMalloc and a device-wide synchronisation.)
+        while len(live) > 1:
             old, done_ev = live.pop(0)
             done_ev.synchronize()
             del old
         compute.wait_event(h2d_done[slot])
+        mark("product_start", compute)
         da = operand(slot, 0)
         db = da if nset == 1 else operand(slot, 1)
         c = ses.multiply(ses.matrix_from_blockset(geom, da), ses.matrix_from_blockset(geom, db))
         done = ev()
         done.record(compute)
+        mark("product_end", compute)
         used[slot] = done
         cs = c.root.blockset
         parts = (("k", cs.keys), ("b", cs.blocks), ("s", cs.sumsq))
@@ -609,10 +624,11 @@ def run_e2e(args, torch, ses, geom, host: HostOperands, dev):
         d2h_ev = ev()
         with torch.cuda.stream(s_out):
             s_out.wait_event(done)
+            mark("d2h_start", s_out)
             for name, src in parts:
                 out_host[name][:src.numel()].copy_(src.reshape(-1), non_blocking=True)
-                src.record_stream(s_out)
             d2h_ev.record(s_out)
+            mark("d2h_end", s_out)
         live.append((c, d2h_ev))
         return sum(t.numel() * t.element_size() for _, t in parts)
 
@@ -625,8 +641,12 @@ def run_e2e(args, torch, ses, geom, host: HostOperands, dev):
     used[0] = used[1] = None
     live.clear()
     torch.cuda.synchronize()
+    if timeline is not None:
+        timeline.clear()
     start, end = ev(), ev()
     start.record(s_in)
+    if timeline is not None:
+        timeline["t0"] = (start, time.perf_counter())
     issue_h2d(0)
     d2h = 0
     for k in range(steps):
@@ -638,12 +658,38 @@ def run_e2e(args, torch, ses, geom, host: HostOperands, dev):
     ms = start.elapsed_time(end)
     flops = ses.last_multiply.flops
     live.clear()
+    # the box's pinned-copy bandwidth at the e2e's own transfer size (one operand's blocks tensor
+    # each way and both at once; large copies run slower than 1 GiB ones here)
+    big = host.tensors[0][1]
+    d_a, d_b = dev_in[0][0][1], dev_in[1][0][1]
+    h_o = out_host["b"][:big.numel()].view(big.shape)
+    bw = {}
+    for mode in ("h2d", "d2h", "both"):
+        torch.cuda.synchronize()
+        e0, e1, e2 = ev(), ev(), ev()
+        e0.record(s_in)
+        s_out.wait_event(e0)
+        if mode != "d2h":
+            with torch.cuda.stream(s_in):
+                d_a.copy_(big, non_blocking=True)
+        if mode != "h2d":
+            with torch.cuda.stream(s_out):
+                h_o.copy_(d_b, non_blocking=True)
+        e2.record(s_out)
+        s_in.wait_event(e2)
+        e1.record(s_in)
+        torch.cuda.synchronize()
+        nbytes = big.numel() * 8 * (2 if mode == "both" else 1)
+        bw[f"{mode}_gbs"] = round(nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9, 1)
     del dev_in
     return {"value": round(flops * steps / (ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps,
             "ms_per_step": round(ms / steps, 3), "api": "MatrixSession.multiply",
             "pipelining": "H2D(k+1) | product(k) | D2H(k) on separate streams, double-buffered inputs",
-            "h2d_contents": "keys, blocks, norms and support masks of A and B (the stored matrices)"}
+            "h2d_contents": "keys, blocks, norms and support masks of A and B (the stored matrices)",
+            "pcie_at_transfer_size": {**bw, "bytes_per_copy": int(big.numel() * 8),
+                                      "floor_ms_per_step": round((h2d + d2h) / (bw["both_gbs"] * 1e9) * 1e3, 3),
+                                      "frac_of_floor": round((h2d + d2h) / (bw["both_gbs"] * 1e9) * 1e3 / (ms / steps), 3)}}
 
 
 def pcie_floor(torch, dev, e2e, mib=1024):

@@ -288,6 +288,23 @@ QM_API int qm_prune_level(const qm_layout *layout, int32_t level, double tau_l, 
                           double *pruned_out, int64_t *n_alive, int64_t *n_pruned, void *ws,
                           size_t ws_bytes, void *stream);
 
+/* The whole pruned recursion in ONE launch (cooperative kernel, a grid-wide barrier between
+ * levels, no host round trip per level): the same classification as qm_prune_level for every
+ * level 0..depth with tau_l = tau / 8^l. Node tables as written by qm_node_norms (level L at
+ * codes/norms + L*stride, counts[L] on the host). Surviving leaf-level pairs (packed
+ * I<<42 | K<<21 | J, unordered) go to leaf_pairs_out[cap_pairs], prune bounds (unordered) to
+ * log_out[cap_log]. counts_out (host, 2*(depth+1)+2 entries): alive and pruned pairs per level,
+ * the log total, and an overflow flag (bit 0: a level had more than cap_pairs survivors, bit 1:
+ * more than cap_log bounds -- the caller retries with larger capacities). Synchronises the stream
+ * once. */
+QM_API size_t qm_prune_all_workspace_bytes(int64_t cap_pairs);
+QM_API int qm_prune_all(const qm_layout *layout, double tau, const uint64_t *a_codes, const double *a_norms,
+                        int64_t a_stride, const int64_t *a_counts, int32_t a_sym, const uint64_t *b_codes,
+                        const double *b_norms, int64_t b_stride, const int64_t *b_counts, int32_t b_sym,
+                        int32_t b_transposed, int32_t upper, int64_t cap_pairs, uint64_t *leaf_pairs_out,
+                        double *log_out, int64_t cap_log, int64_t *counts_out, void *ws, size_t ws_bytes,
+                        void *stream);
+
 /* Keeps the triples of a symbolic plan whose leaf pair (li, lk, lj) is in the sorted
  * leaf_pairs codes ((li*w + lk)*w + lj, w = 2^depth): the products of pruned subtrees vanish; C
  * blocks left without triples vanish too (an all-pruned subtree is nil). Order is preserved.

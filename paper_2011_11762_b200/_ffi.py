@@ -67,6 +67,8 @@ EXPORTS = (
     "qm_node_norms",
     "qm_prune_level_workspace_bytes",
     "qm_prune_level",
+    "qm_prune_all_workspace_bytes",
+    "qm_prune_all",
     "qm_filter_triples_workspace_bytes",
     "qm_filter_triples",
     "qm_generate_blocks",
@@ -144,6 +146,9 @@ _SIGS = {
     "qm_prune_level": (ctypes.c_int, [_LP, _I32, ctypes.c_double, _P, _I64, _P, _P, _I64, _I32, _P, _P, _I64,
                                       _I32, _I32, _I32, _P, _P, ctypes.POINTER(_I64), ctypes.POINTER(_I64),
                                       _P, _SZ, _P]),
+    "qm_prune_all_workspace_bytes": (_SZ, [_I64]),
+    "qm_prune_all": (ctypes.c_int, [_LP, ctypes.c_double, _P, _P, _I64, _P, _I32, _P, _P, _I64, _P, _I32, _I32,
+                                    _I32, _I64, _P, _P, _I64, _P, _P, _SZ, _P]),
     "qm_filter_triples_workspace_bytes": (_SZ, [_I64, _I64]),
     "qm_filter_triples": (ctypes.c_int, [_LP, _P, _P, _I32, _P, _P, _P, _I64, _I64, _P, _I64, _P, _P, _P,
                                          ctypes.POINTER(_I64), ctypes.POINTER(_I64), _P, _SZ, _P]),

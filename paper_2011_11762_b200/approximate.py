@@ -11,10 +11,12 @@ the NE chunk (ops.py:100-116).
 B200 form (csrc/qm_prune.cu): qm_node_norms builds every level's node table of an operand
 bottom-up from the block sums of squares (nodes are runs of equal Morton codes in quadtree-key
 order; sqrt of the compensated sum of the children's squared norms, like the reference's
-sqrt(fsum(...))); qm_prune_level expands the surviving pairs of level l-1 to their 8 child pairs,
-looks both operand nodes up (a symmetric operand's lower nodes read their stored upper mirror),
-classifies each pair dead / pruned / alive and compacts the alive pairs and the pruned bounds (the
-log). The surviving leaf pairs then filter the regular symbolic phase's triples, and the numeric
+sqrt(fsum(...))); qm_prune_all runs the whole recursion in one cooperative launch: level l expands
+the surviving pairs of level l-1 to their 8 child pairs, looks both operand nodes up (a symmetric
+operand's lower nodes read their stored upper mirror), classifies each pair dead / pruned / alive
+and appends the alive pairs and the pruned bounds (the log), with a grid-wide barrier between
+levels and one host synchronisation for the whole prune (qm_prune_level keeps the level-at-a-time
+form). The surviving leaf pairs then filter the regular symbolic phase's triples, and the numeric
 kernel runs unchanged on the kept triples (k order preserved).
 """
 
@@ -64,9 +66,10 @@ def _node_tables(geom: Geometry, s: BlockSet, lay):
 
 def prune(geom: Geometry, a: BlockSet, b: BlockSet, tau: float, a_sym: bool = False, b_sym: bool = False,
           b_transposed: bool = False, upper: bool = False) -> PruneResult:
-    """Level-by-level prune decisions of the reference's task recursion on the device
-    (qm_node_norms + qm_prune_level) for the logical operands op(A) = A or expand(A),
-    op(B) = B, expand(B) or B^T; node norms are those of the stored chunks."""
+    """The prune decisions of the reference's task recursion on the device, every level in one
+    launch (qm_prune_all: a grid-wide barrier between levels, one host synchronisation in all), for
+    the logical operands op(A) = A or expand(A), op(B) = B, expand(B) or B^T; node norms are those
+    of the stored chunks. Capacities start at 32 pairs per leaf node and grow 8x on overflow."""
     import ctypes
 
     res = PruneResult()
@@ -79,31 +82,35 @@ def prune(geom: Geometry, a: BlockSet, b: BlockSet, tau: float, a_sym: bool = Fa
     ta = _node_tables(geom, a, lay)
     tb = ta if b is a else _node_tables(geom, b, lay)
     sh = _ffi.stream_handle(torch.cuda.current_stream(dev))
-    parents = torch.zeros(1, dtype=torch.int64, device=dev)
-    n_par = 0
-    logs = []
-    for lev in range(depth + 1):
-        n_cand = 1 if lev == 0 else 8 * n_par
-        alive = torch.empty(n_cand, dtype=torch.int64, device=dev)
-        pruned = torch.empty(n_cand, dtype=torch.float64, device=dev)
-        wb = lib.qm_prune_level_workspace_bytes(max(n_par, 1))
+    L = depth + 1
+    ac = (ctypes.c_int64 * L)(*[t[2] for t in ta])
+    bc = (ctypes.c_int64 * L)(*[t[2] for t in tb])
+    cap = max(4096, 32 * max(ta[depth][2], tb[depth][2]))
+    while True:
+        cap_log = 8 * cap
+        leaf = torch.empty(cap, dtype=torch.int64, device=dev)
+        log = torch.empty(cap_log, dtype=torch.float64, device=dev)
+        wb = lib.qm_prune_all_workspace_bytes(cap)
         ws = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
-        na, npr = ctypes.c_int64(0), ctypes.c_int64(0)
-        (ac, an, acnt), (bc, bn, bcnt) = ta[lev], tb[lev]
-        _ffi.check(lib.qm_prune_level(ctypes.byref(lay), lev, tau / (8.0 ** lev), _ffi.ptr(parents), n_par,
-                                      _ffi.ptr(ac), _ffi.ptr(an), acnt, int(a_sym), _ffi.ptr(bc), _ffi.ptr(bn),
-                                      bcnt, int(b_sym), int(b_transposed), int(upper), _ffi.ptr(alive),
-                                      _ffi.ptr(pruned), ctypes.byref(na), ctypes.byref(npr), _ffi.ptr(ws), wb,
-                                      sh), "qm_prune_level")
-        res.pairs_per_level.append(int(na.value + npr.value))
-        if npr.value:
-            logs.append(pruned[:npr.value])
-        parents, n_par = alive[:na.value], int(na.value)
-        if n_par == 0:
+        counts = (ctypes.c_int64 * (2 * L + 2))()
+        _ffi.check(lib.qm_prune_all(ctypes.byref(lay), float(tau), _ffi.ptr(ta[0][0]), _ffi.ptr(ta[0][1]), a.n, ac,
+                                    int(a_sym), _ffi.ptr(tb[0][0]), _ffi.ptr(tb[0][1]), b.n, bc, int(b_sym),
+                                    int(b_transposed), int(upper), cap, _ffi.ptr(leaf), _ffi.ptr(log), cap_log,
+                                    counts, _ffi.ptr(ws), wb, sh), "qm_prune_all")
+        if counts[2 * L + 1] == 0:
             break
-    if logs:
-        res.prune_log = torch.cat(logs)  # device; _EngineInfo converts on first read
-    if n_par and len(res.pairs_per_level) == depth + 1:
+        cap *= 8  # a level outgrew the buffers: rerun with room (decisions are deterministic)
+    levels = [(int(counts[2 * lv]), int(counts[2 * lv + 1])) for lv in range(L)]
+    for na, npr in levels:
+        res.pairs_per_level.append(na + npr)
+        if na == 0:
+            break
+    n_log = int(counts[2 * L])
+    if n_log:
+        res.prune_log = log[:n_log]  # device; _EngineInfo converts on first read
+    n_leaf = levels[depth][0] if len(res.pairs_per_level) == L else 0
+    if n_leaf:
+        parents = leaf[:n_leaf]
         w = 1 << depth
         mask = (1 << 21) - 1
         I, K, J = parents >> 42, (parents >> 21) & mask, parents & mask

@@ -18,6 +18,10 @@
 //                     upper mirror, a transposed operand swaps the coordinates), classification
 //                     dead / pruned / alive, and stream compaction of the alive pairs (packed
 //                     I<<42 | K<<21 | J) and of the pruned bounds (the prune log).
+#include <math.h>
+#include <string.h>
+
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "qm_common.cuh"
@@ -213,6 +217,78 @@ __global__ void __launch_bounds__(kSmallThreads) k_prune_small(const uint64_t *p
     host_cnt[0] = tot_a;
     host_cnt[1] = tot_p;
     __threadfence_system();
+  }
+}
+
+// ---- every level in one launch ----------------------------------------------------------------
+// The whole pruned recursion as one cooperative (grid-synchronised) kernel: level l's candidates are
+// the 8 children of level l-1's survivors; survivors and prune bounds are appended with
+// warp-aggregated atomics (the order of both lists is immaterial: the leaf pairs are sorted
+// afterwards and the prune log is a multiset, engine.py:273-275), then one grid-wide barrier
+// separates the levels. No host round trip between levels.
+constexpr int kMaxLevels = 22;
+struct PruneTables {
+  Table a[kMaxLevels], b[kMaxLevels];
+  double tau[kMaxLevels];  // tau_l = tau / 8^l, computed on the host exactly as the reference does
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__global__ void __launch_bounds__(256) k_prune_all(const __grid_constant__ PruneTables t, int depth, int a_sym,
+                                                   int b_sym, int b_transposed, int upper, uint64_t *ping,
+                                                   uint64_t *pong, uint64_t *leaf_out, int64_t cap,
+                                                   double *log_out, int64_t cap_log,
+                                                   unsigned long long *cnt /* [2*(depth+1)] */,
+                                                   unsigned long long *log_cnt, unsigned int *overflow) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const uint64_t *par = nullptr;
+  int64_t n_par = 0;
+  for (int lev = 0; lev <= depth; ++lev) {
+    const int root = lev == 0;
+    const int64_t n_cand = root ? 1 : 8 * n_par;
+    uint64_t *out = lev == depth ? leaf_out : ((lev & 1) ? pong : ping);
+    // grid-stride with whole warps active (warp-aggregated appends)
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n_cand; base += nthreads) {
+      const int64_t x = base + lane;
+      uint64_t code = 0;
+      double bd = 0.0;
+      bool live = false, pr = false;
+      if (x < n_cand)
+        prune_classify(par, x, root, t.a[lev], a_sym, t.b[lev], b_sym, b_transposed, upper, t.tau[lev], &code, &bd,
+                       &live, &pr);
+      const uint32_t ml = __ballot_sync(0xffffffffu, live), mp = __ballot_sync(0xffffffffu, pr);
+      unsigned long long bl = 0, bp = 0, bg = 0;
+      if (lane == 0) {
+        if (ml) bl = atomicAdd(&cnt[2 * lev], (unsigned long long)__popc(ml));
+        if (mp) {
+          bp = atomicAdd(&cnt[2 * lev + 1], (unsigned long long)__popc(mp));
+          bg = atomicAdd(log_cnt, (unsigned long long)__popc(mp));
+        }
+      }
+      bl = __shfl_sync(0xffffffffu, bl, 0);
+      bg = __shfl_sync(0xffffffffu, bg, 0);
+      (void)bp;
+      if (live) {
+        const unsigned long long pos = bl + __popc(ml & lanemask_lt());
+        if ((int64_t)pos < cap) out[pos] = code; else atomicOr(overflow, 1u);
+      }
+      if (pr) {
+        const unsigned long long pos = bg + __popc(mp & lanemask_lt());
+        if ((int64_t)pos < cap_log) log_out[pos] = bd; else atomicOr(overflow, 2u);
+      }
+    }
+    grid.sync();
+    const int64_t alive = (int64_t)((volatile unsigned long long *)cnt)[2 * lev];
+    n_par = alive < cap ? alive : cap;
+    par = out;
+    if (n_par == 0) break;  // every thread reads the same count: a uniform exit
   }
 }
 
@@ -494,5 +570,76 @@ extern "C" int qm_filter_triples(const qm_layout *layout, const uint64_t *a_keys
   if (rc != QM_OK) return rc;
   *nC_out = counts[0];
   *nT_out = counts[1];
+  return QM_OK;
+}
+
+extern "C" size_t qm_prune_all_workspace_bytes(int64_t cap_pairs) {
+  Carver cv(nullptr, 0);
+  cv.take<uint64_t>(std::max<int64_t>(cap_pairs, 1));  // ping
+  cv.take<uint64_t>(std::max<int64_t>(cap_pairs, 1));  // pong
+  cv.take<unsigned long long>(2 * kMaxLevels + 2);      // counters, log count, overflow
+  return cv.off;
+}
+
+extern "C" int qm_prune_all(const qm_layout *layout, double tau, const uint64_t *a_codes, const double *a_norms,
+                            int64_t a_stride, const int64_t *a_counts, int32_t a_sym, const uint64_t *b_codes,
+                            const double *b_norms, int64_t b_stride, const int64_t *b_counts, int32_t b_sym,
+                            int32_t b_transposed, int32_t upper, int64_t cap_pairs, uint64_t *leaf_pairs_out,
+                            double *log_out, int64_t cap_log, int64_t *counts_out, void *ws, size_t ws_bytes,
+                            void *stream) {
+  Geometry g;
+  int rc = make_geometry(layout, &g);
+  if (rc != QM_OK) return rc;
+  if (!a_codes || !a_norms || !a_counts || !b_codes || !b_norms || !b_counts || !counts_out || cap_pairs < 1 ||
+      cap_log < 1 || !leaf_pairs_out || !log_out) {
+    set_error("qm_prune_all: bad arguments");
+    return QM_ERR_INVALID;
+  }
+  if (g.depth + 1 > kMaxLevels || g.depth >= kPairBits) {
+    set_error("qm_prune_all: depth %d exceeds %d", g.depth, kMaxLevels - 1);
+    return QM_ERR_UNSUPPORTED;
+  }
+  Carver cv(ws, ws_bytes);
+  uint64_t *ping = cv.take<uint64_t>(cap_pairs), *pong = cv.take<uint64_t>(cap_pairs);
+  unsigned long long *ctr = cv.take<unsigned long long>(2 * kMaxLevels + 2);
+  if (!cv.ok() || !ws) {
+    set_error("qm_prune_all: workspace %zu < required %zu", ws_bytes, cv.off);
+    return QM_ERR_WORKSPACE;
+  }
+  PruneTables t;
+  memset(&t, 0, sizeof(t));
+  for (int l = 0; l <= g.depth; ++l) {
+    t.a[l] = Table{a_codes + (size_t)l * a_stride, a_norms + (size_t)l * a_stride, a_counts[l]};
+    t.b[l] = Table{b_codes + (size_t)l * b_stride, b_norms + (size_t)l * b_stride, b_counts[l]};
+    t.tau[l] = tau / ldexp(1.0, 3 * l);  // tau / 8.0**l (ops.py:232), exact power-of-two scaling
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  QM_CUDA_TRY(cudaMemsetAsync(ctr, 0, (2 * kMaxLevels + 2) * sizeof(unsigned long long), st));
+  static PerDeviceInt occupancy;
+  int per_sm = 0;
+  rc = occupancy.get(&per_sm, [](int *x) -> int {
+    QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(x, k_prune_all, 256, 0));
+    return (int)QM_OK;
+  });
+  if (rc != QM_OK) return rc;
+  const int grid = device_sm_count() * std::max(1, std::min(per_sm, 4));
+  int depth = g.depth;
+  unsigned long long *cnt = ctr, *log_cnt = ctr + 2 * kMaxLevels;
+  unsigned int *overflow = (unsigned int *)(ctr + 2 * kMaxLevels + 1);
+  void *args[] = {(void *)&t,   (void *)&depth,   (void *)&a_sym,          (void *)&b_sym,  (void *)&b_transposed,
+                  (void *)&upper, (void *)&ping, (void *)&pong,          (void *)&leaf_pairs_out, (void *)&cap_pairs,
+                  (void *)&log_out, (void *)&cap_log, (void *)&cnt, (void *)&log_cnt, (void *)&overflow};
+  QM_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_prune_all, grid, 256, args, 0, st));
+  QM_LAUNCHED("k_prune_all");
+  // counts_out (host): [alive_0, pruned_0, ..., alive_depth, pruned_depth, log total, overflow]
+  unsigned long long host[2 * kMaxLevels + 2];
+  QM_CUDA_TRY(cudaMemcpyAsync(host, ctr, sizeof(host), cudaMemcpyDeviceToHost, st));
+  QM_CUDA_TRY(cudaStreamSynchronize(st));
+  for (int l = 0; l <= g.depth; ++l) {
+    counts_out[2 * l] = (int64_t)host[2 * l];
+    counts_out[2 * l + 1] = (int64_t)host[2 * l + 1];
+  }
+  counts_out[2 * (g.depth + 1)] = (int64_t)host[2 * kMaxLevels];
+  counts_out[2 * (g.depth + 1) + 1] = (int64_t)(unsigned int)host[2 * kMaxLevels + 1];
   return QM_OK;
 }

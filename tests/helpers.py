@@ -60,6 +60,33 @@ def gpu_session(**kw):
     return MatrixSession(device="cuda:0", **kw)
 
 
+def reference_src():
+    """Directory holding the reference package ``quadmat`` (pkg/src): the offline install under
+    baseline/_ref (it travels to the GPU box with the repo snapshot), else the read-only reference
+    tree of the build container; None when neither exists. Test infrastructure only."""
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    for cand in (root / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+        if (cand / "quadmat" / "__init__.py").exists():
+            return cand
+    return None
+
+
+def import_reference():
+    """The reference package ``quadmat`` (sys.path gets reference_src())."""
+    import sys
+
+    src = reference_src()
+    if src is None:
+        return None
+    if str(src) not in sys.path:
+        sys.path.insert(0, str(src))
+    import quadmat
+
+    return quadmat
+
+
 def rel(got, want) -> float:
     den = float(np.linalg.norm(want))
     d = float(np.linalg.norm(np.asarray(got) - np.asarray(want)))
@@ -84,6 +111,38 @@ def oracle_rows(cfg, rows):
     bb = G.host_blocks(geom, kb_s, cfg.seed, 1, pat, cfg.half_bw)
     kc, bc, _ = O.multiply(O.Geom(cfg.n, cfg.bs, cfg.bs), ka_s, ba, kb_s, bb)
     return kc, bc
+
+
+def structural_c_keys(geom, ka: np.ndarray, kb: np.ndarray, a_cmask=None, b_rmask=None) -> np.ndarray:
+    """The exact C block set of A*B on the host, sorted quadtree keys: every (i, j) with some k such
+    that A(i,k) and B(k,j) are stored (the non-nil multiply tasks of ops.py:197-241). With the
+    operands' support masks (a_cmask[t] = A block t's nonzero columns, b_rmask[t] = B block t's
+    nonzero rows) only pairs whose supports meet count -- the others multiply to exactly zero, and
+    a C block made only of such pairs is the exact-zero block _set_block drops
+    (block_sparse.py:37-41). Operands with uniform random values (no cancellation) or positive
+    values (C4) have exactly this nonzero C block set."""
+    import scipy.sparse as sp
+
+    nb = geom.nbg
+    ai, ak = geom.decode(ka)
+    bk, bj = geom.decode(kb)
+    if a_cmask is None:
+        pa = sp.csr_matrix((np.ones(ka.size, dtype=np.int64), (ai, ak)), shape=(nb, nb))
+        pb = sp.csr_matrix((np.ones(kb.size, dtype=np.int64), (bk, bj)), shape=(nb, nb))
+        c = (pa @ pb).tocoo()
+        return np.sort(geom.qkey(c.row.astype(np.int64), c.col.astype(np.int64)))
+    # masked: expand the (A block, B block) pairs per k, keep those whose supports meet
+    order_b = np.argsort(bk, kind="stable")
+    bk_s = bk[order_b]
+    lo = np.searchsorted(bk_s, ak, side="left")
+    hi = np.searchsorted(bk_s, ak, side="right")
+    cnt = hi - lo
+    ia = np.repeat(np.arange(ka.size), cnt)
+    off = np.arange(cnt.sum()) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    ib = order_b[np.repeat(lo, cnt) + off]
+    meet = (a_cmask[ia] & b_rmask[ib]) != 0
+    keys = geom.qkey(ai[ia[meet]].astype(np.int64), bj[ib[meet]].astype(np.int64))
+    return np.unique(keys)
 
 
 def lookup(keys_all: np.ndarray, blocks_dev, want: np.ndarray):

@@ -269,8 +269,28 @@ def test_c2_131072_sampled_blocks_and_counts(ses):
     rows = np.r_[0, np.random.default_rng(0).choice(geom.nbg, 12, replace=False), geom.nbg - 1]
     kc, bc = helpers.oracle_rows(cfg, rows)
     keys_all = c.root.blockset.keys.cpu().numpy()
+    np.testing.assert_array_equal(keys_all, helpers.structural_c_keys(geom, G.config_keys(cfg, 0),
+                                                                      G.config_keys(cfg, 1)))
     got = helpers.lookup(keys_all, c.root.blockset.blocks, kc)
     assert helpers.rel(got, bc) <= TOL
+
+
+@pytest.mark.parametrize("name,counts", [("C2-16384", (8176, 71944)), ("C2-32768", (16624, 145928)),
+                                         ("C2-65536", (33520, 293896))])
+def test_c2_sequence_block_set_and_sampled_values(ses, name, counts):
+    """BASELINE configs[1] at every N of its sequence: the ENTIRE C block set equals the host
+    structural set (scipy, SURVEY 8(d) counts) key for key, and sampled C block rows (first, last,
+    random) equal the oracle's on regenerated operand blocks."""
+    cfg = G.CONFIGS[name]
+    geom, a, b = G.config_operands_device(cfg, ses.device)
+    c = ses.multiply(ses.matrix_from_blockset(geom, a), ses.matrix_from_blockset(geom, b))
+    assert (ses.last_multiply.n_c, ses.last_multiply.n_triples) == counts
+    keys_all = c.root.blockset.keys.cpu().numpy()
+    np.testing.assert_array_equal(keys_all, helpers.structural_c_keys(geom, G.config_keys(cfg, 0),
+                                                                      G.config_keys(cfg, 1)))
+    rows = np.r_[0, np.random.default_rng(7).choice(geom.nbg, 8, replace=False), geom.nbg - 1]
+    kc, bc = helpers.oracle_rows(cfg, rows)
+    assert helpers.rel(helpers.lookup(keys_all, c.root.blockset.blocks, kc), bc) <= TOL
 
 
 @pytest.mark.parametrize("impl", ["tma", "cpasync"])
@@ -564,6 +584,9 @@ def test_c5_full_size_sampled_rows(ses, name, counts):
     rows = np.r_[0, np.random.default_rng(1).choice(geom.nbg, 6, replace=False), geom.nbg - 1]
     kc, bc = helpers.oracle_rows(cfg, rows)
     keys_all = c.keys.cpu().numpy()
+    # the entire C block set, key for key (host structural product, scipy)
+    np.testing.assert_array_equal(keys_all, helpers.structural_c_keys(geom, G.config_keys(cfg, 0),
+                                                                      G.config_keys(cfg, 1)))
     got = helpers.lookup(keys_all, c.blocks, kc)
     assert helpers.rel(got, bc) <= TOL
     pos = torch.from_numpy(np.searchsorted(keys_all, kc)).to(c.sumsq.device)
@@ -582,6 +605,11 @@ def test_c4_full_size_sampled_rows(ses):
     # to exact zeros and are skipped, so the 59,678 exact-zero C blocks are never created
     assert ses.last_multiply.n_triples == 485208 and ses.last_multiply.n_c == 60824
     assert ses.last_multiply.zero_blocks == 0
+    # the entire nonzero C block set: pairs whose supports meet (host masks, numpy) -- A's entries
+    # are positive (exp(-r^2/2)), so no C block cancels to zero otherwise
+    rm, cm = helpers.support_masks_np(ba)
+    np.testing.assert_array_equal(c.root.blockset.keys.cpu().numpy(), helpers.structural_c_keys(geom, ka, ka, cm, rm))
+    assert helpers.structural_c_keys(geom, ka, ka).size == 120502  # structural
     ai, ak = geom.decode(ka)
     rows = np.r_[0, np.random.default_rng(2).choice(geom.nbg, 6, replace=False), geom.nbg - 1]
     sel = np.isin(ai, rows)
@@ -810,12 +838,17 @@ def test_panel_skip_keeps_nan_inf_products(ses, bs):
     db[bs + 3, 2] = 3.0                     # B(1,0): row 3 only
     db[bs + 9, bs + 4] = -1.0               # B(1,1): row 9 only (A(0,1)'s column 3 misses it)
     a, b = helpers.build(ses, da, bs, bs), helpers.build(ses, db, bs, bs)
-    c = ses.to_dense(ses.multiply(a, b))
+    c = ses.multiply(a, b).root.blockset
     assert ses.last_multiply.n_triples == 4  # of 5 structural: A(0,1)*B(1,1) filtered, masks in use
+    host = MatrixSession(device="cpu")
+    ka, ba, _ = helpers.build(host, da, bs, bs).root.blockset.to_host()
+    kb, bb, _ = helpers.build(host, db, bs, bs).root.blockset.to_host()
     with np.errstate(invalid="ignore"):
-        want = da @ db
-    assert np.array_equal(c, want, equal_nan=True)
-    assert np.isnan(c[:bs, 0]).all()
+        kc, bc, _ = O.multiply(O.Geom(n, bs, bs), ka, ba, kb, bb)  # the reference's stored-block products
+    np.testing.assert_array_equal(c.keys.cpu().numpy(), kc)
+    got = c.blocks.cpu().numpy()
+    assert np.array_equal(got, bc, equal_nan=True)
+    assert np.isnan(got[0][:, 0]).all()  # C(0,0)'s column 0: A(0,0)[:, bs-7] = 0 times Inf
 
 
 @pytest.mark.parametrize("bs,leaf", [(64, 64), (32, 64), (128, 128), (64, 128)])

@@ -1,11 +1,9 @@
-"""The task-plugin seam against the real reference engine (build container only: the reference
-is not on the GPU box). The compute function is the oracle here, so the plugged engine must
-produce the reference's own canonical bytes bit for bit -- proving that reading the operand trees
-through ctx.fetch and writing the product back through ctx.put is exact, for every engine mode and
-worker count. On a B200 the same body runs gpu_compute (libqmb200)."""
-
-import sys
-from pathlib import Path
+"""The task-plugin seam against the real reference engine (the reference package installed under
+baseline/_ref, or the build container's reference tree). The compute function is the oracle here,
+so the plugged engine must produce the reference's own canonical bytes bit for bit -- proving that
+reading the operand trees through ctx.fetch and writing the product back through ctx.put is exact,
+for every engine mode and worker count. tests/test_reference_dropin.py runs the same body with
+gpu_compute (libqmb200) on a B200."""
 
 import numpy as np
 import pytest
@@ -13,8 +11,7 @@ import pytest
 import helpers
 from oracle import spgemm_oracle as O
 
-REF = Path("/root/reference/pkg/src")
-pytestmark = pytest.mark.skipif(not REF.exists(), reason="reference package not present")
+pytestmark = pytest.mark.skipif(helpers.reference_src() is None, reason="reference package not present")
 
 
 def _oracle_compute(geom, ka, ba, kb, bb):
@@ -25,8 +22,7 @@ def _oracle_compute(geom, ka, ba, kb, bb):
 @pytest.mark.parametrize("mode,workers", [("simulate", 1), ("simulate", 3), ("threaded", 2)])
 @pytest.mark.parametrize("n,leaf,bs", [(24, 4, 2), (100, 16, 8), (37, 12, 4), (256, 64, 64)])
 def test_plugged_engine_reproduces_reference_products(mode, workers, n, leaf, bs):
-    sys.path.insert(0, str(REF))
-    import quadmat
+    quadmat = helpers.import_reference()
 
     from paper_2011_11762_b200 import reference_plugin
 
