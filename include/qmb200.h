@@ -132,6 +132,20 @@ QM_API int qm_spgemm_count_masked(const qm_layout *layout, const uint64_t *a_key
                                   int64_t nA, const uint64_t *b_keys, const uint64_t *b_rmask, int64_t nB,
                                   int32_t flags, void *ws, size_t ws_bytes, int64_t *n_c_out,
                                   int64_t *n_triples_out, void *stream);
+/* The symbolic count of ONE rank of a multi-GPU product (the reference's per-worker task
+ * expansion: each worker only expands the tasks it owns, ops.py:197-241 / engine.py:286-300).
+ * A cheap global pass over the (all-gathered) structure counts the structural triples of every C
+ * tile -- an aligned quadtree subtree, 4^min(depth, 8) of them in Morton order -- at O(nA) cost;
+ * the tiles are cut into `world` contiguous ranges of nearly equal work, and this rank's C key range
+ * [part_out[0], part_out[1]) is a union of whole subtrees (the ranks' ranges tile the key space in
+ * rank order). Only C blocks inside the range are counted here and emitted by the fill calls of the
+ * same workspace (keys, offsets and triples local to the rank). part_out (host int64[3]): key range
+ * and the total tile work; key_cuts (device uint64[world+1], may be NULL): every rank's range bound.
+ * Support masks as in qm_spgemm_count_masked. Synchronises the stream once. */
+QM_API int qm_spgemm_count_part(const qm_layout *layout, const uint64_t *a_keys, const uint64_t *a_cmask,
+                                int64_t nA, const uint64_t *b_keys, const uint64_t *b_rmask, int64_t nB,
+                                int32_t world, int32_t rank, void *ws, size_t ws_bytes, int64_t *n_c_out,
+                                int64_t *n_triples_out, int64_t *part_out, uint64_t *key_cuts, void *stream);
 QM_API size_t qm_spgemm_fill_workspace_bytes(const qm_layout *layout, int64_t nC);
 /* Emits the C key set in quadtree-key order (c_keys[nC]), the triple offsets c_tptr[nC+1] and the
  * triples tri[2*nT] = (a_index, b_index) pairs, grouped by C block, k ascending within a group --

@@ -41,6 +41,7 @@ EXPORTS = (
     "qm_spgemm_workspace_bytes",
     "qm_spgemm_count",
     "qm_spgemm_count_masked",
+    "qm_spgemm_count_part",
     "qm_spgemm_fill_workspace_bytes",
     "qm_spgemm_fill",
     "qm_spgemm_fill_keys",
@@ -113,6 +114,9 @@ _SIGS = {
                                        ctypes.POINTER(_I64), _P]),
     "qm_spgemm_count_masked": (ctypes.c_int, [_LP, _P, _P, _I64, _P, _P, _I64, _I32, _P, _SZ,
                                              ctypes.POINTER(_I64), ctypes.POINTER(_I64), _P]),
+    "qm_spgemm_count_part": (ctypes.c_int, [_LP, _P, _P, _I64, _P, _P, _I64, _I32, _I32, _P, _SZ,
+                                            ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64), _P,
+                                            _P]),
     "qm_spgemm_fill_workspace_bytes": (_SZ, [_LP, _I64]),
     "qm_spgemm_fill": (ctypes.c_int, [_LP, _I64, _I64, _I64, _I64, _P, _SZ, _P, _SZ, _P, _P, _P, _P]),
     "qm_spgemm_fill_keys": (ctypes.c_int, [_LP, _I64, _I64, _I64, _P, _SZ, _P, _SZ, _P, _P, _P]),

@@ -185,6 +185,43 @@ __device__ __forceinline__ uint32_t lower_bound_col(const uint32_t *b_scol, uint
   return b0;
 }
 
+// Flags word of the symbolic workspace (k_cols_rowptr, k_tile_cut): bit 0 support masks given,
+// bit 1 upper variant, bit 2 key-ranged (a multi-GPU rank's own C key range in krange[0..1]).
+constexpr int kFlagMasked = 1, kFlagUpper = 2, kFlagRanged = 4;
+
+// Column interval [*jlo, *jhi) of block row i whose quadtree keys lie in [klo, khi): keys are
+// monotone in the column for a fixed row, so it is one interval (binary searches over j).
+__device__ __forceinline__ void row_key_cols(uint32_t i, uint64_t klo, uint64_t khi, int64_t nbg, int nbl,
+                                             int lbits, uint32_t *jlo, uint32_t *jhi) {
+  uint32_t lo = 0, hi = (uint32_t)nbg;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (qkey(i, mid, nbl, lbits) < klo) lo = mid + 1; else hi = mid;
+  }
+  *jlo = lo;
+  hi = (uint32_t)nbg;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (qkey(i, mid, nbl, lbits) < khi) lo = mid + 1; else hi = mid;
+  }
+  *jhi = lo;
+}
+
+// Applies the per-row column restrictions of the workspace flags to a row span: the upper variant
+// (leaves li <= lj) and a rank's key range. Returns false when the row has nothing left.
+__device__ __forceinline__ bool clamp_row(RowSpan &s, int64_t i, int flags, const uint64_t *krange, int64_t nbg,
+                                          int nbl, int lbits) {
+  if (flags & kFlagUpper) s.jmin = max(s.jmin, (uint32_t)((i / nbl) * nbl));
+  if (flags & kFlagRanged) {
+    uint32_t jlo, jhi;
+    row_key_cols((uint32_t)i, krange[0], krange[1], nbg, nbl, lbits, &jlo, &jhi);
+    s.jmin = max(s.jmin, jlo);
+    if (jhi == 0) return false;
+    s.jmax = min(s.jmax, jhi - 1u);
+  }
+  return s.nt > 0 && s.jmin <= s.jmax;
+}
+
 // Calls f(x, y, j) for every pair (A entry x of the row, B entry y of row k(x)) whose column j is
 // inside [wbase, wbase + kWin). Warps take A entries, lanes take B entries; no ordering.
 // Only pairs whose supports meet are visited: A(i,k)'s nonzero columns and B(k,j)'s nonzero rows
@@ -196,7 +233,7 @@ __device__ void for_window_pairs(const RowSpan &s, uint32_t wbase, bool multi, c
                                  const uint32_t *b_rp, const uint32_t *b_scol, const uint64_t *smask, bool masked,
                                  F f) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const uint32_t wend = wbase + kWin;
+  const uint32_t wend = min(wbase + (uint32_t)kWin, s.jmax + 1u);  // s.jmax: the row's (clamped) last column
   for (uint32_t x = s.a0 + warp; x < s.a1; x += nw) {
     uint32_t k = a_scol[x];
     const uint64_t am = masked ? smask[x] : ~0ull;
@@ -216,29 +253,30 @@ __device__ void for_window_pairs(const RowSpan &s, uint32_t wbase, bool multi, c
 // read-back.
 __global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const uint32_t *a_scol,
                                                    const uint32_t *b_rp, const uint32_t *b_scol,
-                                                   const uint64_t *smask, const int *masked_flag, int64_t nbg,
-                                                   int nbl, uint64_t *cnt, uint64_t *off, unsigned int *done,
+                                                   const uint64_t *smask, const int *masked_flag,
+                                                   const uint64_t *krange, int64_t nbg, int nbl, int lbits,
+                                                   uint64_t *cnt, uint64_t *off, unsigned int *done,
                                                    volatile int64_t *host_tot) {
   __shared__ uint32_t bm[kWin / 32];
   __shared__ uint64_t red64[32];
   __shared__ uint32_t red32[32];
   __shared__ bool last;
-  const bool masked = (*masked_flag & 1) != 0;
-  const bool upper = (*masked_flag & 2) != 0;  // only C blocks of leaves (li, lj) with li <= lj
+  const int flags = *masked_flag;
+  const bool masked = (flags & kFlagMasked) != 0;
+  const bool clamped = (flags & (kFlagUpper | kFlagRanged)) != 0;  // rows start past their first column
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt[2 * nbg] = 0;  // exclusive-scan tail
   for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
     RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
-    if (upper) s.jmin = max(s.jmin, (uint32_t)((i / nbl) * nbl));
     uint32_t total = 0;
     uint64_t ntri = 0;  // surviving triples of the row (<= s.nt, the structural count)
-    if (s.nt > 0) {
+    if (clamp_row(s, i, flags, krange, nbg, nbl, lbits)) {
       const bool multi = (s.jmax - s.jmin) >= (uint32_t)kWin;
       for (uint64_t wb = s.jmin; wb <= s.jmax; wb += kWin) {
         const uint32_t wbase = (uint32_t)wb;
         for (int w = threadIdx.x; w < kWin / 32; w += blockDim.x) bm[w] = 0u;
         __syncthreads();
         uint64_t mine = 0;
-        for_window_pairs(s, wbase, multi || upper, a_scol, b_rp, b_scol, smask, masked, [&](uint32_t, uint32_t, uint32_t j) {
+        for_window_pairs(s, wbase, multi || clamped, a_scol, b_rp, b_scol, smask, masked, [&](uint32_t, uint32_t, uint32_t j) {
           uint32_t o = j - wbase;
           atomicOr(&bm[o >> 5], 1u << (o & 31));
           ++mine;
@@ -273,27 +311,27 @@ __global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const u
 
 __global__ void __launch_bounds__(kNT) k_sym_emit_c(const uint32_t *a_rp, const uint32_t *a_scol,
                                                     const uint32_t *b_rp, const uint32_t *b_scol,
-                                                    const uint64_t *smask, const int *masked_flag, int64_t nbg,
-                                                    int nbl, int lbits,
+                                                    const uint64_t *smask, const int *masked_flag,
+                                                    const uint64_t *krange, int64_t nbg, int nbl, int lbits,
                                                     const uint64_t *rowC_off, uint64_t *rm_key,
                                                     uint32_t *rm_cnt, uint32_t *rm_iota, unsigned int *done) {
   __shared__ uint32_t cnt[kWin];
   __shared__ uint64_t red64[32];
   __shared__ uint32_t red32[32];
   if (blockIdx.x == 0 && threadIdx.x == 0) *done = 0u;  // k_inv_counts' completion ticket
-  const bool masked = (*masked_flag & 1) != 0;
-  const bool upper = (*masked_flag & 2) != 0;  // only C blocks of leaves (li, lj) with li <= lj
+  const int flags = *masked_flag;
+  const bool masked = (flags & kFlagMasked) != 0;
+  const bool clamped = (flags & (kFlagUpper | kFlagRanged)) != 0;
   for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
     RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
-    if (upper) s.jmin = max(s.jmin, (uint32_t)((i / nbl) * nbl));
-    if (s.nt > 0) {
+    if (clamp_row(s, i, flags, krange, nbg, nbl, lbits)) {
       uint64_t out = rowC_off[i];
       const bool multi = (s.jmax - s.jmin) >= (uint32_t)kWin;
       for (uint64_t wb = s.jmin; wb <= s.jmax; wb += kWin) {
         const uint32_t wbase = (uint32_t)wb;
         for (int w = threadIdx.x; w < kWin; w += blockDim.x) cnt[w] = 0u;
         __syncthreads();
-        for_window_pairs(s, wbase, multi || upper, a_scol, b_rp, b_scol, smask, masked,
+        for_window_pairs(s, wbase, multi || clamped, a_scol, b_rp, b_scol, smask, masked,
                          [&](uint32_t, uint32_t, uint32_t j) { atomicAdd(&cnt[j - wbase], 1u); });
         __syncthreads();
         const int s0 = threadIdx.x * kPer;
@@ -330,8 +368,8 @@ static_assert(kPerT == 8, "slot ownership assumes 8 slots per thread");
 
 __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
     const uint32_t *a_rp, const uint32_t *a_scol, const uint32_t *a_perm, const uint32_t *b_rp,
-    const uint32_t *b_scol, const uint32_t *b_perm, const uint64_t *smask, const int *masked_flag, int64_t nbg,
-    int nbl, const uint64_t *rowC_off,
+    const uint32_t *b_scol, const uint32_t *b_perm, const uint64_t *smask, const int *masked_flag,
+    const uint64_t *krange, int64_t nbg, int nbl, int lbits, const uint64_t *rowC_off,
     const uint32_t *inv, const int64_t *c_tptr, int64_t t_lo, int64_t t_hi, uint2 *tri) {
   __shared__ uint32_t mask[kWinT];
   __shared__ int64_t cur[kWinT];
@@ -341,8 +379,9 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kNT >> 5;
   const int s0 = threadIdx.x * kPerT;
   const bool ranged = t_lo > 0 || t_hi < c_tptr[rowC_off[nbg]];
-  const bool masked = (*masked_flag & 1) != 0;
-  const bool upper = (*masked_flag & 2) != 0;  // only C blocks of leaves (li, lj) with li <= lj
+  const int flags = *masked_flag;
+  const bool masked = (flags & kFlagMasked) != 0;
+  const bool upper = (flags & (kFlagUpper | kFlagRanged)) != 0;  // rows start past their first column
   for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
     if (ranged) {
       // A multi-GPU rank emits one triple range: skip rows none of whose C blocks reach it
@@ -359,13 +398,12 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
       if (hi <= t_lo || lo >= t_hi) continue;
     }
     RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
-    if (upper) s.jmin = max(s.jmin, (uint32_t)((i / nbl) * nbl));
-    if (s.nt > 0) {
+    if (clamp_row(s, i, flags, krange, nbg, nbl, lbits)) {
       uint64_t out = rowC_off[i];
       const bool multi = (s.jmax - s.jmin) >= (uint32_t)kWinT;
       for (uint64_t wb = s.jmin; wb <= s.jmax; wb += kWinT) {
         const uint32_t wbase = (uint32_t)wb;
-        const uint32_t wend = wbase + kWinT;
+        const uint32_t wend = min(wbase + (uint32_t)kWinT, s.jmax + 1u);
         if (threadIdx.x < kWinT / 32) bm[threadIdx.x] = 0u;
         __syncthreads();
         // occupied C columns of the window
@@ -456,6 +494,71 @@ __global__ void k_inv_counts(const uint32_t *perm, const uint32_t *rm_cnt, int64
   cta_exclusive_scan64((const uint64_t *)cnt_q, (uint64_t *)c_tptr, nC + 1, wsum);
 }
 
+// ---- multi-GPU partition of the symbolic phase ------------------------------------------------
+// Structural triples per C tile (aligned square of 2^shift leaves per side, Morton tile code): for
+// every A entry (i, k), B row k's columns are split at the tile-column boundaries by binary search,
+// so the pass costs O(nA x tiles a B row spans) -- not O(triples). Masks are ignored (this only
+// balances the ranks; every rank still filters its own pairs exactly).
+__global__ void k_tile_work(const uint32_t *srow, const uint32_t *scol, int64_t nA, const uint32_t *b_rp, int nbl,
+                            int shift, uint64_t *tiles) {
+  const uint32_t tw = (uint32_t)nbl << shift;  // tile width in blocks
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nA; x += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = srow[x], k = scol[x];
+    const uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
+    if (b0 == b1) continue;
+    const uint32_t I = (i / (uint32_t)nbl) >> shift;
+    const uint32_t J0 = scol[b0] / tw, J1 = scol[b1 - 1] / tw;
+    uint32_t lo = b0;
+    for (uint32_t J = J0; J <= J1; ++J) {
+      const uint32_t hi = J == J1 ? b1 : lower_bound_col(scol, lo, b1, (J + 1) * tw);
+      if (hi > lo) atomicAdd((unsigned long long *)&tiles[(spread_bits(I) << 1) | spread_bits(J)],
+                             (unsigned long long)(hi - lo));
+      lo = hi;
+    }
+  }
+}
+
+// One CTA: prefix of the tile work in Morton order, cut into `world` contiguous tile ranges of
+// (nearly) equal work (the first tile whose exclusive prefix reaches r*W/world starts rank r, as
+// distributed.partition cuts c_tptr), and this rank's C key range [krange[0], krange[1]) -- a union
+// of whole quadtree subtrees, so C stays a contiguous Morton range per rank.
+__global__ void __launch_bounds__(kNT) k_tile_cut(const uint64_t *tiles, int64_t ntiles, uint64_t *prefix,
+                                                  int world, int rank, int kshift, uint64_t *krange,
+                                                  uint64_t *key_cuts, int *flags, volatile int64_t *host_out) {
+  __shared__ uint64_t wsum[32];
+  cta_exclusive_scan64(tiles, prefix, ntiles + 1, wsum);  // tiles[ntiles] is the zeroed tail
+  __syncthreads();
+  const uint64_t W = prefix[ntiles];
+  for (int r = threadIdx.x; r <= world; r += blockDim.x) {
+    int64_t cut;
+    if (r == 0) {
+      cut = 0;
+    } else if (r == world) {
+      cut = ntiles;
+    } else {
+      const uint64_t target = (uint64_t)((unsigned __int128)W * (unsigned)r / (unsigned)world);
+      int64_t lo = 0, hi = ntiles;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (prefix[mid] < target) lo = mid + 1; else hi = mid;
+      }
+      cut = lo;
+    }
+    const uint64_t key = (uint64_t)cut << kshift;
+    if (key_cuts) key_cuts[r] = key;
+    if (r == rank) krange[0] = key;
+    if (r == rank + 1) krange[1] = key;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *flags |= kFlagRanged;
+    __threadfence();
+    host_out[2] = (int64_t)krange[0];
+    host_out[3] = (int64_t)krange[1];
+    host_out[4] = (int64_t)W;
+  }
+}
+
 inline int grid_for(int64_t n, int threads = 256) {
   int64_t g = (n + threads - 1) / threads;
   if (g < 1) g = 1;
@@ -479,6 +582,9 @@ struct SymWs {
   uint64_t *cnt;   // [2*nbg+1]: C blocks per row, triples per row, 0
   uint64_t *off;   // exclusive scan of cnt: rowC_off = off, nC = off[nbg], nT = off[2nbg] - off[nbg]
   unsigned int *done;  // k_sym_count's completion ticket
+  uint64_t *krange;    // [2]: this rank's C key range (flag kFlagRanged; qm_spgemm_count_part)
+  uint64_t *tiles;     // [4^tile_levels]: structural triples per C tile (qm_spgemm_count_part)
+  int tile_levels;
   void *cub;
   size_t cub_bytes;
 };
@@ -492,7 +598,12 @@ size_t cub_bytes_count(int64_t n, int64_t nbg) {
   return std::max(a, b);
 }
 
-SymWs carve_sym(Carver &cv, int64_t nA, int64_t nB, int64_t nbg) {
+// C tiles of the multi-GPU partition: aligned squares of 2^(depth - tile_levels) leaves per side,
+// 4^tile_levels of them in Morton order (at most 65536).
+constexpr int kMaxTileLevels = 8;
+inline int tile_levels_for(const Geometry &g) { return g.depth < kMaxTileLevels ? g.depth : kMaxTileLevels; }
+
+SymWs carve_sym(Carver &cv, int64_t nA, int64_t nB, int64_t nbg, int tile_levels) {
   SymWs w;
   const int64_t n = nA + nB;
   w.rowkey = cv.take<uint32_t>(n); w.val = cv.take<uint32_t>(n); w.srow = cv.take<uint32_t>(n);
@@ -503,6 +614,9 @@ SymWs carve_sym(Carver &cv, int64_t nA, int64_t nB, int64_t nbg) {
   w.cnt = cv.take<uint64_t>(2 * nbg + 1);
   w.off = cv.take<uint64_t>(2 * nbg + 1);
   w.done = cv.take<unsigned int>(1);
+  w.krange = cv.take<uint64_t>(2);
+  w.tile_levels = tile_levels;
+  w.tiles = cv.take<uint64_t>(2 * ((size_t)1 << (2 * tile_levels)) + 2);  // work [+ tail], prefix
   w.cub_bytes = cub_bytes_count(n, nbg);
   w.cub = cv.take<char>(w.cub_bytes);
   return w;
@@ -574,14 +688,15 @@ extern "C" size_t qm_spgemm_workspace_bytes(const qm_layout *layout, int64_t nA,
   Geometry g;
   if (make_geometry(layout, &g) != QM_OK) return 0;
   Carver cv(nullptr, 0);
-  carve_sym(cv, nA, nB, g.nbg);
+  carve_sym(cv, nA, nB, g.nbg, tile_levels_for(g));
   return cv.off;
 }
 
-extern "C" int qm_spgemm_count_masked(const qm_layout *layout, const uint64_t *a_keys, const uint64_t *a_cmask,
-                                      int64_t nA, const uint64_t *b_keys, const uint64_t *b_rmask, int64_t nB,
-                                      int32_t flags, void *ws, size_t ws_bytes, int64_t *n_c_out,
-                                      int64_t *n_triples_out, void *stream) {
+namespace {
+int count_impl(const qm_layout *layout, const uint64_t *a_keys, const uint64_t *a_cmask, int64_t nA,
+               const uint64_t *b_keys, const uint64_t *b_rmask, int64_t nB, int32_t flags, int world, int rank,
+               void *ws, size_t ws_bytes, int64_t *n_c_out, int64_t *n_triples_out, int64_t *part_out,
+               uint64_t *key_cuts, void *stream) {
   Geometry g;
   int rc = make_geometry(layout, &g);
   if (rc != QM_OK) return rc;
@@ -591,7 +706,7 @@ extern "C" int qm_spgemm_count_masked(const qm_layout *layout, const uint64_t *a
   }
   cudaStream_t st = (cudaStream_t)stream;
   Carver cv(ws, ws_bytes);
-  SymWs w = carve_sym(cv, nA, nB, g.nbg);
+  SymWs w = carve_sym(cv, nA, nB, g.nbg, tile_levels_for(g));
   if (!cv.ok() || !ws) {
     set_error("qm_spgemm_count: workspace %zu bytes < required %zu", ws_bytes, cv.off);
     return QM_ERR_WORKSPACE;
@@ -605,18 +720,57 @@ extern "C" int qm_spgemm_count_masked(const qm_layout *layout, const uint64_t *a
   int64_t *host_tot = nullptr, *dev_tot = nullptr;
   rc = mapped_i64(&host_tot, &dev_tot);
   if (rc != QM_OK) return rc;
-  k_sym_count<<<row_grid(g.nbg), kNT, 0, st>>>(a_rp, w.scol, b_rp, w.scol, w.smask, w.masked, g.nbg, g.nbl,
-                                               w.cnt, w.off, w.done, dev_tot);
+  if (world > 0) {  // multi-GPU partition: this rank's C key range from the tile work
+    const int tl = w.tile_levels;
+    const int64_t ntiles = (int64_t)1 << (2 * tl);
+    QM_CUDA_TRY(cudaMemsetAsync(w.tiles, 0, (size_t)(ntiles + 1) * sizeof(uint64_t), st));
+    if (nA > 0) {
+      k_tile_work<<<grid_for(nA), 256, 0, st>>>(w.srow, w.scol, nA, b_rp, g.nbl, g.depth - tl, w.tiles);
+      QM_LAUNCHED("k_tile_work");
+    }
+    k_tile_cut<<<1, kNT, 0, st>>>(w.tiles, ntiles, w.tiles + ntiles + 1, world, rank,
+                                   2 * (g.depth - tl) + 2 * g.lbits, w.krange, key_cuts, w.masked, dev_tot);
+    QM_LAUNCHED("k_tile_cut");
+  }
+  k_sym_count<<<row_grid(g.nbg), kNT, 0, st>>>(a_rp, w.scol, b_rp, w.scol, w.smask, w.masked, w.krange, g.nbg,
+                                               g.nbl, g.lbits, w.cnt, w.off, w.done, dev_tot);
   QM_LAUNCHED("k_sym_count");
   QM_CUDA_TRY(cudaStreamSynchronize(st));
-  uint64_t tot[2] = {(uint64_t)((volatile int64_t *)host_tot)[0], (uint64_t)((volatile int64_t *)host_tot)[1]};
+  volatile int64_t *ht = (volatile int64_t *)host_tot;
+  uint64_t tot[2] = {(uint64_t)ht[0], (uint64_t)ht[1]};
   if (tot[0] >= (1ull << 32)) {
     set_error("product has %llu C blocks; this build indexes C with 32 bits", (unsigned long long)tot[0]);
     return QM_ERR_UNSUPPORTED;
   }
   *n_c_out = (int64_t)tot[0];
   *n_triples_out = (int64_t)tot[1];
+  if (part_out) {
+    part_out[0] = ht[2];
+    part_out[1] = ht[3];
+    part_out[2] = ht[4];
+  }
   return QM_OK;
+}
+}  // namespace
+
+extern "C" int qm_spgemm_count_masked(const qm_layout *layout, const uint64_t *a_keys, const uint64_t *a_cmask,
+                                      int64_t nA, const uint64_t *b_keys, const uint64_t *b_rmask, int64_t nB,
+                                      int32_t flags, void *ws, size_t ws_bytes, int64_t *n_c_out,
+                                      int64_t *n_triples_out, void *stream) {
+  return count_impl(layout, a_keys, a_cmask, nA, b_keys, b_rmask, nB, flags, 0, 0, ws, ws_bytes, n_c_out,
+                    n_triples_out, nullptr, nullptr, stream);
+}
+
+extern "C" int qm_spgemm_count_part(const qm_layout *layout, const uint64_t *a_keys, const uint64_t *a_cmask,
+                                    int64_t nA, const uint64_t *b_keys, const uint64_t *b_rmask, int64_t nB,
+                                    int32_t world, int32_t rank, void *ws, size_t ws_bytes, int64_t *n_c_out,
+                                    int64_t *n_triples_out, int64_t *part_out, uint64_t *key_cuts, void *stream) {
+  if (world < 1 || rank < 0 || rank >= world || !part_out) {
+    set_error("qm_spgemm_count_part: bad world %d / rank %d", world, rank);
+    return QM_ERR_INVALID;
+  }
+  return count_impl(layout, a_keys, a_cmask, nA, b_keys, b_rmask, nB, 0, world, rank, ws, ws_bytes, n_c_out,
+                    n_triples_out, part_out, key_cuts, stream);
 }
 
 extern "C" int qm_spgemm_count(const qm_layout *layout, const uint64_t *a_keys, int64_t nA,
@@ -641,7 +795,7 @@ int fill_setup(const qm_layout *layout, int64_t nA, int64_t nB, int64_t nC, void
   int rc = make_geometry(layout, g);
   if (rc != QM_OK) return rc;
   Carver cv(ws, ws_bytes);
-  *w = carve_sym(cv, nA, nB, g->nbg);
+  *w = carve_sym(cv, nA, nB, g->nbg, tile_levels_for(*g));
   if (!cv.ok() || !ws) {
     set_error("qm_spgemm_fill: workspace too small");
     return QM_ERR_WORKSPACE;
@@ -668,8 +822,8 @@ extern "C" int qm_spgemm_fill_keys(const qm_layout *layout, int64_t nA, int64_t 
   if (rc != QM_OK) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   if (nC == 0) return cudaMemsetAsync(c_tptr, 0, sizeof(int64_t), st) == cudaSuccess ? QM_OK : QM_ERR_CUDA;
-  k_sym_emit_c<<<row_grid(g.nbg), kNT, 0, st>>>(w.rp, w.scol, w.rp + g.nbg, w.scol, w.smask, w.masked, g.nbg, g.nbl,
-                                                g.lbits, w.off, f.rm_key, f.rm_cnt, f.rm_iota, f.done);
+  k_sym_emit_c<<<row_grid(g.nbg), kNT, 0, st>>>(w.rp, w.scol, w.rp + g.nbg, w.scol, w.smask, w.masked, w.krange,
+                                                g.nbg, g.nbl, g.lbits, w.off, f.rm_key, f.rm_cnt, f.rm_iota, f.done);
   QM_LAUNCHED("k_sym_emit_c");
   size_t tb = f.cub_bytes;
   QM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(f.cub, tb, f.rm_key, c_keys, f.rm_iota, f.perm, nC, 0,
@@ -698,8 +852,8 @@ extern "C" int qm_spgemm_fill_triples(const qm_layout *layout, int64_t nA, int64
   if (nC == 0 || t_hi <= t_lo) return QM_OK;
   cudaStream_t st = (cudaStream_t)stream;
   k_sym_emit_tri<<<row_grid(g.nbg), kNT, 0, st>>>(w.rp, w.scol, w.perm, w.rp + g.nbg, w.scol,
-                                                  w.perm, w.smask, w.masked, g.nbg, g.nbl, w.off, f.inv, c_tptr, t_lo,
-                                                  t_hi, (uint2 *)tri);
+                                                  w.perm, w.smask, w.masked, w.krange, g.nbg, g.nbl, g.lbits, w.off,
+                                                  f.inv, c_tptr, t_lo, t_hi, (uint2 *)tri);
   QM_LAUNCHED("k_sym_emit_tri");
   return QM_OK;
 }

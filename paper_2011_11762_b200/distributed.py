@@ -73,6 +73,39 @@ class Comm:
         self.dist.all_gather(outs, pad, group=self.group)
         return self._out(torch.cat([o[:c] for o, c in zip(outs, counts)]), dev), counts
 
+    def allgather_varlen_many(self, ts: list) -> tuple[list, list]:
+        """allgather_varlen of several 1-D tensors with ONE size exchange (one host sync): returns
+        the per-tensor concatenations and the per-tensor rank counts."""
+        dev = ts[0].device
+        n = torch.tensor([int(t.shape[0]) for t in ts], dtype=torch.int64,
+                         device="cpu" if self.stage else dev)
+        ns = [torch.zeros_like(n) for _ in range(self.world)]
+        self.dist.all_gather(ns, n, group=self.group)
+        allc = torch.stack(ns).cpu().tolist()  # [world][len(ts)]
+        outs, counts = [], []
+        for i, t in enumerate(ts):
+            c = [int(allc[r][i]) for r in range(self.world)]
+            outs.append(self.gather_known(t, c))
+            counts.append(c)
+        return outs, counts
+
+    def gather_known(self, t: torch.Tensor, counts: list) -> torch.Tensor:
+        """Concatenation over ranks of 1-D tensors whose lengths `counts` every rank already knows."""
+        dev = t.device
+        t = self._in(t)
+        mx = max(counts) if counts else 0
+        pad = torch.zeros(mx, dtype=t.dtype, device=t.device)
+        pad[: t.shape[0]] = t
+        outs = [torch.empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(outs, pad, group=self.group)
+        return self._out(torch.cat([o[:c] for o, c in zip(outs, counts)]), dev)
+
+    def allreduce_max_vec(self, xs: list, device) -> list:
+        """Element-wise max over ranks of a few host floats (one collective)."""
+        t = torch.tensor(xs, dtype=torch.float64, device="cpu" if self.stage else device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return [float(x) for x in t.cpu().tolist()]
+
     def allgather_fixed(self, t: torch.Tensor) -> torch.Tensor:
         """[world, *t.shape]: every rank's tensor of the same shape, in rank order."""
         dev = t.device
@@ -81,16 +114,18 @@ class Comm:
         self.dist.all_gather(outs, t, group=self.group)
         return self._out(torch.stack(outs), dev)
 
-    def alltoallv(self, send: torch.Tensor, send_counts: list[int]) -> tuple[torch.Tensor, list[int]]:
+    def alltoallv(self, send: torch.Tensor, send_counts: list[int],
+                  recv_counts: list[int] | None = None) -> tuple[torch.Tensor, list[int]]:
         """Rows send[sum(send_counts[:d]) : ...] go to rank d; returns received rows (source rank
-        order) and the per-source counts."""
+        order) and the per-source counts (exchanged first unless the caller knows them)."""
         dev0 = send.device
         send = self._in(send)
         dev = send.device
-        sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
-        rc = torch.empty_like(sc)
-        self.dist.all_to_all_single(rc, sc, group=self.group)
-        recv_counts = [int(x) for x in rc.cpu().tolist()]
+        if recv_counts is None:
+            sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
+            rc = torch.empty_like(sc)
+            self.dist.all_to_all_single(rc, sc, group=self.group)
+            recv_counts = [int(x) for x in rc.cpu().tolist()]
         flat = send.reshape(send.shape[0], -1) if send.dim() > 1 else send.reshape(-1, 1)
         out = torch.empty((sum(recv_counts), flat.shape[1]), dtype=send.dtype, device=dev)
         self.dist.all_to_all_single(out, flat.contiguous(), recv_counts, send_counts, group=self.group)
@@ -113,10 +148,19 @@ class LocalComm:
     def allgather_varlen(self, t):
         return t, [int(t.shape[0])]
 
+    def allgather_varlen_many(self, ts):
+        return list(ts), [[int(t.shape[0])] for t in ts]
+
+    def gather_known(self, t, counts):
+        return t
+
+    def allreduce_max_vec(self, xs, device):
+        return list(xs)
+
     def allgather_fixed(self, t):
         return t.unsqueeze(0)
 
-    def alltoallv(self, send, send_counts):
+    def alltoallv(self, send, send_counts, recv_counts=None):
         return send, list(send_counts)
 
     def barrier(self):
@@ -159,9 +203,10 @@ class CudaBackend:
     def __init__(self, stream=None):
         self.stream = stream
 
-    def symbolic_state(self, layout, a_keys: torch.Tensor, b_keys: torch.Tensor, a_cmask=None, b_rmask=None):
+    def symbolic_state(self, layout, a_keys: torch.Tensor, b_keys: torch.Tensor, a_cmask=None, b_rmask=None,
+                       part=None):
         return spgemm.SymbolicState(layout, a_keys, int(a_keys.shape[0]), b_keys, int(b_keys.shape[0]),
-                                    self.stream, a_cmask, b_rmask)
+                                    self.stream, a_cmask, b_rmask, part=part)
 
     def gather_blocks(self, blocks: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
         import ctypes  # noqa: F401
@@ -192,14 +237,44 @@ class DistStats:
     world: int = 1
     n_c_global: int = 0
     n_triples_global: int = 0
-    c_range: tuple = (0, 0)
-    t_range: tuple = (0, 0)
+    c_range: tuple = (0, 0)   # this rank's C key range [lo, hi) (a union of quadtree subtrees)
+    t_range: tuple = (0, 0)   # (0, this rank's triples)
+    tile_work: int = 0        # total structural triples of the partition pass
     n_c_local: int = 0
     bytes_received: int = 0
     bytes_sent: int = 0
     blocks_received: int = 0
     mode: str = "exchange"
     phase_s: dict = field(default_factory=dict)
+
+
+MAX_TILE_LEVELS = 8  # csrc/qm_symbolic.cu kMaxTileLevels
+
+
+def tile_partition(geom, ka: np.ndarray, kb: np.ndarray, world: int) -> list[int]:
+    """Host statement of qm_spgemm_count_part's partition (its CPU twin and test oracle): C tiles =
+    aligned quadtree subtrees at level min(depth, 8) (tile code = C key >> kshift), weighed by their
+    structural triples; tiles are cut in Morton order where the exclusive work prefix first reaches
+    r*W // world. Returns the world+1 key bounds; rank r owns C keys [bounds[r], bounds[r+1])."""
+    import scipy.sparse as sp  # noqa: PLC0415
+
+    depth = geom.params.depth
+    tl = min(depth, MAX_TILE_LEVELS)
+    kshift = 2 * (depth - tl) + 2 * geom.lbits
+    ntiles = 1 << (2 * tl)
+    nb = geom.nbg
+    ai, ak = geom.decode(np.asarray(ka, dtype=np.int64))
+    bk, bj = geom.decode(np.asarray(kb, dtype=np.int64))
+    pa = sp.csr_matrix((np.ones(ai.size, dtype=np.int64), (ai, ak)), shape=(nb, nb))
+    pb = sp.csr_matrix((np.ones(bk.size, dtype=np.int64), (bk, bj)), shape=(nb, nb))
+    c = (pa @ pb).tocoo()
+    tiles = geom.qkey(c.row.astype(np.int64), c.col.astype(np.int64)) >> kshift
+    work = np.bincount(tiles, weights=c.data, minlength=ntiles).astype(np.int64)
+    prefix = np.concatenate([[0], np.cumsum(work)])
+    W = int(prefix[-1])
+    cuts = [0] + [int(np.searchsorted(prefix[:ntiles], (W * r) // world, side="left")) for r in range(1, world)]
+    cuts.append(ntiles)
+    return [x << kshift for x in cuts]
 
 
 def partition(c_tptr: torch.Tensor, world: int) -> tuple[list[int], list[int]]:
@@ -333,7 +408,8 @@ def _fetch(comm, backend, local_blocks: torch.Tensor, offsets: list[int], need: 
     wanted, serve_counts = comm.alltoallv(need, req_counts)  # indices peers want from me
     local_idx = wanted.reshape(-1) - offsets[comm.rank]
     payload = backend.gather_blocks(local_blocks, local_idx)
-    blocks, got_counts = comm.alltoallv(payload, serve_counts)
+    # every owner returns exactly the blocks requested from it: the receive counts are known
+    blocks, got_counts = comm.alltoallv(payload, serve_counts, recv_counts=req_counts)
     bsz = int(local_blocks.shape[1]) ** 2 * local_blocks.element_size()
     peers_in = sum(c for r, c in enumerate(got_counts) if r != comm.rank)
     peers_out = sum(c for r, c in enumerate(serve_counts) if r != comm.rank)
@@ -365,62 +441,82 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     stats = DistStats(rank=comm.rank, world=comm.world)
     clock = timer or (lambda: time.perf_counter())
     t0 = clock()
-    ka, a_counts = comm.allgather_varlen(a_local.keys)
-    kb, b_counts = (ka, a_counts) if b_is_a else comm.allgather_varlen(b_local.keys)
+    bs = layout.block_size
+    dev = a_local.blocks.device
+    empty = BlockSet.empty(bs, dev)
+    # Support masks (spgemm.symbolic): gathered with the keys when the operands' blocks have
+    # partial supports, so every rank skips the same exactly-zero block pairs and k panels. The
+    # filter is needed unless ALL of A's blocks have full column supports or ALL of B's full row
+    # supports: one max-reduction of the two "not full" flags over the ranks.
+    bl = a_local if b_is_a else b_local
+    use_masks = False
+    if spgemm.support_filter_enabled() and a_local.blocks.is_cuda:
+        a_local.support_masks()
+        if not b_is_a:
+            b_local.support_masks()
+        a_part, b_part = comm.allreduce_max_vec([0.0 if a_local.masks_full[1] else 1.0,
+                                                 0.0 if bl.masks_full[0] else 1.0], dev)
+        use_masks = a_part > 0.0 and b_part > 0.0
+    # structure (+ masks): one size exchange, then the payload gathers
+    send = [a_local.keys] if b_is_a else [a_local.keys, b_local.keys]
+    if use_masks:
+        send += [a_local.masks[1].contiguous(), bl.masks[0].contiguous(), a_local.masks[2].contiguous()]
+        if not b_is_a:
+            send.append(bl.masks[2].contiguous())
+    got, counts = comm.allgather_varlen_many(send)
+    ka, a_counts = got[0], counts[0]
+    kb, b_counts = (ka, a_counts) if b_is_a else (got[1], counts[1])
+    ma = mb = fa = fb = None
+    if use_masks:
+        o = 1 if b_is_a else 2
+        ma, mb, fa = got[o], got[o + 1], got[o + 2]
+        fb = fa if b_is_a else got[o + 3]
     if ka.shape[0] > 1 and bool((ka[1:] <= ka[:-1]).any()):
         raise ContractViolationError("distributed operands must own ascending, disjoint key ranges")
     if kb.shape[0] > 1 and bool((kb[1:] <= kb[:-1]).any()):
         raise ContractViolationError("distributed operands must own ascending, disjoint key ranges")
     a_off = [0] + list(np.cumsum(a_counts).tolist())
     b_off = [0] + list(np.cumsum(b_counts).tolist())
-    bs = layout.block_size
-    dev = a_local.blocks.device
-    empty = BlockSet.empty(bs, dev)
     if ka.shape[0] == 0 or kb.shape[0] == 0:
         return empty, stats
-    # Support masks (spgemm.symbolic): gathered with the keys when some rank's blocks have partial
-    # supports, so every rank skips the same exactly-zero block pairs and k panels.
-    ma = mb = fa = fb = None
-    if spgemm.support_filter_enabled() and a_local.blocks.is_cuda:
-        a_local.support_masks()
-        if not b_is_a:
-            b_local.support_masks()
-        # the filter is needed unless ALL of A's blocks have full column supports or ALL of B's
-        # full row supports (a max-reduction of "not full" per operand, then the global test)
-        bl = a_local if b_is_a else b_local
-        a_part = comm.allreduce_max(0.0 if a_local.masks_full[1] else 1.0, dev) > 0.0
-        b_part = comm.allreduce_max(0.0 if bl.masks_full[0] else 1.0, dev) > 0.0
-        if a_part and b_part:
-            ma, _ = comm.allgather_varlen(a_local.masks[1].contiguous())
-            mb, _ = comm.allgather_varlen(bl.masks[0].contiguous())
-            fa, _ = comm.allgather_varlen(a_local.masks[2].contiguous())  # NaN/Inf flags
-            fb = fa if b_is_a else comm.allgather_varlen(bl.masks[2].contiguous())[0]
     t1 = clock()
-    st = (backend.symbolic_state(layout, ka, kb, a_cmask=ma, b_rmask=mb) if ma is not None
-          else backend.symbolic_state(layout, ka, kb))
-    stats.n_c_global, stats.n_triples_global = st.n_c, st.n_t
-    if st.n_c == 0:
+    # Partitioned symbolic phase (qm_spgemm_count_part): a cheap global pass weighs the C tiles
+    # (quadtree subtrees), cuts them into `world` contiguous key ranges of equal work, and this
+    # rank counts and emits only the C blocks of its own range (the reference's workers likewise
+    # expand only the tasks they execute, ops.py:197-241 / engine.py:286-300).
+    st = backend.symbolic_state(layout, ka, kb, a_cmask=ma, b_rmask=mb, part=(comm.world, comm.rank))
+    stats.c_range, stats.tile_work = st.key_range, st.tile_work
+    stats.n_c_local, stats.t_range = st.n_c, (0, st.n_t)
+    tot = comm.allgather_fixed(torch.tensor([st.n_c, st.n_t], dtype=torch.int64,
+                                            device="cpu" if getattr(comm, "stage", True) else dev))
+    tot = tot.reshape(-1, 2).sum(dim=0).tolist()
+    stats.n_c_global, stats.n_triples_global = int(tot[0]), int(tot[1])
+    if stats.n_c_global == 0:
         return empty, stats
-    c_keys, c_tptr = st.keys()
-    cb, tb = partition(c_tptr, comm.world)
-    m0, m1 = cb[comm.rank], cb[comm.rank + 1]
-    lo, hi = tb[comm.rank], tb[comm.rank + 1]
-    stats.c_range, stats.t_range = (m0, m1), (lo, hi)
-    tri = st.triples(c_tptr, lo, hi).view(-1, 2).to(torch.int64)
+    lo, hi = 0, st.n_t
+    if st.n_c:  # (a rank with an empty range still takes part in every collective below)
+        c_keys, c_tptr = st.keys()
+        tri = st.triples(c_tptr, lo, hi).view(-1, 2).to(torch.int64)
+    else:
+        c_keys = torch.zeros(0, dtype=torch.int64, device=dev)
+        c_tptr = torch.zeros(1, dtype=torch.int64, device=dev)
+        tri = torch.zeros((0, 2), dtype=torch.int64, device=dev)
     t2 = clock()
     fused_ok = (comm.world > 1 and mode != "exchange" and hasattr(backend, "numeric_pools")
                 and layout.block_size in (32, 64, 128) and comm.world <= 8)
-    if fused_ok and hi > lo:
+    if fused_ok:
         offa = torch.tensor(a_off, dtype=torch.int64, device=dev)
         offb = offa if b_is_a else torch.tensor(b_off, dtype=torch.int64, device=dev)
         pa_idx, own_a = _pack_owner(tri[:, 0].contiguous(), offa)
         pb_idx, own_b = _pack_owner(tri[:, 1].contiguous(), offb)
         blk_bytes = bs * bs * 8
-        remote_refs = int(((own_a != comm.rank).sum() + (own_b != comm.rank).sum()).item())
+        remote_refs = int(((own_a != comm.rank).sum() + (own_b != comm.rank).sum()).item()) if hi > lo else 0
         fused_s = remote_refs * blk_bytes / (NVLINK_GBS * 1e9)
         compute_s = 2.0 * bs ** 3 * (hi - lo) / (FP64_TFLOPS * 1e12)
+        # every rank must take the same path (the fused mode's mappings are collective)
+        prefer_exchange = 0.0 if (mode == "fused" or fused_s <= 0.25 * compute_s) else 1.0
         pools = None
-        if mode == "fused" or fused_s <= 0.25 * compute_s:
+        if comm.allreduce_max_vec([prefer_exchange], dev)[0] == 0.0:
             if dev.type == "cuda":
                 torch.cuda.synchronize(dev)  # this rank's pools are written (any stream) ...
             comm.barrier()  # ... on every rank, before anyone reads them
@@ -435,11 +531,9 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
                 pools = None
         if pools is not None:
             tri_packed = torch.stack([pa_idx, pb_idx], dim=1).to(torch.int32).reshape(-1).contiguous()
-            c_tptr_local = (c_tptr[m0:m1 + 1] - lo).contiguous()
             try:
-                c = backend.numeric_pools(layout, pools.ptrs[0], pools.counts[0], pools.ptrs[-1],
-                                          pools.counts[-1], tri_packed, c_tptr_local,
-                                          c_keys[m0:m1].contiguous())
+                c = (backend.numeric_pools(layout, pools.ptrs[0], pools.counts[0], pools.ptrs[-1],
+                                           pools.counts[-1], tri_packed, c_tptr, c_keys) if hi > lo else empty)
                 torch.cuda.synchronize(dev)
             finally:
                 pools.close()
@@ -465,8 +559,6 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     la = torch.searchsorted(need_a, tri[:, 0].contiguous())
     lb = torch.searchsorted(need_b, tri[:, 1].contiguous())
     tri_local = torch.stack([la, lb], dim=1).to(torch.int32).reshape(-1).contiguous()
-    c_tptr_local = (c_tptr[m0:m1 + 1] - lo).contiguous()
-    c_keys_local = c_keys[m0:m1].contiguous()
     dummy_a = torch.empty(0, dtype=torch.float64, device=dev)
     # pool keys are the blocks' quadtree keys (the bs-16 grouping and claim orders decode them)
     pk_a, pk_b = ka[need_a], kb[need_b]
@@ -479,7 +571,7 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
         pa = BlockSet(pk_a, pool_a, dummy_a, masks_full=(True, True))
         pb = BlockSet(pk_b, pool_b, dummy_a, masks_full=(True, True))
         pa.masks = pb.masks = torch.empty((3, 0), dtype=torch.int64, device=dev)
-    c = backend.numeric(layout, pa, pb, tri_local, c_tptr_local, c_keys_local)
+    c = backend.numeric(layout, pa, pb, tri_local, c_tptr, c_keys)
     t4 = clock()
     stats.n_c_local = c.n
     stats.mode = "exchange"

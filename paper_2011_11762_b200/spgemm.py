@@ -68,7 +68,10 @@ class SymbolicState:
     """Workspaces of one symbolic phase (row indexes, fill scratch) kept between its steps."""
 
     def __init__(self, layout, a_keys: torch.Tensor, n_a: int, b_keys: torch.Tensor, n_b: int, stream=None,
-                 a_cmask: torch.Tensor | None = None, b_rmask: torch.Tensor | None = None, upper: bool = False):
+                 a_cmask: torch.Tensor | None = None, b_rmask: torch.Tensor | None = None, upper: bool = False,
+                 part: tuple[int, int] | None = None):
+        """part = (world, rank): the rank's share of a multi-GPU product (qm_spgemm_count_part) --
+        only the C blocks of its own key range (self.key_range) are counted and emitted."""
         self.lib = _ffi.load()
         self.layout = layout
         self.lp = ctypes.byref(layout)
@@ -79,12 +82,27 @@ class SymbolicState:
         self.ws = _alloc(max(self.ws_bytes, 1), torch.uint8, self.dev)
         n_c = ctypes.c_int64(0)
         n_t = ctypes.c_int64(0)
-        _ffi.check(  # support masks (None = full support): pairs whose product is exactly zero are skipped
-            self.lib.qm_spgemm_count_masked(self.lp, _ffi.ptr(a_keys), _ffi.ptr(a_cmask), n_a, _ffi.ptr(b_keys),
-                                            _ffi.ptr(b_rmask), n_b, 1 if upper else 0, _ffi.ptr(self.ws),
-                                            self.ws_bytes, ctypes.byref(n_c), ctypes.byref(n_t), self.sh),
-            "qm_spgemm_count_masked",
-        )
+        self.key_range, self.tile_work, self.key_cuts = None, 0, None
+        if part is not None:
+            world, rank = part
+            po = (ctypes.c_int64 * 3)()
+            self.key_cuts = _alloc(world + 1, torch.int64, self.dev)
+            _ffi.check(
+                self.lib.qm_spgemm_count_part(self.lp, _ffi.ptr(a_keys), _ffi.ptr(a_cmask), n_a, _ffi.ptr(b_keys),
+                                              _ffi.ptr(b_rmask), n_b, world, rank, _ffi.ptr(self.ws), self.ws_bytes,
+                                              ctypes.byref(n_c), ctypes.byref(n_t), po, _ffi.ptr(self.key_cuts),
+                                              self.sh),
+                "qm_spgemm_count_part",
+            )
+            self.key_range = (int(po[0]) & (2**64 - 1), int(po[1]) & (2**64 - 1))
+            self.tile_work = int(po[2])
+        else:
+            _ffi.check(  # support masks (None = full support): pairs whose product is exactly zero are skipped
+                self.lib.qm_spgemm_count_masked(self.lp, _ffi.ptr(a_keys), _ffi.ptr(a_cmask), n_a, _ffi.ptr(b_keys),
+                                                _ffi.ptr(b_rmask), n_b, 1 if upper else 0, _ffi.ptr(self.ws),
+                                                self.ws_bytes, ctypes.byref(n_c), ctypes.byref(n_t), self.sh),
+                "qm_spgemm_count_masked",
+            )
         self.n_c, self.n_t = int(n_c.value), int(n_t.value)
         self.fill_bytes = self.lib.qm_spgemm_fill_workspace_bytes(self.lp, self.n_c)
         self.fws = _alloc(max(self.fill_bytes, 1), torch.uint8, self.dev)

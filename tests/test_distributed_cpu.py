@@ -27,13 +27,26 @@ class OracleBackend:
         self.geom = geom
         self.og = O.Geom(geom.params.n_logical, geom.params.leaf_dim, geom.bs)
 
-    def symbolic_state(self, layout, a_keys, b_keys):
+    def symbolic_state(self, layout, a_keys, b_keys, a_cmask=None, b_rmask=None, part=None):
+        """The oracle's symbolic product restricted, like qm_spgemm_count_part, to this rank's C key
+        range from the tile partition (D.tile_partition, the host statement of the device cut)."""
         outer = self
         self.ka = a_keys.numpy()
         kc, cptr, ta, tb, tk = O.symbolic(self.og, a_keys.numpy(), b_keys.numpy())
+        key_range = None
+        if part is not None:
+            world, rank = part
+            bounds = D.tile_partition(self.geom, a_keys.numpy(), b_keys.numpy(), world)
+            key_range = (bounds[rank], bounds[rank + 1])
+            sel = (kc >= key_range[0]) & (kc < key_range[1])
+            c0, c1 = int(np.argmax(sel)) if sel.any() else 0, int(sel.sum())
+            t0, t1 = int(cptr[c0]), int(cptr[c0 + c1])
+            kc, cptr = kc[c0:c0 + c1], cptr[c0:c0 + c1 + 1] - t0
+            ta, tb = ta[t0:t1], tb[t0:t1]
 
         class St:
             n_c, n_t = int(kc.size), int(ta.size)
+            tile_work = 0
 
             def keys(self):
                 return torch.from_numpy(kc), torch.from_numpy(cptr)
@@ -41,6 +54,7 @@ class OracleBackend:
             def triples(self, c_tptr, lo, hi):
                 return torch.from_numpy(np.stack([ta[lo:hi], tb[lo:hi]], 1).astype(np.int32).reshape(-1))
 
+        St.key_range = key_range
         _ = outer
         return St()
 
@@ -136,6 +150,34 @@ def test_fused_mode_falls_back_on_every_rank_when_pools_cannot_be_mapped(tmp_pat
     kc, bc, _ = O.multiply(O.Geom(cfg.n, cfg.bs, cfg.bs), ka, ba, kb, bb)
     np.testing.assert_array_equal(out["keys"], kc)
     np.testing.assert_array_equal(out["blocks"].reshape(bc.shape), bc)
+
+
+@pytest.mark.parametrize("name,world", [("C1", 2), ("C1", 8), ("C2-16384", 4), ("C3", 8), ("C5-64", 8)])
+def test_tile_partition_is_balanced_and_covers_the_key_space(name, world):
+    """tile_partition (host twin of qm_spgemm_count_part's cut): world+1 monotone key bounds from
+    0 to the end of the key space, each range a union of whole tiles, and balanced: every rank's
+    structural triples are within one tile's work of W/world."""
+    cfg = G.CONFIGS[name]
+    geom = cfg.geometry
+    ka, kb = G.config_keys(cfg, 0), G.config_keys(cfg, 1)
+    bounds = D.tile_partition(geom, ka, kb, world)
+    depth = geom.params.depth
+    tl = min(depth, D.MAX_TILE_LEVELS)
+    kshift = 2 * (depth - tl) + 2 * geom.lbits
+    assert bounds[0] == 0 and bounds[-1] == 1 << (2 * depth + 2 * geom.lbits)
+    assert all(x <= y for x, y in zip(bounds, bounds[1:])) and all(b % (1 << kshift) == 0 for b in bounds)
+    import scipy.sparse as sp
+
+    nb = geom.nbg
+    ai, ak = geom.decode(ka)
+    bk, bj = geom.decode(kb)
+    c = (sp.csr_matrix((np.ones(ai.size), (ai, ak)), shape=(nb, nb)) @
+         sp.csr_matrix((np.ones(bk.size), (bk, bj)), shape=(nb, nb))).tocoo()
+    keys = geom.qkey(c.row.astype(np.int64), c.col.astype(np.int64))
+    share = np.array([c.data[(keys >= bounds[r]) & (keys < bounds[r + 1])].sum() for r in range(world)])
+    tile_work = np.bincount(keys >> kshift, weights=c.data)
+    assert share.sum() == c.data.sum()
+    assert np.abs(share - c.data.sum() / world).max() <= tile_work.max() + 1
 
 
 def test_partition_bounds_are_balanced_and_monotone():

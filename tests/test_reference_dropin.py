@@ -12,6 +12,7 @@ Test infrastructure only: the product path never imports the reference.
 """
 
 import re
+import sys
 import types
 
 import numpy as np
@@ -43,6 +44,7 @@ def _reference_bench_module():
     src2, n = re.subn(r"^from \.(\w+) import", r"from paper_2011_11762_b200.\1 import", src, flags=re.M)
     assert n >= 4 and "from ." not in src2  # errors, generators, ops, session
     mod = types.ModuleType("quadmat_bench_on_b200")
+    sys.modules[mod.__name__] = mod  # dataclasses resolve their module through sys.modules
     exec(compile(src2, "quadmat/bench.py (imports -> paper_2011_11762_b200)", "exec"), mod.__dict__)
     return mod
 
