@@ -331,6 +331,25 @@ QM_API int qm_filter_triples(const qm_layout *layout, const uint64_t *a_keys, co
                              int64_t n_pairs, uint32_t *tri_out, int64_t *c_tptr_out, uint64_t *c_keys_out,
                              int64_t *nC_out, int64_t *nT_out, void *ws, size_t ws_bytes, void *stream);
 
+/* Ancestor norms of block entries: out[l*n + m] = the norm (from qm_node_norms tables, level L at
+ * codes/norms + L*stride, counts[L] on the host) of the level-l quadtree node containing entry
+ * m's block, 0 when absent; sym: a lower node reads its stored upper mirror (symmetric operands). */
+QM_API int qm_ancestor_norms(const qm_layout *layout, const uint64_t *keys, int64_t n, const uint64_t *codes,
+                             const double *norms, int64_t stride, const int64_t *counts, int32_t sym,
+                             double *out, void *stream);
+/* The approximate multiply's filter in one pass over the triples: a leaf product survives the
+ * reference's pruned recursion iff none of its ancestor tasks was pruned, i.e. at every level l
+ * norm(A ancestor) * norm(B ancestor) >= tau / 8^l (ops.py:199-204, 232; both ancestors exist
+ * because the blocks do). anc_a [(depth+1)*nA] / anc_b from qm_ancestor_norms of the operands as
+ * the plan indexes them (bit 31 of a triple index -- a transposed reference -- is ignored).
+ * Compacts like qm_filter_triples (C blocks left without triples vanish; counts to the host,
+ * one synchronisation). The prune log itself (qm_prune_all) is not needed for the product. */
+QM_API int qm_filter_triples_norms(const qm_layout *layout, double tau, const uint32_t *tri, const int64_t *c_tptr,
+                                   const uint64_t *c_keys, int64_t nC, int64_t nT, const double *anc_a, int64_t nA,
+                                   const double *anc_b, int64_t nB, uint32_t *tri_out, int64_t *c_tptr_out,
+                                   uint64_t *c_keys_out, int64_t *nC_out, int64_t *nT_out, void *ws,
+                                   size_t ws_bytes, void *stream);
+
 /* ---- synthetic inputs (device side of the block-keyed generator) -------- */
 /* For each key, fills the block with numpy's default_rng([seed, matrix_id, bi, bj]).uniform(-1, 1,
  * (bs, bs)) -- bit-identical PCG64 + SeedSequence -- then zeroes entries outside the element

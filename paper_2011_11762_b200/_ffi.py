@@ -72,6 +72,8 @@ EXPORTS = (
     "qm_prune_all",
     "qm_filter_triples_workspace_bytes",
     "qm_filter_triples",
+    "qm_ancestor_norms",
+    "qm_filter_triples_norms",
     "qm_generate_blocks",
     "qm_fp64_peak_kernel",
 )
@@ -156,6 +158,10 @@ _SIGS = {
     "qm_filter_triples_workspace_bytes": (_SZ, [_I64, _I64]),
     "qm_filter_triples": (ctypes.c_int, [_LP, _P, _P, _I32, _P, _P, _P, _I64, _I64, _P, _I64, _P, _P, _P,
                                          ctypes.POINTER(_I64), ctypes.POINTER(_I64), _P, _SZ, _P]),
+    "qm_ancestor_norms": (ctypes.c_int, [_LP, _P, _I64, _P, _P, _I64, _P, _I32, _P, _P]),
+    "qm_filter_triples_norms": (ctypes.c_int, [_LP, ctypes.c_double, _P, _P, _P, _I64, _I64, _P, _I64, _P, _I64,
+                                               _P, _P, _P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), _P, _SZ,
+                                               _P]),
     "qm_generate_blocks": (ctypes.c_int, [_LP, _P, _I64, ctypes.c_uint64, ctypes.c_uint32, _I32,
                                           _I64, _P, _P, _P]),
     "qm_fp64_peak_kernel": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _I64, _P,

@@ -147,3 +147,85 @@ def filter_plan(geom: Geometry, plan, a: BlockSet, b: BlockSet, pr: PruneResult,
                                      _ffi.stream_handle(torch.cuda.current_stream(dev))), "qm_filter_triples")
     n_c, n_t = int(nc2.value), int(nt2.value)
     return SymbolicPlan(n_c, n_t, c_keys[:n_c], c_tptr[:n_c + 1], tri[:2 * n_t])
+
+
+class Pruner:
+    """The approximate variant on the product's hot path (session.run_spec).
+
+    The prune *decisions* needed for the product reduce to a per-triple test: a leaf product
+    survives the reference's pruned recursion iff none of its ancestor tasks was pruned, i.e. at
+    every level l, norm(A ancestor) * norm(B ancestor) >= tau / 8^l (ops.py:199-204, 232). So the
+    hot path is: ancestor norms of the operands' entries (qm_ancestor_norms; cached on a stored
+    block set, recomputed for a per-product view), then one filter pass over the symbolic plan
+    (qm_filter_triples_norms) -- no level-by-level recursion, no per-level synchronisation. The
+    prune *log* (the bounds of the pruned tasks, engine.prune_log) is computed from the same node
+    tables on first access only (qm_prune_all, every level in one launch)."""
+
+    def __init__(self, geom: Geometry, a_src: BlockSet, b_src: BlockSet, tau: float, a_sym: bool = False,
+                 b_sym: bool = False, upper: bool = False):
+        self.geom, self.tau = geom, float(tau)
+        self.a_src, self.b_src = a_src, b_src
+        self.a_sym, self.b_sym, self.upper = a_sym, b_sym, upper
+        self.lay = _ffi.make_layout(geom.params, geom.bs)
+        self.ta = _node_tables(geom, a_src, self.lay)
+        self.tb = self.ta if b_src is a_src else _node_tables(geom, b_src, self.lay)
+        self._result = None
+
+    def _ancestors(self, x: BlockSet, src: BlockSet, tables, sym: bool) -> torch.Tensor:
+        """[(depth+1) * n] ancestor norms of x's entries in src's node tables (cached on x)."""
+        import ctypes
+
+        cache = getattr(x, "_anc_cache", None)
+        key = (id(src), bool(sym), self.geom.params.depth)
+        if cache is not None and key in cache and cache[key][0] is tables:
+            return cache[key][1]
+        L = self.geom.params.depth + 1
+        out = torch.empty(max(L * x.n, 1), dtype=torch.float64, device=x.keys.device)
+        counts = (ctypes.c_int64 * L)(*[t[2] for t in tables])
+        _ffi.check(_ffi.load().qm_ancestor_norms(ctypes.byref(self.lay), _ffi.ptr(x.keys), x.n, _ffi.ptr(tables[0][0]),
+                                                 _ffi.ptr(tables[0][1]), src.n, counts, int(sym), _ffi.ptr(out),
+                                                 _ffi.stream_handle(torch.cuda.current_stream(x.keys.device))),
+                   "qm_ancestor_norms")
+        if cache is None:
+            cache = {}
+            try:
+                x._anc_cache = cache
+            except AttributeError:
+                pass
+        cache[key] = (tables, out)
+        return out
+
+    def filter(self, plan, ax: BlockSet, bx: BlockSet):
+        """The plan's triples whose ancestor tasks all survive (C blocks left empty vanish)."""
+        import ctypes
+
+        from .spgemm import SymbolicPlan
+
+        dev = plan.c_keys.device
+        if plan.n_triples == 0:
+            return plan
+        anc_a = self._ancestors(ax, self.a_src, self.ta, self.a_sym)
+        anc_b = self._ancestors(bx, self.b_src, self.tb, self.b_sym)
+        lib = _ffi.load()
+        nc, nt = plan.n_c, plan.n_triples
+        tri = torch.empty(2 * nt, dtype=torch.int32, device=dev)
+        c_tptr = torch.empty(nc + 1, dtype=torch.int64, device=dev)
+        c_keys = torch.empty(nc, dtype=torch.int64, device=dev)
+        wb = lib.qm_filter_triples_workspace_bytes(nc, nt)
+        ws = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
+        nc2, nt2 = ctypes.c_int64(0), ctypes.c_int64(0)
+        _ffi.check(lib.qm_filter_triples_norms(ctypes.byref(self.lay), self.tau, _ffi.ptr(plan.tri),
+                                               _ffi.ptr(plan.c_tptr), _ffi.ptr(plan.c_keys), nc, nt, _ffi.ptr(anc_a),
+                                               ax.n, _ffi.ptr(anc_b), bx.n, _ffi.ptr(tri), _ffi.ptr(c_tptr),
+                                               _ffi.ptr(c_keys), ctypes.byref(nc2), ctypes.byref(nt2), _ffi.ptr(ws),
+                                               wb, _ffi.stream_handle(torch.cuda.current_stream(dev))),
+                   "qm_filter_triples_norms")
+        n_c, n_t = int(nc2.value), int(nt2.value)
+        return SymbolicPlan(n_c, n_t, c_keys[:n_c], c_tptr[:n_c + 1], tri[:2 * n_t])
+
+    def result(self) -> PruneResult:
+        """The full prune (log and pairs per level), computed on first request."""
+        if self._result is None:
+            self._result = prune(self.geom, self.a_src, self.b_src, self.tau, a_sym=self.a_sym, b_sym=self.b_sym,
+                                 upper=self.upper)
+        return self._result

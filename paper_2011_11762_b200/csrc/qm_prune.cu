@@ -526,6 +526,73 @@ extern "C" size_t qm_filter_triples_workspace_bytes(int64_t nC, int64_t nT) {
   return cv.off;
 }
 
+namespace qm {
+namespace {
+// Compaction of a symbolic plan by per-triple keep flags (keep[nT] = 0 tail set by the caller's
+// keep kernel): C blocks left without triples vanish, order preserved; counts to the host.
+int filter_compact(const uint2 *t2, const int64_t *c_tptr, const uint64_t *c_keys, int64_t nC, int64_t nT,
+                   int64_t *keep, int64_t *kpos, int64_t *cnt, int64_t *alive, int64_t *cpos, int64_t *apos,
+                   void *cub, size_t sb, uint32_t *tri_out, int64_t *c_tptr_out, uint64_t *c_keys_out,
+                   int64_t *nC_out, int64_t *nT_out, cudaStream_t st) {
+  k_filter_count<<<grid_for(nC + 1), 256, 0, st>>>(c_tptr, nC, keep, cnt, alive);
+  QM_LAUNCHED("k_filter_count");
+  size_t tb = sb;
+  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub, tb, keep, kpos, nT + 1, st));
+  tb = sb;
+  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub, tb, cnt, cpos, nC + 1, st));
+  tb = sb;
+  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub, tb, alive, apos, nC + 1, st));
+  k_filter_scatter_tri<<<grid_for(nT), 256, 0, st>>>(t2, nT, keep, kpos, (uint2 *)tri_out);
+  QM_LAUNCHED("k_filter_scatter_tri");
+  k_filter_scatter_c<<<grid_for(nC + 1), 256, 0, st>>>(c_keys, nC, alive, apos, cpos, c_keys_out, c_tptr_out);
+  QM_LAUNCHED("k_filter_scatter_c");
+  int64_t counts[2];
+  int rc = read_device_i64(apos + nC, 1, counts, st, kpos + nT);
+  if (rc != QM_OK) return rc;
+  *nC_out = counts[0];
+  *nT_out = counts[1];
+  return QM_OK;
+}
+
+// out[l*n + m] = norm of the level-l ancestor node of entry m (key -> leaf coordinates >> (depth-l);
+// sym: a lower node reads its stored upper mirror), looked up in that level's node table.
+__global__ void k_ancestor_norms(const uint64_t *keys, int64_t n, int nbl, int lbits, int depth,
+                                 const __grid_constant__ PruneTables t, int sym, double *out) {
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n; m += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t bi, bj;
+    qkey_decode(keys[m], nbl, lbits, &bi, &bj);
+    const uint32_t li = bi / (uint32_t)nbl, lj = bj / (uint32_t)nbl;
+    for (int l = 0; l <= depth; ++l) {
+      double v = 0.0;
+      lookup(t.a[l], li >> (depth - l), lj >> (depth - l), sym != 0, &v);
+      out[(size_t)l * n + m] = v;
+    }
+  }
+}
+
+// keep[t]: no ancestor pair of triple t was pruned -- norm(A anc_l) * norm(B anc_l) >= tau_l at every
+// level l (the reference prunes a task when the product is < tau_l, ops.py:199-204, 232; a leaf
+// product survives iff none of its ancestor tasks was pruned, and its ancestors' nodes all exist).
+__global__ void k_keep_by_norms(const uint2 *tri, int64_t nT, const double *anc_a, int64_t nA, const double *anc_b,
+                                int64_t nB, int depth, const __grid_constant__ PruneTables t, int64_t *keep) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x <= nT; x += (int64_t)gridDim.x * blockDim.x) {
+    if (x == nT) {
+      keep[x] = 0;  // exclusive-scan tail
+      continue;
+    }
+    const uint32_t a = tri[x].x & 0x7FFFFFFFu, b = tri[x].y & 0x7FFFFFFFu;
+    int64_t k = 1;
+    for (int l = 0; l <= depth; ++l)
+      if (anc_a[(size_t)l * nA + a] * anc_b[(size_t)l * nB + b] < t.tau[l]) {
+        k = 0;
+        break;
+      }
+    keep[x] = k;
+  }
+}
+}  // namespace
+}  // namespace qm
+
 extern "C" int qm_filter_triples(const qm_layout *layout, const uint64_t *a_keys, const uint64_t *b_keys,
                                  int32_t b_transposed, const uint32_t *tri, const int64_t *c_tptr,
                                  const uint64_t *c_keys, int64_t nC, int64_t nT, const uint64_t *leaf_pairs,
@@ -553,93 +620,67 @@ extern "C" int qm_filter_triples(const qm_layout *layout, const uint64_t *a_keys
   k_filter_keep<<<grid_for(nT + 1), 256, 0, st>>>(t2, nT, a_keys, b_keys, b_transposed, g.nbl, g.lbits, g.depth,
                                                   leaf_pairs, n_pairs, keep);
   QM_LAUNCHED("k_filter_keep");
-  k_filter_count<<<grid_for(nC + 1), 256, 0, st>>>(c_tptr, nC, keep, cnt, alive);
-  QM_LAUNCHED("k_filter_count");
-  size_t tb = sb;
-  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub, tb, keep, kpos, nT + 1, st));
-  tb = sb;
-  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub, tb, cnt, cpos, nC + 1, st));
-  tb = sb;
-  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub, tb, alive, apos, nC + 1, st));
-  k_filter_scatter_tri<<<grid_for(nT), 256, 0, st>>>(t2, nT, keep, kpos, (uint2 *)tri_out);
-  QM_LAUNCHED("k_filter_scatter_tri");
-  k_filter_scatter_c<<<grid_for(nC + 1), 256, 0, st>>>(c_keys, nC, alive, apos, cpos, c_keys_out, c_tptr_out);
-  QM_LAUNCHED("k_filter_scatter_c");
-  int64_t counts[2];
-  rc = read_device_i64(apos + nC, 1, counts, st, kpos + nT);
-  if (rc != QM_OK) return rc;
-  *nC_out = counts[0];
-  *nT_out = counts[1];
-  return QM_OK;
+  return filter_compact(t2, c_tptr, c_keys, nC, nT, keep, kpos, cnt, alive, cpos, apos, cub, sb, tri_out,
+                        c_tptr_out, c_keys_out, nC_out, nT_out, st);
 }
 
-extern "C" size_t qm_prune_all_workspace_bytes(int64_t cap_pairs) {
-  Carver cv(nullptr, 0);
-  cv.take<uint64_t>(std::max<int64_t>(cap_pairs, 1));  // ping
-  cv.take<uint64_t>(std::max<int64_t>(cap_pairs, 1));  // pong
-  cv.take<unsigned long long>(2 * kMaxLevels + 2);      // counters, log count, overflow
-  return cv.off;
-}
-
-extern "C" int qm_prune_all(const qm_layout *layout, double tau, const uint64_t *a_codes, const double *a_norms,
-                            int64_t a_stride, const int64_t *a_counts, int32_t a_sym, const uint64_t *b_codes,
-                            const double *b_norms, int64_t b_stride, const int64_t *b_counts, int32_t b_sym,
-                            int32_t b_transposed, int32_t upper, int64_t cap_pairs, uint64_t *leaf_pairs_out,
-                            double *log_out, int64_t cap_log, int64_t *counts_out, void *ws, size_t ws_bytes,
-                            void *stream) {
+extern "C" int qm_ancestor_norms(const qm_layout *layout, const uint64_t *keys, int64_t n, const uint64_t *codes,
+                                 const double *norms, int64_t stride, const int64_t *counts, int32_t sym,
+                                 double *out, void *stream) {
   Geometry g;
   int rc = make_geometry(layout, &g);
   if (rc != QM_OK) return rc;
-  if (!a_codes || !a_norms || !a_counts || !b_codes || !b_norms || !b_counts || !counts_out || cap_pairs < 1 ||
-      cap_log < 1 || !leaf_pairs_out || !log_out) {
-    set_error("qm_prune_all: bad arguments");
+  if (n < 0 || !counts || (n > 0 && (!keys || !codes || !norms || !out))) {
+    set_error("qm_ancestor_norms: bad arguments");
     return QM_ERR_INVALID;
   }
-  if (g.depth + 1 > kMaxLevels || g.depth >= kPairBits) {
-    set_error("qm_prune_all: depth %d exceeds %d", g.depth, kMaxLevels - 1);
+  if (g.depth + 1 > kMaxLevels) {
+    set_error("qm_ancestor_norms: depth %d exceeds %d", g.depth, kMaxLevels - 1);
+    return QM_ERR_UNSUPPORTED;
+  }
+  if (n == 0) return QM_OK;
+  PruneTables t;
+  memset(&t, 0, sizeof(t));
+  for (int l = 0; l <= g.depth; ++l) t.a[l] = Table{codes + (size_t)l * stride, norms + (size_t)l * stride, counts[l]};
+  cudaStream_t st = (cudaStream_t)stream;
+  k_ancestor_norms<<<grid_for(n), 256, 0, st>>>(keys, n, g.nbl, g.lbits, g.depth, t, sym, out);
+  QM_LAUNCHED("k_ancestor_norms");
+  return QM_OK;
+}
+
+extern "C" int qm_filter_triples_norms(const qm_layout *layout, double tau, const uint32_t *tri, const int64_t *c_tptr,
+                                       const uint64_t *c_keys, int64_t nC, int64_t nT, const double *anc_a,
+                                       int64_t nA, const double *anc_b, int64_t nB, uint32_t *tri_out,
+                                       int64_t *c_tptr_out, uint64_t *c_keys_out, int64_t *nC_out, int64_t *nT_out,
+                                       void *ws, size_t ws_bytes, void *stream) {
+  Geometry g;
+  int rc = make_geometry(layout, &g);
+  if (rc != QM_OK) return rc;
+  if (nC < 0 || nT < 0 || !nC_out || !nT_out || (nT > 0 && (!anc_a || !anc_b))) {
+    set_error("qm_filter_triples_norms: bad arguments");
+    return QM_ERR_INVALID;
+  }
+  if (g.depth + 1 > kMaxLevels) {
+    set_error("qm_filter_triples_norms: depth %d exceeds %d", g.depth, kMaxLevels - 1);
     return QM_ERR_UNSUPPORTED;
   }
   Carver cv(ws, ws_bytes);
-  uint64_t *ping = cv.take<uint64_t>(cap_pairs), *pong = cv.take<uint64_t>(cap_pairs);
-  unsigned long long *ctr = cv.take<unsigned long long>(2 * kMaxLevels + 2);
+  int64_t *keep = cv.take<int64_t>(nT + 1), *kpos = cv.take<int64_t>(nT + 1);
+  int64_t *cnt = cv.take<int64_t>(nC + 1), *alive = cv.take<int64_t>(nC + 1);
+  int64_t *cpos = cv.take<int64_t>(nC + 1), *apos = cv.take<int64_t>(nC + 1);
+  const size_t sb = std::max(scan_bytes(nT + 1), scan_bytes(nC + 1));
+  void *cub = cv.take<char>(sb);
   if (!cv.ok() || !ws) {
-    set_error("qm_prune_all: workspace %zu < required %zu", ws_bytes, cv.off);
+    set_error("qm_filter_triples_norms: workspace %zu < required %zu", ws_bytes, cv.off);
     return QM_ERR_WORKSPACE;
   }
   PruneTables t;
   memset(&t, 0, sizeof(t));
-  for (int l = 0; l <= g.depth; ++l) {
-    t.a[l] = Table{a_codes + (size_t)l * a_stride, a_norms + (size_t)l * a_stride, a_counts[l]};
-    t.b[l] = Table{b_codes + (size_t)l * b_stride, b_norms + (size_t)l * b_stride, b_counts[l]};
-    t.tau[l] = tau / ldexp(1.0, 3 * l);  // tau / 8.0**l (ops.py:232), exact power-of-two scaling
-  }
+  for (int l = 0; l <= g.depth; ++l) t.tau[l] = tau / ldexp(1.0, 3 * l);  // tau / 8.0**l (ops.py:232)
   cudaStream_t st = (cudaStream_t)stream;
-  QM_CUDA_TRY(cudaMemsetAsync(ctr, 0, (2 * kMaxLevels + 2) * sizeof(unsigned long long), st));
-  static PerDeviceInt occupancy;
-  int per_sm = 0;
-  rc = occupancy.get(&per_sm, [](int *x) -> int {
-    QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(x, k_prune_all, 256, 0));
-    return (int)QM_OK;
-  });
-  if (rc != QM_OK) return rc;
-  const int grid = device_sm_count() * std::max(1, std::min(per_sm, 4));
-  int depth = g.depth;
-  unsigned long long *cnt = ctr, *log_cnt = ctr + 2 * kMaxLevels;
-  unsigned int *overflow = (unsigned int *)(ctr + 2 * kMaxLevels + 1);
-  void *args[] = {(void *)&t,   (void *)&depth,   (void *)&a_sym,          (void *)&b_sym,  (void *)&b_transposed,
-                  (void *)&upper, (void *)&ping, (void *)&pong,          (void *)&leaf_pairs_out, (void *)&cap_pairs,
-                  (void *)&log_out, (void *)&cap_log, (void *)&cnt, (void *)&log_cnt, (void *)&overflow};
-  QM_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_prune_all, grid, 256, args, 0, st));
-  QM_LAUNCHED("k_prune_all");
-  // counts_out (host): [alive_0, pruned_0, ..., alive_depth, pruned_depth, log total, overflow]
-  unsigned long long host[2 * kMaxLevels + 2];
-  QM_CUDA_TRY(cudaMemcpyAsync(host, ctr, sizeof(host), cudaMemcpyDeviceToHost, st));
-  QM_CUDA_TRY(cudaStreamSynchronize(st));
-  for (int l = 0; l <= g.depth; ++l) {
-    counts_out[2 * l] = (int64_t)host[2 * l];
-    counts_out[2 * l + 1] = (int64_t)host[2 * l + 1];
-  }
-  counts_out[2 * (g.depth + 1)] = (int64_t)host[2 * kMaxLevels];
-  counts_out[2 * (g.depth + 1) + 1] = (int64_t)(unsigned int)host[2 * kMaxLevels + 1];
-  return QM_OK;
+  const uint2 *t2 = (const uint2 *)tri;
+  k_keep_by_norms<<<grid_for(nT + 1), 256, 0, st>>>(t2, nT, anc_a, nA, anc_b, nB, g.depth, t, keep);
+  QM_LAUNCHED("k_keep_by_norms");
+  return filter_compact(t2, c_tptr, c_keys, nC, nT, keep, kpos, cnt, alive, cpos, apos, cub, sb, tri_out,
+                        c_tptr_out, c_keys_out, nC_out, nT_out, st);
 }

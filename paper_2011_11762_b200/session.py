@@ -264,11 +264,11 @@ class MatrixSession:
                     from . import approximate  # noqa: PLC0415
 
                     b_norms, b_sym = (b, False) if args.get("tb") else (b_stored, bool(args.get("b_sym")))
-                    pr = approximate.prune(geom, a_stored, b_norms, tau, a_sym=bool(args.get("a_sym")),
-                                           b_sym=b_sym, upper=bool(args.get("upper")))
-                    self.last_engine = _EngineInfo(pr.prune_log, pr.pairs_per_level)
+                    pruner = approximate.Pruner(geom, a_stored, b_norms, tau, a_sym=bool(args.get("a_sym")),
+                                                b_sym=b_sym, upper=bool(args.get("upper")))
+                    self.last_engine = _EngineInfo(pruner)  # the prune log is computed on first read
                     ax, bx = a, b
-                    plan_filter = lambda plan: approximate.filter_plan(geom, plan, ax, bx, pr)  # noqa: E731
+                    plan_filter = lambda plan: pruner.filter(plan, ax, bx)  # noqa: E731
             # upper variants: the symbolic phase enumerates only the kept (upper-leaf) C blocks
             c = spgemm.multiply_blocks(layout, a, b, stats=stats, plan_filter=plan_filter,
                                        upper=bool(args.get("upper")))
@@ -517,19 +517,29 @@ class MatrixSession:
 
 class _EngineInfo:
     """What the reference's ``session.last_engine`` exposes for the approximate variant:
-    ``prune_log`` = bounds of the pruned subproducts (engine.py:156, 273-275). The bounds stay on
-    the device until first read (a product can prune ~10^5 tasks; the list is built on access)."""
+    ``prune_log`` = bounds of the pruned subproducts (engine.py:156, 273-275). The product itself
+    only needs the per-triple survival test (approximate.Pruner.filter); the log -- ~10^5 bounds --
+    is computed from the same node tables on first read and kept."""
 
-    def __init__(self, prune_log, pairs_per_level: list):
-        self._log = prune_log
-        self._list = None if isinstance(prune_log, torch.Tensor) else list(prune_log)
-        self.pairs_per_level = pairs_per_level
+    def __init__(self, source, pairs_per_level: list | None = None):
+        self._source = source  # an approximate.Pruner, or a ready log (list / device tensor)
+        self._list = None
+        self._pairs = pairs_per_level
 
     @property
     def prune_log(self) -> list:
         if self._list is None:
-            self._list = self._log.tolist()
+            src = self._source
+            log = src.result().prune_log if hasattr(src, "result") else src
+            self._list = log.tolist() if isinstance(log, torch.Tensor) else list(log)
         return self._list
+
+    @property
+    def pairs_per_level(self) -> list:
+        if self._pairs is None:
+            src = self._source
+            self._pairs = src.result().pairs_per_level if hasattr(src, "result") else []
+        return self._pairs
 
 
 def _read_coordinate_text(path):

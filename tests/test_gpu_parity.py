@@ -460,6 +460,46 @@ def test_approximate_multiply_matches_reference(ses, ci):
     assert diff <= skipped + 1e-12 and skipped <= tau + 1e-12
 
 
+@pytest.mark.parametrize("variant", ["approximate", "symmetric_square", "rank_k"])
+@pytest.mark.parametrize("n,leaf,bs,rel", [(512, 64, 16, 1e-4), (1024, 64, 64, 1e-6), (1000, 128, 32, 1e-3),
+                                           (2048, 256, 64, 1e-8)])
+def test_ancestor_norm_filter_equals_the_level_recursion(ses, monkeypatch, variant, n, leaf, bs, rel):
+    """The product's approximate filter (ancestor norms >= tau/8^l at every level, one pass over the
+    triples) keeps exactly the triples of the level-by-level pruned recursion (qm_prune_all's
+    surviving leaf pairs, filtered by qm_filter_triples), for general, symmetric and transposed
+    (rank_k) operands -- same triples in the same order, so bitwise the same product."""
+    from paper_2011_11762_b200 import approximate, variants
+
+    da = helpers.decay_sparse(n, n + bs, scale=3.0)
+    if variant == "symmetric_square":
+        sym = np.triu(da + da.T)
+        r, cc = np.nonzero(sym)
+        m = ses.matrix_from_triplets(n, r, cc, sym[r, cc], leaf_dim=leaf, block_size=bs, symmetric=True)
+    else:
+        m = helpers.build(ses, da, leaf, bs)
+    s = m.root.require()
+    geom = m.geometry
+    tau = rel * float(s.sumsq.sum().item())
+    lay = _ffi.make_layout(geom.params, bs)
+    a_sym = variant == "symmetric_square"
+    ax = variants.expand_symmetric_view(geom, s) if a_sym and variants.virtual_ok(bs) else (
+        variants.expand_symmetric(geom, s) if a_sym else s)
+    if variant == "rank_k":
+        bx = variants.transpose_view(geom, s) if variants.virtual_ok(bs) else variants.transpose(geom, s)
+        b_src, b_sym = bx, False
+    else:
+        bx, b_src, b_sym = ax, s, a_sym
+    upper = variant != "approximate"
+    plan = spgemm.symbolic(lay, ax, bx, upper=upper)
+    pruner = approximate.Pruner(geom, s, b_src, tau, a_sym=a_sym, b_sym=b_sym, upper=upper)
+    fast = pruner.filter(plan, ax, bx)
+    slow = approximate.filter_plan(geom, plan, ax, bx, pruner.result())
+    assert fast.n_triples < plan.n_triples or rel < 1e-7  # something was pruned (most cases)
+    assert (fast.n_c, fast.n_triples) == (slow.n_c, slow.n_triples)
+    assert torch.equal(fast.c_keys, slow.c_keys) and torch.equal(fast.c_tptr, slow.c_tptr)
+    assert torch.equal(fast.tri, slow.tri)
+
+
 @pytest.mark.parametrize("n,leaf,bs", [(512, 64, 16), (1000, 32, 32), (4096, 256, 64)])
 def test_node_norms_follow_the_reference_recursion(ses, n, leaf, bs):
     """qm_node_norms: every level's nodes are the non-nil quadtree nodes, and each norm is
