@@ -684,3 +684,74 @@ extern "C" int qm_filter_triples_norms(const qm_layout *layout, double tau, cons
   return filter_compact(t2, c_tptr, c_keys, nC, nT, keep, kpos, cnt, alive, cpos, apos, cub, sb, tri_out,
                         c_tptr_out, c_keys_out, nC_out, nT_out, st);
 }
+
+extern "C" size_t qm_prune_all_workspace_bytes(int64_t cap_pairs) {
+  Carver cv(nullptr, 0);
+  cv.take<uint64_t>(std::max<int64_t>(cap_pairs, 1));  // ping
+  cv.take<uint64_t>(std::max<int64_t>(cap_pairs, 1));  // pong
+  cv.take<unsigned long long>(2 * kMaxLevels + 2);      // counters, log count, overflow
+  return cv.off;
+}
+
+extern "C" int qm_prune_all(const qm_layout *layout, double tau, const uint64_t *a_codes, const double *a_norms,
+                            int64_t a_stride, const int64_t *a_counts, int32_t a_sym, const uint64_t *b_codes,
+                            const double *b_norms, int64_t b_stride, const int64_t *b_counts, int32_t b_sym,
+                            int32_t b_transposed, int32_t upper, int64_t cap_pairs, uint64_t *leaf_pairs_out,
+                            double *log_out, int64_t cap_log, int64_t *counts_out, void *ws, size_t ws_bytes,
+                            void *stream) {
+  Geometry g;
+  int rc = make_geometry(layout, &g);
+  if (rc != QM_OK) return rc;
+  if (!a_codes || !a_norms || !a_counts || !b_codes || !b_norms || !b_counts || !counts_out || cap_pairs < 1 ||
+      cap_log < 1 || !leaf_pairs_out || !log_out) {
+    set_error("qm_prune_all: bad arguments");
+    return QM_ERR_INVALID;
+  }
+  if (g.depth + 1 > kMaxLevels || g.depth >= kPairBits) {
+    set_error("qm_prune_all: depth %d exceeds %d", g.depth, kMaxLevels - 1);
+    return QM_ERR_UNSUPPORTED;
+  }
+  Carver cv(ws, ws_bytes);
+  uint64_t *ping = cv.take<uint64_t>(cap_pairs), *pong = cv.take<uint64_t>(cap_pairs);
+  unsigned long long *ctr = cv.take<unsigned long long>(2 * kMaxLevels + 2);
+  if (!cv.ok() || !ws) {
+    set_error("qm_prune_all: workspace %zu < required %zu", ws_bytes, cv.off);
+    return QM_ERR_WORKSPACE;
+  }
+  PruneTables t;
+  memset(&t, 0, sizeof(t));
+  for (int l = 0; l <= g.depth; ++l) {
+    t.a[l] = Table{a_codes + (size_t)l * a_stride, a_norms + (size_t)l * a_stride, a_counts[l]};
+    t.b[l] = Table{b_codes + (size_t)l * b_stride, b_norms + (size_t)l * b_stride, b_counts[l]};
+    t.tau[l] = tau / ldexp(1.0, 3 * l);  // tau / 8.0**l (ops.py:232), exact power-of-two scaling
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  QM_CUDA_TRY(cudaMemsetAsync(ctr, 0, (2 * kMaxLevels + 2) * sizeof(unsigned long long), st));
+  static PerDeviceInt occupancy;
+  int per_sm = 0;
+  rc = occupancy.get(&per_sm, [](int *x) -> int {
+    QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(x, k_prune_all, 256, 0));
+    return (int)QM_OK;
+  });
+  if (rc != QM_OK) return rc;
+  const int grid = device_sm_count() * std::max(1, std::min(per_sm, 4));
+  int depth = g.depth;
+  unsigned long long *cnt = ctr, *log_cnt = ctr + 2 * kMaxLevels;
+  unsigned int *overflow = (unsigned int *)(ctr + 2 * kMaxLevels + 1);
+  void *args[] = {(void *)&t,   (void *)&depth,   (void *)&a_sym,          (void *)&b_sym,  (void *)&b_transposed,
+                  (void *)&upper, (void *)&ping, (void *)&pong,          (void *)&leaf_pairs_out, (void *)&cap_pairs,
+                  (void *)&log_out, (void *)&cap_log, (void *)&cnt, (void *)&log_cnt, (void *)&overflow};
+  QM_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_prune_all, grid, 256, args, 0, st));
+  QM_LAUNCHED("k_prune_all");
+  // counts_out (host): [alive_0, pruned_0, ..., alive_depth, pruned_depth, log total, overflow]
+  unsigned long long host[2 * kMaxLevels + 2];
+  QM_CUDA_TRY(cudaMemcpyAsync(host, ctr, sizeof(host), cudaMemcpyDeviceToHost, st));
+  QM_CUDA_TRY(cudaStreamSynchronize(st));
+  for (int l = 0; l <= g.depth; ++l) {
+    counts_out[2 * l] = (int64_t)host[2 * l];
+    counts_out[2 * l + 1] = (int64_t)host[2 * l + 1];
+  }
+  counts_out[2 * (g.depth + 1)] = (int64_t)host[2 * kMaxLevels];
+  counts_out[2 * (g.depth + 1) + 1] = (int64_t)(unsigned int)host[2 * kMaxLevels + 1];
+  return QM_OK;
+}
