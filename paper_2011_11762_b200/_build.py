@@ -1,8 +1,9 @@
 """In-tree build of libqmb200.so (sm_100a) with nvcc.
 
 The shared library is written next to this file so it travels with the repo snapshot to the GPU
-box (a JIT cache under ~/.cache would not). Objects are rebuilt only when a source or header is
-newer than the library.
+box (a JIT cache under ~/.cache would not). The library is rebuilt when the content digest of its
+sources, headers, this script and the flags differs from the one recorded next to it
+(libqmb200.so.sha256), never on timestamps alone.
 """
 
 from __future__ import annotations
@@ -45,22 +46,37 @@ def sources() -> list[Path]:
     return sorted(CSRC.glob("*.cu"))
 
 
-def _stale() -> bool:
-    if not LIB.exists():
+STAMP = LIB.with_name(LIB.name + ".sha256")
+
+
+def source_digest(extra_flags=()) -> str:
+    """sha256 over every source and header the library is built from, this build script and the
+    compiler flags: the library is rebuilt whenever any of them changes (content, not mtime)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    deps = sorted(sources()) + sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.glob("*.h")) + [Path(__file__)]
+    for p in deps:
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    h.update(" ".join([*NVCC_FLAGS, *extra_flags]).encode())
+    return h.hexdigest()
+
+
+def _stale(extra_flags=()) -> bool:
+    if not LIB.exists() or not STAMP.exists():
         return True
-    t = LIB.stat().st_mtime
-    deps = list(sources()) + list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h")) + [Path(__file__)]
-    return any(p.stat().st_mtime > t for p in deps)
+    return STAMP.read_text().strip() != source_digest(extra_flags)
 
 
 def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) -> Path:
     """Compile every .cu under csrc/ for sm_100a and link libqmb200.so in-tree."""
-    if not force and not _stale():
+    extra = ["-Xptxas", "-v"] if ptxas_info else []
+    extra += os.environ.get("QM_NVCC_EXTRA", "").split()  # experiments only (e.g. -DQM_EXP_...)
+    if not force and not _stale(extra):
         return LIB
     nvcc = nvcc_path()
     OBJ_DIR.mkdir(parents=True, exist_ok=True)
-    extra = ["-Xptxas", "-v"] if ptxas_info else []
-    extra += os.environ.get("QM_NVCC_EXTRA", "").split()  # experiments only (e.g. -DQM_EXP_...)
 
     def compile_one(src: Path) -> tuple[Path, str]:
         obj = OBJ_DIR / (src.stem + ".o")
@@ -82,6 +98,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    STAMP.write_text(source_digest(extra) + "\n")
     return LIB
 
 

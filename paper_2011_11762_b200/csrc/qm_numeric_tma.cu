@@ -125,14 +125,24 @@ __device__ __forceinline__ bool cur_last(const Cur &c) {
 // Advances the producer's cursor; a finished unit is replaced by the next one claimed from the
 // global work counter just in time (claiming a unit ahead widened the window of units in flight
 // and raised DRAM re-reads of A/B by 2x with 3 CTAs/SM).
+// ahead: the next claim is taken one unit early (*next holds it), so the counter's round trip
+// overlaps the current unit's loads instead of stalling the producer between units -- for units of
+// one or two stages (about one triple per C block) that latency is a visible share of the unit.
 template <class Cfg>
 __device__ __forceinline__ void cur_next(Cur &c, int64_t nU, const int64_t *tptr, const uint32_t *order,
-                                         const uint8_t *tri_sm, unsigned long long *counter) {
+                                         const uint8_t *tri_sm, unsigned long long *counter, bool ahead,
+                                         int64_t *next) {
   const uint32_t rest = c.sm & ~((2u << c.p) - 1u);
   if (rest) {
     c.p = __ffs(rest) - 1;
   } else if (++c.t == c.tend) {
-    cur_start<Cfg>(c, (int64_t)gridDim.x + (int64_t)atomicAdd(counter, 1ull), nU, tptr, order, tri_sm);
+    if (ahead) {
+      const int64_t u = *next;
+      *next = u < nU ? (int64_t)gridDim.x + (int64_t)atomicAdd(counter, 1ull) : u;
+      cur_start<Cfg>(c, u, nU, tptr, order, tri_sm);
+    } else {
+      cur_start<Cfg>(c, (int64_t)gridDim.x + (int64_t)atomicAdd(counter, 1ull), nU, tptr, order, tri_sm);
+    }
   } else {
     c.sm = triple_panels<Cfg>(tri_sm, c.t);
     c.p = __ffs(c.sm) - 1;
@@ -146,7 +156,8 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
                   double *__restrict__ C, double *__restrict__ csq, uint8_t *__restrict__ cnz,
                   int64_t *__restrict__ zero_count, double *__restrict__ part_sq,
                   uint8_t *__restrict__ part_nz, unsigned long long *__restrict__ counter,
-                  const uint32_t *__restrict__ order, const uint8_t *__restrict__ tri_sm, uint64_t zmask) {
+                  const uint32_t *__restrict__ order, const uint8_t *__restrict__ tri_sm, uint64_t zmask,
+                  bool claim_ahead) {
   constexpr int BS = Cfg::BS, MT = Cfg::MT, NT = Cfg::NT, STAGES = Cfg::STAGES;
   const int64_t nU = nC * Cfg::NQ;
   // Align to 1 KB (SWIZZLE_128B atoms) by offsetting the __shared__ array itself: the pointer keeps
@@ -181,6 +192,7 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
       // and no CTA is left with a long tail of heavy units.
       Cur L;
       cur_start<Cfg>(L, blockIdx.x, nU, tptr, order, tri_sm);
+      int64_t next = claim_ahead && L.unit < nU ? (int64_t)gridDim.x + (int64_t)atomicAdd(counter, 1ull) : nU;
       int s = 0;
       uint32_t phase = 0;
       while (true) {
@@ -235,7 +247,7 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
             tma_load_2d(st + Cfg::A_BYTES + q * Cfg::B_SP_BYTES, &maps.b[bo], col0 + q * 16,
                         (int)(bl * BS + L.p * Cfg::KP), &full[s]);
         }
-        cur_next<Cfg>(L, nU, tptr, order, tri_sm, counter);
+        cur_next<Cfg>(L, nU, tptr, order, tri_sm, counter, claim_ahead, &next);
         if (++s == STAGES) {
           s = 0;
           phase ^= 1u;
@@ -440,6 +452,15 @@ __global__ void k_triple_panels(const uint2 *tri, int64_t nT, const uint64_t *a_
 
 int sm_count_tma() { return device_sm_count(); }
 
+// Claim-ahead policy (cur_next): QM_CLAIM_AHEAD=1|0 forces it; by default it is used when C blocks
+// have fewer than 2 triples on average (units of one or two stages).
+bool claim_ahead(int64_t nC, int64_t nT) {
+  const char *e = getenv("QM_CLAIM_AHEAD");
+  if (e && e[0] == '1') return true;
+  if (e && e[0] == '0') return false;
+  return nT < 2 * nC;
+}
+
 // Claim order of the C blocks. Quadtree-key order is the default: neighbouring block rows and
 // columns of A/B stay in L2 when C blocks have several triples (banded, decay). Two alternatives,
 // measured and kept as options (QM_UNIT_ORDER=k|lpt):
@@ -582,7 +603,8 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
     panel_fill = -1;  // counted by k_triple_panels
   }
   k_numeric_tma<Cfg, NPOOL, TR><<<(int)grid, Cfg::NTHR, Cfg::SMEM, st>>>(
-      maps, tri, tptr, nC, C, csq, cnz, zc, part_sq, part_nz, counter, order, tri_sm, /*zmask=*/0ull);
+      maps, tri, tptr, nC, C, csq, cnz, zc, part_sq, part_nz, counter, order, tri_sm, /*zmask=*/0ull,
+      claim_ahead(nC, nT));
   QM_LAUNCHED("k_numeric_tma");
   {
     int64_t g = std::min<int64_t>((nC + 255) / 256, (int64_t)sm_count_tma() * 8);

@@ -208,18 +208,28 @@ __device__ __forceinline__ void row_key_cols(uint32_t i, uint64_t klo, uint64_t 
 }
 
 // Applies the per-row column restrictions of the workspace flags to a row span: the upper variant
-// (leaves li <= lj) and a rank's key range. Returns false when the row has nothing left.
-__device__ __forceinline__ bool clamp_row(RowSpan &s, int64_t i, int flags, const uint64_t *krange, int64_t nbg,
-                                          int nbl, int lbits) {
+// (leaves li <= lj) and a rank's key range (per-row column bounds rb[i] = (jlo, jhi), k_row_bounds).
+// Returns false when the row has nothing left; *raised = the first column moved past the row's own
+// first column (the pair loops must then binary-search their B rows' start).
+__device__ __forceinline__ bool clamp_row(RowSpan &s, int64_t i, int flags, const uint2 *rb, int nbl,
+                                          bool *raised) {
+  const uint32_t j0 = s.jmin;
   if (flags & kFlagUpper) s.jmin = max(s.jmin, (uint32_t)((i / nbl) * nbl));
   if (flags & kFlagRanged) {
-    uint32_t jlo, jhi;
-    row_key_cols((uint32_t)i, krange[0], krange[1], nbg, nbl, lbits, &jlo, &jhi);
-    s.jmin = max(s.jmin, jlo);
-    if (jhi == 0) return false;
-    s.jmax = min(s.jmax, jhi - 1u);
+    const uint2 b = rb[i];
+    s.jmin = max(s.jmin, b.x);
+    if (b.y == 0) return false;
+    s.jmax = min(s.jmax, b.y - 1u);
   }
+  *raised = s.jmin > j0;
   return s.nt > 0 && s.jmin <= s.jmax;
+}
+
+// A ranged row with no column in the rank's key range (skipped before any of its work).
+__device__ __forceinline__ bool row_out_of_range(int64_t i, int flags, const uint2 *rb) {
+  if (!(flags & kFlagRanged)) return false;
+  const uint2 b = rb[i];
+  return b.x >= b.y;
 }
 
 // Calls f(x, y, j) for every pair (A entry x of the row, B entry y of row k(x)) whose column j is
@@ -254,7 +264,7 @@ __device__ void for_window_pairs(const RowSpan &s, uint32_t wbase, bool multi, c
 __global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const uint32_t *a_scol,
                                                    const uint32_t *b_rp, const uint32_t *b_scol,
                                                    const uint64_t *smask, const int *masked_flag,
-                                                   const uint64_t *krange, int64_t nbg, int nbl, int lbits,
+                                                   const uint2 *rb, int64_t nbg, int nbl, int lbits,
                                                    uint64_t *cnt, uint64_t *off, unsigned int *done,
                                                    volatile int64_t *host_tot) {
   __shared__ uint32_t bm[kWin / 32];
@@ -263,20 +273,22 @@ __global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const u
   __shared__ bool last;
   const int flags = *masked_flag;
   const bool masked = (flags & kFlagMasked) != 0;
-  const bool clamped = (flags & (kFlagUpper | kFlagRanged)) != 0;  // rows start past their first column
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt[2 * nbg] = 0;  // exclusive-scan tail
   for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
-    RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
     uint32_t total = 0;
     uint64_t ntri = 0;  // surviving triples of the row (<= s.nt, the structural count)
-    if (clamp_row(s, i, flags, krange, nbg, nbl, lbits)) {
+    bool raised = false;
+    RowSpan s;
+    if (!row_out_of_range(i, flags, rb)) s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
+    else s.nt = 0;
+    if (s.nt > 0 && clamp_row(s, i, flags, rb, nbl, &raised)) {
       const bool multi = (s.jmax - s.jmin) >= (uint32_t)kWin;
       for (uint64_t wb = s.jmin; wb <= s.jmax; wb += kWin) {
         const uint32_t wbase = (uint32_t)wb;
         for (int w = threadIdx.x; w < kWin / 32; w += blockDim.x) bm[w] = 0u;
         __syncthreads();
         uint64_t mine = 0;
-        for_window_pairs(s, wbase, multi || clamped, a_scol, b_rp, b_scol, smask, masked, [&](uint32_t, uint32_t, uint32_t j) {
+        for_window_pairs(s, wbase, multi || raised, a_scol, b_rp, b_scol, smask, masked, [&](uint32_t, uint32_t, uint32_t j) {
           uint32_t o = j - wbase;
           atomicOr(&bm[o >> 5], 1u << (o & 31));
           ++mine;
@@ -312,7 +324,7 @@ __global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const u
 __global__ void __launch_bounds__(kNT) k_sym_emit_c(const uint32_t *a_rp, const uint32_t *a_scol,
                                                     const uint32_t *b_rp, const uint32_t *b_scol,
                                                     const uint64_t *smask, const int *masked_flag,
-                                                    const uint64_t *krange, int64_t nbg, int nbl, int lbits,
+                                                    const uint2 *rb, int64_t nbg, int nbl, int lbits,
                                                     const uint64_t *rowC_off, uint64_t *rm_key,
                                                     uint32_t *rm_cnt, uint32_t *rm_iota, unsigned int *done) {
   __shared__ uint32_t cnt[kWin];
@@ -321,17 +333,18 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_c(const uint32_t *a_rp, const 
   if (blockIdx.x == 0 && threadIdx.x == 0) *done = 0u;  // k_inv_counts' completion ticket
   const int flags = *masked_flag;
   const bool masked = (flags & kFlagMasked) != 0;
-  const bool clamped = (flags & (kFlagUpper | kFlagRanged)) != 0;
   for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
+    if (rowC_off[i + 1] == rowC_off[i]) continue;  // no C block in this row (block-uniform)
     RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
-    if (clamp_row(s, i, flags, krange, nbg, nbl, lbits)) {
+    bool raised = false;
+    if (clamp_row(s, i, flags, rb, nbl, &raised)) {
       uint64_t out = rowC_off[i];
       const bool multi = (s.jmax - s.jmin) >= (uint32_t)kWin;
       for (uint64_t wb = s.jmin; wb <= s.jmax; wb += kWin) {
         const uint32_t wbase = (uint32_t)wb;
         for (int w = threadIdx.x; w < kWin; w += blockDim.x) cnt[w] = 0u;
         __syncthreads();
-        for_window_pairs(s, wbase, multi || clamped, a_scol, b_rp, b_scol, smask, masked,
+        for_window_pairs(s, wbase, multi || raised, a_scol, b_rp, b_scol, smask, masked,
                          [&](uint32_t, uint32_t, uint32_t j) { atomicAdd(&cnt[j - wbase], 1u); });
         __syncthreads();
         const int s0 = threadIdx.x * kPer;
@@ -369,7 +382,7 @@ static_assert(kPerT == 8, "slot ownership assumes 8 slots per thread");
 __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
     const uint32_t *a_rp, const uint32_t *a_scol, const uint32_t *a_perm, const uint32_t *b_rp,
     const uint32_t *b_scol, const uint32_t *b_perm, const uint64_t *smask, const int *masked_flag,
-    const uint64_t *krange, int64_t nbg, int nbl, int lbits, const uint64_t *rowC_off,
+    const uint2 *rb, int64_t nbg, int nbl, int lbits, const uint64_t *rowC_off,
     const uint32_t *inv, const int64_t *c_tptr, int64_t t_lo, int64_t t_hi, uint2 *tri) {
   __shared__ uint32_t mask[kWinT];
   __shared__ int64_t cur[kWinT];
@@ -381,7 +394,6 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
   const bool ranged = t_lo > 0 || t_hi < c_tptr[rowC_off[nbg]];
   const int flags = *masked_flag;
   const bool masked = (flags & kFlagMasked) != 0;
-  const bool upper = (flags & (kFlagUpper | kFlagRanged)) != 0;  // rows start past their first column
   for (int64_t i = blockIdx.x; i < nbg; i += gridDim.x) {
     if (ranged) {
       // A multi-GPU rank emits one triple range: skip rows none of whose C blocks reach it
@@ -397,8 +409,10 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
                                  red64) - 1;
       if (hi <= t_lo || lo >= t_hi) continue;
     }
+    if (rowC_off[i + 1] == rowC_off[i]) continue;  // no C block in this row (block-uniform)
     RowSpan s = row_span(i, a_rp, a_scol, b_rp, b_scol, red64, red32);
-    if (clamp_row(s, i, flags, krange, nbg, nbl, lbits)) {
+    bool upper = false;  // the row's first column was raised: binary-search the B rows' start
+    if (clamp_row(s, i, flags, rb, nbl, &upper)) {
       uint64_t out = rowC_off[i];
       const bool multi = (s.jmax - s.jmin) >= (uint32_t)kWinT;
       for (uint64_t wb = s.jmin; wb <= s.jmax; wb += kWinT) {
@@ -522,13 +536,10 @@ __global__ void k_tile_work(const uint32_t *srow, const uint32_t *scol, int64_t 
 // (nearly) equal work (the first tile whose exclusive prefix reaches r*W/world starts rank r, as
 // distributed.partition cuts c_tptr), and this rank's C key range [krange[0], krange[1]) -- a union
 // of whole quadtree subtrees, so C stays a contiguous Morton range per rank.
-__global__ void __launch_bounds__(kNT) k_tile_cut(const uint64_t *tiles, int64_t ntiles, uint64_t *prefix,
+__global__ void __launch_bounds__(kNT) k_tile_cut(const uint64_t *prefix, int64_t ntiles,
                                                   int world, int rank, int kshift, uint64_t *krange,
                                                   uint64_t *key_cuts, int *flags, volatile int64_t *host_out) {
-  __shared__ uint64_t wsum[32];
-  cta_exclusive_scan64(tiles, prefix, ntiles + 1, wsum);  // tiles[ntiles] is the zeroed tail
-  __syncthreads();
-  const uint64_t W = prefix[ntiles];
+  const uint64_t W = prefix[ntiles];  // exclusive prefix of the tile work (tail = total)
   for (int r = threadIdx.x; r <= world; r += blockDim.x) {
     int64_t cut;
     if (r == 0) {
@@ -559,6 +570,17 @@ __global__ void __launch_bounds__(kNT) k_tile_cut(const uint64_t *tiles, int64_t
   }
 }
 
+// Per-row column bounds of this rank's key range: rb[i] = (first, end) column of row i whose keys
+// lie in [krange[0], krange[1]) -- one interval, keys being monotone in the column.
+__global__ void k_row_bounds(const uint64_t *krange, int64_t nbg, int nbl, int lbits, uint2 *rb) {
+  const uint64_t klo = krange[0], khi = krange[1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nbg; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t jlo, jhi;
+    row_key_cols((uint32_t)i, klo, khi, nbg, nbl, lbits, &jlo, &jhi);
+    rb[i] = make_uint2(jlo, jhi);
+  }
+}
+
 inline int grid_for(int64_t n, int threads = 256) {
   int64_t g = (n + threads - 1) / threads;
   if (g < 1) g = 1;
@@ -583,6 +605,7 @@ struct SymWs {
   uint64_t *off;   // exclusive scan of cnt: rowC_off = off, nC = off[nbg], nT = off[2nbg] - off[nbg]
   unsigned int *done;  // k_sym_count's completion ticket
   uint64_t *krange;    // [2]: this rank's C key range (flag kFlagRanged; qm_spgemm_count_part)
+  uint2 *rb;           // [nbg]: per-row column bounds of the key range (k_row_bounds)
   uint64_t *tiles;     // [4^tile_levels]: structural triples per C tile (qm_spgemm_count_part)
   int tile_levels;
   void *cub;
@@ -603,6 +626,12 @@ size_t cub_bytes_count(int64_t n, int64_t nbg) {
 constexpr int kMaxTileLevels = 8;
 inline int tile_levels_for(const Geometry &g) { return g.depth < kMaxTileLevels ? g.depth : kMaxTileLevels; }
 
+size_t cub_bytes_scan(int64_t ntiles) {
+  size_t b = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (uint64_t *)nullptr, (uint64_t *)nullptr, ntiles + 1);
+  return b;
+}
+
 SymWs carve_sym(Carver &cv, int64_t nA, int64_t nB, int64_t nbg, int tile_levels) {
   SymWs w;
   const int64_t n = nA + nB;
@@ -615,9 +644,10 @@ SymWs carve_sym(Carver &cv, int64_t nA, int64_t nB, int64_t nbg, int tile_levels
   w.off = cv.take<uint64_t>(2 * nbg + 1);
   w.done = cv.take<unsigned int>(1);
   w.krange = cv.take<uint64_t>(2);
+  w.rb = cv.take<uint2>(nbg);
   w.tile_levels = tile_levels;
   w.tiles = cv.take<uint64_t>(2 * ((size_t)1 << (2 * tile_levels)) + 2);  // work [+ tail], prefix
-  w.cub_bytes = cub_bytes_count(n, nbg);
+  w.cub_bytes = std::max(cub_bytes_count(n, nbg), cub_bytes_scan((int64_t)1 << (2 * tile_levels)));
   w.cub = cv.take<char>(w.cub_bytes);
   return w;
 }
@@ -728,11 +758,16 @@ int count_impl(const qm_layout *layout, const uint64_t *a_keys, const uint64_t *
       k_tile_work<<<grid_for(nA), 256, 0, st>>>(w.srow, w.scol, nA, b_rp, g.nbl, g.depth - tl, w.tiles);
       QM_LAUNCHED("k_tile_work");
     }
-    k_tile_cut<<<1, kNT, 0, st>>>(w.tiles, ntiles, w.tiles + ntiles + 1, world, rank,
-                                   2 * (g.depth - tl) + 2 * g.lbits, w.krange, key_cuts, w.masked, dev_tot);
+    uint64_t *prefix = w.tiles + ntiles + 1;
+    size_t tb = w.cub_bytes;
+    QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(w.cub, tb, w.tiles, prefix, ntiles + 1, st));
+    k_tile_cut<<<1, kNT, 0, st>>>(prefix, ntiles, world, rank, 2 * (g.depth - tl) + 2 * g.lbits, w.krange,
+                                   key_cuts, w.masked, dev_tot);
     QM_LAUNCHED("k_tile_cut");
+    k_row_bounds<<<grid_for(g.nbg), 256, 0, st>>>(w.krange, g.nbg, g.nbl, g.lbits, w.rb);
+    QM_LAUNCHED("k_row_bounds");
   }
-  k_sym_count<<<row_grid(g.nbg), kNT, 0, st>>>(a_rp, w.scol, b_rp, w.scol, w.smask, w.masked, w.krange, g.nbg,
+  k_sym_count<<<row_grid(g.nbg), kNT, 0, st>>>(a_rp, w.scol, b_rp, w.scol, w.smask, w.masked, w.rb, g.nbg,
                                                g.nbl, g.lbits, w.cnt, w.off, w.done, dev_tot);
   QM_LAUNCHED("k_sym_count");
   QM_CUDA_TRY(cudaStreamSynchronize(st));
@@ -822,7 +857,7 @@ extern "C" int qm_spgemm_fill_keys(const qm_layout *layout, int64_t nA, int64_t 
   if (rc != QM_OK) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   if (nC == 0) return cudaMemsetAsync(c_tptr, 0, sizeof(int64_t), st) == cudaSuccess ? QM_OK : QM_ERR_CUDA;
-  k_sym_emit_c<<<row_grid(g.nbg), kNT, 0, st>>>(w.rp, w.scol, w.rp + g.nbg, w.scol, w.smask, w.masked, w.krange,
+  k_sym_emit_c<<<row_grid(g.nbg), kNT, 0, st>>>(w.rp, w.scol, w.rp + g.nbg, w.scol, w.smask, w.masked, w.rb,
                                                 g.nbg, g.nbl, g.lbits, w.off, f.rm_key, f.rm_cnt, f.rm_iota, f.done);
   QM_LAUNCHED("k_sym_emit_c");
   size_t tb = f.cub_bytes;
@@ -852,7 +887,7 @@ extern "C" int qm_spgemm_fill_triples(const qm_layout *layout, int64_t nA, int64
   if (nC == 0 || t_hi <= t_lo) return QM_OK;
   cudaStream_t st = (cudaStream_t)stream;
   k_sym_emit_tri<<<row_grid(g.nbg), kNT, 0, st>>>(w.rp, w.scol, w.perm, w.rp + g.nbg, w.scol,
-                                                  w.perm, w.smask, w.masked, w.krange, g.nbg, g.nbl, g.lbits, w.off,
+                                                  w.perm, w.smask, w.masked, w.rb, g.nbg, g.nbl, g.lbits, w.off,
                                                   f.inv, c_tptr, t_lo, t_hi, (uint2 *)tri);
   QM_LAUNCHED("k_sym_emit_tri");
   return QM_OK;
