@@ -178,7 +178,8 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        # QM_LIB_PATH: an experimental build of the same library (A/B kernel variants); default in-tree
+        p = Path(path) if path else Path(os.environ.get("QM_LIB_PATH") or LIB_PATH)
         if not p.exists():
             raise DeviceUnavailableError(
                 f"{p} is not built; run paper_2011_11762_b200._build.build() (nvcc, sm_100a)"

@@ -195,6 +195,9 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
       int64_t next = claim_ahead && L.unit < nU ? (int64_t)gridDim.x + (int64_t)atomicAdd(counter, 1ull) : nU;
       int s = 0;
       uint32_t phase = 0;
+#if defined(QM_EXP_DEPHASE) && QM_EXP_DEPHASE > 0
+      if (blockIdx.x >= gridDim.x / 2) __nanosleep(QM_EXP_DEPHASE);
+#endif
       while (true) {
         mbar_wait(&empty[s], phase ^ 1u);
         if (L.unit >= nU) {
@@ -364,16 +367,22 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
           const double v0 = acc[i][n][0], v1 = acc[i][n][1];
+#if !defined(QM_EXP_EPI) || QM_EXP_EPI != 1
           st_evict_first(cb + (size_t)(wm0 + i * 8 + g) * BS + wn0 + n * 8 + 2 * tq, v0, v1, c_policy);
+#endif
           ss0 = fma(v0, v0, ss0);
           ss1 = fma(v1, v1, ss1);
           nz |= (v0 != 0.0) | (v1 != 0.0);
           acc[i][n][0] = acc[i][n][1] = 0.0;
         }
       double ss = ss0 + ss1;
+#if defined(QM_EXP_EPI) && QM_EXP_EPI == 2
+      const bool wnz = true;
+#else
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
       const bool wnz = __any_sync(0xffffffffu, nz);
+#endif
       if (lane == 0) {
         part_sq[unit * Cfg::NCW + warp] = ss;
         part_nz[unit * Cfg::NCW + warp] = wnz;
