@@ -217,6 +217,52 @@ QM_API int qm_numeric_pools(const qm_layout *layout, const double *const *a_pool
 QM_API int qm_ipc_export(const void *ptr, void *handle_out, int64_t *offset_out);
 QM_API int qm_ipc_open(const void *handle, void **base_out);
 QM_API int qm_ipc_close(void *base);
+/* Halo of a staged multi-GPU product: the blocks one rank reads from its peers' pools. */
+#define QM_MAX_RANKS 8
+typedef struct qm_halo {
+  int32_t world;                      /* ranks (<= QM_MAX_RANKS) */
+  int32_t reserved;                   /* must be 0 */
+  const uint32_t *index[2];           /* device: global block indices of the A / B halo, ascending */
+  int64_t count[2];                   /* entries of index[0] / index[1] */
+  double *pool[2];                    /* device: halo pools; block x of index[o] lands at pool[o] + x */
+  uint64_t peer_base[2][QM_MAX_RANKS];/* address of rank r's A / B pool (peer memory mapped by qm_ipc_open) */
+  int64_t offset[2][QM_MAX_RANKS + 1];/* rank r owns global indices [offset[o][r], offset[o][r+1]) */
+  int64_t min_ns;                     /* measurement only: the gather lasts at least this long */
+} qm_halo;
+
+/* Staged multi-GPU numeric phase (replaces the remote-operand fetches of the reference's transfer
+ * layer, TransferSim.fetch chunkstore.py:188-210, for the blocks one worker's tasks read). As
+ * qm_numeric_pools, plus:
+ *   mask_tri / a_cmask, a_flags / b_rmask, b_flags: support masks (A's column masks, B's row masks,
+ *     NaN/Inf flags; qm_block_meta's rows) indexed by mask_tri (the triples in the masks' index
+ *     space, e.g. global block indices), so k panels are skipped as in qm_numeric_masked (all NULL:
+ *     no skipping);
+ *   order: claim order, one C block index per claim (NULL: key order);
+ *   halo (NULL: none): before the numeric kernel, a gather kernel copies the halo blocks from the
+ *     peer pools (read over NVLink) into the halo pools with bulk (TMA) copies on a few SMs; the
+ *     numeric kernel is launched as its programmatic dependent and runs meanwhile: claims <
+ *     gate_units (the local-only C blocks, put first by `order`) go ahead, claims >= gate_units wait
+ *     for the gather grid to complete. */
+QM_API int qm_numeric_pools_ex(const qm_layout *layout, const double *const *a_pools, const int64_t *a_counts,
+                               int32_t n_a_pools, const double *const *b_pools, const int64_t *b_counts,
+                               int32_t n_b_pools, const uint32_t *tri, const uint32_t *mask_tri,
+                               const uint64_t *a_cmask, const uint64_t *a_flags, const uint64_t *b_rmask,
+                               const uint64_t *b_flags, const uint32_t *order, const qm_halo *halo, int64_t gate_units,
+                               const int64_t *c_tptr, int64_t nC, int64_t nT, double *c_blocks, double *c_sumsq,
+                               uint8_t *c_nonzero, int64_t *zero_count, int64_t *panel_count, void *ws,
+                               size_t ws_bytes, void *stream);
+/* Staging plan of one rank (device; the host only reads the three counts). tri: the rank's
+ * triples in global block indices (uint32 pairs); the rank owns A indices [a_lo, a_hi) of nA and
+ * B indices [b_lo, b_hi) of nB (b_is_a: one operand, one halo). Writes
+ *   tri_packed[2*nT]: local index, or (1 << 28) | halo position for a block owned by a peer;
+ *   order[nC]: C blocks whose triples are all local first, then the others (key order in each);
+ *   halo_a / halo_b: the distinct peer-owned indices, ascending (capacity nA - (a_hi - a_lo), ...);
+ *   counts_out (host): [local-only C blocks, halo_a entries, halo_b entries]. Synchronises. */
+QM_API size_t qm_stage_plan_workspace_bytes(int64_t nA, int64_t nB, int64_t nC, int32_t b_is_a);
+QM_API int qm_stage_plan(const uint32_t *tri, int64_t nT, const int64_t *c_tptr, int64_t nC, int64_t a_lo,
+                         int64_t a_hi, int64_t nA, int64_t b_lo, int64_t b_hi, int64_t nB, int32_t b_is_a,
+                         void *ws, size_t ws_bytes, uint32_t *tri_packed, uint32_t *order, uint32_t *halo_a,
+                         uint32_t *halo_b, int64_t *counts_out, void *stream);
 /* Which numeric kernel qm_numeric uses for this block size: 2 = TMA + mbarrier warp-specialised
  * DMMA (bs 32/64/128; bs 16 as grouped leaf-row segments when a leaf holds >= 2 blocks per side),
  * 1 = cp.async DMMA (QM_NUMERIC=cpasync, or bs 16 with one block per leaf), 0 = FP64 SIMT. */

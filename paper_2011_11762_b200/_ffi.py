@@ -53,6 +53,9 @@ EXPORTS = (
     "qm_ipc_export",
     "qm_ipc_open",
     "qm_ipc_close",
+    "qm_numeric_pools_ex",
+    "qm_stage_plan_workspace_bytes",
+    "qm_stage_plan",
     "qm_numeric_path",
     "qm_compact_workspace_bytes",
     "qm_compact",
@@ -99,6 +102,23 @@ _I32 = ctypes.c_int32
 _SZ = ctypes.c_size_t
 _LP = ctypes.POINTER(QmLayout)
 
+MAX_RANKS = 8  # QM_MAX_RANKS
+
+
+class QmHalo(ctypes.Structure):
+    """include/qmb200.h qm_halo: the peer-owned blocks one rank gathers (staged multi-GPU product)."""
+
+    _fields_ = [
+        ("world", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("index", ctypes.c_void_p * 2),
+        ("count", ctypes.c_int64 * 2),
+        ("pool", ctypes.c_void_p * 2),
+        ("peer_base", (ctypes.c_uint64 * MAX_RANKS) * 2),
+        ("offset", (ctypes.c_int64 * (MAX_RANKS + 1)) * 2),
+        ("min_ns", ctypes.c_int64),
+    ]
+
 _SIGS = {
     "qm_abi_version": (ctypes.c_int, []),
     "qm_last_error": (ctypes.c_char_p, []),
@@ -132,6 +152,11 @@ _SIGS = {
     "qm_ipc_export": (ctypes.c_int, [_P, _P, ctypes.POINTER(_I64)]),
     "qm_ipc_open": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
     "qm_ipc_close": (ctypes.c_int, [_P]),
+    "qm_numeric_pools_ex": (ctypes.c_int, [_LP, _P, _P, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
+                                           _I64, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "qm_stage_plan_workspace_bytes": (_SZ, [_I64, _I64, _I64, _I32]),
+    "qm_stage_plan": (ctypes.c_int, [_P, _I64, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _P, _SZ, _P, _P,
+                                     _P, _P, ctypes.POINTER(_I64), _P]),
     "qm_numeric_pools": (ctypes.c_int, [_LP, _P, _P, _I32, _P, _P, _I32, _P, _P, _I64, _I64, _P, _P, _P, _P,
                                         _P, _SZ, _P]),
     "qm_numeric_path": (ctypes.c_int, [_I32]),

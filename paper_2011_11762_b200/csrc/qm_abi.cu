@@ -6,6 +6,7 @@
 #include <string.h>
 
 #include <atomic>
+#include <vector>
 
 #include <cuda.h>
 #include <cudaTypedefs.h>

@@ -118,9 +118,21 @@ struct NumericAux {
   const uint64_t *a_keys = nullptr;
   int32_t nbl = 1, lbits = 0;
   int64_t nbg = 1;
-  const uint64_t *a_masks = nullptr, *b_masks = nullptr;  // [3, n]: row masks, column masks, flags (bit 0: NaN/Inf)
+  // support masks of the operands' blocks (row masks, column masks, flags with bit 0 = NaN/Inf);
+  // the kernels read A's columns and B's rows (their rows / columns only for transposed references)
+  const uint64_t *a_rows = nullptr, *a_cols = nullptr, *a_flags = nullptr;
+  const uint64_t *b_rows = nullptr, *b_cols = nullptr, *b_flags = nullptr;
+  bool masked() const { return a_cols && a_flags && b_rows && b_flags; }
   bool transpose_bits = false;  // triple indices carry a transpose flag in bit 31 (virtual transposes)
   int64_t *panel_count = nullptr;
+  // Staged multi-GPU products (qm_numeric_pools_ex): the caller's claim order (one C block per
+  // claim, overriding QM_UNIT_ORDER); triple indices into the masks' index space when the operands
+  // come from several pools; and the halo gathered by k_halo_gather while the numeric kernel runs,
+  // whose claims >= gate_units wait for it.
+  const uint32_t *order = nullptr;
+  const uint32_t *mask_tri = nullptr;
+  const qm_halo *halo = nullptr;
+  int64_t gate_units = 0;
 };
 
 inline int make_geometry(const qm_layout *l, Geometry *g) {

@@ -497,8 +497,10 @@ extern "C" int qm_numeric_masked(const qm_layout *layout, const uint64_t *a_keys
     oi.nbl = g.nbl;
     oi.lbits = g.lbits;
     oi.nbg = g.nbg;
-    oi.a_masks = a_masks;
-    oi.b_masks = b_masks;
+    if (a_masks && b_masks) {
+      oi.a_rows = a_masks, oi.a_cols = a_masks + nA, oi.a_flags = a_masks + 2 * nA;
+      oi.b_rows = b_masks, oi.b_cols = b_masks + nB, oi.b_flags = b_masks + 2 * nB;
+    }
     oi.transpose_bits = tbits;
     oi.panel_count = panel_count;
     rc = launch_numeric_tma(g.bs, &a_blocks, &nA, 1, &b_blocks, &nB, 1, tri, c_tptr, nC, nT, oi, c_blocks,
@@ -575,4 +577,52 @@ extern "C" int qm_numeric_pools(const qm_layout *layout, const double *const *a_
   return launch_numeric_tma(g.bs, a_pools, a_counts, n_a_pools, b_pools, b_counts, n_b_pools, tri, c_tptr,
                             nC, nT, NumericAux(), c_blocks, c_sumsq, c_nonzero, zero_count, ws, ws_bytes,
                             (cudaStream_t)stream);
+}
+
+extern "C" int qm_numeric_pools_ex(const qm_layout *layout, const double *const *a_pools, const int64_t *a_counts,
+                                   int32_t n_a_pools, const double *const *b_pools, const int64_t *b_counts,
+                                   int32_t n_b_pools, const uint32_t *tri, const uint32_t *mask_tri,
+                                   const uint64_t *a_cmask, const uint64_t *a_flags, const uint64_t *b_rmask,
+                                   const uint64_t *b_flags, const uint32_t *order, const qm_halo *halo,
+                                   int64_t gate_units, const int64_t *c_tptr, int64_t nC, int64_t nT, double *c_blocks, double *c_sumsq,
+                                   uint8_t *c_nonzero, int64_t *zero_count, int64_t *panel_count, void *ws,
+                                   size_t ws_bytes, void *stream) {
+  Geometry g;
+  int rc = make_geometry(layout, &g);
+  if (rc != QM_OK) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (zero_count) QM_CUDA_TRY(cudaMemsetAsync(zero_count, 0, sizeof(int64_t), st));
+  if (panel_count) QM_CUDA_TRY(cudaMemsetAsync(panel_count, nC == 0 ? 0 : 0xff, sizeof(int64_t), st));
+  if (nC <= 0) return nC < 0 ? QM_ERR_INVALID : QM_OK;
+  if (!a_pools || !b_pools || !a_counts || !b_counts) {
+    set_error("qm_numeric_pools_ex: NULL pool arrays");
+    return QM_ERR_INVALID;
+  }
+  const bool any_mask = a_cmask || a_flags || b_rmask || b_flags;
+  if (any_mask && (!a_cmask || !a_flags || !b_rmask || !b_flags || (!mask_tri && (n_a_pools > 1 || n_b_pools > 1)))) {
+    set_error("qm_numeric_pools_ex: masks need A's column masks and flags, B's row masks and flags, and, for "
+              "several pools, mask_tri");
+    return QM_ERR_INVALID;
+  }
+  if (halo && (halo->world < 1 || halo->world > QM_MAX_RANKS || halo->count[0] < 0 || halo->count[1] < 0 ||
+               (halo->count[0] && (!halo->index[0] || !halo->pool[0])) ||
+               (halo->count[1] && (!halo->index[1] || !halo->pool[1])) || gate_units < 0)) {
+    set_error("qm_numeric_pools_ex: bad halo arguments");
+    return QM_ERR_INVALID;
+  }
+  NumericAux oi;
+  oi.nbl = g.nbl;
+  oi.lbits = g.lbits;
+  oi.nbg = g.nbg;
+  if (any_mask) {
+    oi.a_cols = a_cmask, oi.a_flags = a_flags;
+    oi.b_rows = b_rmask, oi.b_flags = b_flags;
+  }
+  oi.panel_count = panel_count;
+  oi.order = order;
+  oi.mask_tri = mask_tri;
+  oi.halo = (halo && halo->count[0] + halo->count[1] > 0) ? halo : nullptr;
+  oi.gate_units = gate_units;
+  return launch_numeric_tma(g.bs, a_pools, a_counts, n_a_pools, b_pools, b_counts, n_b_pools, tri, c_tptr, nC, nT,
+                            oi, c_blocks, c_sumsq, c_nonzero, zero_count, ws, ws_bytes, st);
 }

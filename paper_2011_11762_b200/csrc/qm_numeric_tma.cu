@@ -149,6 +149,90 @@ __device__ __forceinline__ void cur_next(Cur &c, int64_t nU, const int64_t *tptr
   }
 }
 
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Halo gather of a staged multi-GPU product: copies the halo blocks from the peer pools (read over
+// NVLink) into the local halo pools with bulk copies through shared memory -- the TMA engine moves
+// the bytes; kGatherLanes lanes per CTA each keep two chunks in flight (bulk async-groups are
+// per thread). It lets the numeric kernel launch right away (programmatic dependent launch); that
+// kernel's claims reading the halo execute griddepcontrol.wait, i.e. wait for this grid to finish.
+// min_ns (measurement only): the grid does not finish before min_ns after it started (emulates a
+// slower link on a one-GPU box).
+constexpr int kGatherChunk = 8192, kGatherLanes = 8, kGatherCtas = 32;
+constexpr int kGatherSmem = kGatherLanes * 2 * kGatherChunk;
+
+struct GatherArgs {
+  const uint32_t *index[2];
+  int64_t count[2];
+  double *pool[2];
+  uint64_t base[2][QM_MAX_RANKS];
+  int64_t off[2][QM_MAX_RANKS + 1];
+  int32_t world;
+  int64_t block_bytes, min_ns;
+};
+
+__global__ void __launch_bounds__(32) k_halo_gather(const __grid_constant__ GatherArgs ga) {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  extern __shared__ __align__(128) uint8_t gbuf[];
+  __shared__ __align__(8) uint64_t bar[kGatherLanes][2];
+  const int lane = threadIdx.x;
+  if (lane >= kGatherLanes) return;
+  const uint64_t t0 = global_ns();
+  mbar_init(&bar[lane][0], 1);
+  mbar_init(&bar[lane][1], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  const int64_t cpb = (ga.block_bytes + kGatherChunk - 1) / kGatherChunk;  // chunks per block
+  const int64_t jobs = (ga.count[0] + ga.count[1]) * cpb;
+  const int64_t first = (int64_t)blockIdx.x * kGatherLanes + lane, step = (int64_t)gridDim.x * kGatherLanes;
+  uint8_t *buf[2] = {gbuf + (lane * 2) * kGatherChunk, gbuf + (lane * 2 + 1) * kGatherChunk};
+  // chunk j: (source, destination, bytes)
+  auto where = [&](int64_t j, uint64_t *src, uint64_t *dst) -> uint32_t {
+    int64_t x = j / cpb;
+    const int64_t co = (j % cpb) * kGatherChunk;
+    const int o = x < ga.count[0] ? 0 : 1;
+    if (o) x -= ga.count[0];
+    const int64_t gi = ga.index[o][x];
+    int r = 0;
+    while (r + 1 < ga.world && gi >= ga.off[o][r + 1]) ++r;
+    *src = ga.base[o][r] + (uint64_t)(gi - ga.off[o][r]) * (uint64_t)ga.block_bytes + (uint64_t)co;
+    *dst = (uint64_t)ga.pool[o] + (uint64_t)x * (uint64_t)ga.block_bytes + (uint64_t)co;
+    const int64_t rest = ga.block_bytes - co;
+    return (uint32_t)(rest < kGatherChunk ? rest : (int64_t)kGatherChunk);
+  };
+  auto load = [&](int64_t j, int b) {
+    uint64_t src, dst;
+    const uint32_t bytes = where(j, &src, &dst);
+    mbar_expect_tx(&bar[lane][b], bytes);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(buf[b])),
+        "l"(src), "r"(bytes), "r"(smem_u32(&bar[lane][b]))
+        : "memory");
+  };
+  if (first < jobs) load(first, 0);
+  if (first + step < jobs) load(first + step, 1);
+  for (int64_t k = 0; first + k * step < jobs; ++k) {
+    const int b = (int)(k & 1);
+    mbar_wait(&bar[lane][b], (uint32_t)((k >> 1) & 1));
+    uint64_t src, dst;
+    const uint32_t bytes = where(first + k * step, &src, &dst);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(buf[b])),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    if (first + (k + 2) * step < jobs) {
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // buf b has been read out
+      load(first + (k + 2) * step, b);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  while (ga.min_ns > 0 && global_ns() - t0 < (uint64_t)ga.min_ns) __nanosleep(1000);
+}
+
 template <class Cfg, int NPOOL, bool TR>
 __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
     k_numeric_tma(const __grid_constant__ TmaMaps<NPOOL, TR> maps,
@@ -157,7 +241,7 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
                   int64_t *__restrict__ zero_count, double *__restrict__ part_sq,
                   uint8_t *__restrict__ part_nz, unsigned long long *__restrict__ counter,
                   const uint32_t *__restrict__ order, const uint8_t *__restrict__ tri_sm, uint64_t zmask,
-                  bool claim_ahead) {
+                  bool claim_ahead, int64_t gate_units) {
   constexpr int BS = Cfg::BS, MT = Cfg::MT, NT = Cfg::NT, STAGES = Cfg::STAGES;
   const int64_t nU = nC * Cfg::NQ;
   // Align to 1 KB (SWIZZLE_128B atoms) by offsetting the __shared__ array itself: the pointer keeps
@@ -195,6 +279,7 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
       int64_t next = claim_ahead && L.unit < nU ? (int64_t)gridDim.x + (int64_t)atomicAdd(counter, 1ull) : nU;
       int s = 0;
       uint32_t phase = 0;
+      bool gated = gate_units < nU;  // claims >= gate_units read the staged halo
 #if defined(QM_EXP_DEPHASE) && QM_EXP_DEPHASE > 0
       if (blockIdx.x >= gridDim.x / 2) __nanosleep(QM_EXP_DEPHASE);
 #endif
@@ -204,6 +289,13 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
           meta[s] = -1;
           mbar_arrive(&full[s]);  // tx-free completion: tells the consumers to stop
           break;
+        }
+        if (gated && L.unit >= gate_units) {
+          // the halo gather (the preceding grid, programmatic dependent launch) has completed and
+          // its bulk stores are visible; then order this generic-proxy wait before the TMA reads
+          asm volatile("griddepcontrol.wait;\n" ::: "memory");
+          asm volatile("fence.proxy.async.global;\n" ::: "memory");
+          gated = false;
         }
         const uint2 ab = tri[L.t];
         const uint32_t ao = NPOOL > 1 ? ab.x >> kOwnerShift : 0u;
@@ -432,8 +524,9 @@ __global__ void k_order_key(const uint2 *tri, const int64_t *tptr, const uint64_
 // phase) keep one panel.
 // Also counts the k rows to execute (KP per panel; warp partials, one atomic per warp).
 template <class Cfg>
-__global__ void k_triple_panels(const uint2 *tri, int64_t nT, const uint64_t *a_masks, int64_t nA,
-                                const uint64_t *b_masks, int64_t nB, uint8_t *sm, unsigned long long *panels) {
+__global__ void k_triple_panels(const uint2 *tri, int64_t nT, const uint64_t *a_rows, const uint64_t *a_cols,
+                                const uint64_t *a_flags, const uint64_t *b_rows, const uint64_t *b_cols,
+                                const uint64_t *b_flags, uint8_t *sm, unsigned long long *panels) {
   constexpr int W = 64 * Cfg::KP / (Cfg::BS > 64 ? Cfg::BS : 64);
   constexpr uint64_t kW = W >= 64 ? ~0ull : ((1ull << W) - 1ull);
   uint32_t cnt = 0;
@@ -441,8 +534,8 @@ __global__ void k_triple_panels(const uint2 *tri, int64_t nT, const uint64_t *a_
     const uint2 ab = tri[t];
     // A's columns are the stored block's rows when it is used transposed (bit 31), B's rows its columns
     const uint32_t a = ab.x & ~kTransposed, b = ab.y & ~kTransposed;
-    const uint64_t ac = (ab.x & kTransposed) ? a_masks[a] : a_masks[nA + a];
-    const uint64_t br = (ab.y & kTransposed) ? b_masks[nB + b] : b_masks[b];
+    const uint64_t ac = (ab.x & kTransposed) ? a_rows[a] : a_cols[a];
+    const uint64_t br = (ab.y & kTransposed) ? b_cols[b] : b_rows[b];
     const uint64_t ov = ac & br;
     uint32_t m = 0;
 #pragma unroll
@@ -450,7 +543,7 @@ __global__ void k_triple_panels(const uint2 *tri, int64_t nT, const uint64_t *a_
       if ((ov >> (p * W)) & kW) m |= 1u << p;
     if (!m) m = 1u;
     // a block holding NaN/Inf (flags row, bit 0): every panel runs, so 0 * Inf still yields NaN
-    if ((a_masks[2 * nA + a] | b_masks[2 * nB + b]) & 1ull) m = (1u << Cfg::NP) - 1u;
+    if ((a_flags[a] | b_flags[b]) & 1ull) m = (1u << Cfg::NP) - 1u;
     sm[t] = (uint8_t)m;
     cnt += __popc(m) * Cfg::KP;  // k rows executed
   }
@@ -591,29 +684,76 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
   const int64_t nU = nC * Cfg::NQ;
   int64_t grid = (int64_t)sm_count_tma() * per_sm;
   if (grid > nU) grid = nU;
-  uint32_t *order = nullptr;
+  const uint32_t *order = oi.order;  // the caller's claim order (staged multi-GPU products)
   // (not with transposed references: their triple indices name stored blocks, not view entries)
-  if (oi.a_keys && na == 1 && nb == 1 && !TR) {
+  if (!order && oi.a_keys && na == 1 && nb == 1 && !TR) {
     const int kind = claim_order();
     if (kind != kOrderKey) {
-      rc = make_order<Cfg>(kind, tri, tptr, oi.a_keys, oi.nbl, oi.lbits, oi.nbg, nC, ws, &order, st);
+      uint32_t *o = nullptr;
+      rc = make_order<Cfg>(kind, tri, tptr, oi.a_keys, oi.nbl, oi.lbits, oi.nbg, nC, ws, &o, st);
       if (rc != QM_OK) return rc;
+      order = o;
     }
   }
   uint8_t *tri_sm = nullptr;
   int64_t panel_fill = (int64_t)Cfg::BS * nT;  // every k row of every triple
-  if (oi.a_masks && oi.b_masks && na == 1 && nb == 1 && Cfg::NP > 1 && nT > 0) {
+  // panel masks: single pools index the masks with the triples themselves; several pools need the
+  // triples' indices in the masks' index space (mask_tri, e.g. global block indices)
+  const bool one_pool = na == 1 && nb == 1;
+  if (oi.masked() && (one_pool || oi.mask_tri) && Cfg::NP > 1 && nT > 0) {
     tri_sm = (uint8_t *)ws + tma_ws_panels_offset<Cfg>(nC);
     if (oi.panel_count) QM_CUDA_TRY(cudaMemsetAsync(oi.panel_count, 0, sizeof(int64_t), st));
     const int g = (int)std::min<int64_t>((nT + 255) / 256, (int64_t)sm_count_tma() * 16);
-    k_triple_panels<Cfg><<<g, 256, 0, st>>>(tri, nT, oi.a_masks, nA[0], oi.b_masks, nB[0], tri_sm,
-                                            (unsigned long long *)oi.panel_count);
+    const uint2 *mt = oi.mask_tri ? (const uint2 *)oi.mask_tri : tri;
+    k_triple_panels<Cfg><<<g, 256, 0, st>>>(mt, nT, oi.a_rows, oi.a_cols, oi.a_flags, oi.b_rows, oi.b_cols,
+                                            oi.b_flags, tri_sm, (unsigned long long *)oi.panel_count);
     QM_LAUNCHED("k_triple_panels");
     panel_fill = -1;  // counted by k_triple_panels
   }
-  k_numeric_tma<Cfg, NPOOL, TR><<<(int)grid, Cfg::NTHR, Cfg::SMEM, st>>>(
-      maps, tri, tptr, nC, C, csq, cnz, zc, part_sq, part_nz, counter, order, tri_sm, /*zmask=*/0ull,
-      claim_ahead(nC, nT));
+  if (oi.halo) {
+    // staged halo: the gather runs on a few SMs' TMA engines while this kernel computes the
+    // local-only C blocks; its claims >= gate_units wait for the gather grid (griddepcontrol.wait)
+    GatherArgs ga;
+    memset(&ga, 0, sizeof(ga));
+    for (int o = 0; o < 2; ++o) {
+      ga.index[o] = oi.halo->index[o];
+      ga.count[o] = oi.halo->count[o];
+      ga.pool[o] = oi.halo->pool[o];
+      for (int r = 0; r < QM_MAX_RANKS; ++r) ga.base[o][r] = oi.halo->peer_base[o][r];
+      for (int r = 0; r <= QM_MAX_RANKS; ++r) ga.off[o][r] = oi.halo->offset[o][r];
+    }
+    ga.world = oi.halo->world;
+    ga.block_bytes = (int64_t)Cfg::BS * Cfg::BS * (int64_t)sizeof(double);
+    ga.min_ns = oi.halo->min_ns;
+    const int64_t jobs = (ga.count[0] + ga.count[1]) * ((ga.block_bytes + kGatherChunk - 1) / kGatherChunk);
+    const int gg = (int)std::max<int64_t>(1, std::min<int64_t>((jobs + kGatherLanes - 1) / kGatherLanes, kGatherCtas));
+    static PerDeviceOnce gonce;
+    rc = gonce.run([]() -> int {
+      QM_CUDA_TRY(cudaFuncSetAttribute(k_halo_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, kGatherSmem));
+      return (int)QM_OK;
+    });
+    if (rc != QM_OK) return rc;
+    k_halo_gather<<<gg, 32, kGatherSmem, st>>>(ga);
+    QM_LAUNCHED("k_halo_gather");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(Cfg::NTHR);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const int64_t gate_units = std::max<int64_t>(0, std::min<int64_t>(oi.gate_units, nU));
+    QM_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_numeric_tma<Cfg, NPOOL, TR>, maps, tri, tptr, nC, C, csq, cnz, zc,
+                                   part_sq, part_nz, counter, order, (const uint8_t *)tri_sm, (uint64_t)0ull,
+                                   claim_ahead(nC, nT), gate_units));
+  } else {
+    k_numeric_tma<Cfg, NPOOL, TR><<<(int)grid, Cfg::NTHR, Cfg::SMEM, st>>>(
+        maps, tri, tptr, nC, C, csq, cnz, zc, part_sq, part_nz, counter, order, tri_sm, /*zmask=*/0ull,
+        claim_ahead(nC, nT), nU);
+  }
   QM_LAUNCHED("k_numeric_tma");
   {
     int64_t g = std::min<int64_t>((nC + 255) / 256, (int64_t)sm_count_tma() * 8);
@@ -673,7 +813,7 @@ using Tma64k16 = TmaCfg<64, 64, 2, 2, 16, 4, 3>;
 using Tma32k16 = TmaCfg<32, 32, 2, 2, 16, 4, 6>;  // same for bs 32: 4 stages of 8 KB, 6 CTAs/SM
 bool use_k16(const NumericAux &oi) {
   const char *e = getenv("QM_PANEL16");
-  return oi.a_masks && oi.b_masks && !(e && strcmp(e, "0") == 0);
+  return oi.masked() && !(e && strcmp(e, "0") == 0);
 }
 
 using Tma128 = TmaCfg<128, 64, 2, 2, 32, 3, 2>;

@@ -509,25 +509,40 @@ __global__ void k_inv_counts(const uint32_t *perm, const uint32_t *rm_cnt, int64
 }
 
 // ---- multi-GPU partition of the symbolic phase ------------------------------------------------
-// Structural triples per C tile (aligned square of 2^shift leaves per side, Morton tile code): for
-// every A entry (i, k), B row k's columns are split at the tile-column boundaries by binary search,
-// so the pass costs O(nA x tiles a B row spans) -- not O(triples). Masks are ignored (this only
-// balances the ranks; every rank still filters its own pairs exactly).
-__global__ void k_tile_work(const uint32_t *srow, const uint32_t *scol, int64_t nA, const uint32_t *b_rp, int nbl,
-                            int shift, uint64_t *tiles) {
+// Work per C tile (aligned square of 2^shift leaves per side, Morton tile code). One warp per A
+// entry (i, k): the lanes read B row k's entries 32 at a time (coalesced), and since the row's
+// columns ascend, the lanes of one tile column form a contiguous run -- one match + reduce per run
+// and one atomic per (entry, tile). Weight of a pair: 1 (structural triple) without support masks;
+// with masks, the number of 16-row k panels where A(i,k)'s columns and B(k,j)'s rows meet (0: the
+// pair is skipped as exactly zero), i.e. the k depth the numeric kernel executes -- so ranks are
+// balanced on executed work, not on structural triples. (Balance only: every rank still filters
+// its own pairs exactly.) Host twin: distributed.tile_partition.
+__device__ __forceinline__ uint32_t panel_groups(uint64_t m) {
+  return (uint32_t)((m & 0xffffull) != 0) + (uint32_t)(((m >> 16) & 0xffffull) != 0) +
+         (uint32_t)(((m >> 32) & 0xffffull) != 0) + (uint32_t)((m >> 48) != 0);
+}
+
+__global__ void k_tile_work(const uint32_t *srow, const uint32_t *scol, const uint64_t *smask,
+                            const int *masked_flag, int64_t nA, const uint32_t *b_rp, int nbl, int shift,
+                            uint64_t *tiles) {
   const uint32_t tw = (uint32_t)nbl << shift;  // tile width in blocks
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nA; x += (int64_t)gridDim.x * blockDim.x) {
+  const bool masked = (*masked_flag & kFlagMasked) != 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t x = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); x < nA; x += nwarps) {
     const uint32_t i = srow[x], k = scol[x];
     const uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
-    if (b0 == b1) continue;
-    const uint32_t I = (i / (uint32_t)nbl) >> shift;
-    const uint32_t J0 = scol[b0] / tw, J1 = scol[b1 - 1] / tw;
-    uint32_t lo = b0;
-    for (uint32_t J = J0; J <= J1; ++J) {
-      const uint32_t hi = J == J1 ? b1 : lower_bound_col(scol, lo, b1, (J + 1) * tw);
-      if (hi > lo) atomicAdd((unsigned long long *)&tiles[(spread_bits(I) << 1) | spread_bits(J)],
-                             (unsigned long long)(hi - lo));
-      lo = hi;
+    const uint64_t am = masked ? smask[x] : ~0ull;
+    const uint64_t I = spread_bits((i / (uint32_t)nbl) >> shift) << 1;
+    for (uint32_t base = b0; base < b1; base += 32) {
+      const uint32_t y = base + lane;
+      const bool valid = y < b1;
+      const uint32_t J = valid ? scol[y] / tw : 0xffffffffu;
+      const uint32_t w = !valid ? 0u : masked ? panel_groups(am & smask[y]) : 1u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, J);
+      const uint32_t sum = __reduce_add_sync(peers, w);
+      if (valid && sum && lane == __ffs(peers) - 1)
+        atomicAdd((unsigned long long *)&tiles[I | spread_bits(J)], (unsigned long long)sum);
     }
   }
 }
@@ -755,7 +770,8 @@ int count_impl(const qm_layout *layout, const uint64_t *a_keys, const uint64_t *
     const int64_t ntiles = (int64_t)1 << (2 * tl);
     QM_CUDA_TRY(cudaMemsetAsync(w.tiles, 0, (size_t)(ntiles + 1) * sizeof(uint64_t), st));
     if (nA > 0) {
-      k_tile_work<<<grid_for(nA), 256, 0, st>>>(w.srow, w.scol, nA, b_rp, g.nbl, g.depth - tl, w.tiles);
+      k_tile_work<<<grid_for(nA * 32), 256, 0, st>>>(w.srow, w.scol, w.smask, w.masked, nA, b_rp, g.nbl,
+                                                      g.depth - tl, w.tiles);
       QM_LAUNCHED("k_tile_work");
     }
     uint64_t *prefix = w.tiles + ntiles + 1;

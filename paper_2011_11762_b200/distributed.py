@@ -25,6 +25,7 @@ with a test backend); ``LocalComm`` is the single-rank case.
 from __future__ import annotations
 
 import atexit
+import ctypes
 import os
 import time
 import warnings
@@ -173,35 +174,17 @@ class LocalComm:
 class CudaBackend:
     """The product backend: libqmb200 kernels on the rank's GPU."""
 
-    def numeric_pools(self, layout, pa: list, na: list, pb: list, nb: list, tri: torch.Tensor,
-                      c_tptr: torch.Tensor, c_keys: torch.Tensor) -> BlockSet:
-        import ctypes
-
-        from . import _ffi
-
-        lib = _ffi.load()
-        bs = layout.block_size
-        dev = c_keys.device
-        nc = int(c_keys.shape[0])
-        arr_p = lambda v: (ctypes.c_void_p * len(v))(*v)  # noqa: E731
-        arr_n = lambda v: (ctypes.c_int64 * len(v))(*v)  # noqa: E731
-        out = BlockSet(c_keys, torch.empty((nc, bs, bs), dtype=torch.float64, device=dev),
-                       torch.empty(nc, dtype=torch.float64, device=dev))
-        nz = torch.empty(nc, dtype=torch.uint8, device=dev)
-        zc = torch.zeros(1, dtype=torch.int64, device=dev)
-        wb = lib.qm_numeric_workspace_bytes(bs, nc, int(tri.numel()) // 2)
-        ws = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
-        stream = self.stream if self.stream is not None else torch.cuda.current_stream(dev)
-        _ffi.check(lib.qm_numeric_pools(ctypes.byref(layout), arr_p(pa), arr_n(na), len(pa), arr_p(pb),
-                                        arr_n(nb), len(pb), _ffi.ptr(tri), _ffi.ptr(c_tptr), nc,
-                                        int(tri.numel()) // 2,
-                                        _ffi.ptr(out.blocks), _ffi.ptr(out.sumsq), _ffi.ptr(nz), _ffi.ptr(zc),
-                                        _ffi.ptr(ws), wb, _ffi.stream_handle(stream)), "qm_numeric_pools")
-        n_zero = spgemm._sync_item(zc, stream)
-        return spgemm.compact(bs, out, nz, n_zero, self.stream)
-
     def __init__(self, stream=None):
         self.stream = stream
+
+    def numeric_peer(self, layout, tri, c_tptr, c_keys, rank, a_off, b_off, a_bases, b_bases, a_local,
+                     b_local, b_is_a, masks, staged=True, info=None):
+        """staged_numeric on this rank's GPU, then the exact-zero drop."""
+        stream = self.stream if self.stream is not None else torch.cuda.current_stream(c_keys.device)
+        c, nz, zc = staged_numeric(layout, tri, c_tptr, c_keys, rank, a_off, b_off, a_bases, b_bases,
+                                   a_local, b_local, b_is_a, masks, stream, staged=staged, info=info)
+        n_zero = spgemm._sync_item(zc, stream)
+        return spgemm.compact(layout.block_size, c, nz, n_zero, self.stream)
 
     def symbolic_state(self, layout, a_keys: torch.Tensor, b_keys: torch.Tensor, a_cmask=None, b_rmask=None,
                        part=None):
@@ -246,16 +229,29 @@ class DistStats:
     blocks_received: int = 0
     mode: str = "exchange"
     phase_s: dict = field(default_factory=dict)
+    extra: dict = field(default_factory=dict)
 
 
 MAX_TILE_LEVELS = 8  # csrc/qm_symbolic.cu kMaxTileLevels
 
 
-def tile_partition(geom, ka: np.ndarray, kb: np.ndarray, world: int) -> list[int]:
+def _panel_groups(m: np.ndarray) -> np.ndarray:
+    """Nonzero 16-bit groups of each mask (csrc k_tile_work's panel_groups)."""
+    m = m.astype(np.uint64)
+    g = np.zeros(m.shape, dtype=np.int64)
+    for s in (0, 16, 32, 48):
+        g += ((m >> np.uint64(s)) & np.uint64(0xFFFF)) != 0
+    return g
+
+
+def tile_partition(geom, ka: np.ndarray, kb: np.ndarray, world: int, a_cmask=None, b_rmask=None) -> list[int]:
     """Host statement of qm_spgemm_count_part's partition (its CPU twin and test oracle): C tiles =
     aligned quadtree subtrees at level min(depth, 8) (tile code = C key >> kshift), weighed by their
-    structural triples; tiles are cut in Morton order where the exclusive work prefix first reaches
-    r*W // world. Returns the world+1 key bounds; rank r owns C keys [bounds[r], bounds[r+1])."""
+    work; tiles are cut in Morton order where the exclusive work prefix first reaches r*W // world.
+    Work of a block pair A(i,k)*B(k,j): 1 without support masks (structural triples); with masks
+    (A's column masks, B's row masks) the number of 16-row k panels where they meet, the depth the
+    numeric kernel executes (0 for disjoint supports). Returns the world+1 key bounds; rank r owns
+    C keys [bounds[r], bounds[r+1])."""
     import scipy.sparse as sp  # noqa: PLC0415
 
     depth = geom.params.depth
@@ -265,11 +261,26 @@ def tile_partition(geom, ka: np.ndarray, kb: np.ndarray, world: int) -> list[int
     nb = geom.nbg
     ai, ak = geom.decode(np.asarray(ka, dtype=np.int64))
     bk, bj = geom.decode(np.asarray(kb, dtype=np.int64))
-    pa = sp.csr_matrix((np.ones(ai.size, dtype=np.int64), (ai, ak)), shape=(nb, nb))
-    pb = sp.csr_matrix((np.ones(bk.size, dtype=np.int64), (bk, bj)), shape=(nb, nb))
-    c = (pa @ pb).tocoo()
-    tiles = geom.qkey(c.row.astype(np.int64), c.col.astype(np.int64)) >> kshift
-    work = np.bincount(tiles, weights=c.data, minlength=ntiles).astype(np.int64)
+    if a_cmask is None and b_rmask is None:
+        pa = sp.csr_matrix((np.ones(ai.size, dtype=np.int64), (ai, ak)), shape=(nb, nb))
+        pb = sp.csr_matrix((np.ones(bk.size, dtype=np.int64), (bk, bj)), shape=(nb, nb))
+        c = (pa @ pb).tocoo()
+        tiles = geom.qkey(c.row.astype(np.int64), c.col.astype(np.int64)) >> kshift
+        work = np.bincount(tiles, weights=c.data, minlength=ntiles).astype(np.int64)
+    else:  # every pair, weighed by its executed k panels
+        full = np.full(1, np.iinfo(np.uint64).max, dtype=np.uint64)
+        am = np.asarray(a_cmask).view(np.uint64) if a_cmask is not None else np.broadcast_to(full, ai.shape)
+        bm = np.asarray(b_rmask).view(np.uint64) if b_rmask is not None else np.broadcast_to(full, bk.shape)
+        order = np.argsort(bk, kind="stable")
+        bptr = np.searchsorted(bk[order], np.arange(nb + 1))
+        cnt = bptr[ak + 1] - bptr[ak]
+        a_idx = np.repeat(np.arange(ai.size), cnt)
+        start = np.repeat(bptr[ak], cnt)
+        within = np.arange(a_idx.size) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+        b_idx = order[start + within]
+        w = _panel_groups(am[a_idx] & bm[b_idx])
+        tiles = geom.qkey(ai[a_idx].astype(np.int64), bj[b_idx].astype(np.int64)) >> kshift
+        work = np.bincount(tiles, weights=w, minlength=ntiles).astype(np.int64)
     prefix = np.concatenate([[0], np.cumsum(work)])
     W = int(prefix[-1])
     cuts = [0] + [int(np.searchsorted(prefix[:ntiles], (W * r) // world, side="left")) for r in range(1, world)]
@@ -391,11 +402,118 @@ class PeerPools:
         """Mappings stay cached for the next product (release_peer_mappings closes them)."""
 
 
-def _pack_owner(idx: torch.Tensor, offsets: torch.Tensor):
-    """Global block index -> (owner << 28) | local index, and the owner."""
-    owner = torch.searchsorted(offsets[1:], idx, right=True)
-    local = idx - offsets[owner]
-    return (owner << 28) | local, owner
+def staged_numeric(layout, tri: torch.Tensor, c_tptr: torch.Tensor, c_keys: torch.Tensor, rank: int,
+                   a_off: list, b_off: list, a_bases: list, b_bases: list, a_local: torch.Tensor,
+                   b_local: torch.Tensor, b_is_a: bool, masks=None, stream=None, staged: bool = True,
+                   info: dict | None = None, emulate_link_gbs: float | None = None):
+    """Numeric phase of one rank over the operands of every rank (SURVEY 8(e) "needed A/B subtrees
+    fetched over NVLink"), C blocks needing no remote block first.
+
+    tri: int32 [2T] triples (a, b) in global block indices (rank r owns A indices [a_off[r],
+    a_off[r+1]), likewise B); a_bases[r] / b_bases[r]: device address of rank r's pool (mapped peer
+    memory; ignored for `rank`). staged=True: qm_stage_plan (device) finds the peer-owned blocks,
+    re-indexes the triples into [local pool | halo pool] and orders the C blocks needing no halo
+    first; k_halo_gather copies each halo block once (bulk copies on a few SMs, reading the peer
+    pools over NVLink) while the numeric kernel, launched as its programmatic dependent, computes
+    the local-only C blocks; its claims of the other C blocks wait for the gather grid
+    (qm_numeric_pools_ex). staged=False ("fused"): the kernel's TMA reads remote blocks from the peer
+    pools directly, every reference over NVLink. Per-C-block summation order is the triples' order
+    either way: bitwise the single-GPU product.
+    masks = (a column masks, b row masks, a flags, b flags) in global indices, or None.
+    emulate_link_gbs (measurement only): the gather lasts at least halo bytes / this bandwidth,
+    emulating NVLink when the "peers" are slices of pools on this GPU (scaling projection).
+    Returns (C BlockSet before compaction, nonzero flags, [zero blocks, k rows] device counters)."""
+    from . import _ffi
+
+    lib = _ffi.load()
+    bs = layout.block_size
+    dev = c_keys.device
+    nc, nt = int(c_keys.shape[0]), int(tri.numel()) // 2
+    stream = stream if stream is not None else torch.cuda.current_stream(dev)
+    sh = _ffi.stream_handle(stream)
+    blk = bs * bs * 8
+    info = info if info is not None else {}
+    world = len(a_off) - 1
+    if a_local.shape[0] == 0 or b_local.shape[0] == 0:  # (an empty pool still needs a valid address)
+        dummy = torch.zeros((1, bs, bs), dtype=torch.float64, device=dev)
+    la = a_local if a_local.shape[0] else dummy
+    lb = b_local if b_local.shape[0] else dummy
+    na_g, nb_g = a_off[-1], b_off[-1]
+    order = halo = None
+    gate_units = 0
+    keep = []
+    # outputs and workspace first: they do not depend on the plan's counts
+    out = BlockSet(c_keys, torch.empty((nc, bs, bs), dtype=torch.float64, device=dev),
+                   torch.empty(nc, dtype=torch.float64, device=dev))
+    nz = torch.empty(nc, dtype=torch.uint8, device=dev)
+    zc = torch.empty(2, dtype=torch.int64, device=dev)  # (zeroed by the library)
+    wb = lib.qm_numeric_workspace_bytes(bs, nc, nt)
+    ws = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
+    if staged:
+        tri_packed = torch.empty(2 * nt, dtype=torch.int32, device=dev)
+        order = torch.empty(max(nc, 1), dtype=torch.int32, device=dev)
+        cap_a = max(na_g - (a_off[rank + 1] - a_off[rank]), 1)
+        cap_b = max(nb_g - (b_off[rank + 1] - b_off[rank]), 1)
+        ha = torch.empty(cap_a, dtype=torch.int32, device=dev)
+        hb = ha if b_is_a else torch.empty(cap_b, dtype=torch.int32, device=dev)
+        swb = lib.qm_stage_plan_workspace_bytes(na_g, nb_g, nc, 1 if b_is_a else 0)
+        sws = torch.empty(max(swb, 1), dtype=torch.uint8, device=dev)
+        counts = (ctypes.c_int64 * 3)()
+        _ffi.check(lib.qm_stage_plan(_ffi.ptr(tri), nt, _ffi.ptr(c_tptr), nc, a_off[rank], a_off[rank + 1], na_g,
+                                     b_off[rank], b_off[rank + 1], nb_g, 1 if b_is_a else 0, _ffi.ptr(sws), swb,
+                                     _ffi.ptr(tri_packed), _ffi.ptr(order), _ffi.ptr(ha),
+                                     None if b_is_a else _ffi.ptr(hb), counts, sh), "qm_stage_plan")
+        n_local, n_ha, n_hb = int(counts[0]), int(counts[1]), int(counts[2])
+        pool_a = torch.empty((max(n_ha, 1), bs, bs), dtype=torch.float64, device=dev)
+        pool_b = pool_a if b_is_a else torch.empty((max(n_hb, 1), bs, bs), dtype=torch.float64, device=dev)
+        halo = _ffi.QmHalo()
+        halo.world = world
+        halo.index[0], halo.count[0], halo.pool[0] = _ffi.ptr(ha), n_ha, _ffi.ptr(pool_a)
+        if not b_is_a:
+            halo.index[1], halo.count[1], halo.pool[1] = _ffi.ptr(hb), n_hb, _ffi.ptr(pool_b)
+        for o, (bases, off) in enumerate(((a_bases, a_off), (b_bases, b_off))):
+            for r in range(world):
+                halo.peer_base[o][r] = int(bases[r]) if r != rank else 0
+            for r in range(world + 1):
+                halo.offset[o][r] = int(off[r])
+        n_halo = n_ha + (0 if b_is_a else n_hb)
+        if emulate_link_gbs:
+            halo.min_ns = int(n_halo * blk / (emulate_link_gbs * 1e9) * 1e9)
+        gate_units = n_local * (1 if bs <= 64 else (bs // 64) ** 2)
+        info["halo_bytes"] = n_halo * blk
+        info["local_c_blocks"], info["c_blocks"] = n_local, nc
+        counts_a, counts_b = [int(la.shape[0]), max(n_ha, 1)], [int(lb.shape[0]), max(pool_b.shape[0], 1)]
+        ptrs_a, ptrs_b = [_ffi.ptr(la), _ffi.ptr(pool_a)], [_ffi.ptr(lb), _ffi.ptr(pool_b)]
+        keep += [pool_a, pool_b, ha, hb, sws, order]
+    else:  # fused: every pool is a (mapped) rank pool; index = owner << 28 | local
+        offa = torch.tensor(a_off, dtype=torch.int64, device=dev)
+        offb = offa if b_is_a else torch.tensor(b_off, dtype=torch.int64, device=dev)
+        t2 = tri.view(-1, 2).to(torch.int64)
+        ga, gb = t2[:, 0].contiguous(), t2[:, 1].contiguous()
+        own_a = torch.searchsorted(offa[1:], ga, right=True)
+        own_b = torch.searchsorted(offb[1:], gb, right=True)
+        tri_packed = torch.stack([(own_a << 28) | (ga - offa[own_a]), (own_b << 28) | (gb - offb[own_b])],
+                                 dim=1).to(torch.int32).reshape(-1).contiguous()
+        ptrs_a = [int(a_bases[r]) if r != rank else _ffi.ptr(la) for r in range(world)]
+        ptrs_b = [int(b_bases[r]) if r != rank else _ffi.ptr(lb) for r in range(world)]
+        counts_a = [max(a_off[r + 1] - a_off[r], 1) for r in range(world)]
+        counts_b = [max(b_off[r + 1] - b_off[r], 1) for r in range(world)]
+    ma = mb = fa = fb = mask_tri = None
+    if masks is not None:  # the kernel reads A's column masks and B's row masks (+ NaN/Inf flags)
+        ma, mb, fa, fb = masks
+        mask_tri = tri
+    arr_p = lambda v: (ctypes.c_void_p * len(v))(*v)  # noqa: E731
+    arr_n = lambda v: (ctypes.c_int64 * len(v))(*v)  # noqa: E731
+    _ffi.check(lib.qm_numeric_pools_ex(ctypes.byref(layout), arr_p(ptrs_a), arr_n(counts_a), len(ptrs_a),
+                                       arr_p(ptrs_b), arr_n(counts_b), len(ptrs_b), _ffi.ptr(tri_packed),
+                                       _ffi.ptr(mask_tri), _ffi.ptr(ma), _ffi.ptr(fa), _ffi.ptr(mb), _ffi.ptr(fb),
+                                       _ffi.ptr(order),
+                                       ctypes.byref(halo) if halo is not None else None, gate_units,
+                                       _ffi.ptr(c_tptr), nc, nt, _ffi.ptr(out.blocks), _ffi.ptr(out.sumsq),
+                                       _ffi.ptr(nz), _ffi.ptr(zc), _ffi.ptr(zc[1:]), _ffi.ptr(ws), wb, sh),
+               "qm_numeric_pools_ex")
+    info["_keep"] = keep + [ws, tri_packed]  # alive until the caller synchronises
+    return out, nz, zc
 
 
 def _fetch(comm, backend, local_blocks: torch.Tensor, offsets: list[int], need: torch.Tensor):
@@ -428,16 +546,20 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     mode "exchange": request/serve halo exchange, then the local numeric kernel.
     mode "fused":    no exchange; the numeric kernel's TMA producer reads remote blocks directly
                      from their owners' pools (PeerPools, CUDA IPC over NVLink), overlapped with
-                     the math (qm_numeric_pools).
+                     the math (qm_numeric_pools_ex).
+    mode "staged":   each remote block is gathered once from the peer pools into a local halo
+                     pool (bulk copies on a few SMs) while the numeric kernel runs the C blocks
+                     whose triples are all local; claims of the others wait for the gather
+                     (staged_numeric). No collective for the halo.
     mode None:       $QM_DIST_MODE, default "auto".
     mode "auto":     fused when its estimated NVLink time (every remote block reference is a
                      remote read: peer loads bypass the local L2) stays under a quarter of the
-                     estimated compute time, else exchange (heavy reuse of remote blocks, e.g.
-                     random patterns)."""
+                     estimated compute time, else staged (heavy reuse of remote blocks: decay,
+                     random patterns); the exchange when some rank cannot map its peers."""
     backend = backend or CudaBackend()
     mode = mode or os.environ.get("QM_DIST_MODE", "auto")
-    if mode not in ("auto", "exchange", "fused"):
-        raise ConfigurationError(f"unknown distributed mode {mode!r} (auto, exchange, fused)")
+    if mode not in ("auto", "exchange", "fused", "staged"):
+        raise ConfigurationError(f"unknown distributed mode {mode!r} (auto, exchange, fused, staged)")
     stats = DistStats(rank=comm.rank, world=comm.world)
     clock = timer or (lambda: time.perf_counter())
     t0 = clock()
@@ -502,48 +624,55 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
         c_tptr = torch.zeros(1, dtype=torch.int64, device=dev)
         tri = torch.zeros((0, 2), dtype=torch.int64, device=dev)
     t2 = clock()
-    fused_ok = (comm.world > 1 and mode != "exchange" and hasattr(backend, "numeric_pools")
-                and layout.block_size in (32, 64, 128) and comm.world <= 8)
-    if fused_ok:
+    peer_ok = (comm.world > 1 and mode != "exchange" and hasattr(backend, "numeric_peer")
+               and layout.block_size in (32, 64, 128) and comm.world <= 8)
+    if peer_ok:
         offa = torch.tensor(a_off, dtype=torch.int64, device=dev)
         offb = offa if b_is_a else torch.tensor(b_off, dtype=torch.int64, device=dev)
-        pa_idx, own_a = _pack_owner(tri[:, 0].contiguous(), offa)
-        pb_idx, own_b = _pack_owner(tri[:, 1].contiguous(), offb)
+        own_a = torch.searchsorted(offa[1:], tri[:, 0].contiguous(), right=True)
+        own_b = torch.searchsorted(offb[1:], tri[:, 1].contiguous(), right=True)
         blk_bytes = bs * bs * 8
         remote_refs = int(((own_a != comm.rank).sum() + (own_b != comm.rank).sum()).item()) if hi > lo else 0
         fused_s = remote_refs * blk_bytes / (NVLINK_GBS * 1e9)
         compute_s = 2.0 * bs ** 3 * (hi - lo) / (FP64_TFLOPS * 1e12)
-        # every rank must take the same path (the fused mode's mappings are collective)
-        prefer_exchange = 0.0 if (mode == "fused" or fused_s <= 0.25 * compute_s) else 1.0
-        pools = None
-        if comm.allreduce_max_vec([prefer_exchange], dev)[0] == 0.0:
-            if dev.type == "cuda":
-                torch.cuda.synchronize(dev)  # this rank's pools are written (any stream) ...
-            comm.barrier()  # ... on every rank, before anyone reads them
-            pools = PeerPools(comm, [a_local.blocks] if b_is_a else [a_local.blocks, b_local.blocks])
-            if comm.allreduce_max(0.0 if pools.ok else 1.0, dev) > 0.0:
-                # some rank cannot map its peers' pools: every rank takes the exchange path
-                if not pools.ok:
-                    warnings.warn(f"rank {comm.rank}: fused mode unavailable ({pools.error}); "
-                                  "using the halo exchange", RuntimeWarning, stacklevel=2)
-                pools.close()
-                comm.barrier()
-                pools = None
+        # 0 = fused (the kernel's TMA reads remote blocks in place: few remote references),
+        # 1 = staged (copy engines pull the halo once while local-only C blocks compute);
+        # every rank must take the same path (the peer mappings are collective)
+        want = 0.0 if mode == "fused" else 1.0 if mode == "staged" else (0.0 if fused_s <= 0.25 * compute_s else 1.0)
+        want = comm.allreduce_max_vec([want], dev)[0]
+        if dev.type == "cuda":
+            torch.cuda.synchronize(dev)  # this rank's pools are written (any stream) ...
+        comm.barrier()  # ... on every rank, before anyone reads them
+        pools = PeerPools(comm, [a_local.blocks] if b_is_a else [a_local.blocks, b_local.blocks])
+        if comm.allreduce_max(0.0 if pools.ok else 1.0, dev) > 0.0:
+            # some rank cannot map its peers' pools: every rank takes the exchange path
+            if not pools.ok:
+                warnings.warn(f"rank {comm.rank}: peer pools unavailable ({pools.error}); "
+                              "using the halo exchange", RuntimeWarning, stacklevel=2)
+            pools.close()
+            comm.barrier()
+            pools = None
         if pools is not None:
-            tri_packed = torch.stack([pa_idx, pb_idx], dim=1).to(torch.int32).reshape(-1).contiguous()
+            info = {}
+            masks = (ma, mb, fa, fb) if ma is not None else None
             try:
-                c = (backend.numeric_pools(layout, pools.ptrs[0], pools.counts[0], pools.ptrs[-1],
-                                           pools.counts[-1], tri_packed, c_tptr, c_keys) if hi > lo else empty)
+                tri32 = tri.to(torch.int32).reshape(-1).contiguous()
+                c = (backend.numeric_peer(layout, tri32, c_tptr, c_keys, comm.rank, a_off, b_off, pools.ptrs[0],
+                                          pools.ptrs[-1], a_local.blocks, bl.blocks, b_is_a, masks,
+                                          staged=want > 0.0, info=info) if hi > lo else empty)
                 torch.cuda.synchronize(dev)
             finally:
                 pools.close()
             comm.barrier()  # every rank has finished reading the others' pools
             t4 = clock()
             stats.n_c_local = c.n
-            stats.mode = "fused"
-            stats.bytes_received = remote_refs * blk_bytes  # NVLink reads of the fused kernel
+            stats.mode = "staged" if want > 0.0 else "fused"
+            # NVLink bytes: the staged halo (each remote block once), or every remote reference (fused)
+            stats.bytes_received = info.get("halo_bytes", remote_refs * blk_bytes)
+            stats.blocks_received = stats.bytes_received // blk_bytes
             stats.phase_s = {"structure": t1 - t0, "symbolic": t2 - t1, "exchange": 0.0,
                              "numeric": t4 - t2}
+            stats.extra = {k: v for k, v in info.items() if not k.startswith("_")}
             return c, stats
     need_a = torch.unique(tri[:, 0]) if hi > lo else tri.new_zeros(0)
     need_b = torch.unique(tri[:, 1]) if hi > lo else tri.new_zeros(0)

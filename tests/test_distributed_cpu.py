@@ -82,11 +82,11 @@ CASES = {
 
 
 class NoPoolsBackend(OracleBackend):
-    """Offers the fused path, which must not run: on a host without peer-mappable device memory
-    PeerPools cannot export, and every rank has to agree on the exchange instead."""
+    """Offers the peer paths (fused / staged), which must not run: on a host without peer-mappable
+    device memory PeerPools cannot export, and every rank has to agree on the exchange instead."""
 
-    def numeric_pools(self, *args, **kwargs):
-        raise AssertionError("fused kernel launched although a rank could not map its peers")
+    def numeric_peer(self, *args, **kwargs):
+        raise AssertionError("peer-pool kernel launched although a rank could not map its peers")
 
 
 def _worker(rank, world, port, case, outdir, mode="auto"):
@@ -103,15 +103,15 @@ def _worker(rank, world, port, case, outdir, mode="auto"):
     lb = BlockSet(torch.from_numpy(kb[qb[rank]:qb[rank + 1]]), torch.from_numpy(bb[qb[rank]:qb[rank + 1]]),
                   torch.zeros(0))
     comm = D.Comm()
-    backend = NoPoolsBackend(geom) if mode == "fused" else OracleBackend(geom)
-    if mode == "fused":
+    backend = NoPoolsBackend(geom) if mode in ("fused", "staged") else OracleBackend(geom)
+    if mode in ("fused", "staged"):
         import warnings
 
         with warnings.catch_warnings(record=True) as w:
             warnings.simplefilter("always")
             c, st = D.multiply(comm, make_layout(geom.params, geom.bs), la, lb, backend=backend, mode=mode)
         assert st.mode == "exchange"
-        assert any("fused mode unavailable" in str(x.message) for x in w)
+        assert any("peer pools unavailable" in str(x.message) for x in w)
     else:
         c, st = D.multiply(comm, make_layout(geom.params, geom.bs), la, lb, backend=backend)
     keys, _ = comm.allgather_varlen(c.keys)
@@ -142,8 +142,9 @@ def test_distributed_product_equals_single_process(tmp_path, world, case):
     assert out["recv"][:, 0].sum() > 0  # halo blocks crossed ranks
 
 
-def test_fused_mode_falls_back_on_every_rank_when_pools_cannot_be_mapped(tmp_path):
-    mp.spawn(_worker, args=(2, _free_port(), "banded", str(tmp_path), "fused"), nprocs=2, join=True)
+@pytest.mark.parametrize("mode", ["fused", "staged"])
+def test_peer_modes_fall_back_on_every_rank_when_pools_cannot_be_mapped(tmp_path, mode):
+    mp.spawn(_worker, args=(2, _free_port(), "banded", str(tmp_path), mode), nprocs=2, join=True)
     out = np.load(tmp_path / "out.npz")
     cfg = CASES["banded"]
     geom, (ka, ba), (kb, bb) = G.config_operands_host(cfg)

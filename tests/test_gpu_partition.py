@@ -35,7 +35,8 @@ def test_ranks_partition_the_product_exactly(dev, name, world):
     ref_keys = full.c_keys.cpu().numpy()
     ref_tptr = full.c_tptr.cpu().numpy()
     ref_tri = full.tri.view(-1, 2).cpu().numpy()
-    bounds = D.tile_partition(geom, a.keys.cpu().numpy(), b.keys.cpu().numpy(), world)
+    bounds = D.tile_partition(geom, a.keys.cpu().numpy(), b.keys.cpu().numpy(), world,
+                              am.cpu().numpy() if use else None, bm.cpu().numpy() if use else None)
     keys, tris, blocks = [], [], []
     c_full = spgemm.multiply_blocks(lay, a, b)
     for r in range(world):
@@ -76,3 +77,60 @@ def test_partitioned_distributed_path_single_rank_session(dev):
     c2, st = D.multiply(D.LocalComm(), _ffi.make_layout(geom.params, geom.bs), a, b)
     assert st.c_range == (0, 1 << (2 * geom.params.depth + 2 * geom.lbits))
     assert torch.equal(c1.keys, c2.keys) and torch.equal(c1.blocks, c2.blocks)
+
+
+def _in_process_peers(t: torch.Tensor, off: list) -> list:
+    """Device addresses of every rank's pool when all of them are slices of one tensor (the one-GPU
+    stand-in for CUDA-IPC-mapped peer pools)."""
+    blk = t.shape[1] * t.shape[2] * t.element_size()
+    return [t.data_ptr() + off[r] * blk for r in range(len(off) - 1)]
+
+
+@pytest.mark.parametrize("name,world,staged", [("C4", 4, True), ("C4", 8, True), ("C2-16384", 3, True),
+                                               ("C3", 2, True), ("C4", 4, False)])
+def test_staged_and_fused_rank_numeric_equal_single_gpu(dev, name, world, staged):
+    """staged_numeric for every rank, the operands' other ranks being slices of the same pools:
+    staged (halo gathered by k_halo_gather while the numeric kernel -- its programmatic dependent --
+    runs the local-only C blocks, the rest waiting for the gather) and fused (TMA reads of the peer
+    pools) give each rank's C blocks bitwise as the single-GPU product; the halo holds each remote
+    block once (halo_bytes = unique remote blocks). Also with an emulated slow link (the gather
+    lasts >= halo bytes / 20 GB/s), so the gated claims really wait."""
+    cfg = G.CONFIGS[name]
+    geom, a, b = G.config_operands_device(cfg, dev)
+    b_is_a = cfg.same_operand
+    if b_is_a:
+        b = a
+    lay = _ffi.make_layout(geom.params, geom.bs)
+    use = spgemm._use_masks(a, b)
+    am, bm = (a.masks[1], b.masks[0]) if use else (None, None)
+    c_full = spgemm.multiply_blocks(lay, a, b)
+    a_off = [(a.n * r) // world for r in range(world + 1)]
+    b_off = a_off if b_is_a else [(b.n * r) // world for r in range(world + 1)]
+    masks = (a.masks[1], b.masks[0], a.masks[2], b.masks[2]) if use else None
+    keys, blocks = [], []
+    for r in range(world):
+        st = spgemm.SymbolicState(lay, a.keys, a.n, b.keys, b.n, None, am, bm, part=(world, r))
+        if st.n_c == 0:
+            continue
+        ck, ct = st.keys()
+        tri32 = st.triples(ct)
+        tri = tri32.view(-1, 2).to(torch.int64)
+        info = {}
+        c, nz, zc = D.staged_numeric(lay, tri32, ct, ck, r, a_off, b_off, _in_process_peers(a.blocks, a_off),
+                                           _in_process_peers(b.blocks, b_off), a.blocks[a_off[r]:a_off[r + 1]],
+                                           b.blocks[b_off[r]:b_off[r + 1]], b_is_a, masks, staged=staged,
+                                           info=info, emulate_link_gbs=20.0 if r == 1 else None)
+        torch.cuda.synchronize()
+        if staged:
+            t = tri
+            ra = (t[:, 0] < a_off[r]) | (t[:, 0] >= a_off[r + 1])
+            rb = (t[:, 1] < b_off[r]) | (t[:, 1] >= b_off[r + 1])
+            uniq = (torch.unique(torch.cat([t[:, 0][ra], t[:, 1][rb]])).numel() if b_is_a else
+                    torch.unique(t[:, 0][ra]).numel() + torch.unique(t[:, 1][rb]).numel())
+            assert info["halo_bytes"] == uniq * geom.bs ** 2 * 8
+            assert 0 <= info["local_c_blocks"] <= st.n_c
+        c = spgemm.compact(geom.bs, c, nz, _ffi.read_i64(zc))
+        keys.append(c.keys)
+        blocks.append(c.blocks)
+    assert torch.equal(torch.cat(keys), c_full.keys)
+    assert torch.equal(torch.cat(blocks), c_full.blocks)
