@@ -35,13 +35,21 @@ namespace {
 
 // A CTA computes one TILE x TILE tile of a C block (TILE = BS, or 64 for BS = 128: the block is
 // then NQ = (BS/TILE)^2 work units whose partial norms are combined in a fixed order afterwards).
-template <int BS_, int TILE_, int WARPS_M_, int WARPS_N_, int KP_, int STAGES_, int MINB_>
+// EW (epilogue warp): the consumers write a finished tile into the stage holding the unit's last
+// k panel (32 KB = one bs-64 tile) instead of storing it themselves; an extra warp TMA-stores it
+// (cp.async.bulk.tensor, SASS UTMASTG) and computes its norm / exact-zero flag from shared memory,
+// then hands the stage back to the producer. The math warps' epilogue shrinks to a barrier and 16
+// shared stores -- for units of one or two triples (random patterns) it was ~7% of the kernel.
+// EW_ = 2: the consumers still compute the norms / flags from registers (only the stores move).
+template <int BS_, int TILE_, int WARPS_M_, int WARPS_N_, int KP_, int STAGES_, int MINB_, int EW_ = 0>
 struct TmaCfg {
   static constexpr int BS = BS_, TILE = TILE_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, KP = KP_;
   static constexpr int STAGES = STAGES_, MINB = MINB_;
+  static constexpr bool EW = EW_ != 0, EW_NORM = EW_ == 1;
   static constexpr int NQN = BS / TILE, NQ = NQN * NQN;  // tiles per C block
   static constexpr int NCW = WARPS_M * WARPS_N;         // consumer warps
-  static constexpr int NTHR = 32 * (NCW + 1);           // + one producer warp
+  static constexpr int NTHR = 32 * (NCW + 1 + (EW ? 1 : 0));  // + one producer warp (+ the epilogue warp)
+  static constexpr int NPART = EW_NORM ? 1 : NCW;       // partial norms per work unit
   static constexpr int TM = TILE / WARPS_M, TN = TILE / WARPS_N;
   static constexpr int MT = TM / 8, NT = TN / 8;
   static constexpr int NP = BS / KP;                    // k panels per triple
@@ -52,7 +60,8 @@ struct TmaCfg {
   static constexpr int A_BYTES = KSP * A_SP_BYTES;
   static constexpr int B_BYTES = NSP * B_SP_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 3 * STAGES * 8 + 2 * 32 * 8;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 5 * STAGES * 8 + 2 * 32 * 8;
+  static_assert(!EW || (size_t)TILE * TILE * 8 <= (size_t)STAGE_BYTES, "EW: a C tile must fit in one stage");
   static_assert(KP % 16 == 0 && BS % KP == 0 && TILE % 16 == 0 && BS % TILE == 0, "panels");
   static_assert(TM % 8 == 0 && TN % 8 == 0, "warp tile");
   static_assert(A_SP_BYTES % 1024 == 0 && B_SP_BYTES % 1024 == 0, "swizzle-128B atoms need 1 KB alignment");
@@ -71,6 +80,7 @@ template <int NPOOL, bool TR = false>
 struct __align__(64) TmaMaps {
   CUtensorMap a[NPOOL];
   CUtensorMap b[NPOOL];
+  CUtensorMap c;  // the C pool (EW variants: TMA stores of finished tiles)
 };
 // TR: triple indices may carry a transpose flag (bit 31): the stored block is used transposed, the
 // reference's virtual transposes (ops.py:100-116) as TMA box / shared-memory addressing choices.
@@ -79,6 +89,7 @@ template <int NPOOL>
 struct __align__(64) TmaMaps<NPOOL, true> {
   CUtensorMap a[NPOOL];
   CUtensorMap b[NPOOL];
+  CUtensorMap c;
   CUtensorMap at, bt;
 };
 constexpr uint32_t kTransposed = 1u << 31;
@@ -252,16 +263,90 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
   uint64_t *full = (uint64_t *)(smem + (size_t)STAGES * Cfg::STAGE_BYTES);
   uint64_t *empty = full + STAGES;
   volatile int64_t *meta = (volatile int64_t *)(empty + STAGES);  // per stage: unit*2 + last, -1 = end
+  // EW: finished tiles queued for the epilogue warp: slot j holds (unit << 4 | stage), -1 = end
+  uint64_t *cfull = (uint64_t *)(meta + STAGES);
+  volatile int64_t *cq = (volatile int64_t *)(cfull + STAGES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], Cfg::NCW);
+      if constexpr (Cfg::EW) mbar_init(&cfull[s], Cfg::NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+
+  if constexpr (Cfg::EW) {
+    if (warp == Cfg::NCW + 1) {
+      // ------------------------------ epilogue warp ------------------------------
+      // Per finished tile (in the consumers' order): TMA-store it from its stage (4 column
+      // sub-panels of TILE rows x 16 doubles, the SWIZZLE_128B layout the consumers wrote), sum
+      // its squares / test it for exact zero from shared memory meanwhile (fixed order: lane =
+      // row within each 32-row group, chunks in order, then a fixed shuffle tree), and give the
+      // stage back to the producer once the store has read it.
+      if (lane == 0) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&maps.c) : "memory");
+      const uint64_t c_policy = l2_evict_first_policy();
+      for (int64_t j = 0;; ++j) {
+        const int q = (int)(j % STAGES);
+        mbar_wait(&cfull[q], (uint32_t)((j / STAGES) & 1));
+        const int64_t e = cq[q];
+        if (e < 0) break;
+        const int64_t unit = e >> 4;
+        const int s = (int)(e & 15);
+        const uint8_t *st = smem + (size_t)s * Cfg::STAGE_BYTES;
+        const int64_t m = unit / Cfg::NQ;
+        const int qt = (int)(unit % Cfg::NQ);
+        const int row0 = (qt / Cfg::NQN) * Cfg::TILE, col0 = (qt % Cfg::NQN) * Cfg::TILE;
+        if (lane == 0) {
+#pragma unroll
+          for (int sp = 0; sp < Cfg::TILE / 16; ++sp)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;\n" ::"l"(
+                    &maps.c),
+                "r"(col0 + sp * 16), "r"((int)(m * BS + row0)), "r"(smem_u32(st + sp * Cfg::A_SP_BYTES)),
+                "l"(c_policy)
+                : "memory");
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+        if constexpr (Cfg::EW_NORM) {
+        double ss0 = 0.0, ss1 = 0.0;
+        bool nz = false;
+#pragma unroll 1
+        for (int sp = 0; sp < Cfg::TILE / 16; ++sp)
+#pragma unroll
+          for (int rr = 0; rr < Cfg::TILE / 32; ++rr) {
+            const int r = rr * 32 + lane;
+            const uint8_t *row = st + sp * Cfg::A_SP_BYTES + r * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const double2 v = *(const double2 *)(row + ((c ^ (r & 7)) << 4));
+              ss0 = fma(v.x, v.x, ss0);
+              ss1 = fma(v.y, v.y, ss1);
+              nz |= (v.x != 0.0) | (v.y != 0.0);
+            }
+          }
+        double ss = ss0 + ss1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        const bool wnz = __any_sync(0xffffffffu, nz);
+        if (lane == 0) {
+          part_sq[unit] = ss;
+          part_nz[unit] = wnz;
+        }
+        }
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // the store has read the stage
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&empty[s])), "r"(Cfg::NCW)
+                       : "memory");
+        }
+        __syncwarp();
+      }
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+      return;
+    }
+  }
 
   if (warp == Cfg::NCW) {
     // ------------------------------ producer warp ------------------------------
@@ -378,10 +463,20 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
 
   int s = 0;
   uint32_t phase = 0;
+  int64_t jq = 0;  // EW: tiles queued so far
   while (true) {
     mbar_wait(&full[s], phase);
     int64_t mt = meta[s];
-    if (mt < 0) break;
+    if (mt < 0) {
+      if constexpr (Cfg::EW) {  // tell the epilogue warp to finish
+        __syncwarp();
+        if (lane == 0) {
+          if (warp == 0) cq[jq % STAGES] = -1;
+          mbar_arrive(&cfull[jq % STAGES]);
+        }
+      }
+      break;
+    }
     bool ta = false, tb = false;
     if constexpr (TR) {
       ta = (mt >> 1) & 1;
@@ -437,13 +532,59 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
     // not drain its DMMA queue before releasing.
     dep &= zmask;
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s] + (uint32_t)dep);
+    if constexpr (Cfg::EW) {
+      if (mt & 1) {
+        // the unit's last stage becomes its C tile: every consumer warp is past its operand reads
+        // (named barrier), then writes its fragments in the TMA store layout and queues the tile;
+        // the epilogue warp releases the stage to the producer after storing it
+        asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::NCW * 32) : "memory");
+        uint8_t *cs = smem + (size_t)s * Cfg::STAGE_BYTES;
+        double ss0 = 0.0, ss1 = 0.0;
+        bool nz = false;
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            const int r = wm0 + i * 8 + g, c = wn0 + n * 8 + 2 * tq;
+            const uint32_t a = smem_u32(cs + (c >> 4) * Cfg::A_SP_BYTES + r * 128 + ((((c & 15) >> 1) ^ (r & 7)) << 4));
+            const double v0 = acc[i][n][0], v1 = acc[i][n][1];
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a), "d"(v0), "d"(v1) : "memory");
+            if constexpr (!Cfg::EW_NORM) {
+              ss0 = fma(v0, v0, ss0);
+              ss1 = fma(v1, v1, ss1);
+              nz |= (v0 != 0.0) | (v1 != 0.0);
+            }
+            acc[i][n][0] = acc[i][n][1] = 0.0;
+          }
+        if constexpr (!Cfg::EW_NORM) {
+          double ss = ss0 + ss1;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+          const bool wnz = __any_sync(0xffffffffu, nz);
+          if (lane == 0) {
+            part_sq[(mt >> 1) * Cfg::NPART + warp] = ss;
+            part_nz[(mt >> 1) * Cfg::NPART + warp] = wnz;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          if (warp == 0) cq[jq % STAGES] = ((mt >> 1) << 4) | s;
+          mbar_arrive(&cfull[jq % STAGES]);
+        }
+        ++jq;
+      } else if (lane == 0) {
+        mbar_arrive(&empty[s] + (uint32_t)dep);
+      }
+    } else {
+      if (lane == 0) mbar_arrive(&empty[s] + (uint32_t)dep);
+    }
     if (++s == STAGES) {
       s = 0;
       phase ^= 1u;
     }
 
-    if (mt & 1) {
+    if (!Cfg::EW && (mt & 1)) {
       const int64_t unit = mt >> 1;
       const int64_t m = unit / Cfg::NQ;
       const int qt = (int)(unit % Cfg::NQ);
@@ -454,30 +595,70 @@ __global__ void __launch_bounds__(Cfg::NTHR, Cfg::MINB)
       // fixed order afterwards (deterministic, no named barrier between the consumer warps).
       double ss0 = 0.0, ss1 = 0.0;
       bool nz = false;
+      uint32_t nz_lo = 0u, nz_hi = 0u;
+#if defined(QM_EXP_EPI) && QM_EXP_EPI == 3
+      uint64_t xbits[4] = {0, 0, 0, 0};
+#endif
 #pragma unroll
       for (int i = 0; i < MT; ++i)
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
           const double v0 = acc[i][n][0], v1 = acc[i][n][1];
-#if !defined(QM_EXP_EPI) || QM_EXP_EPI != 1
+#if !defined(QM_EXP_EPI) || (QM_EXP_EPI != 1 && QM_EXP_EPI != 3)
           st_evict_first(cb + (size_t)(wm0 + i * 8 + g) * BS + wn0 + n * 8 + 2 * tq, v0, v1, c_policy);
 #endif
+#if defined(QM_EXP_EPI) && QM_EXP_EPI == 3  // experiment: no epilogue work at all (upper bound)
+          xbits[(i * NT + n) & 3] ^= (uint64_t)__double_as_longlong(v0) ^ (uint64_t)__double_as_longlong(v1);
+#elif defined(QM_EXP_NZ_INT)  // measured slower (C3 1.078 -> 1.130 ms): integer exact-zero test
+          ss0 = fma(v0, v0, ss0);
+          ss1 = fma(v1, v1, ss1);
+          const uint64_t b0 = (uint64_t)__double_as_longlong(v0), b1 = (uint64_t)__double_as_longlong(v1);
+          nz_lo |= (uint32_t)b0 | (uint32_t)b1;
+          nz_hi |= (uint32_t)(b0 >> 32) | (uint32_t)(b1 >> 32);
+#elif defined(QM_EXP_NZ_SS)  // measured slower (C3 1.075 -> 1.18..1.21 ms): exact-zero test from ss
+          ss0 = fma(v0, v0, ss0);
+          ss1 = fma(v1, v1, ss1);
+#else
           ss0 = fma(v0, v0, ss0);
           ss1 = fma(v1, v1, ss1);
           nz |= (v0 != 0.0) | (v1 != 0.0);
+#endif
+#if !defined(QM_EXP_NZ_SS)
           acc[i][n][0] = acc[i][n][1] = 0.0;
+#endif
         }
       double ss = ss0 + ss1;
-#if defined(QM_EXP_EPI) && QM_EXP_EPI == 2
+#if defined(QM_EXP_EPI) && QM_EXP_EPI == 3
+      ss = __longlong_as_double((long long)((xbits[0] ^ xbits[1] ^ xbits[2] ^ xbits[3]) & 1ull));
+#endif
+#if defined(QM_EXP_EPI) && (QM_EXP_EPI == 2 || QM_EXP_EPI == 3)
       const bool wnz = true;
 #else
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+#if !defined(QM_EXP_NZ_SS)
+      nz |= (nz_lo | (nz_hi & 0x7fffffffu)) != 0u;
+#else
+      // Exact-zero test (_set_block's np.any) from the sum of squares: a nonzero, NaN or Inf square
+      // means a nonzero value. Only a warp whose squares all vanish -- an exactly zero tile, or
+      // values so small their squares underflow -- compares its values one by one.
+      nz = ss != 0.0;
+      if (!nz) {
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int n = 0; n < NT; ++n) nz |= (acc[i][n][0] != 0.0) | (acc[i][n][1] != 0.0);
+      }
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) acc[i][n][0] = acc[i][n][1] = 0.0;
+#endif
       const bool wnz = __any_sync(0xffffffffu, nz);
 #endif
       if (lane == 0) {
-        part_sq[unit * Cfg::NCW + warp] = ss;
-        part_nz[unit * Cfg::NCW + warp] = wnz;
+        part_sq[unit * Cfg::NPART + warp] = ss;
+        part_nz[unit * Cfg::NPART + warp] = wnz;
       }
     }
   }
@@ -639,7 +820,7 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
   }
   unsigned long long *counter = (unsigned long long *)ws;
   double *part_sq = (double *)((char *)ws + 256);
-  uint8_t *part_nz = (uint8_t *)(part_sq + nC * Cfg::NQ * Cfg::NCW);
+  uint8_t *part_nz = (uint8_t *)(part_sq + nC * Cfg::NQ * Cfg::NPART);
   QM_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
   for (int i = 0; i < na; ++i)
     if (nA[i] * (int64_t)Cfg::BS >= ((int64_t)1 << 31)) {
@@ -657,6 +838,10 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
     int rc = make_map(&maps.a[i], A[i < na ? i : 0], nA[i < na ? i : 0], Cfg::BS, Cfg::TILE);
     if (rc != QM_OK) return rc;
     rc = make_map(&maps.b[i], B[i < nb ? i : 0], nB[i < nb ? i : 0], Cfg::BS, Cfg::KP);
+    if (rc != QM_OK) return rc;
+  }
+  if constexpr (Cfg::EW) {
+    int rc = make_map(&maps.c, C, nC, Cfg::BS, Cfg::TILE);
     if (rc != QM_OK) return rc;
   }
   if constexpr (TR) {
@@ -757,7 +942,7 @@ int launch_tma_pools(const double *const *A, const int64_t *nA, int na, const do
   QM_LAUNCHED("k_numeric_tma");
   {
     int64_t g = std::min<int64_t>((nC + 255) / 256, (int64_t)sm_count_tma() * 8);
-    k_combine_tiles<<<(int)std::max<int64_t>(g, 1), 256, 0, st>>>(part_sq, part_nz, Cfg::NQ * Cfg::NCW,
+    k_combine_tiles<<<(int)std::max<int64_t>(g, 1), 256, 0, st>>>(part_sq, part_nz, Cfg::NQ * Cfg::NPART,
                                                                    nC, csq, cnz, zc, oi.panel_count, panel_fill);
     QM_LAUNCHED("k_combine_tiles");
   }
@@ -793,6 +978,17 @@ using Tma64 = TmaCfg<64, 64, 2, 2, 32, 3, 2>;
 // overheads; C2-131072 -0.7%, C4 -0.9%); about one triple per block (random patterns, C3): 2 CTAs
 // with 3 stages (deeper prefetch of DRAM-resident operands; C3 -1.4% against the 3-CTA variant).
 using Tma64m = TmaCfg<64, 64, 2, 2, 32, 2, 3>;
+// The epilogue warp variant of Tma64 (3 stages, 2 CTAs/SM), opt-in with QM_EPILOGUE_WARP=1.
+// Measured and not adopted (C3, r2): numeric 1.077 -> 1.234 ms. Both CTAs' epilogue warps land on
+// the same SM sub-partition, whose FP64 pipe then also runs every tile's sum-of-squares DFMAs
+// (4096 per tile), and the consumers' per-unit named barrier couples all four math warps to that
+// slowest sub-partition; C2-16384 1.104 -> 1.126 ms, banded / decay products unchanged.
+using Tma64e = TmaCfg<64, 64, 2, 2, 32, 3, 2, 1>;
+using Tma64s = TmaCfg<64, 64, 2, 2, 32, 3, 2, 2>;  // QM_EPILOGUE_WARP=2: the TMA store only
+int use_ew() {
+  const char *e = getenv("QM_EPILOGUE_WARP");
+  return e ? atoi(e) : 0;
+}
 constexpr int64_t kManyTriplesPerBlock = 2;
 
 // Variant choice for bs 64/128 (nU work units = C blocks x tiles per block): the 3-CTA variant needs
@@ -826,7 +1022,8 @@ size_t numeric_tma_ws_bytes(int bs, int64_t nC, int64_t nT) {
     case 32: return std::max(tma_ws_bytes<Tma32>(nC, nT), tma_ws_bytes<Tma32k16>(nC, nT));
     case 64:
       return std::max(std::max(tma_ws_bytes<Tma64>(nC, nT), tma_ws_bytes<Tma64m>(nC, nT)),
-                      tma_ws_bytes<Tma64k16>(nC, nT));
+                      std::max(tma_ws_bytes<Tma64k16>(nC, nT),
+                               std::max(tma_ws_bytes<Tma64e>(nC, nT), tma_ws_bytes<Tma64s>(nC, nT))));
     case 128: return std::max(tma_ws_bytes<Tma128>(nC, nT), tma_ws_bytes<Tma128m>(nC, nT));
     default: return 0;
   }
@@ -849,6 +1046,10 @@ int launch_numeric_tma(int bs, const double *const *A, const int64_t *nA, int na
         return launch_tma<Tma64k16>(A, nA, na, B, nB, nb, t2, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes, st);
       if (use_wide(nC, nC, nT))
         return launch_tma<Tma64m>(A, nA, na, B, nB, nb, t2, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes, st);
+      if (use_ew() == 1)
+        return launch_tma<Tma64e>(A, nA, na, B, nB, nb, t2, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes, st);
+      if (use_ew() == 2)
+        return launch_tma<Tma64s>(A, nA, na, B, nB, nb, t2, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes, st);
       return launch_tma<Tma64>(A, nA, na, B, nB, nb, t2, tptr, nC, nT, oi, C, csq, cnz, zc, ws, ws_bytes, st);
     case 128:
       if (use_wide(nC * Tma128::NQ, nC, nT))
