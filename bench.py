@@ -418,6 +418,8 @@ def run_ours(args):
                                        "max": int(m[:, 0].max())},
             "triples_per_gpu": {"min": int(m[:, 1].min()), "max": int(m[:, 1].max())},
             "phases_s_rank0": {k: round(x, 5) for k, x in ds.phase_s.items()},
+            "mode": ds.mode,  # fused (TMA reads of peer pools) / staged (halo gather) / exchange (NCCL)
+            "rank0": {k: v for k, v in ds.extra.items() if isinstance(v, (int, float))},
         }
         line["roofline"]["note"] = ("multi-GPU: 'numeric' phase = the whole distributed step "
                                     "(structure gather + symbolic + exchange + numeric)")

@@ -82,3 +82,34 @@ for _ in range(5):
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
 print("step ms", [round(x, 3) for x in ts])
+
+# host-side cost of each call of the step (no profiler): perf_counter around every call, GPU
+# synchronised only where the code itself synchronises
+def step_timed():
+    t = time.perf_counter
+    T = [t()]
+    st = spgemm.SymbolicState(lay, a.keys, a.n, b.keys, b.n, None, am, bm, part=(world, r))
+    T.append(t())
+    ck, ct = st.keys()
+    T.append(t())
+    tri = st.triples(ct)
+    T.append(t())
+    info = {}
+    c, nz, zc = D.staged_numeric(lay, tri, ct, ck, r, a_off, b_off, pa, pb, a.blocks[a_off[r]:a_off[r + 1]],
+                                 b.blocks[b_off[r]:b_off[r + 1]], b_is_a, masks, info=info,
+                                 emulate_link_gbs=link if link > 0 else None)
+    T.append(t())
+    n0 = _ffi.read_i64(zc)
+    T.append(t())
+    c = spgemm.compact(geom.bs, c, nz, n0)
+    T.append(t())
+    return [1e3 * (y - x) for x, y in zip(T, T[1:])]
+
+
+rows = []
+for _ in range(8):
+    torch.cuda.synchronize()
+    rows.append(step_timed())
+med = [sorted(col)[len(col) // 2] for col in zip(*rows)]
+print("host ms per call (median): count_part %.3f keys %.3f triples %.3f staged_numeric %.3f read %.3f compact %.3f"
+      % tuple(med))
