@@ -310,6 +310,8 @@ def run_ours(args):
                 dist_stats["last"] = ds
             return c
 
+    if world == 1:
+        a._bench_layout = layout  # (for the row-index timing of operand_meta_timing)
     meta = operand_meta_timing(lib, torch, a, stream) if world == 1 else None
     with torch.cuda.stream(stream):
         for _ in range(max(args.warmup, 0)):
@@ -525,11 +527,35 @@ def operand_meta_timing(lib, torch, a, stream) -> dict:
         torch.cuda.synchronize()
         best = min(best, ev[0].elapsed_time(ev[1]))
     nbytes = a.blocks.numel() * 8 + n * (8 + 24)
+    # the row index (the operand's row-sorted view the symbolic phase reads) is metadata too: built
+    # on the block set's first use as a factor and kept with it; timed here once, for the record
+    from paper_2011_11762_b200 import spgemm  # noqa: PLC0415
+    from paper_2011_11762_b200.blocks import BlockSet  # noqa: PLC0415
+
+    ix_ms = None
+    if spgemm.row_index_enabled():
+        geom_lay = getattr(a, "_bench_layout", None)
+        if geom_lay is not None:
+            tmp = BlockSet(a.keys, a.blocks, a.sumsq, a.masks, a.masks_full)
+            tb = float("inf")
+            for _ in range(3):
+                tmp.__dict__.pop("_row_index", None)
+                torch.cuda.synchronize()
+                ev[0].record(stream)
+                tmp.row_index(geom_lay, stream)
+                ev[1].record(stream)
+                torch.cuda.synchronize()
+                tb = min(tb, ev[0].elapsed_time(ev[1]))
+            ix_ms = round(tb, 4)
     return {"where": "computed once by the operands' producer (device generator -> qm_block_meta; "
                      "qm_build_fill_meta for matrix_from_triplets), not inside the product step; "
                      "the e2e step copies it with the blocks",
             "kernel": "k_block_meta", "ms_per_operand": round(best, 4),
-            "gbs": round(nbytes / (best * 1e-3) / 1e9, 1)}
+            "gbs": round(nbytes / (best * 1e-3) / 1e9, 1),
+            "row_index": {"where": "built on the operand's first use as a factor (qm_row_index_build: the "
+                                   "row-sorted view the symbolic phase reads), kept with the block set; the "
+                                   "e2e step's fresh operands build it inside the step",
+                          "ms_per_operand": ix_ms}}
 
 
 class HostOperands:

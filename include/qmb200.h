@@ -146,6 +146,36 @@ QM_API int qm_spgemm_count_part(const qm_layout *layout, const uint64_t *a_keys,
                                 int64_t nA, const uint64_t *b_keys, const uint64_t *b_rmask, int64_t nB,
                                 int32_t world, int32_t rank, void *ws, size_t ws_bytes, int64_t *n_c_out,
                                 int64_t *n_triples_out, int64_t *part_out, uint64_t *key_cuts, void *stream);
+/* Row index of one operand (operand metadata, like its norms and masks: built once per block set
+ * by qm_row_index_build and kept with it): the block set's entries sorted by (row, column) -- positions
+ * `perm`, rows, columns, row pointers [nbg+1] -- plus the support mask each sorted entry brings to a
+ * product (the block's column mask when it is the left operand, its row mask as the right one).
+ * With it the symbolic phase skips its own row indexing (the decode + radix sort of qm_spgemm_count). */
+typedef struct qm_row_index {
+  const uint32_t *rowptr; /* device [nbg + 1] */
+  const uint32_t *row;    /* device [n] */
+  const uint32_t *col;    /* device [n] */
+  const uint32_t *perm;   /* device [n]: index of the sorted entry in the block set */
+  const uint64_t *mask;   /* device [n] or NULL (full supports); both operands' or neither */
+} qm_row_index;
+QM_API size_t qm_row_index_workspace_bytes(const qm_layout *layout, int64_t n);
+/* masks: the block set's [3, n] support masks or NULL; cmask_sorted / rmask_sorted (optional, [n]):
+ * its column / row masks in row-sorted order (the left / right operand roles). */
+QM_API int qm_row_index_build(const qm_layout *layout, const uint64_t *keys, int64_t n, const uint64_t *masks, void *ws,
+                        size_t ws_bytes, uint32_t *rowptr, uint32_t *row, uint32_t *col, uint32_t *perm,
+                        uint64_t *cmask_sorted, uint64_t *rmask_sorted, void *stream);
+/* qm_spgemm_count_masked / _part over caller-held row indexes (world = 0: the whole product;
+ * world >= 1: rank's share, part_out / key_cuts as qm_spgemm_count_part). Same workspace. */
+QM_API int qm_spgemm_count_ix(const qm_layout *layout, const qm_row_index *a, int64_t nA, const qm_row_index *b,
+                              int64_t nB, int32_t flags, int32_t world, int32_t rank, void *ws, size_t ws_bytes,
+                              int64_t *n_c_out, int64_t *n_triples_out, int64_t *part_out, uint64_t *key_cuts,
+                              void *stream);
+/* Fill after qm_spgemm_count_ix: C keys + c_tptr (c_keys non-NULL) and/or triples [t_lo, t_hi) (tri
+ * non-NULL), with the same row indexes and workspaces. */
+QM_API int qm_spgemm_fill_ix(const qm_layout *layout, const qm_row_index *a, int64_t nA, const qm_row_index *b,
+                             int64_t nB, int64_t nC, int64_t t_lo, int64_t t_hi, void *ws, size_t ws_bytes,
+                             void *fill_ws, size_t fill_ws_bytes, uint64_t *c_keys, int64_t *c_tptr, uint32_t *tri,
+                             void *stream);
 QM_API size_t qm_spgemm_fill_workspace_bytes(const qm_layout *layout, int64_t nC);
 /* Emits the C key set in quadtree-key order (c_keys[nC]), the triple offsets c_tptr[nC+1] and the
  * triples tri[2*nT] = (a_index, b_index) pairs, grouped by C block, k ascending within a group --

@@ -42,6 +42,10 @@ EXPORTS = (
     "qm_spgemm_count",
     "qm_spgemm_count_masked",
     "qm_spgemm_count_part",
+    "qm_row_index_workspace_bytes",
+    "qm_row_index_build",
+    "qm_spgemm_count_ix",
+    "qm_spgemm_fill_ix",
     "qm_spgemm_fill_workspace_bytes",
     "qm_spgemm_fill",
     "qm_spgemm_fill_keys",
@@ -105,6 +109,13 @@ _LP = ctypes.POINTER(QmLayout)
 MAX_RANKS = 8  # QM_MAX_RANKS
 
 
+class QmRowIndex(ctypes.Structure):
+    """include/qmb200.h qm_row_index: one operand's row-sorted view (device pointers)."""
+
+    _fields_ = [("rowptr", ctypes.c_void_p), ("row", ctypes.c_void_p), ("col", ctypes.c_void_p),
+                ("perm", ctypes.c_void_p), ("mask", ctypes.c_void_p)]
+
+
 class QmHalo(ctypes.Structure):
     """include/qmb200.h qm_halo: the peer-owned blocks one rank gathers (staged multi-GPU product)."""
 
@@ -139,6 +150,12 @@ _SIGS = {
     "qm_spgemm_count_part": (ctypes.c_int, [_LP, _P, _P, _I64, _P, _P, _I64, _I32, _I32, _P, _SZ,
                                             ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64), _P,
                                             _P]),
+    "qm_row_index_workspace_bytes": (_SZ, [_LP, _I64]),
+    "qm_row_index_build": (ctypes.c_int, [_LP, _P, _I64, _P, _P, _SZ, _P, _P, _P, _P, _P, _P, _P]),
+    "qm_spgemm_count_ix": (ctypes.c_int, [_LP, _P, _I64, _P, _I64, _I32, _I32, _I32, _P, _SZ, ctypes.POINTER(_I64),
+                                          ctypes.POINTER(_I64), _P, _P, _P]),
+    "qm_spgemm_fill_ix": (ctypes.c_int, [_LP, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _SZ, _P, _SZ, _P, _P, _P,
+                                         _P]),
     "qm_spgemm_fill_workspace_bytes": (_SZ, [_LP, _I64]),
     "qm_spgemm_fill": (ctypes.c_int, [_LP, _I64, _I64, _I64, _I64, _P, _SZ, _P, _SZ, _P, _P, _P, _P]),
     "qm_spgemm_fill_keys": (ctypes.c_int, [_LP, _I64, _I64, _I64, _P, _SZ, _P, _SZ, _P, _P, _P]),

@@ -15,6 +15,7 @@ Memory is owned by PyTorch; libqmb200 only ever sees raw pointers.
 
 from __future__ import annotations
 
+import ctypes
 import itertools
 import math
 import threading
@@ -66,6 +67,48 @@ class BlockSet:
             self.masks_full = (True, True)
         self.masks = m
         return self
+
+    def row_index(self, layout, stream=None) -> dict:
+        """The block set's row-sorted view (qm_row_index_build): operand metadata like the norms and
+        masks, built once per (block set, layout) and kept with the immutable set, so a product's
+        symbolic phase skips its own row indexing. Tensors: rowptr, row, col, perm (int32) and the
+        column / row masks in row-sorted order (int64; when the set has masks)."""
+        from . import _ffi  # noqa: PLC0415
+
+        key = (int(layout.n_logical), int(layout.leaf_dim), int(layout.depth), int(layout.block_size))
+        cache = self.__dict__.setdefault("_row_index", {})
+        got = cache.get(key)
+        if got is not None and (got["cmask"] is not None or self.masks is None):
+            return got
+        lib = _ffi.load()
+        dev = self.device
+        n = self.n
+        nbg = (layout.leaf_dim // layout.block_size) << layout.depth
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        ix = {t: torch.empty(max(n, 1), dtype=torch.int32, device=dev) for t in ("row", "col", "perm")}
+        ix["rowptr"] = torch.empty(nbg + 1, dtype=torch.int32, device=dev)
+        has_m = self.masks is not None and n > 0
+        ix["cmask"] = torch.empty(max(n, 1), dtype=torch.int64, device=dev) if has_m else None
+        ix["rmask"] = torch.empty(max(n, 1), dtype=torch.int64, device=dev) if has_m else None
+        wb = lib.qm_row_index_workspace_bytes(ctypes.byref(layout), n)
+        ws = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
+        _ffi.check(lib.qm_row_index_build(ctypes.byref(layout), _ffi.ptr(self.keys), n,
+                                          _ffi.ptr(self.masks) if has_m else 0, _ffi.ptr(ws), wb,
+                                          _ffi.ptr(ix["rowptr"]), _ffi.ptr(ix["row"]), _ffi.ptr(ix["col"]),
+                                          _ffi.ptr(ix["perm"]), _ffi.ptr(ix["cmask"]), _ffi.ptr(ix["rmask"]),
+                                          _ffi.stream_handle(st)), "qm_row_index_build")
+        cache[key] = ix
+        return ix
+
+    @staticmethod
+    def ix_struct(ix: dict, role: str | None):
+        """qm_row_index of a row index as the left (role "a": column masks) or right ("b": row
+        masks) operand; role None: no masks."""
+        from . import _ffi  # noqa: PLC0415
+
+        mask = None if role is None else ix["cmask"] if role == "a" else ix["rmask"]
+        return _ffi.QmRowIndex(_ffi.ptr(ix["rowptr"]), _ffi.ptr(ix["row"]), _ffi.ptr(ix["col"]), _ffi.ptr(ix["perm"]),
+                               _ffi.ptr(mask))
 
     @property
     def n(self) -> int:

@@ -240,19 +240,19 @@ __device__ __forceinline__ bool row_out_of_range(int64_t i, int flags, const uin
 // dropped by _set_block anyway).
 template <class F>
 __device__ void for_window_pairs(const RowSpan &s, uint32_t wbase, bool multi, const uint32_t *a_scol,
-                                 const uint32_t *b_rp, const uint32_t *b_scol, const uint64_t *smask, bool masked,
-                                 F f) {
+                                 const uint32_t *b_rp, const uint32_t *b_scol, const uint64_t *a_smask,
+                                 const uint64_t *b_smask, bool masked, F f) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint32_t wend = min(wbase + (uint32_t)kWin, s.jmax + 1u);  // s.jmax: the row's (clamped) last column
   for (uint32_t x = s.a0 + warp; x < s.a1; x += nw) {
     uint32_t k = a_scol[x];
-    const uint64_t am = masked ? smask[x] : ~0ull;
+    const uint64_t am = masked ? a_smask[x] : ~0ull;
     uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
     if (multi) b0 = lower_bound_col(b_scol, b0, b1, wbase);
     for (uint32_t y = b0 + lane; y < b1; y += 32) {
       uint32_t j = b_scol[y];
       if (j >= wend) break;
-      if (!masked || (am & smask[y])) f(x, y, j);
+      if (!masked || (am & b_smask[y])) f(x, y, j);
     }
   }
 }
@@ -263,7 +263,8 @@ __device__ void for_window_pairs(const RowSpan &s, uint32_t wbase, bool multi, c
 // read-back.
 __global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const uint32_t *a_scol,
                                                    const uint32_t *b_rp, const uint32_t *b_scol,
-                                                   const uint64_t *smask, const int *masked_flag,
+                                                   const uint64_t *a_smask, const uint64_t *b_smask,
+                                                   const int *masked_flag,
                                                    const uint2 *rb, int64_t nbg, int nbl, int lbits,
                                                    uint64_t *cnt, uint64_t *off, unsigned int *done,
                                                    volatile int64_t *host_tot) {
@@ -288,7 +289,8 @@ __global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const u
         for (int w = threadIdx.x; w < kWin / 32; w += blockDim.x) bm[w] = 0u;
         __syncthreads();
         uint64_t mine = 0;
-        for_window_pairs(s, wbase, multi || raised, a_scol, b_rp, b_scol, smask, masked, [&](uint32_t, uint32_t, uint32_t j) {
+        for_window_pairs(s, wbase, multi || raised, a_scol, b_rp, b_scol, a_smask, b_smask, masked,
+                         [&](uint32_t, uint32_t, uint32_t j) {
           uint32_t o = j - wbase;
           atomicOr(&bm[o >> 5], 1u << (o & 31));
           ++mine;
@@ -323,7 +325,8 @@ __global__ void __launch_bounds__(kNT) k_sym_count(const uint32_t *a_rp, const u
 
 __global__ void __launch_bounds__(kNT) k_sym_emit_c(const uint32_t *a_rp, const uint32_t *a_scol,
                                                     const uint32_t *b_rp, const uint32_t *b_scol,
-                                                    const uint64_t *smask, const int *masked_flag,
+                                                    const uint64_t *a_smask, const uint64_t *b_smask,
+                                                    const int *masked_flag,
                                                     const uint2 *rb, int64_t nbg, int nbl, int lbits,
                                                     const uint64_t *rowC_off, uint64_t *rm_key,
                                                     uint32_t *rm_cnt, uint32_t *rm_iota, unsigned int *done) {
@@ -344,7 +347,7 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_c(const uint32_t *a_rp, const 
         const uint32_t wbase = (uint32_t)wb;
         for (int w = threadIdx.x; w < kWin; w += blockDim.x) cnt[w] = 0u;
         __syncthreads();
-        for_window_pairs(s, wbase, multi || raised, a_scol, b_rp, b_scol, smask, masked,
+        for_window_pairs(s, wbase, multi || raised, a_scol, b_rp, b_scol, a_smask, b_smask, masked,
                          [&](uint32_t, uint32_t, uint32_t j) { atomicAdd(&cnt[j - wbase], 1u); });
         __syncthreads();
         const int s0 = threadIdx.x * kPer;
@@ -381,7 +384,8 @@ static_assert(kPerT == 8, "slot ownership assumes 8 slots per thread");
 
 __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
     const uint32_t *a_rp, const uint32_t *a_scol, const uint32_t *a_perm, const uint32_t *b_rp,
-    const uint32_t *b_scol, const uint32_t *b_perm, const uint64_t *smask, const int *masked_flag,
+    const uint32_t *b_scol, const uint32_t *b_perm, const uint64_t *a_smask, const uint64_t *b_smask,
+    const int *masked_flag,
     const uint2 *rb, int64_t nbg, int nbl, int lbits, const uint64_t *rowC_off,
     const uint32_t *inv, const int64_t *c_tptr, int64_t t_lo, int64_t t_hi, uint2 *tri) {
   __shared__ uint32_t mask[kWinT];
@@ -423,13 +427,13 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
         // occupied C columns of the window
         for (uint32_t x = s.a0 + warp; x < s.a1; x += nw) {
           uint32_t k = a_scol[x];
-          const uint64_t am = masked ? smask[x] : ~0ull;
+          const uint64_t am = masked ? a_smask[x] : ~0ull;
           uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
           if (multi || upper) b0 = lower_bound_col(b_scol, b0, b1, wbase);
           for (uint32_t y = b0 + lane; y < b1; y += 32) {
             uint32_t j = b_scol[y];
             if (j >= wend) break;
-            if (!masked || (am & smask[y])) atomicOr(&bm[(j - wbase) >> 5], 1u << ((j - wbase) & 31));
+            if (!masked || (am & b_smask[y])) atomicOr(&bm[(j - wbase) >> 5], 1u << ((j - wbase) & 31));
           }
         }
         __syncthreads();
@@ -446,27 +450,27 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_tri(
           __syncthreads();
           for (uint32_t x = x0 + warp; x < xe; x += nw) {
             uint32_t k = a_scol[x];
-            const uint64_t am = masked ? smask[x] : ~0ull;
+            const uint64_t am = masked ? a_smask[x] : ~0ull;
             uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
             if (multi || upper) b0 = lower_bound_col(b_scol, b0, b1, wbase);
             for (uint32_t y = b0 + lane; y < b1; y += 32) {
               uint32_t j = b_scol[y];
               if (j >= wend) break;
-              if (!masked || (am & smask[y])) atomicOr(&mask[j - wbase], 1u << (x - x0));
+              if (!masked || (am & b_smask[y])) atomicOr(&mask[j - wbase], 1u << (x - x0));
             }
           }
           __syncthreads();
           for (uint32_t x = x0 + warp; x < xe; x += nw) {
             const uint32_t k = a_scol[x];
             const uint32_t ai = a_perm[x];
-            const uint64_t am = masked ? smask[x] : ~0ull;
+            const uint64_t am = masked ? a_smask[x] : ~0ull;
             const uint32_t below = (1u << (x - x0)) - 1u;
             uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
             if (multi || upper) b0 = lower_bound_col(b_scol, b0, b1, wbase);
             for (uint32_t y = b0 + lane; y < b1; y += 32) {
               uint32_t j = b_scol[y];
               if (j >= wend) break;
-              if (masked && !(am & smask[y])) continue;
+              if (masked && !(am & b_smask[y])) continue;
               const int64_t p = cur[j - wbase] + __popc(mask[j - wbase] & below);
               if (p >= t_lo && p < t_hi) tri[p - t_lo] = make_uint2(ai, b_perm[y]);
             }
@@ -522,23 +526,23 @@ __device__ __forceinline__ uint32_t panel_groups(uint64_t m) {
          (uint32_t)(((m >> 32) & 0xffffull) != 0) + (uint32_t)((m >> 48) != 0);
 }
 
-__global__ void k_tile_work(const uint32_t *srow, const uint32_t *scol, const uint64_t *smask,
-                            const int *masked_flag, int64_t nA, const uint32_t *b_rp, int nbl, int shift,
-                            uint64_t *tiles) {
+__global__ void k_tile_work(const uint32_t *srow, const uint32_t *a_scol, const uint64_t *a_smask,
+                            const int *masked_flag, int64_t nA, const uint32_t *b_rp, const uint32_t *b_scol,
+                            const uint64_t *b_smask, int nbl, int shift, uint64_t *tiles) {
   const uint32_t tw = (uint32_t)nbl << shift;  // tile width in blocks
   const bool masked = (*masked_flag & kFlagMasked) != 0;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t x = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); x < nA; x += nwarps) {
-    const uint32_t i = srow[x], k = scol[x];
+    const uint32_t i = srow[x], k = a_scol[x];
     const uint32_t b0 = b_rp[k], b1 = b_rp[k + 1];
-    const uint64_t am = masked ? smask[x] : ~0ull;
+    const uint64_t am = masked ? a_smask[x] : ~0ull;
     const uint64_t I = spread_bits((i / (uint32_t)nbl) >> shift) << 1;
     for (uint32_t base = b0; base < b1; base += 32) {
       const uint32_t y = base + lane;
       const bool valid = y < b1;
-      const uint32_t J = valid ? scol[y] / tw : 0xffffffffu;
-      const uint32_t w = !valid ? 0u : masked ? panel_groups(am & smask[y]) : 1u;
+      const uint32_t J = valid ? b_scol[y] / tw : 0xffffffffu;
+      const uint32_t w = !valid ? 0u : masked ? panel_groups(am & b_smask[y]) : 1u;
       const uint32_t peers = __match_any_sync(0xffffffffu, J);
       const uint32_t sum = __reduce_add_sync(peers, w);
       if (valid && sum && lane == __ffs(peers) - 1)
@@ -724,6 +728,74 @@ int row_grid(int64_t nbg) {
   return (int)std::max<int64_t>(g, 1);
 }
 
+// One operand's block-row index (the row-sorted view of a quadtree-ordered block set): positions
+// of the sorted entries, their rows and columns, the row pointers, and the support mask each entry
+// contributes to a product (its column mask as A, its row mask as B).
+struct Ix {
+  const uint32_t *rp = nullptr, *row = nullptr, *col = nullptr, *perm = nullptr;
+  const uint64_t *mask = nullptr;
+};
+
+// The two operands' indexes inside the symbolic workspace (the joint sort of build_rows): A's
+// entries are [0, nA), B's follow, and B's row pointers are the second half of rp.
+void ws_ix(const SymWs &w, const Geometry &g, int64_t nA, Ix *a, Ix *b) {
+  (void)nA;
+  a->rp = w.rp;
+  a->row = w.srow;
+  a->col = w.scol;
+  a->perm = w.perm;
+  a->mask = w.smask;
+  b->rp = w.rp + g.nbg;
+  b->row = w.srow;
+  b->col = w.scol;
+  b->perm = w.perm;
+  b->mask = w.smask;
+}
+
+Ix from_abi(const qm_row_index *r) {
+  Ix x;
+  x.rp = r->rowptr;
+  x.row = r->row;
+  x.col = r->col;
+  x.perm = r->perm;
+  x.mask = r->mask;
+  return x;
+}
+
+// Workspace flags and the completion ticket when the row indexes come from the caller (no
+// k_decode_rows / k_cols_rowptr to set them).
+__global__ void k_sym_init(int *flags, int value, unsigned int *done) {
+  *flags = value;
+  *done = 0u;
+}
+
+// Row index of one operand: columns, rows and the row pointers of the row-sorted entries, and the
+// column / row masks in that order (either may be NULL).
+__global__ void k_ix_cols(const uint64_t *keys, const uint32_t *srow, const uint32_t *perm, int64_t n, int64_t nbg,
+                          int nbl, int lbits, const uint64_t *masks, uint32_t *col, uint32_t *row, uint32_t *rp,
+                          uint64_t *cmask_sorted, uint64_t *rmask_sorted) {
+  const int64_t span = n > nbg + 1 ? n : nbg + 1;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < span; x += (int64_t)gridDim.x * blockDim.x) {
+    if (x < n) {
+      uint32_t bi, bj;
+      const uint32_t t = perm[x];
+      qkey_decode(keys[t], nbl, lbits, &bi, &bj);
+      col[x] = bj;
+      row[x] = bi;
+      if (cmask_sorted) cmask_sorted[x] = masks ? masks[n + t] : ~0ull;
+      if (rmask_sorted) rmask_sorted[x] = masks ? masks[t] : ~0ull;
+    }
+    if (x <= nbg) {
+      int64_t lo = 0, hi = n;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)srow[mid] < x) lo = mid + 1; else hi = mid;
+      }
+      rp[x] = (uint32_t)lo;
+    }
+  }
+}
+
 }  // namespace
 }  // namespace qm
 
@@ -738,39 +810,19 @@ extern "C" size_t qm_spgemm_workspace_bytes(const qm_layout *layout, int64_t nA,
 }
 
 namespace {
-int count_impl(const qm_layout *layout, const uint64_t *a_keys, const uint64_t *a_cmask, int64_t nA,
-               const uint64_t *b_keys, const uint64_t *b_rmask, int64_t nB, int32_t flags, int world, int rank,
-               void *ws, size_t ws_bytes, int64_t *n_c_out, int64_t *n_triples_out, int64_t *part_out,
-               uint64_t *key_cuts, void *stream) {
-  Geometry g;
-  int rc = make_geometry(layout, &g);
-  if (rc != QM_OK) return rc;
-  if (nA < 0 || nB < 0 || nA + nB >= (int64_t)1 << 32 || !n_c_out || !n_triples_out) {
-    set_error("qm_spgemm_count: bad sizes or output pointers");
-    return QM_ERR_INVALID;
-  }
-  cudaStream_t st = (cudaStream_t)stream;
-  Carver cv(ws, ws_bytes);
-  SymWs w = carve_sym(cv, nA, nB, g.nbg, tile_levels_for(g));
-  if (!cv.ok() || !ws) {
-    set_error("qm_spgemm_count: workspace %zu bytes < required %zu", ws_bytes, cv.off);
-    return QM_ERR_WORKSPACE;
-  }
-  *n_c_out = 0;
-  *n_triples_out = 0;
-  rc = build_rows(a_keys, a_cmask, nA, b_keys, b_rmask, nB, (flags & QM_SPGEMM_UPPER) ? 1 : 0, g, w, st);
-  if (rc != QM_OK) return rc;
-  const uint32_t *a_rp = w.rp, *b_rp = w.rp + g.nbg;
-  if (nA + nB == 0) QM_CUDA_TRY(cudaMemsetAsync(w.done, 0, sizeof(unsigned int), st));  // no k_decode_rows
+// Count phase over two row indexes (built into the workspace by build_rows, or the caller's).
+int count_core(const Geometry &g, const Ix &a, int64_t nA, const Ix &b, int64_t nB, int world, int rank,
+               const SymWs &w, int64_t *n_c_out, int64_t *n_triples_out, int64_t *part_out, uint64_t *key_cuts,
+               cudaStream_t st) {
   int64_t *host_tot = nullptr, *dev_tot = nullptr;
-  rc = mapped_i64(&host_tot, &dev_tot);
+  int rc = mapped_i64(&host_tot, &dev_tot);
   if (rc != QM_OK) return rc;
   if (world > 0) {  // multi-GPU partition: this rank's C key range from the tile work
     const int tl = w.tile_levels;
     const int64_t ntiles = (int64_t)1 << (2 * tl);
     QM_CUDA_TRY(cudaMemsetAsync(w.tiles, 0, (size_t)(ntiles + 1) * sizeof(uint64_t), st));
     if (nA > 0) {
-      k_tile_work<<<grid_for(nA * 32), 256, 0, st>>>(w.srow, w.scol, w.smask, w.masked, nA, b_rp, g.nbl,
+      k_tile_work<<<grid_for(nA * 32), 256, 0, st>>>(a.row, a.col, a.mask, w.masked, nA, b.rp, b.col, b.mask, g.nbl,
                                                       g.depth - tl, w.tiles);
       QM_LAUNCHED("k_tile_work");
     }
@@ -783,7 +835,7 @@ int count_impl(const qm_layout *layout, const uint64_t *a_keys, const uint64_t *
     k_row_bounds<<<grid_for(g.nbg), 256, 0, st>>>(w.krange, g.nbg, g.nbl, g.lbits, w.rb);
     QM_LAUNCHED("k_row_bounds");
   }
-  k_sym_count<<<row_grid(g.nbg), kNT, 0, st>>>(a_rp, w.scol, b_rp, w.scol, w.smask, w.masked, w.rb, g.nbg,
+  k_sym_count<<<row_grid(g.nbg), kNT, 0, st>>>(a.rp, a.col, b.rp, b.col, a.mask, b.mask, w.masked, w.rb, g.nbg,
                                                g.nbl, g.lbits, w.cnt, w.off, w.done, dev_tot);
   QM_LAUNCHED("k_sym_count");
   QM_CUDA_TRY(cudaStreamSynchronize(st));
@@ -801,6 +853,42 @@ int count_impl(const qm_layout *layout, const uint64_t *a_keys, const uint64_t *
     part_out[2] = ht[4];
   }
   return QM_OK;
+}
+
+int count_setup(const qm_layout *layout, int64_t nA, int64_t nB, void *ws, size_t ws_bytes, int64_t *n_c_out,
+                int64_t *n_triples_out, Geometry *g, SymWs *w) {
+  int rc = make_geometry(layout, g);
+  if (rc != QM_OK) return rc;
+  if (nA < 0 || nB < 0 || nA + nB >= (int64_t)1 << 32 || !n_c_out || !n_triples_out) {
+    set_error("qm_spgemm_count: bad sizes or output pointers");
+    return QM_ERR_INVALID;
+  }
+  Carver cv(ws, ws_bytes);
+  *w = carve_sym(cv, nA, nB, g->nbg, tile_levels_for(*g));
+  if (!cv.ok() || !ws) {
+    set_error("qm_spgemm_count: workspace %zu bytes < required %zu", ws_bytes, cv.off);
+    return QM_ERR_WORKSPACE;
+  }
+  *n_c_out = 0;
+  *n_triples_out = 0;
+  return QM_OK;
+}
+
+int count_impl(const qm_layout *layout, const uint64_t *a_keys, const uint64_t *a_cmask, int64_t nA,
+               const uint64_t *b_keys, const uint64_t *b_rmask, int64_t nB, int32_t flags, int world, int rank,
+               void *ws, size_t ws_bytes, int64_t *n_c_out, int64_t *n_triples_out, int64_t *part_out,
+               uint64_t *key_cuts, void *stream) {
+  Geometry g;
+  SymWs w;
+  int rc = count_setup(layout, nA, nB, ws, ws_bytes, n_c_out, n_triples_out, &g, &w);
+  if (rc != QM_OK) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  rc = build_rows(a_keys, a_cmask, nA, b_keys, b_rmask, nB, (flags & QM_SPGEMM_UPPER) ? 1 : 0, g, w, st);
+  if (rc != QM_OK) return rc;
+  if (nA + nB == 0) QM_CUDA_TRY(cudaMemsetAsync(w.done, 0, sizeof(unsigned int), st));  // no k_decode_rows
+  Ix a, b;
+  ws_ix(w, g, nA, &a, &b);
+  return count_core(g, a, nA, b, nB, world, rank, w, n_c_out, n_triples_out, part_out, key_cuts, st);
 }
 }  // namespace
 
@@ -829,6 +917,83 @@ extern "C" int qm_spgemm_count(const qm_layout *layout, const uint64_t *a_keys, 
                                int64_t *n_c_out, int64_t *n_triples_out, void *stream) {
   return qm_spgemm_count_masked(layout, a_keys, nullptr, nA, b_keys, nullptr, nB, 0, ws, ws_bytes, n_c_out,
                                 n_triples_out, stream);
+}
+
+// ---- caller-held row indexes (operand metadata: built once per block set, reused by products) ----
+extern "C" size_t qm_row_index_workspace_bytes(const qm_layout *layout, int64_t n) {
+  Geometry g;
+  if (make_geometry(layout, &g) != QM_OK) return 0;
+  Carver cv(nullptr, 0);
+  cv.take<uint32_t>(std::max<int64_t>(n, 1));  // row keys
+  cv.take<uint32_t>(std::max<int64_t>(n, 1));  // iota
+  cv.take<uint32_t>(std::max<int64_t>(n, 1));  // sorted rows
+  size_t cb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cb, (uint32_t *)nullptr, (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                  (uint32_t *)nullptr, std::max<int64_t>(n, 1), 0, 32);
+  cv.take<char>(cb);
+  cv.take<unsigned int>(1);
+  return cv.off;
+}
+
+extern "C" int qm_row_index_build(const qm_layout *layout, const uint64_t *keys, int64_t n, const uint64_t *masks,
+                            void *ws, size_t ws_bytes, uint32_t *rowptr, uint32_t *row, uint32_t *col, uint32_t *perm,
+                            uint64_t *cmask_sorted, uint64_t *rmask_sorted, void *stream) {
+  Geometry g;
+  int rc = make_geometry(layout, &g);
+  if (rc != QM_OK) return rc;
+  if (n < 0 || n >= ((int64_t)1 << 32) || !rowptr || (n > 0 && (!keys || !row || !col || !perm))) {
+    set_error("qm_row_index_build: bad arguments");
+    return QM_ERR_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  Carver cv(ws, ws_bytes);
+  uint32_t *rowkey = cv.take<uint32_t>(std::max<int64_t>(n, 1));
+  uint32_t *iota = cv.take<uint32_t>(std::max<int64_t>(n, 1));
+  uint32_t *srow = cv.take<uint32_t>(std::max<int64_t>(n, 1));
+  size_t cb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cb, (uint32_t *)nullptr, (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                  (uint32_t *)nullptr, std::max<int64_t>(n, 1), 0, 32);
+  void *cub_tmp = cv.take<char>(cb);
+  unsigned int *done = cv.take<unsigned int>(1);
+  if (!cv.ok() || !ws) {
+    set_error("qm_row_index_build: workspace %zu bytes < required %zu", ws_bytes, cv.off);
+    return QM_ERR_WORKSPACE;
+  }
+  if (n > 0) {
+    k_decode_rows<<<grid_for(n), 256, 0, st>>>(keys, n, nullptr, 0, g.nbg, g.nbl, g.lbits, rowkey, iota, done);
+    QM_LAUNCHED("k_decode_rows");
+    QM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, cb, rowkey, srow, iota, perm, n, 0,
+                                                bits_for((uint64_t)std::max<int64_t>(g.nbg - 1, 1)), st));
+  }
+  k_ix_cols<<<grid_for(std::max<int64_t>(n, g.nbg + 1)), 256, 0, st>>>(keys, srow, perm, n, g.nbg, g.nbl, g.lbits,
+                                                                        masks, col, row, rowptr, cmask_sorted,
+                                                                        rmask_sorted);
+  QM_LAUNCHED("k_ix_cols");
+  return QM_OK;
+}
+
+extern "C" int qm_spgemm_count_ix(const qm_layout *layout, const qm_row_index *a, int64_t nA, const qm_row_index *b,
+                                  int64_t nB, int32_t flags, int32_t world, int32_t rank, void *ws, size_t ws_bytes,
+                                  int64_t *n_c_out, int64_t *n_triples_out, int64_t *part_out, uint64_t *key_cuts,
+                                  void *stream) {
+  if (!a || !b || (world > 0 && (rank < 0 || rank >= world || !part_out)) || world < 0) {
+    set_error("qm_spgemm_count_ix: bad arguments");
+    return QM_ERR_INVALID;
+  }
+  if ((a->mask == nullptr) != (b->mask == nullptr)) {
+    set_error("qm_spgemm_count_ix: give both operands' masks or neither");
+    return QM_ERR_INVALID;
+  }
+  Geometry g;
+  SymWs w;
+  int rc = count_setup(layout, nA, nB, ws, ws_bytes, n_c_out, n_triples_out, &g, &w);
+  if (rc != QM_OK) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  k_sym_init<<<1, 1, 0, st>>>(w.masked, (a->mask ? kFlagMasked : 0) | ((flags & QM_SPGEMM_UPPER) ? kFlagUpper : 0),
+                              w.done);
+  QM_LAUNCHED("k_sym_init");
+  return count_core(g, from_abi(a), nA, from_abi(b), nB, world, rank, w, n_c_out, n_triples_out, part_out, key_cuts,
+                    st);
 }
 
 extern "C" size_t qm_spgemm_fill_workspace_bytes(const qm_layout *layout, int64_t nC) {
@@ -860,21 +1025,12 @@ int fill_setup(const qm_layout *layout, int64_t nA, int64_t nB, int64_t nC, void
   }
   return QM_OK;
 }
-}  // namespace
 
-extern "C" int qm_spgemm_fill_keys(const qm_layout *layout, int64_t nA, int64_t nB, int64_t nC,
-                                   void *ws, size_t ws_bytes, void *fill_ws, size_t fill_ws_bytes,
-                                   uint64_t *c_keys, int64_t *c_tptr, void *stream) {
-  Geometry g;
-  SymWs w;
-  FillWs f;
-  int key_bits;
-  int rc = fill_setup(layout, nA, nB, nC, ws, ws_bytes, fill_ws, fill_ws_bytes, &g, &w, &f, &key_bits);
-  if (rc != QM_OK) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
+int fill_keys_core(const Geometry &g, const Ix &a, const Ix &b, int64_t nC, const SymWs &w, const FillWs &f,
+                   int key_bits, uint64_t *c_keys, int64_t *c_tptr, cudaStream_t st) {
   if (nC == 0) return cudaMemsetAsync(c_tptr, 0, sizeof(int64_t), st) == cudaSuccess ? QM_OK : QM_ERR_CUDA;
-  k_sym_emit_c<<<row_grid(g.nbg), kNT, 0, st>>>(w.rp, w.scol, w.rp + g.nbg, w.scol, w.smask, w.masked, w.rb,
-                                                g.nbg, g.nbl, g.lbits, w.off, f.rm_key, f.rm_cnt, f.rm_iota, f.done);
+  k_sym_emit_c<<<row_grid(g.nbg), kNT, 0, st>>>(a.rp, a.col, b.rp, b.col, a.mask, b.mask, w.masked, w.rb, g.nbg,
+                                                g.nbl, g.lbits, w.off, f.rm_key, f.rm_cnt, f.rm_iota, f.done);
   QM_LAUNCHED("k_sym_emit_c");
   size_t tb = f.cub_bytes;
   QM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(f.cub, tb, f.rm_key, c_keys, f.rm_iota, f.perm, nC, 0,
@@ -890,6 +1046,31 @@ extern "C" int qm_spgemm_fill_keys(const qm_layout *layout, int64_t nA, int64_t 
   return QM_OK;
 }
 
+int fill_triples_core(const Geometry &g, const Ix &a, const Ix &b, int64_t nC, const SymWs &w, const FillWs &f,
+                      const int64_t *c_tptr, int64_t t_lo, int64_t t_hi, uint32_t *tri, cudaStream_t st) {
+  if (nC == 0 || t_hi <= t_lo) return QM_OK;
+  k_sym_emit_tri<<<row_grid(g.nbg), kNT, 0, st>>>(a.rp, a.col, a.perm, b.rp, b.col, b.perm, a.mask, b.mask,
+                                                  w.masked, w.rb, g.nbg, g.nbl, g.lbits, w.off, f.inv, c_tptr, t_lo,
+                                                  t_hi, (uint2 *)tri);
+  QM_LAUNCHED("k_sym_emit_tri");
+  return QM_OK;
+}
+}  // namespace
+
+extern "C" int qm_spgemm_fill_keys(const qm_layout *layout, int64_t nA, int64_t nB, int64_t nC,
+                                   void *ws, size_t ws_bytes, void *fill_ws, size_t fill_ws_bytes,
+                                   uint64_t *c_keys, int64_t *c_tptr, void *stream) {
+  Geometry g;
+  SymWs w;
+  FillWs f;
+  int key_bits;
+  int rc = fill_setup(layout, nA, nB, nC, ws, ws_bytes, fill_ws, fill_ws_bytes, &g, &w, &f, &key_bits);
+  if (rc != QM_OK) return rc;
+  Ix a, b;
+  ws_ix(w, g, nA, &a, &b);
+  return fill_keys_core(g, a, b, nC, w, f, key_bits, c_keys, c_tptr, (cudaStream_t)stream);
+}
+
 extern "C" int qm_spgemm_fill_triples(const qm_layout *layout, int64_t nA, int64_t nB, int64_t nC,
                                       void *ws, size_t ws_bytes, void *fill_ws, size_t fill_ws_bytes,
                                       const int64_t *c_tptr, int64_t t_lo, int64_t t_hi, uint32_t *tri,
@@ -900,13 +1081,9 @@ extern "C" int qm_spgemm_fill_triples(const qm_layout *layout, int64_t nA, int64
   int key_bits;
   int rc = fill_setup(layout, nA, nB, nC, ws, ws_bytes, fill_ws, fill_ws_bytes, &g, &w, &f, &key_bits);
   if (rc != QM_OK) return rc;
-  if (nC == 0 || t_hi <= t_lo) return QM_OK;
-  cudaStream_t st = (cudaStream_t)stream;
-  k_sym_emit_tri<<<row_grid(g.nbg), kNT, 0, st>>>(w.rp, w.scol, w.perm, w.rp + g.nbg, w.scol,
-                                                  w.perm, w.smask, w.masked, w.rb, g.nbg, g.nbl, g.lbits, w.off,
-                                                  f.inv, c_tptr, t_lo, t_hi, (uint2 *)tri);
-  QM_LAUNCHED("k_sym_emit_tri");
-  return QM_OK;
+  Ix a, b;
+  ws_ix(w, g, nA, &a, &b);
+  return fill_triples_core(g, a, b, nC, w, f, c_tptr, t_lo, t_hi, tri, (cudaStream_t)stream);
 }
 
 extern "C" int qm_spgemm_fill(const qm_layout *layout, int64_t nA, int64_t nB, int64_t nC, int64_t nT,
@@ -917,4 +1094,28 @@ extern "C" int qm_spgemm_fill(const qm_layout *layout, int64_t nA, int64_t nB, i
   if (rc != QM_OK) return rc;
   return qm_spgemm_fill_triples(layout, nA, nB, nC, ws, ws_bytes, fill_ws, fill_ws_bytes, c_tptr, 0, nT,
                                 tri, stream);
+}
+
+extern "C" int qm_spgemm_fill_ix(const qm_layout *layout, const qm_row_index *a, int64_t nA, const qm_row_index *b,
+                                 int64_t nB, int64_t nC, int64_t t_lo, int64_t t_hi, void *ws, size_t ws_bytes,
+                                 void *fill_ws, size_t fill_ws_bytes, uint64_t *c_keys, int64_t *c_tptr, uint32_t *tri,
+                                 void *stream) {
+  if (!a || !b) {
+    set_error("qm_spgemm_fill_ix: NULL row index");
+    return QM_ERR_INVALID;
+  }
+  Geometry g;
+  SymWs w;
+  FillWs f;
+  int key_bits;
+  int rc = fill_setup(layout, nA, nB, nC, ws, ws_bytes, fill_ws, fill_ws_bytes, &g, &w, &f, &key_bits);
+  if (rc != QM_OK) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const Ix ia = from_abi(a), ib = from_abi(b);
+  if (c_keys) {  // keys + c_tptr (c_keys NULL: triples only, c_tptr already filled)
+    rc = fill_keys_core(g, ia, ib, nC, w, f, key_bits, c_keys, c_tptr, st);
+    if (rc != QM_OK) return rc;
+  }
+  if (tri) return fill_triples_core(g, ia, ib, nC, w, f, c_tptr, t_lo, t_hi, tri, st);
+  return QM_OK;
 }

@@ -69,10 +69,13 @@ class SymbolicState:
 
     def __init__(self, layout, a_keys: torch.Tensor, n_a: int, b_keys: torch.Tensor, n_b: int, stream=None,
                  a_cmask: torch.Tensor | None = None, b_rmask: torch.Tensor | None = None, upper: bool = False,
-                 part: tuple[int, int] | None = None):
+                 part: tuple[int, int] | None = None, ix=None):
         """part = (world, rank): the rank's share of a multi-GPU product (qm_spgemm_count_part) --
-        only the C blocks of its own key range (self.key_range) are counted and emitted."""
+        only the C blocks of its own key range (self.key_range) are counted and emitted.
+        ix = (qm_row_index of A, of B): the operands' cached row indexes (BlockSet.row_index); the
+        count / fill calls then use them instead of indexing the keys themselves."""
         self.lib = _ffi.load()
+        self.ix = ix
         self.layout = layout
         self.lp = ctypes.byref(layout)
         self.n_a, self.n_b = n_a, n_b
@@ -83,7 +86,22 @@ class SymbolicState:
         n_c = ctypes.c_int64(0)
         n_t = ctypes.c_int64(0)
         self.key_range, self.tile_work, self.key_cuts = None, 0, None
-        if part is not None:
+        if ix is not None:
+            world, rank = part if part is not None else (0, 0)
+            po = (ctypes.c_int64 * 3)()
+            if part is not None:
+                self.key_cuts = _alloc(world + 1, torch.int64, self.dev)
+            _ffi.check(
+                self.lib.qm_spgemm_count_ix(self.lp, ctypes.byref(ix[0]), n_a, ctypes.byref(ix[1]), n_b,
+                                            1 if upper else 0, world, rank, _ffi.ptr(self.ws), self.ws_bytes,
+                                            ctypes.byref(n_c), ctypes.byref(n_t), po if part is not None else None,
+                                            _ffi.ptr(self.key_cuts), self.sh),
+                "qm_spgemm_count_ix",
+            )
+            if part is not None:
+                self.key_range = (int(po[0]) & (2**64 - 1), int(po[1]) & (2**64 - 1))
+                self.tile_work = int(po[2])
+        elif part is not None:
             world, rank = part
             po = (ctypes.c_int64 * 3)()
             self.key_cuts = _alloc(world + 1, torch.int64, self.dev)
@@ -111,6 +129,9 @@ class SymbolicState:
         """C keys (quadtree order) and triple offsets c_tptr[nC+1]."""
         c_keys = _alloc(self.n_c, torch.int64, self.dev)
         c_tptr = _alloc(self.n_c + 1, torch.int64, self.dev)
+        if self.ix is not None:
+            self.fill_ix(c_keys, c_tptr, None, 0, 0)
+            return c_keys, c_tptr
         _ffi.check(
             self.lib.qm_spgemm_fill_keys(self.lp, self.n_a, self.n_b, self.n_c, _ffi.ptr(self.ws),
                                          self.ws_bytes, _ffi.ptr(self.fws), self.fill_bytes,
@@ -123,6 +144,9 @@ class SymbolicState:
         """(a_index, b_index) int32 pairs of triples [t_lo, t_hi)."""
         t_hi = self.n_t if t_hi is None else t_hi
         tri = _alloc(2 * max(t_hi - t_lo, 0), torch.int32, self.dev)
+        if self.ix is not None:
+            self.fill_ix(None, c_tptr, tri, t_lo, t_hi)
+            return tri
         _ffi.check(
             self.lib.qm_spgemm_fill_triples(self.lp, self.n_a, self.n_b, self.n_c, _ffi.ptr(self.ws),
                                             self.ws_bytes, _ffi.ptr(self.fws), self.fill_bytes,
@@ -132,9 +156,24 @@ class SymbolicState:
         return tri
 
 
+    def fill_ix(self, c_keys, c_tptr, tri, t_lo: int, t_hi: int):
+        """qm_spgemm_fill_ix: C keys + c_tptr (c_keys given) and / or triples [t_lo, t_hi)."""
+        _ffi.check(
+            self.lib.qm_spgemm_fill_ix(self.lp, ctypes.byref(self.ix[0]), self.n_a, ctypes.byref(self.ix[1]), self.n_b,
+                                       self.n_c, t_lo, t_hi, _ffi.ptr(self.ws), self.ws_bytes, _ffi.ptr(self.fws),
+                                       self.fill_bytes, _ffi.ptr(c_keys), _ffi.ptr(c_tptr), _ffi.ptr(tri), self.sh),
+            "qm_spgemm_fill_ix",
+        )
+
+
 def support_filter_enabled() -> bool:
     """QM_SUPPORT_FILTER=0 disables the exact-zero product filter (A/B measurements, tests)."""
     return os.environ.get("QM_SUPPORT_FILTER", "1") != "0"
+
+
+def row_index_enabled() -> bool:
+    """QM_ROW_INDEX=0: the symbolic phase indexes the operands' keys itself on every product."""
+    return os.environ.get("QM_ROW_INDEX", "1") != "0"
 
 
 def _use_masks(a: BlockSet, b: BlockSet, stream=None) -> bool:
@@ -153,18 +192,26 @@ def symbolic(layout, a: BlockSet, b: BlockSet, stream=None, upper: bool = False)
     without triples is an exact-zero block the reference computes and then drops (_set_block,
     block_sparse.py:37-41), so the product is unchanged."""
     a_cm = b_rm = None
-    if _use_masks(a, b, stream):
+    use = _use_masks(a, b, stream)
+    if use:
         a_cm, b_rm = a.masks[1], b.masks[0]
-    st = SymbolicState(layout, a.keys, a.n, b.keys, b.n, stream, a_cm, b_rm, upper)
+    ix = None
+    if row_index_enabled() and type(a) is BlockSet and type(b) is BlockSet:  # (views index their entries)
+        ia, ib = a.row_index(layout, stream), b.row_index(layout, stream)
+        ix = (BlockSet.ix_struct(ia, "a" if use else None), BlockSet.ix_struct(ib, "b" if use else None))
+    st = SymbolicState(layout, a.keys, a.n, b.keys, b.n, stream, a_cm, b_rm, upper, ix=ix)
     c_keys = _alloc(st.n_c, torch.int64, st.dev)
     c_tptr = _alloc(st.n_c + 1, torch.int64, st.dev)
     tri = _alloc(2 * st.n_t, torch.int32, st.dev)
-    _ffi.check(  # C keys, c_tptr and every triple in one call (keys() + triples() of SymbolicState)
-        st.lib.qm_spgemm_fill(st.lp, st.n_a, st.n_b, st.n_c, st.n_t, _ffi.ptr(st.ws), st.ws_bytes,
-                              _ffi.ptr(st.fws), st.fill_bytes, _ffi.ptr(c_keys), _ffi.ptr(c_tptr),
-                              _ffi.ptr(tri), st.sh),
-        "qm_spgemm_fill",
-    )
+    if ix is not None:
+        st.fill_ix(c_keys, c_tptr, tri, 0, st.n_t)
+    else:
+        _ffi.check(  # C keys, c_tptr and every triple in one call (keys() + triples() of SymbolicState)
+            st.lib.qm_spgemm_fill(st.lp, st.n_a, st.n_b, st.n_c, st.n_t, _ffi.ptr(st.ws), st.ws_bytes,
+                                  _ffi.ptr(st.fws), st.fill_bytes, _ffi.ptr(c_keys), _ffi.ptr(c_tptr),
+                                  _ffi.ptr(tri), st.sh),
+            "qm_spgemm_fill",
+        )
     return SymbolicPlan(st.n_c, st.n_t, c_keys, c_tptr, tri)
 
 

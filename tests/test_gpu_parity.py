@@ -965,3 +965,40 @@ def test_support_filter_multi_window_rows(ses):
     _, _, ta, tb, _ = O.symbolic(g, ka, ka)
     rm, cm = helpers.support_masks_np(ba)
     assert st.n_triples == int(((cm[ta] & rm[tb]) != 0).sum()) < ta.size
+
+
+@pytest.mark.parametrize("name", ["C1", "C2-16384", "C3", "C4"])
+def test_cached_row_index_symbolic_equals_keys_path(ses, monkeypatch, name):
+    """The symbolic phase over the operands' cached row indexes (qm_row_index_build +
+    qm_spgemm_count_ix / fill_ix) gives the same C keys, c_tptr and triples, in the same order, as
+    the path that indexes the keys itself (QM_ROW_INDEX=0); masked (C4) and unmasked."""
+    cfg = G.CONFIGS[name]
+    geom, a, b = G.config_operands_device(cfg, ses.device)
+    if cfg.same_operand:
+        b = a
+    lay = _ffi.make_layout(geom.params, geom.bs)
+    monkeypatch.setenv("QM_ROW_INDEX", "1")
+    p1 = spgemm.symbolic(lay, a, b)
+    assert "_row_index" in a.__dict__
+    monkeypatch.setenv("QM_ROW_INDEX", "0")
+    p0 = spgemm.symbolic(lay, a, b)
+    assert (p1.n_c, p1.n_triples) == (p0.n_c, p0.n_triples)
+    assert torch.equal(p1.c_keys, p0.c_keys) and torch.equal(p1.c_tptr, p0.c_tptr) and torch.equal(p1.tri, p0.tri)
+
+
+def test_cached_row_index_on_wide_rows(ses, monkeypatch):
+    """Rows spanning several 4096-column windows of the count accumulator (as
+    test_support_filter_multi_window_rows): the row-index path equals the keys path."""
+    n, bs = 16384 * 2, 4
+    rng = np.random.default_rng(3)
+    rows = np.repeat(np.arange(0, n, 97), 40)
+    cols = rng.integers(0, n, rows.size)
+    vals = rng.uniform(-1, 1, rows.size)
+    a = ses.matrix_from_triplets(n, rows, cols, vals, leaf_dim=64, block_size=bs)
+    sa = a.root.blockset
+    lay = _ffi.make_layout(a.geometry.params, bs)
+    monkeypatch.setenv("QM_ROW_INDEX", "1")
+    p1 = spgemm.symbolic(lay, sa, sa)
+    monkeypatch.setenv("QM_ROW_INDEX", "0")
+    p0 = spgemm.symbolic(lay, sa, sa)
+    assert torch.equal(p1.c_keys, p0.c_keys) and torch.equal(p1.tri, p0.tri)
