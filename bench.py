@@ -287,11 +287,19 @@ def run_ours(args):
         geom = cfg.geometry
         layout = _ffi.make_layout(geom.params, geom.bs)
         parts = []
-        for m in (0, 1):
-            keys = G.config_keys(cfg, m)
-            lo, hi = (keys.size * rank) // world, (keys.size * (rank + 1)) // world
-            parts.append(G.device_blocks(geom, keys[lo:hi], cfg.seed, m, G.config_pattern(cfg),
-                                         cfg.half_bw, dev))
+        b_is_a = cfg.same_operand
+        if cfg.kind == "decay":  # host-built operand (C = A*A); each rank keeps its key range of A
+            from paper_2011_11762_b200.blocks import BlockSet
+
+            _, (ka, ba), _ = G.config_operands_host(cfg)
+            lo, hi = (ka.size * rank) // world, (ka.size * (rank + 1)) // world
+            parts = [BlockSet.from_numpy(ka[lo:hi], ba[lo:hi], None, dev).compute_meta()] * 2
+        else:
+            for m in (0, 1):
+                keys = G.config_keys(cfg, m)
+                lo, hi = (keys.size * rank) // world, (keys.size * (rank + 1)) // world
+                parts.append(G.device_blocks(geom, keys[lo:hi], cfg.seed, m, G.config_pattern(cfg),
+                                             cfg.half_bw, dev))
         a, b = parts
         comm = D.Comm()
         backend = D.CudaBackend(stream)
@@ -299,14 +307,23 @@ def run_ours(args):
         def step(stats=None, events=None):
             if events is not None:
                 events["symbolic"].record(stream)
-            c, ds = D.multiply(comm, layout, a, b, backend=backend)
+            c, ds = D.multiply(comm, layout, a, b, backend=backend, b_is_a=b_is_a)
             if events is not None:
                 events["numeric"].record(stream)
                 events["end"].record(stream)
             if stats is not None:
                 stats.n_triples = ds.n_triples_global
-                stats.flops = 2 * geom.bs ** 3 * ds.n_triples_global
                 stats.n_c = ds.n_c_global
+                # executed flops: 2*bs^2 per executed k row summed over the ranks (as on one GPU,
+                # where k panels skipped by the support masks are not counted)
+                kr = torch.tensor([float(ds.k_rows)], dtype=torch.float64, device=cdev)
+                dist.all_reduce(kr, op=dist.ReduceOp.MIN)
+                if kr.item() >= 0:
+                    kr = torch.tensor([float(ds.k_rows)], dtype=torch.float64, device=cdev)
+                    dist.all_reduce(kr)
+                    stats.flops = 2 * geom.bs ** 2 * int(kr.item())
+                else:
+                    stats.flops = 2 * geom.bs ** 3 * ds.n_triples_global
                 dist_stats["last"] = ds
             return c
 

@@ -180,10 +180,14 @@ class CudaBackend:
     def numeric_peer(self, layout, tri, c_tptr, c_keys, rank, a_off, b_off, a_bases, b_bases, a_local,
                      b_local, b_is_a, masks, staged=True, info=None):
         """staged_numeric on this rank's GPU, then the exact-zero drop."""
+        from . import _ffi
+
         stream = self.stream if self.stream is not None else torch.cuda.current_stream(c_keys.device)
         c, nz, zc = staged_numeric(layout, tri, c_tptr, c_keys, rank, a_off, b_off, a_bases, b_bases,
                                    a_local, b_local, b_is_a, masks, stream, staged=staged, info=info)
-        n_zero = spgemm._sync_item(zc, stream)
+        n_zero, k_rows = _ffi.read_i64s(zc, 2, stream)
+        if info is not None:
+            info["k_rows"] = k_rows  # k depth executed (panels skipped by the support masks excluded)
         return spgemm.compact(layout.block_size, c, nz, n_zero, self.stream)
 
     def symbolic_state(self, layout, a_keys: torch.Tensor, b_keys: torch.Tensor, a_cmask=None, b_rmask=None,
@@ -207,10 +211,12 @@ class CudaBackend:
 
     def numeric(self, layout, pool_a: BlockSet, pool_b: BlockSet, tri: torch.Tensor,
                 c_tptr: torch.Tensor, c_keys: torch.Tensor) -> BlockSet:
+        from . import _ffi
+
         plan = spgemm.SymbolicPlan(int(c_keys.shape[0]), int(tri.shape[0] // 2), c_keys, c_tptr, tri)
         c, nz, zc = spgemm.numeric(layout, pool_a, pool_b, plan, self.stream)
         stream = self.stream if self.stream is not None else torch.cuda.current_stream(c_keys.device)
-        n_zero = spgemm._sync_item(zc, stream)
+        n_zero, self.last_k_rows = _ffi.read_i64s(zc, 2, stream)
         return spgemm.compact(layout.block_size, c, nz, n_zero, self.stream)
 
 
@@ -230,6 +236,7 @@ class DistStats:
     mode: str = "exchange"
     phase_s: dict = field(default_factory=dict)
     extra: dict = field(default_factory=dict)
+    k_rows: int = -1          # k depth this rank executed (2*bs^2 flops each); -1 = not counted
 
 
 MAX_TILE_LEVELS = 8  # csrc/qm_symbolic.cu kMaxTileLevels
@@ -673,6 +680,7 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
             stats.phase_s = {"structure": t1 - t0, "symbolic": t2 - t1, "exchange": 0.0,
                              "numeric": t4 - t2}
             stats.extra = {k: v for k, v in info.items() if not k.startswith("_")}
+            stats.k_rows = int(info.get("k_rows", -1)) if hi > lo else 0
             return c, stats
     need_a = torch.unique(tri[:, 0]) if hi > lo else tri.new_zeros(0)
     need_b = torch.unique(tri[:, 1]) if hi > lo else tri.new_zeros(0)
@@ -684,6 +692,7 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     stats.bytes_received, stats.bytes_sent, stats.blocks_received = ra + rb, sa + sb, na + nb
     t3 = clock()
     if hi == lo:
+        stats.k_rows = 0
         return empty, stats
     la = torch.searchsorted(need_a, tri[:, 0].contiguous())
     lb = torch.searchsorted(need_b, tri[:, 1].contiguous())
@@ -701,6 +710,7 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
         pb = BlockSet(pk_b, pool_b, dummy_a, masks_full=(True, True))
         pa.masks = pb.masks = torch.empty((3, 0), dtype=torch.int64, device=dev)
     c = backend.numeric(layout, pa, pb, tri_local, c_tptr, c_keys)
+    stats.k_rows = int(getattr(backend, "last_k_rows", -1))
     t4 = clock()
     stats.n_c_local = c.n
     stats.mode = "exchange"

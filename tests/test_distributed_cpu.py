@@ -231,3 +231,44 @@ def test_weak_scaling_locality(tmp_path):
     assert means[2] > 0
     for low, high in ((2, 4), (4, 8)):
         assert means[high] / means[low] <= 1.5, (low, high, means)
+
+
+def test_tile_partition_with_masks_weighs_executed_panels():
+    """The masked host twin (k_tile_work's weights): every block pair adds the number of 16-row k
+    panels where A's column mask and B's row mask meet (0: an exactly-zero product) to its C tile;
+    checked against a pair-by-pair loop on a small random structure, and the cut is monotone."""
+    from paper_2011_11762_b200.layout import Geometry, MatrixParams
+
+    rng = np.random.default_rng(11)
+    n, bs, leaf = 2048, 64, 64
+    geom = Geometry(MatrixParams.create(n, leaf), bs)
+    nb = geom.nbg
+    pa = np.unique(rng.integers(0, nb, (300, 2)), axis=0)
+    pb = np.unique(rng.integers(0, nb, (300, 2)), axis=0)
+    ka = np.sort(geom.qkey(pa[:, 0], pa[:, 1]))
+    kb = np.sort(geom.qkey(pb[:, 0], pb[:, 1]))
+    am = rng.integers(0, 2**63, ka.size, dtype=np.int64) & rng.integers(0, 2**63, ka.size, dtype=np.int64)
+    bm = rng.integers(0, 2**63, kb.size, dtype=np.int64) & rng.integers(0, 2**63, kb.size, dtype=np.int64)
+    world = 4
+    bounds = D.tile_partition(geom, ka, kb, world, am, bm)
+    assert bounds[0] == 0 and all(x <= y for x, y in zip(bounds, bounds[1:]))
+    depth = geom.params.depth
+    tl = min(depth, D.MAX_TILE_LEVELS)
+    kshift = 2 * (depth - tl) + 2 * geom.lbits
+    ai, ak = geom.decode(ka)
+    bk, bj = geom.decode(kb)
+    work = {}
+    for x in range(ka.size):
+        for y in np.nonzero(bk == ak[x])[0]:
+            m = int(am[x]) & int(bm[y])
+            w = sum(((m >> s) & 0xFFFF) != 0 for s in (0, 16, 32, 48))
+            t = int(geom.qkey(np.array([ai[x]]), np.array([bj[y]]))[0]) >> kshift
+            work[t] = work.get(t, 0) + w
+    tiles = np.zeros(1 << (2 * tl), dtype=np.int64)
+    for t, w in work.items():
+        tiles[t] = w
+    prefix = np.concatenate([[0], np.cumsum(tiles)])
+    W = int(prefix[-1])
+    cuts = [0] + [int(np.searchsorted(prefix[:tiles.size], (W * r) // world, side="left")) for r in range(1, world)]
+    cuts.append(tiles.size)
+    assert bounds == [c << kshift for c in cuts]
