@@ -320,7 +320,6 @@ __global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
 #pragma unroll
     for (int h = 0; h < 2; ++h) boff[j][h] = kk * 128 + ((((h * 4) + (g >> 1)) ^ (kk & 7)) << 4) + (g & 1) * 8;
   }
-  const uint64_t c_policy = l2_evict_first_policy();
   double acc[R][2][2][2][2];  // [row][column of the pair][i][n][2]
 #pragma unroll
   for (int r = 0; r < R; ++r)
@@ -332,23 +331,27 @@ __global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
         for (int n = 0; n < 2; ++n) acc[r][q][i][n][0] = acc[r][q][i][n][1] = 0.0;
   int s = 0;
   uint32_t phase = 0;
-  int64_t cur_unit = -1, c_first = 0;
+  int32_t cur_unit = -1, c_first = 0;  // (32-bit: fewer live registers across the stage loop)
   uint32_t gm = 0;
   while (true) {
     mbar_wait(&full[s], phase);
     const int64_t mt = meta[s];
     if (mt < 0) break;
-    if ((mt >> 1) != cur_unit) {  // a group's first stage: fetch its epilogue metadata now, so the
-      cur_unit = mt >> 1;         // loads complete under the group's DMMAs
+    if ((int32_t)(mt >> 1) != cur_unit) {  // a group's first stage: fetch its epilogue metadata now,
+      cur_unit = (int32_t)(mt >> 1);       // so the loads complete under the group's DMMAs
       gm = gmask[cur_unit];
-      c_first = gfirst[cur_unit];
+      c_first = (int32_t)gfirst[cur_unit];
     }
     const uint32_t pm = pmask[s];
     const uint32_t onb = (pm >> (2 * warp)) & 3u;
     const uint32_t ona = (pm >> kG) & ((1u << R) - 1u);
     uint64_t dep = 0;
-    if (onb == 3u && ona == (1u << R) - 1u)  // every product of the warp present: no guards
+    if (onb == 3u && ona == (1u << R) - 1u) {  // every product of the warp present: no guards
       dep = group_stage<R, true>(smem + (size_t)s * Cfg::STAGE_BYTES, warp, ona, onb, aoff, boff, acc);
+#ifdef QM_EXP_G16_REPEAT  // experiment (wrong results): twice the DMMAs per stage, same stage overhead
+      dep |= group_stage<R, true>(smem + (size_t)s * Cfg::STAGE_BYTES, warp, ona, onb, aoff, boff, acc);
+#endif
+    }
     else if (onb)
       dep = group_stage<R, false>(smem + (size_t)s * Cfg::STAGE_BYTES, warp, ona, onb, aoff, boff, acc);
     // release once this warp's fragments are in registers (see k_numeric_tma)
@@ -360,13 +363,14 @@ __global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
       phase ^= 1u;
     }
     if (mt & 1) {
+      const uint64_t c_policy = l2_evict_first_policy();  // (created here: one register less in the loop)
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int mb = r * kG + 2 * warp + q;
           if ((gm >> mb) & 1u) {
-            const int64_t c = c_first + __popc(gm & ((1u << mb) - 1u));
+            const int64_t c = (int64_t)c_first + __popc(gm & ((1u << mb) - 1u));
             double *cb = C + (size_t)c * (kBlk * kBlk);
             double ss0 = 0.0, ss1 = 0.0;
             bool nz = false;
@@ -509,7 +513,7 @@ int launch_numeric_group16(const Geometry &g, const double *A, int64_t nA, const
                            const uint64_t *a_keys, const uint32_t *tri, const int64_t *c_tptr,
                            const uint64_t *c_keys, int64_t nC, int64_t nT, double *C, double *csq,
                            uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes, cudaStream_t st) {
-  if (g.bs != kBlk || g.nbl < 2 || !a_keys || !c_keys) return QM_ERR_UNSUPPORTED;
+  if (g.bs != kBlk || g.nbl < 2 || !a_keys || !c_keys || nC >= ((int64_t)1 << 31)) return QM_ERR_UNSUPPORTED;
   Carver cv(ws, ws_bytes);
   GroupWs w = carve_group(cv, nC, nT);
   if (!cv.ok() || !ws) {
