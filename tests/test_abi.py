@@ -67,3 +67,35 @@ def test_workspace_and_argument_errors_before_any_device_work():
     too_deep = _ffi.QmLayout(1 << 40, 1, 40, 1, 0)
     assert lib.qm_spgemm_workspace_bytes(ctypes.byref(too_deep), 1, 1) == 0
     assert lib.qm_encode_keys(ctypes.byref(too_deep), None, None, 1, None, None) == _ffi.QM_ERR_UNSUPPORTED
+
+
+def test_multi_gpu_and_row_index_entry_points_reject_bad_arguments():
+    """Caller mistakes on the staged multi-GPU and row-index entry points return status codes
+    before any device work (no GPU needed)."""
+    lib = _ffi.load()
+    lay = _ffi.make_layout(MatrixParams.create(4096, 64), 64)
+    counts = (ctypes.c_int64 * 3)()
+    # ownership range outside the operand
+    rc = lib.qm_stage_plan(None, 0, None, 0, 5, 3, 10, 0, 0, 10, 0, None, 0, None, None, None, None, counts, None)
+    assert rc == _ffi.QM_ERR_INVALID and b"qm_stage_plan" in lib.qm_last_error()
+    # b_is_a with different operand sizes
+    rc = lib.qm_stage_plan(None, 0, None, 0, 0, 1, 10, 0, 1, 11, 1, None, 0, None, None, None, None, counts, None)
+    assert rc == _ffi.QM_ERR_INVALID
+    assert lib.qm_stage_plan_workspace_bytes(100, 100, 10, 0) > lib.qm_stage_plan_workspace_bytes(100, 100, 10, 1)
+    # one operand's masks without the other's
+    ia = _ffi.QmRowIndex(0, 0, 0, 0, 8)
+    ib = _ffi.QmRowIndex(0, 0, 0, 0, 0)
+    nc, nt = ctypes.c_int64(-1), ctypes.c_int64(-1)
+    rc = lib.qm_spgemm_count_ix(ctypes.byref(lay), ctypes.byref(ia), 1, ctypes.byref(ib), 1, 0, 0, 0, None, 0,
+                                ctypes.byref(nc), ctypes.byref(nt), None, None, None)
+    assert rc == _ffi.QM_ERR_INVALID and b"masks" in lib.qm_last_error()
+    # a halo with more ranks than the ABI carries
+    h = _ffi.QmHalo()
+    h.world = 9
+    h.count[0] = 1
+    one = (ctypes.c_void_p * 1)(8)
+    n1 = (ctypes.c_int64 * 1)(1)
+    rc = lib.qm_numeric_pools_ex(ctypes.byref(lay), one, n1, 1, one, n1, 1, None, None, None, None, None, None, None,
+                                 ctypes.byref(h), 0, None, 1, 1, None, None, None, None, None, None, 0, None)
+    assert rc == _ffi.QM_ERR_INVALID and b"halo" in lib.qm_last_error()
+    assert lib.qm_row_index_workspace_bytes(ctypes.byref(lay), 1000) > 0
