@@ -74,22 +74,6 @@ class Comm:
         self.dist.all_gather(outs, pad, group=self.group)
         return self._out(torch.cat([o[:c] for o, c in zip(outs, counts)]), dev), counts
 
-    def allgather_varlen_many(self, ts: list) -> tuple[list, list]:
-        """allgather_varlen of several 1-D tensors with ONE size exchange (one host sync): returns
-        the per-tensor concatenations and the per-tensor rank counts."""
-        dev = ts[0].device
-        n = torch.tensor([int(t.shape[0]) for t in ts], dtype=torch.int64,
-                         device="cpu" if self.stage else dev)
-        ns = [torch.zeros_like(n) for _ in range(self.world)]
-        self.dist.all_gather(ns, n, group=self.group)
-        allc = torch.stack(ns).cpu().tolist()  # [world][len(ts)]
-        outs, counts = [], []
-        for i, t in enumerate(ts):
-            c = [int(allc[r][i]) for r in range(self.world)]
-            outs.append(self.gather_known(t, c))
-            counts.append(c)
-        return outs, counts
-
     def gather_known(self, t: torch.Tensor, counts: list) -> torch.Tensor:
         """Concatenation over ranks of 1-D tensors whose lengths `counts` every rank already knows."""
         dev = t.device
@@ -148,9 +132,6 @@ class LocalComm:
 
     def allgather_varlen(self, t):
         return t, [int(t.shape[0])]
-
-    def allgather_varlen_many(self, ts):
-        return list(ts), [[int(t.shape[0])] for t in ts]
 
     def gather_known(self, t, counts):
         return t
@@ -578,32 +559,37 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     # filter is needed unless ALL of A's blocks have full column supports or ALL of B's full row
     # supports: one max-reduction of the two "not full" flags over the ranks.
     bl = a_local if b_is_a else b_local
-    use_masks = False
-    if spgemm.support_filter_enabled() and a_local.blocks.is_cuda:
+    # One fixed-size header per rank (block counts; whether its blocks have partial supports) is the
+    # only host-synchronising collective before the symbolic phase; the payloads (keys, masks) are
+    # then gathered with known sizes. Support masks are gathered when the filter matters: unless
+    # ALL of A's blocks have full column supports or ALL of B's full row supports.
+    masks_on = spgemm.support_filter_enabled() and a_local.blocks.is_cuda
+    if masks_on:
         a_local.support_masks()
         if not b_is_a:
             b_local.support_masks()
-        a_part, b_part = comm.allreduce_max_vec([0.0 if a_local.masks_full[1] else 1.0,
-                                                 0.0 if bl.masks_full[0] else 1.0], dev)
-        use_masks = a_part > 0.0 and b_part > 0.0
-    # structure (+ masks): one size exchange, then the payload gathers
-    send = [a_local.keys] if b_is_a else [a_local.keys, b_local.keys]
-    if use_masks:
-        send += [a_local.masks[1].contiguous(), bl.masks[0].contiguous(), a_local.masks[2].contiguous()]
-        if not b_is_a:
-            send.append(bl.masks[2].contiguous())
-    got, counts = comm.allgather_varlen_many(send)
-    ka, a_counts = got[0], counts[0]
-    kb, b_counts = (ka, a_counts) if b_is_a else (got[1], counts[1])
+    hdr = torch.tensor([a_local.n, b_local.n, int(masks_on and not a_local.masks_full[1]),
+                        int(masks_on and not bl.masks_full[0])], dtype=torch.int64,
+                       device="cpu" if getattr(comm, "stage", True) else dev)
+    allh = comm.allgather_fixed(hdr).reshape(-1, 4).cpu().tolist()
+    a_counts = [int(r[0]) for r in allh]
+    b_counts = a_counts if b_is_a else [int(r[1]) for r in allh]
+    use_masks = any(r[2] for r in allh) and any(r[3] for r in allh)
+    ka = comm.gather_known(a_local.keys, a_counts)
+    kb = ka if b_is_a else comm.gather_known(b_local.keys, b_counts)
     ma = mb = fa = fb = None
     if use_masks:
-        o = 1 if b_is_a else 2
-        ma, mb, fa = got[o], got[o + 1], got[o + 2]
-        fb = fa if b_is_a else got[o + 3]
-    if ka.shape[0] > 1 and bool((ka[1:] <= ka[:-1]).any()):
-        raise ContractViolationError("distributed operands must own ascending, disjoint key ranges")
-    if kb.shape[0] > 1 and bool((kb[1:] <= kb[:-1]).any()):
-        raise ContractViolationError("distributed operands must own ascending, disjoint key ranges")
+        ma = comm.gather_known(a_local.masks[1].contiguous(), a_counts)
+        mb = comm.gather_known(bl.masks[0].contiguous(), b_counts)
+        fa = comm.gather_known(a_local.masks[2].contiguous(), a_counts)
+        fb = fa if b_is_a else comm.gather_known(bl.masks[2].contiguous(), b_counts)
+    # ownership contract (ascending, disjoint key ranges): checked on the device, read after the
+    # symbolic phase's own synchronisation
+    bad = torch.zeros((), dtype=torch.bool, device=ka.device)
+    if ka.shape[0] > 1:
+        bad |= (ka[1:] <= ka[:-1]).any()
+    if kb.shape[0] > 1 and not b_is_a:
+        bad |= (kb[1:] <= kb[:-1]).any()
     a_off = [0] + list(np.cumsum(a_counts).tolist())
     b_off = [0] + list(np.cumsum(b_counts).tolist())
     if ka.shape[0] == 0 or kb.shape[0] == 0:
@@ -614,14 +600,20 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     # rank counts and emits only the C blocks of its own range (the reference's workers likewise
     # expand only the tasks they execute, ops.py:197-241 / engine.py:286-300).
     st = backend.symbolic_state(layout, ka, kb, a_cmask=ma, b_rmask=mb, part=(comm.world, comm.rank))
+    if bool(bad.item()):
+        raise ContractViolationError("distributed operands must own ascending, disjoint key ranges")
     stats.c_range, stats.tile_work = st.key_range, st.tile_work
     stats.n_c_local, stats.t_range = st.n_c, (0, st.n_t)
-    tot = comm.allgather_fixed(torch.tensor([st.n_c, st.n_t], dtype=torch.int64,
-                                            device="cpu" if getattr(comm, "stage", True) else dev))
-    tot = tot.reshape(-1, 2).sum(dim=0).tolist()
-    stats.n_c_global, stats.n_triples_global = int(tot[0]), int(tot[1])
-    if stats.n_c_global == 0:
-        return empty, stats
+
+    def finish(c):
+        """Global totals of the product, gathered once at the end -- the collective is also the
+        barrier after which no rank reads another's pools."""
+        tot = comm.allgather_fixed(torch.tensor([st.n_c, st.n_t], dtype=torch.int64,
+                                                device="cpu" if getattr(comm, "stage", True) else dev))
+        tot = tot.reshape(-1, 2).sum(dim=0).tolist()
+        stats.n_c_global, stats.n_triples_global = int(tot[0]), int(tot[1])
+        return c, stats
+
     lo, hi = 0, st.n_t
     if st.n_c:  # (a rank with an empty range still takes part in every collective below)
         c_keys, c_tptr = st.keys()
@@ -646,12 +638,13 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
         # 1 = staged (copy engines pull the halo once while local-only C blocks compute);
         # every rank must take the same path (the peer mappings are collective)
         want = 0.0 if mode == "fused" else 1.0 if mode == "staged" else (0.0 if fused_s <= 0.25 * compute_s else 1.0)
-        want = comm.allreduce_max_vec([want], dev)[0]
         if dev.type == "cuda":
-            torch.cuda.synchronize(dev)  # this rank's pools are written (any stream) ...
-        comm.barrier()  # ... on every rank, before anyone reads them
+            torch.cuda.synchronize(dev)  # this rank's pools are written (any stream) before it
+        # exports them; the records' all-gather inside PeerPools completes only once every rank has
+        # done the same, so it is also the barrier before anyone reads a peer's pool
         pools = PeerPools(comm, [a_local.blocks] if b_is_a else [a_local.blocks, b_local.blocks])
-        if comm.allreduce_max(0.0 if pools.ok else 1.0, dev) > 0.0:
+        want, not_ok = comm.allreduce_max_vec([want, 0.0 if pools.ok else 1.0], dev)
+        if not_ok > 0.0:
             # some rank cannot map its peers' pools: every rank takes the exchange path
             if not pools.ok:
                 warnings.warn(f"rank {comm.rank}: peer pools unavailable ({pools.error}); "
@@ -670,7 +663,6 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
                 torch.cuda.synchronize(dev)
             finally:
                 pools.close()
-            comm.barrier()  # every rank has finished reading the others' pools
             t4 = clock()
             stats.n_c_local = c.n
             stats.mode = "staged" if want > 0.0 else "fused"
@@ -681,7 +673,7 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
                              "numeric": t4 - t2}
             stats.extra = {k: v for k, v in info.items() if not k.startswith("_")}
             stats.k_rows = int(info.get("k_rows", -1)) if hi > lo else 0
-            return c, stats
+            return finish(c)  # (its collective: every rank has finished reading the others' pools)
     need_a = torch.unique(tri[:, 0]) if hi > lo else tri.new_zeros(0)
     need_b = torch.unique(tri[:, 1]) if hi > lo else tri.new_zeros(0)
     pool_a, ra, sa, na = _fetch(comm, backend, a_local.blocks, a_off, need_a)
@@ -693,7 +685,7 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     t3 = clock()
     if hi == lo:
         stats.k_rows = 0
-        return empty, stats
+        return finish(empty)
     la = torch.searchsorted(need_a, tri[:, 0].contiguous())
     lb = torch.searchsorted(need_b, tri[:, 1].contiguous())
     tri_local = torch.stack([la, lb], dim=1).to(torch.int32).reshape(-1).contiguous()
@@ -715,7 +707,7 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     stats.n_c_local = c.n
     stats.mode = "exchange"
     stats.phase_s = {"structure": t1 - t0, "symbolic": t2 - t1, "exchange": t3 - t2, "numeric": t4 - t3}
-    return c, stats
+    return finish(c)
 
 
 def owned_range(keys_sorted: np.ndarray, bounds: list[int], rank: int) -> np.ndarray:
