@@ -86,8 +86,15 @@ def _in_process_peers(t: torch.Tensor, off: list) -> list:
     return [t.data_ptr() + off[r] * blk for r in range(len(off) - 1)]
 
 
+EXTRA = {  # the staged path at the other TMA block sizes (bs 128: 4 work units per C block)
+    "banded-bs32": G.BaselineConfig("t32", "banded", 8192, 32, half_bw=256),
+    "banded-bs128": G.BaselineConfig("t128", "banded", 16384, 128, half_bw=512),
+}
+
+
 @pytest.mark.parametrize("name,world,staged", [("C4", 4, True), ("C4", 8, True), ("C2-16384", 3, True),
-                                               ("C3", 2, True), ("C4", 4, False)])
+                                               ("C3", 2, True), ("C4", 4, False), ("banded-bs32", 3, True),
+                                               ("banded-bs128", 3, True), ("banded-bs128", 2, False)])
 def test_staged_and_fused_rank_numeric_equal_single_gpu(dev, name, world, staged):
     """staged_numeric for every rank, the operands' other ranks being slices of the same pools:
     staged (halo gathered by k_halo_gather while the numeric kernel -- its programmatic dependent --
@@ -95,7 +102,7 @@ def test_staged_and_fused_rank_numeric_equal_single_gpu(dev, name, world, staged
     pools) give each rank's C blocks bitwise as the single-GPU product; the halo holds each remote
     block once (halo_bytes = unique remote blocks). Also with an emulated slow link (the gather
     lasts >= halo bytes / 20 GB/s), so the gated claims really wait."""
-    cfg = G.CONFIGS[name]
+    cfg = EXTRA[name] if name in EXTRA else G.CONFIGS[name]
     geom, a, b = G.config_operands_device(cfg, dev)
     b_is_a = cfg.same_operand
     if b_is_a:
