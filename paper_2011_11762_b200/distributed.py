@@ -523,6 +523,11 @@ def _fetch(comm, backend, local_blocks: torch.Tensor, offsets: list[int], need: 
 
 
 NVLINK_GBS = 770.0   # measured peer copy bandwidth per direction (B200_PROFILING.md)
+# auto mode: the fused kernel reads every remote block *reference* over NVLink; it is chosen only
+# when those reads are a small share of the compute (banded: < 1 %), else the staged halo (each
+# remote block once, overlapped with the local-only blocks; decay at P = 2 moves 98 MB instead of
+# 555 MB of references)
+FUSED_MAX_SHARE = 0.05
 FP64_TFLOPS = 35.0   # sustained numeric-kernel rate used by the mode heuristic
 
 
@@ -541,7 +546,7 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
                      (staged_numeric). No collective for the halo.
     mode None:       $QM_DIST_MODE, default "auto".
     mode "auto":     fused when its estimated NVLink time (every remote block reference is a
-                     remote read: peer loads bypass the local L2) stays under a quarter of the
+                     remote read: peer loads bypass the local L2) stays under 5 % of the
                      estimated compute time, else staged (heavy reuse of remote blocks: decay,
                      random patterns); the exchange when some rank cannot map its peers."""
     backend = backend or CudaBackend()
@@ -637,7 +642,8 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
         # 0 = fused (the kernel's TMA reads remote blocks in place: few remote references),
         # 1 = staged (copy engines pull the halo once while local-only C blocks compute);
         # every rank must take the same path (the peer mappings are collective)
-        want = 0.0 if mode == "fused" else 1.0 if mode == "staged" else (0.0 if fused_s <= 0.25 * compute_s else 1.0)
+        want = (0.0 if mode == "fused" else 1.0 if mode == "staged"
+                else (0.0 if fused_s <= FUSED_MAX_SHARE * compute_s else 1.0))
         if dev.type == "cuda":
             torch.cuda.synchronize(dev)  # this rank's pools are written (any stream) before it
         # exports them; the records' all-gather inside PeerPools completes only once every rank has
