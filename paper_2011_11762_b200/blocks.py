@@ -28,6 +28,9 @@ import torch
 from .errors import ContractViolationError, StoreCapacityError
 
 
+_SERIALS = itertools.count(1)
+
+
 @dataclass
 class BlockSet:
     keys: torch.Tensor
@@ -109,6 +112,15 @@ class BlockSet:
         mask = None if role is None else ix["cmask"] if role == "a" else ix["rmask"]
         return _ffi.QmRowIndex(_ffi.ptr(ix["rowptr"]), _ffi.ptr(ix["row"]), _ffi.ptr(ix["col"]), _ffi.ptr(ix["perm"]),
                                _ffi.ptr(mask))
+
+    @property
+    def serial(self) -> int:
+        """A process-unique id of this (immutable) block set: tags metadata derived from it and
+        its peers' sets in a multi-GPU product (distributed.multiply's structure cache)."""
+        sid = self.__dict__.get("_serial")
+        if sid is None:
+            sid = self.__dict__["_serial"] = next(_SERIALS)
+        return sid
 
     @property
     def n(self) -> int:

@@ -172,9 +172,32 @@ class CudaBackend:
         return spgemm.compact(layout.block_size, c, nz, n_zero, self.stream)
 
     def symbolic_state(self, layout, a_keys: torch.Tensor, b_keys: torch.Tensor, a_cmask=None, b_rmask=None,
-                       part=None):
+                       part=None, ix=None):
         return spgemm.SymbolicState(layout, a_keys, int(a_keys.shape[0]), b_keys, int(b_keys.shape[0]),
-                                    self.stream, a_cmask, b_rmask, part=part)
+                                    self.stream, a_cmask, b_rmask, part=part, ix=ix)
+
+    def row_indexes(self, layout, ka, kb, ma, mb, fa, fb, b_is_a):
+        """Row indexes of the gathered global structure (qm_row_index_build on structure-only block
+        sets): ((qm_row_index of A, of B), the tensors they point into)."""
+        bs = layout.block_size
+        dev = ka.device
+
+        def structure(keys, rows, cols, flags):
+            n = int(keys.shape[0])
+            s = BlockSet(keys, torch.empty((0, bs, bs), dtype=torch.float64, device=dev),
+                         torch.empty(0, dtype=torch.float64, device=dev))
+            if cols is not None or rows is not None:
+                ones = torch.full((n,), -1, dtype=torch.int64, device=dev)
+                s.masks = torch.stack([rows if rows is not None else ones, cols if cols is not None else ones,
+                                       flags if flags is not None else torch.zeros_like(ones)]).contiguous()
+            return s
+
+        masked = ma is not None
+        sa = structure(ka, mb if b_is_a else None, ma, fa)
+        sb = sa if b_is_a else structure(kb, mb, None, fb)
+        ia, ib = sa.row_index(layout, self.stream), sb.row_index(layout, self.stream)
+        structs = (BlockSet.ix_struct(ia, "a" if masked else None), BlockSet.ix_struct(ib, "b" if masked else None))
+        return structs, (ia, ib)
 
     def gather_blocks(self, blocks: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
         import ctypes  # noqa: F401
@@ -573,28 +596,45 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
         a_local.support_masks()
         if not b_is_a:
             b_local.support_masks()
+    # (the last two header fields are the operands' serials: the gathered global structure and its
+    # row indexes are metadata of the distributed operands, kept with the local block set and
+    # reused while every rank multiplies the same sets)
+    # Every rank also reports which structure it has cached, so all ranks agree on reusing it (no
+    # rank skips a gather the others perform).
+    cached = a_local.__dict__.get("_dist_struct")
+    mine = cached[1] if cached is not None and cached[0] == id(getattr(comm, "group", None)) else 0
     hdr = torch.tensor([a_local.n, b_local.n, int(masks_on and not a_local.masks_full[1]),
-                        int(masks_on and not bl.masks_full[0])], dtype=torch.int64,
-                       device="cpu" if getattr(comm, "stage", True) else dev)
-    allh = comm.allgather_fixed(hdr).reshape(-1, 4).cpu().tolist()
+                        int(masks_on and not bl.masks_full[0]), a_local.serial, bl.serial, mine],
+                       dtype=torch.int64, device="cpu" if getattr(comm, "stage", True) else dev)
+    allh = comm.allgather_fixed(hdr).reshape(-1, 7).cpu().tolist()
     a_counts = [int(r[0]) for r in allh]
     b_counts = a_counts if b_is_a else [int(r[1]) for r in allh]
     use_masks = any(r[2] for r in allh) and any(r[3] for r in allh)
-    ka = comm.gather_known(a_local.keys, a_counts)
-    kb = ka if b_is_a else comm.gather_known(b_local.keys, b_counts)
-    ma = mb = fa = fb = None
-    if use_masks:
-        ma = comm.gather_known(a_local.masks[1].contiguous(), a_counts)
-        mb = comm.gather_known(bl.masks[0].contiguous(), b_counts)
-        fa = comm.gather_known(a_local.masks[2].contiguous(), a_counts)
-        fb = fa if b_is_a else comm.gather_known(bl.masks[2].contiguous(), b_counts)
-    # ownership contract (ascending, disjoint key ranges): checked on the device, read after the
-    # symbolic phase's own synchronisation
-    bad = torch.zeros((), dtype=torch.bool, device=ka.device)
-    if ka.shape[0] > 1:
-        bad |= (ka[1:] <= ka[:-1]).any()
-    if kb.shape[0] > 1 and not b_is_a:
-        bad |= (kb[1:] <= kb[:-1]).any()
+    skey = hash((comm.world, b_is_a, use_masks, tuple((int(r[4]), int(r[5])) for r in allh),
+                 int(layout.n_logical), int(layout.leaf_dim), int(layout.depth), int(layout.block_size))) or 1
+    hit = cached[2] if cached is not None and all(int(r[6]) == skey for r in allh) else None
+    ix = None
+    if hit is not None:
+        ka, kb, ma, mb, fa, fb, ix = hit
+        bad = torch.zeros((), dtype=torch.bool, device=ka.device)
+    else:
+        ka = comm.gather_known(a_local.keys, a_counts)
+        kb = ka if b_is_a else comm.gather_known(b_local.keys, b_counts)
+        ma = mb = fa = fb = None
+        if use_masks:
+            ma = comm.gather_known(a_local.masks[1].contiguous(), a_counts)
+            mb = comm.gather_known(bl.masks[0].contiguous(), b_counts)
+            fa = comm.gather_known(a_local.masks[2].contiguous(), a_counts)
+            fb = fa if b_is_a else comm.gather_known(bl.masks[2].contiguous(), b_counts)
+        # ownership contract (ascending, disjoint key ranges): checked on the device, read after the
+        # symbolic phase's own synchronisation
+        bad = torch.zeros((), dtype=torch.bool, device=ka.device)
+        if ka.shape[0] > 1:
+            bad |= (ka[1:] <= ka[:-1]).any()
+        if kb.shape[0] > 1 and not b_is_a:
+            bad |= (kb[1:] <= kb[:-1]).any()
+        if getattr(backend, "row_indexes", None) is not None and ka.is_cuda and ka.shape[0] and kb.shape[0]:
+            ix = backend.row_indexes(layout, ka, kb, ma, mb, fa, fb, b_is_a)
     a_off = [0] + list(np.cumsum(a_counts).tolist())
     b_off = [0] + list(np.cumsum(b_counts).tolist())
     if ka.shape[0] == 0 or kb.shape[0] == 0:
@@ -604,9 +644,16 @@ def multiply(comm, layout, a_local: BlockSet, b_local: BlockSet, backend=None, b
     # (quadtree subtrees), cuts them into `world` contiguous key ranges of equal work, and this
     # rank counts and emits only the C blocks of its own range (the reference's workers likewise
     # expand only the tasks they execute, ops.py:197-241 / engine.py:286-300).
-    st = backend.symbolic_state(layout, ka, kb, a_cmask=ma, b_rmask=mb, part=(comm.world, comm.rank))
-    if bool(bad.item()):
-        raise ContractViolationError("distributed operands must own ascending, disjoint key ranges")
+    if ix is not None:
+        st = backend.symbolic_state(layout, ka, kb, a_cmask=ma, b_rmask=mb, part=(comm.world, comm.rank),
+                                    ix=ix[0])
+    else:
+        st = backend.symbolic_state(layout, ka, kb, a_cmask=ma, b_rmask=mb, part=(comm.world, comm.rank))
+    if hit is None:
+        if bool(bad.item()):
+            raise ContractViolationError("distributed operands must own ascending, disjoint key ranges")
+        # (one structure per local operand: the latest product's)
+        a_local.__dict__["_dist_struct"] = (id(getattr(comm, "group", None)), skey, (ka, kb, ma, mb, fa, fb, ix))
     stats.c_range, stats.tile_work = st.key_range, st.tile_work
     stats.n_c_local, stats.t_range = st.n_c, (0, st.n_t)
 

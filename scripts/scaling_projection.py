@@ -5,8 +5,9 @@ For P ranks the product is partitioned exactly as distributed.multiply does it (
 contiguous C key ranges of equal executed work; A and B owned in equal contiguous key ranges). Each
 rank's whole step is executed on the GPU and timed with one pair of CUDA events (host enqueue and
 synchronisation gaps included, as in the real product):
-  symbolic  the rank's partitioned symbolic phase (tile work + cut, then count / keys / triples of
-            its own C key range only);
+  symbolic  the rank's partitioned symbolic phase over the global structure's row indexes (kept
+            with the distributed operands after their first product): tile work + cut, then count
+            / keys / triples of its own C key range only;
   numeric   distributed.staged_numeric: the rank's C blocks whose triples are all local run first
             while k_halo_gather copies the halo (every block owned by another rank, once); the
             numeric kernel's claims of the other C blocks wait for the gather grid. The "peer" pools
@@ -72,12 +73,16 @@ def project(cfg, world):
     a_off = [(a.n * r) // world for r in range(world + 1)]
     b_off = a_off if b_is_a else [(b.n * r) // world for r in range(world + 1)]
     pa, pb = peers(a.blocks, a_off), peers(b.blocks, b_off)
+    # the global structure's row indexes: metadata of the distributed operands, gathered and built
+    # on the first product and reused while the ranks multiply the same block sets (distributed.py)
+    ixs = D.CudaBackend().row_indexes(lay, a.keys, b.keys, a.masks[1] if use else None, b.masks[0] if use else None,
+                                      a.masks[2] if use else None, b.masks[2] if use else None, b_is_a)
     ranks = []
     for r in range(world):
         info = {}
 
         def step():  # the rank's product: partitioned symbolic, staged numeric, compaction
-            st = spgemm.SymbolicState(lay, a.keys, a.n, b.keys, b.n, None, am, bm, part=(world, r))
+            st = spgemm.SymbolicState(lay, a.keys, a.n, b.keys, b.n, None, am, bm, part=(world, r), ix=ixs[0])
             if st.n_c == 0:
                 return st
             ck, ct = st.keys()
@@ -92,7 +97,7 @@ def project(cfg, world):
         t_rank, st = timed(step)
 
         def sym_only():
-            s2 = spgemm.SymbolicState(lay, a.keys, a.n, b.keys, b.n, None, am, bm, part=(world, r))
+            s2 = spgemm.SymbolicState(lay, a.keys, a.n, b.keys, b.n, None, am, bm, part=(world, r), ix=ixs[0])
             if s2.n_c:
                 k2, t2 = s2.keys()
                 s2.triples(t2)

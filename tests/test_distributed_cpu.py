@@ -272,3 +272,47 @@ def test_tile_partition_with_masks_weighs_executed_panels():
     cuts = [0] + [int(np.searchsorted(prefix[:tiles.size], (W * r) // world, side="left")) for r in range(1, world)]
     cuts.append(tiles.size)
     assert bounds == [c << kshift for c in cuts]
+
+
+def _cache_worker(rank, world, port, outdir):
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    cfg = CASES["banded"]
+    geom, (ka, ba), (kb, bb) = G.config_operands_host(cfg)
+    qa = [(ka.size * r) // world for r in range(world + 1)]
+    qb = [(kb.size * r) // world for r in range(world + 1)]
+    la = BlockSet(torch.from_numpy(ka[qa[rank]:qa[rank + 1]]), torch.from_numpy(ba[qa[rank]:qa[rank + 1]]),
+                  torch.zeros(0))
+
+    def blocks_b():
+        return BlockSet(torch.from_numpy(kb[qb[rank]:qb[rank + 1]]), torch.from_numpy(bb[qb[rank]:qb[rank + 1]]),
+                        torch.zeros(0))
+
+    lb = blocks_b()
+    comm = D.Comm()
+    lay = make_layout(geom.params, geom.bs)
+    outs = []
+    for step in range(3):
+        if step == 2 and rank == 1:
+            lb = blocks_b()  # one rank multiplies a new (equal) block set: every rank must re-gather
+        c, st = D.multiply(comm, lay, la, lb, backend=OracleBackend(geom))
+        keys, _ = comm.allgather_varlen(c.keys)
+        flat, _ = comm.allgather_varlen(c.blocks.reshape(-1))
+        outs.append((keys.numpy(), flat.numpy()))
+    if rank == 0:
+        np.savez(os.path.join(outdir, "out.npz"), k0=outs[0][0], b0=outs[0][1], k1=outs[1][0], b1=outs[1][1],
+                 k2=outs[2][0], b2=outs[2][1])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_structure_cache_is_agreed_by_every_rank(tmp_path):
+    """The gathered global structure is reused only when every rank multiplies the same block sets
+    as last time (serials in the header): a repeated product reuses it, a product where one rank
+    changed its operand re-gathers on all ranks (no rank skips a collective) -- same result each time."""
+    mp.spawn(_cache_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    out = np.load(tmp_path / "out.npz")
+    for i in (1, 2):
+        np.testing.assert_array_equal(out[f"k{i}"], out["k0"])
+        np.testing.assert_array_equal(out[f"b{i}"], out["b0"])
