@@ -13,6 +13,8 @@
 //   4. radix sort of C keys into quadtree-key order, exclusive scan of counts -> c_tptr,
 //   5. k_sym_emit_tri: per row i -> (a_index, b_index) triples at their final positions, k
 //      ascending within each C block (BlockSparseLeaf.multiply's k loop, block_sparse.py:121-129).
+#include <stdlib.h>
+
 #include <cub/cub.cuh>
 
 #include "qm_common.cuh"
@@ -512,6 +514,48 @@ __global__ void k_inv_counts(const uint32_t *perm, const uint32_t *rm_cnt, int64
   cta_exclusive_scan64((const uint64_t *)cnt_q, (uint64_t *)c_tptr, nC + 1, wsum);
 }
 
+// Small products (nC <= kSmallSortMax): the C-key sort, the inverse permutation, the per-block
+// triple counts and their scan into c_tptr in ONE launch of one CTA (a block radix sort in shared
+// memory) instead of the device-wide radix sort's histogram / scan / onesweep passes + memsets +
+// k_inv_counts -- about ten launches, which for ~1-8 K C blocks cost more than the sorting itself.
+// Stable like the device-wide sort (padding keys sort last), so the order is the same.
+constexpr int kSmallSortThreads = 512, kSmallSortItems = 16;
+constexpr int64_t kSmallSortMax = (int64_t)kSmallSortThreads * kSmallSortItems;
+using SmallSort = cub::BlockRadixSort<uint64_t, kSmallSortThreads, kSmallSortItems, uint32_t>;
+
+__global__ void __launch_bounds__(kSmallSortThreads) k_sort_small(const uint64_t *rm_key, const uint32_t *rm_cnt,
+                                                                   int64_t nC, int key_bits, uint64_t *c_keys,
+                                                                   uint32_t *perm, uint32_t *inv, int64_t *cnt_q,
+                                                                   int64_t *c_tptr) {
+  extern __shared__ __align__(16) uint8_t sort_smem[];
+  typename SmallSort::TempStorage &temp = *reinterpret_cast<typename SmallSort::TempStorage *>(sort_smem);
+  __shared__ uint64_t wsum[32];
+  const uint64_t pad = key_bits >= 64 ? ~0ull : ((1ull << key_bits) - 1ull);
+  uint64_t keys[kSmallSortItems];
+  uint32_t vals[kSmallSortItems];
+#pragma unroll
+  for (int q = 0; q < kSmallSortItems; ++q) {
+    const int64_t x = (int64_t)threadIdx.x * kSmallSortItems + q;  // blocked arrangement
+    keys[q] = x < nC ? rm_key[x] : pad;
+    vals[q] = (uint32_t)x;
+  }
+  SmallSort(temp).Sort(keys, vals, 0, key_bits);
+#pragma unroll
+  for (int q = 0; q < kSmallSortItems; ++q) {
+    const int64_t r = (int64_t)threadIdx.x * kSmallSortItems + q;
+    if (r < nC) {
+      c_keys[r] = keys[q];
+      perm[r] = vals[q];
+      inv[vals[q]] = (uint32_t)r;
+      cnt_q[r] = rm_cnt[vals[q]];
+    }
+  }
+  if (threadIdx.x == 0) cnt_q[nC] = 0;
+  __threadfence_block();
+  __syncthreads();
+  cta_exclusive_scan64((const uint64_t *)cnt_q, (uint64_t *)c_tptr, nC + 1, wsum);
+}
+
 // ---- multi-GPU partition of the symbolic phase ------------------------------------------------
 // Work per C tile (aligned square of 2^shift leaves per side, Morton tile code). One warp per A
 // entry (i, k): the lanes read B row k's entries 32 at a time (coalesced), and since the row's
@@ -679,6 +723,12 @@ struct FillWs {
   void *cub;
   size_t cub_bytes;
 };
+
+// QM_SMALL_SORT=0: small products use the device-wide sort too (A/B measurements).
+bool small_sort_enabled() {
+  const char *e = getenv("QM_SMALL_SORT");
+  return !(e && e[0] == '0');
+}
 
 // Products with at most this many C blocks scan c_tptr inside k_inv_counts (one CTA).
 constexpr int64_t kFusedTptrScanMax = 32768;
@@ -1032,6 +1082,19 @@ int fill_keys_core(const Geometry &g, const Ix &a, const Ix &b, int64_t nC, cons
   k_sym_emit_c<<<row_grid(g.nbg), kNT, 0, st>>>(a.rp, a.col, b.rp, b.col, a.mask, b.mask, w.masked, w.rb, g.nbg,
                                                 g.nbl, g.lbits, w.off, f.rm_key, f.rm_cnt, f.rm_iota, f.done);
   QM_LAUNCHED("k_sym_emit_c");
+  if (nC <= kSmallSortMax && small_sort_enabled()) {
+    static PerDeviceOnce once;
+    int rc = once.run([]() -> int {
+      QM_CUDA_TRY(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(typename SmallSort::TempStorage)));
+      return (int)QM_OK;
+    });
+    if (rc != QM_OK) return rc;
+    k_sort_small<<<1, kSmallSortThreads, sizeof(typename SmallSort::TempStorage), st>>>(
+        f.rm_key, f.rm_cnt, nC, key_bits, c_keys, f.perm, f.inv, f.cnt_q, c_tptr);
+    QM_LAUNCHED("k_sort_small");
+    return QM_OK;
+  }
   size_t tb = f.cub_bytes;
   QM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(f.cub, tb, f.rm_key, c_keys, f.rm_iota, f.perm, nC, 0,
                                               key_bits, st));
