@@ -111,7 +111,10 @@ class Comm:
             rc = torch.empty_like(sc)
             self.dist.all_to_all_single(rc, sc, group=self.group)
             recv_counts = [int(x) for x in rc.cpu().tolist()]
-        flat = send.reshape(send.shape[0], -1) if send.dim() > 1 else send.reshape(-1, 1)
+        inner = 1
+        for d in send.shape[1:]:
+            inner *= int(d)
+        flat = send.reshape(send.shape[0], inner)  # explicit width: a rank may send zero rows
         out = torch.empty((sum(recv_counts), flat.shape[1]), dtype=send.dtype, device=dev)
         self.dist.all_to_all_single(out, flat.contiguous(), recv_counts, send_counts, group=self.group)
         return self._out(out.reshape((out.shape[0],) + tuple(send.shape[1:])), dev0), recv_counts

@@ -78,6 +78,10 @@ def _free_port():
 CASES = {
     "banded": G.BaselineConfig("t-band", "banded", 2048, 32, half_bw=100),
     "random": G.BaselineConfig("t-rand", "random", 2048, 32, per_row=4),
+    # edge cases: fewer C tiles than ranks (ragged n = 96 -> 3x3 blocks in a 4x4 grid), and a
+    # sparse random pattern with empty block rows/columns (per_row = 1)
+    "tiny": G.BaselineConfig("t-tiny", "banded", 96, 32, half_bw=20),
+    "sparse": G.BaselineConfig("t-sparse", "random", 512, 32, per_row=1),
 }
 
 
@@ -140,6 +144,20 @@ def test_distributed_product_equals_single_process(tmp_path, world, case):
     assert per_rank_triples.sum() == T == int(out["nt"])
     assert per_rank_triples.max() - per_rank_triples.min() <= 2 * 32  # balanced by triples (+- one C row of work)
     assert out["recv"][:, 0].sum() > 0  # halo blocks crossed ranks
+
+
+@pytest.mark.parametrize("world,case", [(3, "tiny"), (4, "tiny"), (3, "sparse")])
+def test_distributed_edge_cases_equal_single_process(tmp_path, world, case):
+    """Ranks left without C blocks (or without owned blocks) still take part in every collective,
+    and the union of the ranks' products is the single-process product bit for bit."""
+    mp.spawn(_worker, args=(world, _free_port(), case, str(tmp_path)), nprocs=world, join=True)
+    out = np.load(tmp_path / "out.npz")
+    cfg = CASES[case]
+    geom, (ka, ba), (kb, bb) = G.config_operands_host(cfg)
+    kc, bc, T = O.multiply(O.Geom(cfg.n, cfg.bs, cfg.bs), ka, ba, kb, bb)
+    np.testing.assert_array_equal(out["keys"], kc)
+    np.testing.assert_array_equal(out["blocks"].reshape(bc.shape), bc)
+    assert out["recv"][:, 1].sum() == T == int(out["nt"])
 
 
 @pytest.mark.parametrize("mode", ["fused", "staged"])

@@ -52,12 +52,17 @@ def _worker(rank, world, port, cfg_name, outdir, mode="exchange"):
             sl = slice(int(cut[rank]), int(cut[rank + 1]))
             parts.append(BlockSet(full[m].keys[sl].clone(), full[m].blocks[sl].clone(), full[m].sumsq[sl].clone()))
     else:
-        cfg = G.CONFIGS[cfg_name] if cfg_name in G.CONFIGS else G.BaselineConfig("r", "random", 8192, 64, per_row=8)
+        cfg = (G.CONFIGS[cfg_name] if cfg_name in G.CONFIGS else
+               G.BaselineConfig("t", "banded", 96, 32, half_bw=20) if cfg_name == "tiny" else
+               G.BaselineConfig("r", "random", 8192, 64, per_row=8))
         geom = cfg.geometry
         parts = []
         for m in (0, 1):
             keys = G.config_keys(cfg, m)
             cut = np.r_[0, np.sort(np.random.default_rng(m).choice(keys.size, world - 1, replace=False)), keys.size]
+            if cfg_name == "tiny":  # rank 0 owns no block (its pool is empty; peers still map it)
+                cut = np.r_[0, 0, np.sort(np.random.default_rng(m).choice(np.arange(1, keys.size), world - 2,
+                                                                          replace=False)), keys.size]
             parts.append(G.device_blocks(geom, keys[cut[rank]:cut[rank + 1]], cfg.seed, m, G.config_pattern(cfg),
                                          cfg.half_bw, dev))
     layout = _ffi.make_layout(geom.params, geom.bs)
@@ -90,7 +95,7 @@ def _worker(rank, world, port, cfg_name, outdir, mode="exchange"):
 
 
 @pytest.mark.parametrize("mode", ["exchange", "fused", "staged"])
-@pytest.mark.parametrize("world,cfg", [(2, "C1"), (3, "C2-16384"), (2, "random"), (3, "masked")])
+@pytest.mark.parametrize("world,cfg", [(2, "C1"), (3, "C2-16384"), (2, "random"), (3, "masked"), (4, "tiny")])
 def test_multirank_cuda_backend_equals_single_gpu(tmp_path, world, cfg, mode):
     """mode "fused": the numeric kernel reads remote blocks through CUDA-IPC-mapped peer pools
     (qm_numeric_pools_ex) instead of an exchange; mode "staged": k_halo_gather pulls the halo

@@ -21,10 +21,18 @@ def dev():
     return torch.device("cuda:0")
 
 
-@pytest.mark.parametrize("name", ["C1", "C2-16384", "C3", "C4"])
+EXTRA = {  # the staged path at the other TMA block sizes (bs 128: 4 work units per C block)
+    "banded-bs32": G.BaselineConfig("t32", "banded", 8192, 32, half_bw=256),
+    "banded-bs128": G.BaselineConfig("t128", "banded", 16384, 128, half_bw=512),
+    # more ranks than C tiles and than owned blocks (ragged n = 96: 3x3 blocks of a 4x4 grid)
+    "tiny": G.BaselineConfig("t-tiny", "banded", 96, 32, half_bw=20),
+}
+
+
+@pytest.mark.parametrize("name", ["C1", "C2-16384", "C3", "C4", "tiny"])
 @pytest.mark.parametrize("world", [2, 3, 8])
 def test_ranks_partition_the_product_exactly(dev, name, world):
-    cfg = G.CONFIGS[name]
+    cfg = EXTRA[name] if name in EXTRA else G.CONFIGS[name]
     geom, a, b = G.config_operands_device(cfg, dev)
     if cfg.same_operand:
         b = a
@@ -86,15 +94,10 @@ def _in_process_peers(t: torch.Tensor, off: list) -> list:
     return [t.data_ptr() + off[r] * blk for r in range(len(off) - 1)]
 
 
-EXTRA = {  # the staged path at the other TMA block sizes (bs 128: 4 work units per C block)
-    "banded-bs32": G.BaselineConfig("t32", "banded", 8192, 32, half_bw=256),
-    "banded-bs128": G.BaselineConfig("t128", "banded", 16384, 128, half_bw=512),
-}
-
-
 @pytest.mark.parametrize("name,world,staged", [("C4", 4, True), ("C4", 8, True), ("C2-16384", 3, True),
                                                ("C3", 2, True), ("C4", 4, False), ("banded-bs32", 3, True),
-                                               ("banded-bs128", 3, True), ("banded-bs128", 2, False)])
+                                               ("banded-bs128", 3, True), ("banded-bs128", 2, False),
+                                               ("tiny", 8, True), ("tiny", 8, False)])
 def test_staged_and_fused_rank_numeric_equal_single_gpu(dev, name, world, staged):
     """staged_numeric for every rank, the operands' other ranks being slices of the same pools:
     staged (halo gathered by k_halo_gather while the numeric kernel -- its programmatic dependent --
