@@ -36,6 +36,12 @@ constexpr int kBlkBytes = kBlk * kBlk * 8;    // 2 KB
 constexpr int kCW = 4;                        // consumer warps: warp w owns columns 2w, 2w+1
 constexpr uint32_t kAbsent = 0xffffffffu;
 
+// Columns of consumer warp w: 2w, 2w+1. (Interleaving them -- w, w+4 -- to spread the contiguous
+// column runs at the ends of a group's k range over the warps measured 4 % slower: more stages take
+// the guarded path.)
+__device__ __forceinline__ int gcol(int warp, int q) { return 2 * warp + q; }
+__device__ __forceinline__ uint32_t gcols_present(uint32_t pm, int warp) { return (pm >> (2 * warp)) & 3u; }
+
 // R = block rows per group (1, or 2 when a leaf row pair is contiguous in key order: <= 8 blocks per
 // leaf side). A group is R x 8 member slots, slot = r * 8 + c, in key order.
 template <int R>
@@ -166,38 +172,39 @@ __global__ void k_group_merge(const uint64_t *c_keys, const int64_t *c_tptr, con
 }
 
 // One stage of a consumer warp: the products of its columns 2w, 2w+1 with every present A row.
-// ALL = every A row and both B columns present (no per-product guards, so loads of the next k step
-// can be scheduled under the DMMAs of this one). Returns the OR of the stage's last fragments (the
-// stage-release dependency, see k_numeric_tma).
-template <int R, bool ALL>
-__device__ __forceinline__ uint64_t group_stage(const uint8_t *sa, int warp, uint32_t ona, uint32_t onb,
-                                                const uint32_t (&aoff)[4], const uint32_t (&boff)[4][2],
-                                                double (&acc)[R][2][2][2][2]) {
+// ONA / ONB = the present A rows / B columns of the warp as compile-time masks: each of the (at most
+// nine) combinations is its own straight-line code without per-product guards, so the loads of the
+// next k step can be scheduled under the DMMAs of this one for partial stages too (the ends of a
+// group's k range, where only some of its columns have a B block). Returns the OR of the stage's
+// last fragments (the stage-release dependency, see k_numeric_tma).
+template <int R, uint32_t ONA, uint32_t ONB>
+__device__ __forceinline__ uint64_t group_stage(const uint8_t *sa, int warp, const uint32_t (&aoff)[4],
+                                                const uint32_t (&boff)[4][2], double (&acc)[R][2][2][2][2]) {
   uint64_t dep = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     double af[R][2], bf[2][2];
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      if (ALL || (ona & (1u << r)))
+      if (ONA & (1u << r))
 #pragma unroll
         for (int i = 0; i < 2; ++i) af[r][i] = *(const double *)(sa + r * kBlkBytes + i * 8 * 128 + aoff[j]);
 #pragma unroll
     for (int q = 0; q < 2; ++q)
-      if (ALL || (onb & (1u << q))) {
-        const uint8_t *sb = sa + (R + 2 * warp + q) * kBlkBytes;
+      if (ONB & (1u << q)) {
+        const uint8_t *sb = sa + (R + gcol(warp, q)) * kBlkBytes;
 #pragma unroll
         for (int n = 0; n < 2; ++n) bf[q][n] = *(const double *)(sb + boff[j][n]);
       }
     if (j == 3) {
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        if (ALL || (ona & (1u << r)))
+        if (ONA & (1u << r))
 #pragma unroll
           for (int i = 0; i < 2; ++i) dep |= (uint64_t)__double_as_longlong(af[r][i]);
 #pragma unroll
       for (int q = 0; q < 2; ++q)
-        if (ALL || (onb & (1u << q)))
+        if (ONB & (1u << q))
 #pragma unroll
           for (int n = 0; n < 2; ++n) dep |= (uint64_t)__double_as_longlong(bf[q][n]);
     }
@@ -205,7 +212,7 @@ __device__ __forceinline__ uint64_t group_stage(const uint8_t *sa, int warp, uin
     for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int q = 0; q < 2; ++q)
-        if (ALL || ((ona & (1u << r)) && (onb & (1u << q))))
+        if ((ONA & (1u << r)) && (ONB & (1u << q)))
 #pragma unroll
           for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -214,7 +221,26 @@ __device__ __forceinline__ uint64_t group_stage(const uint8_t *sa, int warp, uin
   return dep;
 }
 
-template <int R>
+// Dispatch on the warp's present columns for a compile-time set of A rows.
+template <int R, uint32_t ONA>
+__device__ __forceinline__ uint64_t group_stage_b(const uint8_t *sa, int warp, uint32_t onb, const uint32_t (&aoff)[4],
+                                                  const uint32_t (&boff)[4][2], double (&acc)[R][2][2][2][2]) {
+  if (onb == 3u) return group_stage<R, ONA, 3u>(sa, warp, aoff, boff, acc);
+  if (onb == 1u) return group_stage<R, ONA, 1u>(sa, warp, aoff, boff, acc);
+  return group_stage<R, ONA, 2u>(sa, warp, aoff, boff, acc);
+}
+
+// The members' triple lists of a group as the inline-merge producer reads them (INLINE = true: the
+// producer warp merges the lists itself, one entry per stage, instead of reading k_group_merge's
+// entries).
+struct GroupSrc {
+  const uint64_t *c_keys, *a_keys;
+  const uint2 *tri;
+  int64_t nC;
+  int nbl, lbits, mbits;
+};
+
+template <int R, bool INLINE>
 __global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
     k_numeric_group16(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                       const uint32_t *__restrict__ entries, const int64_t *__restrict__ c_tptr,
@@ -222,7 +248,7 @@ __global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
                       const int64_t *__restrict__ gfirst, const uint32_t *__restrict__ gmask,
                       const int64_t *__restrict__ n_groups_dev, double *__restrict__ C, double *__restrict__ csq,
                       uint8_t *__restrict__ cnz, int64_t *__restrict__ zero_count,
-                      unsigned long long *__restrict__ counter, uint64_t zmask) {
+                      unsigned long long *__restrict__ counter, uint64_t zmask, const GroupSrc src) {
   using Cfg = GCfg<R>;
   constexpr int STAGES = Cfg::STAGES, EW = Cfg::EW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -251,6 +277,131 @@ __global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&map_b) : "memory");
     }
     const bool loader = lane < kG + R;
+    if constexpr (INLINE) {
+      // ---- inline merge: lane s < M owns the member in slot s and walks its k-ascending triple
+      // list (its next kD triples and their k prefetched); every stage takes the smallest head k
+      // over the lanes, and the lanes holding it supply the A index of their row and the B index
+      // of their column to the loader lanes -- k_group_merge's step, done here once per stage, so
+      // there is no merge pass, no entries array and no per-group metadata read by the consumers
+      // (the stage word carries the group's first C block, member mask, present blocks and the
+      // last-stage flag). The next group is claimed when at most kAhead entries of some member
+      // remain (just in time for L2 locality, early enough to hide its header loads).
+      constexpr int M = Cfg::M, kD = 4, kAhead = 6;
+      constexpr uint32_t kNone = 0xffffffffu;
+      const int slot = lane < kG ? R + lane : lane - kG;
+      const uint32_t sel = lane < kG ? (R == 2 ? (0x101u << lane) : (1u << lane))       // B column `lane`
+                                     : (loader ? (0xffu << (8 * (lane - kG))) : 0u);     // A row lane - 8
+      int64_t pos = 0, end = 0, npos = 0, nend = 0;
+      int64_t unit = blockIdx.x, nunit = 0;
+      uint32_t mask = 0, nmask = 0;
+      int32_t first = 0, nfirst = 0;
+      bool claimed = false;
+      uint2 t[kD];
+      uint32_t kq[kD];
+      auto header = [&](int64_t g, int64_t &p, int64_t &e, uint32_t &mk, int32_t &c_first) {
+        p = e = 0;
+        mk = 0;
+        c_first = 0;
+        if (g >= nG) return;
+        const int64_t c0 = gfirst[g];
+        const int nm = (int)((g + 1 < nG ? gfirst[g + 1] : src.nC) - c0);
+        uint32_t bit = 0;
+        if (lane < nm) bit = 1u << member_slot<R>(src.c_keys[c0 + lane], src.lbits, src.mbits);
+        mk = __reduce_or_sync(0xffffffffu, bit);
+        c_first = (int32_t)c0;
+        if (lane < M && ((mk >> lane) & 1u)) {  // members are in key order = slot order
+          const int m = __popc(mk & ((1u << lane) - 1u));
+          p = c_tptr[c0 + m];
+          e = c_tptr[c0 + m + 1];
+        }
+      };
+      auto fetch = [&](int d, int64_t at) {
+        kq[d] = kNone;
+        t[d] = make_uint2(0u, 0u);
+        if (at < end) {
+          uint32_t bi;
+          t[d] = src.tri[at];
+          qkey_decode(src.a_keys[t[d].x], src.nbl, src.lbits, &bi, &kq[d]);
+        }
+      };
+      header(unit, pos, end, mask, first);
+#pragma unroll
+      for (int d = 0; d < kD; ++d) fetch(d, pos + d);
+      uint32_t kmin = __reduce_min_sync(0xffffffffu, kq[0]);
+      int s = 0;
+      uint32_t phase = 0;
+      while (true) {
+        if (unit >= nG) {
+          if (lane == 0) {
+            mbar_wait(&empty[s], phase ^ 1u);
+            meta[s] = -1;
+            mbar_arrive(&full[s]);
+          }
+          break;
+        }
+        if (!claimed) {
+          const uint32_t rem = __reduce_max_sync(0xffffffffu, (uint32_t)(end - pos));
+          if (rem <= (uint32_t)kAhead) {
+            unsigned long long got = 0;
+            if (lane == 0) got = atomicAdd(counter, 1ull);
+            nunit = (int64_t)gridDim.x + (int64_t)__shfl_sync(0xffffffffu, got, 0);
+            header(nunit, npos, nend, nmask, nfirst);
+            claimed = true;
+          }
+        }
+        const bool hit = kq[0] == kmin;
+        const uint32_t hits = __ballot_sync(0xffffffffu, hit);
+        const uint32_t mine = hits & sel;
+        const int from = mine ? __ffs(mine) - 1 : 0;
+        const uint32_t av = __shfl_sync(0xffffffffu, t[0].x, from), bv = __shfl_sync(0xffffffffu, t[0].y, from);
+        const uint32_t cur = mine ? (lane < kG ? bv : av) : kAbsent;
+        if (hit) {
+#pragma unroll
+          for (int d = 0; d + 1 < kD; ++d) {
+            t[d] = t[d + 1];
+            kq[d] = kq[d + 1];
+          }
+          ++pos;
+          fetch(kD - 1, pos + kD - 1);
+        }
+        const uint32_t knext = __reduce_min_sync(0xffffffffu, kq[0]);
+        const bool last = knext == kNone;
+        if (lane == 0) mbar_wait(&empty[s], phase ^ 1u);
+        __syncwarp();
+        const uint32_t pm = __ballot_sync(0xffffffffu, cur != kAbsent);
+        uint8_t *st = smem + (size_t)s * Cfg::STAGE_BYTES;
+        if (lane == 0) {
+          meta[s] = ((int64_t)first << 32) | (int64_t)(mask << 16) | (int64_t)(pm << 1) | (last ? 1 : 0);
+          mbar_expect_tx(&full[s], (uint32_t)__popc(pm) * kBlkBytes);
+        }
+        __syncwarp();
+        if (cur != kAbsent)
+          tma_load_2d(st + slot * kBlkBytes, lane < kG ? &map_b : &map_a, 0, (int)(cur * kBlk), &full[s]);
+        if (++s == STAGES) {
+          s = 0;
+          phase ^= 1u;
+        }
+        kmin = knext;
+        if (last) {  // next group (claimed above: a finished group has no entries left)
+          if (!claimed) {
+            unsigned long long got = 0;
+            if (lane == 0) got = atomicAdd(counter, 1ull);
+            nunit = (int64_t)gridDim.x + (int64_t)__shfl_sync(0xffffffffu, got, 0);
+            header(nunit, npos, nend, nmask, nfirst);
+          }
+          unit = nunit;
+          pos = npos;
+          end = nend;
+          mask = nmask;
+          first = nfirst;
+          claimed = false;
+#pragma unroll
+          for (int d = 0; d < kD; ++d) fetch(d, pos + d);
+          kmin = __reduce_min_sync(0xffffffffu, kq[0]);
+        }
+      }
+      return;
+    }
     const int word = lane < kG ? R + lane : lane - kG;  // Entry layout: a[R], b[8]
     // smem slot of this lane's block: A rows first, then the 8 B columns
     const int slot = lane < kG ? R + lane : lane - kG;
@@ -337,23 +488,35 @@ __global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
     mbar_wait(&full[s], phase);
     const int64_t mt = meta[s];
     if (mt < 0) break;
-    if ((int32_t)(mt >> 1) != cur_unit) {  // a group's first stage: fetch its epilogue metadata now,
-      cur_unit = (int32_t)(mt >> 1);       // so the loads complete under the group's DMMAs
-      gm = gmask[cur_unit];
-      c_first = (int32_t)gfirst[cur_unit];
+    uint32_t pm;
+    if constexpr (INLINE) {  // stage word: first C block << 32 | member mask << 16 | present << 1 | last
+      c_first = (int32_t)(mt >> 32);
+      gm = ((uint32_t)mt >> 16) & 0xffffu;
+      pm = ((uint32_t)mt >> 1) & 0x7fffu;
+    } else {
+      const int32_t mt_unit = (int32_t)(mt >> 1);
+      if (mt_unit != cur_unit) {  // a group's first stage: fetch its epilogue metadata now,
+        cur_unit = mt_unit;       // so the loads complete under the group's DMMAs
+        gm = gmask[cur_unit];
+        c_first = (int32_t)gfirst[cur_unit];
+      }
+      pm = pmask[s];
     }
-    const uint32_t pm = pmask[s];
-    const uint32_t onb = (pm >> (2 * warp)) & 3u;
+    const uint32_t onb = gcols_present(pm, warp);
     const uint32_t ona = (pm >> kG) & ((1u << R) - 1u);
     uint64_t dep = 0;
-    if (onb == 3u && ona == (1u << R) - 1u) {  // every product of the warp present: no guards
-      dep = group_stage<R, true>(smem + (size_t)s * Cfg::STAGE_BYTES, warp, ona, onb, aoff, boff, acc);
+    const uint8_t *stg = smem + (size_t)s * Cfg::STAGE_BYTES;
+    if (onb && ona) {
+      if (ona == (1u << R) - 1u) {
+        dep = group_stage_b<R, (1u << R) - 1u>(stg, warp, onb, aoff, boff, acc);
 #ifdef QM_EXP_G16_REPEAT  // experiment (wrong results): twice the DMMAs per stage, same stage overhead
-      dep |= group_stage<R, true>(smem + (size_t)s * Cfg::STAGE_BYTES, warp, ona, onb, aoff, boff, acc);
+        dep |= group_stage_b<R, (1u << R) - 1u>(stg, warp, onb, aoff, boff, acc);
 #endif
+      } else if (R == 2) {
+        dep = ona == 1u ? group_stage_b<R, 1u>(stg, warp, onb, aoff, boff, acc)
+                        : group_stage_b<R, (R == 2 ? 2u : 1u)>(stg, warp, onb, aoff, boff, acc);
+      }
     }
-    else if (onb)
-      dep = group_stage<R, false>(smem + (size_t)s * Cfg::STAGE_BYTES, warp, ona, onb, aoff, boff, acc);
     // release once this warp's fragments are in registers (see k_numeric_tma)
     dep &= zmask;
     __syncwarp();
@@ -368,7 +531,7 @@ __global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
       for (int r = 0; r < R; ++r)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          const int mb = r * kG + 2 * warp + q;
+          const int mb = r * kG + gcol(warp, q);
           if ((gm >> mb) & 1u) {
             const int64_t c = (int64_t)c_first + __popc(gm & ((1u << mb) - 1u));
             double *cb = C + (size_t)c * (kBlk * kBlk);
@@ -430,6 +593,16 @@ struct GroupWs {
 };
 
 // Entries are sized for the widest layout (R = 2: 10 words), one per triple at most.
+// QM_G16_MERGE=kernel: the separate merge pass (k_group_merge + entries array) instead of the
+// producer's inline merge (A/B measurements).
+bool inline_merge() {
+  static const bool on = [] {
+    const char *e = getenv("QM_G16_MERGE");
+    return !(e && strcmp(e, "kernel") == 0);
+  }();
+  return on;
+}
+
 GroupWs carve_group(Carver &cv, int64_t nC, int64_t nT) {
   GroupWs w;
   w.head = cv.take<int64_t>(nC + 1);
@@ -439,7 +612,7 @@ GroupWs carve_group(Carver &cv, int64_t nC, int64_t nT) {
   w.n_groups = cv.take<int64_t>(1);
   w.gmask = cv.take<uint32_t>(nC + 1);
   w.counter = cv.take<unsigned long long>(1);
-  w.entries = cv.take<uint32_t>(std::max<int64_t>(nT, 1) * GCfg<2>::EW);  // <= one entry per triple
+  w.entries = cv.take<uint32_t>(inline_merge() ? 1 : std::max<int64_t>(nT, 1) * GCfg<2>::EW);  // <= one entry per triple
   w.cub_bytes = scan_bytes(nC + 1);
   w.cub = cv.take<char>(w.cub_bytes);
   return w;
@@ -453,7 +626,7 @@ int group_rows(const Geometry &g) {
   return g.lbits <= 3 ? 2 : 1;
 }
 
-template <int R>
+template <int R, bool INLINE>
 int launch_group(const Geometry &g, const double *A, int64_t nA, const double *B, int64_t nB,
                  const uint64_t *a_keys, const uint2 *t2, const int64_t *c_tptr, const uint64_t *c_keys,
                  int64_t nC, int64_t nT, double *C, double *csq, uint8_t *cnz, int64_t *zc, const GroupWs &w,
@@ -466,10 +639,12 @@ int launch_group(const Geometry &g, const double *A, int64_t nA, const double *B
   QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(w.cub, tb, w.head, w.gidx, nC + 1, st));
   k_group_first<<<grid_for(nC + 1), 256, 0, st>>>(w.head, w.gidx, nC, w.gfirst, w.n_groups);
   QM_LAUNCHED("k_group_first");
-  const int merge_grid = (int)std::min<int64_t>((nC + 7) / 8, (int64_t)device_sm_count() * 8);
-  k_group_merge<R><<<merge_grid, 256, 0, st>>>(c_keys, c_tptr, t2, a_keys, nC, g.nbl, g.lbits, mbits, w.gfirst,
-                                               w.n_groups, w.ucount, w.gmask, w.entries);
-  QM_LAUNCHED("k_group_merge");
+  if (!INLINE) {
+    const int merge_grid = (int)std::min<int64_t>((nC + 7) / 8, (int64_t)device_sm_count() * 8);
+    k_group_merge<R><<<merge_grid, 256, 0, st>>>(c_keys, c_tptr, t2, a_keys, nC, g.nbl, g.lbits, mbits, w.gfirst,
+                                                 w.n_groups, w.ucount, w.gmask, w.entries);
+    QM_LAUNCHED("k_group_merge");
+  }
   CUtensorMap ma, mb;
   int rc = make_map(&ma, A, nA, kBlk, kBlk);
   if (rc != QM_OK) return rc;
@@ -477,7 +652,7 @@ int launch_group(const Geometry &g, const double *A, int64_t nA, const double *B
   if (rc != QM_OK) return rc;
   static PerDeviceOnce once;
   rc = once.run([]() -> int {
-    QM_CUDA_TRY(cudaFuncSetAttribute(k_numeric_group16<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    QM_CUDA_TRY(cudaFuncSetAttribute(k_numeric_group16<R, INLINE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)Cfg::SMEM));
     return (int)QM_OK;
   });
@@ -486,16 +661,17 @@ int launch_group(const Geometry &g, const double *A, int64_t nA, const double *B
   int per_sm = 0;
   static PerDeviceInt occupancy;  // cudaOccupancy* costs microseconds of host time per call
   rc = occupancy.get(&per_sm, [](int *x) -> int {
-    QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(x, k_numeric_group16<R>, Cfg::THREADS, Cfg::SMEM));
+    QM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(x, k_numeric_group16<R, INLINE>, Cfg::THREADS, Cfg::SMEM));
     return (int)QM_OK;
   });
   if (rc != QM_OK) return rc;
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)device_sm_count() * per_sm;
   if (grid > nC) grid = nC;  // groups <= C blocks
-  k_numeric_group16<R><<<(int)grid, Cfg::THREADS, Cfg::SMEM, st>>>(
+  const GroupSrc src{c_keys, a_keys, t2, nC, g.nbl, g.lbits, mbits};
+  k_numeric_group16<R, INLINE><<<(int)grid, Cfg::THREADS, Cfg::SMEM, st>>>(
       ma, mb, w.entries, c_tptr, w.ucount, w.gfirst, w.gmask, w.n_groups, C, csq, cnz, zc, w.counter,
-      /*zmask=*/0ull);
+      /*zmask=*/0ull, src);
   QM_LAUNCHED("k_numeric_group16");
   return QM_OK;
 }
@@ -525,9 +701,12 @@ int launch_numeric_group16(const Geometry &g, const double *A, int64_t nA, const
     return QM_ERR_UNSUPPORTED;
   }
   const uint2 *t2 = (const uint2 *)tri;
+  const bool il = inline_merge();
   if (group_rows(g) == 2)
-    return launch_group<2>(g, A, nA, B, nB, a_keys, t2, c_tptr, c_keys, nC, nT, C, csq, cnz, zc, w, st);
-  return launch_group<1>(g, A, nA, B, nB, a_keys, t2, c_tptr, c_keys, nC, nT, C, csq, cnz, zc, w, st);
+    return il ? launch_group<2, true>(g, A, nA, B, nB, a_keys, t2, c_tptr, c_keys, nC, nT, C, csq, cnz, zc, w, st)
+              : launch_group<2, false>(g, A, nA, B, nB, a_keys, t2, c_tptr, c_keys, nC, nT, C, csq, cnz, zc, w, st);
+  return il ? launch_group<1, true>(g, A, nA, B, nB, a_keys, t2, c_tptr, c_keys, nC, nT, C, csq, cnz, zc, w, st)
+            : launch_group<1, false>(g, A, nA, B, nB, a_keys, t2, c_tptr, c_keys, nC, nT, C, csq, cnz, zc, w, st);
 }
 
 }  // namespace qm
