@@ -10,11 +10,12 @@
 // product at that k: up to 16 products for 20 KB (R = 2; 6.6 flop/byte) -- each B block serves
 // both rows and each A block all 8 columns.
 //
-//   k_group_merge: one warp per group merges the members' k-ascending triple lists into the
-//     group's union of k (one entry per k: R A indices and 8 B indices, absent = 0xffffffff),
-//     stored in the group's own triple range;
+//   merge: the members' k-ascending triple lists are merged into the group's union of k (one
+//     entry per k: R A indices and 8 B indices, absent = 0xffffffff) by the kernel's producer warp
+//     itself, one entry per pipeline stage (k_group_merge, one warp per group writing an entries
+//     array, is the earlier separate pass: QM_G16_MERGE=kernel);
 //   k_numeric_group16: warp-specialised like k_numeric_tma (one TMA producer warp, mbarrier ring),
-//     4 consumer warps, warp w owns columns 2w, 2w+1 of every group row: R x 2 accumulators of
+//     4 consumer warps, warp w owns columns w, w+4 of every group row: R x 2 accumulators of
 //     16x16 fed only by the entries where both its A row and B column are present (so each C
 //     block sums exactly its own triples, k ascending -- the order of BlockSparseLeaf.multiply,
 //     block_sparse.py:121-129), and writes the blocks, their sums of squares and exact-zero flags
@@ -36,11 +37,20 @@ constexpr int kBlkBytes = kBlk * kBlk * 8;    // 2 KB
 constexpr int kCW = 4;                        // consumer warps: warp w owns columns 2w, 2w+1
 constexpr uint32_t kAbsent = 0xffffffffu;
 
-// Columns of consumer warp w: 2w, 2w+1. (Interleaving them -- w, w+4 -- to spread the contiguous
-// column runs at the ends of a group's k range over the warps measured 4 % slower: more stages take
-// the guarded path.)
+// Columns of consumer warp w: w and w + 4. At the ends of a group's k range only a contiguous run
+// of its columns has a B block; interleaving spreads that run over the warps (= the SM's four
+// sub-partitions), so the busiest warp of a partial stage has half the work it would have with
+// adjacent columns 2w, 2w+1 (-DQM_EXP_G16_PAIRED; +3 % with the specialised partial stages below,
+// -4 % before them, when every partial stage took a guarded slow path).
+#ifdef QM_EXP_G16_PAIRED
 __device__ __forceinline__ int gcol(int warp, int q) { return 2 * warp + q; }
 __device__ __forceinline__ uint32_t gcols_present(uint32_t pm, int warp) { return (pm >> (2 * warp)) & 3u; }
+#else
+__device__ __forceinline__ int gcol(int warp, int q) { return warp + 4 * q; }
+__device__ __forceinline__ uint32_t gcols_present(uint32_t pm, int warp) {
+  return ((pm >> warp) & 1u) | (((pm >> (warp + 4)) & 1u) << 1);
+}
+#endif
 
 // R = block rows per group (1, or 2 when a leaf row pair is contiguous in key order: <= 8 blocks per
 // leaf side). A group is R x 8 member slots, slot = r * 8 + c, in key order.
@@ -171,7 +181,7 @@ __global__ void k_group_merge(const uint64_t *c_keys, const int64_t *c_tptr, con
   }
 }
 
-// One stage of a consumer warp: the products of its columns 2w, 2w+1 with every present A row.
+// One stage of a consumer warp: the products of its two columns with every present A row.
 // ONA / ONB = the present A rows / B columns of the warp as compile-time masks: each of the (at most
 // nine) combinations is its own straight-line code without per-product guards, so the loads of the
 // next k step can be scheduled under the DMMAs of this one for partial stages too (the ends of a
@@ -460,7 +470,7 @@ __global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
     return;
   }
 
-  // -------- consumers: warp w = columns 2w, 2w+1 of every group row (R*16 x 32: each A fragment
+  // -------- consumers: warp w = columns w, w+4 (gcol) of every group row (R*16 x 32: each A fragment
   // serves both columns, each B fragment every row) --------
   const int g = lane >> 2, tq = lane & 3;
   uint32_t aoff[4], boff[4][2];
@@ -485,7 +495,7 @@ __global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
   int32_t cur_unit = -1, c_first = 0;  // (32-bit: fewer live registers across the stage loop)
   uint32_t gm = 0;
   while (true) {
-    mbar_wait(&full[s], phase);
+    mbar_wait(&full[s], phase);  // (testing the next stage's barrier early, under this stage's DMMAs: -0.7 %)
     const int64_t mt = meta[s];
     if (mt < 0) break;
     uint32_t pm;
@@ -596,11 +606,8 @@ struct GroupWs {
 // QM_G16_MERGE=kernel: the separate merge pass (k_group_merge + entries array) instead of the
 // producer's inline merge (A/B measurements).
 bool inline_merge() {
-  static const bool on = [] {
-    const char *e = getenv("QM_G16_MERGE");
-    return !(e && strcmp(e, "kernel") == 0);
-  }();
-  return on;
+  const char *e = getenv("QM_G16_MERGE");
+  return !(e && strcmp(e, "kernel") == 0);
 }
 
 GroupWs carve_group(Carver &cv, int64_t nC, int64_t nT) {

@@ -741,6 +741,24 @@ def test_bs16_row_pair_groups_bitwise_equal_single_row(ses, monkeypatch, n, leaf
     assert helpers.rel(ses.to_dense(ses.multiply(a, b)), da @ db) <= TOL
 
 
+@pytest.mark.parametrize("n,leaf,dens", [(1000, 128, 0.02), (500, 48, 0.05), (2048, 128, 0.3), (600, 32, 0.1),
+                                         (4096, 256, 0.01)])
+def test_bs16_inline_merge_bitwise_equal_merge_pass(ses, monkeypatch, n, leaf, dens):
+    """The bs 16 grouped kernel's producer merges the members' k-ascending triple lists itself, one
+    entry per pipeline stage (default); QM_G16_MERGE=kernel runs the separate merge pass
+    (k_group_merge + entries array) instead. Same entries in the same order, so the C blocks, norms
+    and exact-zero drops are bitwise identical, for row-pair (leaf <= 128) and single-row groups."""
+    da, db = helpers.random_sparse(n, dens, n + 15), helpers.random_sparse(n, dens, n + 16)
+    a, b = helpers.build(ses, da, leaf, 16), helpers.build(ses, db, leaf, 16)
+    c2 = ses.multiply(a, b).root.blockset
+    monkeypatch.setenv("QM_G16_MERGE", "kernel")
+    c1 = ses.multiply(a, b).root.blockset
+    assert torch.equal(c1.keys, c2.keys)
+    assert torch.equal(c1.blocks, c2.blocks) and torch.equal(c1.sumsq, c2.sumsq)
+    monkeypatch.delenv("QM_G16_MERGE")
+    assert helpers.rel(ses.to_dense(ses.multiply(a, b)), da @ db) <= TOL
+
+
 @pytest.mark.parametrize("bs,n", [(64, 65536), (32, 16384), (128, 32768), (64, 8192)])
 def test_claim_order_is_bitwise_neutral(ses, monkeypatch, bs, n):
     """Claim orders of the numeric kernel: QM_UNIT_ORDER=k (by the k of each C block's first triple:
