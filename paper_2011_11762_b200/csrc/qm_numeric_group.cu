@@ -34,7 +34,7 @@ namespace {
 constexpr int kG = 8;                         // block columns per group
 constexpr int kBlk = 16;                      // block size
 constexpr int kBlkBytes = kBlk * kBlk * 8;    // 2 KB
-constexpr int kCW = 4;                        // consumer warps: warp w owns columns 2w, 2w+1
+constexpr int kCW = 4;                        // consumer warps: warp w owns columns w, w+4 (gcol)
 constexpr uint32_t kAbsent = 0xffffffffu;
 
 // Columns of consumer warp w: w and w + 4. At the ends of a group's k range only a contiguous run
