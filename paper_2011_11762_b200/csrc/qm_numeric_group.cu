@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
   volatile int64_t *meta = (volatile int64_t *)(empty + STAGES);       // unit*2 + last, -1 = end
   volatile uint32_t *pmask = (volatile uint32_t *)(meta + STAGES);     // bits 0-7 B columns, 8.. A rows
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nG = *n_groups_dev;
+  const int64_t nG = INLINE ? 0 : *n_groups_dev;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -294,31 +294,58 @@ __global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
       // of their column to the loader lanes -- k_group_merge's step, done here once per stage, so
       // there is no merge pass, no entries array and no per-group metadata read by the consumers
       // (the stage word carries the group's first C block, member mask, present blocks and the
-      // last-stage flag). The next group is claimed when at most kAhead entries of some member
-      // remain (just in time for L2 locality, early enough to hide its header loads).
+      // last-stage flag).
+      // Work is claimed in chunks of 16 consecutive C blocks: the groups that START in a chunk are
+      // its claimer's (a group has at most 16 members, so every chunk holds a start), found by
+      // comparing neighbouring keys' group codes -- no pre-pass over the C keys at all. The next
+      // group (and, when the chunk is used up, the next chunk) is taken when at most kAhead entries
+      // of some member remain: just in time for L2 locality, early enough to hide its header loads.
       constexpr int M = Cfg::M, kD = 4, kAhead = 6;
       constexpr uint32_t kNone = 0xffffffffu;
       const int slot = lane < kG ? R + lane : lane - kG;
       const uint32_t sel = lane < kG ? (R == 2 ? (0x101u << lane) : (1u << lane))       // B column `lane`
                                      : (loader ? (0xffu << (8 * (lane - kG))) : 0u);     // A row lane - 8
+      const int64_t nQ = (src.nC + 15) >> 4;
       int64_t pos = 0, end = 0, npos = 0, nend = 0;
-      int64_t unit = blockIdx.x, nunit = 0;
-      uint32_t mask = 0, nmask = 0;
-      int32_t first = 0, nfirst = 0;
+      int64_t chunk = blockIdx.x, first = -1, nfirst = -1;
+      uint32_t heads = 0, mask = 0, nmask = 0;
       bool claimed = false;
       uint2 t[kD];
       uint32_t kq[kD];
-      auto header = [&](int64_t g, int64_t &p, int64_t &e, uint32_t &mk, int32_t &c_first) {
+      auto chunk_heads = [&](int64_t q) -> uint32_t {
+        const int64_t c = (q << 4) + lane;
+        bool head = false;
+        if (lane < 16 && c < src.nC)
+          head = c == 0 || group_code<R>(src.c_keys[c], src.lbits, src.mbits) !=
+                               group_code<R>(src.c_keys[c - 1], src.lbits, src.mbits);
+        return __ballot_sync(0xffffffffu, head);
+      };
+      // First C block of the next group of this CTA (-1: no work left); claims chunks as needed.
+      auto next_group = [&]() -> int64_t {
+        while (heads == 0u) {
+          unsigned long long got = 0;
+          if (lane == 0) got = atomicAdd(counter, 1ull);
+          chunk = (int64_t)gridDim.x + (int64_t)__shfl_sync(0xffffffffu, got, 0);
+          if (chunk >= nQ) return -1;
+          heads = chunk_heads(chunk);
+        }
+        const int h = __ffs(heads) - 1;
+        heads &= heads - 1u;
+        return (chunk << 4) + h;
+      };
+      // Members of the group starting at C block c0 (the run of keys with its group code), their
+      // slots and this lane's triple range.
+      auto header = [&](int64_t c0, int64_t &p, int64_t &e, uint32_t &mk) {
         p = e = 0;
         mk = 0;
-        c_first = 0;
-        if (g >= nG) return;
-        const int64_t c0 = gfirst[g];
-        const int nm = (int)((g + 1 < nG ? gfirst[g + 1] : src.nC) - c0);
-        uint32_t bit = 0;
-        if (lane < nm) bit = 1u << member_slot<R>(src.c_keys[c0 + lane], src.lbits, src.mbits);
-        mk = __reduce_or_sync(0xffffffffu, bit);
-        c_first = (int32_t)c0;
+        if (c0 < 0) return;
+        const bool in = lane < 16 && c0 + lane < src.nC;
+        const uint64_t key = in ? src.c_keys[c0 + lane] : 0ull;
+        const uint64_t code = group_code<R>(key, src.lbits, src.mbits);
+        const uint64_t code0 = __shfl_sync(0xffffffffu, code, 0);
+        const uint32_t eq = __ballot_sync(0xffffffffu, in && code == code0);
+        const int nm = __ffs(~eq) - 1;  // length of the run of equal codes from lane 0
+        mk = __reduce_or_sync(0xffffffffu, lane < nm ? 1u << member_slot<R>(key, src.lbits, src.mbits) : 0u);
         if (lane < M && ((mk >> lane) & 1u)) {  // members are in key order = slot order
           const int m = __popc(mk & ((1u << lane) - 1u));
           p = c_tptr[c0 + m];
@@ -334,14 +361,18 @@ __global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
           qkey_decode(src.a_keys[t[d].x], src.nbl, src.lbits, &bi, &kq[d]);
         }
       };
-      header(unit, pos, end, mask, first);
+      if (chunk < nQ) {
+        heads = chunk_heads(chunk);
+        first = next_group();
+      }
+      header(first, pos, end, mask);
 #pragma unroll
       for (int d = 0; d < kD; ++d) fetch(d, pos + d);
       uint32_t kmin = __reduce_min_sync(0xffffffffu, kq[0]);
       int s = 0;
       uint32_t phase = 0;
       while (true) {
-        if (unit >= nG) {
+        if (first < 0) {
           if (lane == 0) {
             mbar_wait(&empty[s], phase ^ 1u);
             meta[s] = -1;
@@ -352,10 +383,8 @@ __global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
         if (!claimed) {
           const uint32_t rem = __reduce_max_sync(0xffffffffu, (uint32_t)(end - pos));
           if (rem <= (uint32_t)kAhead) {
-            unsigned long long got = 0;
-            if (lane == 0) got = atomicAdd(counter, 1ull);
-            nunit = (int64_t)gridDim.x + (int64_t)__shfl_sync(0xffffffffu, got, 0);
-            header(nunit, npos, nend, nmask, nfirst);
+            nfirst = next_group();
+            header(nfirst, npos, nend, nmask);
             claimed = true;
           }
         }
@@ -381,7 +410,7 @@ __global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
         const uint32_t pm = __ballot_sync(0xffffffffu, cur != kAbsent);
         uint8_t *st = smem + (size_t)s * Cfg::STAGE_BYTES;
         if (lane == 0) {
-          meta[s] = ((int64_t)first << 32) | (int64_t)(mask << 16) | (int64_t)(pm << 1) | (last ? 1 : 0);
+          meta[s] = (first << 32) | (int64_t)(mask << 16) | (int64_t)(pm << 1) | (last ? 1 : 0);
           mbar_expect_tx(&full[s], (uint32_t)__popc(pm) * kBlkBytes);
         }
         __syncwarp();
@@ -392,18 +421,15 @@ __global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
           phase ^= 1u;
         }
         kmin = knext;
-        if (last) {  // next group (claimed above: a finished group has no entries left)
+        if (last) {  // next group (taken above: a finished group has no entries left)
           if (!claimed) {
-            unsigned long long got = 0;
-            if (lane == 0) got = atomicAdd(counter, 1ull);
-            nunit = (int64_t)gridDim.x + (int64_t)__shfl_sync(0xffffffffu, got, 0);
-            header(nunit, npos, nend, nmask, nfirst);
+            nfirst = next_group();
+            header(nfirst, npos, nend, nmask);
           }
-          unit = nunit;
+          first = nfirst;
           pos = npos;
           end = nend;
           mask = nmask;
-          first = nfirst;
           claimed = false;
 #pragma unroll
           for (int d = 0; d < kD; ++d) fetch(d, pos + d);
@@ -640,12 +666,14 @@ int launch_group(const Geometry &g, const double *A, int64_t nA, const double *B
                  cudaStream_t st) {
   using Cfg = GCfg<R>;
   const int mbits = std::min(g.lbits, 3);
-  k_group_heads<R><<<grid_for(nC + 1), 256, 0, st>>>(c_keys, nC, g.lbits, mbits, w.head);
-  QM_LAUNCHED("k_group_heads");
-  size_t tb = w.cub_bytes;
-  QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(w.cub, tb, w.head, w.gidx, nC + 1, st));
-  k_group_first<<<grid_for(nC + 1), 256, 0, st>>>(w.head, w.gidx, nC, w.gfirst, w.n_groups);
-  QM_LAUNCHED("k_group_first");
+  if (!INLINE) {
+    k_group_heads<R><<<grid_for(nC + 1), 256, 0, st>>>(c_keys, nC, g.lbits, mbits, w.head);
+    QM_LAUNCHED("k_group_heads");
+    size_t tb = w.cub_bytes;
+    QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(w.cub, tb, w.head, w.gidx, nC + 1, st));
+    k_group_first<<<grid_for(nC + 1), 256, 0, st>>>(w.head, w.gidx, nC, w.gfirst, w.n_groups);
+    QM_LAUNCHED("k_group_first");
+  }
   if (!INLINE) {
     const int merge_grid = (int)std::min<int64_t>((nC + 7) / 8, (int64_t)device_sm_count() * 8);
     k_group_merge<R><<<merge_grid, 256, 0, st>>>(c_keys, c_tptr, t2, a_keys, nC, g.nbl, g.lbits, mbits, w.gfirst,
@@ -674,7 +702,8 @@ int launch_group(const Geometry &g, const double *A, int64_t nA, const double *B
   if (rc != QM_OK) return rc;
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)device_sm_count() * per_sm;
-  if (grid > nC) grid = nC;  // groups <= C blocks
+  const int64_t units = INLINE ? (nC + 15) / 16 : nC;  // chunks of 16 C blocks; groups <= C blocks
+  if (grid > units) grid = units;
   const GroupSrc src{c_keys, a_keys, t2, nC, g.nbl, g.lbits, mbits};
   k_numeric_group16<R, INLINE><<<(int)grid, Cfg::THREADS, Cfg::SMEM, st>>>(
       ma, mb, w.entries, c_tptr, w.ucount, w.gfirst, w.gmask, w.n_groups, C, csq, cnz, zc, w.counter,
