@@ -447,8 +447,15 @@ def run_ours(args):
         step = None  # noqa: F841 -- the timed loop's closure held the device operands
         a = b = None  # the e2e loop double-buffers its own device copies (C5: 2 x 35 GB + 2 x 35 GB of C)
         torch.cuda.empty_cache()
-        line["e2e"] = run_e2e(args, torch, ses, geom, host, dev)
-        line["e2e"]["pcie"] = pcie_floor(torch, dev, line["e2e"])
+        try:
+            line["e2e"] = run_e2e(args, torch, ses, geom, host, dev)
+        except (RuntimeError, MemoryError) as e:  # e.g. a host that cannot pin the operands: keep the line
+            line["e2e"] = {"value": None, "unit": "GFLOP/s", "error": f"{type(e).__name__}: {str(e)[:300]}"}
+        else:
+            try:
+                line["e2e"]["pcie"] = pcie_floor(torch, dev, line["e2e"])
+            except (RuntimeError, MemoryError) as e:
+                line["e2e"]["pcie"] = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
         del host
     elif not args.no_e2e:
         line["e2e"] = run_e2e_distributed(args, torch, geom, a, b, dev, world, dist, cdev)

@@ -1004,6 +1004,23 @@ def test_cached_row_index_symbolic_equals_keys_path(ses, monkeypatch, name):
     assert torch.equal(p1.c_keys, p0.c_keys) and torch.equal(p1.c_tptr, p0.c_tptr) and torch.equal(p1.tri, p0.tri)
 
 
+@pytest.mark.parametrize("cfg", [G.CONFIGS["C1"], G.BaselineConfig("t", "random", 2048, 64, per_row=8),
+                                 G.BaselineConfig("t", "banded", 12288, 64, half_bw=512)])
+def test_single_cta_sort_equals_device_sort(ses, monkeypatch, cfg):
+    """Products with at most 8,192 C blocks order their keys in one launch of one CTA (k_sort_small)
+    instead of the device-wide radix sort's ten launches (QM_SMALL_SORT=0): same C keys, c_tptr and
+    triples, in the same order."""
+    geom, a, b = G.config_operands_device(cfg, ses.device)
+    lay = _ffi.make_layout(geom.params, geom.bs)
+    monkeypatch.setenv("QM_SMALL_SORT", "1")
+    p1 = spgemm.symbolic(lay, a, b)
+    assert 0 < p1.n_c <= 8192
+    monkeypatch.setenv("QM_SMALL_SORT", "0")
+    p0 = spgemm.symbolic(lay, a, b)
+    assert (p1.n_c, p1.n_triples) == (p0.n_c, p0.n_triples)
+    assert torch.equal(p1.c_keys, p0.c_keys) and torch.equal(p1.c_tptr, p0.c_tptr) and torch.equal(p1.tri, p0.tri)
+
+
 def test_cached_row_index_on_wide_rows(ses, monkeypatch):
     """Rows spanning several 4096-column windows of the count accumulator (as
     test_support_filter_multi_window_rows): the row-index path equals the keys path."""
