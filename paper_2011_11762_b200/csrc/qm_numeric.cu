@@ -442,6 +442,11 @@ int launch_numeric_group16(const Geometry &g, const double *A, int64_t nA, const
                            const uint64_t *c_keys, int64_t nC, int64_t nT, double *C, double *csq,
                            uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes, cudaStream_t st);
 
+int launch_numeric_quad32(const Geometry &g, const double *A, int64_t nA, const double *B, int64_t nB,
+                          const uint64_t *a_keys, const uint32_t *tri, const int64_t *c_tptr,
+                          const uint64_t *c_keys, int64_t nC, int64_t nT, double *C, double *csq, uint8_t *cnz,
+                          int64_t *zc, void *ws, size_t ws_bytes, cudaStream_t st);
+
 // Numeric kernel selection: QM_NUMERIC=cpasync forces the v1 cp.async kernel (A/B comparisons).
 static int numeric_impl() {
   const char *e = getenv("QM_NUMERIC");
@@ -489,6 +494,11 @@ extern "C" int qm_numeric_masked(const qm_layout *layout, const uint64_t *a_keys
   if (numeric_impl() == 2 && g.bs == 16) {
     rc = launch_numeric_group16(g, a_blocks, nA, b_blocks, nB, a_keys, tri, c_tptr, c_keys, nC, nT, c_blocks,
                                 c_sumsq, c_nonzero, zero_count, ws, ws_bytes, st);
+    if (rc != QM_ERR_UNSUPPORTED) return rc;
+  }
+  if (numeric_impl() == 2 && g.bs == 32 && !tbits && !(a_masks && b_masks)) {  // quads of C blocks
+    rc = launch_numeric_quad32(g, a_blocks, nA, b_blocks, nB, a_keys, tri, c_tptr, c_keys, nC, nT, c_blocks,
+                               c_sumsq, c_nonzero, zero_count, ws, ws_bytes, st);
     if (rc != QM_ERR_UNSUPPORTED) return rc;
   }
   if (numeric_impl() == 2) {

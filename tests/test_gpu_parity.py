@@ -759,6 +759,51 @@ def test_bs16_inline_merge_bitwise_equal_merge_pass(ses, monkeypatch, n, leaf, d
     assert helpers.rel(ses.to_dense(ses.multiply(a, b)), da @ db) <= TOL
 
 
+@pytest.mark.parametrize("cfg", [G.BaselineConfig("q", "banded", 8192, 32, half_bw=256),
+                                 G.BaselineConfig("q", "random", 16384, 32, per_row=8),
+                                 G.BaselineConfig("q", "banded", 2048 + 32, 32, half_bw=96)])
+def test_bs32_quad_kernel_bitwise_equal_per_block_kernel(ses, monkeypatch, cfg):
+    """QM_QUAD32=1 runs bs 32 products with quads of C blocks per work unit (k_numeric_quad32: the
+    four blocks (2r..2r+1, 2c..2c+1) share one pipeline stage per k, merged by the producer warp;
+    opt-in, measured 2 % slower than the default); the default runs one C block per unit (k_numeric_tma). Every block sums its own triples in ascending k with
+    the same DMMA order, and the norms are accumulated in the per-block kernel's order: blocks,
+    norms and exact-zero drops are bitwise identical (odd block counts: quads with missing members)."""
+    geom, a, b = G.config_operands_device(cfg, ses.device)
+    ma, mb = ses.matrix_from_blockset(geom, a), ses.matrix_from_blockset(geom, b)
+    lib = _ffi.load()
+    ses.multiply(ma, mb)  # (builds the operands' cached row indexes: launch counts below are steady-state)
+    monkeypatch.setenv("QM_QUAD32", "1")
+    l0 = lib.qm_launch_count()
+    c1 = ses.multiply(ma, mb).root.blockset
+    n1 = lib.qm_launch_count() - l0
+    monkeypatch.setenv("QM_QUAD32", "0")
+    l0 = lib.qm_launch_count()
+    c0 = ses.multiply(ma, mb).root.blockset
+    assert lib.qm_launch_count() - l0 == n1 + 1  # the per-block path adds k_combine_tiles: two different kernels ran
+    assert torch.equal(c0.keys, c1.keys)
+    assert torch.equal(c0.blocks, c1.blocks) and torch.equal(c0.sumsq, c1.sumsq)
+
+
+@pytest.mark.parametrize("n,leaf,dens", [(700, 64, 0.05), (1500, 32, 0.02), (2048, 64, 0.3)])
+def test_bs32_quad_kernel_matches_oracle(ses, monkeypatch, n, leaf, dens):
+    """Quads on ragged random patterns, leaf = one block (quad = Morton neighbours) and leaf = 2x2
+    blocks (quad = the leaf): block set exact, values within TOL of the oracle, and bitwise the
+    per-block kernel's; cancelling blocks are dropped alike."""
+    da, db = helpers.random_sparse(n, dens, n + 21), helpers.random_sparse(n, dens, n + 22)
+    a, b = helpers.build(ses, da, leaf, 32), helpers.build(ses, db, leaf, 32)
+    monkeypatch.setenv("QM_QUAD32", "1")
+    c = ses.multiply(a, b)
+    host = MatrixSession(device="cpu")
+    ka, ba, _ = helpers.build(host, da, leaf, 32).root.blockset.to_host()
+    kb, bb, _ = helpers.build(host, db, leaf, 32).root.blockset.to_host()
+    kc, bc, _ = O.multiply(O.Geom(n, leaf, 32), ka, ba, kb, bb)
+    np.testing.assert_array_equal(c.root.blockset.keys.cpu().numpy(), kc)
+    assert helpers.rel(c.root.blockset.blocks.cpu().numpy(), bc) <= TOL
+    monkeypatch.setenv("QM_QUAD32", "0")
+    c0 = ses.multiply(a, b).root.blockset
+    assert torch.equal(c0.blocks, c.root.blockset.blocks) and torch.equal(c0.sumsq, c.root.blockset.sumsq)
+
+
 @pytest.mark.parametrize("bs,n", [(64, 65536), (32, 16384), (128, 32768), (64, 8192)])
 def test_claim_order_is_bitwise_neutral(ses, monkeypatch, bs, n):
     """Claim orders of the numeric kernel: QM_UNIT_ORDER=k (by the k of each C block's first triple:
