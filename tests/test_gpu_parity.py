@@ -759,6 +759,46 @@ def test_bs16_inline_merge_bitwise_equal_merge_pass(ses, monkeypatch, n, leaf, d
     assert helpers.rel(ses.to_dense(ses.multiply(a, b)), da @ db) <= TOL
 
 
+@pytest.mark.parametrize("bs,leaf", [(16, 128), (16, 32), (16, 256), (32, 32), (32, 64)])
+def test_grouped_kernels_on_adversarial_block_patterns(ses, monkeypatch, bs, leaf):
+    """Block patterns chosen against the grouped kernels' producer (inline merge of the members'
+    triple lists, chunk claims): single-member groups, members whose k ranges do not overlap, one
+    member with a k list 20x longer than its neighbours', groups straddling chunk boundaries, a last
+    chunk with one C block. Block set exact, values within TOL of the oracle; the bs 32 quad kernel
+    (opt-in) is bitwise the per-block kernel's."""
+    nb = 40  # blocks per side
+    n = nb * bs
+    rng = np.random.default_rng(bs * 1000 + leaf)
+    pa, pb = np.zeros((nb, nb), bool), np.zeros((nb, nb), bool)
+    pa[0, :] = True                      # one dense block row of A ...
+    pb[:, 3] = True                      # ... against one dense block column of B: C(0,3) sums nb triples
+    pa[5, 0:3] = True                    # members with disjoint k ranges in one group
+    pa[4, 20:23] = True
+    pb[0:3, 8] = pb[20:23, 9] = True
+    pb[0:3, 9] = True
+    for i in range(8, nb, 3):            # scattered single blocks: single-member groups
+        pa[i, (7 * i) % nb] = True
+        pb[(7 * i) % nb, (11 * i) % nb] = True
+    pa[nb - 1, nb - 1] = pb[nb - 1, nb - 1] = True  # the last C block sits alone in its chunk
+    da = np.kron(pa, np.ones((bs, bs))) * rng.uniform(-1, 1, (n, n))
+    db = np.kron(pb, np.ones((bs, bs))) * rng.uniform(-1, 1, (n, n))
+    if bs == 32:
+        monkeypatch.setenv("QM_QUAD32", "1")
+    a, b = helpers.build(ses, da, leaf, bs), helpers.build(ses, db, leaf, bs)
+    c = ses.multiply(a, b).root.blockset
+    host = MatrixSession(device="cpu")
+    ka, ba, _ = helpers.build(host, da, leaf, bs).root.blockset.to_host()
+    kb, bb, _ = helpers.build(host, db, leaf, bs).root.blockset.to_host()
+    kc, bc, _ = O.multiply(O.Geom(n, leaf, bs), ka, ba, kb, bb)
+    np.testing.assert_array_equal(c.keys.cpu().numpy(), kc)
+    assert helpers.rel(c.blocks.cpu().numpy(), bc) <= TOL
+    np.testing.assert_allclose(c.sumsq.cpu().numpy(), np.einsum("nij,nij->n", bc, bc), rtol=1e-12)
+    monkeypatch.setenv("QM_QUAD32", "0")
+    monkeypatch.setenv("QM_G16_MERGE", "kernel")
+    c0 = ses.multiply(a, b).root.blockset
+    assert torch.equal(c0.blocks, c.blocks) and torch.equal(c0.sumsq, c.sumsq)
+
+
 @pytest.mark.parametrize("cfg", [G.BaselineConfig("q", "banded", 8192, 32, half_bw=256),
                                  G.BaselineConfig("q", "random", 16384, 32, per_row=8),
                                  G.BaselineConfig("q", "banded", 2048 + 32, 32, half_bw=96)])
