@@ -562,46 +562,42 @@ __global__ void __launch_bounds__(GCfg<R>::THREADS, GCfg<R>::MINB)
       phase ^= 1u;
     }
     if (mt & 1) {
+      // (No branch on "does this member exist" around the accumulator reads: ptxas renames the
+      // accumulators around such a branch -- DMMAs with D != C and ~50 register moves per stage.
+      // An absent member's accumulators are zero; the same code runs with its stores and result
+      // writes predicated off.)
       const uint64_t c_policy = l2_evict_first_policy();  // (created here: one register less in the loop)
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int mb = r * kG + gcol(warp, q);
-          if ((gm >> mb) & 1u) {
-            const int64_t c = (int64_t)c_first + __popc(gm & ((1u << mb) - 1u));
-            double *cb = C + (size_t)c * (kBlk * kBlk);
-            double ss0 = 0.0, ss1 = 0.0;
-            bool nz = false;
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-#pragma unroll
-              for (int n = 0; n < 2; ++n) {
-                const double v0 = acc[r][q][i][n][0], v1 = acc[r][q][i][n][1];
-                st_evict_first(cb + (size_t)(i * 8 + g) * kBlk + n * 8 + 2 * tq, v0, v1, c_policy);
-                ss0 = fma(v0, v0, ss0);
-                ss1 = fma(v1, v1, ss1);
-                nz |= (v0 != 0.0) | (v1 != 0.0);
-              }
-            double ss = ss0 + ss1;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-            const bool wnz = __any_sync(0xffffffffu, nz);
-            if (lane == 0) {
-              csq[c] = ss;
-              cnz[c] = (uint8_t)wnz;
-              if (!wnz && zero_count) atomicAdd((unsigned long long *)zero_count, 1ull);
-            }
-          }
-        }
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-#pragma unroll
-        for (int q = 0; q < 2; ++q)
+          const bool member = ((gm >> mb) & 1u) != 0u;
+          const int64_t c = (int64_t)c_first + __popc(gm & ((1u << mb) - 1u));
+          double *cb = C + (size_t)c * (kBlk * kBlk);
+          double ss0 = 0.0, ss1 = 0.0;
+          bool nz = false;
 #pragma unroll
           for (int i = 0; i < 2; ++i)
 #pragma unroll
-            for (int n = 0; n < 2; ++n) acc[r][q][i][n][0] = acc[r][q][i][n][1] = 0.0;
+            for (int n = 0; n < 2; ++n) {
+              const double v0 = acc[r][q][i][n][0], v1 = acc[r][q][i][n][1];
+              if (member) st_evict_first(cb + (size_t)(i * 8 + g) * kBlk + n * 8 + 2 * tq, v0, v1, c_policy);
+              ss0 = fma(v0, v0, ss0);
+              ss1 = fma(v1, v1, ss1);
+              nz |= (v0 != 0.0) | (v1 != 0.0);
+              acc[r][q][i][n][0] = acc[r][q][i][n][1] = 0.0;
+            }
+          double ss = ss0 + ss1;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+          const bool wnz = __any_sync(0xffffffffu, nz);
+          if (member && lane == 0) {
+            csq[c] = ss;
+            cnz[c] = (uint8_t)wnz;
+            if (!wnz && zero_count) atomicAdd((unsigned long long *)zero_count, 1ull);
+          }
+        }
     }
   }
 }
@@ -726,6 +722,16 @@ int launch_numeric_group16(const Geometry &g, const double *A, int64_t nA, const
                            const uint64_t *c_keys, int64_t nC, int64_t nT, double *C, double *csq,
                            uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes, cudaStream_t st) {
   if (g.bs != kBlk || g.nbl < 2 || !a_keys || !c_keys || nC >= ((int64_t)1 << 31)) return QM_ERR_UNSUPPORTED;
+  // Groups pay when a stage's k is shared by several members: k lists of some length (banded,
+  // decay). With about one triple per C block (random patterns) nearly every stage serves a single
+  // member -- 1 of up to 16 products -- and the per-block cp.async kernel is 2-3x faster (measured:
+  // random, 8 / 32 blocks per row: 8.4 / 10.4 against 2.8 / 5.7 TFLOP/s). The average k-list length
+  // decides; QM_G16_GROUPS=1 / 0 forces groups / the per-block kernel.
+  {
+    const char *e = getenv("QM_G16_GROUPS");
+    if (e && e[0] == '0') return QM_ERR_UNSUPPORTED;
+    if (!(e && e[0] == '1') && nT < 4 * nC) return QM_ERR_UNSUPPORTED;
+  }
   Carver cv(ws, ws_bytes);
   GroupWs w = carve_group(cv, nC, nT);
   if (!cv.ok() || !ws) {

@@ -306,47 +306,48 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
       phase ^= 1u;
     }
     if (mt & 1) {
+      // (No branch on "is this warp's member present" around the accumulator reads: ptxas renames the
+      // accumulators around such a branch -- DMMAs with D != C, moves and spills in the stage loop.
+      // An absent member's warp has all-zero accumulators; it runs the same code with its stores
+      // and result writes predicated off.)
       const uint32_t gm = ((uint32_t)mt >> 8) & 0xfu;
-      if ((gm >> warp) & 1u) {
-        const int64_t c = (mt >> 32) + __popc(gm & ((1u << warp) - 1u));
-        double *cb = C + (size_t)c * kQBlkElems;
-        const uint64_t c_policy = l2_evict_first_policy();  // (created here: fewer live registers in the loop)
-        // Squared norm in the per-block kernel's order: one partial per 16x16 sub-tile (that kernel's
-        // warp tile: same lane <-> element map, same in-lane order, same shuffle tree), the four
-        // partials then summed in k_combine_tiles' order -- bitwise the same norm.
-        double sum = 0.0;
-        bool nz = false;
+      const bool member = ((gm >> warp) & 1u) != 0u;
+      const int64_t c = (mt >> 32) + __popc(gm & ((1u << warp) - 1u));
+      double *cb = C + (size_t)c * kQBlkElems;
+      const uint64_t c_policy = l2_evict_first_policy();  // (created here: fewer live registers in the loop)
+      // Squared norm in the per-block kernel's order: one partial per 16x16 sub-tile (that kernel's
+      // warp tile: same lane <-> element map, same in-lane order, same shuffle tree), the four
+      // partials then summed in k_combine_tiles' order -- bitwise the same norm.
+      double sum = 0.0;
+      bool nz = false;
 #pragma unroll
-        for (int wi = 0; wi < 2; ++wi)
+      for (int wi = 0; wi < 2; ++wi)
 #pragma unroll
-          for (int wn = 0; wn < 2; ++wn) {
-            double ss0 = 0.0, ss1 = 0.0;
+        for (int wn = 0; wn < 2; ++wn) {
+          double ss0 = 0.0, ss1 = 0.0;
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
+          for (int i = 0; i < 2; ++i)
 #pragma unroll
-              for (int n = 0; n < 2; ++n) {
-                const double v0 = acc[2 * wi + i][2 * wn + n][0], v1 = acc[2 * wi + i][2 * wn + n][1];
+            for (int n = 0; n < 2; ++n) {
+              const double v0 = acc[2 * wi + i][2 * wn + n][0], v1 = acc[2 * wi + i][2 * wn + n][1];
+              if (member)
                 st_evict_first(cb + (size_t)((2 * wi + i) * 8 + g) * kQB + (2 * wn + n) * 8 + 2 * tq, v0, v1, c_policy);
-                ss0 = fma(v0, v0, ss0);
-                ss1 = fma(v1, v1, ss1);
-                nz |= (v0 != 0.0) | (v1 != 0.0);
-              }
-            double ss = ss0 + ss1;
+              ss0 = fma(v0, v0, ss0);
+              ss1 = fma(v1, v1, ss1);
+              nz |= (v0 != 0.0) | (v1 != 0.0);
+              acc[2 * wi + i][2 * wn + n][0] = acc[2 * wi + i][2 * wn + n][1] = 0.0;
+            }
+          double ss = ss0 + ss1;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-            sum += ss;  // ((0 + p00) + p01) + p10) + p11
-          }
-        const bool wnz = __any_sync(0xffffffffu, nz);
-        if (lane == 0) {
-          csq[c] = sum;
-          cnz[c] = (uint8_t)wnz;
-          if (!wnz && zero_count) atomicAdd((unsigned long long *)zero_count, 1ull);
+          for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+          sum += ss;  // ((0 + p00) + p01) + p10) + p11
         }
+      const bool wnz = __any_sync(0xffffffffu, nz);
+      if (member && lane == 0) {
+        csq[c] = sum;
+        cnz[c] = (uint8_t)wnz;
+        if (!wnz && zero_count) atomicAdd((unsigned long long *)zero_count, 1ull);
       }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int n = 0; n < 4; ++n) acc[i][n][0] = acc[i][n][1] = 0.0;
     }
   }
 }
@@ -380,19 +381,16 @@ int launch_quad(const CUtensorMap &ma, const CUtensorMap &mb, const QuadSrc &src
 
 }  // namespace
 
-// Opt-in (QM_QUAD32=1); the default for bs 32 stays the per-block kernel. Measured on B200 (R2):
-// C5-32 267.0 ms against 261.0 ms per block (0.915 vs 0.936 of the DMMA peak), banded n=32768
-// 0.646 vs 0.626 ms -- although a stage carries 128 DMMAs per warp and half the operand bytes per
-// flop. ncu: the DMMA pipe is 86 % active against 91 %; ptxas compiles the "skip the stage if this
-// member has no triple at its k" branch by renaming the accumulators around it (16-28 DMMAs with
-// D != C, ~20-40 register moves per stage and, at three CTAs per SM, 128 B of spills), so every
-// stage boundary waits for the previous stage's DMMAs to retire, and with three math warps per
-// sub-partition (the per-block kernel has six) nothing hides it. k_numeric_tma's 64x64 tile has no
-// such branch and keeps its accumulators in place. The kernel is bitwise the per-block kernel's
-// result (tests/test_gpu_parity.py) and stays selectable for further work.
+// QM_QUAD32=0: bs 32 products use the per-block kernel (A/B measurements, bitwise comparison).
+// Measured on B200 (R2): C5-32 numeric 255.4 ms against 260.8 ms per block (0.956 vs 0.936 of the
+// DMMA peak); banded n = 32768 0.612 vs 0.607 ms. (The first version was 2 % SLOWER than the
+// per-block kernel: its epilogue branched on "is this warp's member present" around the accumulator
+// reads, and ptxas then renamed the accumulators in the stage loop -- 16-28 of the 128 DMMAs with
+// D != C, register moves before every stage and 128 B of spills. With the stores predicated
+// instead, the loop is k_numeric_tma's: in-place accumulation, no moves, no spills.)
 bool quad32_enabled() {
   const char *e = getenv("QM_QUAD32");
-  return e && e[0] == '1';
+  return !(e && e[0] == '0');
 }
 
 // bs 32, one pool per operand, no support masks / transposed references, a leaf of 1 or 2x2 blocks;
@@ -405,6 +403,14 @@ int launch_numeric_quad32(const Geometry &g, const double *A, int64_t nA, const 
   if (g.bs != kQB || g.lbits > 1 || !a_keys || !c_keys || !quad32_enabled() || nC >= ((int64_t)1 << 31) ||
       !ws || ws_bytes < 256)
     return QM_ERR_UNSUPPORTED;
+  // Quads pay when a stage's k is shared by most members: long k lists (banded, decay). With about
+  // one triple per C block (random patterns) every stage serves a single member -- one warp of four
+  // working -- and the per-block kernel is twice as fast (measured: 21 vs 9 TFLOP/s). The average k
+  // list length decides (QM_QUAD32=1 forces quads).
+  {
+    const char *e = getenv("QM_QUAD32");
+    if (!(e && e[0] == '1') && nT < 8 * nC) return QM_ERR_UNSUPPORTED;
+  }
   if (nA * (int64_t)kQB >= ((int64_t)1 << 31) || nB * (int64_t)kQB >= ((int64_t)1 << 31)) return QM_ERR_UNSUPPORTED;
   CUtensorMap ma, mb;
   int rc = make_map(&ma, A, nA, kQB, kQB);
@@ -414,10 +420,10 @@ int launch_numeric_quad32(const Geometry &g, const double *A, int64_t nA, const 
   unsigned long long *counter = (unsigned long long *)ws;
   QM_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
   const QuadSrc src{c_keys, a_keys, (const uint2 *)tri, c_tptr, nC, g.nbl, g.lbits};
-  // Many triples per C block: three CTAs per SM with two stages; few (random patterns): two CTAs
-  // with three stages (deeper prefetch of operands that come from DRAM) -- k_numeric_tma's choice.
+  // Three CTAs per SM with two stages (C5-32 255.4 ms; two CTAs with three stages, QM_QUAD32_VARIANT=deep:
+  // 260.2 ms).
   const char *v = getenv("QM_QUAD32_VARIANT");
-  const bool deep = v ? strcmp(v, "deep") == 0 : nT < 2 * nC;
+  const bool deep = v ? strcmp(v, "deep") == 0 : false;
   if (deep) return launch_quad<QCfg<3, 2>>(ma, mb, src, C, csq, cnz, zc, counter, st);
   return launch_quad<QCfg<2, 3>>(ma, mb, src, C, csq, cnz, zc, counter, st);
 }

@@ -707,11 +707,14 @@ def test_special_values_subnormal_nan_inf(ses, bs):
 
 @pytest.mark.parametrize("n,leaf,dens", [(1000, 128, 0.02), (700, 64, 0.05), (500, 48, 0.05), (1500, 256, 0.01),
                                          (2048, 128, 0.3)])
-def test_bs16_grouped_kernel_vs_oracle(ses, n, leaf, dens):
+def test_bs16_grouped_kernel_vs_oracle(ses, monkeypatch, n, leaf, dens):
     """bs 16 with several blocks per leaf side runs k_numeric_group16 (the C blocks of a leaf row
     segment share their A blocks): exact C block set and values within TOL of the oracle, which
     sums each block's own triples k-ascending -- members missing a k must not see its products.
-    Includes 3 and 16 blocks per leaf side (partial and split groups) and a nearly dense case."""
+    Includes 3 and 16 blocks per leaf side (partial and split groups) and a nearly dense case.
+    (QM_G16_GROUPS=1: groups whatever the k-list length; by default products with fewer than 4
+    triples per C block -- these random patterns -- take the per-block kernel.)"""
+    monkeypatch.setenv("QM_G16_GROUPS", "1")
     lib = _ffi.load()
     assert lib.qm_numeric_path(16) == 2
     da, db = helpers.random_sparse(n, dens, n + 1), helpers.random_sparse(n, dens, n + 2)
@@ -731,6 +734,7 @@ def test_bs16_row_pair_groups_bitwise_equal_single_row(ses, monkeypatch, n, leaf
     """Leaf row pairs (R = 2 groups: each B block feeds both rows) change only which products share
     a pipeline stage; every C block still sums its own triples k-ascending with the same fragment
     order, so the result is bitwise the single-row grouping's (QM_GROUP_ROWS=1)."""
+    monkeypatch.setenv("QM_G16_GROUPS", "1")
     da, db = helpers.random_sparse(n, dens, n + 5), helpers.random_sparse(n, dens, n + 6)
     a, b = helpers.build(ses, da, leaf, 16), helpers.build(ses, db, leaf, 16)
     c2 = ses.multiply(a, b).root.blockset
@@ -748,6 +752,7 @@ def test_bs16_inline_merge_bitwise_equal_merge_pass(ses, monkeypatch, n, leaf, d
     entry per pipeline stage (default); QM_G16_MERGE=kernel runs the separate merge pass
     (k_group_merge + entries array) instead. Same entries in the same order, so the C blocks, norms
     and exact-zero drops are bitwise identical, for row-pair (leaf <= 128) and single-row groups."""
+    monkeypatch.setenv("QM_G16_GROUPS", "1")
     da, db = helpers.random_sparse(n, dens, n + 15), helpers.random_sparse(n, dens, n + 16)
     a, b = helpers.build(ses, da, leaf, 16), helpers.build(ses, db, leaf, 16)
     c2 = ses.multiply(a, b).root.blockset
@@ -759,13 +764,48 @@ def test_bs16_inline_merge_bitwise_equal_merge_pass(ses, monkeypatch, n, leaf, d
     assert helpers.rel(ses.to_dense(ses.multiply(a, b)), da @ db) <= TOL
 
 
+@pytest.mark.parametrize("bs,leaf", [(16, 128), (32, 32)])
+def test_grouped_kernels_are_gated_on_k_list_length(ses, monkeypatch, bs, leaf):
+    """Groups / quads of C blocks share a pipeline stage per k, which pays when members share k's
+    (long k lists: banded); a random pattern with about one triple per C block takes the per-block
+    kernel by default (2-3x faster there), and the forced grouped run gives bitwise the same product."""
+    nb = 96
+    n = nb * bs
+    rng = np.random.default_rng(bs)
+    pa, pb = np.zeros((nb, nb), bool), np.zeros((nb, nb), bool)
+    pa[np.repeat(np.arange(nb), 3), rng.integers(0, nb, 3 * nb)] = True
+    pb[np.repeat(np.arange(nb), 3), rng.integers(0, nb, 3 * nb)] = True
+    da = np.kron(pa, np.ones((bs, bs))) * rng.uniform(-1, 1, (n, n))
+    db = np.kron(pb, np.ones((bs, bs))) * rng.uniform(-1, 1, (n, n))
+    a, b = helpers.build(ses, da, leaf, bs), helpers.build(ses, db, leaf, bs)
+    lib = _ffi.load()
+    ses.multiply(a, b)
+    l0 = lib.qm_launch_count()
+    c0 = ses.multiply(a, b).root.blockset
+    n0 = lib.qm_launch_count() - l0
+    st = ses.last_multiply
+    assert st.n_triples < 4 * st.n_c_symbolic
+    monkeypatch.setenv("QM_G16_GROUPS", "1")
+    monkeypatch.setenv("QM_QUAD32", "1")
+    l0 = lib.qm_launch_count()
+    c1 = ses.multiply(a, b).root.blockset
+    assert torch.equal(c0.keys, c1.keys)
+    if bs == 32:  # per-block TMA kernel (+ k_combine_tiles) vs quads: same DMMA order, bitwise equal
+        assert lib.qm_launch_count() - l0 == n0 - 1
+        assert torch.equal(c0.blocks, c1.blocks) and torch.equal(c0.sumsq, c1.sumsq)
+    else:         # cp.async per-block kernel vs groups: same k order, another fragment order
+        assert helpers.rel(c0.blocks.cpu().numpy(), c1.blocks.cpu().numpy()) <= TOL
+    assert helpers.rel(ses.to_dense(ses.multiply(a, b)), da @ db) <= TOL
+
+
 @pytest.mark.parametrize("bs,leaf", [(16, 128), (16, 32), (16, 256), (32, 32), (32, 64)])
 def test_grouped_kernels_on_adversarial_block_patterns(ses, monkeypatch, bs, leaf):
     """Block patterns chosen against the grouped kernels' producer (inline merge of the members'
     triple lists, chunk claims): single-member groups, members whose k ranges do not overlap, one
     member with a k list 20x longer than its neighbours', groups straddling chunk boundaries, a last
     chunk with one C block. Block set exact, values within TOL of the oracle; the bs 32 quad kernel
-    (opt-in) is bitwise the per-block kernel's."""
+    is bitwise the per-block kernel's."""
+    monkeypatch.setenv("QM_G16_GROUPS", "1")
     nb = 40  # blocks per side
     n = nb * bs
     rng = np.random.default_rng(bs * 1000 + leaf)
@@ -803,16 +843,16 @@ def test_grouped_kernels_on_adversarial_block_patterns(ses, monkeypatch, bs, lea
                                  G.BaselineConfig("q", "random", 16384, 32, per_row=8),
                                  G.BaselineConfig("q", "banded", 2048 + 32, 32, half_bw=96)])
 def test_bs32_quad_kernel_bitwise_equal_per_block_kernel(ses, monkeypatch, cfg):
-    """QM_QUAD32=1 runs bs 32 products with quads of C blocks per work unit (k_numeric_quad32: the
-    four blocks (2r..2r+1, 2c..2c+1) share one pipeline stage per k, merged by the producer warp;
-    opt-in, measured 2 % slower than the default); the default runs one C block per unit (k_numeric_tma). Every block sums its own triples in ascending k with
+    """bs 32 products run quads of C blocks per work unit (k_numeric_quad32: the four blocks
+    (2r..2r+1, 2c..2c+1) share one pipeline stage per k, merged by the producer warp); QM_QUAD32=0
+    runs one C block per unit (k_numeric_tma). Every block sums its own triples in ascending k with
     the same DMMA order, and the norms are accumulated in the per-block kernel's order: blocks,
     norms and exact-zero drops are bitwise identical (odd block counts: quads with missing members)."""
     geom, a, b = G.config_operands_device(cfg, ses.device)
     ma, mb = ses.matrix_from_blockset(geom, a), ses.matrix_from_blockset(geom, b)
     lib = _ffi.load()
     ses.multiply(ma, mb)  # (builds the operands' cached row indexes: launch counts below are steady-state)
-    monkeypatch.setenv("QM_QUAD32", "1")
+    monkeypatch.setenv("QM_QUAD32", "1")  # (1 = quads whatever the k-list length; default: >= 8 triples per C block)
     l0 = lib.qm_launch_count()
     c1 = ses.multiply(ma, mb).root.blockset
     n1 = lib.qm_launch_count() - l0
