@@ -379,7 +379,17 @@ def run_ours(args):
     nk_ms = statistics.mean(numeric_ms)
     bs = geom.bs
     alg_bytes = 8 * bs * bs * (a.n + b.n + stats.n_c) + 8 * (a.n + b.n + stats.n_c) + 8 * stats.n_triples
-    traffic, traffic_note = committed_traffic(cfg.name)
+    # the kernel the library selects for this product (bs 16 groups / bs 32 quads of C blocks for long
+    # k lists, the per-block kernels otherwise; multi-GPU products use the pooled per-block kernel)
+    masked = int(spgemm._use_masks(a, b)) if world == 1 else 0
+    numeric_kernel = "k_numeric_tma"
+    if world == 1:
+        import ctypes
+
+        lay = _ffi.make_layout(geom.params, geom.bs)
+        numeric_kernel = lib.qm_numeric_kernel(ctypes.byref(lay), stats.n_c_symbolic, stats.n_triples, masked,
+                                               0).decode()
+    traffic, traffic_note = committed_traffic(cfg.name, numeric_kernel)
     peaks = fp64_peak(lib, torch, dev)
     peak = max(peaks["dmma"], peaks["dfma"], FP64_NOMINAL_TFLOPS)
     if world > 1:  # the events bracket the whole distributed step; per-GPU share of the flops
@@ -410,7 +420,7 @@ def run_ours(args):
                f"{2 * l2_bytes >> 20} MiB write outside each step's events)" if flush
                else "inputs larger than L2 (no flush)"),
         "phases_ms": {"symbolic": round(statistics.mean(symbolic_ms), 4), "numeric": round(nk_ms, 4)},
-        "roofline": {"bound": "tensor", "kernel": "k_numeric_tma", "achieved": round(achieved, 3),
+        "roofline": {"bound": "tensor", "kernel": numeric_kernel, "achieved": round(achieved, 3),
                      "peak": round(peak, 3), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
                      "peak_source": f"max(measured DMMA {peaks['dmma']:.2f}, measured DFMA "
                                     f"{peaks['dfma']:.2f}, nominal {FP64_NOMINAL_TFLOPS}) TFLOP/s; "
@@ -499,32 +509,39 @@ def structural_counts(geom, a, b, world, cfg) -> dict:
     return {"nnzb_a": a.n, "nnzb_b": b.n, "nnzb_c_structural": st.n_c, "triples_structural": st.n_t}
 
 
-KERNEL_SOURCES = ("csrc/qm_numeric_tma.cu", "csrc/qm_tma.cuh", "csrc/qm_common.cuh")
+KERNEL_SOURCES = {
+    "k_numeric_tma": ("csrc/qm_numeric_tma.cu", "csrc/qm_tma.cuh", "csrc/qm_common.cuh"),
+    "k_numeric_quad32": ("csrc/qm_numeric_quad.cu", "csrc/qm_tma.cuh", "csrc/qm_common.cuh"),
+    "k_numeric_group16": ("csrc/qm_numeric_group.cu", "csrc/qm_tma.cuh", "csrc/qm_common.cuh"),
+}
 
 
-def kernel_source_sha() -> str:
-    """sha256 (16 hex) of the numeric kernel's sources: a committed ncu traffic figure is used only
+def kernel_source_sha(kernel: str = "k_numeric_tma") -> str:
+    """sha256 (16 hex) of a numeric kernel's sources: a committed ncu traffic figure is used only
     for the kernel it was captured on."""
     import hashlib
 
     h = hashlib.sha256()
-    for rel in KERNEL_SOURCES:
+    for rel in KERNEL_SOURCES[kernel]:
         h.update((ROOT / "paper_2011_11762_b200" / rel).read_bytes())
     return h.hexdigest()[:16]
 
 
-def committed_traffic(workload: str):
-    """DRAM read+write bytes of one k_numeric_tma launch on this workload from the committed ncu
-    capture (profiles/ncu_traffic.json), or None when there is none for this kernel source."""
+def committed_traffic(workload: str, kernel: str = "k_numeric_tma"):
+    """DRAM read+write bytes of one launch of the workload's numeric kernel from the committed ncu
+    capture (profiles/ncu_traffic.json), or None when there is none for this kernel and source."""
     tfile = ROOT / "profiles" / "ncu_traffic.json"
     entry = json.loads(tfile.read_text()).get(workload, {}) if tfile.exists() else {}
-    sha = kernel_source_sha()
     if not entry:
         return None, f"no committed ncu capture for {workload}"
+    if entry.get("kernel", "k_numeric_tma") != kernel or kernel not in KERNEL_SOURCES:
+        return None, (f"the committed ncu capture for {workload} is of {entry.get('kernel', 'k_numeric_tma')}, "
+                      f"not {kernel}: not used")
+    sha = kernel_source_sha(kernel)
     if entry.get("kernel_src_sha") != sha:
         return None, (f"committed ncu capture for {workload} is of kernel source "
                       f"{entry.get('kernel_src_sha')}, not the current {sha}: not used")
-    return entry["traffic_bytes"], (f"dram__bytes_read.sum + dram__bytes_write.sum of one k_numeric_tma "
+    return entry["traffic_bytes"], (f"dram__bytes_read.sum + dram__bytes_write.sum of one {kernel} "
                                     f"launch, ncu capture {entry.get('capture')} (kernel source {sha}; "
                                     "profiles/ncu_traffic.json)")
 

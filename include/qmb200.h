@@ -297,6 +297,12 @@ QM_API int qm_stage_plan(const uint32_t *tri, int64_t nT, const int64_t *c_tptr,
  * DMMA (bs 32/64/128; bs 16 as grouped leaf-row segments when a leaf holds >= 2 blocks per side),
  * 1 = cp.async DMMA (QM_NUMERIC=cpasync, or bs 16 with one block per leaf), 0 = FP64 SIMT. */
 QM_API int qm_numeric_path(int32_t block_size);
+/* Name of the numeric kernel qm_numeric / qm_numeric_masked launches for a product of nC C blocks and
+ * nT triples in this layout (masked: support masks passed; flags as qm_numeric_masked): bs 16
+ * groups and bs 32 quads of C blocks are used for products whose C blocks have k lists of some
+ * length (>= 4 / >= 8 triples per block on average), the per-block kernels otherwise. Static string. */
+QM_API const char *qm_numeric_kernel(const qm_layout *layout, int64_t nC, int64_t nT, int32_t masked,
+                                     int32_t flags);
 
 /* ---- exact-zero compaction (replaces _put_leaf / _set_block dropping, ops.py:119-122) --------- */
 QM_API size_t qm_compact_workspace_bytes(int64_t nC);

@@ -61,6 +61,7 @@ EXPORTS = (
     "qm_stage_plan_workspace_bytes",
     "qm_stage_plan",
     "qm_numeric_path",
+    "qm_numeric_kernel",
     "qm_compact_workspace_bytes",
     "qm_compact",
     "qm_block_stats",
@@ -177,6 +178,7 @@ _SIGS = {
     "qm_numeric_pools": (ctypes.c_int, [_LP, _P, _P, _I32, _P, _P, _I32, _P, _P, _I64, _I64, _P, _P, _P, _P,
                                         _P, _SZ, _P]),
     "qm_numeric_path": (ctypes.c_int, [_I32]),
+    "qm_numeric_kernel": (ctypes.c_char_p, [_LP, _I64, _I64, _I32, _I32]),
     "qm_compact_workspace_bytes": (_SZ, [_I64]),
     "qm_compact": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "qm_block_stats": (ctypes.c_int, [_I32, _I64, _P, _P, _P, _P]),

@@ -457,6 +457,25 @@ static int numeric_impl() {
 
 using namespace qm;
 
+namespace qm {
+bool quad32_selected(const Geometry &g, int64_t nC, int64_t nT);
+bool group16_selected(const Geometry &g, int64_t nC, int64_t nT);
+}  // namespace qm
+
+extern "C" const char *qm_numeric_kernel(const qm_layout *layout, int64_t nC, int64_t nT, int32_t masked,
+                                         int32_t flags) {
+  Geometry g;
+  if (make_geometry(layout, &g) != QM_OK) return "";
+  const bool tbits = (flags & QM_NUMERIC_TRANSPOSED_REFS) != 0;
+  if (numeric_impl() == 2) {
+    if (g.bs == 16) return group16_selected(g, nC, nT) ? "k_numeric_group16" : "k_numeric_dmma";
+    if (g.bs == 32 && !masked && !tbits && quad32_selected(g, nC, nT)) return "k_numeric_quad32";
+    if (g.bs == 32 || g.bs == 64 || g.bs == 128) return "k_numeric_tma";
+  }
+  if (g.bs == 16 || g.bs == 32 || g.bs == 64 || g.bs == 128) return "k_numeric_dmma";
+  return "k_numeric_generic";
+}
+
 extern "C" int qm_numeric_path(int32_t bs) {
   if ((bs == 16 || bs == 32 || bs == 64 || bs == 128) && numeric_impl() == 2) return 2;
   return (bs == 16 || bs == 32 || bs == 64 || bs == 128) ? 1 : 0;

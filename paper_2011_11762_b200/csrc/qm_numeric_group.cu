@@ -716,22 +716,25 @@ size_t numeric_group16_ws_bytes(int64_t nC, int64_t nT) {
   return cv.off;
 }
 
+// Whether a bs 16 product runs as groups of C blocks. Groups pay when a stage's k is shared by
+// several members: k lists of some length (banded, decay). With about one triple per C block
+// (random patterns) nearly every stage serves a single member -- 1 of up to 16 products -- and the
+// per-block cp.async kernel is 2-3x faster (measured: random, 8 / 32 blocks per row: 8.4 / 10.4
+// against 2.8 / 5.7 TFLOP/s). The average k-list length decides; QM_G16_GROUPS=1 / 0 forces groups /
+// the per-block kernel.
+bool group16_selected(const Geometry &g, int64_t nC, int64_t nT) {
+  if (g.bs != kBlk || g.nbl < 2 || nC >= ((int64_t)1 << 31)) return false;
+  const char *e = getenv("QM_G16_GROUPS");
+  if (e && e[0] == '0') return false;
+  return (e && e[0] == '1') || nT >= 4 * nC;
+}
+
 // bs 16 with at least two blocks per leaf side; QM_ERR_UNSUPPORTED otherwise (caller falls back).
 int launch_numeric_group16(const Geometry &g, const double *A, int64_t nA, const double *B, int64_t nB,
                            const uint64_t *a_keys, const uint32_t *tri, const int64_t *c_tptr,
                            const uint64_t *c_keys, int64_t nC, int64_t nT, double *C, double *csq,
                            uint8_t *cnz, int64_t *zc, void *ws, size_t ws_bytes, cudaStream_t st) {
-  if (g.bs != kBlk || g.nbl < 2 || !a_keys || !c_keys || nC >= ((int64_t)1 << 31)) return QM_ERR_UNSUPPORTED;
-  // Groups pay when a stage's k is shared by several members: k lists of some length (banded,
-  // decay). With about one triple per C block (random patterns) nearly every stage serves a single
-  // member -- 1 of up to 16 products -- and the per-block cp.async kernel is 2-3x faster (measured:
-  // random, 8 / 32 blocks per row: 8.4 / 10.4 against 2.8 / 5.7 TFLOP/s). The average k-list length
-  // decides; QM_G16_GROUPS=1 / 0 forces groups / the per-block kernel.
-  {
-    const char *e = getenv("QM_G16_GROUPS");
-    if (e && e[0] == '0') return QM_ERR_UNSUPPORTED;
-    if (!(e && e[0] == '1') && nT < 4 * nC) return QM_ERR_UNSUPPORTED;
-  }
+  if (!a_keys || !c_keys || !group16_selected(g, nC, nT)) return QM_ERR_UNSUPPORTED;
   Carver cv(ws, ws_bytes);
   GroupWs w = carve_group(cv, nC, nT);
   if (!cv.ok() || !ws) {

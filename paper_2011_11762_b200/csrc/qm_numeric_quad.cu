@@ -393,6 +393,17 @@ bool quad32_enabled() {
   return !(e && e[0] == '0');
 }
 
+// Whether a bs 32 product of nC blocks / nT triples (no support masks, no transposed references, one
+// pool per operand) runs as quads. Quads pay when a stage's k is shared by most members: long k
+// lists (banded, decay). With about one triple per C block (random patterns) every stage serves a
+// single member -- one warp of four working -- and the per-block kernel is twice as fast (measured:
+// 21 vs 9 TFLOP/s). The average k-list length decides (QM_QUAD32=1 forces quads, 0 disables them).
+bool quad32_selected(const Geometry &g, int64_t nC, int64_t nT) {
+  if (g.bs != kQB || g.lbits > 1 || !quad32_enabled() || nC >= ((int64_t)1 << 31)) return false;
+  const char *e = getenv("QM_QUAD32");
+  return (e && e[0] == '1') || nT >= 8 * nC;
+}
+
 // bs 32, one pool per operand, no support masks / transposed references, a leaf of 1 or 2x2 blocks;
 // QM_ERR_UNSUPPORTED otherwise (the caller falls back to k_numeric_tma). The workspace only needs
 // its first 8 bytes (the chunk counter).
@@ -400,17 +411,7 @@ int launch_numeric_quad32(const Geometry &g, const double *A, int64_t nA, const 
                           const uint64_t *a_keys, const uint32_t *tri, const int64_t *c_tptr,
                           const uint64_t *c_keys, int64_t nC, int64_t nT, double *C, double *csq, uint8_t *cnz,
                           int64_t *zc, void *ws, size_t ws_bytes, cudaStream_t st) {
-  if (g.bs != kQB || g.lbits > 1 || !a_keys || !c_keys || !quad32_enabled() || nC >= ((int64_t)1 << 31) ||
-      !ws || ws_bytes < 256)
-    return QM_ERR_UNSUPPORTED;
-  // Quads pay when a stage's k is shared by most members: long k lists (banded, decay). With about
-  // one triple per C block (random patterns) every stage serves a single member -- one warp of four
-  // working -- and the per-block kernel is twice as fast (measured: 21 vs 9 TFLOP/s). The average k
-  // list length decides (QM_QUAD32=1 forces quads).
-  {
-    const char *e = getenv("QM_QUAD32");
-    if (!(e && e[0] == '1') && nT < 8 * nC) return QM_ERR_UNSUPPORTED;
-  }
+  if (!a_keys || !c_keys || !ws || ws_bytes < 256 || !quad32_selected(g, nC, nT)) return QM_ERR_UNSUPPORTED;
   if (nA * (int64_t)kQB >= ((int64_t)1 << 31) || nB * (int64_t)kQB >= ((int64_t)1 << 31)) return QM_ERR_UNSUPPORTED;
   CUtensorMap ma, mb;
   int rc = make_map(&ma, A, nA, kQB, kQB);

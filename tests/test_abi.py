@@ -99,3 +99,30 @@ def test_multi_gpu_and_row_index_entry_points_reject_bad_arguments():
                                  ctypes.byref(h), 0, None, 1, 1, None, None, None, None, None, None, 0, None)
     assert rc == _ffi.QM_ERR_INVALID and b"halo" in lib.qm_last_error()
     assert lib.qm_row_index_workspace_bytes(ctypes.byref(lay), 1000) > 0
+
+
+def test_numeric_kernel_selection(monkeypatch):
+    """qm_numeric_kernel names the kernel qm_numeric launches: grouped C blocks (bs 16 groups, bs 32
+    quads) only for products with long enough k lists, per-block kernels otherwise (host query)."""
+    for v in ("QM_QUAD32", "QM_G16_GROUPS", "QM_NUMERIC"):
+        monkeypatch.delenv(v, raising=False)
+    lib = _ffi.load()
+
+    def kernel(n, leaf, bs, n_c, n_t, masked=0, flags=0):
+        lay = _ffi.make_layout(MatrixParams.create(n, leaf), bs)
+        return lib.qm_numeric_kernel(ctypes.byref(lay), n_c, n_t, masked, flags).decode()
+
+    assert kernel(1 << 20, 64, 64, 1063904, 17827216) == "k_numeric_tma"        # C5-64
+    assert kernel(1 << 20, 32, 32, 4227008, 138330400) == "k_numeric_quad32"    # C5-32: 33 triples per block
+    assert kernel(65536, 32, 32, 63720, 65536) == "k_numeric_tma"               # random: ~1 triple per block
+    assert kernel(1 << 20, 32, 32, 4227008, 138330400, masked=1) == "k_numeric_tma"
+    assert kernel(1 << 20, 32, 32, 4227008, 138330400, flags=1) == "k_numeric_tma"  # transposed references
+    assert kernel(65536, 128, 32, 1000, 100000) == "k_numeric_tma"              # 4x4 blocks per leaf: no quads
+    assert kernel(32768, 128, 16, 132064, 2215312) == "k_numeric_group16"       # banded, leaf 128
+    assert kernel(32768, 128, 16, 128694, 130472) == "k_numeric_dmma"           # random
+    assert kernel(32768, 16, 16, 132064, 2215312) == "k_numeric_dmma"           # one block per leaf
+    assert kernel(4800, 48, 12, 100, 1000) == "k_numeric_generic"
+    monkeypatch.setenv("QM_QUAD32", "0")
+    assert kernel(1 << 20, 32, 32, 4227008, 138330400) == "k_numeric_tma"
+    monkeypatch.setenv("QM_G16_GROUPS", "1")
+    assert kernel(32768, 128, 16, 128694, 130472) == "k_numeric_group16"
