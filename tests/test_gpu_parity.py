@@ -358,6 +358,38 @@ def test_numeric_kernel_is_deterministic_under_repetition(ses, bs):
     assert bad == 0
 
 
+@pytest.mark.parametrize("bs,leaf", [(16, 128), (16, 256), (32, 64)])
+def test_grouped_kernels_are_deterministic_under_repetition(ses, monkeypatch, bs, leaf):
+    """The grouped kernels (bs 16 groups with the producer's inline merge, leaf 128: row pairs, leaf
+    256: single rows; bs 32 quads with 2x2 blocks per leaf) release a stage once its fragments are
+    in registers, like k_numeric_tma: 60 back-to-back launches of a banded product agree bitwise."""
+    monkeypatch.setenv("QM_G16_GROUPS", "1")
+    monkeypatch.setenv("QM_QUAD32", "1")
+    n, hb = 256 * bs, 8 * bs
+    d = np.arange(-hb, hb + 1)
+    rows = np.repeat(np.arange(n), d.size)
+    cols = rows + np.tile(d, n)
+    keep = (cols >= 0) & (cols < n)
+    rows, cols = rows[keep], cols[keep]
+    vals = np.random.default_rng(bs + leaf).uniform(-1, 1, rows.size)
+    a = ses.matrix_from_triplets(n, rows, cols, vals, leaf_dim=leaf, block_size=bs)
+    x = a.root.blockset
+    layout = _ffi.make_layout(a.geometry.params, bs)
+    lib = _ffi.load()
+    plan = spgemm.symbolic(layout, x, x)
+    import ctypes
+
+    want = "k_numeric_group16" if bs == 16 else "k_numeric_quad32"
+    assert lib.qm_numeric_kernel(ctypes.byref(layout), plan.n_c, plan.n_triples, 0, 0).decode() == want
+    first, _, _ = spgemm.numeric(layout, x, x, plan)
+    bad = 0
+    for _ in range(60):
+        c, _, _ = spgemm.numeric(layout, x, x, plan)
+        bad += int(not (torch.equal(c.blocks, first.blocks) and torch.equal(c.sumsq, first.sumsq)))
+    torch.cuda.synchronize()
+    assert bad == 0
+
+
 @pytest.mark.parametrize("n,leaf,bs", [(13, 4, 2), (100, 16, 4), (37, 12, 4), (300, 64, 16), (1000, 64, 64), (777, 96, 32)])
 def test_device_construction_is_bit_identical_to_host(ses, n, leaf, bs):
     """qm_build_* (GPU construction) == the host build == the reference's build:
