@@ -331,7 +331,8 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_c(const uint32_t *a_rp, const 
                                                     const int *masked_flag,
                                                     const uint2 *rb, int64_t nbg, int nbl, int lbits,
                                                     const uint64_t *rowC_off, uint64_t *rm_key,
-                                                    uint32_t *rm_cnt, uint32_t *rm_iota, unsigned int *done) {
+                                                    uint32_t *rm_cnt, uint32_t *rm_iota, unsigned int *done,
+                                                    unsigned long long *bitmap) {
   __shared__ uint32_t cnt[kWin];
   __shared__ uint64_t red64[32];
   __shared__ uint32_t red32[32];
@@ -362,7 +363,9 @@ __global__ void __launch_bounds__(kNT) k_sym_emit_c(const uint32_t *a_rp, const 
         for (int q = 0; q < kPer; ++q) {
           uint32_t c = cnt[s0 + q];
           if (c) {
-            rm_key[out + pos] = qkey((uint32_t)i, wbase + s0 + q, nbl, lbits);
+            const uint64_t key = qkey((uint32_t)i, wbase + s0 + q, nbl, lbits);
+            rm_key[out + pos] = key;
+            if (bitmap) atomicOr(&bitmap[key >> 6], 1ull << (key & 63ull));  // rank ordering (k_rank_*)
             rm_cnt[out + pos] = c;
             rm_iota[out + pos] = (uint32_t)(out + pos);
             ++pos;
@@ -503,6 +506,67 @@ __global__ void k_inv_counts(const uint32_t *perm, const uint32_t *rm_cnt, int64
     uint32_t c = perm[p];
     inv[c] = (uint32_t)p;
     cnt_q[p] = rm_cnt[c];
+  }
+  if (!c_tptr) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  cta_exclusive_scan64((const uint64_t *)cnt_q, (uint64_t *)c_tptr, nC + 1, wsum);
+}
+
+// Rank ordering of the C keys (products whose key space is small: <= 2^22 keys). C keys are
+// distinct, so their quadtree order is their rank in the set: k_sym_emit_c marks every key in a bitmap
+// of the key space, k_rank_scan turns the bitmap words' popcounts into exclusive prefixes (one
+// CTA), and k_rank_place gives every C block its position = prefix of its word + the set bits below
+// its own -- the device-wide radix sort's histogram / scan / onesweep passes and memsets (about ten
+// launches, ~65 us for C3's 65 K keys) become one memset and two small kernels. Deterministic: the
+// result does not depend on the order of the atomics. k_rank_place also writes the per-block
+// triple counts in key order and, like k_inv_counts, scans them into c_tptr in its last CTA.
+constexpr int kRankMaxBits = 22;
+__global__ void __launch_bounds__(1024) k_rank_scan(const unsigned long long *bitmap, int64_t words, uint32_t *prefix) {
+  // One CTA; every warp owns a contiguous run of words and reads it 32 words at a time (coalesced).
+  __shared__ uint32_t wtot[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int64_t per = ((words + (int64_t)nw * 32 - 1) / ((int64_t)nw * 32)) * 32;
+  const int64_t lo = std::min<int64_t>((int64_t)warp * per, words), hi = std::min<int64_t>(lo + per, words);
+  uint32_t part = 0;
+  for (int64_t q = lo + lane; q < hi; q += 32) part += (uint32_t)__popcll(bitmap[q]);
+  part = __reduce_add_sync(0xffffffffu, part);
+  if (lane == 0) wtot[warp] = part;
+  __syncthreads();
+  uint32_t run = 0;
+  for (int w = 0; w < warp; ++w) run += wtot[w];
+  for (int64_t q0 = lo; q0 < hi; q0 += 32) {
+    const int64_t q = q0 + lane;
+    const uint32_t c = q < hi ? (uint32_t)__popcll(bitmap[q]) : 0u;
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (q < hi) prefix[q] = run + incl - c;
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+__global__ void k_rank_place(const uint64_t *rm_key, const uint32_t *rm_cnt, int64_t nC,
+                             const unsigned long long *bitmap, const uint32_t *prefix, uint64_t *c_keys,
+                             uint32_t *perm, uint32_t *inv, int64_t *cnt_q, int64_t *c_tptr, unsigned int *done) {
+  __shared__ uint64_t wsum[32];
+  __shared__ bool last;
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt_q[nC] = 0;  // exclusive-scan tail
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nC; x += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = rm_key[x];
+    const uint64_t w = key >> 6;
+    const uint32_t p = prefix[w] + (uint32_t)__popcll(bitmap[w] & ((1ull << (key & 63ull)) - 1ull));
+    c_keys[p] = key;
+    perm[p] = (uint32_t)x;
+    inv[x] = p;
+    cnt_q[p] = rm_cnt[x];
   }
   if (!c_tptr) return;
   __threadfence();
@@ -722,7 +786,16 @@ struct FillWs {
   unsigned int *done;
   void *cub;
   size_t cub_bytes;
+  unsigned long long *bitmap;  // rank ordering: one bit per key of the key space (NULL: not used)
+  uint32_t *prefix;
+  int64_t words;
 };
+
+// QM_RANK_ORDER=0: the C keys are always ordered by a sort (A/B measurements, tests).
+bool rank_order_enabled() {
+  const char *e = getenv("QM_RANK_ORDER");
+  return !(e && e[0] == '0');
+}
 
 // QM_SMALL_SORT=0: small products use the device-wide sort too (A/B measurements).
 bool small_sort_enabled() {
@@ -748,6 +821,20 @@ FillWs carve_fill(Carver &cv, int64_t nC, int key_bits) {
   cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t *)nullptr, (int64_t *)nullptr, (int64_t)nC + 1);
   w.cub_bytes = std::max(a, b);
   w.cub = cv.take<char>(w.cub_bytes);
+  // rank ordering: key space of at most 2^22 keys and not much larger than the C set (the bitmap is
+  // zeroed and scanned per product); always carved when eligible, so the workspace size does not
+  // depend on the environment switches
+  w.bitmap = nullptr;
+  w.prefix = nullptr;
+  w.words = 0;
+  if (key_bits <= kRankMaxBits && nC > 0) {
+    const int64_t words = ((int64_t)1 << std::max(key_bits, 6)) / 64;
+    if (words <= 64 * nC + 1024) {
+      w.words = words;
+      w.bitmap = cv.take<unsigned long long>(words);
+      w.prefix = cv.take<uint32_t>(words);
+    }
+  }
   return w;
 }
 
@@ -1079,9 +1166,28 @@ int fill_setup(const qm_layout *layout, int64_t nA, int64_t nB, int64_t nC, void
 int fill_keys_core(const Geometry &g, const Ix &a, const Ix &b, int64_t nC, const SymWs &w, const FillWs &f,
                    int key_bits, uint64_t *c_keys, int64_t *c_tptr, cudaStream_t st) {
   if (nC == 0) return cudaMemsetAsync(c_tptr, 0, sizeof(int64_t), st) == cudaSuccess ? QM_OK : QM_ERR_CUDA;
+  // (single-CTA sort for the smallest products, rank ordering when the key space is small, else the
+  // device-wide radix sort)
+  const bool small = nC <= kSmallSortMax && small_sort_enabled();
+  const bool rank = f.bitmap != nullptr && rank_order_enabled() && !(small && nC <= 2048);
+  if (rank) QM_CUDA_TRY(cudaMemsetAsync(f.bitmap, 0, (size_t)f.words * sizeof(unsigned long long), st));
   k_sym_emit_c<<<row_grid(g.nbg), kNT, 0, st>>>(a.rp, a.col, b.rp, b.col, a.mask, b.mask, w.masked, w.rb, g.nbg,
-                                                g.nbl, g.lbits, w.off, f.rm_key, f.rm_cnt, f.rm_iota, f.done);
+                                                g.nbl, g.lbits, w.off, f.rm_key, f.rm_cnt, f.rm_iota, f.done,
+                                                rank ? f.bitmap : nullptr);
   QM_LAUNCHED("k_sym_emit_c");
+  if (rank) {
+    k_rank_scan<<<1, 1024, 0, st>>>(f.bitmap, f.words, f.prefix);
+    QM_LAUNCHED("k_rank_scan");
+    const bool fused = nC <= kFusedTptrScanMax;
+    k_rank_place<<<grid_for(nC), 256, 0, st>>>(f.rm_key, f.rm_cnt, nC, f.bitmap, f.prefix, c_keys, f.perm, f.inv,
+                                               f.cnt_q, fused ? c_tptr : nullptr, f.done);
+    QM_LAUNCHED("k_rank_place");
+    if (!fused) {
+      size_t tb = f.cub_bytes;
+      QM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(f.cub, tb, f.cnt_q, c_tptr, nC + 1, st));
+    }
+    return QM_OK;
+  }
   if (nC <= kSmallSortMax && small_sort_enabled()) {
     static PerDeviceOnce once;
     int rc = once.run([]() -> int {

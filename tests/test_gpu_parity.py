@@ -1178,6 +1178,31 @@ def test_single_cta_sort_equals_device_sort(ses, monkeypatch, cfg):
     assert torch.equal(p1.c_keys, p0.c_keys) and torch.equal(p1.c_tptr, p0.c_tptr) and torch.equal(p1.tri, p0.tri)
 
 
+@pytest.mark.parametrize("name", ["C1", "C2-16384", "C3", "C4"])
+def test_rank_ordering_equals_sorted_keys(ses, monkeypatch, name):
+    """Products whose key space is small order their C keys by rank in a bitmap of the key space
+    (k_rank_scan / k_rank_place: the keys are distinct, so the order is their rank) instead of a
+    radix sort (QM_RANK_ORDER=0): same C keys, c_tptr and triples, in the same order; masked (C4)
+    and unmasked, with the single-CTA sort switched off so that C1 takes the rank path too."""
+    cfg = G.CONFIGS[name]
+    geom, a, b = G.config_operands_device(cfg, ses.device)
+    if cfg.same_operand:
+        b = a
+    lay = _ffi.make_layout(geom.params, geom.bs)
+    monkeypatch.setenv("QM_SMALL_SORT", "0")
+    lib = _ffi.load()
+    spgemm.symbolic(lay, a, b)
+    l0 = lib.qm_launch_count()
+    p1 = spgemm.symbolic(lay, a, b)
+    n1 = lib.qm_launch_count() - l0
+    monkeypatch.setenv("QM_RANK_ORDER", "0")
+    l0 = lib.qm_launch_count()
+    p0 = spgemm.symbolic(lay, a, b)
+    assert lib.qm_launch_count() - l0 != n1  # (the sort path launches other kernels)
+    assert (p1.n_c, p1.n_triples) == (p0.n_c, p0.n_triples)
+    assert torch.equal(p1.c_keys, p0.c_keys) and torch.equal(p1.c_tptr, p0.c_tptr) and torch.equal(p1.tri, p0.tri)
+
+
 def test_cached_row_index_on_wide_rows(ses, monkeypatch):
     """Rows spanning several 4096-column windows of the count accumulator (as
     test_support_filter_multi_window_rows): the row-index path equals the keys path."""
