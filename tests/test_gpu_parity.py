@@ -1169,6 +1169,7 @@ def test_single_cta_sort_equals_device_sort(ses, monkeypatch, cfg):
     triples, in the same order."""
     geom, a, b = G.config_operands_device(cfg, ses.device)
     lay = _ffi.make_layout(geom.params, geom.bs)
+    monkeypatch.setenv("QM_RANK_ORDER", "0")  # (else 2,048 < nC <= 8,192 and QM_SMALL_SORT=0 take the rank ordering)
     monkeypatch.setenv("QM_SMALL_SORT", "1")
     p1 = spgemm.symbolic(lay, a, b)
     assert 0 < p1.n_c <= 8192
