@@ -41,7 +41,10 @@ constexpr uint32_t kAbsent = 0xffffffffu;
 // of its columns has a B block; interleaving spreads that run over the warps (= the SM's four
 // sub-partitions), so the busiest warp of a partial stage has half the work it would have with
 // adjacent columns 2w, 2w+1 (-DQM_EXP_G16_PAIRED; +3 % with the specialised partial stages below,
-// -4 % before them, when every partial stage took a guarded slow path).
+// -4 % before them, when every partial stage took a guarded slow path). Mirroring the ownership in
+// the second row (columns 3 - w, 7 - w: a run of present columns then loads the warps from both ends)
+// needs separate B fragments per row -- 12 instead of 8 fragment loads per k step -- and measured
+// 2.5 % slower.
 #ifdef QM_EXP_G16_PAIRED
 __device__ __forceinline__ int gcol(int warp, int q) { return 2 * warp + q; }
 __device__ __forceinline__ uint32_t gcols_present(uint32_t pm, int warp) { return (pm >> (2 * warp)) & 3u; }
