@@ -57,3 +57,18 @@ def test_gpu_arm_contract():
                 "--cpu-target-s", "1"])
     assert ref["config"] == line["config"]  # both arms print the same workload definition
     assert line["cpu_baseline"]["value"] > 0 and line["cpu_baseline"]["kind"] == "port"
+
+
+def test_committed_traffic_is_per_kernel_and_source():
+    """roofline.traffic comes from a committed ncu capture only when it was taken on the same
+    kernel and kernel source the bench is running (a stale or foreign entry reads as None)."""
+    import bench
+
+    t, note = bench.committed_traffic("C5-64")  # k_numeric_tma capture of the default workload
+    assert (t is None and "not the current" in note) or t > 7e10
+    t, note = bench.committed_traffic("C5-64", "k_numeric_quad32")
+    assert t is None and "k_numeric_tma" in note
+    t, note = bench.committed_traffic("C5-32", "k_numeric_tma")  # the C5-32 capture is of the quad kernel
+    assert t is None
+    assert bench.committed_traffic("no-such-workload")[0] is None
+    assert bench.kernel_source_sha("k_numeric_tma") != bench.kernel_source_sha("k_numeric_quad32")
